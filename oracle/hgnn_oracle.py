@@ -1,0 +1,464 @@
+"""CPU float64 oracle for the HydraGNN (PNA-GCNN) training step — TEST INFRASTRUCTURE.
+
+This module is the plain, slow, obviously-correct definition of what the CUDA
+path computes. Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` leg may import it. The product package
+(``paper_2207_11333_b200``) never imports it, and it never imports the
+product package: the only code both sides share is the seeded input generator
+``molgen`` (no method arithmetic).
+
+Each function cites the passage it follows (PAPER.md = /root/reference/PAPER.md,
+SPEC.md = /root/reference/SPEC.md, SURVEY = /root/repo/SURVEY.md §8(c) readings
+C1..C21; DESIGN.md "Readings" restates them).
+
+Pins (tests/test_oracle_*.py, ``-m "not gpu"``): hand-derived worked examples
+(P1 two-node graph, P2 star graph, tests/golden/), delta by hand (P3), SPEC
+closed forms (P4), central finite differences (P5), permutation invariance
+(P6), batch independence (P7), DDP split equivalence (P8), an independent
+torch.autograd float64 implementation of the same definition, the dense
+textbook special case {mean} x {identity} (P9iii), and torch.optim.AdamW in
+float64 (P9ii). Every function below is pinned by at least one of them.
+
+Data model: a *store* is the Table-1 dict of PAPER.md:232-253 (as produced by
+``molgen.generate``); a *batch* is the packed layout of SURVEY §8(a2).
+Floating-point math is float64 throughout (inputs are fp32 values upcast).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+MASK64 = (1 << 64) - 1
+GOLDEN = 0x9E3779B97F4A7C15
+KEY2 = 0xD1B54A32D192ED03
+VAR_FLOOR = 1e-10  # epsilon_v
+
+
+# --------------------------------------------------------------------------
+# counter-based RNG: splitmix64 finalizer, all arithmetic mod 2^64
+# --------------------------------------------------------------------------
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """z = x + 0x9E3779B97F4A7C15; z = (z ^ z>>30)*0xBF58476D1CE4E5B9;
+    z = (z ^ z>>27)*0x94D049BB133111EB; return z ^ z>>31."""
+    with np.errstate(over="ignore"):
+        z = np.asarray(x, dtype=np.uint64) + np.uint64(GOLDEN)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def _mul64(a: int, b: np.ndarray) -> np.ndarray:
+    return np.asarray(b, dtype=np.uint64) * np.uint64(a & MASK64)
+
+
+# --------------------------------------------------------------------------
+# model configuration and parameters
+# --------------------------------------------------------------------------
+def param_specs(cfg: dict) -> list:
+    """Ordered (name, shape, fan_in, fan_out) list; the order is tensor_idx.
+
+    Per conv layer l: message matrix M = [M_x | M_e]
+    of shape [H, F_l + Fe] stored as two tensors (same init scale, fan of the
+    whole M), bias b_M [H]; update matrix U [H, 12H] with column index
+    (s*4 + a)*H + c, s in (identity, amplification, attenuation), a in (mean,
+    min, max, std); bias b_U [H]. Head: W1 [Hf, H], b1, W2 [1, Hf], b2.
+    """
+    H, L, F0, Fe = cfg["hidden"], cfg["layers"], cfg["f_node"], cfg["f_edge"]
+    Hf = cfg.get("fc_hidden", H)
+    out = []
+    for l in range(L):
+        Fl = F0 if l == 0 else H
+        out.append((f"conv{l}.M_x", (H, Fl), Fl + Fe, H))
+        out.append((f"conv{l}.M_e", (H, Fe), Fl + Fe, H))
+        out.append((f"conv{l}.b_M", (H,), 0, 0))
+        out.append((f"conv{l}.U", (H, 12 * H), 12 * H, H))
+        out.append((f"conv{l}.b_U", (H,), 0, 0))
+    out.append(("head.W1", (Hf, H), H, Hf))
+    out.append(("head.b1", (Hf,), 0, 0))
+    out.append(("head.W2", (1, Hf), Hf, 1))
+    out.append(("head.b2", (1,), 0, 0))
+    return out
+
+
+def init_params(cfg: dict, seed: int) -> dict:
+    """w ~ uniform(+-sqrt(6/(fan_in+fan_out))), biases zero.
+
+    RNG per SURVEY C12: key = seed ^ (tensor_idx*0x9E3779B97F4A7C15) ^
+    (elem_idx*0xD1B54A32D192ED03); u = (splitmix64(key) >> 11) * 2^-53;
+    w = (2u - 1) * a in f64, rounded to fp32 (round-to-nearest-even), returned
+    as float64 holding fp32 values.
+    """
+    params = {}
+    for t, (name, shape, fi, fo) in enumerate(param_specs(cfg)):
+        n = int(np.prod(shape))
+        if fi == 0:
+            params[name] = np.zeros(shape, np.float64)
+            continue
+        a = math.sqrt(6.0 / (fi + fo))
+        idx = np.arange(n, dtype=np.uint64)
+        key = np.uint64(seed & MASK64) ^ np.uint64((t * GOLDEN) & MASK64) ^ _mul64(KEY2, idx)
+        u = (splitmix64(key) >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+        w = ((2.0 * u - 1.0) * a).astype(np.float32).astype(np.float64)
+        params[name] = w.reshape(shape)
+    return params
+
+
+# --------------------------------------------------------------------------
+# sharding
+# --------------------------------------------------------------------------
+def shard(seed: int, epoch: int, rank: int, world: int, n: int) -> np.ndarray:
+    """Global per-epoch permutation of [0, n): ascending by (key_i, i) with
+    key_i = splitmix64(seed ^ (epoch*GOLDEN) ^ (i*KEY2)); rank r takes the
+    permuted positions p = r (mod world), truncated to floor(n/world) (drop-last)."""
+    if not (0 <= rank < world):
+        raise ValueError("rank out of range")
+    i = np.arange(n, dtype=np.uint64)
+    key = splitmix64(np.uint64(seed & MASK64) ^ np.uint64((epoch * GOLDEN) & MASK64) ^ _mul64(KEY2, i))
+    perm = np.lexsort((np.arange(n), key))  # primary key, then index
+    per = n // world
+    return perm[rank::world][:per].astype(np.int64)
+
+
+# --------------------------------------------------------------------------
+# degree statistic delta
+# --------------------------------------------------------------------------
+def degree_stat(store: dict, ids=None) -> float:
+    """delta = mean over all nodes of the (training) graphs of ln(d + 1), d = in-degree."""
+    no, eo = store["node_offset"], store["edge_offset"]
+    if ids is None:
+        ids = np.arange(len(no) - 1)
+    tot, cnt = 0.0, 0
+    src = store["edge_index"][0]
+    for g in np.asarray(ids):
+        n = int(no[g + 1] - no[g])
+        d = np.bincount(store["edge_index"][1][eo[g]:eo[g + 1]], minlength=n) if n else np.zeros(0)
+        _ = src  # edges are symmetric: in-degree == out-degree
+        tot += float(np.log(d.astype(np.float64) + 1.0).sum())
+        cnt += n
+    return tot / cnt
+
+
+# --------------------------------------------------------------------------
+# pack / collate
+# --------------------------------------------------------------------------
+def pack(store: dict, ids) -> dict:
+    """Disjoint union of the graphs ``ids`` in input order.
+
+    graph_ptr [B+1] i32 (cumulative node counts); x [N, F0]; y [B];
+    CSR over destination nodes: rowptr [N+1] i32, col [E] i32 (in-neighbour
+    ids, ascending within a row), eattr [E, Fe] (attribute of the edge
+    col -> row); slot [E] u8: for entry k of row r with col[k] = c, the
+    position of r inside row c.  Integers only, compared bit-exactly.
+    """
+    ids = np.asarray(ids, dtype=np.int64)
+    if len(ids) == 0:
+        raise ValueError("EmptyBatch (SPEC.md:279)")
+    no, eo = store["node_offset"], store["edge_offset"]
+    xs, eas, srcs, dsts, ys, counts = [], [], [], [], [], [0]
+    base = 0
+    for g in ids:
+        n0, n1, e0, e1 = int(no[g]), int(no[g + 1]), int(eo[g]), int(eo[g + 1])
+        if n1 == n0:
+            raise ValueError("EmptyGraphSlot (SPEC.md:356)")
+        xs.append(store["x"][n0:n1])
+        s = store["edge_index"][0][e0:e1].astype(np.int64)
+        d = store["edge_index"][1][e0:e1].astype(np.int64)
+        srcs.append(s + base)  # SPEC.md:283 offset arithmetic
+        dsts.append(d + base)
+        eas.append(store["edge_attr"][e0:e1])
+        ys.append(store["y"][g])
+        base += n1 - n0
+        counts.append(base)
+    N = base
+    src = np.concatenate(srcs) if srcs else np.zeros(0, np.int64)
+    dst = np.concatenate(dsts) if dsts else np.zeros(0, np.int64)
+    ea = np.concatenate(eas).astype(np.float32)
+    # destination-major CSR: row i = edges (j -> i), ordered by source j ascending
+    order = np.lexsort((src, dst))
+    row, col, eattr = dst[order], src[order], ea[order]
+    rowptr = np.zeros(N + 1, np.int64)
+    np.add.at(rowptr, row + 1, 1)
+    rowptr = np.cumsum(rowptr)
+    pos = np.arange(len(row)) - rowptr[row]
+    # slot: position of r inside row c, found by brute-force search
+    slot = np.zeros(len(row), np.int64)
+    for k in range(len(row)):
+        c, r = col[k], row[k]
+        seg = col[rowptr[c]:rowptr[c + 1]]
+        w = np.nonzero(seg == r)[0]
+        if len(w) != 1:
+            raise ValueError("edge list not symmetric (SPEC.md:103)")
+        slot[k] = w[0]
+    return {
+        "graph_ptr": np.asarray(counts, np.int32),
+        "x": np.concatenate(xs).astype(np.float32),
+        "y": np.asarray(ys, np.float32),
+        "rowptr": rowptr.astype(np.int32),
+        "col": col.astype(np.int32),
+        "eattr": eattr,
+        "slot": slot.astype(np.uint8),
+        "pos": pos.astype(np.int64),
+        "row": row.astype(np.int64),
+    }
+
+
+# --------------------------------------------------------------------------
+# forward
+# --------------------------------------------------------------------------
+def _seg_reduce(ufunc, vals: np.ndarray, rowptr: np.ndarray, fill: float) -> np.ndarray:
+    """Per-row reduction of vals [E, C] over CSR rows; empty rows get ``fill``.
+    (np.ufunc.reduceat returns a wrong value for empty segments, so they are masked.)"""
+    N = len(rowptr) - 1
+    out = np.full((N, vals.shape[1]), fill, np.float64)
+    deg = np.diff(rowptr)
+    ne = np.nonzero(deg > 0)[0]
+    if len(ne):
+        out[ne] = ufunc.reduceat(vals, rowptr[ne], axis=0)
+    return out
+
+
+def scalers(deg: np.ndarray, delta: float):
+    """Degree scalers: amplification
+    ln(d+1)/delta, attenuation delta/ln(d+1); both 1 when d = 0."""
+    ld = np.log(deg.astype(np.float64) + 1.0)
+    amp = np.where(deg > 0, ld / delta, 1.0)
+    att = np.where(deg > 0, delta / np.where(deg > 0, ld, 1.0), 1.0)
+    return amp, att
+
+
+def conv_forward(Xl: np.ndarray, batch: dict, p: dict, l: int, delta: float, var_floor: float = VAR_FLOOR):
+    """One PNA-style GC layer.
+
+    m_{j->i} = M [x_j || e_ji] + b_M over in-neighbours j of i;
+    aggregates mean, min, max (first position attaining it), std =
+    sqrt(max(var, eps_v)) with the population variance computed two-pass
+    (SURVEY C6); d = 0 rows are all zero (C5); S = [A || amp*A || att*A]
+    (scaler-major, C3); Z = S U^T + b_U; X_{l+1} = max(Z, 0).
+    """
+    rowptr = batch["rowptr"].astype(np.int64)
+    col = batch["col"].astype(np.int64)
+    row, pos = batch["row"], batch["pos"]
+    deg = np.diff(rowptr)
+    M = np.concatenate([p[f"conv{l}.M_x"], p[f"conv{l}.M_e"]], axis=1)
+    cat = np.concatenate([Xl[col], batch["eattr"].astype(np.float64)], axis=1)
+    msg = cat @ M.T + p[f"conv{l}.b_M"]
+    N = len(deg)
+    dd = np.maximum(deg, 1).astype(np.float64)[:, None]
+    mean = _seg_reduce(np.add, msg, rowptr, 0.0) / dd
+    mx = _seg_reduce(np.maximum, msg, rowptr, 0.0)
+    mn = _seg_reduce(np.minimum, msg, rowptr, 0.0)
+    big = np.iinfo(np.int64).max
+    posb = np.broadcast_to(pos[:, None], msg.shape)
+    argmax = _seg_reduce(np.minimum, np.where(msg == mx[row], posb, big).astype(np.float64), rowptr, 0).astype(np.int64)
+    argmin = _seg_reduce(np.minimum, np.where(msg == mn[row], posb, big).astype(np.float64), rowptr, 0).astype(np.int64)
+    cen = msg - mean[row]
+    var = _seg_reduce(np.add, cen * cen, rowptr, 0.0) / dd
+    std = np.sqrt(np.maximum(var, var_floor))
+    empty = deg == 0
+    std[empty] = 0.0
+    A = np.concatenate([mean, mn, mx, std], axis=1)
+    amp, att = scalers(deg, delta)
+    S = np.concatenate([A, amp[:, None] * A, att[:, None] * A], axis=1)
+    Z = S @ p[f"conv{l}.U"].T + p[f"conv{l}.b_U"]
+    X1 = np.maximum(Z, 0.0)
+    cache = dict(Xl=Xl, cat=cat, msg=msg, mean=mean, mn=mn, mx=mx, argmax=argmax, argmin=argmin,
+                 var=var, std=std, A=A, S=S, Z=Z, amp=amp, att=att, deg=deg, N=N)
+    return X1, cache
+
+
+def forward(params: dict, batch: dict, cfg: dict, delta: float):
+    """Full forward: L GC layers -> global mean pool ->
+    FC head ReLU(G W1^T + b1) W2^T + b2 -> MSE."""
+    X = batch["x"].astype(np.float64)
+    caches = []
+    for l in range(cfg["layers"]):
+        X, c = conv_forward(X, batch, params, l, delta, cfg.get("var_floor", VAR_FLOOR))
+        caches.append(c)
+    gp = batch["graph_ptr"].astype(np.int64)
+    ng = np.diff(gp)
+    if np.any(ng == 0):
+        raise ValueError("EmptyGraphSlot (SPEC.md:356)")
+    G = np.add.reduceat(X, gp[:-1], axis=0) / ng[:, None]
+    hpre = G @ params["head.W1"].T + params["head.b1"]
+    hid = np.maximum(hpre, 0.0)
+    yhat = (hid @ params["head.W2"].T)[:, 0] + params["head.b2"][0]
+    y = batch["y"].astype(np.float64)
+    loss = float(np.mean((yhat - y) ** 2))
+    head = dict(XL=X, G=G, hpre=hpre, hid=hid, yhat=yhat, ng=ng, gp=gp)
+    return loss, yhat, dict(layers=caches, head=head)
+
+
+# --------------------------------------------------------------------------
+# backward
+# --------------------------------------------------------------------------
+def backward(params: dict, batch: dict, cfg: dict, cache: dict, decisions: dict | None = None) -> dict:
+    """Reverse-mode gradients of the mean MSE loss w.r.t. every parameter.
+
+    Subgradients: ReLU'(0) = 0 (C8); min/max route to the first position
+    attaining the extremum (C7); the std derivative is
+    (m_k - mu)/(d * std) when var > eps_v and 0 otherwise (C6).
+    ``decisions`` (optional, per layer index) replaces the oracle's own
+    discrete decisions in the ambiguity band (SURVEY C8 decision replay):
+    keys 'relu' (bool [N,H], Z > 0), 'argmax'/'argmin' (int [N,H]),
+    'varflag' (bool [N,H], var > eps_v); 'head_relu' (bool [B,Hf]) at top level.
+    """
+    decisions = decisions or {}
+    h = cache["head"]
+    B = len(h["yhat"])
+    y = batch["y"].astype(np.float64)
+    g = {}
+    dy = 2.0 * (h["yhat"] - y) / B
+    g["head.W2"] = (dy @ h["hid"])[None, :]
+    g["head.b2"] = np.array([dy.sum()])
+    dhid = dy[:, None] * params["head.W2"][0][None, :]
+    hmask = decisions.get("head_relu", h["hpre"] > 0)
+    dhpre = dhid * hmask
+    g["head.W1"] = dhpre.T @ h["G"]
+    g["head.b1"] = dhpre.sum(0)
+    dG = dhpre @ params["head.W1"]
+    gp, ng = h["gp"], h["ng"]
+    gid = np.repeat(np.arange(B), ng)
+    dX = dG[gid] / ng[gid][:, None]
+    col = batch["col"].astype(np.int64)
+    row, pos = batch["row"], batch["pos"]
+    H = cfg["hidden"]
+    for l in reversed(range(cfg["layers"])):
+        c = cache["layers"][l]
+        dec = decisions.get(l, {})
+        relu = dec.get("relu", c["Z"] > 0)
+        dZ = dX * relu
+        g[f"conv{l}.U"] = dZ.T @ c["S"]
+        g[f"conv{l}.b_U"] = dZ.sum(0)
+        dS = dZ @ params[f"conv{l}.U"]
+        amp, att = c["amp"][:, None], c["att"][:, None]
+        dA = dS[:, :4 * H] + amp * dS[:, 4 * H:8 * H] + att * dS[:, 8 * H:]
+        dmean, dmin, dmax, dstd = (dA[:, a * H:(a + 1) * H] for a in range(4))
+        argmax = dec.get("argmax", c["argmax"])
+        argmin = dec.get("argmin", c["argmin"])
+        varflag = dec.get("varflag", c["var"] > cfg.get("var_floor", VAR_FLOOR))
+        deg = np.maximum(c["deg"], 1).astype(np.float64)
+        dr = deg[row][:, None]
+        p2 = pos[:, None]
+        dm = (dmean[row] / dr
+              + (p2 == argmax[row]) * dmax[row]
+              + (p2 == argmin[row]) * dmin[row]
+              + varflag[row] * dstd[row] * (c["msg"] - c["mean"][row]) / (dr * np.where(c["std"][row] > 0, c["std"][row], 1.0)))
+        dM = dm.T @ c["cat"]
+        F = c["Xl"].shape[1]
+        g[f"conv{l}.M_x"] = dM[:, :F]
+        g[f"conv{l}.M_e"] = dM[:, F:]
+        g[f"conv{l}.b_M"] = dm.sum(0)
+        if l > 0:
+            dcat = dm @ np.concatenate([params[f"conv{l}.M_x"], params[f"conv{l}.M_e"]], axis=1)
+            dX = np.zeros_like(c["Xl"])
+            np.add.at(dX, col, dcat[:, :F])
+    return g
+
+
+# --------------------------------------------------------------------------
+# AdamW
+# --------------------------------------------------------------------------
+def adamw_step(params: dict, grads: dict, state: dict, lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01):
+    """Decoupled weight decay then bias-corrected Adam (Loshchilov & Hutter,
+    PyTorch ordering), applied to every tensor including biases.
+    state = {'m': {...}, 'v': {...}, 'step': int}; returns (params, state) new copies."""
+    t = state["step"] + 1
+    newp, m, v = {}, {}, {}
+    for k, th in params.items():
+        gk = grads[k]
+        th = th * (1.0 - lr * weight_decay)
+        m[k] = beta1 * state["m"][k] + (1.0 - beta1) * gk
+        v[k] = beta2 * state["v"][k] + (1.0 - beta2) * gk * gk
+        mhat = m[k] / (1.0 - beta1 ** t)
+        vhat = v[k] / (1.0 - beta2 ** t)
+        newp[k] = th - lr * mhat / (np.sqrt(vhat) + eps)
+    return newp, {"m": m, "v": v, "step": t}
+
+
+def zero_state(params: dict) -> dict:
+    return {"m": {k: np.zeros_like(v) for k, v in params.items()},
+            "v": {k: np.zeros_like(v) for k, v in params.items()}, "step": 0}
+
+
+# --------------------------------------------------------------------------
+# DDP
+# --------------------------------------------------------------------------
+def allreduce_mean(per_rank: list) -> dict:
+    """Elementwise mean over ranks (rank-ascending sum, then divide)."""
+    W = len(per_rank)
+    out = {}
+    for k in per_rank[0]:
+        acc = np.zeros_like(per_rank[0][k])
+        for r in range(W):
+            acc = acc + per_rank[r][k]
+        out[k] = acc / W
+    return out
+
+
+def train_step(params, state, store, ids, cfg, delta, hyper=None, world=1):
+    """One DDP iteration simulated in-process: each of ``world``
+    ranks packs its equal sub-batch, runs forward+backward; gradients are
+    averaged; every rank applies the identical AdamW step."""
+    hyper = hyper or {}
+    ids = np.asarray(ids)
+    B = len(ids) // world
+    grads, losses = [], []
+    for r in range(world):
+        b = pack(store, ids[r * B:(r + 1) * B])
+        loss, _, cache = forward(params, b, cfg, delta)
+        grads.append(backward(params, b, cfg, cache))
+        losses.append(loss)
+    g = allreduce_mean(grads)
+    newp, newstate = adamw_step(params, g, state, **hyper)
+    return newp, newstate, float(np.mean(losses)), g
+
+
+# --------------------------------------------------------------------------
+# decision bands for parity
+# --------------------------------------------------------------------------
+def decision_bands(cache: dict, tau: float = 1e-6, var_floor: float = VAR_FLOOR) -> list:
+    """Per layer, boolean masks of the cells whose discrete decision is
+    numerically ambiguous at relative margin ``tau``: |Z| < tau*|Z|_inf (ReLU),
+    top-2 gap between distinct values < tau*|m|_inf (argmax / argmin),
+    |var - eps_v| < 0.5 eps_v (std floor)."""
+    out = []
+    for c in cache["layers"]:
+        zs = np.abs(c["Z"]).max() if c["Z"].size else 0.0
+        relu_band = np.abs(c["Z"]) < tau * zs
+        msg = c["msg"]
+        ms = np.abs(msg).max() if msg.size else 0.0
+        rowptr = np.concatenate([[0], np.cumsum(c["deg"])])
+        row = np.repeat(np.arange(c["N"]), c["deg"])
+        mx2 = _seg_reduce(np.maximum, np.where(msg == c["mx"][row], -np.inf, msg), rowptr, -np.inf)
+        mn2 = _seg_reduce(np.minimum, np.where(msg == c["mn"][row], np.inf, msg), rowptr, np.inf)
+        max_band = (c["mx"] - mx2) < tau * ms
+        min_band = (mn2 - c["mn"]) < tau * ms
+        var_band = np.abs(c["var"] - var_floor) < 0.5 * var_floor
+        out.append(dict(relu=relu_band, argmax=max_band, argmin=min_band, varflag=var_band))
+    return out
+
+
+def replay(cache: dict, gpu: list, tau: float = 1e-6, head_relu_gpu=None):
+    """Build ``decisions`` for ``backward``: inside each ambiguity band adopt the
+    GPU's decision, elsewhere keep the oracle's. Returns (decisions, n_overrides)."""
+    bands = decision_bands(cache, tau)
+    dec, n = {}, 0
+    for l, (c, b, gdec) in enumerate(zip(cache["layers"], bands, gpu)):
+        own = dict(relu=c["Z"] > 0, argmax=c["argmax"], argmin=c["argmin"], varflag=c["var"] > VAR_FLOOR)
+        d = {}
+        for k in own:
+            if k not in gdec:
+                d[k] = own[k]
+                continue
+            sel = b[k] & (np.asarray(gdec[k]) != own[k])
+            n += int(sel.sum())
+            d[k] = np.where(b[k], gdec[k], own[k])
+        dec[l] = d
+    if head_relu_gpu is not None:
+        hp = cache["head"]["hpre"]
+        band = np.abs(hp) < tau * (np.abs(hp).max() if hp.size else 0.0)
+        own = hp > 0
+        n += int((band & (head_relu_gpu != own)).sum())
+        dec["head_relu"] = np.where(band, head_relu_gpu, own)
+    return dec, n
