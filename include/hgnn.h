@@ -1,0 +1,245 @@
+/*
+ * hgnn.h — C-ABI of the B200-native HydraGNN (PNA-GCNN) data-parallel training step.
+ *
+ * The calls follow the paper's problem statement — pack a batch of graphs,
+ * forward, backward, allreduce gradients, step (BASELINE.json north_star;
+ * PAPER.md:160-164 §3.2 "each iteration consists of a forward, backward, and
+ * optimization step"; §4 gradient aggregation with NCCL) —
+ * and mirror the SPEC.md interfaces for this path (SPEC.md:266-283 dataload,
+ * 337-384 gcnn, 435-455 ddp). Everything below is plain C: host or device
+ * pointers, sizes and status codes; no PyTorch types.
+ *
+ * Conventions
+ *  - Every call returns hg_status; HG_OK == 0. On failure hg_last_error()
+ *    returns a thread-local message describing the most recent failure.
+ *  - Argument / shape validation is synchronous. Device work is enqueued
+ *    asynchronously on the ctx's compute stream (the caller's stream handed to
+ *    hg_ctx_create). CUDA / NCCL failures are sticky: once one is seen the ctx
+ *    returns HG_E_STATE from every later device call; hg_sync() reports it.
+ *  - Floating point: fp32 storage and fp32 arithmetic on the device (GEMMs in
+ *    fp32-accurate form); the CPU oracle (tests only) is float64.
+ *  - Ownership: the caller owns every pointer it passes. hg_store_create
+ *    copies (or, with copy == 0, borrows) the arrays; the device workspace is
+ *    caller-owned and must outlive the ctx.
+ */
+#ifndef HGNN_H
+#define HGNN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HG_ABI_VERSION 1
+
+typedef enum {
+  HG_OK = 0,
+  HG_E_INVALID = 1,    /* bad argument (null pointer, negative size, ...) */
+  HG_E_SHAPE = 2,      /* InconsistentFeatureWidth / ShapeMismatch */
+  HG_E_RANGE = 3,      /* IndexOutOfRange: graph id or node id out of range */
+  HG_E_EMPTY = 4,      /* EmptyBatch / EmptyGraphSlot */
+  HG_E_ASYMMETRIC = 5, /* edge list not symmetric with identical attributes */
+  HG_E_DEGREE = 6,     /* a node degree exceeds HG_MAX_DEGREE */
+  HG_E_CAPACITY = 7,   /* batch exceeds the ctx capacities (max_graphs / max_nodes / max_edges) */
+  HG_E_CUDA = 8,       /* CUDA runtime failure */
+  HG_E_NCCL = 9,       /* NCCL failure (TransportFailure) */
+  HG_E_STATE = 10,     /* ctx unusable after a sticky failure, or call out of order */
+  HG_E_UNSORTED = 11   /* per-graph edges not sorted by (src, dst) */
+} hg_status;
+
+/* Largest supported node degree: argmin/argmax positions are stored as u8
+ * with bit 7 reserved for the std variance-floor flag. */
+#define HG_MAX_DEGREE 127
+
+const char *hg_last_error(void);
+int32_t hg_abi_version(void);
+
+/* ======================================================================
+ * Graph store — the Table-1 global arrays (§3.3)
+ * ====================================================================== */
+typedef struct hg_store hg_store;
+
+typedef struct {
+  int64_t num_graphs, num_nodes, num_edges;
+  int32_t f_node, f_edge;            /* F0 = |vocab| + 3, Fe = 4 */
+  const int64_t *node_offset;        /* [num_graphs + 1], starts at 0, non-decreasing */
+  const int64_t *edge_offset;        /* [num_graphs + 1], starts at 0, non-decreasing */
+  const float *x;                    /* [num_nodes][f_node] row-major */
+  const int32_t *edge_index;         /* [2][num_edges]: row 0 = src, row 1 = dst, graph-local ids,
+                                        per graph sorted by (src, dst), each bond in both directions */
+  const float *edge_attr;            /* [num_edges][f_edge] */
+  const float *y;                    /* [num_graphs] target (eV) */
+} hg_store_desc;
+
+/* Validate and adopt a store. copy != 0: arrays are copied (caller may free on
+ * return); copy == 0: arrays are borrowed and must outlive the store.
+ * Validation (multi-threaded over graphs, `threads` <= 0 = all cores):
+ * ids in range (HG_E_RANGE), per-graph (src, dst) order strictly increasing
+ * (HG_E_UNSORTED), symmetry with identical attributes (HG_E_ASYMMETRIC),
+ * degree <= HG_MAX_DEGREE (HG_E_DEGREE), every graph non-empty (HG_E_EMPTY).
+ * Also derives, per directed edge, slot = position of src inside dst's
+ * neighbour row. */
+hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads, hg_store **out);
+hg_status hg_store_destroy(hg_store *s);
+/* Totals and maxima over the store (Table 2 style summary). */
+hg_status hg_store_stats(const hg_store *s, int64_t *graphs, int64_t *nodes, int64_t *edges,
+                         int32_t *max_nodes_per_graph, int32_t *max_degree);
+/* PNA degree statistic delta = mean over the nodes of graphs `ids` of ln(d+1),
+ * float64. ids == NULL: all graphs. */
+hg_status hg_degree_stat(const hg_store *s, const int64_t *ids, int64_t n, double *delta);
+
+/* ======================================================================
+ * Sharding ("shuffled and disjointed subsets")
+ * Global per-epoch permutation of [0, n) ascending by (splitmix64(seed ^
+ * epoch*0x9E3779B97F4A7C15 ^ i*0xD1B54A32D192ED03), i); rank takes positions
+ * p == rank (mod world), drop-last to floor(n/world).
+ * ids_out capacity >= n / world. Host-only, deterministic.
+ * ====================================================================== */
+hg_status hg_shard(uint64_t seed, int64_t epoch, int32_t rank, int32_t world, int64_t n,
+                   int64_t *ids_out, int64_t *n_out);
+
+/* ======================================================================
+ * Model configuration
+ * ====================================================================== */
+typedef struct {
+  int32_t f_node, f_edge;            /* input widths F0, Fe */
+  int32_t hidden;                    /* H: multiple of 32 */
+  int32_t layers;                    /* L >= 1 conv layers */
+  int32_t fc_hidden;                 /* Hf: head hidden width (= H) */
+  int32_t max_graphs;                /* capacity: graphs per batch */
+  int32_t max_nodes;                 /* capacity: nodes per batch */
+  int32_t max_edges;                 /* capacity: directed edges per batch */
+  int32_t n_slots;                   /* device batch slots (>= 1; 2+ to overlap H2D with compute) */
+  int32_t reserved;
+  double delta;                      /* PNA degree statistic (hg_degree_stat) */
+  float var_floor;                   /* epsilon_v for the std aggregator, 1e-10 */
+  float pad;
+} hg_config;
+
+typedef struct {
+  float lr, beta1, beta2, eps, weight_decay;  /* 1e-3, 0.9, 0.999, 1e-8, 0.01 */
+} hg_adamw;
+
+/* ---- packed batch layout -----------------------------------
+ * One contiguous blob per batch (host staging and device slot alike):
+ *   header   int32[16]: B, N, E, F0, Fe, then zeros
+ *   graph_ptr int32[B+1]   cumulative node counts
+ *   y         float[B]
+ *   rowptr    int32[N+1]   CSR over destination nodes
+ *   col       int32[E]     in-neighbour ids, ascending within a row
+ *   x         float[N*F0]
+ *   eattr     float[E*Fe]  attribute of edge col -> row
+ *   slot      uint8[E]     position of row inside col's row
+ * each array starting at a 16-byte aligned offset given by hg_batch_offsets. */
+typedef struct {
+  int64_t graph_ptr, y, rowptr, col, x, eattr, slot, total;  /* byte offsets; total = blob size */
+} hg_batch_offsets;
+hg_status hg_batch_offsets_get(int32_t B, int32_t N, int32_t E, int32_t f_node, int32_t f_edge,
+                               hg_batch_offsets *off);
+
+/* Host-only collate: gather graphs `ids` (B of them, in
+ * order) from the store into `dst` (capacity `cap` bytes) in the layout above.
+ * Fails with HG_E_EMPTY (B == 0), HG_E_RANGE, HG_E_SHAPE (widths differ from
+ * cfg), HG_E_CAPACITY (exceeds cfg capacities or cap). *used = blob bytes. */
+hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const hg_config *cfg,
+                       void *dst, size_t cap, size_t *used);
+
+/* Host-side parameter initialisation into a flat fp32 array laid out like the
+ * device arena (hg_param_info offsets; padding zero). SPEC.md:339, 401 with the
+ * counter-based rule of SURVEY C12. n_elems = hg_param_layout total. */
+hg_status hg_param_layout(const hg_config *c, int32_t *n_tensors, int64_t *n_elems);
+hg_status hg_param_layout_info(const hg_config *c, int32_t i, const char **name, int64_t *offset,
+                               int32_t *rows, int32_t *cols);
+hg_status hg_params_init_host(const hg_config *c, uint64_t seed, float *dst);
+
+/* ======================================================================
+ * Device context (one per rank / GPU)
+ * ====================================================================== */
+typedef struct hg_ctx hg_ctx;
+
+/* Bytes of device workspace the ctx needs (params, grads, Adam moments,
+ * batch slots, per-layer activations, backward scratch), 256-byte aligned. */
+hg_status hg_workspace_bytes(const hg_config *c, size_t *bytes);
+/* workspace: caller-owned device memory of >= hg_workspace_bytes bytes on
+ * `device`; stream: the caller's cudaStream_t (NULL = legacy default stream).
+ * Parameters start zeroed; call hg_params_init or hg_params_set. */
+hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, size_t bytes,
+                        void *stream, hg_ctx **out);
+hg_status hg_ctx_destroy(hg_ctx *x);
+
+hg_status hg_param_count(const hg_ctx *x, int32_t *n_tensors, int64_t *n_elems);
+hg_status hg_param_info(const hg_ctx *x, int32_t i, const char **name, int64_t *offset,
+                        int32_t *rows, int32_t *cols);
+hg_status hg_params_init(hg_ctx *x, uint64_t seed);
+/* on_device != 0: src/dst are device pointers; else host pointers. Arrays are
+ * the flat arena (n_elems floats). Synchronous w.r.t. the compute stream. */
+hg_status hg_params_set(hg_ctx *x, const float *src, int32_t on_device);
+hg_status hg_params_get(hg_ctx *x, float *dst, int32_t on_device);
+hg_status hg_grads_get(hg_ctx *x, float *dst, int32_t on_device);
+hg_status hg_opt_state_get(hg_ctx *x, float *m, float *v, int64_t *step, int32_t on_device);
+hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t step, int32_t on_device);
+
+/* Debug / parity views into the workspace: byte offset and size of a named
+ * buffer. what: 0 = P_l [N,H], 1 = A_l [N,4H] (mean|min|max|std), 2 = arg_l
+ * [N,2H] u8 (argmin | argmax with bit7 = var>floor), 3 = X_{l+1} [N,H],
+ * 4 = batch slot `layer` blob, 5 = yhat [B], 6 = loss [1], 7 = head hidden
+ * pre-activation [B,Hf], 8 = params, 9 = grads, 10 = amp [N], 11 = att [N]. */
+hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_t *offset, int64_t *bytes);
+
+/* Collate `ids` from the store on the host (pinned staging buffer of `slot`)
+ * and enqueue the H2D copy on the ctx's copy stream; later device work on
+ * that slot waits for it. The staging buffer is reused only after its
+ * previous copy completed. Errors as hg_pack_host. */
+hg_status hg_pack(hg_ctx *x, const hg_store *s, const int64_t *ids, int32_t B, int32_t slot);
+/* Copy an already packed blob (host pointer, e.g. from hg_pack_host) into `slot`. */
+hg_status hg_upload_packed(hg_ctx *x, const void *blob, size_t bytes, int32_t slot);
+
+/* Forward pass on the batch in `slot`: L GC layers, global
+ * mean pool, FC head, MSE
+ * loss written to the device loss cell. */
+hg_status hg_forward(hg_ctx *x, int32_t slot);
+/* Backward pass of the last forward on `slot`: writes every
+ * parameter gradient (overwrites, no accumulation). */
+hg_status hg_backward(hg_ctx *x, int32_t slot);
+
+/* NCCL data-parallel plumbing. The 128-byte unique id is
+ * produced on rank 0 and distributed by the caller (e.g. torch.distributed). */
+hg_status hg_nccl_unique_id(void *out128);
+hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world);
+/* Mean over ranks of the gradient arena; no-op when world == 1. */
+hg_status hg_allreduce_grads(hg_ctx *x);
+
+/* Fused AdamW over the whole parameter arena. */
+hg_status hg_step(hg_ctx *x, const hg_adamw *h);
+
+/* forward + backward + allreduce + AdamW in one call; the device work is
+ * captured once per slot into a CUDA graph and replayed (graph == 0 disables). */
+hg_status hg_train_step(hg_ctx *x, int32_t slot, const hg_adamw *h, int32_t graph);
+
+/* Capture (without running) the CUDA graph hg_train_step replays for `slot`. */
+hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h);
+
+/* Instrumented step (no graph): runs forward + backward + allreduce + AdamW
+ * eagerly with CUDA events around every kernel class and returns, per phase,
+ * the summed device milliseconds (ms[HG_PHASE_COUNT]) and kernel launches
+ * (launches[HG_PHASE_COUNT], nullable). Synchronises. (SPEC.md:429-432 PhaseTimings) */
+enum {
+  HG_PHASE_SCALERS = 0, HG_PHASE_PROJ = 1, HG_PHASE_AGG_FWD = 2, HG_PHASE_UPDATE = 3, HG_PHASE_HEAD_FWD = 4,
+  HG_PHASE_HEAD_BWD = 5, HG_PHASE_DA = 6, HG_PHASE_DU = 7, HG_PHASE_AGG_BWD = 8, HG_PHASE_DMX = 9,
+  HG_PHASE_DX = 10, HG_PHASE_ALLREDUCE = 11, HG_PHASE_ADAMW = 12, HG_PHASE_COUNT = 13
+};
+hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms, int64_t *launches);
+
+/* Read the loss of the last forward (synchronises the compute stream). */
+hg_status hg_loss_get(hg_ctx *x, float *loss);
+/* Synchronise the ctx's streams; surfaces sticky CUDA/NCCL errors. */
+hg_status hg_sync(hg_ctx *x);
+/* Number of kernels this ctx has launched (graph replays count their kernel nodes). */
+hg_status hg_launch_count(const hg_ctx *x, int64_t *count);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HGNN_H */

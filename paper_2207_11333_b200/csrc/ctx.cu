@@ -1,0 +1,663 @@
+// ctx.cu — device context of the C-ABI: workspace plan, batch slots with an
+// async H2D ring, the per-step kernel sequence (forward / backward / step),
+// NCCL gradient averaging and CUDA-graph capture of a
+// whole training step.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hgnn.h"
+#include "internal.h"
+#include "kernels.h"
+#include "layout.h"
+
+using namespace hg;
+
+namespace {
+
+struct Plan {
+  size_t params = 0, grads = 0, m = 0, v = 0, adam = 0, loss = 0;
+  std::vector<size_t> slot;
+  size_t blob_max = 0;
+  size_t amp = 0, att = 0;
+  std::vector<size_t> P, A, arg, X;  // X[l] = output of layer l (X_{l+1})
+  size_t dZa = 0, dZb = 0, dA = 0, dP = 0;
+  size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
+  size_t part = 0;
+  size_t total = 0;
+};
+
+Plan make_plan(const hg_config &c) {
+  Plan p;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off = (size_t)align256((int64_t)(off + bytes));
+    return o;
+  };
+  const auto lay = param_layout(c);
+  const size_t PB = sizeof(float) * (size_t)param_total(lay);
+  const size_t N = c.max_nodes, H = c.hidden, B = c.max_graphs, Hf = c.fc_hidden;
+  p.params = take(PB);
+  p.grads = take(PB);
+  p.m = take(PB);
+  p.v = take(PB);
+  p.adam = take(sizeof(AdamDev));
+  p.loss = take(sizeof(float) * 4);
+  p.blob_max = (size_t)batch_offsets(c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge).total;
+  for (int s = 0; s < c.n_slots; ++s) p.slot.push_back(take(p.blob_max));
+  p.amp = take(sizeof(float) * N);
+  p.att = take(sizeof(float) * N);
+  for (int l = 0; l < c.layers; ++l) {
+    p.P.push_back(take(sizeof(float) * N * H));
+    p.A.push_back(take(sizeof(float) * N * 4 * H));
+    p.arg.push_back(take(N * 2 * H));
+    p.X.push_back(take(sizeof(float) * N * H));
+  }
+  const size_t Fmax = std::max<size_t>(H, c.f_node);
+  p.dZa = take(sizeof(float) * N * Fmax);
+  p.dZb = take(sizeof(float) * N * Fmax);
+  p.dA = take(sizeof(float) * N * 4 * H);
+  p.dP = take(sizeof(float) * N * H);
+  p.G = take(sizeof(float) * B * H);
+  p.hpre = take(sizeof(float) * B * Hf);
+  p.dhid = take(sizeof(float) * B * Hf);
+  p.yhat = take(sizeof(float) * B);
+  p.dy = take(sizeof(float) * B);
+  p.sqerr = take(sizeof(float) * B);
+  Caps caps{c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge, c.hidden, c.fc_hidden};
+  size_t pf = std::max({agg_bwd_partial_floats(caps), dU_partial_floats(caps), dMx_partial_floats(caps, c.f_node),
+                        dMx_partial_floats(caps, c.hidden)});
+  p.part = take(sizeof(float) * pf);
+  p.total = off;
+  return p;
+}
+
+}  // namespace
+
+struct hg_ctx {
+  hg_config cfg{};
+  Caps caps{};
+  Plan plan;
+  std::vector<TensorInfo> lay;
+  int64_t n_params = 0;
+  int device = 0;
+  uint8_t *ws = nullptr;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  std::vector<void *> staging;
+  std::vector<cudaEvent_t> copy_done, compute_done;
+  std::vector<cudaGraphExec_t> graphs;
+  std::vector<int64_t> graph_kernels;
+  std::vector<hg_adamw> graph_hyper;
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  int64_t launches = 0;
+  hg_status sticky = HG_OK;
+  std::string sticky_msg;
+
+  float *f(size_t off) const { return reinterpret_cast<float *>(ws + off); }
+  uint8_t *b(size_t off) const { return ws + off; }
+  float *param(const std::string &name) const {
+    for (auto &t : lay)
+      if (t.name == name) return f(plan.params) + t.offset;
+    return nullptr;
+  }
+  float *grad(const std::string &name) const {
+    for (auto &t : lay)
+      if (t.name == name) return f(plan.grads) + t.offset;
+    return nullptr;
+  }
+};
+
+namespace {
+
+hg_status cuda_fail(hg_ctx *x, cudaError_t e, const char *what) {
+  hg_status st = fail(HG_E_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  if (x) {
+    x->sticky = HG_E_CUDA;
+    x->sticky_msg = hg_last_error();
+  }
+  return st;
+}
+
+#define CK(x, call)                                   \
+  do {                                                \
+    cudaError_t e_ = (call);                          \
+    if (e_ != cudaSuccess) return cuda_fail(x, e_, #call); \
+  } while (0)
+
+hg_status nccl_fail(hg_ctx *x, ncclResult_t r, const char *what) {
+  hg_status st = fail(HG_E_NCCL, "%s: %s", what, ncclGetErrorString(r));
+  if (x) {
+    x->sticky = HG_E_NCCL;
+    x->sticky_msg = hg_last_error();
+  }
+  return st;
+}
+
+hg_status usable(hg_ctx *x) {
+  if (!x) return fail(HG_E_INVALID, "null ctx");
+  if (x->sticky != HG_OK) return fail(HG_E_STATE, "ctx unusable after earlier failure: %s", x->sticky_msg.c_str());
+  return HG_OK;
+}
+
+hg_status check_slot(hg_ctx *x, int32_t slot) {
+  if (slot < 0 || slot >= x->cfg.n_slots) return fail(HG_E_RANGE, "slot %d out of range", slot);
+  return HG_OK;
+}
+
+std::string lname(int l, const char *t) { return "conv" + std::to_string(l) + "." + t; }
+
+// Instrumented (non-graph) mode: CUDA events around every kernel-class call
+// (SURVEY §5 "phase timings"; SPEC.md:429-432 PhaseTimings).
+struct Prof {
+  cudaStream_t st;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> marks;
+  std::vector<int64_t> launches;
+  Prof(cudaStream_t s) : st(s), launches(HG_PHASE_COUNT, 0) {}
+  ~Prof() {
+    for (auto &m : marks) {
+      cudaEventDestroy(m.second.first);
+      cudaEventDestroy(m.second.second);
+    }
+  }
+};
+
+template <class F>
+void phase(Prof *pr, int ph, F &&fn) {
+  if (!pr) {
+    fn();
+    return;
+  }
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, pr->st);
+  const int64_t l0 = launches_so_far();
+  fn();
+  pr->launches[ph] += launches_so_far() - l0;
+  cudaEventRecord(b, pr->st);
+  pr->marks.push_back({ph, {a, b}});
+}
+
+// ---- the step's kernel sequence (enqueue only) ----
+void enqueue_forward(hg_ctx *x, int slot, Prof *pr = nullptr) {
+  const hg_config &c = x->cfg;
+  const Plan &p = x->plan;
+  const uint8_t *blob = x->b(p.slot[slot]);
+  cudaStream_t st = x->stream;
+  float *amp = x->f(p.amp), *att = x->f(p.att);
+  phase(pr, HG_PHASE_SCALERS, [&] { launch_scalers(st, x->caps, blob, c.delta, amp, att); });
+  for (int l = 0; l < c.layers; ++l) {
+    const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
+    const int F = l == 0 ? c.f_node : c.hidden;
+    phase(pr, HG_PHASE_PROJ, [&] { launch_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l])); });
+    phase(pr, HG_PHASE_AGG_FWD, [&] {
+      launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
+                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]));
+    });
+    phase(pr, HG_PHASE_UPDATE, [&] {
+      launch_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")), x->param(lname(l, "b_U")),
+                    x->f(p.X[l]));
+    });
+  }
+  phase(pr, HG_PHASE_HEAD_FWD, [&] {
+    launch_head_fwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
+                    x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat), x->f(p.sqerr),
+                    x->f(p.loss));
+  });
+}
+
+void enqueue_backward(hg_ctx *x, int slot, Prof *pr = nullptr) {
+  const hg_config &c = x->cfg;
+  const Plan &p = x->plan;
+  const uint8_t *blob = x->b(p.slot[slot]);
+  cudaStream_t st = x->stream;
+  float *amp = x->f(p.amp), *att = x->f(p.att);
+  float *dZ = x->f(p.dZa), *dZn = x->f(p.dZb);
+  phase(pr, HG_PHASE_HEAD_BWD, [&] {
+    launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"), x->f(p.G),
+                    x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
+                    x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
+  });
+  for (int l = c.layers - 1; l >= 0; --l) {
+    phase(pr, HG_PHASE_DA, [&] { launch_dA(st, x->caps, blob, dZ, amp, att, x->param(lname(l, "U")), x->f(p.dA)); });
+    phase(pr, HG_PHASE_DU, [&] {
+      launch_dU(st, x->caps, blob, dZ, x->f(p.A[l]), amp, att, x->f(p.part), x->grad(lname(l, "U")),
+                x->grad(lname(l, "b_U")));
+    });
+    phase(pr, HG_PHASE_AGG_BWD, [&] {
+      launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), x->f(p.dP), x->f(p.part), x->grad(lname(l, "M_e")));
+    });
+    const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
+    const int F = l == 0 ? c.f_node : c.hidden;
+    phase(pr, HG_PHASE_DMX, [&] {
+      launch_dMx(st, x->caps, blob, x->f(p.dP), Xl, F, x->f(p.part), x->grad(lname(l, "M_x")),
+                 x->grad(lname(l, "b_M")));
+    });
+    if (l > 0) {
+      phase(pr, HG_PHASE_DX, [&] { launch_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn); });
+      std::swap(dZ, dZn);
+    }
+  }
+}
+
+hg_status enqueue_allreduce(hg_ctx *x) {
+  if (x->world <= 1 || !x->comm) return HG_OK;
+  ncclResult_t r = ncclAllReduce(x->f(x->plan.grads), x->f(x->plan.grads), (size_t)x->n_params, ncclFloat32, ncclAvg,
+                                 x->comm, x->stream);
+  if (r != ncclSuccess) return nccl_fail(x, r, "ncclAllReduce");
+  return HG_OK;
+}
+
+void enqueue_step(hg_ctx *x, const hg_adamw &h, Prof *pr = nullptr) {
+  const Plan &p = x->plan;
+  phase(pr, HG_PHASE_ADAMW, [&] {
+    launch_adamw(x->stream, x->f(p.params), x->f(p.grads), x->f(p.m), x->f(p.v), x->n_params,
+                 reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay);
+  });
+}
+
+hg_status after_enqueue(hg_ctx *x, const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(x, e, what);
+  return HG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+hg_status hg_workspace_bytes(const hg_config *c, size_t *bytes) {
+  hg_status st = check_config(c);
+  if (st) return st;
+  if (!bytes) return fail(HG_E_INVALID, "null output");
+  *bytes = make_plan(*c).total;
+  return HG_OK;
+}
+
+hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, size_t bytes, void *stream,
+                        hg_ctx **out) {
+  hg_status st = check_config(c);
+  if (st) return st;
+  if (!out || !workspace) return fail(HG_E_INVALID, "null argument");
+  *out = nullptr;
+  Plan plan = make_plan(*c);
+  if (bytes < plan.total) return fail(HG_E_CAPACITY, "workspace too small: %zu < %zu", bytes, plan.total);
+  if (((uintptr_t)workspace & 255) != 0) return fail(HG_E_INVALID, "workspace must be 256-byte aligned");
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
+  hg_ctx *x = new hg_ctx();
+  x->cfg = *c;
+  x->caps = Caps{c->max_graphs, c->max_nodes, c->max_edges, c->f_node, c->f_edge, c->hidden, c->fc_hidden};
+  x->plan = plan;
+  x->lay = param_layout(*c);
+  x->n_params = param_total(x->lay);
+  x->device = device;
+  x->ws = (uint8_t *)workspace;
+  x->stream = (cudaStream_t)stream;
+  auto bail = [&](cudaError_t err, const char *what) {
+    hg_status s2 = cuda_fail(nullptr, err, what);
+    hg_ctx_destroy(x);
+    return s2;
+  };
+  if ((e = cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail(e, "cudaStreamCreate");
+  for (int s = 0; s < c->n_slots; ++s) {
+    void *h = nullptr;
+    if ((e = cudaHostAlloc(&h, plan.blob_max, cudaHostAllocDefault)) != cudaSuccess) return bail(e, "cudaHostAlloc");
+    x->staging.push_back(h);
+    cudaEvent_t a, b2;
+    if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
+    x->copy_done.push_back(a);
+    if ((e = cudaEventCreateWithFlags(&b2, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
+    x->compute_done.push_back(b2);
+    x->graphs.push_back(nullptr);
+    x->graph_kernels.push_back(0);
+    x->graph_hyper.push_back(hg_adamw{});
+  }
+  if ((e = cudaMemsetAsync(workspace, 0, plan.total, x->stream)) != cudaSuccess) return bail(e, "cudaMemsetAsync");
+  if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
+  *out = x;
+  return HG_OK;
+}
+
+hg_status hg_ctx_destroy(hg_ctx *x) {
+  if (!x) return HG_OK;
+  if (x->stream || x->copy_stream) cudaDeviceSynchronize();
+  for (auto g : x->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto h : x->staging) cudaFreeHost(h);
+  for (auto ev : x->copy_done) cudaEventDestroy(ev);
+  for (auto ev : x->compute_done) cudaEventDestroy(ev);
+  if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
+  if (x->comm) ncclCommDestroy(x->comm);
+  delete x;
+  return HG_OK;
+}
+
+hg_status hg_param_count(const hg_ctx *x, int32_t *n_tensors, int64_t *n_elems) {
+  if (!x) return fail(HG_E_INVALID, "null ctx");
+  if (n_tensors) *n_tensors = (int32_t)x->lay.size();
+  if (n_elems) *n_elems = x->n_params;
+  return HG_OK;
+}
+
+hg_status hg_param_info(const hg_ctx *x, int32_t i, const char **name, int64_t *offset, int32_t *rows,
+                        int32_t *cols) {
+  if (!x) return fail(HG_E_INVALID, "null ctx");
+  if (i < 0 || i >= (int32_t)x->lay.size()) return fail(HG_E_RANGE, "tensor index out of range");
+  if (name) *name = x->lay[i].name.c_str();
+  if (offset) *offset = x->lay[i].offset;
+  if (rows) *rows = x->lay[i].rows;
+  if (cols) *cols = x->lay[i].cols;
+  return HG_OK;
+}
+
+static hg_status copy_arena(hg_ctx *x, void *dst, const void *src, size_t bytes, int on_device, bool to_dev) {
+  cudaMemcpyKind k = on_device ? cudaMemcpyDeviceToDevice : (to_dev ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost);
+  CK(x, cudaMemcpyAsync(dst, src, bytes, k, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  return HG_OK;
+}
+
+hg_status hg_params_init(hg_ctx *x, uint64_t seed) {
+  hg_status st = usable(x);
+  if (st) return st;
+  std::vector<float> h((size_t)x->n_params);
+  init_params_host(x->cfg, seed, h.data());
+  const size_t PB = sizeof(float) * (size_t)x->n_params;
+  CK(x, cudaMemcpyAsync(x->f(x->plan.params), h.data(), PB, cudaMemcpyHostToDevice, x->stream));
+  CK(x, cudaMemsetAsync(x->f(x->plan.m), 0, PB, x->stream));
+  CK(x, cudaMemsetAsync(x->f(x->plan.v), 0, PB, x->stream));
+  CK(x, cudaMemsetAsync(x->f(x->plan.grads), 0, PB, x->stream));
+  CK(x, cudaMemsetAsync(x->b(x->plan.adam), 0, sizeof(AdamDev), x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  return HG_OK;
+}
+
+hg_status hg_params_set(hg_ctx *x, const float *src, int32_t on_device) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!src) return fail(HG_E_INVALID, "null source");
+  return copy_arena(x, x->f(x->plan.params), src, sizeof(float) * (size_t)x->n_params, on_device, true);
+}
+
+hg_status hg_params_get(hg_ctx *x, float *dst, int32_t on_device) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!dst) return fail(HG_E_INVALID, "null destination");
+  return copy_arena(x, dst, x->f(x->plan.params), sizeof(float) * (size_t)x->n_params, on_device, false);
+}
+
+hg_status hg_grads_get(hg_ctx *x, float *dst, int32_t on_device) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!dst) return fail(HG_E_INVALID, "null destination");
+  return copy_arena(x, dst, x->f(x->plan.grads), sizeof(float) * (size_t)x->n_params, on_device, false);
+}
+
+hg_status hg_opt_state_get(hg_ctx *x, float *m, float *v, int64_t *step, int32_t on_device) {
+  hg_status st = usable(x);
+  if (st) return st;
+  const size_t PB = sizeof(float) * (size_t)x->n_params;
+  if (m && (st = copy_arena(x, m, x->f(x->plan.m), PB, on_device, false))) return st;
+  if (v && (st = copy_arena(x, v, x->f(x->plan.v), PB, on_device, false))) return st;
+  if (step) {
+    AdamDev ad;
+    CK(x, cudaMemcpyAsync(&ad, x->b(x->plan.adam), sizeof(ad), cudaMemcpyDeviceToHost, x->stream));
+    CK(x, cudaStreamSynchronize(x->stream));
+    *step = ad.step;
+  }
+  return HG_OK;
+}
+
+hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t step, int32_t on_device) {
+  hg_status st = usable(x);
+  if (st) return st;
+  const size_t PB = sizeof(float) * (size_t)x->n_params;
+  if (m && (st = copy_arena(x, x->f(x->plan.m), m, PB, on_device, true))) return st;
+  if (v && (st = copy_arena(x, x->f(x->plan.v), v, PB, on_device, true))) return st;
+  AdamDev ad{step, 0.f, 0.f};
+  CK(x, cudaMemcpyAsync(x->b(x->plan.adam), &ad, sizeof(ad), cudaMemcpyHostToDevice, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  return HG_OK;
+}
+
+hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_t *offset, int64_t *bytes) {
+  if (!x || !offset || !bytes) return fail(HG_E_INVALID, "null argument");
+  const hg_config &c = x->cfg;
+  const Plan &p = x->plan;
+  const int64_t N = c.max_nodes, H = c.hidden, B = c.max_graphs;
+  const bool needs_layer = what >= 0 && what <= 3;
+  if (needs_layer && (layer < 0 || layer >= c.layers)) return fail(HG_E_RANGE, "layer out of range");
+  switch (what) {
+    case 0: *offset = p.P[layer]; *bytes = 4 * N * H; break;
+    case 1: *offset = p.A[layer]; *bytes = 16 * N * H; break;
+    case 2: *offset = p.arg[layer]; *bytes = 2 * N * H; break;
+    case 3: *offset = p.X[layer]; *bytes = 4 * N * H; break;
+    case 4:
+      if (layer < 0 || layer >= c.n_slots) return fail(HG_E_RANGE, "slot out of range");
+      *offset = p.slot[layer]; *bytes = p.blob_max; break;
+    case 5: *offset = p.yhat; *bytes = 4 * B; break;
+    case 6: *offset = p.loss; *bytes = 4; break;
+    case 7: *offset = p.hpre; *bytes = 4 * B * c.fc_hidden; break;
+    case 8: *offset = p.params; *bytes = 4 * x->n_params; break;
+    case 9: *offset = p.grads; *bytes = 4 * x->n_params; break;
+    case 10: *offset = p.amp; *bytes = 4 * N; break;
+    case 11: *offset = p.att; *bytes = 4 * N; break;
+    default: return fail(HG_E_RANGE, "unknown view %d", what);
+  }
+  return HG_OK;
+}
+
+hg_status hg_pack(hg_ctx *x, const hg_store *s, const int64_t *ids, int32_t B, int32_t slot) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  // the staging buffer may still be the source of an in-flight copy
+  CK(x, cudaEventSynchronize(x->copy_done[slot]));
+  size_t used = 0;
+  st = hg_pack_host(s, ids, B, &x->cfg, x->staging[slot], x->plan.blob_max, &used);
+  if (st) return st;
+  // the device slot may still be read by an earlier step
+  CK(x, cudaStreamWaitEvent(x->copy_stream, x->compute_done[slot], 0));
+  CK(x, cudaMemcpyAsync(x->b(x->plan.slot[slot]), x->staging[slot], used, cudaMemcpyHostToDevice, x->copy_stream));
+  CK(x, cudaEventRecord(x->copy_done[slot], x->copy_stream));
+  return HG_OK;
+}
+
+hg_status hg_upload_packed(hg_ctx *x, const void *blob, size_t bytes, int32_t slot) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  if (!blob || bytes < (size_t)kHeaderInts * 4) return fail(HG_E_INVALID, "bad blob");
+  const int32_t *h = (const int32_t *)blob;
+  if (h[0] < 1) return fail(HG_E_EMPTY, "EmptyBatch");
+  if (h[0] > x->cfg.max_graphs || h[1] > x->cfg.max_nodes || h[2] > x->cfg.max_edges)
+    return fail(HG_E_CAPACITY, "blob exceeds ctx capacity");
+  if (h[3] != x->cfg.f_node || h[4] != x->cfg.f_edge) return fail(HG_E_SHAPE, "blob feature widths differ");
+  const size_t need = (size_t)batch_offsets(h[0], h[1], h[2], h[3], h[4]).total;
+  if (bytes < need) return fail(HG_E_SHAPE, "blob shorter than its header implies");
+  CK(x, cudaEventSynchronize(x->copy_done[slot]));
+  std::memcpy(x->staging[slot], blob, need);
+  CK(x, cudaStreamWaitEvent(x->copy_stream, x->compute_done[slot], 0));
+  CK(x, cudaMemcpyAsync(x->b(x->plan.slot[slot]), x->staging[slot], need, cudaMemcpyHostToDevice, x->copy_stream));
+  CK(x, cudaEventRecord(x->copy_done[slot], x->copy_stream));
+  return HG_OK;
+}
+
+hg_status hg_forward(hg_ctx *x, int32_t slot) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
+  const int64_t l0 = launches_so_far();
+  enqueue_forward(x, slot);
+  x->launches += launches_so_far() - l0;
+  return after_enqueue(x, "forward launch");
+}
+
+hg_status hg_backward(hg_ctx *x, int32_t slot) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  const int64_t l0 = launches_so_far();
+  enqueue_backward(x, slot);
+  x->launches += launches_so_far() - l0;
+  if ((st = after_enqueue(x, "backward launch"))) return st;
+  CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
+  return HG_OK;
+}
+
+hg_status hg_nccl_unique_id(void *out128) {
+  if (!out128) return fail(HG_E_INVALID, "null output");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return nccl_fail(nullptr, r, "ncclGetUniqueId");
+  static_assert(sizeof(ncclUniqueId) == 128, "NCCL unique id must be 128 bytes");
+  std::memcpy(out128, &id, sizeof(id));
+  return HG_OK;
+}
+
+hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!id128 || world < 1 || rank < 0 || rank >= world) return fail(HG_E_INVALID, "bad rank/world");
+  x->rank = rank;
+  x->world = world;
+  if (world == 1) return HG_OK;
+  CK(x, cudaSetDevice(x->device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof(id));
+  ncclResult_t r = ncclCommInitRank(&x->comm, world, id, rank);
+  if (r != ncclSuccess) return nccl_fail(x, r, "ncclCommInitRank");
+  return HG_OK;
+}
+
+hg_status hg_allreduce_grads(hg_ctx *x) {
+  hg_status st = usable(x);
+  if (st) return st;
+  return enqueue_allreduce(x);
+}
+
+hg_status hg_step(hg_ctx *x, const hg_adamw *h) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!h) return fail(HG_E_INVALID, "null hyper");
+  const int64_t l0 = launches_so_far();
+  enqueue_step(x, *h);
+  x->launches += launches_so_far() - l0;
+  return after_enqueue(x, "adamw launch");
+}
+
+hg_status hg_train_step(hg_ctx *x, int32_t slot, const hg_adamw *h, int32_t graph) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  if (!h) return fail(HG_E_INVALID, "null hyper");
+  if (!graph) {
+    if ((st = hg_forward(x, slot)) || (st = hg_backward(x, slot)) || (st = hg_allreduce_grads(x)) ||
+        (st = hg_step(x, h)))
+      return st;
+    return HG_OK;
+  }
+  CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
+  if ((st = hg_capture_step(x, slot, h))) return st;
+  CK(x, cudaGraphLaunch(x->graphs[slot], x->stream));
+  x->launches += x->graph_kernels[slot];
+  CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
+  return HG_OK;
+}
+
+hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  if (!h) return fail(HG_E_INVALID, "null hyper");
+  if (x->graphs[slot] && std::memcmp(&x->graph_hyper[slot], h, sizeof(hg_adamw)) == 0) return HG_OK;
+  if (x->graphs[slot]) {
+    cudaGraphExecDestroy(x->graphs[slot]);
+    x->graphs[slot] = nullptr;
+  }
+  cudaGraph_t g = nullptr;
+  CK(x, cudaStreamBeginCapture(x->stream, cudaStreamCaptureModeThreadLocal));
+  const int64_t l0 = launches_so_far();
+  enqueue_forward(x, slot);
+  enqueue_backward(x, slot);
+  hg_status ar = enqueue_allreduce(x);
+  enqueue_step(x, *h);
+  const int64_t nk = launches_so_far() - l0;
+  cudaError_t e = cudaStreamEndCapture(x->stream, &g);
+  if (ar) {
+    if (g) cudaGraphDestroy(g);
+    return ar;
+  }
+  if (e != cudaSuccess) return cuda_fail(x, e, "cudaStreamEndCapture");
+  cudaGraphExec_t ex = nullptr;
+  e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(x, e, "cudaGraphInstantiate");
+  x->graphs[slot] = ex;
+  x->graph_kernels[slot] = nk;
+  x->graph_hyper[slot] = *h;
+  return HG_OK;
+}
+
+hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms, int64_t *launches) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  if (!h || !ms) return fail(HG_E_INVALID, "null argument");
+  CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
+  Prof pr(x->stream);
+  const int64_t l0 = launches_so_far();
+  enqueue_forward(x, slot, &pr);
+  enqueue_backward(x, slot, &pr);
+  hg_status ar = HG_OK;
+  phase(&pr, HG_PHASE_ALLREDUCE, [&] { ar = enqueue_allreduce(x); });
+  if (ar) return ar;
+  enqueue_step(x, *h, &pr);
+  x->launches += launches_so_far() - l0;
+  if ((st = after_enqueue(x, "profile launch"))) return st;
+  CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  for (int i = 0; i < HG_PHASE_COUNT; ++i) ms[i] = 0.f;
+  for (auto &m : pr.marks) {
+    float t = 0.f;
+    CK(x, cudaEventElapsedTime(&t, m.second.first, m.second.second));
+    ms[m.first] += t;
+  }
+  if (launches)
+    for (int i = 0; i < HG_PHASE_COUNT; ++i) launches[i] = pr.launches[i];
+  return HG_OK;
+}
+
+hg_status hg_loss_get(hg_ctx *x, float *loss) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!loss) return fail(HG_E_INVALID, "null output");
+  CK(x, cudaMemcpyAsync(loss, x->f(x->plan.loss), sizeof(float), cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  return HG_OK;
+}
+
+hg_status hg_sync(hg_ctx *x) {
+  if (!x) return fail(HG_E_INVALID, "null ctx");
+  if (x->sticky != HG_OK) return fail(HG_E_STATE, "%s", x->sticky_msg.c_str());
+  CK(x, cudaStreamSynchronize(x->stream));
+  CK(x, cudaStreamSynchronize(x->copy_stream));
+  if (x->comm) {
+    ncclResult_t ar;
+    ncclResult_t r = ncclCommGetAsyncError(x->comm, &ar);
+    if (r != ncclSuccess) return nccl_fail(x, r, "ncclCommGetAsyncError");
+    if (ar != ncclSuccess) return nccl_fail(x, ar, "NCCL async error");
+  }
+  return HG_OK;
+}
+
+hg_status hg_launch_count(const hg_ctx *x, int64_t *count) {
+  if (!x || !count) return fail(HG_E_INVALID, "null argument");
+  *count = x->launches;
+  return HG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,816 @@
+// kernels.cu — CUDA kernels of the PNA-GCNN training step for sm_100a.
+//
+// Paper passages: message passing GC layer (§3.1; PNA,
+// PAPER.md:148, 315) with the equations SPEC.md:347 fixes; global mean pool
+// (SPEC.md:353); FC head; MSE
+// (SPEC.md:365); backward;
+// AdamW.
+//
+// Design: every reduction is deterministic (fixed order,
+// no float atomics); sizes come from the device-resident batch header so the
+// step is CUDA-graph capturable; segments (CSR rows, degree <= 127) are
+// processed one warp per node with lanes over channels (coalesced 16-byte
+// feature rows).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "kernels.h"
+#include "layout.h"
+
+namespace hg {
+
+std::atomic<int64_t> g_launches{0};
+static inline void counted(int n = 1) { g_launches += n; }
+
+// ------------------------------------------------------------------ batch view
+struct BatchView {
+  int B, N, E, F0, Fe;
+  const int *gp;
+  const float *y;
+  const int *rowptr;
+  const int *col;
+  const float *x;
+  const float *ea;
+  const uint8_t *slot;
+};
+
+__device__ __forceinline__ BatchView load_batch(const uint8_t *blob) {
+  BatchView v;
+  const int *h = reinterpret_cast<const int *>(blob);
+  v.B = h[0]; v.N = h[1]; v.E = h[2]; v.F0 = h[3]; v.Fe = h[4];
+  const BatchOffsets o = batch_offsets(v.B, v.N, v.E, v.F0, v.Fe);
+  v.gp = reinterpret_cast<const int *>(blob + o.graph_ptr);
+  v.y = reinterpret_cast<const float *>(blob + o.y);
+  v.rowptr = reinterpret_cast<const int *>(blob + o.rowptr);
+  v.col = reinterpret_cast<const int *>(blob + o.col);
+  v.x = reinterpret_cast<const float *>(blob + o.x);
+  v.ea = reinterpret_cast<const float *>(blob + o.eattr);
+  v.slot = blob + o.slot;
+  return v;
+}
+
+__device__ __forceinline__ int batch_N(const uint8_t *blob) { return reinterpret_cast<const int *>(blob)[1]; }
+
+static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+static const int kSMs = 148;
+
+// ------------------------------------------------------------------ scalers
+// amplification ln(d+1)/delta and attenuation delta/ln(d+1), both 1 for d = 0
+// (SURVEY C4-C5). Computed in double, stored fp32.
+__global__ void k_scalers(const uint8_t *__restrict__ blob, double delta, float *__restrict__ amp,
+                          float *__restrict__ att) {
+  const BatchView b = load_batch(blob);
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < b.N; i += gridDim.x * blockDim.x) {
+    const int d = b.rowptr[i + 1] - b.rowptr[i];
+    if (d == 0) {
+      amp[i] = 1.0f;
+      att[i] = 1.0f;
+    } else {
+      const double ld = log((double)d + 1.0);
+      amp[i] = (float)(ld / delta);
+      att[i] = (float)(delta / ld);
+    }
+  }
+}
+
+void launch_scalers(cudaStream_t st, const Caps &c, const uint8_t *blob, double delta, float *amp, float *att) {
+  const int blocks = std::min(cdiv(c.maxN, 256), kSMs * 4);
+  k_scalers<<<blocks, 256, 0, st>>>(blob, delta, amp, att);
+  counted();
+}
+
+// ------------------------------------------------------------------ SIMT GEMM (v1)
+// C[M,N] = sum_k a(m,k) b(k,n) with operand transforms supplied by Op; 64x64
+// tiles, BK=16, 256 threads, 4x4 outputs per thread, register-prefetched
+// double-buffered shared memory. A_KMAJ: a(m,k) contiguous in k (else in m);
+// B_KMAJ: b(k,n) contiguous in k (else in n). Persistent over tiles x splits.
+constexpr int GBM = 64, GBN = 64, GBK = 16;
+
+template <bool A_KMAJ, bool B_KMAJ, class Op>
+__global__ void __launch_bounds__(256) k_gemm(Op op_in) {
+  Op op = op_in;
+  op.prepare();
+  __shared__ __align__(16) float As[2][GBK][GBM + 4];
+  __shared__ __align__(16) float Bs[2][GBK][GBN + 4];
+  const int M = op.M(), N = op.N(), K = op.K(), S = op.splits();
+  const int tilesM = (M + GBM - 1) / GBM, tilesN = (N + GBN - 1) / GBN;
+  const int ntiles = tilesM * tilesN * S;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int sp = tile % S;
+    const int t2 = tile / S;
+    const int tn = t2 % tilesN, tm = t2 / tilesN;
+    const int m0 = tm * GBM, n0 = tn * GBN;
+    int kc = (K + S - 1) / S;
+    kc = (kc + GBK - 1) / GBK * GBK;
+    const int kb = sp * kc, ke = min(K, kb + kc);
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+    float ra[4], rb[4];
+    auto load_regs = [&](int k0) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = tid + 256 * r;
+        int ml, kl;
+        if (A_KMAJ) { ml = e / GBK; kl = e % GBK; } else { ml = e % GBM; kl = e / GBM; }
+        const int m = m0 + ml, k = k0 + kl;
+        ra[r] = (m < M && k < ke) ? op.a(m, k) : 0.f;
+        int nl, kl2;
+        if (B_KMAJ) { nl = e / GBK; kl2 = e % GBK; } else { nl = e % GBN; kl2 = e / GBN; }
+        const int n = n0 + nl, k2 = k0 + kl2;
+        rb[r] = (n < N && k2 < ke) ? op.b(k2, n) : 0.f;
+      }
+    };
+    auto store_smem = [&](int buf) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const int e = tid + 256 * r;
+        int ml, kl;
+        if (A_KMAJ) { ml = e / GBK; kl = e % GBK; } else { ml = e % GBM; kl = e / GBM; }
+        As[buf][kl][ml] = ra[r];
+        int nl, kl2;
+        if (B_KMAJ) { nl = e / GBK; kl2 = e % GBK; } else { nl = e % GBN; kl2 = e / GBN; }
+        Bs[buf][kl2][nl] = rb[r];
+      }
+    };
+    if (kb < ke) {
+      load_regs(kb);
+      store_smem(0);
+      __syncthreads();
+      int buf = 0;
+      for (int k0 = kb; k0 < ke; k0 += GBK) {
+        const bool more = k0 + GBK < ke;
+        if (more) load_regs(k0 + GBK);
+#pragma unroll
+        for (int kk = 0; kk < GBK; ++kk) {
+          const float4 a4 = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4]);
+          const float4 b4 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
+          const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+          const float bv[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+        }
+        if (more) {
+          store_smem(buf ^ 1);
+          __syncthreads();
+          buf ^= 1;
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int m = m0 + ty * 4 + i;
+      if (m >= M) continue;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int n = n0 + tx * 4 + j;
+        if (n < N) op.store(m, n, acc[i][j], sp);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <bool AK, bool BK_, class Op>
+static void run_gemm(cudaStream_t st, const Op &op, int maxM, int N, int splits) {
+  const int tiles = cdiv(maxM, GBM) * cdiv(N, GBN) * splits;
+  const int grid = std::max(1, std::min(tiles, kSMs * 8));
+  k_gemm<AK, BK_, Op><<<grid, 256, 0, st>>>(op);
+  counted();
+}
+
+__device__ __forceinline__ float scaler(const float *amp, const float *att, int m, int s) {
+  return s == 0 ? 1.0f : (s == 1 ? amp[m] : att[m]);
+}
+
+// P = X Mx^T  (the message M[x_j || e] + b_M is linear, so the
+// x-part is projected once per node instead of once per edge)
+struct OpProj {
+  const uint8_t *blob; const float *X; const float *Mx; float *P; int F, H;
+  __device__ void prepare() { if (!X) X = load_batch(blob).x; }  // layer 0 reads the batch's x
+  __device__ int M() const { return batch_N(blob); }
+  __device__ int N() const { return H; }
+  __device__ int K() const { return F; }
+  __device__ int splits() const { return 1; }
+  __device__ float a(int m, int k) const { return X[(size_t)m * F + k]; }
+  __device__ float b(int k, int n) const { return Mx[(size_t)n * F + k]; }
+  __device__ void store(int m, int n, float v, int) const { P[(size_t)m * H + n] = v; }
+};
+void launch_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
+                 float *P) {
+  OpProj op{blob, X, Mx, P, F, c.H};
+  run_gemm<true, true>(st, op, c.maxN, c.H, 1);
+}
+
+// Z = [A || amp*A || att*A] U^T + b_U ; X1 = ReLU(Z)
+struct OpUpdate {
+  const uint8_t *blob; const float *A; const float *amp; const float *att; const float *U; const float *bU;
+  float *X1; int H;
+  __device__ void prepare() {}
+  __device__ int M() const { return batch_N(blob); }
+  __device__ int N() const { return H; }
+  __device__ int K() const { return 12 * H; }
+  __device__ int splits() const { return 1; }
+  __device__ float a(int m, int k) const {
+    const int s = k / (4 * H), kk = k - s * 4 * H;
+    return A[(size_t)m * 4 * H + kk] * scaler(amp, att, m, s);
+  }
+  __device__ float b(int k, int n) const { return U[(size_t)n * 12 * H + k]; }
+  __device__ void store(int m, int n, float v, int) const { X1[(size_t)m * H + n] = fmaxf(v + bU[n], 0.0f); }
+};
+void launch_update(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *A, const float *amp,
+                   const float *att, const float *U, const float *bU, float *X1) {
+  OpUpdate op{blob, A, amp, att, U, bU, X1, c.H};
+  run_gemm<true, true>(st, op, c.maxN, c.H, 1);
+}
+
+// dA = sum_s diag(s) dZ U_s : A'[m, s*H+h] = s_m dZ[m,h], B'[s*H+h, n] = U[h, s*4H+n]
+struct OpDA {
+  const uint8_t *blob; const float *dZ; const float *amp; const float *att; const float *U; float *dA; int H;
+  __device__ void prepare() {}
+  __device__ int M() const { return batch_N(blob); }
+  __device__ int N() const { return 4 * H; }
+  __device__ int K() const { return 3 * H; }
+  __device__ int splits() const { return 1; }
+  __device__ float a(int m, int k) const {
+    const int s = k / H, h = k - s * H;
+    return dZ[(size_t)m * H + h] * scaler(amp, att, m, s);
+  }
+  __device__ float b(int k, int n) const {
+    const int s = k / H, h = k - s * H;
+    return U[(size_t)h * 12 * H + s * 4 * H + n];
+  }
+  __device__ void store(int m, int n, float v, int) const { dA[(size_t)m * 4 * H + n] = v; }
+};
+void launch_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *amp,
+               const float *att, const float *U, float *dA) {
+  OpDA op{blob, dZ, amp, att, U, dA, c.H};
+  run_gemm<true, false>(st, op, c.maxN, 4 * c.H, 1);
+}
+
+// split-K partial reduction in fixed split order; column Nc-1 of each row is the bias gradient
+__global__ void k_reduce_split(const float *__restrict__ part, int splits, int Mr, int Nc, float *__restrict__ outW,
+                               float *__restrict__ outB) {
+  const int total = Mr * Nc;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < splits; ++p) s += part[(size_t)p * total + e];
+    const int m = e / Nc, n = e - m * Nc;
+    if (n == Nc - 1) outB[m] = s;
+    else outW[(size_t)m * (Nc - 1) + n] = s;
+  }
+}
+
+constexpr int kDUSplits = 8;
+constexpr int kDMxSplits = 16;
+
+// dU[h, s*4H+k] = sum_i s_i dZ[i,h] A[i,k]; column 12H = ones -> db_U
+struct OpDU {
+  const uint8_t *blob; const float *dZ; const float *A; const float *amp; const float *att; float *part; int H;
+  __device__ void prepare() {}
+  __device__ int M() const { return H; }
+  __device__ int N() const { return 12 * H + 1; }
+  __device__ int K() const { return batch_N(blob); }
+  __device__ int splits() const { return kDUSplits; }
+  __device__ float a(int m, int k) const { return dZ[(size_t)k * H + m]; }
+  __device__ float b(int k, int n) const {
+    if (n == 12 * H) return 1.0f;
+    const int s = n / (4 * H), kk = n - s * 4 * H;
+    return A[(size_t)k * 4 * H + kk] * scaler(amp, att, k, s);
+  }
+  __device__ void store(int m, int n, float v, int sp) const {
+    part[(size_t)sp * H * (12 * H + 1) + (size_t)m * (12 * H + 1) + n] = v;
+  }
+};
+size_t dU_partial_floats(const Caps &c) { return (size_t)kDUSplits * c.H * (12 * c.H + 1); }
+void launch_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
+               const float *amp, const float *att, float *partial, float *dU, float *dbU) {
+  OpDU op{blob, dZ, A, amp, att, partial, c.H};
+  run_gemm<false, false>(st, op, c.H, 12 * c.H + 1, kDUSplits);
+  const int total = c.H * (12 * c.H + 1);
+  k_reduce_split<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(partial, kDUSplits, c.H, 12 * c.H + 1, dU, dbU);
+  counted();
+}
+
+// dM_x[h, f] = sum_i dP[i,h] X[i,f]; column F = ones -> db_M
+struct OpDMx {
+  const uint8_t *blob; const float *dP; const float *X; float *part; int H, F;
+  __device__ void prepare() { if (!X) X = load_batch(blob).x; }
+  __device__ int M() const { return H; }
+  __device__ int N() const { return F + 1; }
+  __device__ int K() const { return batch_N(blob); }
+  __device__ int splits() const { return kDMxSplits; }
+  __device__ float a(int m, int k) const { return dP[(size_t)k * H + m]; }
+  __device__ float b(int k, int n) const { return n == F ? 1.0f : X[(size_t)k * F + n]; }
+  __device__ void store(int m, int n, float v, int sp) const {
+    part[(size_t)sp * H * (F + 1) + (size_t)m * (F + 1) + n] = v;
+  }
+};
+size_t dMx_partial_floats(const Caps &c, int F) { return (size_t)kDMxSplits * c.H * (F + 1); }
+void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
+                float *partial, float *dMx, float *dbM) {
+  OpDMx op{blob, dP, X, partial, c.H, F};
+  run_gemm<false, false>(st, op, c.H, F + 1, kDMxSplits);
+  const int total = c.H * (F + 1);
+  k_reduce_split<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(partial, kDMxSplits, c.H, F + 1, dMx, dbM);
+  counted();
+}
+
+// dZprev = (dP Mx) * [Xl > 0]  (ReLU'(0) = 0)
+struct OpDX {
+  const uint8_t *blob; const float *dP; const float *Mx; const float *Xl; float *dZ; int H, F;
+  __device__ void prepare() {}
+  __device__ int M() const { return batch_N(blob); }
+  __device__ int N() const { return F; }
+  __device__ int K() const { return H; }
+  __device__ int splits() const { return 1; }
+  __device__ float a(int m, int k) const { return dP[(size_t)m * H + k]; }
+  __device__ float b(int k, int n) const { return Mx[(size_t)k * F + n]; }
+  __device__ void store(int m, int n, float v, int) const {
+    const size_t o = (size_t)m * F + n;
+    dZ[o] = Xl[o] > 0.0f ? v : 0.0f;
+  }
+};
+void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
+               const float *Xl, float *dZprev) {
+  OpDX op{blob, dP, Mx, Xl, dZprev, c.H, F};
+  run_gemm<true, false>(st, op, c.maxN, F, 1);
+}
+
+// ------------------------------------------------------------------ K2 aggregation forward
+// One warp per destination node i, lane owns CPL consecutive channels of a
+// 32*CPL-channel chunk (blockIdx.y). Messages m = P[j] + b_M + M_e e_ji are
+// recomputed, never stored. First pass: sum, min, max with
+// first-position argmin/argmax; second pass: centred sum of squares (two-pass
+// variance). d = 0 -> all aggregates 0 (C5).
+constexpr int kFeMax = 8;
+
+template <int CPL>
+__device__ __forceinline__ void load_vec(const float *p, float (&v)[CPL]) {
+  if constexpr (CPL == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
+    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) v[c] = __ldg(p + c);
+  }
+}
+template <int CPL>
+__device__ __forceinline__ void store_vec(float *p, const float (&v)[CPL]) {
+  if constexpr (CPL == 4) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) p[c] = v[c];
+  }
+}
+
+// message for CPL channels: m = (P + b_M) + sum_f M_e[:,f] e_f  (same order in K2 and K8)
+template <int CPL>
+__device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm)[CPL],
+                                        const float (&me)[CPL][kFeMax], const float (&ef)[kFeMax], int Fe,
+                                        float (&m)[CPL]) {
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    float v = pj[c] + bm[c];
+#pragma unroll
+    for (int f = 0; f < kFeMax; ++f)
+      if (f < Fe) v = fmaf(me[c][f], ef[f], v);
+    m[c] = v;
+  }
+}
+
+template <int CPL>
+__global__ void __launch_bounds__(256) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
+                                                 const float *__restrict__ Me, const float *__restrict__ bM,
+                                                 float var_floor, float *__restrict__ A, uint8_t *__restrict__ arg,
+                                                 int H) {
+  const BatchView b = load_batch(blob);
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  const int ch = blockIdx.y * 32 * CPL + lane * CPL;
+  const int Fe = b.Fe;
+  float me[CPL][kFeMax], bm[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    bm[c] = bM[ch + c];
+#pragma unroll
+    for (int f = 0; f < kFeMax; ++f) me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f;
+  }
+  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < b.N; i += gridDim.x * wpb) {
+    const int k0 = b.rowptr[i], k1 = b.rowptr[i + 1], d = k1 - k0;
+    float s[CPL], mx[CPL], mn[CPL];
+    int amx[CPL], amn[CPL];
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) { s[c] = 0.f; mx[c] = -INFINITY; mn[c] = INFINITY; amx[c] = 0; amn[c] = 0; }
+    for (int k = k0; k < k1; ++k) {
+      const int j = b.col[k];
+      float ef[kFeMax];
+#pragma unroll
+      for (int f = 0; f < kFeMax; ++f) ef[f] = f < Fe ? __ldg(b.ea + (size_t)k * Fe + f) : 0.f;
+      float pj[CPL], m[CPL];
+      load_vec<CPL>(P + (size_t)j * H + ch, pj);
+      message<CPL>(pj, bm, me, ef, Fe, m);
+      const int p = k - k0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        s[c] += m[c];
+        if (m[c] > mx[c]) { mx[c] = m[c]; amx[c] = p; }
+        if (m[c] < mn[c]) { mn[c] = m[c]; amn[c] = p; }
+      }
+    }
+    float mean[CPL], sd[CPL];
+    int flag[CPL];
+    if (d == 0) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) { mean[c] = 0.f; mx[c] = 0.f; mn[c] = 0.f; sd[c] = 0.f; flag[c] = 0; }
+    } else {
+      const float fd = (float)d;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) mean[c] = s[c] / fd;
+      float ss[CPL];
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) ss[c] = 0.f;
+      for (int k = k0; k < k1; ++k) {
+        const int j = b.col[k];
+        float ef[kFeMax];
+#pragma unroll
+        for (int f = 0; f < kFeMax; ++f) ef[f] = f < Fe ? __ldg(b.ea + (size_t)k * Fe + f) : 0.f;
+        float pj[CPL], m[CPL];
+        load_vec<CPL>(P + (size_t)j * H + ch, pj);
+        message<CPL>(pj, bm, me, ef, Fe, m);
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          const float t = m[c] - mean[c];
+          ss[c] = fmaf(t, t, ss[c]);
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const float var = ss[c] / fd;
+        flag[c] = var > var_floor;
+        sd[c] = sqrtf(fmaxf(var, var_floor));
+      }
+    }
+    float *Ai = A + (size_t)i * 4 * H + ch;
+    store_vec<CPL>(Ai, mean);
+    store_vec<CPL>(Ai + H, mn);
+    store_vec<CPL>(Ai + 2 * H, mx);
+    store_vec<CPL>(Ai + 3 * H, sd);
+    uint8_t *ai = arg + (size_t)i * 2 * H + ch;
+    if constexpr (CPL == 4) {
+      *reinterpret_cast<uchar4 *>(ai) = make_uchar4(amn[0], amn[1], amn[2], amn[3]);
+      *reinterpret_cast<uchar4 *>(ai + H) =
+          make_uchar4(amx[0] | (flag[0] << 7), amx[1] | (flag[1] << 7), amx[2] | (flag[2] << 7), amx[3] | (flag[3] << 7));
+    } else {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        ai[c] = (uint8_t)amn[c];
+        ai[H + c] = (uint8_t)(amx[c] | (flag[c] << 7));
+      }
+    }
+  }
+}
+
+static int agg_cpl(int H) { return (H % 128 == 0) ? 4 : 1; }
+
+void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
+                    const float *bM, float var_floor, float *A, uint8_t *arg) {
+  const int cpl = agg_cpl(c.H);
+  const dim3 grid(std::min(cdiv(c.maxN, 8), kSMs * 8), c.H / (32 * cpl));
+  if (cpl == 4) k_agg_fwd<4><<<grid, 256, 0, st>>>(blob, P, Me, bM, var_floor, A, arg, c.H);
+  else k_agg_fwd<1><<<grid, 256, 0, st>>>(blob, P, Me, bM, var_floor, A, arg, c.H);
+  counted();
+}
+
+// ------------------------------------------------------------------ K8 aggregation backward
+// One warp per SOURCE node j over its CSR row: by symmetry row j
+// lists every i with an edge j -> i, and slot[k] is j's position inside row i,
+// i.e. where K2 saw message m_{j->i}. Per edge:
+//   dm = dA_mean[i]/d_i + [slot == argmax_i] dA_max[i] + [slot == argmin_i] dA_min[i]
+//        + [var_i > eps] dA_std[i] (m - mu_i)/(d_i sigma_i)
+// dP[j] = sum dm (written once, no atomics); dM_e partials per block reduced in
+// fixed order by k_reduce_rows.
+template <int CPL>
+__global__ void __launch_bounds__(256) k_agg_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
+                                                 const float *__restrict__ Me, const float *__restrict__ bM,
+                                                 const float *__restrict__ A, const uint8_t *__restrict__ arg,
+                                                 const float *__restrict__ dA, float *__restrict__ dP,
+                                                 float *__restrict__ partial, int H) {
+  __shared__ float red[8][32][CPL * kFeMax];
+  const BatchView b = load_batch(blob);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int wpb = blockDim.x >> 5;
+  const int ch = blockIdx.y * 32 * CPL + lane * CPL;
+  const int Fe = b.Fe;
+  float me[CPL][kFeMax], bm[CPL], acc[CPL][kFeMax];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    bm[c] = bM[ch + c];
+#pragma unroll
+    for (int f = 0; f < kFeMax; ++f) { me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f; acc[c][f] = 0.f; }
+  }
+  for (int j = blockIdx.x * wpb + warp; j < b.N; j += gridDim.x * wpb) {
+    const int k0 = b.rowptr[j], k1 = b.rowptr[j + 1];
+    float pj[CPL], dp[CPL];
+    load_vec<CPL>(P + (size_t)j * H + ch, pj);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) dp[c] = 0.f;
+    for (int k = k0; k < k1; ++k) {
+      const int i = b.col[k];
+      const int sl = b.slot[k];
+      const int di = b.rowptr[i + 1] - b.rowptr[i];
+      const float fd = (float)di;
+      float ef[kFeMax];
+#pragma unroll
+      for (int f = 0; f < kFeMax; ++f) ef[f] = f < Fe ? __ldg(b.ea + (size_t)k * Fe + f) : 0.f;
+      float m[CPL];
+      message<CPL>(pj, bm, me, ef, Fe, m);
+      const float *dAi = dA + (size_t)i * 4 * H + ch;
+      const float *Ai = A + (size_t)i * 4 * H + ch;
+      float gmean[CPL], gmin[CPL], gmax[CPL], gstd[CPL], mu[CPL], sg[CPL];
+      load_vec<CPL>(dAi, gmean);
+      load_vec<CPL>(dAi + H, gmin);
+      load_vec<CPL>(dAi + 2 * H, gmax);
+      load_vec<CPL>(dAi + 3 * H, gstd);
+      load_vec<CPL>(Ai, mu);
+      load_vec<CPL>(Ai + 3 * H, sg);
+      uint8_t amn[CPL], amx[CPL];
+      const uint8_t *ai = arg + (size_t)i * 2 * H + ch;
+      if constexpr (CPL == 4) {
+        const uchar4 t0 = *reinterpret_cast<const uchar4 *>(ai);
+        const uchar4 t1 = *reinterpret_cast<const uchar4 *>(ai + H);
+        amn[0] = t0.x; amn[1] = t0.y; amn[2] = t0.z; amn[3] = t0.w;
+        amx[0] = t1.x; amx[1] = t1.y; amx[2] = t1.z; amx[3] = t1.w;
+      } else {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) { amn[c] = ai[c]; amx[c] = ai[H + c]; }
+      }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        float g = gmean[c] / fd;
+        if ((amx[c] & 0x7f) == sl) g += gmax[c];
+        if (amn[c] == sl) g += gmin[c];
+        if (amx[c] & 0x80) g += gstd[c] * (m[c] - mu[c]) / (fd * sg[c]);
+        dp[c] += g;
+#pragma unroll
+        for (int f = 0; f < kFeMax; ++f)
+          if (f < Fe) acc[c][f] = fmaf(g, ef[f], acc[c][f]);
+      }
+    }
+    store_vec<CPL>(dP + (size_t)j * H + ch, dp);
+  }
+  // block reduction of dM_e partials in fixed warp order
+#pragma unroll
+  for (int c = 0; c < CPL; ++c)
+#pragma unroll
+    for (int f = 0; f < kFeMax; ++f) red[warp][lane][c * kFeMax + f] = acc[c][f];
+  __syncthreads();
+  // thread t -> (lane l, c, f) of this chunk
+  const int chunkC = 32 * CPL;
+  for (int t = threadIdx.x; t < chunkC * Fe; t += blockDim.x) {
+    const int cc = t / Fe, f = t - cc * Fe;   // channel within chunk, feature
+    const int l = cc / CPL, c = cc - l * CPL;
+    float s = 0.f;
+    for (int w = 0; w < wpb; ++w) s += red[w][l][c * kFeMax + f];
+    // partial layout: [block][H][Fe] (M_e layout)
+    partial[(size_t)blockIdx.x * H * Fe + (size_t)(blockIdx.y * chunkC + cc) * Fe + f] = s;
+  }
+}
+
+__global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * count + e];
+    out[e] = s;
+  }
+}
+
+static int agg_bwd_blocks(const Caps &c) { return std::min(cdiv(c.maxN, 8), kSMs * 4); }
+size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * c.Fe; }
+
+void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
+                    const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
+                    float *partial, float *dMe) {
+  const int cpl = agg_cpl(c.H);
+  const int nb = agg_bwd_blocks(c);
+  const dim3 grid(nb, c.H / (32 * cpl));
+  if (cpl == 4) k_agg_bwd<4><<<grid, 256, 0, st>>>(blob, P, Me, bM, A, arg, dA, dP, partial, c.H);
+  else k_agg_bwd<1><<<grid, 256, 0, st>>>(blob, P, Me, bM, A, arg, dA, dP, partial, c.H);
+  counted();
+  const int count = c.H * c.Fe;
+  k_reduce_rows<<<std::max(1, std::min(cdiv(count, 128), kSMs)), 128, 0, st>>>(partial, nb, count, dMe);
+  counted();
+}
+
+// ------------------------------------------------------------------ head
+// Block per graph: G_g = mean of X_L rows, hpre = W1 G + b1,
+// yhat = W2 ReLU(hpre) + b2, sqerr = (yhat - y)^2.
+__device__ __forceinline__ float block_sum_256(float v, float *red) {
+  // deterministic tree over a 256-thread block
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) red[threadIdx.x] += red[threadIdx.x + s];
+    __syncthreads();
+  }
+  const float r = red[0];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(256) k_head_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ XL,
+                                                  const float *__restrict__ W1, const float *__restrict__ b1,
+                                                  const float *__restrict__ W2, const float *__restrict__ b2,
+                                                  float *__restrict__ G, float *__restrict__ hpre,
+                                                  float *__restrict__ yhat, float *__restrict__ sqerr, int H,
+                                                  int Hf) {
+  extern __shared__ float sm[];
+  float *Gs = sm, *hs = sm + H, *red = sm + H + Hf;
+  const BatchView b = load_batch(blob);
+  for (int g = blockIdx.x; g < b.B; g += gridDim.x) {
+    const int n0 = b.gp[g], n1 = b.gp[g + 1];
+    const float ng = (float)(n1 - n0);
+    for (int c = threadIdx.x; c < H; c += blockDim.x) {
+      float s = 0.f;
+      for (int i = n0; i < n1; ++i) s += XL[(size_t)i * H + c];
+      const float v = s / ng;
+      Gs[c] = v;
+      G[(size_t)g * H + c] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.x; r < Hf; r += blockDim.x) {
+      float acc = 0.f;
+      const float *w = W1 + (size_t)r * H;
+      for (int c = 0; c < H; ++c) acc = fmaf(w[c], Gs[c], acc);
+      acc += b1[r];
+      hpre[(size_t)g * Hf + r] = acc;
+      hs[r] = fmaxf(acc, 0.f);
+    }
+    __syncthreads();
+    float part = 0.f;
+    for (int r = threadIdx.x; r < Hf; r += blockDim.x) part = fmaf(W2[r], hs[r], part);
+    const float yh = block_sum_256(part, red) + b2[0];
+    if (threadIdx.x == 0) {
+      yhat[g] = yh;
+      const float e = yh - b.y[g];
+      sqerr[g] = e * e;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_loss(const uint8_t *__restrict__ blob, const float *__restrict__ sqerr,
+                                              float *__restrict__ loss) {
+  __shared__ float red[256];
+  const BatchView b = load_batch(blob);
+  float part = 0.f;
+  for (int g = threadIdx.x; g < b.B; g += blockDim.x) part += sqerr[g];
+  const float s = block_sum_256(part, red);
+  if (threadIdx.x == 0) *loss = s / (float)b.B;
+}
+
+void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                     const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
+                     float *sqerr, float *loss) {
+  const size_t smem = sizeof(float) * (c.H + c.Hf + 256);
+  k_head_fwd<<<std::min(c.maxB, kSMs * 4), 256, smem, st>>>(blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, c.H, c.Hf);
+  counted();
+  k_loss<<<1, 256, 0, st>>>(blob, sqerr, loss);
+  counted();
+}
+
+// Block per graph: dy = 2(yhat - y)/B, dhid = dy W2 * [hpre > 0],
+// dG = W1^T dhid, dZ_L[i] = dG / n_g * [X_L[i] > 0].
+__global__ void __launch_bounds__(256) k_head_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ XL,
+                                                  const float *__restrict__ W1, const float *__restrict__ W2,
+                                                  const float *__restrict__ hpre, const float *__restrict__ yhat,
+                                                  float *__restrict__ dy, float *__restrict__ dhid,
+                                                  float *__restrict__ dZL, int H, int Hf) {
+  extern __shared__ float sm[];
+  float *dhs = sm, *dGs = sm + Hf;
+  const BatchView b = load_batch(blob);
+  for (int g = blockIdx.x; g < b.B; g += gridDim.x) {
+    const int n0 = b.gp[g], n1 = b.gp[g + 1];
+    const float ng = (float)(n1 - n0);
+    const float d = 2.0f * (yhat[g] - b.y[g]) / (float)b.B;
+    if (threadIdx.x == 0) dy[g] = d;
+    for (int r = threadIdx.x; r < Hf; r += blockDim.x) {
+      const float v = hpre[(size_t)g * Hf + r] > 0.f ? d * W2[r] : 0.f;
+      dhs[r] = v;
+      dhid[(size_t)g * Hf + r] = v;
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < H; c += blockDim.x) {
+      float acc = 0.f;
+      for (int r = 0; r < Hf; ++r) acc = fmaf(W1[(size_t)r * H + c], dhs[r], acc);
+      dGs[c] = acc / ng;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < (n1 - n0) * H; e += blockDim.x) {
+      const int i = n0 + e / H, c = e % H;
+      const size_t o = (size_t)i * H + c;
+      dZL[o] = XL[o] > 0.f ? dGs[c] : 0.f;
+    }
+    __syncthreads();
+  }
+}
+
+// head parameter gradients: thread per output element, fixed order over graphs
+__global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__restrict__ G,
+                             const float *__restrict__ hpre, const float *__restrict__ dy,
+                             const float *__restrict__ dhid, float *__restrict__ gW1, float *__restrict__ gb1,
+                             float *__restrict__ gW2, float *__restrict__ gb2, int H, int Hf) {
+  const int B = reinterpret_cast<const int *>(blob)[0];
+  const int nW1 = Hf * H;
+  const int total = nW1 + 2 * Hf + 1;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    float s = 0.f;
+    if (e < nW1) {
+      const int r = e / H, c = e - r * H;
+      for (int g = 0; g < B; ++g) s = fmaf(dhid[(size_t)g * Hf + r], G[(size_t)g * H + c], s);
+      gW1[e] = s;
+    } else if (e < nW1 + Hf) {
+      const int r = e - nW1;
+      for (int g = 0; g < B; ++g) s += dhid[(size_t)g * Hf + r];
+      gb1[r] = s;
+    } else if (e < nW1 + 2 * Hf) {
+      const int r = e - nW1 - Hf;
+      for (int g = 0; g < B; ++g) s = fmaf(dy[g], fmaxf(hpre[(size_t)g * Hf + r], 0.f), s);
+      gW2[r] = s;
+    } else {
+      for (int g = 0; g < B; ++g) s += dy[g];
+      gb2[0] = s;
+    }
+  }
+}
+
+void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                     const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
+                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2) {
+  const size_t smem = sizeof(float) * (c.Hf + c.H);
+  k_head_bwd<<<std::min(c.maxB, kSMs * 4), 256, smem, st>>>(blob, XL, W1, W2, hpre, yhat, dy, dhid, dZL, c.H, c.Hf);
+  counted();
+  const int total = c.Hf * c.H + 2 * c.Hf + 1;
+  k_head_grads<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2,
+                                                                       c.H, c.Hf);
+  counted();
+}
+
+// ------------------------------------------------------------------ K10 AdamW
+// theta <- theta (1 - lr wd); m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2;
+// theta <- theta - (lr/bc1) m / (sqrt(v)/sqrt(bc2) + eps)
+__global__ void k_adam_prep(AdamDev *ad, float lr, float beta1, float beta2) {
+  const int64_t t = ad->step + 1;
+  ad->step = t;
+  const double bc1 = 1.0 - pow((double)beta1, (double)t);
+  const double bc2 = 1.0 - pow((double)beta2, (double)t);
+  ad->step_size = (float)((double)lr / bc1);
+  ad->inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
+}
+
+__global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const float4 *__restrict__ g,
+                                               float4 *__restrict__ m, float4 *__restrict__ v, int64_t n4,
+                                               const AdamDev *__restrict__ ad, float lr, float beta1,
+                                               float beta2, float eps, float wd) {
+  const float ss = ad->step_size, ib = ad->inv_sqrt_bc2;
+  const float decay = 1.0f - lr * wd;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    float4 P = p[i], Gv = g[i], Mv = m[i], Vv = v[i];
+    float *pp = &P.x, *gg = &Gv.x, *mm = &Mv.x, *vv = &Vv.x;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const float gc = gg[c];
+      mm[c] = beta1 * mm[c] + (1.0f - beta1) * gc;
+      vv[c] = beta2 * vv[c] + (1.0f - beta2) * gc * gc;
+      const float den = sqrtf(vv[c]) * ib + eps;
+      pp[c] = pp[c] * decay - ss * mm[c] / den;
+    }
+    p[i] = P; m[i] = Mv; v[i] = Vv;
+  }
+}
+
+void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
+                  float lr, float beta1, float beta2, float eps, float wd) {
+  k_adam_prep<<<1, 1, 0, st>>>(ad, lr, beta1, beta2);
+  counted();
+  const int64_t n4 = n / 4;
+  const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, kSMs * 8);
+  k_adamw<<<blocks, 256, 0, st>>>(reinterpret_cast<float4 *>(p), reinterpret_cast<const float4 *>(g),
+                                  reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, ad, lr, beta1,
+                                  beta2, eps, wd);
+  counted();
+}
+
+int64_t launches_so_far() { return g_launches.load(); }
+
+}  // namespace hg

@@ -1,0 +1,69 @@
+// kernels.h — host-side launch wrappers for the CUDA kernels of one training
+// step. Every wrapper enqueues on `st` and reads the
+// batch sizes (B, N, E) from the device-resident batch header, so a whole step
+// is CUDA-graph capturable; grids are sized from the ctx capacities.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace hg {
+
+struct Caps {
+  int maxB, maxN, maxE;
+  int F0, Fe, H, Hf;
+};
+
+// per-node degree scalers amp = ln(d+1)/delta, att = delta/ln(d+1) (1 for d=0)
+void launch_scalers(cudaStream_t st, const Caps &c, const uint8_t *blob, double delta, float *amp, float *att);
+
+// K1 / K9b / K3 / K7a / K7b / K9a GEMMs (SIMT fp32 v1)
+// P[N,H] = X[N,F] * Mx^T
+void launch_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx, float *P);
+// X1 = ReLU(sum_s diag(s) A U_s^T + b_U)
+void launch_update(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *A, const float *amp,
+                   const float *att, const float *U, const float *bU, float *X1);
+// dA[N,4H] = sum_s diag(s) dZ U_s
+void launch_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *amp,
+               const float *att, const float *U, float *dA);
+// dU[H,12H] = sum_i s_i dZ_i^T A_i ; db_U = sum_i dZ_i   (split-K partials then fixed-order reduce)
+void launch_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
+               const float *amp, const float *att, float *partial, float *dU, float *dbU);
+// dM_x[H,F] = dP^T X ; db_M = sum_i dP_i
+void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
+                float *partial, float *dMx, float *dbM);
+// dZprev[N,F] = (dP Mx) * [Xl > 0]
+void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
+               const float *Xl, float *dZprev);
+
+// K2: fused edge gather + message + mean/min/max/std segmented reduction
+void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
+                    const float *bM, float var_floor, float *A, uint8_t *arg);
+// K8: aggregation backward + scatter to sources; dM_e via block partials
+void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
+                    const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
+                    float *partial, float *dMe);
+size_t agg_bwd_partial_floats(const Caps &c);
+size_t dU_partial_floats(const Caps &c);
+size_t dMx_partial_floats(const Caps &c, int F);
+
+// K4/K5: pool + head forward, loss
+void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                     const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
+                     float *sqerr, float *loss);
+// K6: head + pool backward -> dZ of the last layer, then head parameter gradients
+void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                     const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
+                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2);
+
+// K10: AdamW over the flat arena
+struct AdamDev {
+  int64_t step;
+  float step_size, inv_sqrt_bc2;
+};
+void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
+                  float lr, float beta1, float beta2, float eps, float wd);
+
+// process-wide count of kernels launched by the wrappers above
+int64_t launches_so_far();
+
+}  // namespace hg
