@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark: training graphs/s of the PNA-GCNN step on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl ours|reference] [--workload B|A|D|E256|E512]
+
+One process per GPU (torchrun for N > 1; RANK / LOCAL_RANK / WORLD_SIZE from the
+env). A *step* = one pass of the whole hot path: batch
+of B graphs -> 6 GC layers -> pool -> head -> MSE -> backward -> NCCL gradient
+mean -> fused AdamW, replayed as one CUDA graph.
+
+Prints ONE JSON line on rank 0:
+  value   graphs/s over all ranks, inputs resident in HBM (K pre-packed batches
+          in device slots), L2 flushed (512 MB write) between timed steps,
+          each step bracketed by CUDA events on the compute stream, max over ranks.
+  e2e     the same metric through the public C-ABI from HOST buffers: per step
+          hg_pack (host collate from the Table-1 store -> pinned -> H2D),
+          hg_train_step, hg_loss_get (D2H of the loss).
+  roofline / phases_ms from an instrumented eager step (hg_profile_step).
+  cpu_baseline: the float64 oracle (oracle/) timed on a bounded sample (rank 0, N=1).
+--impl reference runs the oracle itself as the reference arm (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train graphs/sec at 1/2/4/8 B200 (PCQM4Mv2-shaped); % HBM/tensor roofline"
+
+WORKLOADS = {
+    # name: (preset, graphs in store, B per GPU, H, L, description)
+    "A": ("tiny", 1000, 64, 32, 2, "A: 1,000 synthetic molecules (<=20 atoms), 2 conv layers hidden 32, batch 64"),
+    "B": ("pcqm", 3_400_000, 128, 128, 6,
+          "B: PCQM4Mv2-shaped 3.4M synthetic molecules (<=51 atoms), 6 conv layers hidden 128, batch 128/GPU"),
+    "D": ("aisd", 10_500_000, 512, 128, 6,
+          "D: AISD HOMO-LUMO-shaped 10.5M synthetic molecules, 6 conv layers hidden 128, batch 512/GPU"),
+    "E256": ("aisd", 10_500_000, 512, 256, 8, "E: AISD-shaped, 8 conv layers hidden 256, batch 512/GPU"),
+    "E512": ("aisd", 10_500_000, 512, 512, 8, "E: AISD-shaped, 8 conv layers hidden 512, batch 512/GPU"),
+}
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="B", choices=list(WORKLOADS))
+    ap.add_argument("--graphs", type=int, default=0, help="override the store size")
+    ap.add_argument("--flush-mb", type=int, default=512)
+    ap.add_argument("--resident", type=int, default=32, help="distinct pre-packed batches resident in HBM")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--store-dir", default="")
+    ap.add_argument("--seed", type=int, default=11)
+    return ap.parse_args()
+
+
+def mem_available_bytes() -> int:
+    try:
+        with open("/proc/meminfo") as f:
+            for line in f:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def store_dir(args, preset, n):
+    if args.store_dir:
+        return args.store_dir
+    need = n * (60 * 136 + 120)  # generous bytes/graph estimate
+    for base in ("/dev/shm", "/tmp"):
+        try:
+            st = os.statvfs(base)
+            if st.f_bavail * st.f_frsize > need * 1.2:
+                return os.path.join(base, f"hgnn_store_{preset}_{n}_{args.seed}")
+        except OSError:
+            continue
+    return os.path.join("/tmp", f"hgnn_store_{preset}_{n}_{args.seed}")
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = f"/tmp/hgnn_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms",
+                                          "100", "-i", str(self.index)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                p = [t.strip() for t in line.split(",")]
+                if len(p) < 9:
+                    continue
+                try:
+                    sm.append(float(p[1]))
+                    mx.append(float(p[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, p[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------ oracle timing
+def oracle_rate(data, ids_list, cfg, delta, seconds, max_steps=None):
+    """Oracle train steps over the given batches until `seconds` elapse; graphs/s."""
+    import oracle as O
+    params = O.init_params(cfg, 2)
+    st = O.zero_state(params)
+    t0 = time.perf_counter()
+    graphs = 0
+    steps = 0
+    for ids in ids_list:
+        params, st, _, _ = O.train_step(params, st, data, ids, cfg, delta)
+        graphs += len(ids)
+        steps += 1
+        if time.perf_counter() - t0 > seconds or (max_steps and steps >= max_steps):
+            break
+    dt = time.perf_counter() - t0
+    return graphs / dt, graphs, steps, dt
+
+
+def blas_threads() -> int:
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = [i.get("num_threads", 1) for i in info if i.get("user_api") == "blas"]
+        return max(n) if n else 1
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+# ------------------------------------------------------------------------ main
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    preset, n_graphs, B, H, L, desc = WORKLOADS[args.workload]
+    if args.graphs:
+        n_graphs = args.graphs
+    import numpy as np
+
+    if args.impl == "reference":
+        return run_reference(args, rank, world, preset, n_graphs, B, H, L, desc)
+
+    import torch
+    import torch.distributed as dist
+    import molgen
+    from paper_2207_11333_b200 import hgnn
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---- dataset: generated once per host into shared memory-mapped files
+    mem_need = n_graphs * 5600 * (2.0 if preset == "aisd" else 1.0)
+    avail = mem_available_bytes()
+    if avail and mem_need > 0.6 * avail:
+        scaled = int(n_graphs * 0.6 * avail / mem_need)
+        log(f"[bench] host memory {avail / 1e9:.1f} GB: store reduced {n_graphs} -> {scaled} graphs")
+        n_graphs = scaled
+    sdir = store_dir(args, preset, n_graphs)
+    t0 = time.time()
+    if local_rank == 0:
+        data = molgen.generate_to(sdir, preset, n_graphs, args.seed)
+    barrier()
+    if local_rank != 0:
+        data = molgen.load_dir(sdir)
+    t_gen = time.time() - t0
+    t0 = time.time()
+    store = hgnn.Store(data, copy=False)
+    st = store.stats()
+    delta = store.degree_stat()
+    t_store = time.time() - t0
+    log(f"[bench] rank {rank}: store {st} delta={delta:.6f} gen {t_gen:.1f}s store {t_store:.1f}s")
+
+    max_nodes = B * st["max_nodes_per_graph"]
+    max_edges = B * int(np.diff(np.asarray(data["edge_offset"])).max())
+    n_res = max(1, min(args.resident, args.steps))
+    e2e_slots = 0 if args.no_e2e else 2
+    cfg = hgnn.make_config(data["f_node"], 4, H, L, B, max_nodes, max_edges, delta, n_slots=n_res + e2e_slots)
+    ctx = hgnn.Context(cfg, device=local_rank)
+    ctx.params_init(1234)
+    ctx.comm_init(rank, world)
+    hyper = dict(hgnn.DEFAULT_ADAMW)
+
+    ids = hgnn.hg_shard(13, 0, rank, world, n_graphs)
+    nb = len(ids) // B
+    batches = [ids[k * B:(k + 1) * B] for k in range(nb)]
+    blobs = [hgnn.hg_pack_host(store, batches[k % nb], cfg) for k in range(n_res)]
+    for s, blob in enumerate(blobs):
+        ctx.upload(blob, s)
+    for s in range(n_res + e2e_slots):
+        ctx.capture_step(s, **hyper)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(args.flush_mb << 20, dtype=torch.uint8, device="cuda")
+    torch.cuda.synchronize()
+
+    # ---- warm-up
+    for k in range(args.warmup):
+        ctx.train_step(k % n_res, graph=True, **hyper)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed: device-resident inputs
+    K = args.steps
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(K)]
+    clocks = Clocks(local_rank)
+    clocks.start()
+    l0 = ctx.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    for k in range(K):
+        flush.zero_()
+        ev0[k].record(stream)
+        ctx.train_step(k % n_res, graph=True, **hyper)
+        ev1[k].record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = ctx.launch_count() - l0
+    total_ms = sum(a.elapsed_time(b) for a, b in zip(ev0, ev1))
+    tmax = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_ms = float(tmax.item())
+    value = world * K * B / (total_ms / 1e3)
+    loss_now = ctx.loss()
+
+    # ---- e2e through the public API from host buffers
+    e2e = None
+    if not args.no_e2e:
+        s0 = n_res
+        off = n_res * 0
+        for k in range(2):  # warm the e2e slots
+            ctx.pack(store, batches[(off + k) % nb], s0 + (k % 2))
+            ctx.train_step(s0 + (k % 2), graph=True, **hyper)
+            ctx.loss()
+        h2d = []
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        ctx.pack(store, batches[(n_res + 2) % nb], s0)
+        h2d.append(int(hgnn.hg_batch_offsets(B, 0, 0, 0, 0)["total"]))
+        for k in range(K):
+            slot = s0 + (k % 2)
+            ctx.train_step(slot, graph=True, **hyper)
+            if k + 1 < K:
+                nxt = batches[(n_res + 3 + k) % nb]
+                ctx.pack(store, nxt, s0 + ((k + 1) % 2))
+            ctx.loss()  # D2H read of the step's result
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        barrier()
+        tt = torch.tensor([dt], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dt = float(tt.item())
+        # exact H2D bytes per step: the packed blob sizes
+        sizes = [hgnn.hg_pack_host(store, batches[(n_res + 2 + k) % nb], cfg).nbytes for k in range(min(K, 8))]
+        e2e = {"value": world * K * B / dt, "unit": "graphs/s", "h2d_bytes_per_step": int(np.mean(sizes)),
+               "d2h_bytes_per_step": 4, "ms_per_step": dt * 1e3 / K,
+               "note": "hg_pack (host collate + pinned H2D, overlapped with the previous step) + hg_train_step "
+                       "(graph) + hg_loss_get each step; wall clock, max over ranks"}
+
+    # ---- instrumented step: per-phase device time -> roofline of the dominant kernel
+    prof = None
+    phases = {}
+    reps = 3
+    for r in range(reps):
+        flush.zero_()
+        p = ctx.profile_step(r % n_res, **hyper)
+        for k, (ms, nl) in p.items():
+            a = phases.setdefault(k, [0.0, 0])
+            a[0] += ms / reps
+            a[1] = nl
+    # algorithmic work per phase
+    Ns, Es = [], []
+    for r in range(reps):
+        hdr = blobs[r % n_res][:64].view(np.int32)
+        Ns.append(int(hdr[1]))
+        Es.append(int(hdr[2]))
+    Nn, Ee = float(np.mean(Ns)), float(np.mean(Es))
+    F0 = data["f_node"]
+    flops = {
+        "update": 24.0 * Nn * H * H * L, "dA": 24.0 * Nn * H * H * L, "dU": 24.0 * Nn * H * H * L,
+        "proj": 2.0 * Nn * H * (F0 + H * (L - 1)), "dMx": 2.0 * Nn * H * (F0 + H * (L - 1)) + 2.0 * Nn * H * L,
+        "dX": 2.0 * Nn * H * H * (L - 1),
+    }
+    hbm_bytes = {
+        "agg_fwd": L * (Nn * (22 * H + 4) + 20 * Ee),
+        "agg_bwd": L * (Nn * (34 * H + 4) + 20 * Ee),
+    }
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # fp32 FFMA TFLOP/s
+    dom = max((k for k in phases if k != "allreduce"), key=lambda k: phases[k][0])
+    step_ms_prof = sum(v[0] for v in phases.values())
+    if dom in flops:
+        ach = flops[dom] / (phases[dom][0] / 1e3) / 1e12
+        prof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": ffma_peak, "unit": "TFLOP/s",
+                "frac": ach / ffma_peak, "traffic": None,
+                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (SIMT fp32 FFMA path)",
+                "share_of_step": phases[dom][0] / step_ms_prof}
+    else:
+        ach = hbm_bytes[dom] / (phases[dom][0] / 1e3) / 1e9
+        prof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
+                "frac": ach / hbm_peak, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "share_of_step": phases[dom][0] / step_ms_prof}
+    agg = {}
+    for k in ("agg_fwd", "agg_bwd"):
+        a = hbm_bytes[k] / (phases[k][0] / 1e3) / 1e9
+        agg[k] = {"achieved_gbs": a, "frac_of_measured_hbm": a / hbm_peak, "ms": phases[k][0]}
+    gemm = {}
+    for k in ("update", "dA", "dU"):
+        a = flops[k] / (phases[k][0] / 1e3) / 1e12
+        gemm[k] = {"achieved_tflops": a, "frac_of_ffma": a / ffma_peak, "ms": phases[k][0]}
+
+    # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        ocfg = {"f_node": data["f_node"], "f_edge": 4, "hidden": H, "layers": L, "fc_hidden": H}
+        sample_batches = [np.asarray(batches[k]) for k in range(min(nb, 64))]
+        sub = {k: np.asarray(data[k]) if k in ("node_offset", "edge_offset", "y") else data[k]
+               for k in ("node_offset", "edge_offset", "x", "edge_index", "edge_attr", "y")}
+        rate, g, s, dt = oracle_rate(sub, sample_batches, ocfg, delta, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "graphs/s", "cores": blas_threads(), "kind": "oracle",
+               "sample": f"{s} oracle train steps (f64 numpy forward+backward+AdamW) on batches of {B} graphs of "
+                         f"this workload, {dt:.1f} s", "host_cores": len(os.sched_getaffinity(0))}
+
+    out = {
+        "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
+        "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic (molgen seeded molecules, Table-2 calibrated; random-init weights)",
+        "config": {"workload": desc, "graphs_in_store": n_graphs, "global_batch": B * world, "batch_per_gpu": B,
+                   "layers": L, "hidden": H, "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
+                   "parallelism": f"dp{world}", "resident_batches": n_res,
+                   "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
+                   "gemm_precision": "fp32 SIMT FFMA"},
+        "roofline": prof, "roofline_agg": agg, "gemm": gemm,
+        "phases_ms": {k: round(v[0], 4) for k, v in phases.items()},
+        "phase_launches": {k: v[1] for k, v in phases.items()},
+        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "loss_after_timed": loss_now,
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    barrier()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args, rank, world, preset, n_graphs, B, H, L, desc):
+    """Reference arm = the float64 CPU oracle as it stands (rank 0 only)."""
+    import numpy as np
+    if rank != 0:
+        return
+    import molgen
+    import oracle as O
+    n = min(n_graphs, 200_000)  # the oracle only touches the sampled batches
+    data = molgen.generate(preset, n, args.seed)
+    delta = O.degree_stat(data, np.arange(min(n, 20000)))
+    ocfg = {"f_node": data["f_node"], "f_edge": 4, "hidden": H, "layers": L, "fc_hidden": H}
+    sample = max(4, min(B, 32))  # graphs per reference step (bounded sample of the batch)
+    ids = O.shard(13, 0, 0, 1, n)
+    batches = [ids[k * sample:(k + 1) * sample] for k in range(args.warmup + args.steps)]
+    params = O.init_params(ocfg, 2)
+    st = O.zero_state(params)
+    for k in range(args.warmup):
+        params, st, _, _ = O.train_step(params, st, data, batches[k], ocfg, delta)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        params, st, _, _ = O.train_step(params, st, data, batches[args.warmup + k], ocfg, delta)
+    dt = time.perf_counter() - t0
+    value = args.steps * sample / dt
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (molgen seeded molecules; random-init weights)",
+           "config": {"workload": desc, "graphs_in_store": n, "batch_per_step": sample, "layers": L, "hidden": H,
+                      "parallelism": "cpu oracle, 1 process"},
+           "cpu_baseline": {"value": value, "unit": "graphs/s", "kind": "oracle", "cores": blas_threads(),
+                            "sample": f"{args.steps} oracle train steps of {sample} graphs each (bounded sample of "
+                                      f"the {B}-graph batch)"},
+           "e2e": {"value": value, "unit": "graphs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

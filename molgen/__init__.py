@@ -127,3 +127,59 @@ def perturb_features(data: dict, seed: int, scale: float = 0.05) -> dict:
     jit = scale * rng.standard_normal((len(uniq), ea.shape[1]))
     out["edge_attr"] = (ea + jit[inv]).astype(np.float32)
     return out
+
+
+_ARRAYS = ("node_offset", "edge_offset", "x", "edge_index", "edge_attr", "y")
+
+
+def generate_to(dirpath: str, preset: str, n_graphs: int, seed: int, threads: int | None = None) -> dict:
+    """Generate straight into .npy files under ``dirpath`` (memory-mapped), so
+    several processes on one host can share one copy of a multi-GB store via
+    the page cache (``load_dir``). Idempotent: a complete directory is reused."""
+    import json
+    lib = _load()
+    threads = threads or default_threads()
+    meta_path = os.path.join(dirpath, "meta.json")
+    if os.path.exists(meta_path):
+        return load_dir(dirpath)
+    os.makedirs(dirpath, exist_ok=True)
+    info = preset_info(preset)
+    n = int(n_graphs)
+    nodes = np.zeros(n, np.int32)
+    edges = np.zeros(n, np.int32)
+    rc = lib.molgen_count(PRESETS[preset], seed, 0, n, _ptr(nodes, ctypes.c_int32), _ptr(edges, ctypes.c_int32),
+                          threads)
+    if rc:
+        raise RuntimeError(f"molgen_count failed: {rc}")
+    mm = np.lib.format.open_memmap
+    no = mm(os.path.join(dirpath, "node_offset.npy"), "w+", np.int64, (n + 1,))
+    eo = mm(os.path.join(dirpath, "edge_offset.npy"), "w+", np.int64, (n + 1,))
+    no[0] = 0
+    eo[0] = 0
+    np.cumsum(nodes, out=no[1:])
+    np.cumsum(edges, out=eo[1:])
+    N, E, F = int(no[-1]), int(eo[-1]), info["f_node"]
+    x = mm(os.path.join(dirpath, "x.npy"), "w+", np.float32, (N, F))
+    ei = mm(os.path.join(dirpath, "edge_index.npy"), "w+", np.int32, (2, E))
+    ea = mm(os.path.join(dirpath, "edge_attr.npy"), "w+", np.float32, (E, 4))
+    y = mm(os.path.join(dirpath, "y.npy"), "w+", np.float32, (n,))
+    rc = lib.molgen_fill(PRESETS[preset], seed, 0, n, _ptr(no, ctypes.c_int64), _ptr(eo, ctypes.c_int64), E,
+                         _ptr(x, ctypes.c_float), _ptr(ei, ctypes.c_int32), _ptr(ea, ctypes.c_float),
+                         _ptr(y, ctypes.c_float), threads)
+    if rc:
+        raise RuntimeError(f"molgen_fill failed: {rc}")
+    for a in (no, eo, x, ei, ea, y):
+        a.flush()
+    with open(meta_path, "w") as f:
+        json.dump({"preset": preset, "n_graphs": n, "seed": seed, "f_node": F, "vocab_z": info["vocab_z"].tolist()}, f)
+    return load_dir(dirpath)
+
+
+def load_dir(dirpath: str) -> dict:
+    import json
+    with open(os.path.join(dirpath, "meta.json")) as f:
+        meta = json.load(f)
+    d = {k: np.load(os.path.join(dirpath, k + ".npy"), mmap_mode="r") for k in _ARRAYS}
+    d.update({"f_node": meta["f_node"], "f_edge": 4, "vocab_z": np.asarray(meta["vocab_z"]), "preset": meta["preset"],
+              "seed": meta["seed"]})
+    return d

@@ -441,9 +441,13 @@ def decision_bands(cache: dict, tau: float = 1e-6, var_floor: float = VAR_FLOOR)
 
 def replay(cache: dict, gpu: list, tau: float = 1e-6, head_relu_gpu=None):
     """Build ``decisions`` for ``backward``: inside each ambiguity band adopt the
-    GPU's decision, elsewhere keep the oracle's. Returns (decisions, n_overrides)."""
+    GPU's decision, elsewhere keep the oracle's. Returns (decisions, counts) with
+    counts = {'overrides': in-band cells where the GPU chose differently (equally
+    valid at margin tau, e.g. automorphic atoms whose f64 states differ only by
+    summation order), 'out_of_band': cells where the GPU disagrees although the
+    oracle's margin exceeds tau (genuine disagreements)}."""
     bands = decision_bands(cache, tau)
-    dec, n = {}, 0
+    dec, n, bad = {}, 0, 0
     for l, (c, b, gdec) in enumerate(zip(cache["layers"], bands, gpu)):
         own = dict(relu=c["Z"] > 0, argmax=c["argmax"], argmin=c["argmin"], varflag=c["var"] > VAR_FLOOR)
         d = {}
@@ -451,8 +455,11 @@ def replay(cache: dict, gpu: list, tau: float = 1e-6, head_relu_gpu=None):
             if k not in gdec:
                 d[k] = own[k]
                 continue
-            sel = b[k] & (np.asarray(gdec[k]) != own[k])
-            n += int(sel.sum())
+            diff = np.asarray(gdec[k]) != own[k]
+            if k in ("argmax", "argmin", "varflag"):
+                diff &= (c["deg"] > 0)[:, None]  # d = 0 rows carry no decision
+            n += int((b[k] & diff).sum())
+            bad += int((~b[k] & diff).sum())
             d[k] = np.where(b[k], gdec[k], own[k])
         dec[l] = d
     if head_relu_gpu is not None:
@@ -460,5 +467,6 @@ def replay(cache: dict, gpu: list, tau: float = 1e-6, head_relu_gpu=None):
         band = np.abs(hp) < tau * (np.abs(hp).max() if hp.size else 0.0)
         own = hp > 0
         n += int((band & (head_relu_gpu != own)).sum())
+        bad += int((~band & (head_relu_gpu != own)).sum())
         dec["head_relu"] = np.where(band, head_relu_gpu, own)
-    return dec, n
+    return dec, {"overrides": n, "out_of_band": bad}

@@ -85,8 +85,9 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
         xs.append(float(np.abs(X - ref).max() / max(np.abs(ref).max(), 1e-30)))
     res["X"] = max(xs)
     hpre = ctx.view_f32(hgnn.VIEW_HPRE)[:B * cfg.fc_hidden].cpu().numpy().reshape(B, cfg.fc_hidden)
-    dec, n_over = O.replay(cache, gpu_decisions(ctx, N, H, L), head_relu_gpu=hpre > 0)
-    res["overrides"] = n_over
+    dec, counts = O.replay(cache, gpu_decisions(ctx, N, H, L), head_relu_gpu=hpre > 0)
+    res["overrides"] = counts["overrides"]
+    res["out_of_band"] = counts["out_of_band"]
     res["cells"] = int(sum(c["Z"].size * 4 for c in cache["layers"]))
     g = O.backward(params, b, ocfg, cache, dec)
     gg = hgnn.arena_to_dict(ctx.grads_get(), layout) if not graph or not do_step else None
@@ -124,7 +125,11 @@ def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
     if "loss" in res:
         assert res["loss"] <= fwd_tol, res["loss"]
     assert res["X"] <= fwd_tol, res["X"]
-    assert res["overrides"] <= max(1, 1e-4 * res["cells"]), res["overrides"]
+    # GPU discrete decisions (ReLU masks, argmin/argmax, std floor) must agree with the
+    # oracle wherever the oracle's margin exceeds tau; in-band
+    # overrides are equally valid choices and only reported.
+    assert res["out_of_band"] <= max(2, 1e-5 * res["cells"]), res["out_of_band"]
+    assert res["overrides"] <= 1e-3 * res["cells"], res["overrides"]
     if "grad_maxscaled" in res:
         for k, v in res["grad_maxscaled"].items():
             assert v <= grad_tol, (k, v)
