@@ -439,15 +439,19 @@ def decision_bands(cache: dict, tau: float = 1e-6, var_floor: float = VAR_FLOOR)
     return out
 
 
-def replay(cache: dict, gpu: list, tau: float = 1e-6, head_relu_gpu=None):
+def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
     """Build ``decisions`` for ``backward``: inside each ambiguity band adopt the
     GPU's decision, elsewhere keep the oracle's. Returns (decisions, counts) with
     counts = {'overrides': in-band cells where the GPU chose differently (equally
     valid at margin tau, e.g. automorphic atoms whose f64 states differ only by
     summation order), 'out_of_band': cells where the GPU disagrees although the
-    oracle's margin exceeds tau (genuine disagreements)}."""
+    oracle's margin exceeds tau (genuine disagreements), 'out_of_band_by': per
+    decision kind}. tau defaults to the forward tolerance 1e-4 (DESIGN.md
+    reading R-replay): a decision whose margin is below the accepted forward
+    error is not determined by a computation at that tolerance."""
     bands = decision_bands(cache, tau)
     dec, n, bad = {}, 0, 0
+    by = {"relu": 0, "argmax": 0, "argmin": 0, "varflag": 0, "head_relu": 0}
     for l, (c, b, gdec) in enumerate(zip(cache["layers"], bands, gpu)):
         own = dict(relu=c["Z"] > 0, argmax=c["argmax"], argmin=c["argmin"], varflag=c["var"] > VAR_FLOOR)
         d = {}
@@ -459,7 +463,9 @@ def replay(cache: dict, gpu: list, tau: float = 1e-6, head_relu_gpu=None):
             if k in ("argmax", "argmin", "varflag"):
                 diff &= (c["deg"] > 0)[:, None]  # d = 0 rows carry no decision
             n += int((b[k] & diff).sum())
-            bad += int((~b[k] & diff).sum())
+            nb = int((~b[k] & diff).sum())
+            bad += nb
+            by[k] += nb
             d[k] = np.where(b[k], gdec[k], own[k])
         dec[l] = d
     if head_relu_gpu is not None:
@@ -467,6 +473,8 @@ def replay(cache: dict, gpu: list, tau: float = 1e-6, head_relu_gpu=None):
         band = np.abs(hp) < tau * (np.abs(hp).max() if hp.size else 0.0)
         own = hp > 0
         n += int((band & (head_relu_gpu != own)).sum())
-        bad += int((~band & (head_relu_gpu != own)).sum())
+        nb = int((~band & (head_relu_gpu != own)).sum())
+        bad += nb
+        by["head_relu"] += nb
         dec["head_relu"] = np.where(band, head_relu_gpu, own)
-    return dec, {"overrides": n, "out_of_band": bad}
+    return dec, {"overrides": n, "out_of_band": bad, "out_of_band_by": by}

@@ -87,7 +87,7 @@ struct hg_ctx {
   int64_t n_params = 0;
   int device = 0;
   uint8_t *ws = nullptr;
-  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  cudaStream_t stream = nullptr, copy_stream = nullptr, cap_stream = nullptr;
   std::vector<void *> staging;
   std::vector<cudaEvent_t> copy_done, compute_done;
   std::vector<cudaGraphExec_t> graphs;
@@ -185,11 +185,10 @@ void phase(Prof *pr, int ph, F &&fn) {
 }
 
 // ---- the step's kernel sequence (enqueue only) ----
-void enqueue_forward(hg_ctx *x, int slot, Prof *pr = nullptr) {
+void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
-  cudaStream_t st = x->stream;
   float *amp = x->f(p.amp), *att = x->f(p.att);
   phase(pr, HG_PHASE_SCALERS, [&] { launch_scalers(st, x->caps, blob, c.delta, amp, att); });
   for (int l = 0; l < c.layers; ++l) {
@@ -212,11 +211,10 @@ void enqueue_forward(hg_ctx *x, int slot, Prof *pr = nullptr) {
   });
 }
 
-void enqueue_backward(hg_ctx *x, int slot, Prof *pr = nullptr) {
+void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
-  cudaStream_t st = x->stream;
   float *amp = x->f(p.amp), *att = x->f(p.att);
   float *dZ = x->f(p.dZa), *dZn = x->f(p.dZb);
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
@@ -247,18 +245,18 @@ void enqueue_backward(hg_ctx *x, int slot, Prof *pr = nullptr) {
   }
 }
 
-hg_status enqueue_allreduce(hg_ctx *x) {
+hg_status enqueue_allreduce(hg_ctx *x, cudaStream_t st) {
   if (x->world <= 1 || !x->comm) return HG_OK;
   ncclResult_t r = ncclAllReduce(x->f(x->plan.grads), x->f(x->plan.grads), (size_t)x->n_params, ncclFloat32, ncclAvg,
-                                 x->comm, x->stream);
+                                 x->comm, st);
   if (r != ncclSuccess) return nccl_fail(x, r, "ncclAllReduce");
   return HG_OK;
 }
 
-void enqueue_step(hg_ctx *x, const hg_adamw &h, Prof *pr = nullptr) {
+void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr = nullptr) {
   const Plan &p = x->plan;
   phase(pr, HG_PHASE_ADAMW, [&] {
-    launch_adamw(x->stream, x->f(p.params), x->f(p.grads), x->f(p.m), x->f(p.v), x->n_params,
+    launch_adamw(st, x->f(p.params), x->f(p.grads), x->f(p.m), x->f(p.v), x->n_params,
                  reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay);
   });
 }
@@ -308,6 +306,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   };
   if ((e = cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bail(e, "cudaStreamCreate");
+  if ((e = cudaStreamCreateWithFlags(&x->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
+    return bail(e, "cudaStreamCreate");
   for (int s = 0; s < c->n_slots; ++s) {
     void *h = nullptr;
     if ((e = cudaHostAlloc(&h, plan.blob_max, cudaHostAllocDefault)) != cudaSuccess) return bail(e, "cudaHostAlloc");
@@ -336,6 +336,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   for (auto ev : x->copy_done) cudaEventDestroy(ev);
   for (auto ev : x->compute_done) cudaEventDestroy(ev);
   if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
+  if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
   if (x->comm) ncclCommDestroy(x->comm);
   delete x;
   return HG_OK;
@@ -495,7 +496,7 @@ hg_status hg_forward(hg_ctx *x, int32_t slot) {
   if (st || (st = check_slot(x, slot))) return st;
   CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
   const int64_t l0 = launches_so_far();
-  enqueue_forward(x, slot);
+  enqueue_forward(x, x->stream, slot);
   x->launches += launches_so_far() - l0;
   return after_enqueue(x, "forward launch");
 }
@@ -504,7 +505,7 @@ hg_status hg_backward(hg_ctx *x, int32_t slot) {
   hg_status st = usable(x);
   if (st || (st = check_slot(x, slot))) return st;
   const int64_t l0 = launches_so_far();
-  enqueue_backward(x, slot);
+  enqueue_backward(x, x->stream, slot);
   x->launches += launches_so_far() - l0;
   if ((st = after_enqueue(x, "backward launch"))) return st;
   CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
@@ -539,7 +540,7 @@ hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world
 hg_status hg_allreduce_grads(hg_ctx *x) {
   hg_status st = usable(x);
   if (st) return st;
-  return enqueue_allreduce(x);
+  return enqueue_allreduce(x, x->stream);
 }
 
 hg_status hg_step(hg_ctx *x, const hg_adamw *h) {
@@ -547,7 +548,7 @@ hg_status hg_step(hg_ctx *x, const hg_adamw *h) {
   if (st) return st;
   if (!h) return fail(HG_E_INVALID, "null hyper");
   const int64_t l0 = launches_so_far();
-  enqueue_step(x, *h);
+  enqueue_step(x, x->stream, *h);
   x->launches += launches_so_far() - l0;
   return after_enqueue(x, "adamw launch");
 }
@@ -579,15 +580,17 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
     cudaGraphExecDestroy(x->graphs[slot]);
     x->graphs[slot] = nullptr;
   }
+  // capture on the ctx's private stream (the caller's may be the legacy
+  // default stream, which cannot be captured); replays go to the caller's stream
   cudaGraph_t g = nullptr;
-  CK(x, cudaStreamBeginCapture(x->stream, cudaStreamCaptureModeThreadLocal));
+  CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
-  enqueue_forward(x, slot);
-  enqueue_backward(x, slot);
-  hg_status ar = enqueue_allreduce(x);
-  enqueue_step(x, *h);
+  enqueue_forward(x, x->cap_stream, slot);
+  enqueue_backward(x, x->cap_stream, slot);
+  hg_status ar = enqueue_allreduce(x, x->cap_stream);
+  enqueue_step(x, x->cap_stream, *h);
   const int64_t nk = launches_so_far() - l0;
-  cudaError_t e = cudaStreamEndCapture(x->stream, &g);
+  cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
   if (ar) {
     if (g) cudaGraphDestroy(g);
     return ar;
@@ -610,12 +613,12 @@ hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms,
   CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
   Prof pr(x->stream);
   const int64_t l0 = launches_so_far();
-  enqueue_forward(x, slot, &pr);
-  enqueue_backward(x, slot, &pr);
+  enqueue_forward(x, x->stream, slot, &pr);
+  enqueue_backward(x, x->stream, slot, &pr);
   hg_status ar = HG_OK;
-  phase(&pr, HG_PHASE_ALLREDUCE, [&] { ar = enqueue_allreduce(x); });
+  phase(&pr, HG_PHASE_ALLREDUCE, [&] { ar = enqueue_allreduce(x, x->stream); });
   if (ar) return ar;
-  enqueue_step(x, *h, &pr);
+  enqueue_step(x, x->stream, *h, &pr);
   x->launches += launches_so_far() - l0;
   if ((st = after_enqueue(x, "profile launch"))) return st;
   CK(x, cudaEventRecord(x->compute_done[slot], x->stream));

@@ -88,6 +88,7 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
     dec, counts = O.replay(cache, gpu_decisions(ctx, N, H, L), head_relu_gpu=hpre > 0)
     res["overrides"] = counts["overrides"]
     res["out_of_band"] = counts["out_of_band"]
+    res["out_of_band_by"] = counts["out_of_band_by"]
     res["cells"] = int(sum(c["Z"].size * 4 for c in cache["layers"]))
     g = O.backward(params, b, ocfg, cache, dec)
     gg = hgnn.arena_to_dict(ctx.grads_get(), layout) if not graph or not do_step else None
@@ -121,23 +122,32 @@ def make_ctx(data, B, H, L, seed=2, n_slots=2, Hf=None):
 
 
 def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
-    assert res["yhat"] <= fwd_tol, res["yhat"]
-    if "loss" in res:
-        assert res["loss"] <= fwd_tol, res["loss"]
-    assert res["X"] <= fwd_tol, res["X"]
+    bad = []
+    if res["yhat"] > fwd_tol:
+        bad.append(("yhat", res["yhat"]))
+    if "loss" in res and res["loss"] > fwd_tol:
+        bad.append(("loss", res["loss"]))
+    if res["X"] > fwd_tol:
+        bad.append(("X", res["X"]))
     # GPU discrete decisions (ReLU masks, argmin/argmax, std floor) must agree with the
     # oracle wherever the oracle's margin exceeds tau; in-band
-    # overrides are equally valid choices and only reported.
-    assert res["out_of_band"] <= max(2, 1e-5 * res["cells"]), res["out_of_band"]
-    assert res["overrides"] <= 1e-3 * res["cells"], res["overrides"]
+    # overrides are equally valid choices and only bounded loosely.
+    if res["out_of_band"] > max(2, 1e-5 * res["cells"]):
+        bad.append(("out_of_band", res["out_of_band"], res["out_of_band_by"]))
+    if res["overrides"] > 1e-3 * res["cells"]:
+        bad.append(("overrides", res["overrides"], res["cells"]))
     if "grad_maxscaled" in res:
         for k, v in res["grad_maxscaled"].items():
-            assert v <= grad_tol, (k, v)
+            if v > grad_tol:
+                bad.append(("grad_maxscaled", k, v))
         for k, v in res["grad_normwise"].items():
-            assert v <= grad_tol, (k, v)
+            if v > grad_tol:
+                bad.append(("grad_normwise", k, v))
     if "param_normwise" in res:
         for k, v in res["param_normwise"].items():
-            assert v <= param_tol, (k, v)
+            if v > param_tol:
+                bad.append(("param_normwise", k, v))
+    assert not bad, bad
 
 
 def generate(preset, n, seed):

@@ -504,7 +504,7 @@ def test_decision_replay_is_identity_on_own_decisions(pcqm_small):
     _, _, cache = O.forward(p, b, cfg, delta)
     own = [dict(relu=c["Z"] > 0, argmax=c["argmax"], argmin=c["argmin"]) for c in cache["layers"]]
     dec, n = O.replay(cache, own)
-    assert n == {"overrides": 0, "out_of_band": 0}
+    assert n["overrides"] == 0 and n["out_of_band"] == 0
     g0 = O.backward(p, b, cfg, cache)
     g1 = O.backward(p, b, cfg, cache, dec)
     for k in g0:
