@@ -440,41 +440,78 @@ def decision_bands(cache: dict, tau: float = 1e-6, var_floor: float = VAR_FLOOR)
 
 
 def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
-    """Build ``decisions`` for ``backward``: inside each ambiguity band adopt the
-    GPU's decision, elsewhere keep the oracle's. Returns (decisions, counts) with
-    counts = {'overrides': in-band cells where the GPU chose differently (equally
-    valid at margin tau, e.g. automorphic atoms whose f64 states differ only by
-    summation order), 'out_of_band': cells where the GPU disagrees although the
-    oracle's margin exceeds tau (genuine disagreements), 'out_of_band_by': per
-    decision kind}. tau defaults to the forward tolerance 1e-4 (DESIGN.md
-    reading R-replay): a decision whose margin is below the accepted forward
-    error is not determined by a computation at that tolerance."""
-    bands = decision_bands(cache, tau)
+    """Decision replay for parity: where several discrete
+    decisions are correct at tolerance tau, adopt the GPU's; check the rest.
+
+    For every cell the GPU's decision is *valid* if it is optimal within tau
+    in the oracle's own float64 values:
+      argmax: m[gpu position] >= max - tau*|m|_inf   (argmin symmetric),
+      relu:   Z >= -tau*|Z|_inf if the GPU kept the unit, Z <= tau*|Z|_inf if not,
+      varflag: var within 0.5*eps_v of eps_v, or the same side as the GPU.
+    Valid GPU decisions are adopted (exact ties such as automorphic atoms,
+    whose float64 and fp32 roundings can break the tie differently, are
+    legitimately resolved either way); invalid ones are counted and the
+    oracle keeps its own decision, so they show up in the gradient error too.
+    tau defaults to the forward tolerance 1e-4 (reading R-replay).
+    Returns (decisions, {'overrides', 'out_of_band', 'out_of_band_by'})."""
     dec, n, bad = {}, 0, 0
     by = {"relu": 0, "argmax": 0, "argmin": 0, "varflag": 0, "head_relu": 0}
-    for l, (c, b, gdec) in enumerate(zip(cache["layers"], bands, gpu)):
+    for l, (c, gdec) in enumerate(zip(cache["layers"], gpu)):
+        zs = np.abs(c["Z"]).max() if c["Z"].size else 0.0
+        msg = c["msg"]
+        ms = np.abs(msg).max() if msg.size else 0.0
+        deg = c["deg"]
+        rowptr = np.concatenate([[0], np.cumsum(deg)])
+        has = (deg > 0)[:, None]
         own = dict(relu=c["Z"] > 0, argmax=c["argmax"], argmin=c["argmin"], varflag=c["var"] > VAR_FLOOR)
-        d = {}
-        for k in own:
+        d = dict(own)
+        if "relu" in gdec:
+            g = np.asarray(gdec["relu"])
+            valid = np.where(g, c["Z"] >= -tau * zs, c["Z"] <= tau * zs)
+            diff = g != own["relu"]
+            n += int((valid & diff).sum())
+            nb = int((~valid & diff).sum())
+            bad += nb
+            by["relu"] += nb
+            d["relu"] = np.where(valid, g, own["relu"])
+        for k, sign in (("argmax", 1.0), ("argmin", -1.0)):
             if k not in gdec:
-                d[k] = own[k]
                 continue
-            diff = np.asarray(gdec[k]) != own[k]
-            if k in ("argmax", "argmin", "varflag"):
-                diff &= (c["deg"] > 0)[:, None]  # d = 0 rows carry no decision
-            n += int((b[k] & diff).sum())
-            nb = int((~b[k] & diff).sum())
+            g = np.asarray(gdec[k]).astype(np.int64)
+            gpos = np.clip(g, 0, np.maximum(deg - 1, 0)[:, None])
+            idx = rowptr[:-1][:, None] + gpos
+            idx = np.where(has, idx, 0)
+            chan = np.broadcast_to(np.arange(msg.shape[1] if msg.size else g.shape[1]), g.shape)
+            gval = msg[idx, chan] if msg.size else np.zeros(g.shape)
+            ext = c["mx"] if sign > 0 else c["mn"]
+            valid = (sign * (gval - ext) >= -tau * ms) & (g < np.maximum(deg, 1)[:, None])
+            valid |= ~has
+            diff = (g != own[k]) & has
+            n += int((valid & diff).sum())
+            nb = int((~valid & diff).sum())
             bad += nb
             by[k] += nb
-            d[k] = np.where(b[k], gdec[k], own[k])
+            d[k] = np.where(valid & has, g, own[k])
+        if "varflag" in gdec:
+            g = np.asarray(gdec["varflag"])
+            band = np.abs(c["var"] - VAR_FLOOR) < 0.5 * VAR_FLOOR
+            diff = (g != own["varflag"]) & has
+            n += int((band & diff).sum())
+            nb = int((~band & diff).sum())
+            bad += nb
+            by["varflag"] += nb
+            d["varflag"] = np.where(band, g, own["varflag"])
         dec[l] = d
     if head_relu_gpu is not None:
         hp = cache["head"]["hpre"]
-        band = np.abs(hp) < tau * (np.abs(hp).max() if hp.size else 0.0)
+        hs = np.abs(hp).max() if hp.size else 0.0
+        g = np.asarray(head_relu_gpu)
         own = hp > 0
-        n += int((band & (head_relu_gpu != own)).sum())
-        nb = int((~band & (head_relu_gpu != own)).sum())
+        valid = np.where(g, hp >= -tau * hs, hp <= tau * hs)
+        diff = g != own
+        n += int((valid & diff).sum())
+        nb = int((~valid & diff).sum())
         bad += nb
         by["head_relu"] += nb
-        dec["head_relu"] = np.where(band, head_relu_gpu, own)
+        dec["head_relu"] = np.where(valid, g, own)
     return dec, {"overrides": n, "out_of_band": bad, "out_of_band_by": by}

@@ -509,3 +509,25 @@ def test_decision_replay_is_identity_on_own_decisions(pcqm_small):
     g1 = O.backward(p, b, cfg, cache, dec)
     for k in g0:
         np.testing.assert_array_equal(g0[k], g1[k])
+
+
+def test_replay_accepts_exact_ties_and_rejects_wrong_choices():
+    """Star graph with two identical leaves (an exact tie in exact arithmetic):
+    either leaf is a valid argmax; a clearly non-maximal choice is flagged."""
+    x = [[0.0], [2.0], [2.0], [1.0]]
+    st = make_store([(x, [(0, 1, [1.0]), (0, 2, [1.0]), (0, 3, [1.0])], 0.0)])
+    cfg = {"f_node": 1, "f_edge": 1, "hidden": 1, "layers": 1, "fc_hidden": 1}
+    p = {"conv0.M_x": np.ones((1, 1)), "conv0.M_e": np.zeros((1, 1)), "conv0.b_M": np.zeros(1),
+         "conv0.U": np.full((1, 12), 0.1), "conv0.b_U": np.zeros(1), "head.W1": np.ones((1, 1)),
+         "head.b1": np.zeros(1), "head.W2": np.ones((1, 1)), "head.b2": np.zeros(1)}
+    b = O.pack(st, [0])
+    _, _, cache = O.forward(p, b, cfg, 1.0)
+    c = cache["layers"][0]
+    assert c["argmax"][0, 0] == 0  # first of the tied leaves 1, 2
+    g = dict(argmax=c["argmax"].copy(), argmin=c["argmin"].copy())
+    g["argmax"][0, 0] = 1  # the other tied leaf: valid
+    _, cnt = O.replay(cache, [g])
+    assert cnt["overrides"] == 1 and cnt["out_of_band"] == 0
+    g["argmax"][0, 0] = 2  # leaf with x = 1: not a maximum
+    _, cnt = O.replay(cache, [g])
+    assert cnt["out_of_band"] == 1 and cnt["out_of_band_by"]["argmax"] == 1
