@@ -112,11 +112,15 @@ typedef struct {
   int32_t max_nodes;                 /* capacity: nodes per batch */
   int32_t max_edges;                 /* capacity: directed edges per batch */
   int32_t n_slots;                   /* device batch slots (>= 1; 2+ to overlap H2D with compute) */
-  int32_t reserved;
+  int32_t flags;                     /* HG_FLAG_*; 0 = defaults */
   double delta;                      /* PNA degree statistic (hg_degree_stat) */
   float var_floor;                   /* epsilon_v for the std aggregator, 1e-10 */
   float pad;
 } hg_config;
+
+/* hg_config.flags: force the SIMT fp32 GEMMs instead of the tcgen05 3xTF32
+ * tensor-core GEMMs (which are used whenever hidden % 128 == 0). */
+#define HG_FLAG_SIMT_GEMM 1
 
 typedef struct {
   float lr, beta1, beta2, eps, weight_decay;  /* 1e-3, 0.9, 0.999, 1e-8, 0.01 */

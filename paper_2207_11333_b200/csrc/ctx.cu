@@ -28,6 +28,7 @@ struct Plan {
   size_t dZa = 0, dZb = 0, dA = 0, dP = 0;
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
   size_t part = 0;
+  size_t UT = 0, u_off = 0;
   size_t total = 0;
 };
 
@@ -72,7 +73,10 @@ Plan make_plan(const hg_config &c) {
   Caps caps{c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge, c.hidden, c.fc_hidden};
   size_t pf = std::max({agg_bwd_partial_floats(caps), dU_partial_floats(caps), dMx_partial_floats(caps, c.f_node),
                         dMx_partial_floats(caps, c.hidden)});
+  if (tc_supported(caps)) pf = std::max(pf, tc_dU_partial_floats(caps));
   p.part = take(sizeof(float) * pf);
+  p.UT = take(sizeof(float) * (size_t)c.layers * 12 * H * H);
+  p.u_off = take(sizeof(int64_t) * (size_t)c.layers);
   p.total = off;
   return p;
 }
@@ -96,6 +100,7 @@ struct hg_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   int64_t launches = 0;
+  bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
   hg_status sticky = HG_OK;
   std::string sticky_msg;
 
@@ -200,8 +205,12 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) {
                      c.var_floor, x->f(p.A[l]), x->b(p.arg[l]));
     });
     phase(pr, HG_PHASE_UPDATE, [&] {
-      launch_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")), x->param(lname(l, "b_U")),
-                    x->f(p.X[l]));
+      if (x->use_tc)
+        launch_tc_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")),
+                         x->param(lname(l, "b_U")), x->f(p.X[l]));
+      else
+        launch_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")), x->param(lname(l, "b_U")),
+                      x->f(p.X[l]));
     });
   }
   phase(pr, HG_PHASE_HEAD_FWD, [&] {
@@ -222,11 +231,25 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) 
                     x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
                     x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
   });
+  if (x->use_tc)
+    phase(pr, HG_PHASE_DA, [&] {
+      launch_prep_UT(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers,
+                     x->f(p.UT));
+    });
   for (int l = c.layers - 1; l >= 0; --l) {
-    phase(pr, HG_PHASE_DA, [&] { launch_dA(st, x->caps, blob, dZ, amp, att, x->param(lname(l, "U")), x->f(p.dA)); });
+    phase(pr, HG_PHASE_DA, [&] {
+      if (x->use_tc)
+        launch_tc_dA(st, x->caps, blob, dZ, amp, att, x->f(p.UT) + (size_t)l * 12 * c.hidden * c.hidden, x->f(p.dA));
+      else
+        launch_dA(st, x->caps, blob, dZ, amp, att, x->param(lname(l, "U")), x->f(p.dA));
+    });
     phase(pr, HG_PHASE_DU, [&] {
-      launch_dU(st, x->caps, blob, dZ, x->f(p.A[l]), amp, att, x->f(p.part), x->grad(lname(l, "U")),
-                x->grad(lname(l, "b_U")));
+      if (x->use_tc)
+        launch_tc_dU(st, x->caps, blob, dZ, x->f(p.A[l]), amp, att, x->f(p.part), x->grad(lname(l, "U")),
+                     x->grad(lname(l, "b_U")));
+      else
+        launch_dU(st, x->caps, blob, dZ, x->f(p.A[l]), amp, att, x->f(p.part), x->grad(lname(l, "U")),
+                  x->grad(lname(l, "b_U")));
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
@@ -322,6 +345,17 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     x->graph_hyper.push_back(hg_adamw{});
   }
   if ((e = cudaMemsetAsync(workspace, 0, plan.total, x->stream)) != cudaSuccess) return bail(e, "cudaMemsetAsync");
+  x->use_tc = tc_supported(x->caps) && !(c->flags & HG_FLAG_SIMT_GEMM);
+  if (x->use_tc && (e = tc_configure()) != cudaSuccess) return bail(e, "tc_configure");
+  {
+    std::vector<int64_t> uo;
+    for (int l = 0; l < c->layers; ++l)
+      for (auto &t : x->lay)
+        if (t.name == lname(l, "U")) uo.push_back(t.offset);
+    if ((e = cudaMemcpyAsync(x->b(plan.u_off), uo.data(), sizeof(int64_t) * uo.size(), cudaMemcpyHostToDevice,
+                             x->stream)) != cudaSuccess)
+      return bail(e, "cudaMemcpyAsync");
+  }
   if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
   *out = x;
   return HG_OK;

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <atomic>
 
+#include "common.cuh"
 #include "kernels.h"
 #include "layout.h"
 
@@ -25,38 +26,6 @@ namespace hg {
 
 std::atomic<int64_t> g_launches{0};
 static inline void counted(int n = 1) { g_launches += n; }
-
-// ------------------------------------------------------------------ batch view
-struct BatchView {
-  int B, N, E, F0, Fe;
-  const int *gp;
-  const float *y;
-  const int *rowptr;
-  const int *col;
-  const float *x;
-  const float *ea;
-  const uint8_t *slot;
-};
-
-__device__ __forceinline__ BatchView load_batch(const uint8_t *blob) {
-  BatchView v;
-  const int *h = reinterpret_cast<const int *>(blob);
-  v.B = h[0]; v.N = h[1]; v.E = h[2]; v.F0 = h[3]; v.Fe = h[4];
-  const BatchOffsets o = batch_offsets(v.B, v.N, v.E, v.F0, v.Fe);
-  v.gp = reinterpret_cast<const int *>(blob + o.graph_ptr);
-  v.y = reinterpret_cast<const float *>(blob + o.y);
-  v.rowptr = reinterpret_cast<const int *>(blob + o.rowptr);
-  v.col = reinterpret_cast<const int *>(blob + o.col);
-  v.x = reinterpret_cast<const float *>(blob + o.x);
-  v.ea = reinterpret_cast<const float *>(blob + o.eattr);
-  v.slot = blob + o.slot;
-  return v;
-}
-
-__device__ __forceinline__ int batch_N(const uint8_t *blob) { return reinterpret_cast<const int *>(blob)[1]; }
-
-static inline int cdiv(int a, int b) { return (a + b - 1) / b; }
-static const int kSMs = 148;
 
 // ------------------------------------------------------------------ scalers
 // amplification ln(d+1)/delta and attenuation delta/ln(d+1), both 1 for d = 0

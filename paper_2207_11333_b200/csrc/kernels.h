@@ -63,6 +63,20 @@ struct AdamDev {
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
                   float lr, float beta1, float beta2, float eps, float wd);
 
+// tcgen05 3xTF32 GEMMs (tcgemm.cu); require H % 128 == 0
+bool tc_supported(const Caps &c);
+cudaError_t tc_configure();  // opt-in shared-memory sizes (call once, outside graph capture)
+void launch_tc_update(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *A, const float *amp,
+                      const float *att, const float *U, const float *bU, float *X1);
+void launch_tc_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *amp,
+                  const float *att, const float *UT, float *dA);
+void launch_tc_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
+                  const float *amp, const float *att, float *partial, float *dU, float *dbU);
+size_t tc_dU_partial_floats(const Caps &c);
+// UT[l][s*4H + n][h] = U_l[h][s*4H + n] for all layers (u_off: device array of U offsets in floats)
+void launch_prep_UT(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L,
+                    float *UT);
+
 // process-wide count of kernels launched by the wrappers above
 int64_t launches_so_far();
 

@@ -1,0 +1,422 @@
+// tcgemm.cu — fp32-accurate (3xTF32) tensor-core GEMMs on sm_100a (tcgen05 + TMEM)
+// for the three dense contractions of the PNA layer:
+//
+//   G1 update  Z = sum_s diag(s) A U_s^T + b_U, X' = ReLU(Z)
+//   G2 dA      dA = sum_s diag(s) dZ U_s
+//   G3 dU      dU_s = (diag(s) dZ)^T A   (split-K partials)
+//
+// The three degree scalers s in (identity, amplification, attenuation) are
+// per-row scalars, so G1/G2 keep THREE accumulators in TMEM (one per scaler,
+// stacked along the MMA N dimension: B rows = [U_id; U_amp; U_att] slices) and
+// fold amp/att in the epilogue — the 12H-wide concat is never materialised.
+// G3 has the scaler on the K (node) dimension, so it scales the B operand.
+//
+// Kernel structure (one 128-row output tile per CTA, 160 threads):
+//   warps 0-3  producers: global fp32 -> registers -> (scale) -> hi/lo split
+//              (3xTF32: a*b ~ ah*bh + ah*bl + al*bh) -> SW128 K-major smem stages;
+//              then the epilogue: tcgen05.ld of their 32 TMEM lanes -> global.
+//   warp 4     TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32,
+//              M=128, N = 3*BN), tcgen05.commit -> mbarriers.
+// Deterministic: every output element is produced by exactly one CTA (G3's
+// split-K partials are reduced in fixed order by k_reduce_parts).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace hg {
+
+extern std::atomic<int64_t> g_launches;
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 32;  // fp32 elements per 128-byte smem row
+constexpr int TC_PROD_WARPS = 4;
+constexpr int TC_THREADS = 32 * (TC_PROD_WARPS + 1);
+
+template <int N>
+struct TmemCols {
+  static constexpr int v = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
+};
+
+template <class Op>
+constexpr int tc_stage_bytes() {
+  return 2 * TC_BM * 128 + 2 * Op::NMMA * 128;
+}
+template <class Op>
+constexpr int tc_smem_bytes() {
+  return Op::STAGES * tc_stage_bytes<Op>() + 1024 /*align slack*/ + 8 * (2 * Op::STAGES + 1) + 16;
+}
+
+__device__ __forceinline__ float4 split_hi(float4 v, float4 &lo) {
+  float4 hi;
+  tc::split_tf32(v.x, hi.x, lo.x);
+  tc::split_tf32(v.y, hi.y, lo.y);
+  tc::split_tf32(v.z, hi.z, lo.z);
+  tc::split_tf32(v.w, hi.w, lo.w);
+  return hi;
+}
+
+template <class Op>
+__global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
+  Op op = op_in;
+  op.prepare();
+  int m0, n0, kb, ke;
+  if (!op.tile(blockIdx.x, m0, n0, kb, ke)) return;  // uniform: tile beyond the device-side size
+
+  constexpr int NMMA = Op::NMMA, ST = Op::STAGES, NACC = Op::NACC, BN = Op::BN;
+  constexpr int A_BYTES = TC_BM * 128, B_BYTES = NMMA * 128;
+  constexpr int STAGE = tc_stage_bytes<Op>();
+  constexpr int TCOLS = TmemCols<NMMA>::v;
+  static_assert(NMMA % 16 == 0 && NMMA <= 256, "MMA N for M=128 must be a multiple of 16 <= 256");
+  static_assert(NMMA == NACC * BN && BN % 32 == 0, "accumulator tiling");
+  static_assert(B_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE);
+  uint64_t *empty = full + ST;
+  uint64_t *accf = empty + ST;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NPROD = TC_PROD_WARPS * 32;
+  if (warp == TC_PROD_WARPS) tc::tmem_alloc<TCOLS>(tmem_holder);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ST; ++s) {
+      tc::mbar_init(&full[s], NPROD);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(accf, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_holder;
+  const int nchunks = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;
+
+  if (warp < TC_PROD_WARPS) {
+    const int t = threadIdx.x;
+    for (int c = 0; c < nchunks; ++c) {
+      const int s = c % ST;
+      if (c >= ST) tc::mbar_wait(&empty[s], ((c / ST) - 1) & 1);
+      uint8_t *sAh = smem + s * STAGE;
+      uint8_t *sAl = sAh + A_BYTES;
+      uint8_t *sBh = sAl + A_BYTES;
+      uint8_t *sBl = sBh + B_BYTES;
+      const int k0 = kb + c * TC_BK;
+#pragma unroll 4
+      for (int task = t; task < TC_BM * 8; task += NPROD) {
+        int r, j;
+        if (Op::A_MN) { r = task % TC_BM; j = task / TC_BM; } else { r = task >> 3; j = task & 7; }
+        float4 lo;
+        const float4 hi = split_hi(op.a4(m0 + r, k0 + 4 * j, ke), lo);
+        const uint32_t o = tc::sw128_off(r, j);
+        *reinterpret_cast<float4 *>(sAh + o) = hi;
+        *reinterpret_cast<float4 *>(sAl + o) = lo;
+      }
+#pragma unroll 4
+      for (int task = t; task < NMMA * 8; task += NPROD) {
+        int r, j;
+        if (Op::B_MN) { r = task % NMMA; j = task / NMMA; } else { r = task >> 3; j = task & 7; }
+        float4 lo;
+        const float4 hi = split_hi(op.b4(n0, r, k0 + 4 * j, ke), lo);
+        const uint32_t o = tc::sw128_off(r, j);
+        *reinterpret_cast<float4 *>(sBh + o) = hi;
+        *reinterpret_cast<float4 *>(sBl + o) = lo;
+      }
+      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&full[s]);
+    }
+    // ---- epilogue: this thread owns accumulator row (TMEM lane) warp*32 + lane
+    tc::mbar_wait(accf, 0);
+    tc::fence_after_sync();
+    const int row = warp * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+    for (int q = 0; q < BN / 32; ++q) {
+      float acc[NACC][32];
+#pragma unroll
+      for (int a = 0; a < NACC; ++a) {
+        if (nchunks) {
+          tc::tmem_ld32(trow + (uint32_t)(a * BN + q * 32), acc[a]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) acc[a][i] = 0.f;
+        }
+      }
+      op.store(m0 + row, n0, q * 32, acc);
+    }
+  } else if (warp == TC_PROD_WARPS) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(TC_BM, NMMA);
+      for (int c = 0; c < nchunks; ++c) {
+        const int s = c % ST;
+        tc::mbar_wait(&full[s], (c / ST) & 1);
+        tc::fence_after_sync();
+        const uint32_t aH = tc::smem_u32(smem + s * STAGE);
+        const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < TC_BK / 8; ++ks) {  // K = 8 tf32 (32 bytes) per MMA
+          const uint32_t off = ks * 32;
+          const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
+          const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+          tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
+          tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
+          tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+        }
+        tc::mma_commit(&empty[s]);  // frees the stage when these MMAs have read it
+      }
+      tc::mma_commit(accf);  // accumulators complete
+    }
+    __syncwarp();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == TC_PROD_WARPS) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<TCOLS>(tmem);
+  }
+}
+
+template <class Op>
+static cudaError_t configure_tc() {
+  return cudaFuncSetAttribute(k_tcgemm<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, tc_smem_bytes<Op>());
+}
+
+template <class Op>
+static void run_tc(cudaStream_t st, const Op &op, int grid) {
+  k_tcgemm<Op><<<std::max(grid, 1), TC_THREADS, tc_smem_bytes<Op>(), st>>>(op);
+  g_launches += 1;
+}
+
+__device__ __forceinline__ float scal(const float *amp, const float *att, int m, int s) {
+  return s == 0 ? 1.0f : (s == 1 ? amp[m] : att[m]);
+}
+
+// ---------------------------------------------------------------- G1 update
+struct TcUpdate {
+  static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 3;
+  static constexpr bool A_MN = false, B_MN = false;
+  const uint8_t *blob; const float *A; const float *amp; const float *att; const float *U; const float *bU;
+  float *X1; int H; int N;
+  __device__ void prepare() { N = batch_N(blob); }
+  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) const {
+    const int nt = H / BN;
+    m0 = (t / nt) * TC_BM;
+    n0 = (t % nt) * BN;
+    kb = 0;
+    ke = 4 * H;
+    return m0 < N;
+  }
+  __device__ float4 a4(int m, int k, int) const {
+    return m < N ? ldg4(A + (size_t)m * 4 * H + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ float4 b4(int n0, int r, int k, int) const {
+    const int s = r / BN, c = r - s * BN;
+    return ldg4(U + (size_t)(n0 + c) * 12 * H + s * 4 * H + k);
+  }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
+    if (m >= N) return;
+    const float a1 = amp[m], a2 = att[m];
+    float *out = X1 + (size_t)m * H + n0 + q0;
+    const float *b = bU + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 z;
+      z.x = fmaxf(acc[0][i + 0] + a1 * acc[1][i + 0] + a2 * acc[2][i + 0] + b[i + 0], 0.f);
+      z.y = fmaxf(acc[0][i + 1] + a1 * acc[1][i + 1] + a2 * acc[2][i + 1] + b[i + 1], 0.f);
+      z.z = fmaxf(acc[0][i + 2] + a1 * acc[1][i + 2] + a2 * acc[2][i + 2] + b[i + 2], 0.f);
+      z.w = fmaxf(acc[0][i + 3] + a1 * acc[1][i + 3] + a2 * acc[2][i + 3] + b[i + 3], 0.f);
+      *reinterpret_cast<float4 *>(out + i) = z;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- G2 dA
+// B_s[n, h] = U[h, s*4H + n] read from the transposed copy UT[s][n][h] (prepared per step)
+struct TcDA {
+  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2;
+  static constexpr bool A_MN = false, B_MN = false;
+  const uint8_t *blob; const float *dZ; const float *amp; const float *att; const float *UT; float *dA; int H; int N;
+  __device__ void prepare() { N = batch_N(blob); }
+  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) const {
+    const int nt = 4 * H / BN;
+    m0 = (t / nt) * TC_BM;
+    n0 = (t % nt) * BN;
+    kb = 0;
+    ke = H;
+    return m0 < N;
+  }
+  __device__ float4 a4(int m, int k, int) const {
+    return m < N ? ldg4(dZ + (size_t)m * H + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ float4 b4(int n0, int r, int k, int) const {
+    const int s = r / BN, c = r - s * BN;
+    return ldg4(UT + ((size_t)s * 4 * H + n0 + c) * H + k);
+  }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
+    if (m >= N) return;
+    const float a1 = amp[m], a2 = att[m];
+    float *out = dA + (size_t)m * 4 * H + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      float4 z;
+      z.x = acc[0][i + 0] + a1 * acc[1][i + 0] + a2 * acc[2][i + 0];
+      z.y = acc[0][i + 1] + a1 * acc[1][i + 1] + a2 * acc[2][i + 1];
+      z.z = acc[0][i + 2] + a1 * acc[1][i + 2] + a2 * acc[2][i + 2];
+      z.w = acc[0][i + 3] + a1 * acc[1][i + 3] + a2 * acc[2][i + 3];
+      *reinterpret_cast<float4 *>(out + i) = z;
+    }
+  }
+};
+
+// ---------------------------------------------------------------- G3 dU (split-K over nodes)
+// A(m=h, k=i) = dZ[i, h] (MN-major), B(r=(s,c), k=i) = s_i A_l[i, n0+c]; output
+// partial[sp][h][s*4H + n] for the fixed-order reduction.
+constexpr int kTcDUSplits = 16;
+struct TcDU {
+  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2;
+  static constexpr bool A_MN = true, B_MN = true;
+  const uint8_t *blob; const float *dZ; const float *A; const float *amp; const float *att; float *part; int H;
+  int N; int sp;
+  __device__ void prepare() { N = batch_N(blob); }
+  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) {
+    const int nt = 4 * H / BN, mt = H / TC_BM;
+    sp = t % kTcDUSplits;
+    const int t2 = t / kTcDUSplits;
+    n0 = (t2 % nt) * BN;
+    m0 = (t2 / nt) * TC_BM;
+    if (m0 >= mt * TC_BM) return false;
+    int kc = (N + kTcDUSplits - 1) / kTcDUSplits;
+    kc = (kc + TC_BK - 1) / TC_BK * TC_BK;
+    kb = sp * kc;
+    ke = min(N, kb + kc);
+    return true;  // empty splits still write their (zero) partial
+  }
+  __device__ float4 a4(int m, int k, int ke) const {
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = (k + u < ke) ? __ldg(dZ + (size_t)(k + u) * H + m) : 0.f;
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ float4 b4(int n0, int r, int k, int ke) const {
+    const int s = r / BN, c = r - s * BN;
+    float v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      v[u] = (k + u < ke) ? __ldg(A + (size_t)(k + u) * 4 * H + n0 + c) * scal(amp, att, k + u, s) : 0.f;
+    return make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
+    float *base = part + (size_t)sp * H * 12 * H + (size_t)m * 12 * H;
+#pragma unroll
+    for (int s = 0; s < 3; ++s) {
+      float *out = base + s * 4 * H + n0 + q0;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4 *>(out + i) = make_float4(acc[s][i], acc[s][i + 1], acc[s][i + 2], acc[s][i + 3]);
+    }
+  }
+};
+
+__global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
+  const int c4 = count / 4;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < c4; e += gridDim.x * blockDim.x) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int p = 0; p < nparts; ++p) {
+      const float4 v = ldg4(part + (size_t)p * count + 4 * (size_t)e);
+      s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+    }
+    reinterpret_cast<float4 *>(out)[e] = s;
+  }
+}
+
+// db_U = sum_i dZ[i, :] — per-chunk partial column sums then fixed-order reduce
+constexpr int kColsumChunks = 64;
+__global__ void k_colsum_part(const uint8_t *__restrict__ blob, const float *__restrict__ X, int H,
+                              float *__restrict__ part) {
+  const int N = batch_N(blob);
+  const int per = (N + kColsumChunks - 1) / kColsumChunks;
+  const int ch = blockIdx.x;
+  const int i0 = ch * per, i1 = min(N, i0 + per);
+  for (int h = threadIdx.x; h < H; h += blockDim.x) {
+    float s = 0.f;
+    for (int i = i0; i < i1; ++i) s += X[(size_t)i * H + h];
+    part[(size_t)ch * H + h] = s;
+  }
+}
+
+// UT[l][s][n][h] = U_l[h][s*4H + n] for every layer (32x32 smem-tiled transpose)
+__global__ void k_prep_UT(const float *__restrict__ params, const int64_t *__restrict__ u_off, int L, int H,
+                          float *__restrict__ UT) {
+  __shared__ float tile[32][33];
+  const int W = 12 * H;  // U row length
+  const int tilesC = W / 32, tilesR = H / 32;
+  const int per_layer = tilesC * tilesR;
+  for (int t = blockIdx.x; t < L * per_layer; t += gridDim.x) {
+    const int l = t / per_layer, tt = t % per_layer;
+    const int tr = tt / tilesC, tc = tt % tilesC;  // rows h, cols j = s*4H + n
+    const float *U = params + u_off[l];
+    for (int r = threadIdx.y; r < 32; r += blockDim.y)
+      tile[r][threadIdx.x] = U[(size_t)(tr * 32 + r) * W + tc * 32 + threadIdx.x];
+    __syncthreads();
+    float *out = UT + (size_t)l * W * H;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y)  // out row = j (= s*4H + n), col = h
+      out[(size_t)(tc * 32 + r) * H + tr * 32 + threadIdx.x] = tile[threadIdx.x][r];
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- launch wrappers
+static int mtiles(int n) { return (n + TC_BM - 1) / TC_BM; }
+
+void launch_tc_update(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *A, const float *amp,
+                      const float *att, const float *U, const float *bU, float *X1) {
+  TcUpdate op{blob, A, amp, att, U, bU, X1, c.H, 0};
+  run_tc(st, op, mtiles(c.maxN) * (c.H / TcUpdate::BN));
+}
+
+void launch_tc_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *amp,
+                  const float *att, const float *UT, float *dA) {
+  TcDA op{blob, dZ, amp, att, UT, dA, c.H, 0};
+  run_tc(st, op, mtiles(c.maxN) * (4 * c.H / TcDA::BN));
+}
+
+size_t tc_dU_partial_floats(const Caps &c) {
+  return std::max((size_t)kTcDUSplits * c.H * 12 * c.H, (size_t)kColsumChunks * c.H);
+}
+
+void launch_tc_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
+                  const float *amp, const float *att, float *partial, float *dU, float *dbU) {
+  TcDU op{blob, dZ, A, amp, att, partial, c.H, 0, 0};
+  run_tc(st, op, (c.H / TC_BM) * (4 * c.H / TcDU::BN) * kTcDUSplits);
+  const int count = c.H * 12 * c.H;
+  k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDUSplits, count, dU);
+  k_colsum_part<<<kColsumChunks, 128, 0, st>>>(blob, dZ, c.H, partial);
+  k_reduce_parts<<<1, 256, 0, st>>>(partial, kColsumChunks, c.H, dbU);
+  g_launches += 3;
+}
+
+void launch_prep_UT(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L,
+                    float *UT) {
+  const int blocks = std::min(L * (12 * c.H / 32) * (c.H / 32), kSMs * 8);
+  k_prep_UT<<<blocks, dim3(32, 8), 0, st>>>(params, u_off_dev, L, c.H, UT);
+  g_launches += 1;
+}
+
+bool tc_supported(const Caps &c) { return c.H % 128 == 0; }
+
+cudaError_t tc_configure() {
+  cudaError_t e;
+  if ((e = configure_tc<TcUpdate>()) != cudaSuccess) return e;
+  if ((e = configure_tc<TcDA>()) != cudaSuccess) return e;
+  return configure_tc<TcDU>();
+}
+
+}  // namespace hg

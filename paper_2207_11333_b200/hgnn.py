@@ -51,7 +51,7 @@ class hg_config(ctypes.Structure):
     _fields_ = [("f_node", ctypes.c_int32), ("f_edge", ctypes.c_int32), ("hidden", ctypes.c_int32),
                 ("layers", ctypes.c_int32), ("fc_hidden", ctypes.c_int32), ("max_graphs", ctypes.c_int32),
                 ("max_nodes", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("n_slots", ctypes.c_int32),
-                ("reserved", ctypes.c_int32), ("delta", ctypes.c_double), ("var_floor", ctypes.c_float),
+                ("flags", ctypes.c_int32), ("delta", ctypes.c_double), ("var_floor", ctypes.c_float),
                 ("pad", ctypes.c_float)]
 
 
@@ -150,10 +150,13 @@ def _ptr(a: np.ndarray):
 DEFAULT_ADAMW = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
 
 
+HG_FLAG_SIMT_GEMM = 1
+
+
 def make_config(f_node, f_edge, hidden, layers, max_graphs, max_nodes, max_edges, delta, fc_hidden=None,
-                n_slots=2, var_floor=1e-10) -> hg_config:
+                n_slots=2, var_floor=1e-10, flags=0) -> hg_config:
     return hg_config(f_node=f_node, f_edge=f_edge, hidden=hidden, layers=layers, fc_hidden=fc_hidden or hidden,
-                     max_graphs=max_graphs, max_nodes=max_nodes, max_edges=max_edges, n_slots=n_slots, reserved=0,
+                     max_graphs=max_graphs, max_nodes=max_nodes, max_edges=max_edges, n_slots=n_slots, flags=flags,
                      delta=float(delta), var_floor=var_floor, pad=0.0)
 
 

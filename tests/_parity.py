@@ -14,7 +14,7 @@ import numpy as np
 import molgen
 import oracle as O
 from paper_2207_11333_b200 import hgnn
-from tests._util import max_scaled, normwise
+from tests._util import max_scaled, normwise  # noqa: F401
 
 FWD_TOL = 1e-4
 GRAD_TOL = 1e-3

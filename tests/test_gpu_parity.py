@@ -74,6 +74,7 @@ def test_config_a_free_running_epoch(torch_cuda):
     ("aisd", 64, 128, 3),    # AISD-shaped molecules (F0 = 9)
     ("pcqm", 16, 256, 2),    # two 128-channel chunks per node
     ("tiny", 7, 64, 2),      # H not a multiple of 128 (one channel per lane), ragged batch
+    ("tiny", 300, 128, 2),   # 128-row tiles with a ragged last tile, many tiny graphs
 ])
 def test_one_step_parity(torch_cuda, preset, B, H, L):
     data = PT.generate(preset, max(600, 4 * B), 21)
@@ -82,6 +83,27 @@ def test_one_step_parity(torch_cuda, preset, B, H, L):
     res = PT.run_step_parity(data, ids, ctx, cfg, delta)
     print(preset, B, H, L, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     PT.assert_parity(res)
+
+
+def test_simt_and_tcgen05_paths_agree(torch_cuda):
+    """The tcgen05 3xTF32 GEMMs and the SIMT fp32 GEMMs compute the same step:
+    both within the oracle bars, and close to each other (config B shape)."""
+    data = PT.generate("pcqm", 600, 51)
+    ids = O.shard(5, 0, 0, 1, 600)[:128]
+    grads = []
+    for flags in (hgnn.HG_FLAG_SIMT_GEMM, 0):
+        delta = O.degree_stat(data)
+        maxn, maxe = PT.capacity_for(data, 128)
+        cfg = hgnn.make_config(data["f_node"], 4, 128, 6, 128, maxn, maxe, delta, flags=flags)
+        ctx = hgnn.Context(cfg)
+        ctx.params_init(7)
+        ctx._store = hgnn.Store(data)
+        res = PT.run_step_parity(data, ids, ctx, cfg, delta, do_step=False)
+        print("flags", flags, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
+        PT.assert_parity(res)
+        grads.append(hgnn.arena_to_dict(ctx.grads_get(), ctx.layout))
+    for k in grads[0]:
+        assert PT.max_scaled(grads[1][k], grads[0][k]) <= 1e-3, k
 
 
 def test_edge_cases_isolated_nodes_single_graph_max_degree(torch_cuda):
