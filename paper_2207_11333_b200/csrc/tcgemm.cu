@@ -35,7 +35,7 @@ extern std::atomic<int64_t> g_launches;
 
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;  // fp32 elements per 128-byte smem row
-constexpr int TC_PROD_WARPS = 4;
+constexpr int TC_PROD_WARPS = 8;  // two warpgroups: producers, then the epilogue
 constexpr int TC_THREADS = 32 * (TC_PROD_WARPS + 1);
 
 template <int N>
@@ -102,6 +102,28 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
 
   if (warp < TC_PROD_WARPS) {
     const int t = threadIdx.x;
+    // register-staged software pipeline: the loads of chunk c+1 are in flight
+    // while chunk c is split, stored and consumed by the tensor core
+    constexpr int NA = TC_BM * 8 / NPROD, NB = (NMMA * 8 + NPROD - 1) / NPROD;
+    float4 ra[NA], rb[NB];
+    auto load = [&](int c) {
+      const int k0 = kb + c * TC_BK;
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int task = t + i * NPROD;
+        int r, j;
+        if (Op::A_MN) { r = task % TC_BM; j = task / TC_BM; } else { r = task >> 3; j = task & 7; }
+        ra[i] = op.a4(m0 + r, k0 + 4 * j, ke);
+      }
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const int task = t + i * NPROD;
+        int r, j;
+        if (Op::B_MN) { r = task % NMMA; j = task / NMMA; } else { r = task >> 3; j = task & 7; }
+        if (task < NMMA * 8) rb[i] = op.b4(n0, r, k0 + 4 * j, ke);
+      }
+    };
+    if (nchunks) load(0);
     for (int c = 0; c < nchunks; ++c) {
       const int s = c % ST;
       if (c >= ST) tc::mbar_wait(&empty[s], ((c / ST) - 1) & 1);
@@ -109,37 +131,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
       uint8_t *sAl = sAh + A_BYTES;
       uint8_t *sBh = sAl + A_BYTES;
       uint8_t *sBl = sBh + B_BYTES;
-      const int k0 = kb + c * TC_BK;
-#pragma unroll 4
-      for (int task = t; task < TC_BM * 8; task += NPROD) {
+#pragma unroll
+      for (int i = 0; i < NA; ++i) {
+        const int task = t + i * NPROD;
         int r, j;
         if (Op::A_MN) { r = task % TC_BM; j = task / TC_BM; } else { r = task >> 3; j = task & 7; }
         float4 lo;
-        const float4 hi = split_hi(op.a4(m0 + r, k0 + 4 * j, ke), lo);
+        const float4 hi = split_hi(ra[i], lo);
         const uint32_t o = tc::sw128_off(r, j);
         *reinterpret_cast<float4 *>(sAh + o) = hi;
         *reinterpret_cast<float4 *>(sAl + o) = lo;
       }
-#pragma unroll 4
-      for (int task = t; task < NMMA * 8; task += NPROD) {
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        const int task = t + i * NPROD;
+        if (task >= NMMA * 8) break;
         int r, j;
         if (Op::B_MN) { r = task % NMMA; j = task / NMMA; } else { r = task >> 3; j = task & 7; }
         float4 lo;
-        const float4 hi = split_hi(op.b4(n0, r, k0 + 4 * j, ke), lo);
+        const float4 hi = split_hi(rb[i], lo);
         const uint32_t o = tc::sw128_off(r, j);
         *reinterpret_cast<float4 *>(sBh + o) = hi;
         *reinterpret_cast<float4 *>(sBl + o) = lo;
       }
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full[s]);
+      if (c + 1 < nchunks) load(c + 1);
     }
-    // ---- epilogue: this thread owns accumulator row (TMEM lane) warp*32 + lane
+    // ---- epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one accumulator row per
+    // thread); the two warpgroups split the 32-column chunks of each accumulator
     tc::mbar_wait(accf, 0);
     tc::fence_after_sync();
-    const int row = warp * 32 + lane;
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    const int wq = warp & 3, wg = warp >> 2;
+    const int row = wq * 32 + lane;
+    const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
 #pragma unroll 1
-    for (int q = 0; q < BN / 32; ++q) {
+    for (int q = wg; q < BN / 32; q += TC_PROD_WARPS / 4) {
       float acc[NACC][32];
 #pragma unroll
       for (int a = 0; a < NACC; ++a) {
