@@ -556,11 +556,17 @@ __global__ void __launch_bounds__(256) k_agg_bwd(const uint8_t *__restrict__ blo
   }
 }
 
+// fixed-order reduction of nparts partial vectors: one warp per output element;
+// lanes stride over the parts, then a fixed xor-shuffle tree (deterministic)
 __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < count; e += gridDim.x * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < count; e += gridDim.x * wpb) {
     float s = 0.f;
-    for (int p = 0; p < nparts; ++p) s += part[(size_t)p * count + e];
-    out[e] = s;
+    for (int p = lane; p < nparts; p += 32) s += part[(size_t)p * count + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[e] = s;
   }
 }
 
@@ -577,7 +583,7 @@ void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
   else k_agg_bwd<1><<<grid, 256, 0, st>>>(blob, P, Me, bM, A, arg, dA, dP, partial, c.H);
   counted();
   const int count = c.H * c.Fe;
-  k_reduce_rows<<<std::max(1, std::min(cdiv(count, 128), kSMs)), 128, 0, st>>>(partial, nb, count, dMe);
+  k_reduce_rows<<<std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st>>>(partial, nb, count, dMe);
   counted();
 }
 

@@ -77,9 +77,11 @@ __device__ __forceinline__ void mma_commit(uint64_t *bar) {
                : "memory");
 }
 
-// instruction descriptor: fp32 accumulate, A = B = TF32, both K-major, M = 128
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+// instruction descriptor: fp32 accumulate, A = B = TF32, M x N; a_mn / b_mn select
+// MN-major (1) instead of K-major (0) operand layouts
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn = false, bool b_mn = false) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
 // shared-memory descriptor: K-major, SWIZZLE_128B (layout type 2), SBO = 1024 B
@@ -87,6 +89,20 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1u << 16) | ((uint64_t)(1024u >> 4) << 32) |
          ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+
+// shared-memory descriptor: MN-major, SWIZZLE_128B. Atom = 8 k-rows x 128 bytes
+// (32 tf32 along MN); LBO = stride between 32-element MN blocks, SBO = stride
+// between 8-row K groups.
+__device__ __forceinline__ uint64_t desc_sw128_mn(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
+}
+
+// byte offset of the 16-byte chunk holding MN elements [4c, 4c+4) of MN block b at
+// k-row kr (0..31 within a 32-k stage) in an MN-major SW128 tile with nblk MN blocks
+__device__ __forceinline__ uint32_t sw128_mn_off(int b, int c, int kr, int nblk) {
+  return (uint32_t)((kr >> 3) * nblk * 1024 + b * 1024 + (kr & 7) * 128 + ((c ^ (kr & 7)) << 4));
 }
 
 // byte offset of 16-byte chunk j (0..7) of row r inside a SW128 K-major tile

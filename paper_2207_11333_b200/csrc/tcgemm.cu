@@ -61,6 +61,25 @@ __device__ __forceinline__ float4 split_hi(float4 v, float4 &lo) {
   return hi;
 }
 
+// operand tile geometry inside one K-chunk stage (ROWS x 32 k):
+//   K-major  : task -> (row r = task/8, 16-byte k-chunk j = task%8); load 4 k's of row r
+//   MN-major : task -> (k-row kr = task/(ROWS/4), 4-row group g = task%(ROWS/4)); load 4 rows at k
+template <bool MN, int ROWS>
+__device__ __forceinline__ void task_coords(int task, int &r, int &kk) {
+  if (MN) { kk = task / (ROWS / 4); r = (task % (ROWS / 4)) * 4; }
+  else { r = task >> 3; kk = (task & 7) * 4; }
+}
+template <bool MN, int ROWS>
+__device__ __forceinline__ uint32_t tile_off(int r, int kk) {
+  if (MN) return tc::sw128_mn_off((r >> 5), (r >> 2) & 7, kk, ROWS / 32);
+  return tc::sw128_off(r, kk >> 2);
+}
+template <bool MN, int ROWS>
+__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
+  if (MN) return tc::desc_sw128_mn(base + ks * (ROWS / 32) * 1024, 1024, (ROWS / 32) * 1024);
+  return tc::desc_sw128(base + ks * 32);
+}
+
 template <class Op>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   Op op = op_in;
@@ -68,13 +87,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   int m0, n0, kb, ke;
   if (!op.tile(blockIdx.x, m0, n0, kb, ke)) return;  // uniform: tile beyond the device-side size
 
-  constexpr int NMMA = Op::NMMA, ST = Op::STAGES, NACC = Op::NACC, BN = Op::BN;
+  constexpr int NMMA = Op::NMMA, ST = Op::STAGES, NACC = Op::NACC, BN = Op::BN, PF = Op::PF;
+  constexpr bool AMN = Op::A_MN, BMN = Op::B_MN;
   constexpr int A_BYTES = TC_BM * 128, B_BYTES = NMMA * 128;
   constexpr int STAGE = tc_stage_bytes<Op>();
   constexpr int TCOLS = TmemCols<NMMA>::v;
   static_assert(NMMA % 16 == 0 && NMMA <= 256, "MMA N for M=128 must be a multiple of 16 <= 256");
   static_assert(NMMA == NACC * BN && BN % 32 == 0, "accumulator tiling");
-  static_assert(B_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
+  static_assert(B_BYTES % 1024 == 0 && (!BMN || NMMA % 32 == 0), "SW128 tiles need 1024-byte alignment");
+  static_assert(PF >= 1 && PF <= 4, "prefetch depth");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -102,61 +123,78 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
 
   if (warp < TC_PROD_WARPS) {
     const int t = threadIdx.x;
-    // register-staged software pipeline: the loads of chunk c+1 are in flight
-    // while chunk c is split, stored and consumed by the tensor core
+    // PF-deep register ring: raw global loads of chunk c+PF-1 are issued before
+    // chunk c is transformed (operand fix-up, 3xTF32 split) and stored, so PF-1
+    // chunks of loads are always in flight behind the tensor core.
     constexpr int NA = TC_BM * 8 / NPROD, NB = (NMMA * 8 + NPROD - 1) / NPROD;
-    float4 ra[NA], rb[NB];
-    auto load = [&](int c) {
+    float4 ra[PF][NA], rb[PF][NB];
+    auto issue = [&](int c, float4 (&xa)[NA], float4 (&xb)[NB]) {
       const int k0 = kb + c * TC_BK;
 #pragma unroll
       for (int i = 0; i < NA; ++i) {
-        const int task = t + i * NPROD;
-        int r, j;
-        if (Op::A_MN) { r = task % TC_BM; j = task / TC_BM; } else { r = task >> 3; j = task & 7; }
-        ra[i] = op.a4(m0 + r, k0 + 4 * j, ke);
+        int r, kk;
+        task_coords<AMN, TC_BM>(t + i * NPROD, r, kk);
+        xa[i] = op.a_ld(m0 + r, k0 + kk, ke);
       }
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
         const int task = t + i * NPROD;
-        int r, j;
-        if (Op::B_MN) { r = task % NMMA; j = task / NMMA; } else { r = task >> 3; j = task & 7; }
-        if (task < NMMA * 8) rb[i] = op.b4(n0, r, k0 + 4 * j, ke);
+        if (task < NMMA * 8) {
+          int r, kk;
+          task_coords<BMN, NMMA>(task, r, kk);
+          xb[i] = op.b_ld(n0, r, k0 + kk, ke);
+        }
       }
     };
-    if (nchunks) load(0);
-    for (int c = 0; c < nchunks; ++c) {
+    auto commit = [&](int c, const float4 (&xa)[NA], const float4 (&xb)[NB]) {
       const int s = c % ST;
       if (c >= ST) tc::mbar_wait(&empty[s], ((c / ST) - 1) & 1);
       uint8_t *sAh = smem + s * STAGE;
       uint8_t *sAl = sAh + A_BYTES;
       uint8_t *sBh = sAl + A_BYTES;
       uint8_t *sBl = sBh + B_BYTES;
+      const int k0 = kb + c * TC_BK;
 #pragma unroll
       for (int i = 0; i < NA; ++i) {
-        const int task = t + i * NPROD;
-        int r, j;
-        if (Op::A_MN) { r = task % TC_BM; j = task / TC_BM; } else { r = task >> 3; j = task & 7; }
+        int r, kk;
+        task_coords<AMN, TC_BM>(t + i * NPROD, r, kk);
         float4 lo;
-        const float4 hi = split_hi(ra[i], lo);
-        const uint32_t o = tc::sw128_off(r, j);
+        const float4 hi = split_hi(op.a_fix(xa[i], m0 + r, k0 + kk, ke), lo);
+        const uint32_t o = tile_off<AMN, TC_BM>(r, kk);
         *reinterpret_cast<float4 *>(sAh + o) = hi;
         *reinterpret_cast<float4 *>(sAl + o) = lo;
       }
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
         const int task = t + i * NPROD;
-        if (task >= NMMA * 8) break;
-        int r, j;
-        if (Op::B_MN) { r = task % NMMA; j = task / NMMA; } else { r = task >> 3; j = task & 7; }
-        float4 lo;
-        const float4 hi = split_hi(rb[i], lo);
-        const uint32_t o = tc::sw128_off(r, j);
-        *reinterpret_cast<float4 *>(sBh + o) = hi;
-        *reinterpret_cast<float4 *>(sBl + o) = lo;
+        if (task < NMMA * 8) {
+          int r, kk;
+          task_coords<BMN, NMMA>(task, r, kk);
+          float4 lo;
+          const float4 hi = split_hi(op.b_fix(xb[i], n0, r, k0 + kk, ke), lo);
+          const uint32_t o = tile_off<BMN, NMMA>(r, kk);
+          *reinterpret_cast<float4 *>(sBh + o) = hi;
+          *reinterpret_cast<float4 *>(sBl + o) = lo;
+        }
       }
       tc::fence_proxy_async_smem();
       tc::mbar_arrive(&full[s]);
-      if (c + 1 < nchunks) load(c + 1);
+    };
+#pragma unroll
+    for (int p = 0; p < PF - 1; ++p)
+      if (p < nchunks) issue(p, ra[p], rb[p]);
+    for (int c0 = 0; c0 < nchunks; c0 += PF) {
+#pragma unroll
+      for (int p = 0; p < PF; ++p) {
+        const int c = c0 + p;
+        if (c < nchunks) {
+          constexpr int dummy = 0;
+          (void)dummy;
+          const int q = (p + PF - 1) % PF;  // ring slot freed by chunk c-1
+          if (c + PF - 1 < nchunks) issue(c + PF - 1, ra[q], rb[q]);
+          commit(c, ra[p], rb[p]);
+        }
+      }
     }
     // ---- epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one accumulator row per
     // thread); the two warpgroups split the 32-column chunks of each accumulator
@@ -181,7 +219,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
     }
   } else if (warp == TC_PROD_WARPS) {
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(TC_BM, NMMA);
+      constexpr uint32_t idesc = tc::idesc_tf32(TC_BM, NMMA, AMN, BMN);
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % ST;
         tc::mbar_wait(&full[s], (c / ST) & 1);
@@ -189,10 +227,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
         const uint32_t aH = tc::smem_u32(smem + s * STAGE);
         const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
 #pragma unroll
-        for (int ks = 0; ks < TC_BK / 8; ++ks) {  // K = 8 tf32 (32 bytes) per MMA
-          const uint32_t off = ks * 32;
-          const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
-          const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+        for (int ks = 0; ks < TC_BK / 8; ++ks) {  // K = 8 tf32 per MMA
+          const uint64_t dah = tile_desc<AMN, TC_BM>(aH, ks), dal = tile_desc<AMN, TC_BM>(aL, ks);
+          const uint64_t dbh = tile_desc<BMN, NMMA>(bH, ks), dbl = tile_desc<BMN, NMMA>(bL, ks);
           tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
           tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
           tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
@@ -228,7 +265,7 @@ __device__ __forceinline__ float scal(const float *amp, const float *att, int m,
 
 // ---------------------------------------------------------------- G1 update
 struct TcUpdate {
-  static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 3;
+  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2, PF = 3;
   static constexpr bool A_MN = false, B_MN = false;
   const uint8_t *blob; const float *A; const float *amp; const float *att; const float *U; const float *bU;
   float *X1; int H; int N;
@@ -241,13 +278,15 @@ struct TcUpdate {
     ke = 4 * H;
     return m0 < N;
   }
-  __device__ float4 a4(int m, int k, int) const {
+  __device__ float4 a_ld(int m, int k, int) const {
     return m < N ? ldg4(A + (size_t)m * 4 * H + k) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  __device__ float4 b4(int n0, int r, int k, int) const {
+  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
+  __device__ float4 b_ld(int n0, int r, int k, int) const {
     const int s = r / BN, c = r - s * BN;
     return ldg4(U + (size_t)(n0 + c) * 12 * H + s * 4 * H + k);
   }
+  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
   __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
     if (m >= N) return;
     const float a1 = amp[m], a2 = att[m];
@@ -268,7 +307,7 @@ struct TcUpdate {
 // ---------------------------------------------------------------- G2 dA
 // B_s[n, h] = U[h, s*4H + n] read from the transposed copy UT[s][n][h] (prepared per step)
 struct TcDA {
-  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2;
+  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2, PF = 3;
   static constexpr bool A_MN = false, B_MN = false;
   const uint8_t *blob; const float *dZ; const float *amp; const float *att; const float *UT; float *dA; int H; int N;
   __device__ void prepare() { N = batch_N(blob); }
@@ -280,13 +319,15 @@ struct TcDA {
     ke = H;
     return m0 < N;
   }
-  __device__ float4 a4(int m, int k, int) const {
+  __device__ float4 a_ld(int m, int k, int) const {
     return m < N ? ldg4(dZ + (size_t)m * H + k) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  __device__ float4 b4(int n0, int r, int k, int) const {
+  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
+  __device__ float4 b_ld(int n0, int r, int k, int) const {
     const int s = r / BN, c = r - s * BN;
     return ldg4(UT + ((size_t)s * 4 * H + n0 + c) * H + k);
   }
+  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
   __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
     if (m >= N) return;
     const float a1 = amp[m], a2 = att[m];
@@ -308,7 +349,7 @@ struct TcDA {
 // partial[sp][h][s*4H + n] for the fixed-order reduction.
 constexpr int kTcDUSplits = 16;
 struct TcDU {
-  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2;
+  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2, PF = 3;
   static constexpr bool A_MN = true, B_MN = true;
   const uint8_t *blob; const float *dZ; const float *A; const float *amp; const float *att; float *part; int H;
   int N; int sp;
@@ -326,19 +367,20 @@ struct TcDU {
     ke = min(N, kb + kc);
     return true;  // empty splits still write their (zero) partial
   }
-  __device__ float4 a4(int m, int k, int ke) const {
-    float v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = (k + u < ke) ? __ldg(dZ + (size_t)(k + u) * H + m) : 0.f;
-    return make_float4(v[0], v[1], v[2], v[3]);
+  // MN-major operands: one float4 = 4 consecutive rows (h, or B rows) at node k
+  __device__ float4 a_ld(int m, int k, int ke) const {
+    return k < ke ? ldg4(dZ + (size_t)k * H + m) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  __device__ float4 b4(int n0, int r, int k, int ke) const {
+  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
+  __device__ float4 b_ld(int n0, int r, int k, int ke) const {
     const int s = r / BN, c = r - s * BN;
-    float v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      v[u] = (k + u < ke) ? __ldg(A + (size_t)(k + u) * 4 * H + n0 + c) * scal(amp, att, k + u, s) : 0.f;
-    return make_float4(v[0], v[1], v[2], v[3]);
+    return k < ke ? ldg4(A + (size_t)k * 4 * H + n0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  __device__ float4 b_fix(float4 v, int, int r, int k, int ke) const {
+    const int s = r / BN;
+    if (s == 0 || k >= ke) return v;
+    const float f = scal(amp, att, k, s);
+    return make_float4(v.x * f, v.y * f, v.z * f, v.w * f);
   }
   __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
     float *base = part + (size_t)sp * H * 12 * H + (size_t)m * 12 * H;
@@ -351,6 +393,8 @@ struct TcDU {
     }
   }
 };
+
+__global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
 
 __global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
   const int c4 = count / 4;
@@ -426,7 +470,7 @@ void launch_tc_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const flo
   const int count = c.H * 12 * c.H;
   k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDUSplits, count, dU);
   k_colsum_part<<<kColsumChunks, 128, 0, st>>>(blob, dZ, c.H, partial);
-  k_reduce_parts<<<1, 256, 0, st>>>(partial, kColsumChunks, c.H, dbU);
+  k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(partial, kColsumChunks, c.H, dbU);
   g_launches += 3;
 }
 
