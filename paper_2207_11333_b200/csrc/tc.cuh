@@ -128,6 +128,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// 16-byte async global->shared copy (L2 only); src_bytes = 0 zero-fills the destination
+__device__ __forceinline__ void cp_async16(void *dst_smem, const void *src, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst_smem)), "l"(src), "r"(src_bytes)
+               : "memory");
+}
+// arrive on `bar` when all prior cp.async of this thread have completed (counts
+// against the barrier's expected arrivals; the issuing thread does not block)
+__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 // 3xTF32 split: hi keeps the 10 explicit mantissa bits TF32 uses, lo = x - hi (exact)
 __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);

@@ -34,22 +34,26 @@ namespace hg {
 extern std::atomic<int64_t> g_launches;
 
 constexpr int TC_BM = 128;
-constexpr int TC_BK = 32;  // fp32 elements per 128-byte smem row
-constexpr int TC_PROD_WARPS = 8;  // two warpgroups: producers, then the epilogue
-constexpr int TC_THREADS = 32 * (TC_PROD_WARPS + 1);
+constexpr int TC_BK = 32;            // fp32 elements per 128-byte smem row
+constexpr int TC_XF_WARPS = 8;       // transform (+ epilogue) warps
+constexpr int TC_LD_WARPS = 2;       // cp.async loader warps
+constexpr int TC_MMA_WARP = TC_XF_WARPS + TC_LD_WARPS;
+constexpr int TC_THREADS = 32 * (TC_MMA_WARP + 1);
 
 template <int N>
 struct TmemCols {
   static constexpr int v = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
 };
 
+// shared memory: RS raw stages (A raw 16 KB + B raw NMMA*128 B, cp.async targets)
+// and ST operand stages (A hi, A lo, B hi, B lo in K-major SW128 layout)
 template <class Op>
-constexpr int tc_stage_bytes() {
-  return 2 * TC_BM * 128 + 2 * Op::NMMA * 128;
-}
+constexpr int tc_raw_bytes() { return TC_BM * 128 + Op::NMMA * 128; }
+template <class Op>
+constexpr int tc_stage_bytes() { return 2 * TC_BM * 128 + 2 * Op::NMMA * 128; }
 template <class Op>
 constexpr int tc_smem_bytes() {
-  return Op::STAGES * tc_stage_bytes<Op>() + 1024 /*align slack*/ + 8 * (2 * Op::STAGES + 1) + 16;
+  return Op::STAGES * tc_stage_bytes<Op>() + Op::RAW * tc_raw_bytes<Op>() + 1024 + 8 * (2 * Op::STAGES + 2 * Op::RAW + 1) + 16;
 }
 
 __device__ __forceinline__ float4 split_hi(float4 v, float4 &lo) {
@@ -61,23 +65,37 @@ __device__ __forceinline__ float4 split_hi(float4 v, float4 &lo) {
   return hi;
 }
 
-// operand tile geometry inside one K-chunk stage (ROWS x 32 k):
-//   K-major  : task -> (row r = task/8, 16-byte k-chunk j = task%8); load 4 k's of row r
-//   MN-major : task -> (k-row kr = task/(ROWS/4), 4-row group g = task%(ROWS/4)); load 4 rows at k
+// raw staging layouts: K-major source -> raw[row][32 k] (128-byte rows);
+// MN-major source -> raw[k][ROWS] (rows contiguous along MN).
 template <bool MN, int ROWS>
-__device__ __forceinline__ void task_coords(int task, int &r, int &kk) {
-  if (MN) { kk = task / (ROWS / 4); r = (task % (ROWS / 4)) * 4; }
-  else { r = task >> 3; kk = (task & 7) * 4; }
+__device__ __forceinline__ void load_piece(int p, int &r, int &k, uint32_t &raw_off) {
+  if (MN) {  // piece = 4 consecutive rows at one k
+    k = p / (ROWS / 4);
+    r = (p % (ROWS / 4)) * 4;
+    raw_off = (uint32_t)(k * ROWS * 4 + r * 4);
+  } else {   // piece = 4 consecutive k of one row
+    r = p >> 3;
+    k = (p & 7) * 4;
+    raw_off = (uint32_t)(r * 128 + k * 4);
+  }
 }
+
+// transform one 16-byte K-major chunk (row r, k-chunk j) from the raw stage
 template <bool MN, int ROWS>
-__device__ __forceinline__ uint32_t tile_off(int r, int kk) {
-  if (MN) return tc::sw128_mn_off((r >> 5), (r >> 2) & 7, kk, ROWS / 32);
-  return tc::sw128_off(r, kk >> 2);
+__device__ __forceinline__ float4 read_raw(const uint8_t *raw, int r, int j) {
+  if (MN) {
+    const float *f = reinterpret_cast<const float *>(raw);
+    return make_float4(f[(4 * j + 0) * ROWS + r], f[(4 * j + 1) * ROWS + r], f[(4 * j + 2) * ROWS + r],
+                       f[(4 * j + 3) * ROWS + r]);
+  }
+  return *reinterpret_cast<const float4 *>(raw + r * 128 + j * 16);
 }
+// task -> (row, k-chunk): lanes over rows for MN sources (conflict-free column reads),
+// over k-chunks for K sources (contiguous 128-byte rows)
 template <bool MN, int ROWS>
-__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int ks) {
-  if (MN) return tc::desc_sw128_mn(base + ks * (ROWS / 32) * 1024, 1024, (ROWS / 32) * 1024);
-  return tc::desc_sw128(base + ks * 32);
+__device__ __forceinline__ void xf_coords(int task, int &r, int &j) {
+  if (MN) { r = task % ROWS; j = task / ROWS; }
+  else { r = task >> 3; j = task & 7; }
 }
 
 template <class Op>
@@ -87,30 +105,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   int m0, n0, kb, ke;
   if (!op.tile(blockIdx.x, m0, n0, kb, ke)) return;  // uniform: tile beyond the device-side size
 
-  constexpr int NMMA = Op::NMMA, ST = Op::STAGES, NACC = Op::NACC, BN = Op::BN, PF = Op::PF;
+  constexpr int NMMA = Op::NMMA, ST = Op::STAGES, RS = Op::RAW, NACC = Op::NACC, BN = Op::BN;
   constexpr bool AMN = Op::A_MN, BMN = Op::B_MN;
   constexpr int A_BYTES = TC_BM * 128, B_BYTES = NMMA * 128;
-  constexpr int STAGE = tc_stage_bytes<Op>();
+  constexpr int STAGE = tc_stage_bytes<Op>(), RAWB = tc_raw_bytes<Op>();
   constexpr int TCOLS = TmemCols<NMMA>::v;
   static_assert(NMMA % 16 == 0 && NMMA <= 256, "MMA N for M=128 must be a multiple of 16 <= 256");
   static_assert(NMMA == NACC * BN && BN % 32 == 0, "accumulator tiling");
-  static_assert(B_BYTES % 1024 == 0 && (!BMN || NMMA % 32 == 0), "SW128 tiles need 1024-byte alignment");
-  static_assert(PF >= 1 && PF <= 4, "prefetch depth");
+  static_assert(B_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE);
+  uint8_t *raw0 = smem + ST * STAGE;
+  uint64_t *full = reinterpret_cast<uint64_t *>(raw0 + RS * RAWB);
   uint64_t *empty = full + ST;
-  uint64_t *accf = empty + ST;
+  uint64_t *rfull = empty + ST;
+  uint64_t *rempty = rfull + RS;
+  uint64_t *accf = rempty + RS;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(accf + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NPROD = TC_PROD_WARPS * 32;
-  if (warp == TC_PROD_WARPS) tc::tmem_alloc<TCOLS>(tmem_holder);
+  constexpr int NXF = TC_XF_WARPS * 32, NLD = TC_LD_WARPS * 32;
+  if (warp == TC_MMA_WARP) tc::tmem_alloc<TCOLS>(tmem_holder);
   if (threadIdx.x == 0) {
     for (int s = 0; s < ST; ++s) {
-      tc::mbar_init(&full[s], NPROD);
+      tc::mbar_init(&full[s], NXF);
       tc::mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < RS; ++s) {
+      tc::mbar_init(&rfull[s], NLD);
+      tc::mbar_init(&rempty[s], NXF);
     }
     tc::mbar_init(accf, 1);
     tc::fence_mbar_init();
@@ -121,82 +145,71 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   const uint32_t tmem = *tmem_holder;
   const int nchunks = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;
 
-  if (warp < TC_PROD_WARPS) {
-    const int t = threadIdx.x;
-    // PF-deep register ring: raw global loads of chunk c+PF-1 are issued before
-    // chunk c is transformed (operand fix-up, 3xTF32 split) and stored, so PF-1
-    // chunks of loads are always in flight behind the tensor core.
-    constexpr int NA = TC_BM * 8 / NPROD, NB = (NMMA * 8 + NPROD - 1) / NPROD;
-    float4 ra[PF][NA], rb[PF][NB];
-    auto issue = [&](int c, float4 (&xa)[NA], float4 (&xb)[NB]) {
+  if (warp >= TC_XF_WARPS && warp < TC_MMA_WARP) {
+    // ---------------- loaders: cp.async raw fp32 tiles, completion -> rfull[rs]
+    const int t = threadIdx.x - NXF;
+    const float *dummy = op.any_src();
+    for (int c = 0; c < nchunks; ++c) {
+      const int rs = c % RS;
+      if (c >= RS) tc::mbar_wait(&rempty[rs], ((c / RS) - 1) & 1);
+      uint8_t *rA = raw0 + rs * RAWB;
+      uint8_t *rB = rA + A_BYTES;
       const int k0 = kb + c * TC_BK;
-#pragma unroll
-      for (int i = 0; i < NA; ++i) {
-        int r, kk;
-        task_coords<AMN, TC_BM>(t + i * NPROD, r, kk);
-        xa[i] = op.a_ld(m0 + r, k0 + kk, ke);
+      for (int p = t; p < TC_BM * 8; p += NLD) {
+        int r, k;
+        uint32_t off;
+        load_piece<AMN, TC_BM>(p, r, k, off);
+        const float *src = op.a_src(m0 + r, k0 + k, ke);
+        tc::cp_async16(rA + off, src ? src : dummy, src ? 16u : 0u);
       }
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const int task = t + i * NPROD;
-        if (task < NMMA * 8) {
-          int r, kk;
-          task_coords<BMN, NMMA>(task, r, kk);
-          xb[i] = op.b_ld(n0, r, k0 + kk, ke);
-        }
+      for (int p = t; p < NMMA * 8; p += NLD) {
+        int r, k;
+        uint32_t off;
+        load_piece<BMN, NMMA>(p, r, k, off);
+        const float *src = op.b_src(n0, r, k0 + k, ke);
+        tc::cp_async16(rB + off, src ? src : dummy, src ? 16u : 0u);
       }
-    };
-    auto commit = [&](int c, const float4 (&xa)[NA], const float4 (&xb)[NB]) {
-      const int s = c % ST;
+      tc::cp_async_arrive(&rfull[rs]);
+    }
+  } else if (warp < TC_XF_WARPS) {
+    // ---------------- transform: raw -> (fix-up) -> 3xTF32 hi/lo K-major SW128 tiles
+    const int t = threadIdx.x;
+    for (int c = 0; c < nchunks; ++c) {
+      const int rs = c % RS, s = c % ST;
+      tc::mbar_wait(&rfull[rs], (c / RS) & 1);
       if (c >= ST) tc::mbar_wait(&empty[s], ((c / ST) - 1) & 1);
+      const uint8_t *rA = raw0 + rs * RAWB;
+      const uint8_t *rB = rA + A_BYTES;
       uint8_t *sAh = smem + s * STAGE;
       uint8_t *sAl = sAh + A_BYTES;
       uint8_t *sBh = sAl + A_BYTES;
       uint8_t *sBl = sBh + B_BYTES;
       const int k0 = kb + c * TC_BK;
-#pragma unroll
-      for (int i = 0; i < NA; ++i) {
-        int r, kk;
-        task_coords<AMN, TC_BM>(t + i * NPROD, r, kk);
+#pragma unroll 4
+      for (int task = t; task < TC_BM * 8; task += NXF) {
+        int r, j;
+        xf_coords<AMN, TC_BM>(task, r, j);
         float4 lo;
-        const float4 hi = split_hi(op.a_fix(xa[i], m0 + r, k0 + kk, ke), lo);
-        const uint32_t o = tile_off<AMN, TC_BM>(r, kk);
+        const float4 hi = split_hi(op.a_fix(read_raw<AMN, TC_BM>(rA, r, j), m0 + r, k0 + 4 * j, ke), lo);
+        const uint32_t o = tc::sw128_off(r, j);
         *reinterpret_cast<float4 *>(sAh + o) = hi;
         *reinterpret_cast<float4 *>(sAl + o) = lo;
       }
-#pragma unroll
-      for (int i = 0; i < NB; ++i) {
-        const int task = t + i * NPROD;
-        if (task < NMMA * 8) {
-          int r, kk;
-          task_coords<BMN, NMMA>(task, r, kk);
-          float4 lo;
-          const float4 hi = split_hi(op.b_fix(xb[i], n0, r, k0 + kk, ke), lo);
-          const uint32_t o = tile_off<BMN, NMMA>(r, kk);
-          *reinterpret_cast<float4 *>(sBh + o) = hi;
-          *reinterpret_cast<float4 *>(sBl + o) = lo;
-        }
+#pragma unroll 4
+      for (int task = t; task < NMMA * 8; task += NXF) {
+        int r, j;
+        xf_coords<BMN, NMMA>(task, r, j);
+        float4 lo;
+        const float4 hi = split_hi(op.b_fix(read_raw<BMN, NMMA>(rB, r, j), n0, r, k0 + 4 * j, ke), lo);
+        const uint32_t o = tc::sw128_off(r, j);
+        *reinterpret_cast<float4 *>(sBh + o) = hi;
+        *reinterpret_cast<float4 *>(sBl + o) = lo;
       }
-      tc::fence_proxy_async_smem();
+      tc::mbar_arrive(&rempty[rs]);     // raw stage may be refilled
+      tc::fence_proxy_async_smem();     // operand tiles -> visible to the tensor core
       tc::mbar_arrive(&full[s]);
-    };
-#pragma unroll
-    for (int p = 0; p < PF - 1; ++p)
-      if (p < nchunks) issue(p, ra[p], rb[p]);
-    for (int c0 = 0; c0 < nchunks; c0 += PF) {
-#pragma unroll
-      for (int p = 0; p < PF; ++p) {
-        const int c = c0 + p;
-        if (c < nchunks) {
-          constexpr int dummy = 0;
-          (void)dummy;
-          const int q = (p + PF - 1) % PF;  // ring slot freed by chunk c-1
-          if (c + PF - 1 < nchunks) issue(c + PF - 1, ra[q], rb[q]);
-          commit(c, ra[p], rb[p]);
-        }
-      }
     }
-    // ---- epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one accumulator row per
+    // ---------------- epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one row per
     // thread); the two warpgroups split the 32-column chunks of each accumulator
     tc::mbar_wait(accf, 0);
     tc::fence_after_sync();
@@ -204,7 +217,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
     const int row = wq * 32 + lane;
     const uint32_t trow = tmem + ((uint32_t)(wq * 32) << 16);
 #pragma unroll 1
-    for (int q = wg; q < BN / 32; q += TC_PROD_WARPS / 4) {
+    for (int q = wg; q < BN / 32; q += TC_XF_WARPS / 4) {
       float acc[NACC][32];
 #pragma unroll
       for (int a = 0; a < NACC; ++a) {
@@ -217,9 +230,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
       }
       op.store(m0 + row, n0, q * 32, acc);
     }
-  } else if (warp == TC_PROD_WARPS) {
+  } else {
+    // ---------------- MMA issuer (one thread)
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_tf32(TC_BM, NMMA, AMN, BMN);
+      constexpr uint32_t idesc = tc::idesc_tf32(TC_BM, NMMA);
       for (int c = 0; c < nchunks; ++c) {
         const int s = c % ST;
         tc::mbar_wait(&full[s], (c / ST) & 1);
@@ -227,9 +241,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
         const uint32_t aH = tc::smem_u32(smem + s * STAGE);
         const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
 #pragma unroll
-        for (int ks = 0; ks < TC_BK / 8; ++ks) {  // K = 8 tf32 per MMA
-          const uint64_t dah = tile_desc<AMN, TC_BM>(aH, ks), dal = tile_desc<AMN, TC_BM>(aL, ks);
-          const uint64_t dbh = tile_desc<BMN, NMMA>(bH, ks), dbl = tile_desc<BMN, NMMA>(bL, ks);
+        for (int ks = 0; ks < TC_BK / 8; ++ks) {  // K = 8 tf32 (32 bytes) per MMA
+          const uint32_t off = ks * 32;
+          const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
+          const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
           tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
           tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
           tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
@@ -242,7 +257,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == TC_PROD_WARPS) {
+  if (warp == TC_MMA_WARP) {
     tc::fence_after_sync();
     tc::tmem_dealloc<TCOLS>(tmem);
   }
@@ -265,7 +280,7 @@ __device__ __forceinline__ float scal(const float *amp, const float *att, int m,
 
 // ---------------------------------------------------------------- G1 update
 struct TcUpdate {
-  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2, PF = 3;
+  static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 2, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
   const uint8_t *blob; const float *A; const float *amp; const float *att; const float *U; const float *bU;
   float *X1; int H; int N;
@@ -278,13 +293,12 @@ struct TcUpdate {
     ke = 4 * H;
     return m0 < N;
   }
-  __device__ float4 a_ld(int m, int k, int) const {
-    return m < N ? ldg4(A + (size_t)m * 4 * H + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  __device__ const float *any_src() const { return U; }
+  __device__ const float *a_src(int m, int k, int) const { return m < N ? A + (size_t)m * 4 * H + k : nullptr; }
   __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
-  __device__ float4 b_ld(int n0, int r, int k, int) const {
+  __device__ const float *b_src(int n0, int r, int k, int) const {
     const int s = r / BN, c = r - s * BN;
-    return ldg4(U + (size_t)(n0 + c) * 12 * H + s * 4 * H + k);
+    return U + (size_t)(n0 + c) * 12 * H + s * 4 * H + k;
   }
   __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
   __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
@@ -307,7 +321,7 @@ struct TcUpdate {
 // ---------------------------------------------------------------- G2 dA
 // B_s[n, h] = U[h, s*4H + n] read from the transposed copy UT[s][n][h] (prepared per step)
 struct TcDA {
-  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2, PF = 3;
+  static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 2, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
   const uint8_t *blob; const float *dZ; const float *amp; const float *att; const float *UT; float *dA; int H; int N;
   __device__ void prepare() { N = batch_N(blob); }
@@ -319,13 +333,12 @@ struct TcDA {
     ke = H;
     return m0 < N;
   }
-  __device__ float4 a_ld(int m, int k, int) const {
-    return m < N ? ldg4(dZ + (size_t)m * H + k) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  __device__ const float *any_src() const { return UT; }
+  __device__ const float *a_src(int m, int k, int) const { return m < N ? dZ + (size_t)m * H + k : nullptr; }
   __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
-  __device__ float4 b_ld(int n0, int r, int k, int) const {
+  __device__ const float *b_src(int n0, int r, int k, int) const {
     const int s = r / BN, c = r - s * BN;
-    return ldg4(UT + ((size_t)s * 4 * H + n0 + c) * H + k);
+    return UT + ((size_t)s * 4 * H + n0 + c) * H + k;
   }
   __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
   __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
@@ -349,7 +362,7 @@ struct TcDA {
 // partial[sp][h][s*4H + n] for the fixed-order reduction.
 constexpr int kTcDUSplits = 16;
 struct TcDU {
-  static constexpr int BN = 64, NACC = 3, NMMA = 192, STAGES = 2, PF = 3;
+  static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 2, RAW = 3;
   static constexpr bool A_MN = true, B_MN = true;
   const uint8_t *blob; const float *dZ; const float *A; const float *amp; const float *att; float *part; int H;
   int N; int sp;
@@ -367,20 +380,22 @@ struct TcDU {
     ke = min(N, kb + kc);
     return true;  // empty splits still write their (zero) partial
   }
-  // MN-major operands: one float4 = 4 consecutive rows (h, or B rows) at node k
-  __device__ float4 a_ld(int m, int k, int ke) const {
-    return k < ke ? ldg4(dZ + (size_t)k * H + m) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
+  // MN-major sources: a 16-byte piece = 4 consecutive rows (h, or B rows) at node k;
+  // the transform stage transposes them into K-major operand tiles
+  __device__ const float *any_src() const { return dZ; }
+  __device__ const float *a_src(int m, int k, int ke) const { return k < ke ? dZ + (size_t)k * H + m : nullptr; }
   __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
-  __device__ float4 b_ld(int n0, int r, int k, int ke) const {
+  __device__ const float *b_src(int n0, int r, int k, int ke) const {
     const int s = r / BN, c = r - s * BN;
-    return k < ke ? ldg4(A + (size_t)k * 4 * H + n0 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return k < ke ? A + (size_t)k * 4 * H + n0 + c : nullptr;
   }
+  // the transformed chunk holds 4 consecutive k (nodes) of B row r: scale each by s_k
   __device__ float4 b_fix(float4 v, int, int r, int k, int ke) const {
     const int s = r / BN;
-    if (s == 0 || k >= ke) return v;
-    const float f = scal(amp, att, k, s);
-    return make_float4(v.x * f, v.y * f, v.z * f, v.w * f);
+    if (s == 0) return v;
+    const float *sc = s == 1 ? amp : att;
+    return make_float4(k + 0 < ke ? v.x * sc[k + 0] : 0.f, k + 1 < ke ? v.y * sc[k + 1] : 0.f,
+                       k + 2 < ke ? v.z * sc[k + 2] : 0.f, k + 3 < ke ? v.w * sc[k + 3] : 0.f);
   }
   __device__ void store(int m, int n0, int q0, const float (&acc)[3][32]) const {
     float *base = part + (size_t)sp * H * 12 * H + (size_t)m * 12 * H;
