@@ -114,8 +114,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   static_assert(NMMA == NACC * BN && BN % 32 == 0, "accumulator tiling");
   static_assert(B_BYTES % 1024 == 0, "SW128 tiles need 1024-byte alignment");
 
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // align within the shared window by indexing smem_raw (keeps the pointer in the
+  // shared state space, so the compiler emits LDS/STS rather than generic LD/ST)
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t *raw0 = smem + ST * STAGE;
   uint64_t *full = reinterpret_cast<uint64_t *>(raw0 + RS * RAWB);
   uint64_t *empty = full + ST;
