@@ -73,7 +73,8 @@ Plan make_plan(const hg_config &c) {
   Caps caps{c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge, c.hidden, c.fc_hidden};
   size_t pf = std::max({agg_bwd_partial_floats(caps), dU_partial_floats(caps), dMx_partial_floats(caps, c.f_node),
                         dMx_partial_floats(caps, c.hidden)});
-  if (tc_supported(caps)) pf = std::max(pf, tc_dU_partial_floats(caps));
+  if (tc_supported(caps))
+    pf = std::max({pf, tc_dU_partial_floats(caps), tc_dMx_partial_floats(caps, c.hidden)});
   p.part = take(sizeof(float) * pf);
   p.UT = take(sizeof(float) * (size_t)c.layers * 12 * H * H);
   p.u_off = take(sizeof(int64_t) * (size_t)c.layers);
@@ -199,7 +200,12 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) {
   for (int l = 0; l < c.layers; ++l) {
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
-    phase(pr, HG_PHASE_PROJ, [&] { launch_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l])); });
+    phase(pr, HG_PHASE_PROJ, [&] {
+      if (x->use_tc && l > 0 && tc_proj_ok(x->caps, F))
+        launch_tc_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
+      else
+        launch_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
+    });
     phase(pr, HG_PHASE_AGG_FWD, [&] {
       launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
                      c.var_floor, x->f(p.A[l]), x->b(p.arg[l]));
@@ -258,11 +264,20 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) 
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
     phase(pr, HG_PHASE_DMX, [&] {
-      launch_dMx(st, x->caps, blob, x->f(p.dP), Xl, F, x->f(p.part), x->grad(lname(l, "M_x")),
-                 x->grad(lname(l, "b_M")));
+      if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
+        launch_tc_dMx(st, x->caps, blob, x->f(p.dP), Xl, F, x->f(p.part), x->grad(lname(l, "M_x")),
+                      x->grad(lname(l, "b_M")));
+      else
+        launch_dMx(st, x->caps, blob, x->f(p.dP), Xl, F, x->f(p.part), x->grad(lname(l, "M_x")),
+                   x->grad(lname(l, "b_M")));
     });
     if (l > 0) {
-      phase(pr, HG_PHASE_DX, [&] { launch_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn); });
+      phase(pr, HG_PHASE_DX, [&] {
+        if (x->use_tc && F % 64 == 0)
+          launch_tc_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn);
+        else
+          launch_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn);
+      });
       std::swap(dZ, dZn);
     }
   }

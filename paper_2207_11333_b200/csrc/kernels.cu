@@ -320,8 +320,10 @@ void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float 
 // 32*CPL-channel chunk (blockIdx.y). Messages m = P[j] + b_M + M_e e_ji are
 // recomputed, never stored. First pass: sum, min, max with
 // first-position argmin/argmax; second pass: centred sum of squares (two-pass
-// variance). d = 0 -> all aggregates 0 (C5).
-constexpr int kFeMax = 8;
+// variance) over messages kept in registers for the first KREG
+// edges (molecules: degree <= 4). d = 0 -> all aggregates 0 (C5).
+// FE: compile-time edge-feature width (4 for the molecular encoding; 8 = generic <= 8).
+constexpr int kKReg = 4;
 
 template <int CPL>
 __device__ __forceinline__ void load_vec(const float *p, float (&v)[CPL]) {
@@ -343,53 +345,66 @@ __device__ __forceinline__ void store_vec(float *p, const float (&v)[CPL]) {
   }
 }
 
+template <int FE>
+__device__ __forceinline__ void load_edge(const float *ea, int Fe, int k, float (&ef)[FE]) {
+  if constexpr (FE == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4 *>(ea + (size_t)k * 4));
+    ef[0] = t.x; ef[1] = t.y; ef[2] = t.z; ef[3] = t.w;
+  } else {
+#pragma unroll
+    for (int f = 0; f < FE; ++f) ef[f] = f < Fe ? __ldg(ea + (size_t)k * Fe + f) : 0.f;
+  }
+}
+
 // message for CPL channels: m = (P + b_M) + sum_f M_e[:,f] e_f  (same order in K2 and K8)
-template <int CPL>
-__device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm)[CPL],
-                                        const float (&me)[CPL][kFeMax], const float (&ef)[kFeMax], int Fe,
-                                        float (&m)[CPL]) {
+template <int CPL, int FE>
+__device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm)[CPL], const float (&me)[CPL][FE],
+                                        const float (&ef)[FE], float (&m)[CPL]) {
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     float v = pj[c] + bm[c];
 #pragma unroll
-    for (int f = 0; f < kFeMax; ++f)
-      if (f < Fe) v = fmaf(me[c][f], ef[f], v);
+    for (int f = 0; f < FE; ++f) v = fmaf(me[c][f], ef[f], v);
     m[c] = v;
   }
 }
 
-template <int CPL>
-__global__ void __launch_bounds__(256) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
-                                                 const float *__restrict__ Me, const float *__restrict__ bM,
-                                                 float var_floor, float *__restrict__ A, uint8_t *__restrict__ arg,
-                                                 int H) {
+template <int CPL, int FE>
+__global__ void __launch_bounds__(256, 3) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
+                                                    const float *__restrict__ Me, const float *__restrict__ bM,
+                                                    float var_floor, float *__restrict__ A,
+                                                    uint8_t *__restrict__ arg, int H) {
   const BatchView b = load_batch(blob);
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   const int ch = blockIdx.y * 32 * CPL + lane * CPL;
   const int Fe = b.Fe;
-  float me[CPL][kFeMax], bm[CPL];
+  float me[CPL][FE], bm[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     bm[c] = bM[ch + c];
 #pragma unroll
-    for (int f = 0; f < kFeMax; ++f) me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f;
+    for (int f = 0; f < FE; ++f) me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f;
   }
   for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < b.N; i += gridDim.x * wpb) {
     const int k0 = b.rowptr[i], k1 = b.rowptr[i + 1], d = k1 - k0;
-    float s[CPL], mx[CPL], mn[CPL];
+    float s[CPL], mx[CPL], mn[CPL], mr[kKReg][CPL];
     int amx[CPL], amn[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) { s[c] = 0.f; mx[c] = -INFINITY; mn[c] = INFINITY; amx[c] = 0; amn[c] = 0; }
     for (int k = k0; k < k1; ++k) {
       const int j = b.col[k];
-      float ef[kFeMax];
-#pragma unroll
-      for (int f = 0; f < kFeMax; ++f) ef[f] = f < Fe ? __ldg(b.ea + (size_t)k * Fe + f) : 0.f;
-      float pj[CPL], m[CPL];
+      float ef[FE], pj[CPL], m[CPL];
+      load_edge<FE>(b.ea, Fe, k, ef);
       load_vec<CPL>(P + (size_t)j * H + ch, pj);
-      message<CPL>(pj, bm, me, ef, Fe, m);
+      message<CPL, FE>(pj, bm, me, ef, m);
       const int p = k - k0;
+#pragma unroll
+      for (int e = 0; e < kKReg; ++e)
+        if (p == e) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) mr[e][c] = m[c];
+        }
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         s[c] += m[c];
@@ -404,19 +419,24 @@ __global__ void __launch_bounds__(256) k_agg_fwd(const uint8_t *__restrict__ blo
       for (int c = 0; c < CPL; ++c) { mean[c] = 0.f; mx[c] = 0.f; mn[c] = 0.f; sd[c] = 0.f; flag[c] = 0; }
     } else {
       const float fd = (float)d;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) mean[c] = s[c] / fd;
       float ss[CPL];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) ss[c] = 0.f;
-      for (int k = k0; k < k1; ++k) {
-        const int j = b.col[k];
-        float ef[kFeMax];
+      for (int c = 0; c < CPL; ++c) { mean[c] = s[c] / fd; ss[c] = 0.f; }
 #pragma unroll
-        for (int f = 0; f < kFeMax; ++f) ef[f] = f < Fe ? __ldg(b.ea + (size_t)k * Fe + f) : 0.f;
-        float pj[CPL], m[CPL];
+      for (int e = 0; e < kKReg; ++e)
+        if (e < d) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            const float t = mr[e][c] - mean[c];
+            ss[c] = fmaf(t, t, ss[c]);
+          }
+        }
+      for (int k = k0 + kKReg; k < k1; ++k) {  // high-degree tail: recompute
+        const int j = b.col[k];
+        float ef[FE], pj[CPL], m[CPL];
+        load_edge<FE>(b.ea, Fe, k, ef);
         load_vec<CPL>(P + (size_t)j * H + ch, pj);
-        message<CPL>(pj, bm, me, ef, Fe, m);
+        message<CPL, FE>(pj, bm, me, ef, m);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
           const float t = m[c] - mean[c];
@@ -452,12 +472,20 @@ __global__ void __launch_bounds__(256) k_agg_fwd(const uint8_t *__restrict__ blo
 
 static int agg_cpl(int H) { return (H % 128 == 0) ? 4 : 1; }
 
+template <int CPL, int FE>
+static void agg_fwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
+                           const float *bM, float var_floor, float *A, uint8_t *arg) {
+  const dim3 grid(std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 6)), c.H / (32 * CPL));
+  k_agg_fwd<CPL, FE><<<grid, 256, 0, st>>>(blob, P, Me, bM, var_floor, A, arg, c.H);
+}
+
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, float var_floor, float *A, uint8_t *arg) {
   const int cpl = agg_cpl(c.H);
-  const dim3 grid(std::min(cdiv(c.maxN, 8), kSMs * 8), c.H / (32 * cpl));
-  if (cpl == 4) k_agg_fwd<4><<<grid, 256, 0, st>>>(blob, P, Me, bM, var_floor, A, arg, c.H);
-  else k_agg_fwd<1><<<grid, 256, 0, st>>>(blob, P, Me, bM, var_floor, A, arg, c.H);
+  if (cpl == 4 && c.Fe == 4) agg_fwd_launch<4, 4>(st, c, blob, P, Me, bM, var_floor, A, arg);
+  else if (cpl == 4) agg_fwd_launch<4, 8>(st, c, blob, P, Me, bM, var_floor, A, arg);
+  else if (c.Fe == 4) agg_fwd_launch<1, 4>(st, c, blob, P, Me, bM, var_floor, A, arg);
+  else agg_fwd_launch<1, 8>(st, c, blob, P, Me, bM, var_floor, A, arg);
   counted();
 }
 
@@ -467,26 +495,28 @@ void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
 // i.e. where K2 saw message m_{j->i}. Per edge:
 //   dm = dA_mean[i]/d_i + [slot == argmax_i] dA_max[i] + [slot == argmin_i] dA_min[i]
 //        + [var_i > eps] dA_std[i] (m - mu_i)/(d_i sigma_i)
-// dP[j] = sum dm (written once, no atomics); dM_e partials per block reduced in
+// dP[j] = sum dm (written once, no atomics); dM_e per-block partials reduced in
 // fixed order by k_reduce_rows.
-template <int CPL>
-__global__ void __launch_bounds__(256) k_agg_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
-                                                 const float *__restrict__ Me, const float *__restrict__ bM,
-                                                 const float *__restrict__ A, const uint8_t *__restrict__ arg,
-                                                 const float *__restrict__ dA, float *__restrict__ dP,
-                                                 float *__restrict__ partial, int H) {
-  __shared__ float red[8][32][CPL * kFeMax];
+constexpr int kAggBwdWarps = 8;
+
+template <int CPL, int FE>
+__global__ void __launch_bounds__(256, 3) k_agg_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
+                                                    const float *__restrict__ Me, const float *__restrict__ bM,
+                                                    const float *__restrict__ A, const uint8_t *__restrict__ arg,
+                                                    const float *__restrict__ dA, float *__restrict__ dP,
+                                                    float *__restrict__ partial, int H) {
+  __shared__ float red[kAggBwdWarps][32][CPL * FE];
   const BatchView b = load_batch(blob);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
   const int ch = blockIdx.y * 32 * CPL + lane * CPL;
   const int Fe = b.Fe;
-  float me[CPL][kFeMax], bm[CPL], acc[CPL][kFeMax];
+  float me[CPL][FE], bm[CPL], acc[CPL][FE];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     bm[c] = bM[ch + c];
 #pragma unroll
-    for (int f = 0; f < kFeMax; ++f) { me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f; acc[c][f] = 0.f; }
+    for (int f = 0; f < FE; ++f) { me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f; acc[c][f] = 0.f; }
   }
   for (int j = blockIdx.x * wpb + warp; j < b.N; j += gridDim.x * wpb) {
     const int k0 = b.rowptr[j], k1 = b.rowptr[j + 1];
@@ -499,11 +529,10 @@ __global__ void __launch_bounds__(256) k_agg_bwd(const uint8_t *__restrict__ blo
       const int sl = b.slot[k];
       const int di = b.rowptr[i + 1] - b.rowptr[i];
       const float fd = (float)di;
-      float ef[kFeMax];
-#pragma unroll
-      for (int f = 0; f < kFeMax; ++f) ef[f] = f < Fe ? __ldg(b.ea + (size_t)k * Fe + f) : 0.f;
+      float ef[FE];
+      load_edge<FE>(b.ea, Fe, k, ef);
       float m[CPL];
-      message<CPL>(pj, bm, me, ef, Fe, m);
+      message<CPL, FE>(pj, bm, me, ef, m);
       const float *dAi = dA + (size_t)i * 4 * H + ch;
       const float *Ai = A + (size_t)i * 4 * H + ch;
       float gmean[CPL], gmin[CPL], gmax[CPL], gstd[CPL], mu[CPL], sg[CPL];
@@ -532,8 +561,7 @@ __global__ void __launch_bounds__(256) k_agg_bwd(const uint8_t *__restrict__ blo
         if (amx[c] & 0x80) g += gstd[c] * (m[c] - mu[c]) / (fd * sg[c]);
         dp[c] += g;
 #pragma unroll
-        for (int f = 0; f < kFeMax; ++f)
-          if (f < Fe) acc[c][f] = fmaf(g, ef[f], acc[c][f]);
+        for (int f = 0; f < FE; ++f) acc[c][f] = fmaf(g, ef[f], acc[c][f]);
       }
     }
     store_vec<CPL>(dP + (size_t)j * H + ch, dp);
@@ -542,15 +570,14 @@ __global__ void __launch_bounds__(256) k_agg_bwd(const uint8_t *__restrict__ blo
 #pragma unroll
   for (int c = 0; c < CPL; ++c)
 #pragma unroll
-    for (int f = 0; f < kFeMax; ++f) red[warp][lane][c * kFeMax + f] = acc[c][f];
+    for (int f = 0; f < FE; ++f) red[warp][lane][c * FE + f] = acc[c][f];
   __syncthreads();
-  // thread t -> (lane l, c, f) of this chunk
   const int chunkC = 32 * CPL;
   for (int t = threadIdx.x; t < chunkC * Fe; t += blockDim.x) {
     const int cc = t / Fe, f = t - cc * Fe;   // channel within chunk, feature
     const int l = cc / CPL, c = cc - l * CPL;
     float s = 0.f;
-    for (int w = 0; w < wpb; ++w) s += red[w][l][c * kFeMax + f];
+    for (int w = 0; w < wpb; ++w) s += red[w][l][c * FE + f];
     // partial layout: [block][H][Fe] (M_e layout)
     partial[(size_t)blockIdx.x * H * Fe + (size_t)(blockIdx.y * chunkC + cc) * Fe + f] = s;
   }
@@ -570,20 +597,28 @@ __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int co
   }
 }
 
-static int agg_bwd_blocks(const Caps &c) { return std::min(cdiv(c.maxN, 8), kSMs * 4); }
+static int agg_bwd_blocks(const Caps &c) { return std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 3)); }
 size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * c.Fe; }
+
+template <int CPL, int FE>
+static void agg_bwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
+                           const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
+                           float *partial) {
+  const dim3 grid(agg_bwd_blocks(c), c.H / (32 * CPL));
+  k_agg_bwd<CPL, FE><<<grid, 32 * kAggBwdWarps, 0, st>>>(blob, P, Me, bM, A, arg, dA, dP, partial, c.H);
+}
 
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
                     float *partial, float *dMe) {
   const int cpl = agg_cpl(c.H);
-  const int nb = agg_bwd_blocks(c);
-  const dim3 grid(nb, c.H / (32 * cpl));
-  if (cpl == 4) k_agg_bwd<4><<<grid, 256, 0, st>>>(blob, P, Me, bM, A, arg, dA, dP, partial, c.H);
-  else k_agg_bwd<1><<<grid, 256, 0, st>>>(blob, P, Me, bM, A, arg, dA, dP, partial, c.H);
+  if (cpl == 4 && c.Fe == 4) agg_bwd_launch<4, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
+  else if (cpl == 4) agg_bwd_launch<4, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
+  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
+  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
   counted();
   const int count = c.H * c.Fe;
-  k_reduce_rows<<<std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st>>>(partial, nb, count, dMe);
+  k_reduce_rows<<<std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st>>>(partial, agg_bwd_blocks(c), count, dMe);
   counted();
 }
 
@@ -617,19 +652,37 @@ __global__ void __launch_bounds__(256) k_head_fwd(const uint8_t *__restrict__ bl
     const float ng = (float)(n1 - n0);
     for (int c = threadIdx.x; c < H; c += blockDim.x) {
       float s = 0.f;
-      for (int i = n0; i < n1; ++i) s += XL[(size_t)i * H + c];
+      int i = n0;
+      for (; i + 4 <= n1; i += 4) {  // 4 independent loads in flight
+        const float a0 = XL[(size_t)i * H + c], a1 = XL[(size_t)(i + 1) * H + c];
+        const float a2 = XL[(size_t)(i + 2) * H + c], a3 = XL[(size_t)(i + 3) * H + c];
+        s += a0;
+        s += a1;
+        s += a2;
+        s += a3;
+      }
+      for (; i < n1; ++i) s += XL[(size_t)i * H + c];
       const float v = s / ng;
       Gs[c] = v;
       G[(size_t)g * H + c] = v;
     }
     __syncthreads();
-    for (int r = threadIdx.x; r < Hf; r += blockDim.x) {
-      float acc = 0.f;
-      const float *w = W1 + (size_t)r * H;
-      for (int c = 0; c < H; ++c) acc = fmaf(w[c], Gs[c], acc);
-      acc += b1[r];
-      hpre[(size_t)g * Hf + r] = acc;
-      hs[r] = fmaxf(acc, 0.f);
+    // hpre[r] = b1[r] + W1[r,:] . G : one warp per output row, lanes over the
+    // (coalesced) row, fixed xor-shuffle reduction order
+    {
+      const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+      for (int r = threadIdx.x >> 5; r < Hf; r += wpb) {
+        const float *w = W1 + (size_t)r * H;
+        float acc = 0.f;
+        for (int c = lane; c < H; c += 32) acc = fmaf(w[c], Gs[c], acc);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+          acc += b1[r];
+          hpre[(size_t)g * Hf + r] = acc;
+          hs[r] = fmaxf(acc, 0.f);
+        }
+      }
     }
     __syncthreads();
     float part = 0.f;

@@ -73,6 +73,15 @@ void launch_tc_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const flo
 void launch_tc_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
                   const float *amp, const float *att, float *partial, float *dU, float *dbU);
 size_t tc_dU_partial_floats(const Caps &c);
+bool tc_proj_ok(const Caps &c, int F);  // X rows 16-byte aligned
+bool tc_dmx_ok(const Caps &c, int F);
+void launch_tc_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
+                    float *P);
+void launch_tc_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
+                  const float *Xl, float *dZprev);
+size_t tc_dMx_partial_floats(const Caps &c, int F);
+void launch_tc_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
+                   float *partial, float *dMx, float *dbM);
 // UT[l][s*4H + n][h] = U_l[h][s*4H + n] for all layers (u_off: device array of U offsets in floats)
 void launch_prep_UT(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L,
                     float *UT);

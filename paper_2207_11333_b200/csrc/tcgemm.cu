@@ -411,6 +411,106 @@ struct TcDU {
   }
 };
 
+// ---------------------------------------------------------------- K1 projection (F % 4 == 0)
+// P[N, H] = X[N, F] M_x^T : A = X rows (K = F), B = M_x rows
+struct TcProj {
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 2, RAW = 3;
+  static constexpr bool A_MN = false, B_MN = false;
+  const uint8_t *blob; const float *X; const float *Mx; float *P; int F, H; int N;
+  __device__ void prepare() { N = batch_N(blob); }
+  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) const {
+    const int nt = H / BN;
+    m0 = (t / nt) * TC_BM;
+    n0 = (t % nt) * BN;
+    kb = 0;
+    ke = F;
+    return m0 < N;
+  }
+  __device__ const float *any_src() const { return Mx; }
+  __device__ const float *a_src(int m, int k, int ke) const {
+    return (m < N && k < ke) ? X + (size_t)m * F + k : nullptr;
+  }
+  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
+  __device__ const float *b_src(int n0, int r, int k, int ke) const {
+    return k < ke ? Mx + (size_t)(n0 + r) * F + k : nullptr;
+  }
+  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[1][32]) const {
+    if (m >= N) return;
+    float *out = P + (size_t)m * H + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[0][i], acc[0][i + 1], acc[0][i + 2], acc[0][i + 3]);
+  }
+};
+
+// ---------------------------------------------------------------- K9b dX (l > 0)
+// dZprev[N, F] = (dP[N, H] M_x[H, F]) * [X_l > 0] : A = dP rows (K = H), B(f, h) = M_x[h, f] (MN source)
+struct TcDX {
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 2, RAW = 3;
+  static constexpr bool A_MN = false, B_MN = true;
+  const uint8_t *blob; const float *dP; const float *Mx; const float *Xl; float *dZ; int H, F; int N;
+  __device__ void prepare() { N = batch_N(blob); }
+  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) const {
+    const int nt = F / BN;
+    m0 = (t / nt) * TC_BM;
+    n0 = (t % nt) * BN;
+    kb = 0;
+    ke = H;
+    return m0 < N;
+  }
+  __device__ const float *any_src() const { return Mx; }
+  __device__ const float *a_src(int m, int k, int) const { return m < N ? dP + (size_t)m * H + k : nullptr; }
+  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
+  __device__ const float *b_src(int n0, int r, int k, int) const { return Mx + (size_t)k * F + n0 + r; }
+  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[1][32]) const {
+    if (m >= N) return;
+    const size_t o = (size_t)m * F + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 x = ldg4(Xl + o + i);
+      *reinterpret_cast<float4 *>(dZ + o + i) =
+          make_float4(x.x > 0.f ? acc[0][i] : 0.f, x.y > 0.f ? acc[0][i + 1] : 0.f, x.z > 0.f ? acc[0][i + 2] : 0.f,
+                      x.w > 0.f ? acc[0][i + 3] : 0.f);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- K9a dM_x (split-K over nodes, F % 64 == 0)
+// dM_x[h, f] = sum_i dP[i, h] X_l[i, f]: A(h, i) = dP[i, h], B(f, i) = X_l[i, f] (both MN sources)
+constexpr int kTcDMxSplits = 16;
+struct TcDMx {
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 2, RAW = 3;
+  static constexpr bool A_MN = true, B_MN = true;
+  const uint8_t *blob; const float *dP; const float *X; float *part; int H, F; int N; int sp;
+  __device__ void prepare() { N = batch_N(blob); }
+  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) {
+    const int nt = F / BN, mt = H / TC_BM;
+    sp = t % kTcDMxSplits;
+    const int t2 = t / kTcDMxSplits;
+    n0 = (t2 % nt) * BN;
+    m0 = (t2 / nt) * TC_BM;
+    if (m0 >= mt * TC_BM) return false;
+    int kc = (N + kTcDMxSplits - 1) / kTcDMxSplits;
+    kc = (kc + TC_BK - 1) / TC_BK * TC_BK;
+    kb = sp * kc;
+    ke = min(N, kb + kc);
+    return true;
+  }
+  __device__ const float *any_src() const { return dP; }
+  __device__ const float *a_src(int m, int k, int ke) const { return k < ke ? dP + (size_t)k * H + m : nullptr; }
+  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
+  __device__ const float *b_src(int n0, int r, int k, int ke) const { return k < ke ? X + (size_t)k * F + n0 + r : nullptr; }
+  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[1][32]) const {
+    float *out = part + (size_t)sp * H * F + (size_t)m * F + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[0][i], acc[0][i + 1], acc[0][i + 2], acc[0][i + 3]);
+  }
+};
+
 __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
 
 __global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
@@ -504,7 +604,40 @@ cudaError_t tc_configure() {
   cudaError_t e;
   if ((e = configure_tc<TcUpdate>()) != cudaSuccess) return e;
   if ((e = configure_tc<TcDA>()) != cudaSuccess) return e;
+  if ((e = configure_tc<TcProj>()) != cudaSuccess) return e;
+  if ((e = configure_tc<TcDX>()) != cudaSuccess) return e;
+  if ((e = configure_tc<TcDMx>()) != cudaSuccess) return e;
   return configure_tc<TcDU>();
+}
+
+bool tc_proj_ok(const Caps &c, int F) { return c.H % 128 == 0 && F % 4 == 0; }
+bool tc_dmx_ok(const Caps &c, int F) { return c.H % 128 == 0 && F % 64 == 0; }
+
+void launch_tc_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
+                    float *P) {
+  TcProj op{blob, X, Mx, P, F, c.H, 0};
+  run_tc(st, op, mtiles(c.maxN) * (c.H / TcProj::BN));
+}
+
+void launch_tc_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
+                  const float *Xl, float *dZprev) {
+  TcDX op{blob, dP, Mx, Xl, dZprev, c.H, F, 0};
+  run_tc(st, op, mtiles(c.maxN) * (F / TcDX::BN));
+}
+
+size_t tc_dMx_partial_floats(const Caps &c, int F) {
+  return std::max((size_t)kTcDMxSplits * c.H * F, (size_t)kColsumChunks * c.H);
+}
+
+void launch_tc_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
+                   float *partial, float *dMx, float *dbM) {
+  TcDMx op{blob, dP, X, partial, c.H, F, 0, 0};
+  run_tc(st, op, (c.H / TC_BM) * (F / TcDMx::BN) * kTcDMxSplits);
+  const int count = c.H * F;
+  k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDMxSplits, count, dMx);
+  k_colsum_part<<<kColsumChunks, 128, 0, st>>>(blob, dP, c.H, partial);
+  k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(partial, kColsumChunks, c.H, dbM);
+  g_launches += 3;
 }
 
 }  // namespace hg
