@@ -191,7 +191,7 @@ void phase(Prof *pr, int ph, F &&fn) {
 }
 
 // ---- the step's kernel sequence (enqueue only) ----
-void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) {
+void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool fuse_head_bwd = false) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
@@ -220,13 +220,18 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) {
     });
   }
   phase(pr, HG_PHASE_HEAD_FWD, [&] {
-    launch_head_fwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
-                    x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat), x->f(p.sqerr),
-                    x->f(p.loss));
+    if (fuse_head_bwd)
+      launch_head_fused(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
+                        x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
+                        x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZa));
+    else
+      launch_head_fwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
+                      x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
+                      x->f(p.sqerr), x->f(p.loss));
   });
 }
 
-void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) {
+void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
@@ -235,7 +240,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr) 
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
     launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"), x->f(p.G),
                     x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
-                    x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
+                    x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), head_done);
   });
   if (x->use_tc)
     phase(pr, HG_PHASE_DA, [&] {
@@ -361,6 +366,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   }
   if ((e = cudaMemsetAsync(workspace, 0, plan.total, x->stream)) != cudaSuccess) return bail(e, "cudaMemsetAsync");
   x->use_tc = tc_supported(x->caps) && !(c->flags & HG_FLAG_SIMT_GEMM);
+  head_configure(x->caps);
   if (x->use_tc && (e = tc_configure()) != cudaSuccess) return bail(e, "tc_configure");
   {
     std::vector<int64_t> uo;
@@ -634,8 +640,8 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   cudaGraph_t g = nullptr;
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
-  enqueue_forward(x, x->cap_stream, slot);
-  enqueue_backward(x, x->cap_stream, slot);
+  enqueue_forward(x, x->cap_stream, slot, nullptr, true);
+  enqueue_backward(x, x->cap_stream, slot, nullptr, true);
   hg_status ar = enqueue_allreduce(x, x->cap_stream);
   enqueue_step(x, x->cap_stream, *h);
   const int64_t nk = launches_so_far() - l0;
@@ -662,8 +668,8 @@ hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms,
   CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
   Prof pr(x->stream);
   const int64_t l0 = launches_so_far();
-  enqueue_forward(x, x->stream, slot, &pr);
-  enqueue_backward(x, x->stream, slot, &pr);
+  enqueue_forward(x, x->stream, slot, &pr, true);
+  enqueue_backward(x, x->stream, slot, &pr, true);
   hg_status ar = HG_OK;
   phase(&pr, HG_PHASE_ALLREDUCE, [&] { ar = enqueue_allreduce(x, x->stream); });
   if (ar) return ar;

@@ -638,41 +638,57 @@ __device__ __forceinline__ float block_sum_256(float v, float *red) {
   return r;
 }
 
-__global__ void __launch_bounds__(256) k_head_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ XL,
-                                                  const float *__restrict__ W1, const float *__restrict__ b1,
-                                                  const float *__restrict__ W2, const float *__restrict__ b2,
-                                                  float *__restrict__ G, float *__restrict__ hpre,
-                                                  float *__restrict__ yhat, float *__restrict__ sqerr, int H,
-                                                  int Hf) {
+// Head kernel, block per graph (grid-stride), W1 staged in shared memory when it
+// fits. FWD: G_g = mean of X_L rows, hpre = W1 G + b1,
+// yhat = W2 ReLU(hpre) + b2, sqerr = (yhat - y)^2.
+// BWD: dy = 2(yhat - y)/B, dhid = dy W2 * [hpre > 0],
+// dG = W1^T dhid, dZ_L[i] = dG / n_g * [X_L[i] > 0].
+// FWD && BWD fuses both when a training step runs them back to back.
+template <bool FWD, bool BWD>
+__global__ void __launch_bounds__(256) k_head(const uint8_t *__restrict__ blob, const float *__restrict__ XL,
+                                              const float *__restrict__ W1, const float *__restrict__ b1,
+                                              const float *__restrict__ W2, const float *__restrict__ b2,
+                                              float *__restrict__ G, float *__restrict__ hpre,
+                                              float *__restrict__ yhat, float *__restrict__ sqerr,
+                                              float *__restrict__ dy, float *__restrict__ dhid,
+                                              float *__restrict__ dZL, int H, int Hf, int w1_in_smem) {
   extern __shared__ float sm[];
-  float *Gs = sm, *hs = sm + H, *red = sm + H + Hf;
+  float *Gs = sm, *hs = Gs + H, *dh = hs + Hf, *red = dh + Hf, *W1s = red + 256;
+  const float *Wr = W1;
+  if (w1_in_smem) {
+    const int n4 = Hf * H / 4;
+    for (int e = threadIdx.x; e < n4; e += blockDim.x)
+      reinterpret_cast<float4 *>(W1s)[e] = __ldg(reinterpret_cast<const float4 *>(W1) + e);
+    Wr = W1s;
+    __syncthreads();
+  }
   const BatchView b = load_batch(blob);
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
   for (int g = blockIdx.x; g < b.B; g += gridDim.x) {
     const int n0 = b.gp[g], n1 = b.gp[g + 1];
     const float ng = (float)(n1 - n0);
-    for (int c = threadIdx.x; c < H; c += blockDim.x) {
-      float s = 0.f;
-      int i = n0;
-      for (; i + 4 <= n1; i += 4) {  // 4 independent loads in flight
-        const float a0 = XL[(size_t)i * H + c], a1 = XL[(size_t)(i + 1) * H + c];
-        const float a2 = XL[(size_t)(i + 2) * H + c], a3 = XL[(size_t)(i + 3) * H + c];
-        s += a0;
-        s += a1;
-        s += a2;
-        s += a3;
+    float yh;
+    if (FWD) {
+      for (int c = threadIdx.x; c < H; c += blockDim.x) {
+        float s = 0.f;
+        int i = n0;
+        for (; i + 4 <= n1; i += 4) {  // 4 independent loads in flight
+          const float a0 = XL[(size_t)i * H + c], a1 = XL[(size_t)(i + 1) * H + c];
+          const float a2 = XL[(size_t)(i + 2) * H + c], a3 = XL[(size_t)(i + 3) * H + c];
+          s += a0;
+          s += a1;
+          s += a2;
+          s += a3;
+        }
+        for (; i < n1; ++i) s += XL[(size_t)i * H + c];
+        const float v = s / ng;
+        Gs[c] = v;
+        G[(size_t)g * H + c] = v;
       }
-      for (; i < n1; ++i) s += XL[(size_t)i * H + c];
-      const float v = s / ng;
-      Gs[c] = v;
-      G[(size_t)g * H + c] = v;
-    }
-    __syncthreads();
-    // hpre[r] = b1[r] + W1[r,:] . G : one warp per output row, lanes over the
-    // (coalesced) row, fixed xor-shuffle reduction order
-    {
-      const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+      __syncthreads();
+      // hpre[r] = b1[r] + W1[r,:] . G : warp per output row, fixed xor-shuffle order
       for (int r = threadIdx.x >> 5; r < Hf; r += wpb) {
-        const float *w = W1 + (size_t)r * H;
+        const float *w = Wr + (size_t)r * H;
         float acc = 0.f;
         for (int c = lane; c < H; c += 32) acc = fmaf(w[c], Gs[c], acc);
 #pragma unroll
@@ -680,18 +696,43 @@ __global__ void __launch_bounds__(256) k_head_fwd(const uint8_t *__restrict__ bl
         if (lane == 0) {
           acc += b1[r];
           hpre[(size_t)g * Hf + r] = acc;
-          hs[r] = fmaxf(acc, 0.f);
+          hs[r] = acc;
         }
       }
+      __syncthreads();
+      float part = 0.f;
+      for (int r = threadIdx.x; r < Hf; r += blockDim.x) part = fmaf(W2[r], fmaxf(hs[r], 0.f), part);
+      yh = block_sum_256(part, red) + b2[0];
+      if (threadIdx.x == 0) {
+        yhat[g] = yh;
+        const float e = yh - b.y[g];
+        sqerr[g] = e * e;
+      }
+    } else {
+      for (int r = threadIdx.x; r < Hf; r += blockDim.x) hs[r] = hpre[(size_t)g * Hf + r];
+      yh = yhat[g];
+      __syncthreads();
     }
-    __syncthreads();
-    float part = 0.f;
-    for (int r = threadIdx.x; r < Hf; r += blockDim.x) part = fmaf(W2[r], hs[r], part);
-    const float yh = block_sum_256(part, red) + b2[0];
-    if (threadIdx.x == 0) {
-      yhat[g] = yh;
-      const float e = yh - b.y[g];
-      sqerr[g] = e * e;
+    if (BWD) {
+      const float d = 2.0f * (yh - b.y[g]) / (float)b.B;
+      if (threadIdx.x == 0) dy[g] = d;
+      for (int r = threadIdx.x; r < Hf; r += blockDim.x) {
+        const float v = hs[r] > 0.f ? d * W2[r] : 0.f;
+        dh[r] = v;
+        dhid[(size_t)g * Hf + r] = v;
+      }
+      __syncthreads();
+      for (int c = threadIdx.x; c < H; c += blockDim.x) {
+        float acc = 0.f;
+        for (int r = 0; r < Hf; ++r) acc = fmaf(Wr[(size_t)r * H + c], dh[r], acc);
+        Gs[c] = acc / ng;
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < (n1 - n0) * H; e += blockDim.x) {
+        const int i = n0 + e / H, c = e % H;
+        const size_t o = (size_t)i * H + c;
+        dZL[o] = XL[o] > 0.f ? Gs[c] : 0.f;
+      }
     }
     __syncthreads();
   }
@@ -707,50 +748,43 @@ __global__ void __launch_bounds__(256) k_loss(const uint8_t *__restrict__ blob, 
   if (threadIdx.x == 0) *loss = s / (float)b.B;
 }
 
+template <bool FWD, bool BWD>
+static void head_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                        const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
+                        float *sqerr, float *dy, float *dhid, float *dZL) {
+  const size_t base = sizeof(float) * (c.H + 2 * c.Hf + 256);
+  const size_t w1 = sizeof(float) * (size_t)c.Hf * c.H;
+  const int in_smem = base + w1 <= 200 * 1024 ? 1 : 0;  // attribute set once by head_configure
+  const size_t smem = base + (in_smem ? w1 : 0);
+  k_head<FWD, BWD><<<std::min(c.maxB, kSMs), 256, smem, st>>>(blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
+                                                               dhid, dZL, c.H, c.Hf, in_smem);
+}
+
+void head_configure(const Caps &c) {  // outside graph capture: opt into large dynamic smem
+  const size_t base = sizeof(float) * (c.H + 2 * c.Hf + 256);
+  const size_t w1 = sizeof(float) * (size_t)c.Hf * c.H;
+  const int v = (int)(base + (base + w1 <= 200 * 1024 ? w1 : 0));
+  cudaFuncSetAttribute(k_head<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+  cudaFuncSetAttribute(k_head<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+  cudaFuncSetAttribute(k_head<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, v);
+}
+
 void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
                      float *sqerr, float *loss) {
-  const size_t smem = sizeof(float) * (c.H + c.Hf + 256);
-  k_head_fwd<<<std::min(c.maxB, kSMs * 4), 256, smem, st>>>(blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, c.H, c.Hf);
+  head_launch<true, false>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, nullptr, nullptr, nullptr);
   counted();
   k_loss<<<1, 256, 0, st>>>(blob, sqerr, loss);
   counted();
 }
 
-// Block per graph: dy = 2(yhat - y)/B, dhid = dy W2 * [hpre > 0],
-// dG = W1^T dhid, dZ_L[i] = dG / n_g * [X_L[i] > 0].
-__global__ void __launch_bounds__(256) k_head_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ XL,
-                                                  const float *__restrict__ W1, const float *__restrict__ W2,
-                                                  const float *__restrict__ hpre, const float *__restrict__ yhat,
-                                                  float *__restrict__ dy, float *__restrict__ dhid,
-                                                  float *__restrict__ dZL, int H, int Hf) {
-  extern __shared__ float sm[];
-  float *dhs = sm, *dGs = sm + Hf;
-  const BatchView b = load_batch(blob);
-  for (int g = blockIdx.x; g < b.B; g += gridDim.x) {
-    const int n0 = b.gp[g], n1 = b.gp[g + 1];
-    const float ng = (float)(n1 - n0);
-    const float d = 2.0f * (yhat[g] - b.y[g]) / (float)b.B;
-    if (threadIdx.x == 0) dy[g] = d;
-    for (int r = threadIdx.x; r < Hf; r += blockDim.x) {
-      const float v = hpre[(size_t)g * Hf + r] > 0.f ? d * W2[r] : 0.f;
-      dhs[r] = v;
-      dhid[(size_t)g * Hf + r] = v;
-    }
-    __syncthreads();
-    for (int c = threadIdx.x; c < H; c += blockDim.x) {
-      float acc = 0.f;
-      for (int r = 0; r < Hf; ++r) acc = fmaf(W1[(size_t)r * H + c], dhs[r], acc);
-      dGs[c] = acc / ng;
-    }
-    __syncthreads();
-    for (int e = threadIdx.x; e < (n1 - n0) * H; e += blockDim.x) {
-      const int i = n0 + e / H, c = e % H;
-      const size_t o = (size_t)i * H + c;
-      dZL[o] = XL[o] > 0.f ? dGs[c] : 0.f;
-    }
-    __syncthreads();
-  }
+void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                       const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
+                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL) {
+  head_launch<true, true>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy, dhid, dZL);
+  counted();
+  k_loss<<<1, 256, 0, st>>>(blob, sqerr, loss);
+  counted();
 }
 
 // head parameter gradients: thread per output element, fixed order over graphs
@@ -784,10 +818,12 @@ __global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__re
 
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
-                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2) {
-  const size_t smem = sizeof(float) * (c.Hf + c.H);
-  k_head_bwd<<<std::min(c.maxB, kSMs * 4), 256, smem, st>>>(blob, XL, W1, W2, hpre, yhat, dy, dhid, dZL, c.H, c.Hf);
-  counted();
+                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done) {
+  if (!head_done) {
+    head_launch<false, true>(st, c, blob, XL, W1, nullptr, W2, nullptr, nullptr, const_cast<float *>(hpre),
+                             const_cast<float *>(yhat), nullptr, dy, dhid, dZL);
+    counted();
+  }
   const int total = c.Hf * c.H + 2 * c.Hf + 1;
   k_head_grads<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2,
                                                                        c.H, c.Hf);

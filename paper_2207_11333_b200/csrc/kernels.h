@@ -50,10 +50,16 @@ size_t dMx_partial_floats(const Caps &c, int F);
 void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
                      float *sqerr, float *loss);
-// K6: head + pool backward -> dZ of the last layer, then head parameter gradients
+// K5+K6 fused (a training step): pool, head forward, loss terms and the head/pool
+// backward down to dZ of the last layer
+void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                       const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
+                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL);
+// K6: head + pool backward -> dZ of the last layer (skipped if head_done), then head parameter gradients
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
-                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2);
+                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done);
+void head_configure(const Caps &c);
 
 // K10: AdamW over the flat arena
 struct AdamDev {

@@ -525,18 +525,29 @@ __global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int c
   }
 }
 
-// db_U = sum_i dZ[i, :] — per-chunk partial column sums then fixed-order reduce
-constexpr int kColsumChunks = 64;
-__global__ void k_colsum_part(const uint8_t *__restrict__ blob, const float *__restrict__ X, int H,
-                              float *__restrict__ part) {
+// column sums (db_U = sum_i dZ[i, :], db_M = sum_i dP[i, :]): fixed 64-row chunks,
+// 8 independent loads in flight per thread, then a fixed-order reduction of the
+// chunk partials (k_reduce_rows)
+constexpr int kColsumRows = 64;
+constexpr int kColsumChunks = 128;  // partial slots; chunks beyond ceil(N/64) write zeros
+__global__ void __launch_bounds__(256) k_colsum_part(const uint8_t *__restrict__ blob, const float *__restrict__ X,
+                                                     int H, float *__restrict__ part) {
   const int N = batch_N(blob);
-  const int per = (N + kColsumChunks - 1) / kColsumChunks;
-  const int ch = blockIdx.x;
-  const int i0 = ch * per, i1 = min(N, i0 + per);
-  for (int h = threadIdx.x; h < H; h += blockDim.x) {
-    float s = 0.f;
-    for (int i = i0; i < i1; ++i) s += X[(size_t)i * H + h];
-    part[(size_t)ch * H + h] = s;
+  const int per = max(kColsumRows, (N + kColsumChunks - 1) / kColsumChunks);
+  for (int ch = blockIdx.x; ch < kColsumChunks; ch += gridDim.x) {
+    const int i0 = ch * per, i1 = min(N, i0 + per);
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+      float s[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      int i = i0;
+      for (; i + 8 <= i1; i += 8) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s[u] += X[(size_t)(i + u) * H + h];
+      }
+      float tail = 0.f;
+      for (; i < i1; ++i) tail += X[(size_t)i * H + h];
+      s[0] += tail;
+      part[(size_t)ch * H + h] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+    }
   }
 }
 
@@ -586,7 +597,7 @@ void launch_tc_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const flo
   run_tc(st, op, (c.H / TC_BM) * (4 * c.H / TcDU::BN) * kTcDUSplits);
   const int count = c.H * 12 * c.H;
   k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDUSplits, count, dU);
-  k_colsum_part<<<kColsumChunks, 128, 0, st>>>(blob, dZ, c.H, partial);
+  k_colsum_part<<<kColsumChunks, std::min(c.H, 256), 0, st>>>(blob, dZ, c.H, partial);
   k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(partial, kColsumChunks, c.H, dbU);
   g_launches += 3;
 }
@@ -635,7 +646,7 @@ void launch_tc_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
   run_tc(st, op, (c.H / TC_BM) * (F / TcDMx::BN) * kTcDMxSplits);
   const int count = c.H * F;
   k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDMxSplits, count, dMx);
-  k_colsum_part<<<kColsumChunks, 128, 0, st>>>(blob, dP, c.H, partial);
+  k_colsum_part<<<kColsumChunks, std::min(c.H, 256), 0, st>>>(blob, dP, c.H, partial);
   k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(partial, kColsumChunks, c.H, dbM);
   g_launches += 3;
 }
