@@ -320,16 +320,17 @@ void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float 
 // 32*CPL-channel chunk (blockIdx.y). Messages m = P[j] + b_M + M_e e_ji are
 // recomputed, never stored. First pass: sum, min, max with
 // first-position argmin/argmax; second pass: centred sum of squares (two-pass
-// variance) over messages kept in registers for the first KREG
-// edges (molecules: degree <= 4). d = 0 -> all aggregates 0 (C5).
+// variance) over recomputed messages. d = 0 -> all aggregates 0 (C5).
 // FE: compile-time edge-feature width (4 for the molecular encoding; 8 = generic <= 8).
-constexpr int kKReg = 4;
 
 template <int CPL>
 __device__ __forceinline__ void load_vec(const float *p, float (&v)[CPL]) {
   if constexpr (CPL == 4) {
     const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
     v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+  } else if constexpr (CPL == 2) {
+    const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
+    v[0] = t.x; v[1] = t.y;
   } else {
 #pragma unroll
     for (int c = 0; c < CPL; ++c) v[c] = __ldg(p + c);
@@ -339,6 +340,8 @@ template <int CPL>
 __device__ __forceinline__ void store_vec(float *p, const float (&v)[CPL]) {
   if constexpr (CPL == 4) {
     *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  } else if constexpr (CPL == 2) {
+    *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
   } else {
 #pragma unroll
     for (int c = 0; c < CPL; ++c) p[c] = v[c];
@@ -370,7 +373,7 @@ __device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm
 }
 
 template <int CPL, int FE>
-__global__ void __launch_bounds__(256, 3) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
+__global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
                                                     const float *__restrict__ Me, const float *__restrict__ bM,
                                                     float var_floor, float *__restrict__ A,
                                                     uint8_t *__restrict__ arg, int H) {
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(256, 3) k_agg_fwd(const uint8_t *__restrict__ 
   }
   for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < b.N; i += gridDim.x * wpb) {
     const int k0 = b.rowptr[i], k1 = b.rowptr[i + 1], d = k1 - k0;
-    float s[CPL], mx[CPL], mn[CPL], mr[kKReg][CPL];
+    float s[CPL], mx[CPL], mn[CPL];
     int amx[CPL], amn[CPL];
 #pragma unroll
     for (int c = 0; c < CPL; ++c) { s[c] = 0.f; mx[c] = -INFINITY; mn[c] = INFINITY; amx[c] = 0; amn[c] = 0; }
@@ -399,12 +402,6 @@ __global__ void __launch_bounds__(256, 3) k_agg_fwd(const uint8_t *__restrict__ 
       load_vec<CPL>(P + (size_t)j * H + ch, pj);
       message<CPL, FE>(pj, bm, me, ef, m);
       const int p = k - k0;
-#pragma unroll
-      for (int e = 0; e < kKReg; ++e)
-        if (p == e) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) mr[e][c] = m[c];
-        }
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
         s[c] += m[c];
@@ -422,16 +419,7 @@ __global__ void __launch_bounds__(256, 3) k_agg_fwd(const uint8_t *__restrict__ 
       float ss[CPL];
 #pragma unroll
       for (int c = 0; c < CPL; ++c) { mean[c] = s[c] / fd; ss[c] = 0.f; }
-#pragma unroll
-      for (int e = 0; e < kKReg; ++e)
-        if (e < d) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const float t = mr[e][c] - mean[c];
-            ss[c] = fmaf(t, t, ss[c]);
-          }
-        }
-      for (int k = k0 + kKReg; k < k1; ++k) {  // high-degree tail: recompute
+      for (int k = k0; k < k1; ++k) {  // second pass: recompute (P rows are L1-resident)
         const int j = b.col[k];
         float ef[FE], pj[CPL], m[CPL];
         load_edge<FE>(b.ea, Fe, k, ef);
@@ -460,6 +448,9 @@ __global__ void __launch_bounds__(256, 3) k_agg_fwd(const uint8_t *__restrict__ 
       *reinterpret_cast<uchar4 *>(ai) = make_uchar4(amn[0], amn[1], amn[2], amn[3]);
       *reinterpret_cast<uchar4 *>(ai + H) =
           make_uchar4(amx[0] | (flag[0] << 7), amx[1] | (flag[1] << 7), amx[2] | (flag[2] << 7), amx[3] | (flag[3] << 7));
+    } else if constexpr (CPL == 2) {
+      *reinterpret_cast<uchar2 *>(ai) = make_uchar2(amn[0], amn[1]);
+      *reinterpret_cast<uchar2 *>(ai + H) = make_uchar2(amx[0] | (flag[0] << 7), amx[1] | (flag[1] << 7));
     } else {
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
@@ -470,20 +461,20 @@ __global__ void __launch_bounds__(256, 3) k_agg_fwd(const uint8_t *__restrict__ 
   }
 }
 
-static int agg_cpl(int H) { return (H % 128 == 0) ? 4 : 1; }
+static int agg_cpl(int H) { return (H % 64 == 0) ? 2 : 1; }
 
 template <int CPL, int FE>
 static void agg_fwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                            const float *bM, float var_floor, float *A, uint8_t *arg) {
-  const dim3 grid(std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 6)), c.H / (32 * CPL));
+  const dim3 grid(std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 4)), c.H / (32 * CPL));
   k_agg_fwd<CPL, FE><<<grid, 256, 0, st>>>(blob, P, Me, bM, var_floor, A, arg, c.H);
 }
 
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, float var_floor, float *A, uint8_t *arg) {
   const int cpl = agg_cpl(c.H);
-  if (cpl == 4 && c.Fe == 4) agg_fwd_launch<4, 4>(st, c, blob, P, Me, bM, var_floor, A, arg);
-  else if (cpl == 4) agg_fwd_launch<4, 8>(st, c, blob, P, Me, bM, var_floor, A, arg);
+  if (cpl == 2 && c.Fe == 4) agg_fwd_launch<2, 4>(st, c, blob, P, Me, bM, var_floor, A, arg);
+  else if (cpl == 2) agg_fwd_launch<2, 8>(st, c, blob, P, Me, bM, var_floor, A, arg);
   else if (c.Fe == 4) agg_fwd_launch<1, 4>(st, c, blob, P, Me, bM, var_floor, A, arg);
   else agg_fwd_launch<1, 8>(st, c, blob, P, Me, bM, var_floor, A, arg);
   counted();
@@ -500,7 +491,7 @@ void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
 constexpr int kAggBwdWarps = 8;
 
 template <int CPL, int FE>
-__global__ void __launch_bounds__(256, 3) k_agg_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
+__global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
                                                     const float *__restrict__ Me, const float *__restrict__ bM,
                                                     const float *__restrict__ A, const uint8_t *__restrict__ arg,
                                                     const float *__restrict__ dA, float *__restrict__ dP,
@@ -528,7 +519,7 @@ __global__ void __launch_bounds__(256, 3) k_agg_bwd(const uint8_t *__restrict__ 
       const int i = b.col[k];
       const int sl = b.slot[k];
       const int di = b.rowptr[i + 1] - b.rowptr[i];
-      const float fd = (float)di;
+      const float inv_d = 1.0f / (float)di;
       float ef[FE];
       load_edge<FE>(b.ea, Fe, k, ef);
       float m[CPL];
@@ -549,16 +540,21 @@ __global__ void __launch_bounds__(256, 3) k_agg_bwd(const uint8_t *__restrict__ 
         const uchar4 t1 = *reinterpret_cast<const uchar4 *>(ai + H);
         amn[0] = t0.x; amn[1] = t0.y; amn[2] = t0.z; amn[3] = t0.w;
         amx[0] = t1.x; amx[1] = t1.y; amx[2] = t1.z; amx[3] = t1.w;
+      } else if constexpr (CPL == 2) {
+        const uchar2 t0 = *reinterpret_cast<const uchar2 *>(ai);
+        const uchar2 t1 = *reinterpret_cast<const uchar2 *>(ai + H);
+        amn[0] = t0.x; amn[1] = t0.y;
+        amx[0] = t1.x; amx[1] = t1.y;
       } else {
 #pragma unroll
         for (int c = 0; c < CPL; ++c) { amn[c] = ai[c]; amx[c] = ai[H + c]; }
       }
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        float g = gmean[c] / fd;
+        float g = gmean[c] * inv_d;
         if ((amx[c] & 0x7f) == sl) g += gmax[c];
         if (amn[c] == sl) g += gmin[c];
-        if (amx[c] & 0x80) g += gstd[c] * (m[c] - mu[c]) / (fd * sg[c]);
+        if (amx[c] & 0x80) g += gstd[c] * (m[c] - mu[c]) * inv_d * __frcp_rn(sg[c]);
         dp[c] += g;
 #pragma unroll
         for (int f = 0; f < FE; ++f) acc[c][f] = fmaf(g, ef[f], acc[c][f]);
@@ -597,7 +593,7 @@ __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int co
   }
 }
 
-static int agg_bwd_blocks(const Caps &c) { return std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 3)); }
+static int agg_bwd_blocks(const Caps &c) { return std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 2)); }
 size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * c.Fe; }
 
 template <int CPL, int FE>
@@ -612,8 +608,8 @@ void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
                     float *partial, float *dMe) {
   const int cpl = agg_cpl(c.H);
-  if (cpl == 4 && c.Fe == 4) agg_bwd_launch<4, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
-  else if (cpl == 4) agg_bwd_launch<4, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
+  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
+  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
   else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
   else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
   counted();
