@@ -221,7 +221,8 @@ def main():
     max_edges = B * int(np.diff(np.asarray(data["edge_offset"])).max())
     n_res = max(1, min(args.resident, args.steps))
     e2e_slots = 0 if args.no_e2e else 2
-    cfg = hgnn.make_config(data["f_node"], 4, H, L, B, max_nodes, max_edges, delta, n_slots=n_res + e2e_slots)
+    cfg = hgnn.make_config(data["f_node"], 4, H, L, B, max_nodes, max_edges, delta, n_slots=n_res + e2e_slots,
+                           max_degree=st["max_degree"])
     ctx = hgnn.Context(cfg, device=local_rank)
     ctx.params_init(1234)
     ctx.comm_init(rank, world)
@@ -386,7 +387,7 @@ def main():
                    "layers": L, "hidden": H, "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
                    "parallelism": f"dp{world}", "resident_batches": n_res,
                    "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
-                   "gemm_precision": "fp32 SIMT FFMA"},
+                   "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs"},
         "roofline": prof, "roofline_agg": agg, "gemm": gemm,
         "phases_ms": {k: round(v[0], 4) for k, v in phases.items()},
         "phase_launches": {k: v[1] for k, v in phases.items()},

@@ -115,7 +115,8 @@ typedef struct {
   int32_t flags;                     /* HG_FLAG_*; 0 = defaults */
   double delta;                      /* PNA degree statistic (hg_degree_stat) */
   float var_floor;                   /* epsilon_v for the std aggregator, 1e-10 */
-  float pad;
+  int32_t max_degree;                /* capacity: largest node degree in a batch (0 = HG_MAX_DEGREE).
+                                        <= 15 enables the degree-class GEMMs. */
 } hg_config;
 
 /* hg_config.flags: force the SIMT fp32 GEMMs instead of the tcgen05 3xTF32

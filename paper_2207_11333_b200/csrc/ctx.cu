@@ -29,6 +29,8 @@ struct Plan {
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
   size_t part = 0;
   size_t UT = 0, u_off = 0;
+  int cmax = 0;  // degree-class slots (0 = class GEMMs off)
+  size_t perm = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
   size_t total = 0;
 };
 
@@ -76,8 +78,19 @@ Plan make_plan(const hg_config &c) {
   if (tc_supported(caps))
     pf = std::max({pf, tc_dU_partial_floats(caps), tc_dMx_partial_floats(caps, c.hidden)});
   p.part = take(sizeof(float) * pf);
-  p.UT = take(sizeof(float) * (size_t)c.layers * 12 * H * H);
+  p.cmax = tc_num_classes(caps, c.max_degree);
+  p.UT = take(p.cmax ? 256 : sizeof(float) * (size_t)c.layers * 12 * H * H);
   p.u_off = take(sizeof(int64_t) * (size_t)c.layers);
+  p.perm = take(sizeof(int) * N);
+  p.deginfo = take(sizeof(DegInfo));
+  if (p.cmax) {
+    p.tiles = take(sizeof(int4) * (size_t)tc_max_tiles(caps, p.cmax));
+    p.splits = take(sizeof(int4) * (size_t)tc_max_splits(caps, p.cmax));
+    p.Wf = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+    p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+    pf = std::max(pf, tc_gram_partial_floats(caps, p.cmax));
+    p.part = take(sizeof(float) * pf);  // (re-take: the class partials are larger)
+  }
   p.total = off;
   return p;
 }
@@ -196,7 +209,17 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
   float *amp = x->f(p.amp), *att = x->f(p.att);
-  phase(pr, HG_PHASE_SCALERS, [&] { launch_scalers(st, x->caps, blob, c.delta, amp, att); });
+  phase(pr, HG_PHASE_SCALERS, [&] {
+    launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
+                   reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
+                   reinterpret_cast<int4 *>(x->b(p.splits)));
+  });
+  const bool cls = x->use_tc && p.cmax > 0;
+  if (cls)
+    phase(pr, HG_PHASE_UPDATE, [&] {
+      launch_prep_W(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
+                    reinterpret_cast<const DegInfo *>(x->b(p.deginfo)), x->f(p.Wf), x->f(p.WbT));
+    });
   for (int l = 0; l < c.layers; ++l) {
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
@@ -211,7 +234,13 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
                      c.var_floor, x->f(p.A[l]), x->b(p.arg[l]));
     });
     phase(pr, HG_PHASE_UPDATE, [&] {
-      if (x->use_tc)
+      if (cls)
+        launch_tc_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), reinterpret_cast<const int *>(x->b(p.perm)),
+                             reinterpret_cast<const DegInfo *>(x->b(p.deginfo)),
+                             reinterpret_cast<const int4 *>(x->b(p.tiles)),
+                             x->f(p.Wf) + (size_t)l * p.cmax * c.hidden * 4 * c.hidden, x->param(lname(l, "b_U")),
+                             x->f(p.X[l]));
+      else if (x->use_tc)
         launch_tc_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")),
                          x->param(lname(l, "b_U")), x->f(p.X[l]));
       else
@@ -242,20 +271,30 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
                     x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
                     x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), head_done);
   });
-  if (x->use_tc)
+  const bool cls = x->use_tc && p.cmax > 0;
+  const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
+  const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
+  if (x->use_tc && !cls)
     phase(pr, HG_PHASE_DA, [&] {
       launch_prep_UT(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers,
                      x->f(p.UT));
     });
   for (int l = c.layers - 1; l >= 0; --l) {
     phase(pr, HG_PHASE_DA, [&] {
-      if (x->use_tc)
+      if (cls)
+        launch_tc_dA_cls(st, x->caps, p.cmax, dZ, perm, dinfo, reinterpret_cast<const int4 *>(x->b(p.tiles)),
+                         x->f(p.WbT) + (size_t)l * p.cmax * c.hidden * 4 * c.hidden, x->f(p.dA));
+      else if (x->use_tc)
         launch_tc_dA(st, x->caps, blob, dZ, amp, att, x->f(p.UT) + (size_t)l * 12 * c.hidden * c.hidden, x->f(p.dA));
       else
         launch_dA(st, x->caps, blob, dZ, amp, att, x->param(lname(l, "U")), x->f(p.dA));
     });
     phase(pr, HG_PHASE_DU, [&] {
-      if (x->use_tc)
+      if (cls)
+        launch_tc_dU_cls(st, x->caps, p.cmax, blob, dZ, x->f(p.A[l]), perm, dinfo,
+                         reinterpret_cast<const int4 *>(x->b(p.splits)), x->f(p.part), x->grad(lname(l, "U")),
+                         x->grad(lname(l, "b_U")));
+      else if (x->use_tc)
         launch_tc_dU(st, x->caps, blob, dZ, x->f(p.A[l]), amp, att, x->f(p.part), x->grad(lname(l, "U")),
                      x->grad(lname(l, "b_U")));
       else

@@ -105,6 +105,7 @@ hg_status check_config(const hg_config *c) {
     return fail(HG_E_INVALID, "capacities must be positive");
   if (!(c->delta > 0.0)) return fail(HG_E_INVALID, "delta must be > 0 (SPEC.md:329)");
   if (!(c->var_floor > 0.0f)) return fail(HG_E_INVALID, "var_floor must be > 0");
+  if (c->max_degree < 0 || c->max_degree > HG_MAX_DEGREE) return fail(HG_E_INVALID, "max_degree out of range");
   return HG_OK;
 }
 
@@ -318,6 +319,7 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
   float *ea = (float *)(base + o.eattr);
   uint8_t *sl = base + o.slot;
   int64_t nb = 0, eb = 0;
+  const int maxdeg = cfg->max_degree > 0 ? cfg->max_degree : HG_MAX_DEGREE;
   gp[0] = 0;
   rp[0] = 0;
   for (int32_t b = 0; b < B; ++b) {
@@ -331,10 +333,14 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
     // in-neighbours are their dst values, already ascending.
     int64_t k = 0;
     for (int64_t i = 0; i < n; ++i) {
+      const int64_t kstart = k;
       while (k < e && s->src[e0 + k] == i) {
         col[eb + k] = (int32_t)(s->dst[e0 + k] + nb);
         ++k;
       }
+      if (k - kstart > maxdeg)
+        return fail(HG_E_CAPACITY, "graph %lld has a node of degree %lld > max_degree %d", (long long)g,
+                    (long long)(k - kstart), maxdeg);
       rp[nb + i + 1] = (int32_t)(eb + k);
     }
     nb += n;

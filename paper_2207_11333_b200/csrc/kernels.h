@@ -69,6 +69,32 @@ struct AdamDev {
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
                   float lr, float beta1, float beta2, float eps, float wd);
 
+// degree classes (tcgemm.cu): one class per distinct degree present in the batch
+constexpr int kMaxClasses = 16;
+constexpr int kGramKS = 256;  // nodes per K-split of the per-class Gram GEMM
+constexpr int HG_MAX_DEGREE_DEV = 127;
+struct DegInfo {
+  int C, T, S, pad;
+  int deg[kMaxClasses], start[kMaxClasses], count[kMaxClasses];
+  float amp[kMaxClasses], att[kMaxClasses];
+};
+int tc_num_classes(const Caps &c, int max_degree);  // class slots (max_degree+1) or 0 = class path off
+int tc_max_tiles(const Caps &c, int cmax);
+int tc_max_splits(const Caps &c, int cmax);
+// stable degree sort + per-node scalers (+ class table / tiles / splits when cmax > 0)
+void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
+                    DegInfo *info, int4 *tiles, int4 *splits);
+void launch_prep_W(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
+                   const DegInfo *info, float *Wf, float *WbT);
+void launch_tc_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm,
+                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *bU, float *X1);
+void launch_tc_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const int *perm, const DegInfo *info,
+                      const int4 *tiles, const float *WbT, float *dA);
+size_t tc_gram_partial_floats(const Caps &c, int cmax);
+void launch_tc_dU_cls(cudaStream_t st, const Caps &c, int cmax, const uint8_t *blob, const float *dZ, const float *A,
+                      const int *perm, const DegInfo *info, const int4 *splits, float *partial, float *dU,
+                      float *dbU);
+
 // tcgen05 3xTF32 GEMMs (tcgemm.cu); require H % 128 == 0
 bool tc_supported(const Caps &c);
 cudaError_t tc_configure();  // opt-in shared-memory sizes (call once, outside graph capture)

@@ -52,7 +52,7 @@ class hg_config(ctypes.Structure):
                 ("layers", ctypes.c_int32), ("fc_hidden", ctypes.c_int32), ("max_graphs", ctypes.c_int32),
                 ("max_nodes", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("n_slots", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("delta", ctypes.c_double), ("var_floor", ctypes.c_float),
-                ("pad", ctypes.c_float)]
+                ("max_degree", ctypes.c_int32)]
 
 
 class hg_adamw(ctypes.Structure):
@@ -154,10 +154,10 @@ HG_FLAG_SIMT_GEMM = 1
 
 
 def make_config(f_node, f_edge, hidden, layers, max_graphs, max_nodes, max_edges, delta, fc_hidden=None,
-                n_slots=2, var_floor=1e-10, flags=0) -> hg_config:
+                n_slots=2, var_floor=1e-10, flags=0, max_degree=0) -> hg_config:
     return hg_config(f_node=f_node, f_edge=f_edge, hidden=hidden, layers=layers, fc_hidden=fc_hidden or hidden,
                      max_graphs=max_graphs, max_nodes=max_nodes, max_edges=max_edges, n_slots=n_slots, flags=flags,
-                     delta=float(delta), var_floor=var_floor, pad=0.0)
+                     delta=float(delta), var_floor=var_floor, max_degree=max_degree)
 
 
 def make_adamw(**kw) -> hg_adamw:

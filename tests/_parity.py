@@ -111,13 +111,17 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
     return res
 
 
-def make_ctx(data, B, H, L, seed=2, n_slots=2, Hf=None):
+def make_ctx(data, B, H, L, seed=2, n_slots=2, Hf=None, flags=0, max_degree=None):
     delta = O.degree_stat(data)
     maxn, maxe = capacity_for(data, B)
-    cfg = hgnn.make_config(data["f_node"], 4, H, L, B, maxn, maxe, delta, fc_hidden=Hf, n_slots=n_slots)
+    store = hgnn.Store(data)
+    if max_degree is None:
+        max_degree = store.stats()["max_degree"]
+    cfg = hgnn.make_config(data["f_node"], 4, H, L, B, maxn, maxe, delta, fc_hidden=Hf, n_slots=n_slots,
+                           flags=flags, max_degree=max_degree)
     ctx = hgnn.Context(cfg)
     ctx.params_init(seed)
-    ctx._store = hgnn.Store(data)
+    ctx._store = store
     return ctx, cfg, delta
 
 

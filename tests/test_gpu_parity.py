@@ -85,25 +85,19 @@ def test_one_step_parity(torch_cuda, preset, B, H, L):
     PT.assert_parity(res)
 
 
-def test_simt_and_tcgen05_paths_agree(torch_cuda):
-    """The tcgen05 3xTF32 GEMMs and the SIMT fp32 GEMMs compute the same step:
-    both within the oracle bars, and close to each other (config B shape)."""
+@pytest.mark.parametrize("mode", ["simt", "tc_3acc", "tc_classes"])
+def test_gemm_paths_agree(torch_cuda, mode):
+    """Three implementations of the dense contractions compute the same step,
+    each within the oracle bars: SIMT fp32 GEMMs, tcgen05 3xTF32 with three
+    scaler accumulators, and tcgen05 3xTF32 per degree class (config B shape)."""
     data = PT.generate("pcqm", 600, 51)
     ids = O.shard(5, 0, 0, 1, 600)[:128]
-    grads = []
-    for flags in (hgnn.HG_FLAG_SIMT_GEMM, 0):
-        delta = O.degree_stat(data)
-        maxn, maxe = PT.capacity_for(data, 128)
-        cfg = hgnn.make_config(data["f_node"], 4, 128, 6, 128, maxn, maxe, delta, flags=flags)
-        ctx = hgnn.Context(cfg)
-        ctx.params_init(7)
-        ctx._store = hgnn.Store(data)
-        res = PT.run_step_parity(data, ids, ctx, cfg, delta, do_step=False)
-        print("flags", flags, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
-        PT.assert_parity(res)
-        grads.append(hgnn.arena_to_dict(ctx.grads_get(), ctx.layout))
-    for k in grads[0]:
-        assert PT.max_scaled(grads[1][k], grads[0][k]) <= 1e-3, k
+    flags = hgnn.HG_FLAG_SIMT_GEMM if mode == "simt" else 0
+    max_degree = 127 if mode == "tc_3acc" else None  # > 15 disables the class path
+    ctx, cfg, delta = PT.make_ctx(data, 128, 128, 6, seed=7, flags=flags, max_degree=max_degree)
+    res = PT.run_step_parity(data, ids, ctx, cfg, delta, do_step=False)
+    print(mode, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
+    PT.assert_parity(res)
 
 
 def test_edge_cases_isolated_nodes_single_graph_max_degree(torch_cuda):
