@@ -36,7 +36,7 @@ extern std::atomic<int64_t> g_launches;
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;            // fp32 elements per 128-byte smem row
 constexpr int TC_XF_WARPS = 8;       // transform (+ epilogue) warps
-constexpr int TC_LD_WARPS = 2;       // cp.async loader warps
+constexpr int TC_LD_WARPS = 4;       // cp.async loader warps
 constexpr int TC_MMA_WARP = TC_XF_WARPS + TC_LD_WARPS;
 constexpr int TC_THREADS = 32 * (TC_MMA_WARP + 1);
 
@@ -148,28 +148,54 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   const int nchunks = ke > kb ? (ke - kb + TC_BK - 1) / TC_BK : 0;
 
   if (warp >= TC_XF_WARPS && warp < TC_MMA_WARP) {
-    // ---------------- loaders: cp.async raw fp32 tiles, completion -> rfull[rs]
+    // ---------------- loaders: cp.async raw fp32 tiles, completion -> rfull[rs].
+    // K-major sources: the rows a thread copies are fixed for the whole tile, so
+    // their (possibly gathered) base pointers are resolved once, outside the K loop.
     const int t = threadIdx.x - NXF;
     const float *dummy = op.any_src();
+    constexpr int NPA = TC_BM * 8 / NLD, NPB = (NMMA * 8 + NLD - 1) / NLD;
+    const float *arow[AMN ? 1 : NPA];
+    const float *brow[BMN ? 1 : NPB];
+    if constexpr (!AMN) {
+#pragma unroll
+      for (int i = 0; i < NPA; ++i) arow[i] = op.a_src(m0 + ((t + i * NLD) >> 3), kb, ke);
+    }
+    if constexpr (!BMN) {
+#pragma unroll
+      for (int i = 0; i < NPB; ++i) {
+        const int p = t + i * NLD;
+        brow[i] = p < NMMA * 8 ? op.b_src(n0, p >> 3, kb, ke) : nullptr;
+      }
+    }
     for (int c = 0; c < nchunks; ++c) {
       const int rs = c % RS;
       if (c >= RS) tc::mbar_wait(&rempty[rs], ((c / RS) - 1) & 1);
       uint8_t *rA = raw0 + rs * RAWB;
       uint8_t *rB = rA + A_BYTES;
       const int k0 = kb + c * TC_BK;
-      for (int p = t; p < TC_BM * 8; p += NLD) {
+#pragma unroll
+      for (int i = 0; i < NPA; ++i) {
+        const int p = t + i * NLD;
         int r, k;
         uint32_t off;
         load_piece<AMN, TC_BM>(p, r, k, off);
-        const float *src = op.a_src(m0 + r, k0 + k, ke);
+        const float *src;
+        if constexpr (AMN) src = op.a_src(m0 + r, k0 + k, ke);
+        else src = (arow[i] && k0 + k < ke) ? arow[i] + (k0 - kb) + k : nullptr;
         tc::cp_async16(rA + off, src ? src : dummy, src ? 16u : 0u);
       }
-      for (int p = t; p < NMMA * 8; p += NLD) {
-        int r, k;
-        uint32_t off;
-        load_piece<BMN, NMMA>(p, r, k, off);
-        const float *src = op.b_src(n0, r, k0 + k, ke);
-        tc::cp_async16(rB + off, src ? src : dummy, src ? 16u : 0u);
+#pragma unroll
+      for (int i = 0; i < NPB; ++i) {
+        const int p = t + i * NLD;
+        if (p < NMMA * 8) {
+          int r, k;
+          uint32_t off;
+          load_piece<BMN, NMMA>(p, r, k, off);
+          const float *src;
+          if constexpr (BMN) src = op.b_src(n0, r, k0 + k, ke);
+          else src = (brow[i] && k0 + k < ke) ? brow[i] + (k0 - kb) + k : nullptr;
+          tc::cp_async16(rB + off, src ? src : dummy, src ? 16u : 0u);
+        }
       }
       tc::cp_async_arrive(&rfull[rs]);
     }
@@ -535,7 +561,7 @@ __global__ void k_prep_W(const float *__restrict__ params, const int64_t *__rest
 
 // ---------------------------------------------------------------- G1 update, class tiles
 struct TcUpdC {
-  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 2, RAW = 3;
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
   const float *A; const int *perm; const DegInfo *info; const int4 *tiles; const float *Wf; const float *bU;
   float *X1; int H; int cmax; int row_end; const float *W;
@@ -573,7 +599,7 @@ struct TcUpdC {
 
 // ---------------------------------------------------------------- G2 dA, class tiles
 struct TcDAC {
-  static constexpr int BN = 128, NACC = 1, NMMA = 128, STAGES = 2, RAW = 3;
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
   const float *dZ; const int *perm; const DegInfo *info; const int4 *tiles; const float *WbT; float *dA; int H;
   int row_end; const float *W;
@@ -607,7 +633,7 @@ struct TcDAC {
 // ---------------------------------------------------------------- G3 per-class Gram partials
 // part[sp][h][n] = sum_{k in split sp} dZ[perm[k], h] A[perm[k], n]
 struct TcGramC {
-  static constexpr int BN = 128, NACC = 1, NMMA = 128, STAGES = 2, RAW = 3;
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = true, B_MN = true;
   const float *dZ; const float *A; const int *perm; const DegInfo *info; const int4 *splits; float *part; int H;
   int smax; int sp; int s0;
@@ -668,7 +694,7 @@ __global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInf
 // ---------------------------------------------------------------- K1 projection (F % 4 == 0)
 // P[N, H] = X[N, F] M_x^T : A = X rows (K = F), B = M_x rows
 struct TcProj {
-  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 2, RAW = 3;
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
   const uint8_t *blob; const float *X; const float *Mx; float *P; int F, H; int N;
   __device__ void prepare() { N = batch_N(blob); }
@@ -701,7 +727,7 @@ struct TcProj {
 // ---------------------------------------------------------------- K9b dX (l > 0)
 // dZprev[N, F] = (dP[N, H] M_x[H, F]) * [X_l > 0] : A = dP rows (K = H), B(f, h) = M_x[h, f] (MN source)
 struct TcDX {
-  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 2, RAW = 3;
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = true;
   const uint8_t *blob; const float *dP; const float *Mx; const float *Xl; float *dZ; int H, F; int N;
   __device__ void prepare() { N = batch_N(blob); }
@@ -735,7 +761,7 @@ struct TcDX {
 // dM_x[h, f] = sum_i dP[i, h] X_l[i, f]: A(h, i) = dP[i, h], B(f, i) = X_l[i, f] (both MN sources)
 constexpr int kTcDMxSplits = 16;
 struct TcDMx {
-  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 2, RAW = 3;
+  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = true, B_MN = true;
   const uint8_t *blob; const float *dP; const float *X; float *part; int H, F; int N; int sp;
   __device__ void prepare() { N = batch_N(blob); }
