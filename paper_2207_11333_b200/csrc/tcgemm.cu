@@ -202,6 +202,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
   } else if (warp < TC_XF_WARPS) {
     // ---------------- transform: raw -> (fix-up) -> 3xTF32 hi/lo K-major SW128 tiles
     const int t = threadIdx.x;
+    // optional fused column sum of an MN-major A operand (bias gradients): with
+    // NXF = 2 * TC_BM each thread always transforms the same row r = t % TC_BM
+    float csum = 0.f;
+    static_assert(!Op::COLSUM || (AMN && NXF == 2 * TC_BM), "fused column sum layout");
     for (int c = 0; c < nchunks; ++c) {
       const int rs = c % RS, s = c % ST;
       tc::mbar_wait(&rfull[rs], (c / RS) & 1);
@@ -218,7 +222,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
         int r, j;
         xf_coords<AMN, TC_BM>(task, r, j);
         float4 lo;
-        const float4 hi = split_hi(op.a_fix(read_raw<AMN, TC_BM>(rA, r, j), m0 + r, k0 + 4 * j, ke), lo);
+        const float4 av = op.a_fix(read_raw<AMN, TC_BM>(rA, r, j), m0 + r, k0 + 4 * j, ke);
+        if constexpr (Op::COLSUM) csum += (av.x + av.y) + (av.z + av.w);
+        const float4 hi = split_hi(av, lo);
         const uint32_t o = tc::sw128_off(r, j);
         *reinterpret_cast<float4 *>(sAh + o) = hi;
         *reinterpret_cast<float4 *>(sAl + o) = lo;
@@ -236,6 +242,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
       tc::mbar_arrive(&rempty[rs]);     // raw stage may be refilled
       tc::fence_proxy_async_smem();     // operand tiles -> visible to the tensor core
       tc::mbar_arrive(&full[s]);
+    }
+    if constexpr (Op::COLSUM) {
+      // combine the two half-sums of each row in fixed order (smem reuse of the
+      // barrier-free raw region is unsafe, so use a small dedicated array)
+      __shared__ float cs[2][TC_BM];
+      cs[t / TC_BM][t % TC_BM] = csum;
+      asm volatile("bar.sync 1, %0;" ::"n"(NXF));  // transform warps only
+      if (t < TC_BM) op.colsum(m0 + t, n0, cs[0][t] + cs[1][t]);
     }
     // ---------------- epilogue: warp w reads TMEM lanes 32*(w%4)..+31 (one row per
     // thread); the two warpgroups split the 32-column chunks of each accumulator
@@ -310,6 +324,7 @@ __device__ __forceinline__ float scal(const float *amp, const float *att, int m,
 struct TcUpdate {
   static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 2, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
+  static constexpr bool COLSUM = false;
   const uint8_t *blob; const float *A; const float *amp; const float *att; const float *U; const float *bU;
   float *X1; int H; int N;
   __device__ void prepare() { N = batch_N(blob); }
@@ -351,6 +366,7 @@ struct TcUpdate {
 struct TcDA {
   static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 2, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
+  static constexpr bool COLSUM = false;
   const uint8_t *blob; const float *dZ; const float *amp; const float *att; const float *UT; float *dA; int H; int N;
   __device__ void prepare() { N = batch_N(blob); }
   __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) const {
@@ -392,6 +408,7 @@ constexpr int kTcDUSplits = 16;
 struct TcDU {
   static constexpr int BN = 32, NACC = 3, NMMA = 96, STAGES = 2, RAW = 3;
   static constexpr bool A_MN = true, B_MN = true;
+  static constexpr bool COLSUM = false;
   const uint8_t *blob; const float *dZ; const float *A; const float *amp; const float *att; float *part; int H;
   int N; int sp;
   __device__ void prepare() { N = batch_N(blob); }
@@ -563,6 +580,7 @@ __global__ void k_prep_W(const float *__restrict__ params, const int64_t *__rest
 struct TcUpdC {
   static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
+  static constexpr bool COLSUM = false;
   const float *A; const int *perm; const DegInfo *info; const int4 *tiles; const float *Wf; const float *bU;
   float *X1; int H; int cmax; int row_end; const float *W;
   __device__ void prepare() {}
@@ -601,6 +619,7 @@ struct TcUpdC {
 struct TcDAC {
   static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
+  static constexpr bool COLSUM = false;
   const float *dZ; const int *perm; const DegInfo *info; const int4 *tiles; const float *WbT; float *dA; int H;
   int row_end; const float *W;
   __device__ void prepare() {}
@@ -635,8 +654,12 @@ struct TcDAC {
 struct TcGramC {
   static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = true, B_MN = true;
+  static constexpr bool COLSUM = true;
   const float *dZ; const float *A; const int *perm; const DegInfo *info; const int4 *splits; float *part; int H;
-  int smax; int sp; int s0;
+  int smax; float *cs_part; int sp; int s0;
+  __device__ void colsum(int m, int n0, float v) const {
+    if (n0 == 0) cs_part[(size_t)sp * H + m] = v;
+  }
   __device__ void prepare() {}
   __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) {
     const int nt = 4 * H / BN, mt = H / TC_BM;
@@ -669,6 +692,21 @@ struct TcGramC {
   }
 };
 
+// db_U[h] = sum over the S (device-side) class splits of the fused column sums,
+// one warp per output, fixed xor-shuffle order
+__global__ void k_reduce_splits_rows(const float *__restrict__ cs, const DegInfo *__restrict__ info, int H,
+                                     float *__restrict__ out) {
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const int S = info->S;
+  for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < H; e += gridDim.x * wpb) {
+    float s = 0.f;
+    for (int p = lane; p < S; p += 32) s += cs[(size_t)p * H + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) out[e] = s;
+  }
+}
+
 // dU[h][s*4H + n] = sum_sp s(class(sp)) part[sp][h][n], fixed split order
 __global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInfo *__restrict__ info,
                                     const int4 *__restrict__ splits, int H, float *__restrict__ dU) {
@@ -696,6 +734,7 @@ __global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInf
 struct TcProj {
   static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = false;
+  static constexpr bool COLSUM = false;
   const uint8_t *blob; const float *X; const float *Mx; float *P; int F, H; int N;
   __device__ void prepare() { N = batch_N(blob); }
   __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) const {
@@ -729,6 +768,7 @@ struct TcProj {
 struct TcDX {
   static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = false, B_MN = true;
+  static constexpr bool COLSUM = false;
   const uint8_t *blob; const float *dP; const float *Mx; const float *Xl; float *dZ; int H, F; int N;
   __device__ void prepare() { N = batch_N(blob); }
   __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) const {
@@ -763,7 +803,11 @@ constexpr int kTcDMxSplits = 16;
 struct TcDMx {
   static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
   static constexpr bool A_MN = true, B_MN = true;
-  const uint8_t *blob; const float *dP; const float *X; float *part; int H, F; int N; int sp;
+  static constexpr bool COLSUM = true;
+  const uint8_t *blob; const float *dP; const float *X; float *part; int H, F; int N; float *cs_part; int sp;
+  __device__ void colsum(int m, int n0, float v) const {
+    if (n0 == 0) cs_part[(size_t)sp * H + m] = v;
+  }
   __device__ void prepare() { N = batch_N(blob); }
   __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) {
     const int nt = F / BN, mt = H / TC_BM;
@@ -924,20 +968,20 @@ void launch_tc_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ,
 }
 
 size_t tc_gram_partial_floats(const Caps &c, int cmax) {
-  return (size_t)tc_max_splits(c, cmax) * c.H * 4 * c.H;
+  return (size_t)tc_max_splits(c, cmax) * (c.H * 4 * c.H + c.H);
 }
 
 void launch_tc_dU_cls(cudaStream_t st, const Caps &c, int cmax, const uint8_t *blob, const float *dZ, const float *A,
                       const int *perm, const DegInfo *info, const int4 *splits, float *partial, float *dU,
                       float *dbU) {
   const int smax = tc_max_splits(c, cmax);
-  TcGramC op{dZ, A, perm, info, splits, partial, c.H, smax, 0, 0};
-  run_tc(st, op, (c.H / TC_BM) * (4 * c.H / TcGramC::BN) * smax);
   const int total = c.H * 4 * c.H;
+  float *cs = partial + (size_t)smax * total;  // per-split column sums of dZ (db_U)
+  TcGramC op{dZ, A, perm, info, splits, partial, c.H, smax, cs, 0, 0};
+  run_tc(st, op, (c.H / TC_BM) * (4 * c.H / TcGramC::BN) * smax);
   k_reduce_dU_classes<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(partial, info, splits, c.H, dU);
-  k_colsum_part<<<kColsumChunks, std::min(c.H, 256), 0, st>>>(blob, dZ, c.H, partial);
-  k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(partial, kColsumChunks, c.H, dbU);
-  g_launches += 4;
+  k_reduce_splits_rows<<<cdiv(c.H, 8), 256, 0, st>>>(cs, info, c.H, dbU);
+  g_launches += 2;
 }
 
 cudaError_t tc_configure() {
@@ -969,18 +1013,18 @@ void launch_tc_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const flo
 }
 
 size_t tc_dMx_partial_floats(const Caps &c, int F) {
-  return std::max((size_t)kTcDMxSplits * c.H * F, (size_t)kColsumChunks * c.H);
+  return (size_t)kTcDMxSplits * (c.H * F + c.H);
 }
 
 void launch_tc_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
                    float *partial, float *dMx, float *dbM) {
-  TcDMx op{blob, dP, X, partial, c.H, F, 0, 0};
-  run_tc(st, op, (c.H / TC_BM) * (F / TcDMx::BN) * kTcDMxSplits);
   const int count = c.H * F;
+  float *cs = partial + (size_t)kTcDMxSplits * count;  // per-split column sums of dP (db_M)
+  TcDMx op{blob, dP, X, partial, c.H, F, 0, cs, 0};
+  run_tc(st, op, (c.H / TC_BM) * (F / TcDMx::BN) * kTcDMxSplits);
   k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDMxSplits, count, dMx);
-  k_colsum_part<<<kColsumChunks, std::min(c.H, 256), 0, st>>>(blob, dP, c.H, partial);
-  k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(partial, kColsumChunks, c.H, dbM);
-  g_launches += 3;
+  k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(cs, kTcDMxSplits, c.H, dbM);
+  g_launches += 2;
 }
 
 }  // namespace hg
