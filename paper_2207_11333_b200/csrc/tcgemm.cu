@@ -33,6 +33,11 @@ namespace hg {
 
 extern std::atomic<int64_t> g_launches;
 
+// debug/experiment switch for the tcgen05 pipeline (0 = normal). 1: MMA issues no
+// tcgen05.mma (commits only); 2: transform does no LDS/split/STS; 3: loaders issue
+// no cp.async (arrive only). Results are wrong in modes 1-3: timing experiments only.
+__constant__ int g_tc_mode = 0;
+
 constexpr int TC_BM = 128;
 constexpr int TC_BK = 32;            // fp32 elements per 128-byte smem row
 constexpr int TC_XF_WARPS = 8;       // transform (+ epilogue) warps
@@ -182,7 +187,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
         const float *src;
         if constexpr (AMN) src = op.a_src(m0 + r, k0 + k, ke);
         else src = (arow[i] && k0 + k < ke) ? arow[i] + (k0 - kb) + k : nullptr;
-        tc::cp_async16(rA + off, src ? src : dummy, src ? 16u : 0u);
+        if (g_tc_mode != 3 && g_tc_mode != 4) tc::cp_async16(rA + off, src ? src : dummy, src ? 16u : 0u);
       }
 #pragma unroll
       for (int i = 0; i < NPB; ++i) {
@@ -194,7 +199,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
           const float *src;
           if constexpr (BMN) src = op.b_src(n0, r, k0 + k, ke);
           else src = (brow[i] && k0 + k < ke) ? brow[i] + (k0 - kb) + k : nullptr;
-          tc::cp_async16(rB + off, src ? src : dummy, src ? 16u : 0u);
+          if (g_tc_mode != 3 && g_tc_mode != 4) tc::cp_async16(rB + off, src ? src : dummy, src ? 16u : 0u);
         }
       }
       tc::cp_async_arrive(&rfull[rs]);
@@ -217,6 +222,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
       uint8_t *sBh = sAl + A_BYTES;
       uint8_t *sBl = sBh + B_BYTES;
       const int k0 = kb + c * TC_BK;
+      if (g_tc_mode != 2 && g_tc_mode != 4) {
 #pragma unroll 4
       for (int task = t; task < TC_BM * 8; task += NXF) {
         int r, j;
@@ -238,6 +244,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
         const uint32_t o = tc::sw128_off(r, j);
         *reinterpret_cast<float4 *>(sBh + o) = hi;
         *reinterpret_cast<float4 *>(sBl + o) = lo;
+      }
       }
       tc::mbar_arrive(&rempty[rs]);     // raw stage may be refilled
       tc::fence_proxy_async_smem();     // operand tiles -> visible to the tensor core
@@ -287,9 +294,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
           const uint32_t off = ks * 32;
           const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
           const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
-          tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
-          tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
-          tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+          if (g_tc_mode != 1 && g_tc_mode != 4) {
+            tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
+            tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
+            tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+          }
         }
         tc::mma_commit(&empty[s]);  // frees the stage when these MMAs have read it
       }
@@ -934,6 +943,12 @@ void launch_prep_UT(cudaStream_t st, const Caps &c, const float *params, const i
 }
 
 bool tc_supported(const Caps &c) { return c.H % 128 == 0; }
+
+}  // namespace hg
+extern "C" int hg_debug_set_tc_mode(int mode) {  // experiments only (not part of the ABI header)
+  return (int)cudaMemcpyToSymbol(hg::g_tc_mode, &mode, sizeof(int));
+}
+namespace hg {
 
 int tc_num_classes(const Caps &c, int max_degree) {
   const int cm = (max_degree > 0 ? max_degree : HG_MAX_DEGREE_DEV) + 1;
