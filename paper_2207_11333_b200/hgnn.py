@@ -388,17 +388,7 @@ class Context:
 
     def comm_init(self, rank: int, world: int, group=None):
         """Create the NCCL communicator; the 128-byte id travels over torch.distributed."""
-        import torch
-        import torch.distributed as dist
-        buf = np.zeros(128, np.uint8)
-        if world > 1:
-            if rank == 0:
-                _check(_lib.hg_nccl_unique_id(_ptr(buf)))
-            backend = dist.get_backend(group)
-            dev = f"cuda:{self.device}" if backend == "nccl" else "cpu"
-            t = torch.from_numpy(buf).to(dev)
-            dist.broadcast(t, src=0, group=group)
-            buf = t.cpu().numpy().copy()
+        buf = nccl_unique_id_broadcast(rank, world, group, device=self.device)
         _check(_lib.hg_comm_init(self.handle, _ptr(buf), rank, world))
 
     def allreduce_grads(self):
@@ -436,6 +426,24 @@ class Context:
         c = _I64()
         _check(_lib.hg_launch_count(self.handle, ctypes.byref(c)))
         return c.value
+
+
+def nccl_unique_id_broadcast(rank: int, world: int, group=None, device: int = 0) -> np.ndarray:
+    """Rank 0 creates the NCCL unique id (hg_nccl_unique_id); torch.distributed
+    broadcasts the 128 bytes to every rank (gloo: CPU tensor, nccl: CUDA tensor)."""
+    load()
+    buf = np.zeros(128, np.uint8)
+    if world <= 1:
+        return buf
+    import torch
+    import torch.distributed as dist
+    if rank == 0:
+        _check(_lib.hg_nccl_unique_id(_ptr(buf)))
+    backend = dist.get_backend(group)
+    dev = f"cuda:{device}" if backend == "nccl" else "cpu"
+    t = torch.from_numpy(buf).to(dev)
+    dist.broadcast(t, src=0, group=group)
+    return t.cpu().numpy().copy()
 
 
 # C-named module-level entry points (same names as include/hgnn.h)
