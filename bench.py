@@ -31,6 +31,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's own log lines (e.g. NCCL_DEBUG=VERSION) go to stderr: stdout carries ONE JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "train graphs/sec at 1/2/4/8 B200 (PCQM4Mv2-shaped); % HBM/tensor roofline"
 

@@ -113,6 +113,9 @@ struct hg_ctx {
   std::vector<hg_adamw> graph_hyper;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
+  cudaStream_t comm_stream = nullptr;           // bucketed allreduce overlapping the backward
+  std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
+  cudaEvent_t comm_done = nullptr;
   int64_t launches = 0;
   bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
   hg_status sticky = HG_OK;
@@ -203,6 +206,8 @@ void phase(Prof *pr, int ph, F &&fn) {
   pr->marks.push_back({ph, {a, b}});
 }
 
+hg_status enqueue_bucket(hg_ctx *x, cudaStream_t st, int b);
+
 // ---- the step's kernel sequence (enqueue only) ----
 void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool fuse_head_bwd = false) {
   const hg_config &c = x->cfg;
@@ -260,7 +265,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   });
 }
 
-void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false) {
+void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false,
+                      bool overlap_allreduce = false) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
@@ -271,6 +277,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
                     x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
                     x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), head_done);
   });
+  if (overlap_allreduce) enqueue_bucket(x, st, 0);
   const bool cls = x->use_tc && p.cmax > 0;
   const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
   const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
@@ -315,6 +322,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         launch_dMx(st, x->caps, blob, x->f(p.dP), Xl, F, x->f(p.part), x->grad(lname(l, "M_x")),
                    x->grad(lname(l, "b_M")));
     });
+    if (overlap_allreduce) enqueue_bucket(x, st, c.layers - l);  // conv l gradients complete
     if (l > 0) {
       phase(pr, HG_PHASE_DX, [&] {
         if (x->use_tc && F % 64 == 0)
@@ -325,6 +333,45 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       std::swap(dZ, dZn);
     }
   }
+}
+
+// gradient buckets in backward order: head first, then conv L-1 ... conv 0 (each a
+// contiguous range of the flat gradient arena)
+std::pair<int64_t, int64_t> bucket_range(hg_ctx *x, int b) {
+  const int L = x->cfg.layers;
+  auto off = [&](const std::string &name) {
+    for (auto &t : x->lay)
+      if (t.name == name) return t.offset;
+    return (int64_t)-1;
+  };
+  if (b == 0) return {off("head.W1"), x->n_params};
+  const int l = L - b;
+  const int64_t beg = off(lname(l, "M_x"));
+  const int64_t end = l + 1 < L ? off(lname(l + 1, "M_x")) : off("head.W1");
+  return {beg, end};
+}
+
+// enqueue the allreduce of bucket b on the comm stream once the compute stream reaches this point
+hg_status enqueue_bucket(hg_ctx *x, cudaStream_t st, int b) {
+  if (x->world <= 1 || !x->comm) return HG_OK;
+  auto r = bucket_range(x, b);
+  cudaError_t e;
+  if ((e = cudaEventRecord(x->bucket_ready[b], st)) != cudaSuccess) return cuda_fail(x, e, "cudaEventRecord");
+  if ((e = cudaStreamWaitEvent(x->comm_stream, x->bucket_ready[b], 0)) != cudaSuccess)
+    return cuda_fail(x, e, "cudaStreamWaitEvent");
+  float *g = x->f(x->plan.grads) + r.first;
+  ncclResult_t nr = ncclAllReduce(g, g, (size_t)(r.second - r.first), ncclFloat32, ncclAvg, x->comm, x->comm_stream);
+  if (nr != ncclSuccess) return nccl_fail(x, nr, "ncclAllReduce");
+  return HG_OK;
+}
+
+// join: the compute stream waits for every bucket's allreduce
+hg_status join_buckets(hg_ctx *x, cudaStream_t st) {
+  if (x->world <= 1 || !x->comm) return HG_OK;
+  cudaError_t e;
+  if ((e = cudaEventRecord(x->comm_done, x->comm_stream)) != cudaSuccess) return cuda_fail(x, e, "cudaEventRecord");
+  if ((e = cudaStreamWaitEvent(st, x->comm_done, 0)) != cudaSuccess) return cuda_fail(x, e, "cudaStreamWaitEvent");
+  return HG_OK;
 }
 
 hg_status enqueue_allreduce(hg_ctx *x, cudaStream_t st) {
@@ -432,6 +479,9 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
   if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
   if (x->comm) ncclCommDestroy(x->comm);
+  for (auto ev : x->bucket_ready) cudaEventDestroy(ev);
+  if (x->comm_done) cudaEventDestroy(x->comm_done);
+  if (x->comm_stream) cudaStreamDestroy(x->comm_stream);
   delete x;
   return HG_OK;
 }
@@ -628,6 +678,19 @@ hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world
   std::memcpy(&id, id128, sizeof(id));
   ncclResult_t r = ncclCommInitRank(&x->comm, world, id, rank);
   if (r != ncclSuccess) return nccl_fail(x, r, "ncclCommInitRank");
+  CK(x, cudaStreamCreateWithFlags(&x->comm_stream, cudaStreamNonBlocking));
+  for (int b = 0; b <= x->cfg.layers; ++b) {
+    cudaEvent_t ev;
+    CK(x, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    x->bucket_ready.push_back(ev);
+  }
+  CK(x, cudaEventCreateWithFlags(&x->comm_done, cudaEventDisableTiming));
+  // graphs captured before the communicator existed do not contain the allreduce
+  for (auto &g : x->graphs)
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
   return HG_OK;
 }
 
@@ -680,8 +743,8 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->cap_stream, slot, nullptr, true);
-  enqueue_backward(x, x->cap_stream, slot, nullptr, true);
-  hg_status ar = enqueue_allreduce(x, x->cap_stream);
+  enqueue_backward(x, x->cap_stream, slot, nullptr, true, true);  // bucketed, overlapped allreduce
+  hg_status ar = join_buckets(x, x->cap_stream);
   enqueue_step(x, x->cap_stream, *h);
   const int64_t nk = launches_so_far() - l0;
   cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
@@ -742,6 +805,7 @@ hg_status hg_sync(hg_ctx *x) {
   if (x->sticky != HG_OK) return fail(HG_E_STATE, "%s", x->sticky_msg.c_str());
   CK(x, cudaStreamSynchronize(x->stream));
   CK(x, cudaStreamSynchronize(x->copy_stream));
+  if (x->comm_stream) CK(x, cudaStreamSynchronize(x->comm_stream));
   if (x->comm) {
     ncclResult_t ar;
     ncclResult_t r = ncclCommGetAsyncError(x->comm, &ar);
