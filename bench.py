@@ -185,6 +185,12 @@ def main():
     if args.impl == "reference":
         return run_reference(args, rank, world, preset, n_graphs, B, H, L, desc)
 
+    # stdout carries exactly ONE JSON line: anything libraries print while we run
+    # (e.g. "NCCL version ...") is routed to stderr until the result is printed
+    sys.stdout.flush()
+    saved_stdout = os.dup(1)
+    os.dup2(2, 1)
+
     import torch
     import torch.distributed as dist
     import molgen
@@ -399,8 +405,11 @@ def main():
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
         "loss_after_timed": loss_now,
     }
+    sys.stdout.flush()
+    os.dup2(saved_stdout, 1)
     if rank == 0:
         print(json.dumps(out), flush=True)
+    os.dup2(2, 1)
     barrier()
     if world > 1:
         dist.destroy_process_group()
