@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
         float4 lo;
         const float4 av = op.a_fix(read_raw<AMN, TC_BM>(rA, r, j), m0 + r, k0 + 4 * j, ke);
         if constexpr (Op::COLSUM) csum += (av.x + av.y) + (av.z + av.w);
-        const float4 hi = split_hi(av, lo);
+        const float4 hi = g_tc_mode == 5 ? (split_hi(av, lo), av) : split_hi(av, lo);
         const uint32_t o = tc::sw128_off(r, j);
         *reinterpret_cast<float4 *>(sAh + o) = hi;
         *reinterpret_cast<float4 *>(sAl + o) = lo;
