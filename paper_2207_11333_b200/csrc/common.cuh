@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "layout.h"
 
 namespace hg {
@@ -37,6 +39,36 @@ __device__ __forceinline__ BatchView load_batch(const uint8_t *blob) {
 __device__ __forceinline__ int batch_N(const uint8_t *blob) { return reinterpret_cast<const int *>(blob)[1]; }
 
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+// ------------------------------------------------ programmatic dependent launch
+// Every kernel of the step is launched with programmatic stream serialization:
+// its CTAs may become resident while the previous kernel is still running, and
+// each kernel starts with pdl_enter(), which blocks until the previous grid has
+// completed and flushed its writes (griddepcontrol.wait), then lets the next
+// kernel begin launching (griddepcontrol.launch_dependents). Because EVERY
+// kernel waits before touching global memory, completion of kernel k implies
+// completion of all kernels before it, so stream order is preserved
+// transitively; the gain is that launch latency overlaps the previous kernel.
+extern bool g_pdl;
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                             Args &&...args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 constexpr int kSMs = 148;
 
 

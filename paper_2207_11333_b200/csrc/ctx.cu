@@ -6,6 +6,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -30,7 +31,10 @@ struct Plan {
   size_t part = 0;
   size_t UT = 0, u_off = 0;
   int cmax = 0;  // degree-class slots (0 = class GEMMs off)
-  size_t perm = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
+  size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
+  // direct-GEMM residuals x - trunc19(x) (class path): operands and weights
+  size_t A_lo = 0, X_lo = 0, dZa_lo = 0, dZb_lo = 0, dP_lo = 0, Wf_lo = 0, WbT_lo = 0;
+  size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t total = 0;
 };
 
@@ -82,12 +86,24 @@ Plan make_plan(const hg_config &c) {
   p.UT = take(p.cmax ? 256 : sizeof(float) * (size_t)c.layers * 12 * H * H);
   p.u_off = take(sizeof(int64_t) * (size_t)c.layers);
   p.perm = take(sizeof(int) * N);
+  p.pos = take(sizeof(int) * N);
   p.deginfo = take(sizeof(DegInfo));
   if (p.cmax) {
     p.tiles = take(sizeof(int4) * (size_t)tc_max_tiles(caps, p.cmax));
     p.splits = take(sizeof(int4) * (size_t)tc_max_splits(caps, p.cmax));
     p.Wf = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
     p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+    p.Wf_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+    p.WbT_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+    p.A_lo = take(sizeof(float) * N * 4 * H);
+    p.X_lo = take(sizeof(float) * N * H);
+    p.dZa_lo = take(sizeof(float) * N * H);
+    p.dZb_lo = take(sizeof(float) * N * H);
+    p.dP_lo = take(sizeof(float) * N * H);
+    p.Mx_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
+    p.MxT = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
+    p.MxT_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
+    p.mx_off = take(sizeof(int64_t) * (size_t)c.layers);
     pf = std::max(pf, tc_gram_partial_floats(caps, p.cmax));
     p.part = take(sizeof(float) * pf);  // (re-take: the class partials are larger)
   }
@@ -217,34 +233,42 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   phase(pr, HG_PHASE_SCALERS, [&] {
     launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
                    reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
-                   reinterpret_cast<int4 *>(x->b(p.splits)));
+                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)));
   });
   const bool cls = x->use_tc && p.cmax > 0;
+  const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
+  const size_t HH = (size_t)c.hidden * c.hidden;
   if (cls)
     phase(pr, HG_PHASE_UPDATE, [&] {
-      launch_prep_W(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
-                    reinterpret_cast<const DegInfo *>(x->b(p.deginfo)), x->f(p.Wf), x->f(p.WbT));
+      launch_prep_W2(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
+                     reinterpret_cast<const DegInfo *>(x->b(p.deginfo)), x->f(p.Wf), x->f(p.Wf_lo), x->f(p.WbT),
+                     x->f(p.WbT_lo));
+      launch_prep_Mx(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
+                     x->f(p.Mx_lo), x->f(p.MxT), x->f(p.MxT_lo));
     });
   for (int l = 0; l < c.layers; ++l) {
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
     phase(pr, HG_PHASE_PROJ, [&] {
-      if (x->use_tc && l > 0 && tc_proj_ok(x->caps, F))
+      if (cls && l > 0)
+        launch_d_proj(st, x->caps, blob, Xl, x->f(p.X_lo), F, x->param(lname(l, "M_x")),
+                      x->f(p.Mx_lo) + (size_t)(l - 1) * HH, x->f(p.P[l]));
+      else if (x->use_tc && l > 0 && tc_proj_ok(x->caps, F))
         launch_tc_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
       else
         launch_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
     });
     phase(pr, HG_PHASE_AGG_FWD, [&] {
       launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]));
+                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), cls ? x->f(p.A_lo) : nullptr, pos);
     });
     phase(pr, HG_PHASE_UPDATE, [&] {
       if (cls)
-        launch_tc_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), reinterpret_cast<const int *>(x->b(p.perm)),
-                             reinterpret_cast<const DegInfo *>(x->b(p.deginfo)),
-                             reinterpret_cast<const int4 *>(x->b(p.tiles)),
-                             x->f(p.Wf) + (size_t)l * p.cmax * c.hidden * 4 * c.hidden, x->param(lname(l, "b_U")),
-                             x->f(p.X[l]));
+        launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), x->f(p.A_lo), reinterpret_cast<const int *>(x->b(p.perm)),
+                            reinterpret_cast<const DegInfo *>(x->b(p.deginfo)),
+                            reinterpret_cast<const int4 *>(x->b(p.tiles)),
+                            x->f(p.Wf) + (size_t)l * p.cmax * 4 * HH, x->f(p.Wf_lo) + (size_t)l * p.cmax * 4 * HH,
+                            x->param(lname(l, "b_U")), x->f(p.X[l]), x->f(p.X_lo));
       else if (x->use_tc)
         launch_tc_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")),
                          x->param(lname(l, "b_U")), x->f(p.X[l]));
@@ -257,7 +281,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     if (fuse_head_bwd)
       launch_head_fused(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
                         x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
-                        x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZa));
+                        x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZa),
+                        cls ? x->f(p.dZa_lo) : nullptr, pos);
     else
       launch_head_fwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
                       x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
@@ -272,13 +297,16 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   const uint8_t *blob = x->b(p.slot[slot]);
   float *amp = x->f(p.amp), *att = x->f(p.att);
   float *dZ = x->f(p.dZa), *dZn = x->f(p.dZb);
+  const bool cls = x->use_tc && p.cmax > 0;
+  float *dZl = cls ? x->f(p.dZa_lo) : nullptr, *dZnl = cls ? x->f(p.dZb_lo) : nullptr;
+  const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
+  const size_t HH = (size_t)c.hidden * c.hidden;
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
     launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"), x->f(p.G),
                     x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
-                    x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), head_done);
+                    x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), head_done, dZl, pos);
   });
   if (overlap_allreduce) enqueue_bucket(x, st, 0);
-  const bool cls = x->use_tc && p.cmax > 0;
   const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
   const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
   if (x->use_tc && !cls)
@@ -289,8 +317,9 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   for (int l = c.layers - 1; l >= 0; --l) {
     phase(pr, HG_PHASE_DA, [&] {
       if (cls)
-        launch_tc_dA_cls(st, x->caps, p.cmax, dZ, perm, dinfo, reinterpret_cast<const int4 *>(x->b(p.tiles)),
-                         x->f(p.WbT) + (size_t)l * p.cmax * c.hidden * 4 * c.hidden, x->f(p.dA));
+        launch_d_dA_cls(st, x->caps, p.cmax, dZ, dZl, perm, dinfo, reinterpret_cast<const int4 *>(x->b(p.tiles)),
+                        x->f(p.WbT) + (size_t)l * p.cmax * 4 * HH, x->f(p.WbT_lo) + (size_t)l * p.cmax * 4 * HH,
+                        x->f(p.dA));
       else if (x->use_tc)
         launch_tc_dA(st, x->caps, blob, dZ, amp, att, x->f(p.UT) + (size_t)l * 12 * c.hidden * c.hidden, x->f(p.dA));
       else
@@ -298,7 +327,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     });
     phase(pr, HG_PHASE_DU, [&] {
       if (cls)
-        launch_tc_dU_cls(st, x->caps, p.cmax, blob, dZ, x->f(p.A[l]), perm, dinfo,
+        launch_tc_dU_cls(st, x->caps, p.cmax, blob, dZ, x->f(p.A[l]), nullptr /* rows pre-sorted */, dinfo,
                          reinterpret_cast<const int4 *>(x->b(p.splits)), x->f(p.part), x->grad(lname(l, "U")),
                          x->grad(lname(l, "b_U")));
       else if (x->use_tc)
@@ -310,7 +339,8 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), x->f(p.dP), x->f(p.part), x->grad(lname(l, "M_e")));
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), x->f(p.dP), x->f(p.part), x->grad(lname(l, "M_e")),
+                     cls && l > 0 ? x->f(p.dP_lo) : nullptr, pos);
     });
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
@@ -325,12 +355,16 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     if (overlap_allreduce) enqueue_bucket(x, st, c.layers - l);  // conv l gradients complete
     if (l > 0) {
       phase(pr, HG_PHASE_DX, [&] {
-        if (x->use_tc && F % 64 == 0)
+        if (cls)
+          launch_d_dX(st, x->caps, blob, x->f(p.dP), x->f(p.dP_lo), x->f(p.MxT) + (size_t)(l - 1) * HH,
+                      x->f(p.MxT_lo) + (size_t)(l - 1) * HH, F, Xl, dZn, dZnl, pos);
+        else if (x->use_tc && F % 64 == 0)
           launch_tc_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn);
         else
           launch_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn);
       });
       std::swap(dZ, dZn);
+      std::swap(dZl, dZnl);
     }
   }
 }
@@ -454,6 +488,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   x->use_tc = tc_supported(x->caps) && !(c->flags & HG_FLAG_SIMT_GEMM);
   head_configure(x->caps);
   if (x->use_tc && (e = tc_configure()) != cudaSuccess) return bail(e, "tc_configure");
+  if (x->use_tc && (e = tcd_configure()) != cudaSuccess) return bail(e, "tcd_configure");
+  if (const char *pe = getenv("HG_PDL")) g_pdl = atoi(pe) != 0;  // A/B switch for launch overlap
   {
     std::vector<int64_t> uo;
     for (int l = 0; l < c->layers; ++l)
@@ -462,6 +498,16 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     if ((e = cudaMemcpyAsync(x->b(plan.u_off), uo.data(), sizeof(int64_t) * uo.size(), cudaMemcpyHostToDevice,
                              x->stream)) != cudaSuccess)
       return bail(e, "cudaMemcpyAsync");
+    if (plan.mx_off) {
+      std::vector<int64_t> mo;
+      for (int l = 0; l < c->layers; ++l)
+        for (auto &t : x->lay)
+          if (t.name == lname(l, "M_x")) mo.push_back(t.offset);
+      if ((e = cudaMemcpyAsync(x->b(plan.mx_off), mo.data(), sizeof(int64_t) * mo.size(), cudaMemcpyHostToDevice,
+                               x->stream)) != cudaSuccess)
+        return bail(e, "cudaMemcpyAsync");
+    }
+    if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
   }
   if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
   *out = x;

@@ -25,6 +25,7 @@
 namespace hg {
 
 std::atomic<int64_t> g_launches{0};
+bool g_pdl = true;
 static inline void counted(int n = 1) { g_launches += n; }
 
 // ------------------------------------------------------------------ scalers
@@ -32,6 +33,7 @@ static inline void counted(int n = 1) { g_launches += n; }
 // (SURVEY C4-C5). Computed in double, stored fp32.
 __global__ void k_scalers(const uint8_t *__restrict__ blob, double delta, float *__restrict__ amp,
                           float *__restrict__ att) {
+  pdl_enter();
   const BatchView b = load_batch(blob);
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < b.N; i += gridDim.x * blockDim.x) {
     const int d = b.rowptr[i + 1] - b.rowptr[i];
@@ -48,7 +50,7 @@ __global__ void k_scalers(const uint8_t *__restrict__ blob, double delta, float 
 
 void launch_scalers(cudaStream_t st, const Caps &c, const uint8_t *blob, double delta, float *amp, float *att) {
   const int blocks = std::min(cdiv(c.maxN, 256), kSMs * 4);
-  k_scalers<<<blocks, 256, 0, st>>>(blob, delta, amp, att);
+  launch_ex(k_scalers, blocks, 256, 0, st, blob, delta, amp, att);
   counted();
 }
 
@@ -61,6 +63,7 @@ constexpr int GBM = 64, GBN = 64, GBK = 16;
 
 template <bool A_KMAJ, bool B_KMAJ, class Op>
 __global__ void __launch_bounds__(256) k_gemm(Op op_in) {
+  pdl_enter();
   Op op = op_in;
   op.prepare();
   __shared__ __align__(16) float As[2][GBK][GBM + 4];
@@ -153,7 +156,7 @@ template <bool AK, bool BK_, class Op>
 static void run_gemm(cudaStream_t st, const Op &op, int maxM, int N, int splits) {
   const int tiles = cdiv(maxM, GBM) * cdiv(N, GBN) * splits;
   const int grid = std::max(1, std::min(tiles, kSMs * 8));
-  k_gemm<AK, BK_, Op><<<grid, 256, 0, st>>>(op);
+  launch_ex(k_gemm<AK, BK_, Op>, grid, 256, 0, st, op);
   counted();
 }
 
@@ -229,6 +232,7 @@ void launch_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float 
 // split-K partial reduction in fixed split order; column Nc-1 of each row is the bias gradient
 __global__ void k_reduce_split(const float *__restrict__ part, int splits, int Mr, int Nc, float *__restrict__ outW,
                                float *__restrict__ outB) {
+  pdl_enter();
   const int total = Mr * Nc;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
     float s = 0.f;
@@ -266,7 +270,7 @@ void launch_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float 
   OpDU op{blob, dZ, A, amp, att, partial, c.H};
   run_gemm<false, false>(st, op, c.H, 12 * c.H + 1, kDUSplits);
   const int total = c.H * (12 * c.H + 1);
-  k_reduce_split<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(partial, kDUSplits, c.H, 12 * c.H + 1, dU, dbU);
+  launch_ex(k_reduce_split, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, kDUSplits, c.H, 12 * c.H + 1, dU, dbU);
   counted();
 }
 
@@ -290,7 +294,7 @@ void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float
   OpDMx op{blob, dP, X, partial, c.H, F};
   run_gemm<false, false>(st, op, c.H, F + 1, kDMxSplits);
   const int total = c.H * (F + 1);
-  k_reduce_split<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(partial, kDMxSplits, c.H, F + 1, dMx, dbM);
+  launch_ex(k_reduce_split, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, kDMxSplits, c.H, F + 1, dMx, dbM);
   counted();
 }
 
@@ -359,6 +363,17 @@ __device__ __forceinline__ void load_edge(const float *ea, int Fe, int k, float 
   }
 }
 
+// 3xTF32 residual of a value (x - x with the 13 low mantissa bits cleared): written next
+// to operands the direct tensor-core GEMMs consume (tcdirect.cu)
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+template <int CPL>
+__device__ __forceinline__ void store_vec_lo(float *p, const float (&v)[CPL]) {
+  float l[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) l[c] = tf32_lo(v[c]);
+  store_vec<CPL>(p, l);
+}
+
 // message for CPL channels: m = (P + b_M) + sum_f M_e[:,f] e_f  (same order in K2 and K8)
 template <int CPL, int FE>
 __device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm)[CPL], const float (&me)[CPL][FE],
@@ -376,7 +391,9 @@ template <int CPL, int FE>
 __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
                                                     const float *__restrict__ Me, const float *__restrict__ bM,
                                                     float var_floor, float *__restrict__ A,
-                                                    uint8_t *__restrict__ arg, int H) {
+                                                    uint8_t *__restrict__ arg, int H, float *__restrict__ A_lo,
+                                                    const int *__restrict__ pos) {
+  pdl_enter();
   const BatchView b = load_batch(blob);
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
@@ -438,11 +455,19 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
         sd[c] = sqrtf(fmaxf(var, var_floor));
       }
     }
-    float *Ai = A + (size_t)i * 4 * H + ch;
+    const size_t arow = (size_t)(pos ? pos[i] : i) * 4 * H + ch;  // degree-sorted row when pos is given
+    float *Ai = A + arow;
     store_vec<CPL>(Ai, mean);
     store_vec<CPL>(Ai + H, mn);
     store_vec<CPL>(Ai + 2 * H, mx);
     store_vec<CPL>(Ai + 3 * H, sd);
+    if (A_lo) {
+      float *Li = A_lo + arow;
+      store_vec_lo<CPL>(Li, mean);
+      store_vec_lo<CPL>(Li + H, mn);
+      store_vec_lo<CPL>(Li + 2 * H, mx);
+      store_vec_lo<CPL>(Li + 3 * H, sd);
+    }
     uint8_t *ai = arg + (size_t)i * 2 * H + ch;
     if constexpr (CPL == 4) {
       *reinterpret_cast<uchar4 *>(ai) = make_uchar4(amn[0], amn[1], amn[2], amn[3]);
@@ -465,18 +490,18 @@ static int agg_cpl(int H) { return (H % 64 == 0) ? 2 : 1; }
 
 template <int CPL, int FE>
 static void agg_fwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                           const float *bM, float var_floor, float *A, uint8_t *arg) {
+                           const float *bM, float var_floor, float *A, uint8_t *arg, float *A_lo, const int *pos) {
   const dim3 grid(std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 4)), c.H / (32 * CPL));
-  k_agg_fwd<CPL, FE><<<grid, 256, 0, st>>>(blob, P, Me, bM, var_floor, A, arg, c.H);
+  launch_ex(k_agg_fwd<CPL, FE>, grid, 256, 0, st, blob, P, Me, bM, var_floor, A, arg, c.H, A_lo, pos);
 }
 
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, float var_floor, float *A, uint8_t *arg) {
+                    const float *bM, float var_floor, float *A, uint8_t *arg, float *A_lo, const int *pos) {
   const int cpl = agg_cpl(c.H);
-  if (cpl == 2 && c.Fe == 4) agg_fwd_launch<2, 4>(st, c, blob, P, Me, bM, var_floor, A, arg);
-  else if (cpl == 2) agg_fwd_launch<2, 8>(st, c, blob, P, Me, bM, var_floor, A, arg);
-  else if (c.Fe == 4) agg_fwd_launch<1, 4>(st, c, blob, P, Me, bM, var_floor, A, arg);
-  else agg_fwd_launch<1, 8>(st, c, blob, P, Me, bM, var_floor, A, arg);
+  if (cpl == 2 && c.Fe == 4) agg_fwd_launch<2, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
+  else if (cpl == 2) agg_fwd_launch<2, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
+  else if (c.Fe == 4) agg_fwd_launch<1, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
+  else agg_fwd_launch<1, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
   counted();
 }
 
@@ -495,7 +520,9 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
                                                     const float *__restrict__ Me, const float *__restrict__ bM,
                                                     const float *__restrict__ A, const uint8_t *__restrict__ arg,
                                                     const float *__restrict__ dA, float *__restrict__ dP,
-                                                    float *__restrict__ partial, int H) {
+                                                    float *__restrict__ partial, int H, float *__restrict__ dP_lo,
+                                                    const int *__restrict__ pos) {
+  pdl_enter();
   __shared__ float red[kAggBwdWarps][32][CPL * FE];
   const BatchView b = load_batch(blob);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -525,7 +552,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
       float m[CPL];
       message<CPL, FE>(pj, bm, me, ef, m);
       const float *dAi = dA + (size_t)i * 4 * H + ch;
-      const float *Ai = A + (size_t)i * 4 * H + ch;
+      const float *Ai = A + (size_t)(pos ? pos[i] : i) * 4 * H + ch;
       float gmean[CPL], gmin[CPL], gmax[CPL], gstd[CPL], mu[CPL], sg[CPL];
       load_vec<CPL>(dAi, gmean);
       load_vec<CPL>(dAi + H, gmin);
@@ -561,6 +588,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
       }
     }
     store_vec<CPL>(dP + (size_t)j * H + ch, dp);
+    if (dP_lo) store_vec_lo<CPL>(dP_lo + (size_t)j * H + ch, dp);
   }
   // block reduction of dM_e partials in fixed warp order
 #pragma unroll
@@ -582,6 +610,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
 // fixed-order reduction of nparts partial vectors: one warp per output element;
 // lanes stride over the parts, then a fixed xor-shuffle tree (deterministic)
 __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
+  pdl_enter();
   const int lane = threadIdx.x & 31;
   const int wpb = blockDim.x >> 5;
   for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < count; e += gridDim.x * wpb) {
@@ -599,22 +628,23 @@ size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) 
 template <int CPL, int FE>
 static void agg_bwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                            const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                           float *partial) {
+                           float *partial, float *dP_lo, const int *pos) {
   const dim3 grid(agg_bwd_blocks(c), c.H / (32 * CPL));
-  k_agg_bwd<CPL, FE><<<grid, 32 * kAggBwdWarps, 0, st>>>(blob, P, Me, bM, A, arg, dA, dP, partial, c.H);
+  launch_ex(k_agg_bwd<CPL, FE>, grid, 32 * kAggBwdWarps, 0, st, blob, P, Me, bM, A, arg, dA, dP, partial, c.H, dP_lo,
+            pos);
 }
 
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe) {
+                    float *partial, float *dMe, float *dP_lo, const int *pos) {
   const int cpl = agg_cpl(c.H);
-  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
-  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
-  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
-  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial);
+  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
+  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
+  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
+  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
   counted();
   const int count = c.H * c.Fe;
-  k_reduce_rows<<<std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st>>>(partial, agg_bwd_blocks(c), count, dMe);
+  launch_ex(k_reduce_rows, std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st, partial, agg_bwd_blocks(c), count, dMe);
   counted();
 }
 
@@ -647,7 +677,9 @@ __global__ void __launch_bounds__(256) k_head(const uint8_t *__restrict__ blob, 
                                               float *__restrict__ G, float *__restrict__ hpre,
                                               float *__restrict__ yhat, float *__restrict__ sqerr,
                                               float *__restrict__ dy, float *__restrict__ dhid,
-                                              float *__restrict__ dZL, int H, int Hf, int w1_in_smem) {
+                                              float *__restrict__ dZL, int H, int Hf, int w1_in_smem,
+                                              float *__restrict__ dZL_lo, const int *__restrict__ pos) {
+  pdl_enter();
   extern __shared__ float sm[];
   float *Gs = sm, *hs = Gs + H, *dh = hs + Hf, *red = dh + Hf, *W1s = red + 256;
   const float *Wr = W1;
@@ -727,7 +759,10 @@ __global__ void __launch_bounds__(256) k_head(const uint8_t *__restrict__ blob, 
       for (int e = threadIdx.x; e < (n1 - n0) * H; e += blockDim.x) {
         const int i = n0 + e / H, c = e % H;
         const size_t o = (size_t)i * H + c;
-        dZL[o] = XL[o] > 0.f ? Gs[c] : 0.f;
+        const float v = XL[o] > 0.f ? Gs[c] : 0.f;
+        const size_t od = pos ? (size_t)pos[i] * H + c : o;  // degree-sorted row when pos is given
+        dZL[od] = v;
+        if (dZL_lo) dZL_lo[od] = tf32_lo(v);
       }
     }
     __syncthreads();
@@ -736,6 +771,7 @@ __global__ void __launch_bounds__(256) k_head(const uint8_t *__restrict__ blob, 
 
 __global__ void __launch_bounds__(256) k_loss(const uint8_t *__restrict__ blob, const float *__restrict__ sqerr,
                                               float *__restrict__ loss) {
+  pdl_enter();
   __shared__ float red[256];
   const BatchView b = load_batch(blob);
   float part = 0.f;
@@ -747,13 +783,14 @@ __global__ void __launch_bounds__(256) k_loss(const uint8_t *__restrict__ blob, 
 template <bool FWD, bool BWD>
 static void head_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                         const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
-                        float *sqerr, float *dy, float *dhid, float *dZL) {
+                        float *sqerr, float *dy, float *dhid, float *dZL, float *dZL_lo = nullptr,
+                        const int *pos = nullptr) {
   const size_t base = sizeof(float) * (c.H + 2 * c.Hf + 256);
   const size_t w1 = sizeof(float) * (size_t)c.Hf * c.H;
   const int in_smem = base + w1 <= 200 * 1024 ? 1 : 0;  // attribute set once by head_configure
   const size_t smem = base + (in_smem ? w1 : 0);
-  k_head<FWD, BWD><<<std::min(c.maxB, kSMs), 256, smem, st>>>(blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
-                                                               dhid, dZL, c.H, c.Hf, in_smem);
+  launch_ex(k_head<FWD, BWD>, std::min(c.maxB, kSMs), 256, smem, st, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
+            dhid, dZL, c.H, c.Hf, in_smem, dZL_lo, pos);
 }
 
 void head_configure(const Caps &c) {  // outside graph capture: opt into large dynamic smem
@@ -770,16 +807,17 @@ void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const 
                      float *sqerr, float *loss) {
   head_launch<true, false>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, nullptr, nullptr, nullptr);
   counted();
-  k_loss<<<1, 256, 0, st>>>(blob, sqerr, loss);
+  launch_ex(k_loss, 1, 256, 0, st, blob, sqerr, loss);
   counted();
 }
 
 void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                        const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
-                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL) {
-  head_launch<true, true>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy, dhid, dZL);
+                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL, float *dZL_lo,
+                       const int *pos) {
+  head_launch<true, true>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy, dhid, dZL, dZL_lo, pos);
   counted();
-  k_loss<<<1, 256, 0, st>>>(blob, sqerr, loss);
+  launch_ex(k_loss, 1, 256, 0, st, blob, sqerr, loss);
   counted();
 }
 
@@ -788,6 +826,7 @@ __global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__re
                              const float *__restrict__ hpre, const float *__restrict__ dy,
                              const float *__restrict__ dhid, float *__restrict__ gW1, float *__restrict__ gb1,
                              float *__restrict__ gW2, float *__restrict__ gb2, int H, int Hf) {
+  pdl_enter();
   const int B = reinterpret_cast<const int *>(blob)[0];
   const int nW1 = Hf * H;
   const int total = nW1 + 2 * Hf + 1;
@@ -814,14 +853,15 @@ __global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__re
 
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
-                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done) {
+                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done,
+                     float *dZL_lo, const int *pos) {
   if (!head_done) {
     head_launch<false, true>(st, c, blob, XL, W1, nullptr, W2, nullptr, nullptr, const_cast<float *>(hpre),
-                             const_cast<float *>(yhat), nullptr, dy, dhid, dZL);
+                             const_cast<float *>(yhat), nullptr, dy, dhid, dZL, dZL_lo, pos);
     counted();
   }
   const int total = c.Hf * c.H + 2 * c.Hf + 1;
-  k_head_grads<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2,
+  launch_ex(k_head_grads, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2,
                                                                        c.H, c.Hf);
   counted();
 }
@@ -830,6 +870,7 @@ void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const 
 // theta <- theta (1 - lr wd); m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2;
 // theta <- theta - (lr/bc1) m / (sqrt(v)/sqrt(bc2) + eps)
 __global__ void k_adam_prep(AdamDev *ad, float lr, float beta1, float beta2) {
+  pdl_enter();
   const int64_t t = ad->step + 1;
   ad->step = t;
   const double bc1 = 1.0 - pow((double)beta1, (double)t);
@@ -842,6 +883,7 @@ __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const flo
                                                float4 *__restrict__ m, float4 *__restrict__ v, int64_t n4,
                                                const AdamDev *__restrict__ ad, float lr, float beta1,
                                                float beta2, float eps, float wd) {
+  pdl_enter();
   const float ss = ad->step_size, ib = ad->inv_sqrt_bc2;
   const float decay = 1.0f - lr * wd;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
@@ -861,11 +903,11 @@ __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const flo
 
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
                   float lr, float beta1, float beta2, float eps, float wd) {
-  k_adam_prep<<<1, 1, 0, st>>>(ad, lr, beta1, beta2);
+  launch_ex(k_adam_prep, 1, 1, 0, st, ad, lr, beta1, beta2);
   counted();
   const int64_t n4 = n / 4;
   const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, kSMs * 8);
-  k_adamw<<<blocks, 256, 0, st>>>(reinterpret_cast<float4 *>(p), reinterpret_cast<const float4 *>(g),
+  launch_ex(k_adamw, blocks, 256, 0, st, reinterpret_cast<float4 *>(p), reinterpret_cast<const float4 *>(g),
                                   reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, ad, lr, beta1,
                                   beta2, eps, wd);
   counted();

@@ -7,6 +7,7 @@
 #include <stdint.h>
 
 namespace hg {
+extern bool g_pdl;  // launch kernels with programmatic dependent launch (common.cuh)
 
 struct Caps {
   int maxB, maxN, maxE;
@@ -37,11 +38,12 @@ void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float 
 
 // K2: fused edge gather + message + mean/min/max/std segmented reduction
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, float var_floor, float *A, uint8_t *arg);
+                    const float *bM, float var_floor, float *A, uint8_t *arg, float *A_lo = nullptr,
+                    const int *pos = nullptr);  // pos: write A row i at pos[i] (degree-sorted)
 // K8: aggregation backward + scatter to sources; dM_e via block partials
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe);
+                    float *partial, float *dMe, float *dP_lo = nullptr, const int *pos = nullptr);
 size_t agg_bwd_partial_floats(const Caps &c);
 size_t dU_partial_floats(const Caps &c);
 size_t dMx_partial_floats(const Caps &c, int F);
@@ -54,11 +56,13 @@ void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const 
 // backward down to dZ of the last layer
 void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                        const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
-                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL);
+                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL, float *dZL_lo = nullptr,
+                       const int *pos = nullptr);
 // K6: head + pool backward -> dZ of the last layer (skipped if head_done), then head parameter gradients
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
-                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done);
+                     float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done,
+                     float *dZL_lo = nullptr, const int *pos = nullptr);
 void head_configure(const Caps &c);
 
 // K10: AdamW over the flat arena
@@ -82,8 +86,9 @@ int tc_num_classes(const Caps &c, int max_degree);  // class slots (max_degree+1
 int tc_max_tiles(const Caps &c, int cmax);
 int tc_max_splits(const Caps &c, int cmax);
 // stable degree sort + per-node scalers (+ class table / tiles / splits when cmax > 0)
+// perm[r] = node at degree-sorted row r, pos = its inverse (pos may be null)
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
-                    DegInfo *info, int4 *tiles, int4 *splits);
+                    DegInfo *info, int4 *tiles, int4 *splits, int *pos = nullptr);
 void launch_prep_W(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
                    const DegInfo *info, float *Wf, float *WbT);
 void launch_tc_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm,
@@ -94,6 +99,24 @@ size_t tc_gram_partial_floats(const Caps &c, int cmax);
 void launch_tc_dU_cls(cudaStream_t st, const Caps &c, int cmax, const uint8_t *blob, const float *dZ, const float *A,
                       const int *perm, const DegInfo *info, const int4 *splits, float *partial, float *dU,
                       float *dbU);
+
+// TMA-fed tcgen05 GEMMs over pre-split operands (tcdirect.cu). A / dZ operands of
+// the class GEMMs are stored in degree-sorted row order (row pos[i] for node i).
+cudaError_t tcd_configure();
+void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
+                         const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
+                         float *X1, float *X1_lo);
+void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
+                     const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA);
+void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
+                   const float *Mx, const float *Mx_lo, float *P);
+void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
+                 const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
+                 const int *pos);
+void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,
+                    float *Mx_lo, float *MxT, float *MxT_lo);
+void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
+                    const DegInfo *info, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo);
 
 // tcgen05 3xTF32 GEMMs (tcgemm.cu); require H % 128 == 0
 bool tc_supported(const Caps &c);

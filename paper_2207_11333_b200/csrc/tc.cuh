@@ -139,6 +139,24 @@ __device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// ---------------------------------------------------------------- TMA
+// expect `bytes` of async-proxy transactions on `bar` and arrive once
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+// 2D tiled bulk tensor copy global -> shared (box per the tensor map), completion
+// counted in bytes on `bar`; x = innermost (element) coordinate, y = row
+__device__ __forceinline__ void tma_load_2d(void *dst, const void *tmap, int x, int y, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(smem_u32(dst)),
+      "l"(tmap), "r"(x), "r"(y), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void *tmap) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
+}
+
 // 3xTF32 split: hi keeps the 10 explicit mantissa bits TF32 uses, lo = x - hi (exact)
 __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);

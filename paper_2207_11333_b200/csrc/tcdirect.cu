@@ -1,0 +1,533 @@
+// tcdirect.cu — TMA-fed fp32-accurate tensor-core GEMM for K-major operands.
+//
+// The tf32 MMA reads the top 19 bits of each 32-bit operand (measured on B200:
+// feeding raw fp32 as the 3xTF32 "hi" term is bitwise identical to feeding the
+// explicitly truncated value, tools/exp_tf32_trunc.py). So an operand x is used
+// as-is for the hi term, and its producer also writes x_lo = x - trunc19(x)
+// (tc::split_tf32). With both terms already in global memory, and every operand
+// row-contiguous (class GEMM operands are stored in degree-sorted row order),
+// each K-chunk of a tile is four plain 2-D TMA boxes:
+//   warps 0-3  epilogue (TMEM lanes 0..127 -> registers -> global)
+//   warp 4     one thread: cp.async.bulk.tensor of A, A_lo (128 x 32 fp32) and
+//              B, B_lo (BN x 32) into SWIZZLE_128B stages, completion counted
+//              in bytes on the stage's mbarrier
+//   warp 5     TMEM allocation + single-thread tcgen05.mma issue:
+//              D += Ah*Bh + Ah*Bl + Al*Bh per K=8 step (3xTF32)
+// One 128-row x BN output tile per CTA. The prologue (barrier init, TMEM
+// allocation, descriptor prefetch) runs before griddepcontrol.wait, so under
+// programmatic dependent launch it overlaps the previous kernel.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+
+#include <algorithm>
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace hg {
+
+extern std::atomic<int64_t> g_launches;
+int g_tma_bn = 64;  // output-tile width of the TMA GEMMs (HG_TMA_BN=128 for A/B runs)
+
+// the four operand tensor maps of one launch (kernel parameter, __grid_constant__)
+struct TmaMaps {
+  CUtensorMap ah, al, bh, bl;
+};
+
+// experiments only: per-CTA %globaltimer trace of one Op type (hg_debug_set_trace)
+__device__ unsigned long long *g_trace = nullptr;
+__device__ int g_trace_id = -1;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TTRACE(j)                                                                     \
+  do {                                                                                \
+    if (g_trace && g_trace_id == Op::ID) g_trace[blockIdx.x * 8 + (j)] = gtimer();   \
+  } while (0)
+
+namespace {
+
+constexpr int T_BM = 128;
+constexpr int T_BK = 32;  // fp32 per 128-byte swizzle row
+constexpr int T_TMA_WARP = 4;
+constexpr int T_MMA_WARP = 5;
+constexpr int T_THREADS = 192;
+
+template <int N>
+struct TCols {
+  static constexpr int v = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
+};
+
+template <class Op>
+constexpr int t_stage_bytes() { return 2 * T_BM * 128 + 2 * Op::BN * 128; }
+template <class Op>
+constexpr int t_stages() {
+  return (200 * 1024) / t_stage_bytes<Op>() < 8 ? (200 * 1024) / t_stage_bytes<Op>() : 8;
+}
+template <class Op>
+constexpr int t_smem_bytes() { return t_stages<Op>() * t_stage_bytes<Op>() + 1024 + 8 * (2 * t_stages<Op>() + 1) + 16; }
+
+}  // namespace
+
+template <class Op>
+__global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ TmaMaps mp, Op op_in) {
+  constexpr int BN = Op::BN, ST = t_stages<Op>();
+  constexpr int A_BYTES = T_BM * 128, B_BYTES = BN * 128, STAGE = t_stage_bytes<Op>();
+  constexpr int TCOLS = TCols<BN>::v;
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
+  static_assert(ST >= 2, "stages");
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE);
+  uint64_t *empty = full + ST;
+  uint64_t *accf = empty + ST;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(accf + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TTRACE(0);
+  // prologue: no global memory written by earlier kernels is touched before pdl_enter
+  if (warp == T_MMA_WARP) tc::tmem_alloc<TCOLS>(tmem_holder);
+  if (threadIdx.x == T_TMA_WARP * 32) {
+    tc::tma_prefetch_desc(&mp.ah);
+    tc::tma_prefetch_desc(&mp.al);
+    tc::tma_prefetch_desc(&mp.bh);
+    tc::tma_prefetch_desc(&mp.bl);
+    for (int s = 0; s < ST; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(accf, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_holder;
+  pdl_enter();
+  if (threadIdx.x == 0) {
+    TTRACE(1);
+    if (g_trace && g_trace_id == Op::ID) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      g_trace[blockIdx.x * 8 + 7] = smid;
+    }
+  }
+
+  Op op = op_in;
+  int m0, n0, ke, ay, by;
+  if (op.tile(blockIdx.x, m0, n0, ke, ay, by)) {  // uniform per CTA
+    const int nchunks = (ke + T_BK - 1) / T_BK;
+    if (warp == T_TMA_WARP) {
+      // ---------------- TMA producer
+      if (lane == 0) {
+        for (int c = 0; c < nchunks; ++c) {
+          const int s = c % ST;
+          if (c >= ST) tc::mbar_wait(&empty[s], ((c / ST) - 1) & 1);
+          uint8_t *sa = smem + s * STAGE;
+          tc::mbar_expect_tx(&full[s], STAGE);
+          const int k0 = c * T_BK;
+          tc::tma_load_2d(sa, &mp.ah, k0, ay, &full[s]);
+          tc::tma_load_2d(sa + A_BYTES, &mp.al, k0, ay, &full[s]);
+          tc::tma_load_2d(sa + 2 * A_BYTES, &mp.bh, k0, by, &full[s]);
+          tc::tma_load_2d(sa + 2 * A_BYTES + B_BYTES, &mp.bl, k0, by, &full[s]);
+          if (c == 0) TTRACE(2);
+        }
+      }
+      __syncwarp();
+    } else if (warp == T_MMA_WARP) {
+      // ---------------- MMA issuer
+      if (lane == 0) {
+        constexpr uint32_t idesc = tc::idesc_tf32(T_BM, BN);
+        for (int c = 0; c < nchunks; ++c) {
+          const int s = c % ST;
+          tc::mbar_wait(&full[s], (c / ST) & 1);
+          tc::fence_after_sync();
+          if (c == 0) TTRACE(3);
+          const uint32_t aH = tc::smem_u32(smem + s * STAGE);
+          const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < T_BK / 8; ++ks) {
+            const uint32_t off = ks * 32;
+            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
+            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+            tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
+            tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
+            tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+          }
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(accf);
+        TTRACE(4);
+      }
+      __syncwarp();
+    } else {
+      // ---------------- epilogue: thread = accumulator row
+      tc::mbar_wait(accf, 0);
+      tc::fence_after_sync();
+      if (threadIdx.x == 0) TTRACE(5);
+      const int row = warp * 32 + lane;
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+      for (int q = 0; q < BN / 32; ++q) {
+        float acc[32];
+        tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
+        op.store(m0 + row, n0, q * 32, acc);
+      }
+      if (threadIdx.x == 0) TTRACE(6);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == T_MMA_WARP) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<TCOLS>(tmem);
+  }
+}
+
+__device__ __forceinline__ float lo_of(float x) {
+  float hi, lo;
+  tc::split_tf32(x, hi, lo);
+  return lo;
+}
+__device__ __forceinline__ float4 lo4(float4 v) { return make_float4(lo_of(v.x), lo_of(v.y), lo_of(v.z), lo_of(v.w)); }
+
+// ---------------------------------------------------------------- ops
+// tile(t, m0, n0, ke, ay, by): output rows m0.., columns n0.., K extent, and the
+// row coordinates of the A and B boxes in their tensor maps.
+
+// G1 update per degree class (A in sorted rows): X1[perm[m]] = ReLU(A[m] W_c^T + b_U), also X1_lo
+template <int BN_>
+struct TUpdC {
+  static constexpr int BN = BN_, ID = 0;
+  const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1, *X1_lo; int H; int row_end;
+  __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
+    const int nt = H / BN, ti = t / nt;
+    if (ti >= info->T) return false;
+    const int4 tl = tiles[ti];
+    m0 = ay = tl.y;
+    row_end = tl.y + tl.z;
+    n0 = (t % nt) * BN;
+    by = tl.x * H + n0;
+    ke = 4 * H;
+    return true;
+  }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+    if (m >= row_end) return;
+    const size_t o = (size_t)perm[m] * H + n0 + q0;
+    const float *b = bU + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 z = make_float4(fmaxf(acc[i] + b[i], 0.f), fmaxf(acc[i + 1] + b[i + 1], 0.f),
+                                   fmaxf(acc[i + 2] + b[i + 2], 0.f), fmaxf(acc[i + 3] + b[i + 3], 0.f));
+      *reinterpret_cast<float4 *>(X1 + o + i) = z;
+      *reinterpret_cast<float4 *>(X1_lo + o + i) = lo4(z);
+    }
+  }
+};
+
+// G2 dA per degree class (dZ in sorted rows): dA[perm[m]] = dZ[m] W_c
+template <int BN_>
+struct TDAC {
+  static constexpr int BN = BN_, ID = 1;
+  const int *perm; const DegInfo *info; const int4 *tiles; float *dA; int H; int row_end;
+  __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
+    const int nt = 4 * H / BN, ti = t / nt;
+    if (ti >= info->T) return false;
+    const int4 tl = tiles[ti];
+    m0 = ay = tl.y;
+    row_end = tl.y + tl.z;
+    n0 = (t % nt) * BN;
+    by = tl.x * 4 * H + n0;
+    ke = H;
+    return true;
+  }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+    if (m >= row_end) return;
+    float *out = dA + (size_t)perm[m] * 4 * H + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+  }
+};
+
+// K1 projection (layers > 0): P = X M_x^T
+template <int BN_>
+struct TProj {
+  static constexpr int BN = BN_, ID = 2;
+  const uint8_t *blob; float *P; int F, H; int N;
+  __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
+    N = batch_N(blob);
+    const int nt = H / BN;
+    m0 = ay = (t / nt) * T_BM;
+    n0 = by = (t % nt) * BN;
+    ke = F;
+    return m0 < N;
+  }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+    if (m >= N) return;
+    float *out = P + (size_t)m * H + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4)
+      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+  }
+};
+
+// K9b dX (layers > 0): dZprev[pos[m]] = (dP[m] M_x) * [X_l[m] > 0] (sorted rows), also its lo
+template <int BN_>
+struct TDX {
+  static constexpr int BN = BN_, ID = 3;
+  const uint8_t *blob; const float *Xl; float *dZ, *dZ_lo; const int *pos; int H, F; int N;
+  __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
+    N = batch_N(blob);
+    const int nt = F / BN;
+    m0 = ay = (t / nt) * T_BM;
+    n0 = by = (t % nt) * BN;
+    ke = H;
+    return m0 < N;
+  }
+  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+    if (m >= N) return;
+    const size_t o = (size_t)m * F + n0 + q0;
+    const size_t od = (size_t)pos[m] * F + n0 + q0;
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float4 x = ldg4(Xl + o + i);
+      const float4 z = make_float4(x.x > 0.f ? acc[i] : 0.f, x.y > 0.f ? acc[i + 1] : 0.f,
+                                   x.z > 0.f ? acc[i + 2] : 0.f, x.w > 0.f ? acc[i + 3] : 0.f);
+      *reinterpret_cast<float4 *>(dZ + od + i) = z;
+      *reinterpret_cast<float4 *>(dZ_lo + od + i) = lo4(z);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- weight preparation
+// per layer l >= 1: Mx_lo = lo(M_x) [H][F]; MxT = M_x^T [F][H] and its lo
+__global__ void k_prep_Mx(const float *__restrict__ params, const int64_t *__restrict__ mx_off, int L, int H, int F,
+                          float *__restrict__ Mx_lo, float *__restrict__ MxT, float *__restrict__ MxT_lo) {
+  pdl_enter();
+  __shared__ float tile[32][33];
+  const int tf = F / 32, th = H / 32, per = tf * th;
+  for (int t = blockIdx.x; t < (L - 1) * per; t += gridDim.x) {
+    const int l = 1 + t / per, tt = t % per, h0 = (tt / tf) * 32, f0 = (tt % tf) * 32;
+    const float *M = params + mx_off[l];
+    const size_t lo_base = (size_t)(l - 1) * H * F;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const size_t o = (size_t)(h0 + r) * F + f0 + threadIdx.x;
+      const float v = M[o];
+      Mx_lo[lo_base + o] = lo_of(v);
+      tile[r][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const float v = tile[threadIdx.x][r];
+      const size_t o = lo_base + (size_t)(f0 + r) * H + h0 + threadIdx.x;
+      MxT[o] = v;
+      MxT_lo[o] = lo_of(v);
+    }
+    __syncthreads();
+  }
+}
+
+// class weights with their lo terms: Wf[c] = W_d [H][4H], WbT[c] = W_d^T [4H][H]
+__global__ void k_prep_W2(const float *__restrict__ params, const int64_t *__restrict__ u_off, int L, int H, int cmax,
+                          const DegInfo *__restrict__ info, float *__restrict__ Wf, float *__restrict__ Wf_lo,
+                          float *__restrict__ WbT, float *__restrict__ WbT_lo) {
+  pdl_enter();
+  __shared__ float tile[32][33];
+  const int K = 4 * H, tk = K / 32, th = H / 32;
+  const int per_cls = tk * th;
+  const int C = info->C;
+  for (int t = blockIdx.x; t < L * cmax * per_cls; t += gridDim.x) {
+    const int l = t / (cmax * per_cls);
+    const int c = (t / per_cls) % cmax;
+    if (c >= C) continue;  // uniform per block
+    const int tt = t % per_cls, h0 = (tt / tk) * 32, k0 = (tt % tk) * 32;
+    const float *U = params + u_off[l];
+    const float a = info->amp[c], b = info->att[c];
+    const size_t base = ((size_t)l * cmax + c) * H * K;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const float *u = U + (size_t)(h0 + r) * 3 * K + k0 + threadIdx.x;
+      const float w = u[0] + a * u[K] + b * u[2 * K];
+      const size_t o = base + (size_t)(h0 + r) * K + k0 + threadIdx.x;
+      Wf[o] = w;
+      Wf_lo[o] = lo_of(w);
+      tile[r][threadIdx.x] = w;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+      const float w = tile[threadIdx.x][r];
+      const size_t o = base + (size_t)(k0 + r) * H + h0 + threadIdx.x;
+      WbT[o] = w;
+      WbT_lo[o] = lo_of(w);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- tensor maps + launch wrappers
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::mutex g_map_mu;
+struct MapEntry {
+  const void *p;
+  uint64_t rows, cols;
+  uint32_t box;
+  CUtensorMap m;
+};
+std::vector<MapEntry> g_maps;
+
+// row-major fp32 [rows][cols] (cols contiguous, rows 16-byte aligned); box = box_rows x 32
+// fp32 (one 128-byte swizzle row), SWIZZLE_128B, out-of-range elements read as zero.
+// Encoded on the host once per (pointer, shape, box) and cached.
+CUtensorMap map2d(const float *p, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  std::lock_guard<std::mutex> g(g_map_mu);
+  for (const auto &e : g_maps)
+    if (e.p == p && e.rows == rows && e.cols == cols && e.box == box_rows) return e.m;
+  MapEntry e{p, rows, cols, box_rows, {}};
+  const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
+  const cuuint64_t strides[1] = {cols * sizeof(float)};
+  const cuuint32_t box[2] = {32, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(&e.m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p), dims, strides, box, es,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {  // shapes are validated at context creation: this is an internal invariant
+    fprintf(stderr, "hgnn: cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u\n", (int)r,
+            (unsigned long long)rows, (unsigned long long)cols, box_rows);
+    abort();
+  }
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps.push_back(e);
+  return e.m;
+}
+
+template <class Op>
+cudaError_t tconfigure() {
+  return cudaFuncSetAttribute(k_tma<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem_bytes<Op>());
+}
+template <class Op>
+void trun(cudaStream_t st, const TmaMaps &mp, const Op &op, int grid) {
+  launch_ex(k_tma<Op>, std::max(grid, 1), T_THREADS, t_smem_bytes<Op>(), st, mp, op);
+  g_launches += 1;
+}
+int mt(int n) { return (n + T_BM - 1) / T_BM; }
+
+template <int BN>
+cudaError_t tconfigure_bn() {
+  cudaError_t e;
+  if ((e = tconfigure<TUpdC<BN>>()) != cudaSuccess) return e;
+  if ((e = tconfigure<TDAC<BN>>()) != cudaSuccess) return e;
+  if ((e = tconfigure<TProj<BN>>()) != cudaSuccess) return e;
+  return tconfigure<TDX<BN>>();
+}
+
+template <int BN>
+void update_bn(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
+               const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU, float *X1,
+               float *X1_lo) {
+  const int K = 4 * c.H;
+  const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, BN),
+                   map2d(Wf_lo, (uint64_t)cmax * c.H, K, BN)};
+  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0};
+  trun(st, mp, op, tc_max_tiles(c, cmax) * (c.H / BN));
+}
+template <int BN>
+void dA_bn(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
+           const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
+  const TmaMaps mp{map2d(dZ, c.maxN, c.H, T_BM), map2d(dZ_lo, c.maxN, c.H, T_BM),
+                   map2d(WbT, (uint64_t)cmax * 4 * c.H, c.H, BN), map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, c.H, BN)};
+  TDAC<BN> op{perm, info, tiles, dA, c.H, 0};
+  trun(st, mp, op, tc_max_tiles(c, cmax) * (4 * c.H / BN));
+}
+template <int BN>
+void proj_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
+             const float *Mx, const float *Mx_lo, float *P) {
+  const TmaMaps mp{map2d(X, c.maxN, F, T_BM), map2d(X_lo, c.maxN, F, T_BM), map2d(Mx, c.H, F, BN),
+                   map2d(Mx_lo, c.H, F, BN)};
+  TProj<BN> op{blob, P, F, c.H, 0};
+  trun(st, mp, op, mt(c.maxN) * (c.H / BN));
+}
+template <int BN>
+void dX_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo, const float *MxT,
+           const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo, const int *pos) {
+  const TmaMaps mp{map2d(dP, c.maxN, c.H, T_BM), map2d(dP_lo, c.maxN, c.H, T_BM), map2d(MxT, F, c.H, BN),
+                   map2d(MxT_lo, F, c.H, BN)};
+  TDX<BN> op{blob, Xl, dZ, dZ_lo, pos, c.H, F, 0};
+  trun(st, mp, op, mt(c.maxN) * (F / BN));
+}
+}  // namespace
+
+cudaError_t tcd_configure() {
+  if (!g_encode) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess) return e;
+    if (q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  if (const char *v = getenv("HG_TMA_BN")) g_tma_bn = atoi(v) == 128 ? 128 : 64;
+  cudaError_t e;
+  if ((e = tconfigure_bn<64>()) != cudaSuccess) return e;
+  return tconfigure_bn<128>();
+}
+
+void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
+                         const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
+                         float *X1, float *X1_lo) {
+  if (g_tma_bn == 128) update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
+  else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
+}
+
+void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
+                     const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
+  if (g_tma_bn == 128) dA_bn<128>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
+  else dA_bn<64>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
+}
+
+void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
+                   const float *Mx, const float *Mx_lo, float *P) {
+  if (g_tma_bn == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+  else proj_bn<64>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+}
+
+void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
+                 const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
+                 const int *pos) {
+  if (g_tma_bn == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+  else dX_bn<64>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+}
+
+void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,
+                    float *Mx_lo, float *MxT, float *MxT_lo) {
+  if (L < 2) return;
+  const int blocks = std::min((L - 1) * (c.H / 32) * (c.H / 32), kSMs * 4);
+  launch_ex(k_prep_Mx, blocks, dim3(32, 8), 0, st, params, mx_off_dev, L, c.H, c.H, Mx_lo, MxT, MxT_lo);
+  g_launches += 1;
+}
+
+void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
+                    const DegInfo *info, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo) {
+  const int blocks = std::min(L * cmax * (4 * c.H / 32) * (c.H / 32), kSMs * 8);
+  launch_ex(k_prep_W2, blocks, dim3(32, 8), 0, st, params, u_off_dev, L, c.H, cmax, info, Wf, Wf_lo, WbT, WbT_lo);
+  g_launches += 1;
+}
+
+}  // namespace hg
+
+extern "C" int hg_debug_set_trace(void *buf, int op_id) {  // experiments only (not part of the ABI header)
+  cudaError_t e = cudaMemcpyToSymbol(hg::g_trace, &buf, sizeof(void *));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(hg::g_trace_id, &op_id, sizeof(int));
+  return (int)e;
+}

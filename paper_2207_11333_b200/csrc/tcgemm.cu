@@ -105,6 +105,7 @@ __device__ __forceinline__ void xf_coords(int task, int &r, int &j) {
 
 template <class Op>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_tcgemm(Op op_in) {
+  pdl_enter();
   Op op = op_in;
   op.prepare();
   int m0, n0, kb, ke;
@@ -321,7 +322,7 @@ static cudaError_t configure_tc() {
 
 template <class Op>
 static void run_tc(cudaStream_t st, const Op &op, int grid) {
-  k_tcgemm<Op><<<std::max(grid, 1), TC_THREADS, tc_smem_bytes<Op>(), st>>>(op);
+  launch_ex(k_tcgemm<Op>, std::max(grid, 1), TC_THREADS, tc_smem_bytes<Op>(), st, op);
   g_launches += 1;
 }
 
@@ -479,7 +480,9 @@ struct TcDU {
 __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ blob, double delta, int cmax,
                                                   int ks, float *__restrict__ amp, float *__restrict__ att,
                                                   int *__restrict__ perm, DegInfo *__restrict__ info,
-                                                  int4 *__restrict__ tiles, int4 *__restrict__ splits) {
+                                                  int4 *__restrict__ tiles, int4 *__restrict__ splits,
+                                                  int *__restrict__ pos) {
+  pdl_enter();
   __shared__ int hist[kMaxClasses], bstart[kMaxClasses], run[kMaxClasses], cls_of[kMaxClasses];
   __shared__ int wcnt[32][kMaxClasses];
   const BatchView b = load_batch(blob);
@@ -550,7 +553,11 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
       run[tid] = acc;
     }
     __syncthreads();
-    if (d >= 0) perm[bstart[d] + wcnt[warp][d] + rank] = i;
+    if (d >= 0) {
+      const int r = bstart[d] + wcnt[warp][d] + rank;
+      perm[r] = i;
+      if (pos) pos[i] = r;
+    }
     __syncthreads();
   }
 }
@@ -559,6 +566,7 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
 // for all layers (32x32 tiles; the transposed copy goes through shared memory)
 __global__ void k_prep_W(const float *__restrict__ params, const int64_t *__restrict__ u_off, int L, int H, int cmax,
                          const DegInfo *__restrict__ info, float *__restrict__ Wf, float *__restrict__ WbT) {
+  pdl_enter();
   __shared__ float tile[32][33];
   const int K = 4 * H, tk = K / 32, th = H / 32;
   const int per_cls = tk * th;
@@ -686,11 +694,11 @@ struct TcGramC {
   }
   __device__ const float *any_src() const { return dZ; }
   __device__ const float *a_src(int m, int k, int ke) const {
-    return k < ke ? dZ + (size_t)perm[s0 + k] * H + m : nullptr;
+    return k < ke ? dZ + (size_t)(perm ? perm[s0 + k] : s0 + k) * H + m : nullptr;  // perm null: rows pre-sorted
   }
   __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
   __device__ const float *b_src(int n0, int r, int k, int ke) const {
-    return k < ke ? A + (size_t)perm[s0 + k] * 4 * H + n0 + r : nullptr;
+    return k < ke ? A + (size_t)(perm ? perm[s0 + k] : s0 + k) * 4 * H + n0 + r : nullptr;
   }
   __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
   __device__ void store(int m, int n0, int q0, const float (&acc)[1][32]) const {
@@ -705,6 +713,7 @@ struct TcGramC {
 // one warp per output, fixed xor-shuffle order
 __global__ void k_reduce_splits_rows(const float *__restrict__ cs, const DegInfo *__restrict__ info, int H,
                                      float *__restrict__ out) {
+  pdl_enter();
   const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
   const int S = info->S;
   for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < H; e += gridDim.x * wpb) {
@@ -719,6 +728,7 @@ __global__ void k_reduce_splits_rows(const float *__restrict__ cs, const DegInfo
 // dU[h][s*4H + n] = sum_sp s(class(sp)) part[sp][h][n], fixed split order
 __global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInfo *__restrict__ info,
                                     const int4 *__restrict__ splits, int H, float *__restrict__ dU) {
+  pdl_enter();
   const int S = info->S;
   const int K = 4 * H, total = H * K;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
@@ -847,6 +857,7 @@ struct TcDMx {
 __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
 
 __global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
+  pdl_enter();
   const int c4 = count / 4;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < c4; e += gridDim.x * blockDim.x) {
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -865,6 +876,7 @@ constexpr int kColsumRows = 64;
 constexpr int kColsumChunks = 128;  // partial slots; chunks beyond ceil(N/64) write zeros
 __global__ void __launch_bounds__(256) k_colsum_part(const uint8_t *__restrict__ blob, const float *__restrict__ X,
                                                      int H, float *__restrict__ part) {
+  pdl_enter();
   const int N = batch_N(blob);
   const int per = max(kColsumRows, (N + kColsumChunks - 1) / kColsumChunks);
   for (int ch = blockIdx.x; ch < kColsumChunks; ch += gridDim.x) {
@@ -887,6 +899,7 @@ __global__ void __launch_bounds__(256) k_colsum_part(const uint8_t *__restrict__
 // UT[l][s][n][h] = U_l[h][s*4H + n] for every layer (32x32 smem-tiled transpose)
 __global__ void k_prep_UT(const float *__restrict__ params, const int64_t *__restrict__ u_off, int L, int H,
                           float *__restrict__ UT) {
+  pdl_enter();
   __shared__ float tile[32][33];
   const int W = 12 * H;  // U row length
   const int tilesC = W / 32, tilesR = H / 32;
@@ -929,16 +942,16 @@ void launch_tc_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const flo
   TcDU op{blob, dZ, A, amp, att, partial, c.H, 0, 0};
   run_tc(st, op, (c.H / TC_BM) * (4 * c.H / TcDU::BN) * kTcDUSplits);
   const int count = c.H * 12 * c.H;
-  k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDUSplits, count, dU);
-  k_colsum_part<<<kColsumChunks, std::min(c.H, 256), 0, st>>>(blob, dZ, c.H, partial);
-  k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(partial, kColsumChunks, c.H, dbU);
+  launch_ex(k_reduce_parts, std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st, partial, kTcDUSplits, count, dU);
+  launch_ex(k_colsum_part, kColsumChunks, std::min(c.H, 256), 0, st, blob, dZ, c.H, partial);
+  launch_ex(k_reduce_rows, cdiv(c.H, 8), 256, 0, st, partial, kColsumChunks, c.H, dbU);
   g_launches += 3;
 }
 
 void launch_prep_UT(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L,
                     float *UT) {
   const int blocks = std::min(L * (12 * c.H / 32) * (c.H / 32), kSMs * 8);
-  k_prep_UT<<<blocks, dim3(32, 8), 0, st>>>(params, u_off_dev, L, c.H, UT);
+  launch_ex(k_prep_UT, blocks, dim3(32, 8), 0, st, params, u_off_dev, L, c.H, UT);
   g_launches += 1;
 }
 
@@ -958,15 +971,15 @@ int tc_max_tiles(const Caps &c, int cmax) { return mtiles(c.maxN) + cmax; }
 int tc_max_splits(const Caps &c, int cmax) { return (c.maxN + kGramKS - 1) / kGramKS + cmax; }
 
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
-                    DegInfo *info, int4 *tiles, int4 *splits) {
-  k_degsort<<<1, 1024, 0, st>>>(blob, delta, cmax, kGramKS, amp, att, perm, info, tiles, splits);
+                    DegInfo *info, int4 *tiles, int4 *splits, int *pos) {
+  launch_ex(k_degsort, 1, 1024, 0, st, blob, delta, cmax, kGramKS, amp, att, perm, info, tiles, splits, pos);
   g_launches += 1;
 }
 
 void launch_prep_W(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
                    const DegInfo *info, float *Wf, float *WbT) {
   const int blocks = std::min(L * cmax * (4 * c.H / 32) * (c.H / 32), kSMs * 8);
-  k_prep_W<<<blocks, dim3(32, 8), 0, st>>>(params, u_off_dev, L, c.H, cmax, info, Wf, WbT);
+  launch_ex(k_prep_W, blocks, dim3(32, 8), 0, st, params, u_off_dev, L, c.H, cmax, info, Wf, WbT);
   g_launches += 1;
 }
 
@@ -994,8 +1007,8 @@ void launch_tc_dU_cls(cudaStream_t st, const Caps &c, int cmax, const uint8_t *b
   float *cs = partial + (size_t)smax * total;  // per-split column sums of dZ (db_U)
   TcGramC op{dZ, A, perm, info, splits, partial, c.H, smax, cs, 0, 0};
   run_tc(st, op, (c.H / TC_BM) * (4 * c.H / TcGramC::BN) * smax);
-  k_reduce_dU_classes<<<std::min(cdiv(total, 256), kSMs * 4), 256, 0, st>>>(partial, info, splits, c.H, dU);
-  k_reduce_splits_rows<<<cdiv(c.H, 8), 256, 0, st>>>(cs, info, c.H, dbU);
+  launch_ex(k_reduce_dU_classes, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, info, splits, c.H, dU);
+  launch_ex(k_reduce_splits_rows, cdiv(c.H, 8), 256, 0, st, cs, info, c.H, dbU);
   g_launches += 2;
 }
 
@@ -1037,8 +1050,8 @@ void launch_tc_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
   float *cs = partial + (size_t)kTcDMxSplits * count;  // per-split column sums of dP (db_M)
   TcDMx op{blob, dP, X, partial, c.H, F, 0, cs, 0};
   run_tc(st, op, (c.H / TC_BM) * (F / TcDMx::BN) * kTcDMxSplits);
-  k_reduce_parts<<<std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st>>>(partial, kTcDMxSplits, count, dMx);
-  k_reduce_rows<<<cdiv(c.H, 8), 256, 0, st>>>(cs, kTcDMxSplits, c.H, dbM);
+  launch_ex(k_reduce_parts, std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st, partial, kTcDMxSplits, count, dMx);
+  launch_ex(k_reduce_rows, cdiv(c.H, 8), 256, 0, st, cs, kTcDMxSplits, c.H, dbM);
   g_launches += 2;
 }
 
