@@ -50,6 +50,10 @@ inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 // completion of all kernels before it, so stream order is preserved
 // transitively; the gain is that launch latency overlaps the previous kernel.
 extern bool g_pdl;
+// launch priority: kernels enqueued while g_low_prio is set (side-stream weight
+// gradients) get the device's lowest priority, all others its highest
+extern bool g_low_prio;
+extern int g_prio_lo, g_prio_hi;
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -57,16 +61,18 @@ __device__ __forceinline__ void pdl_enter() {
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                              Args &&...args) {
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = g_low_prio ? g_prio_lo : g_prio_hi;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 constexpr int kSMs = 148;

@@ -28,7 +28,7 @@ struct Plan {
   std::vector<size_t> P, A, arg, X;  // X[l] = output of layer l (X_{l+1})
   size_t dZa = 0, dZb = 0, dA = 0, dP = 0;
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
-  size_t part = 0;
+  size_t part = 0, part2 = 0, part3 = 0;  // scratch: agg_bwd (dM_e), Gram (dU), dM_x partials
   size_t UT = 0, u_off = 0;
   int cmax = 0;  // degree-class slots (0 = class GEMMs off)
   size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
@@ -107,6 +107,8 @@ Plan make_plan(const hg_config &c) {
     pf = std::max(pf, tc_gram_partial_floats(caps, p.cmax));
     p.part = take(sizeof(float) * pf);  // (re-take: the class partials are larger)
   }
+  p.part2 = take(sizeof(float) * pf);
+  p.part3 = take(sizeof(float) * pf);
   p.total = off;
   return p;
 }
@@ -132,6 +134,8 @@ struct hg_ctx {
   cudaStream_t comm_stream = nullptr;           // bucketed allreduce overlapping the backward
   std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
   cudaEvent_t comm_done = nullptr;
+  cudaStream_t side_stream = nullptr;            // weight-gradient GEMMs beside the critical chain
+  std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side;  // per layer fork / join points
   int64_t launches = 0;
   bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
   hg_status sticky = HG_OK;
@@ -314,7 +318,36 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       launch_prep_UT(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers,
                      x->f(p.UT));
     });
+  // Weight-gradient GEMMs (dU / db_U from the class Gram, dM_x / db_M) feed only
+  // the allreduce and AdamW, so they run on a low-priority side stream while the
+  // main stream walks the critical chain dA -> agg_bwd -> dX of each layer.
+  // Hazards: dX_l overwrites the dZ buffer Gram_{l+1} read; agg_bwd_l overwrites
+  // the dP dM_x(l+1) read -> the main stream waits for the side events first.
+  const bool fork = !pr && x->side_stream != nullptr;
+  cudaStream_t side = fork ? x->side_stream : st;
+  auto rec = [&](cudaEvent_t ev, cudaStream_t s) { if (fork) cudaEventRecord(ev, s); };
+  auto wait = [&](cudaStream_t s, cudaEvent_t ev) { if (fork) cudaStreamWaitEvent(s, ev, 0); };
+  float *part_agg = x->f(p.part), *part_dU = x->f(p.part2), *part_dMx = x->f(p.part3);
   for (int l = c.layers - 1; l >= 0; --l) {
+    // ---- side: Gram (dU, db_U) as soon as dZ_l is ready
+    rec(x->ev_dz[l], st);
+    wait(side, x->ev_dz[l]);
+    g_low_prio = fork;
+    phase(pr, HG_PHASE_DU, [&] {
+      if (cls)
+        launch_tc_dU_cls(side, x->caps, p.cmax, blob, dZ, x->f(p.A[l]), nullptr /* rows pre-sorted */, dinfo,
+                         reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
+                         x->grad(lname(l, "b_U")));
+      else if (x->use_tc)
+        launch_tc_dU(side, x->caps, blob, dZ, x->f(p.A[l]), amp, att, part_dU, x->grad(lname(l, "U")),
+                     x->grad(lname(l, "b_U")));
+      else
+        launch_dU(side, x->caps, blob, dZ, x->f(p.A[l]), amp, att, part_dU, x->grad(lname(l, "U")),
+                  x->grad(lname(l, "b_U")));
+    });
+    rec(x->ev_gram[l], side);
+    g_low_prio = false;
+    // ---- main: dA, aggregation backward
     phase(pr, HG_PHASE_DA, [&] {
       if (cls)
         launch_d_dA_cls(st, x->caps, p.cmax, dZ, dZl, perm, dinfo, reinterpret_cast<const int4 *>(x->b(p.tiles)),
@@ -325,35 +358,32 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       else
         launch_dA(st, x->caps, blob, dZ, amp, att, x->param(lname(l, "U")), x->f(p.dA));
     });
-    phase(pr, HG_PHASE_DU, [&] {
-      if (cls)
-        launch_tc_dU_cls(st, x->caps, p.cmax, blob, dZ, x->f(p.A[l]), nullptr /* rows pre-sorted */, dinfo,
-                         reinterpret_cast<const int4 *>(x->b(p.splits)), x->f(p.part), x->grad(lname(l, "U")),
-                         x->grad(lname(l, "b_U")));
-      else if (x->use_tc)
-        launch_tc_dU(st, x->caps, blob, dZ, x->f(p.A[l]), amp, att, x->f(p.part), x->grad(lname(l, "U")),
-                     x->grad(lname(l, "b_U")));
-      else
-        launch_dU(st, x->caps, blob, dZ, x->f(p.A[l]), amp, att, x->f(p.part), x->grad(lname(l, "U")),
-                  x->grad(lname(l, "b_U")));
-    });
+    if (l + 1 < c.layers) wait(st, x->ev_side[l + 1]);  // dM_x(l+1) finished reading dP
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), x->f(p.dP), x->f(p.part), x->grad(lname(l, "M_e")),
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), x->f(p.dP), part_agg, x->grad(lname(l, "M_e")),
                      cls && l > 0 ? x->f(p.dP_lo) : nullptr, pos);
     });
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
+    // ---- side: dM_x, db_M once dP_l is ready; then layer l's gradients are complete
+    rec(x->ev_dp[l], st);
+    wait(side, x->ev_dp[l]);
+    g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
       if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
-        launch_tc_dMx(st, x->caps, blob, x->f(p.dP), Xl, F, x->f(p.part), x->grad(lname(l, "M_x")),
+        launch_tc_dMx(side, x->caps, blob, x->f(p.dP), Xl, F, part_dMx, x->grad(lname(l, "M_x")),
                       x->grad(lname(l, "b_M")));
       else
-        launch_dMx(st, x->caps, blob, x->f(p.dP), Xl, F, x->f(p.part), x->grad(lname(l, "M_x")),
+        launch_dMx(side, x->caps, blob, x->f(p.dP), Xl, F, part_dMx, x->grad(lname(l, "M_x")),
                    x->grad(lname(l, "b_M")));
     });
-    if (overlap_allreduce) enqueue_bucket(x, st, c.layers - l);  // conv l gradients complete
+    g_low_prio = false;
+    if (overlap_allreduce) enqueue_bucket(x, side, c.layers - l);  // conv l gradients complete
+    rec(x->ev_side[l], side);
+    // ---- main: dX into the other dZ buffer
     if (l > 0) {
+      if (l + 1 < c.layers) wait(st, x->ev_gram[l + 1]);  // Gram_{l+1} finished reading dZn
       phase(pr, HG_PHASE_DX, [&] {
         if (cls)
           launch_d_dX(st, x->caps, blob, x->f(p.dP), x->f(p.dP_lo), x->f(p.MxT) + (size_t)(l - 1) * HH,
@@ -367,6 +397,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       std::swap(dZl, dZnl);
     }
   }
+  wait(st, x->ev_side[0]);  // join: every gradient is complete on the main stream
 }
 
 // gradient buckets in backward order: head first, then conv L-1 ... conv 0 (each a
@@ -469,8 +500,20 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   };
   if ((e = cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking)) != cudaSuccess)
     return bail(e, "cudaStreamCreate");
-  if ((e = cudaStreamCreateWithFlags(&x->cap_stream, cudaStreamNonBlocking)) != cudaSuccess)
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  if ((e = cudaStreamCreateWithPriority(&x->cap_stream, cudaStreamNonBlocking, prio_hi)) != cudaSuccess)
     return bail(e, "cudaStreamCreate");
+  if ((e = cudaStreamCreateWithPriority(&x->side_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
+    return bail(e, "cudaStreamCreate");
+  g_prio_lo = prio_lo;
+  g_prio_hi = prio_hi;
+  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
+    for (int l = 0; l < c->layers; ++l) {
+      cudaEvent_t ev;
+      if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
+      v->push_back(ev);
+    }
   for (int s = 0; s < c->n_slots; ++s) {
     void *h = nullptr;
     if ((e = cudaHostAlloc(&h, plan.blob_max, cudaHostAllocDefault)) != cudaSuccess) return bail(e, "cudaHostAlloc");
@@ -524,6 +567,9 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   for (auto ev : x->compute_done) cudaEventDestroy(ev);
   if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
   if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
+  if (x->side_stream) cudaStreamDestroy(x->side_stream);
+  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
+    for (auto ev : *v) cudaEventDestroy(ev);
   if (x->comm) ncclCommDestroy(x->comm);
   for (auto ev : x->bucket_ready) cudaEventDestroy(ev);
   if (x->comm_done) cudaEventDestroy(x->comm_done);
@@ -800,7 +846,7 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   }
   if (e != cudaSuccess) return cuda_fail(x, e, "cudaStreamEndCapture");
   cudaGraphExec_t ex = nullptr;
-  e = cudaGraphInstantiate(&ex, g, 0);
+  e = cudaGraphInstantiate(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
   cudaGraphDestroy(g);
   if (e != cudaSuccess) return cuda_fail(x, e, "cudaGraphInstantiate");
   x->graphs[slot] = ex;

@@ -26,6 +26,8 @@ namespace hg {
 
 std::atomic<int64_t> g_launches{0};
 bool g_pdl = true;
+bool g_low_prio = false;
+int g_prio_lo = 0, g_prio_hi = 0;
 static inline void counted(int n = 1) { g_launches += n; }
 
 // ------------------------------------------------------------------ scalers

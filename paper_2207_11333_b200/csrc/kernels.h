@@ -7,7 +7,9 @@
 #include <stdint.h>
 
 namespace hg {
-extern bool g_pdl;  // launch kernels with programmatic dependent launch (common.cuh)
+extern bool g_pdl;
+extern bool g_low_prio;
+extern int g_prio_lo, g_prio_hi;  // launch kernels with programmatic dependent launch (common.cuh)
 
 struct Caps {
   int maxB, maxN, maxE;

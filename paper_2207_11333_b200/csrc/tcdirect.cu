@@ -68,31 +68,44 @@ struct TCols {
   static constexpr int v = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : N <= 256 ? 256 : 512;
 };
 
+constexpr int T_STG_LD = 36;                                  // staging row stride (floats)
+constexpr int T_STG_BYTES = 4 * 32 * T_STG_LD * 4;            // 4 epilogue warps x 32 rows
+
 template <class Op>
 constexpr int t_stage_bytes() { return 2 * T_BM * 128 + 2 * Op::BN * 128; }
 template <class Op>
 constexpr int t_stages() {
-  return (200 * 1024) / t_stage_bytes<Op>() < 8 ? (200 * 1024) / t_stage_bytes<Op>() : 8;
+  return (224 * 1024 - T_STG_BYTES) / t_stage_bytes<Op>() < 8 ? (224 * 1024 - T_STG_BYTES) / t_stage_bytes<Op>() : 8;
 }
 template <class Op>
-constexpr int t_smem_bytes() { return t_stages<Op>() * t_stage_bytes<Op>() + 1024 + 8 * (2 * t_stages<Op>() + 1) + 16; }
+constexpr int t_smem_bytes() {
+  return t_stages<Op>() * t_stage_bytes<Op>() + T_STG_BYTES + 1024 + 8 * (2 * t_stages<Op>() + 4) + 16;
+}
 
 }  // namespace
 
+// Persistent: CTA b handles work items b, b + gridDim.x, ... (items past the
+// device-side count are skipped by every role alike). The smem ring continues
+// across items and the accumulator is double-buffered in TMEM (2 x BN columns),
+// so the epilogue of item i overlaps the loads and MMAs of item i + 1.
+// Epilogue: TMEM -> registers -> per-warp staging tile -> Op::emit, one float4
+// per lane with 8 lanes per row, so global stores are 128-byte coalesced rows.
 template <class Op>
 __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ TmaMaps mp, Op op_in) {
   constexpr int BN = Op::BN, ST = t_stages<Op>();
   constexpr int A_BYTES = T_BM * 128, B_BYTES = BN * 128, STAGE = t_stage_bytes<Op>();
-  constexpr int TCOLS = TCols<BN>::v;
+  constexpr int TCOLS = TCols<2 * BN>::v;
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(ST >= 2, "stages");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE);
+  float *stg_all = reinterpret_cast<float *>(smem + ST * STAGE);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE + T_STG_BYTES);
   uint64_t *empty = full + ST;
-  uint64_t *accf = empty + ST;
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(accf + 1);
+  uint64_t *accf = empty + ST;  // [2] MMA -> epilogue
+  uint64_t *acce = accf + 2;    // [2] epilogue -> MMA
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acce + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTRACE(0);
@@ -107,7 +120,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(accf, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&accf[b], 1);
+      tc::mbar_init(&acce[b], 4);
+    }
     tc::fence_mbar_init();
   }
   tc::fence_before_sync();
@@ -125,15 +141,18 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
   }
 
   Op op = op_in;
-  int m0, n0, ke, ay, by;
-  if (op.tile(blockIdx.x, m0, n0, ke, ay, by)) {  // uniform per CTA
-    const int nchunks = (ke + T_BK - 1) / T_BK;
-    if (warp == T_TMA_WARP) {
-      // ---------------- TMA producer
-      if (lane == 0) {
-        for (int c = 0; c < nchunks; ++c) {
-          const int s = c % ST;
-          if (c >= ST) tc::mbar_wait(&empty[s], ((c / ST) - 1) & 1);
+  const int items = op.items_cap;
+  if (warp == T_TMA_WARP) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        int m0, n0, ke, ay, by;
+        if (!op.tile(item, m0, n0, ke, ay, by)) continue;
+        const int nchunks = (ke + T_BK - 1) / T_BK;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int s = it % ST;
+          if (it >= ST) tc::mbar_wait(&empty[s], ((it / ST) - 1) & 1);
           uint8_t *sa = smem + s * STAGE;
           tc::mbar_expect_tx(&full[s], STAGE);
           const int k0 = c * T_BK;
@@ -141,19 +160,29 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
           tc::tma_load_2d(sa + A_BYTES, &mp.al, k0, ay, &full[s]);
           tc::tma_load_2d(sa + 2 * A_BYTES, &mp.bh, k0, by, &full[s]);
           tc::tma_load_2d(sa + 2 * A_BYTES + B_BYTES, &mp.bl, k0, by, &full[s]);
-          if (c == 0) TTRACE(2);
+          if (it == 0) TTRACE(2);
         }
       }
-      __syncwarp();
-    } else if (warp == T_MMA_WARP) {
-      // ---------------- MMA issuer
-      if (lane == 0) {
-        constexpr uint32_t idesc = tc::idesc_tf32(T_BM, BN);
-        for (int c = 0; c < nchunks; ++c) {
-          const int s = c % ST;
-          tc::mbar_wait(&full[s], (c / ST) & 1);
+    }
+    __syncwarp();
+  } else if (warp == T_MMA_WARP) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = tc::idesc_tf32(T_BM, BN);
+      int it = 0, tcount = 0;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        int m0, n0, ke, ay, by;
+        if (!op.tile(item, m0, n0, ke, ay, by)) continue;
+        const int buf = tcount & 1;
+        if (tcount >= 2) tc::mbar_wait(&acce[buf], ((tcount >> 1) - 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t d = tmem + (uint32_t)(buf * BN);
+        const int nchunks = (ke + T_BK - 1) / T_BK;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int s = it % ST;
+          tc::mbar_wait(&full[s], (it / ST) & 1);
           tc::fence_after_sync();
-          if (c == 0) TTRACE(3);
+          if (it == 0) TTRACE(3);
           const uint32_t aH = tc::smem_u32(smem + s * STAGE);
           const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
 #pragma unroll
@@ -161,31 +190,57 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
             const uint32_t off = ks * 32;
             const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
             const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
-            tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
-            tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
-            tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+            tc::mma_tf32(d, dah, dbh, idesc, (c | ks) != 0);
+            tc::mma_tf32(d, dah, dbl, idesc, 1u);
+            tc::mma_tf32(d, dal, dbh, idesc, 1u);
           }
           tc::mma_commit(&empty[s]);
         }
-        tc::mma_commit(accf);
-        TTRACE(4);
+        tc::mma_commit(&accf[buf]);
+        ++tcount;
       }
-      __syncwarp();
-    } else {
-      // ---------------- epilogue: thread = accumulator row
-      tc::mbar_wait(accf, 0);
+      TTRACE(4);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (warps 0-3; warp w owns accumulator lanes 32w..32w+31)
+    float *stg = stg_all + warp * 32 * T_STG_LD;
+    int tcount = 0;
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+      int m0, n0, ke, ay, by;
+      if (!op.tile(item, m0, n0, ke, ay, by)) continue;
+      const int buf = tcount & 1;
+      tc::mbar_wait(&accf[buf], (tcount >> 1) & 1);
       tc::fence_after_sync();
-      if (threadIdx.x == 0) TTRACE(5);
-      const int row = warp * 32 + lane;
-      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+      if (threadIdx.x == 0 && tcount == 0) TTRACE(5);
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
       for (int q = 0; q < BN / 32; ++q) {
         float acc[32];
         tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
-        op.store(m0 + row, n0, q * 32, acc);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) =
+              make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+        __syncwarp();
+        // all global loads of the 8 rows first (emit's stores may alias them), then the stores
+        const int cc = 4 * (lane & 7), n = n0 + q * 32 + cc;
+        typename Op::Pre pre[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) pre[j] = op.pre(m0 + warp * 32 + 4 * j + (lane >> 3), n);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = 4 * j + (lane >> 3);
+          op.emit(m0 + warp * 32 + r, n, *reinterpret_cast<const float4 *>(stg + r * T_STG_LD + cc), pre[j]);
+        }
+        __syncwarp();
       }
-      if (threadIdx.x == 0) TTRACE(6);
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acce[buf]);
+      ++tcount;
     }
+    if (threadIdx.x == 0) TTRACE(6);
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -203,14 +258,16 @@ __device__ __forceinline__ float lo_of(float x) {
 __device__ __forceinline__ float4 lo4(float4 v) { return make_float4(lo_of(v.x), lo_of(v.y), lo_of(v.z), lo_of(v.w)); }
 
 // ---------------------------------------------------------------- ops
-// tile(t, m0, n0, ke, ay, by): output rows m0.., columns n0.., K extent, and the
-// row coordinates of the A and B boxes in their tensor maps.
+// tile(item, m0, n0, ke, ay, by): output rows m0.., columns n0.., K extent and
+// the row coordinates of the A and B boxes in their tensor maps (false: no
+// work for this item). emit(m, n, v): epilogue for output row m, columns n..n+3.
 
 // G1 update per degree class (A in sorted rows): X1[perm[m]] = ReLU(A[m] W_c^T + b_U), also X1_lo
 template <int BN_>
 struct TUpdC {
   static constexpr int BN = BN_, ID = 0;
-  const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1, *X1_lo; int H; int row_end;
+  const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1, *X1_lo; int H; int items_cap;
+  int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     const int nt = H / BN, ti = t / nt;
     if (ti >= info->T) return false;
@@ -222,17 +279,16 @@ struct TUpdC {
     ke = 4 * H;
     return true;
   }
-  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+  struct Pre { int node; float4 b; };
+  __device__ Pre pre(int m, int n) const { return Pre{m < row_end ? perm[m] : 0, ldg4(bU + n)}; }
+  __device__ void emit(int m, int n, float4 v, const Pre &p) const {
     if (m >= row_end) return;
-    const size_t o = (size_t)perm[m] * H + n0 + q0;
-    const float *b = bU + n0 + q0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      const float4 z = make_float4(fmaxf(acc[i] + b[i], 0.f), fmaxf(acc[i + 1] + b[i + 1], 0.f),
-                                   fmaxf(acc[i + 2] + b[i + 2], 0.f), fmaxf(acc[i + 3] + b[i + 3], 0.f));
-      *reinterpret_cast<float4 *>(X1 + o + i) = z;
-      *reinterpret_cast<float4 *>(X1_lo + o + i) = lo4(z);
-    }
+    const size_t o = (size_t)p.node * H + n;
+    const float4 b = p.b;
+    const float4 z = make_float4(fmaxf(v.x + b.x, 0.f), fmaxf(v.y + b.y, 0.f), fmaxf(v.z + b.z, 0.f),
+                                 fmaxf(v.w + b.w, 0.f));
+    *reinterpret_cast<float4 *>(X1 + o) = z;
+    *reinterpret_cast<float4 *>(X1_lo + o) = lo4(z);
   }
 };
 
@@ -240,7 +296,8 @@ struct TUpdC {
 template <int BN_>
 struct TDAC {
   static constexpr int BN = BN_, ID = 1;
-  const int *perm; const DegInfo *info; const int4 *tiles; float *dA; int H; int row_end;
+  const int *perm; const DegInfo *info; const int4 *tiles; float *dA; int H; int items_cap;
+  int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     const int nt = 4 * H / BN, ti = t / nt;
     if (ti >= info->T) return false;
@@ -252,12 +309,11 @@ struct TDAC {
     ke = H;
     return true;
   }
-  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+  struct Pre { int node; };
+  __device__ Pre pre(int m, int) const { return Pre{m < row_end ? perm[m] : 0}; }
+  __device__ void emit(int m, int n, float4 v, const Pre &p) const {
     if (m >= row_end) return;
-    float *out = dA + (size_t)perm[m] * 4 * H + n0 + q0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+    *reinterpret_cast<float4 *>(dA + (size_t)p.node * 4 * H + n) = v;
   }
 };
 
@@ -265,7 +321,8 @@ struct TDAC {
 template <int BN_>
 struct TProj {
   static constexpr int BN = BN_, ID = 2;
-  const uint8_t *blob; float *P; int F, H; int N;
+  const uint8_t *blob; float *P; int F, H; int items_cap;
+  int N;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     N = batch_N(blob);
     const int nt = H / BN;
@@ -274,12 +331,11 @@ struct TProj {
     ke = F;
     return m0 < N;
   }
-  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+  struct Pre {};
+  __device__ Pre pre(int, int) const { return Pre{}; }
+  __device__ void emit(int m, int n, float4 v, const Pre &) const {
     if (m >= N) return;
-    float *out = P + (size_t)m * H + n0 + q0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]);
+    *reinterpret_cast<float4 *>(P + (size_t)m * H + n) = v;
   }
 };
 
@@ -287,7 +343,8 @@ struct TProj {
 template <int BN_>
 struct TDX {
   static constexpr int BN = BN_, ID = 3;
-  const uint8_t *blob; const float *Xl; float *dZ, *dZ_lo; const int *pos; int H, F; int N;
+  const uint8_t *blob; const float *Xl; float *dZ, *dZ_lo; const int *pos; int H, F; int items_cap;
+  int N;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     N = batch_N(blob);
     const int nt = F / BN;
@@ -296,18 +353,18 @@ struct TDX {
     ke = H;
     return m0 < N;
   }
-  __device__ void store(int m, int n0, int q0, const float (&acc)[32]) const {
+  struct Pre { int row; float4 x; };
+  __device__ Pre pre(int m, int n) const {
+    return m < N ? Pre{pos[m], ldg4(Xl + (size_t)m * F + n)} : Pre{0, make_float4(0.f, 0.f, 0.f, 0.f)};
+  }
+  __device__ void emit(int m, int n, float4 v, const Pre &p) const {
     if (m >= N) return;
-    const size_t o = (size_t)m * F + n0 + q0;
-    const size_t od = (size_t)pos[m] * F + n0 + q0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      const float4 x = ldg4(Xl + o + i);
-      const float4 z = make_float4(x.x > 0.f ? acc[i] : 0.f, x.y > 0.f ? acc[i + 1] : 0.f,
-                                   x.z > 0.f ? acc[i + 2] : 0.f, x.w > 0.f ? acc[i + 3] : 0.f);
-      *reinterpret_cast<float4 *>(dZ + od + i) = z;
-      *reinterpret_cast<float4 *>(dZ_lo + od + i) = lo4(z);
-    }
+    const float4 x = p.x;
+    const float4 z = make_float4(x.x > 0.f ? v.x : 0.f, x.y > 0.f ? v.y : 0.f, x.z > 0.f ? v.z : 0.f,
+                                 x.w > 0.f ? v.w : 0.f);
+    const size_t od = (size_t)p.row * F + n;
+    *reinterpret_cast<float4 *>(dZ + od) = z;
+    *reinterpret_cast<float4 *>(dZ_lo + od) = lo4(z);
   }
 };
 
@@ -417,8 +474,9 @@ cudaError_t tconfigure() {
   return cudaFuncSetAttribute(k_tma<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize, t_smem_bytes<Op>());
 }
 template <class Op>
-void trun(cudaStream_t st, const TmaMaps &mp, const Op &op, int grid) {
-  launch_ex(k_tma<Op>, std::max(grid, 1), T_THREADS, t_smem_bytes<Op>(), st, mp, op);
+void trun(cudaStream_t st, const TmaMaps &mp, Op op, int items) {
+  op.items_cap = items;
+  launch_ex(k_tma<Op>, std::max(1, std::min(items, kSMs)), T_THREADS, t_smem_bytes<Op>(), st, mp, op);
   g_launches += 1;
 }
 int mt(int n) { return (n + T_BM - 1) / T_BM; }
@@ -439,7 +497,7 @@ void update_bn(cudaStream_t st, const Caps &c, int cmax, const float *A, const f
   const int K = 4 * c.H;
   const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, BN),
                    map2d(Wf_lo, (uint64_t)cmax * c.H, K, BN)};
-  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0};
+  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0, 0};
   trun(st, mp, op, tc_max_tiles(c, cmax) * (c.H / BN));
 }
 template <int BN>
@@ -447,7 +505,7 @@ void dA_bn(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const floa
            const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
   const TmaMaps mp{map2d(dZ, c.maxN, c.H, T_BM), map2d(dZ_lo, c.maxN, c.H, T_BM),
                    map2d(WbT, (uint64_t)cmax * 4 * c.H, c.H, BN), map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, c.H, BN)};
-  TDAC<BN> op{perm, info, tiles, dA, c.H, 0};
+  TDAC<BN> op{perm, info, tiles, dA, c.H, 0, 0};
   trun(st, mp, op, tc_max_tiles(c, cmax) * (4 * c.H / BN));
 }
 template <int BN>
@@ -455,7 +513,7 @@ void proj_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X
              const float *Mx, const float *Mx_lo, float *P) {
   const TmaMaps mp{map2d(X, c.maxN, F, T_BM), map2d(X_lo, c.maxN, F, T_BM), map2d(Mx, c.H, F, BN),
                    map2d(Mx_lo, c.H, F, BN)};
-  TProj<BN> op{blob, P, F, c.H, 0};
+  TProj<BN> op{blob, P, F, c.H, 0, 0};
   trun(st, mp, op, mt(c.maxN) * (c.H / BN));
 }
 template <int BN>
@@ -463,7 +521,7 @@ void dX_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP,
            const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo, const int *pos) {
   const TmaMaps mp{map2d(dP, c.maxN, c.H, T_BM), map2d(dP_lo, c.maxN, c.H, T_BM), map2d(MxT, F, c.H, BN),
                    map2d(MxT_lo, F, c.H, BN)};
-  TDX<BN> op{blob, Xl, dZ, dZ_lo, pos, c.H, F, 0};
+  TDX<BN> op{blob, Xl, dZ, dZ_lo, pos, c.H, F, 0, 0};
   trun(st, mp, op, mt(c.maxN) * (F / BN));
 }
 }  // namespace
