@@ -26,14 +26,19 @@ struct Plan {
   size_t blob_max = 0;
   size_t amp = 0, att = 0;
   std::vector<size_t> P, A, arg, X;  // X[l] = output of layer l (X_{l+1})
-  size_t dZa = 0, dZb = 0, dA = 0, dP = 0;
+  size_t dA = 0;
+  // per layer l: dZ[l] = dL/dX_l (class path: degree-sorted rows), dP[l], their lo
+  // terms and the dM_e block partials -- one buffer per layer so the side-stream
+  // readers never hold up the main chain (no write-after-read waits)
+  std::vector<size_t> dZ, dZ_lo, dPl, dPl_lo, pagg;
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
   size_t part = 0, part2 = 0, part3 = 0;  // scratch: agg_bwd (dM_e), Gram (dU), dM_x partials
   size_t UT = 0, u_off = 0;
   int cmax = 0;  // degree-class slots (0 = class GEMMs off)
   size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
   // direct-GEMM residuals x - trunc19(x) (class path): operands and weights
-  size_t A_lo = 0, X_lo = 0, dZa_lo = 0, dZb_lo = 0, dP_lo = 0, Wf_lo = 0, WbT_lo = 0;
+  size_t Wf_lo = 0, WbT_lo = 0, ones = 0;
+  std::vector<size_t> A_lo, X_lo;  // per layer (the backward Grams read them)
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t total = 0;
 };
@@ -66,10 +71,11 @@ Plan make_plan(const hg_config &c) {
     p.X.push_back(take(sizeof(float) * N * H));
   }
   const size_t Fmax = std::max<size_t>(H, c.f_node);
-  p.dZa = take(sizeof(float) * N * Fmax);
-  p.dZb = take(sizeof(float) * N * Fmax);
+  for (int l = 0; l < c.layers; ++l) {
+    p.dZ.push_back(take(sizeof(float) * N * Fmax));
+    p.dPl.push_back(take(sizeof(float) * N * H));
+  }
   p.dA = take(sizeof(float) * N * 4 * H);
-  p.dP = take(sizeof(float) * N * H);
   p.G = take(sizeof(float) * B * H);
   p.hpre = take(sizeof(float) * B * Hf);
   p.dhid = take(sizeof(float) * B * Hf);
@@ -95,20 +101,26 @@ Plan make_plan(const hg_config &c) {
     p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
     p.Wf_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
     p.WbT_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-    p.A_lo = take(sizeof(float) * N * 4 * H);
-    p.X_lo = take(sizeof(float) * N * H);
-    p.dZa_lo = take(sizeof(float) * N * H);
-    p.dZb_lo = take(sizeof(float) * N * H);
-    p.dP_lo = take(sizeof(float) * N * H);
+    for (int l = 0; l < c.layers; ++l) {
+      p.A_lo.push_back(take(sizeof(float) * N * 4 * H));
+      p.X_lo.push_back(take(sizeof(float) * N * H));
+    }
+    p.ones = take(sizeof(float) * N * 32);  // B operand of the column-sum tiles
+    for (int l = 0; l < c.layers; ++l) {
+      p.dZ_lo.push_back(take(sizeof(float) * N * H));
+      p.dPl_lo.push_back(take(sizeof(float) * N * H));
+    }
     p.Mx_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
     p.MxT = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
     p.MxT_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
     p.mx_off = take(sizeof(int64_t) * (size_t)c.layers);
-    pf = std::max(pf, tc_gram_partial_floats(caps, p.cmax));
+    pf = std::max({pf, tc_gram_partial_floats(caps, p.cmax), mn_gram_partial_floats(caps, p.cmax),
+                   mn_dmx_partial_floats(caps, H)});
     p.part = take(sizeof(float) * pf);  // (re-take: the class partials are larger)
   }
   p.part2 = take(sizeof(float) * pf);
   p.part3 = take(sizeof(float) * pf);
+  for (int l = 0; l < c.layers; ++l) p.pagg.push_back(take(sizeof(float) * agg_bwd_partial_floats(caps)));
   p.total = off;
   return p;
 }
@@ -136,6 +148,7 @@ struct hg_ctx {
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr;            // weight-gradient GEMMs beside the critical chain
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side;  // per layer fork / join points
+  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr;
   int64_t launches = 0;
   bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
   hg_status sticky = HG_OK;
@@ -242,20 +255,29 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   const bool cls = x->use_tc && p.cmax > 0;
   const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
   const size_t HH = (size_t)c.hidden * c.hidden;
+  // class weights (needs the degree classes) and M_x splits: on the side stream,
+  // concurrent with layer 0's projection and aggregation; joined before layer 0's update
+  const bool fork = cls && !pr && x->side_stream != nullptr;
+  cudaStream_t pst = fork ? x->side_stream : st;
+  if (fork) {
+    cudaEventRecord(x->ev_deg, st);
+    cudaStreamWaitEvent(pst, x->ev_deg, 0);
+  }
   if (cls)
     phase(pr, HG_PHASE_UPDATE, [&] {
-      launch_prep_W2(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
+      launch_prep_W2(pst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
                      reinterpret_cast<const DegInfo *>(x->b(p.deginfo)), x->f(p.Wf), x->f(p.Wf_lo), x->f(p.WbT),
                      x->f(p.WbT_lo));
-      launch_prep_Mx(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
+      launch_prep_Mx(pst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
                      x->f(p.Mx_lo), x->f(p.MxT), x->f(p.MxT_lo));
     });
+  if (fork) cudaEventRecord(x->ev_prep, pst);
   for (int l = 0; l < c.layers; ++l) {
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
     phase(pr, HG_PHASE_PROJ, [&] {
       if (cls && l > 0)
-        launch_d_proj(st, x->caps, blob, Xl, x->f(p.X_lo), F, x->param(lname(l, "M_x")),
+        launch_d_proj(st, x->caps, blob, Xl, x->f(p.X_lo[l - 1]), F, x->param(lname(l, "M_x")),
                       x->f(p.Mx_lo) + (size_t)(l - 1) * HH, x->f(p.P[l]));
       else if (x->use_tc && l > 0 && tc_proj_ok(x->caps, F))
         launch_tc_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
@@ -264,15 +286,17 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     });
     phase(pr, HG_PHASE_AGG_FWD, [&] {
       launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), cls ? x->f(p.A_lo) : nullptr, pos);
+                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), cls ? x->f(p.A_lo[l]) : nullptr, pos);
     });
+    if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_prep, 0);
     phase(pr, HG_PHASE_UPDATE, [&] {
       if (cls)
-        launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), x->f(p.A_lo), reinterpret_cast<const int *>(x->b(p.perm)),
+        launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), x->f(p.A_lo[l]),
+                            reinterpret_cast<const int *>(x->b(p.perm)),
                             reinterpret_cast<const DegInfo *>(x->b(p.deginfo)),
                             reinterpret_cast<const int4 *>(x->b(p.tiles)),
                             x->f(p.Wf) + (size_t)l * p.cmax * 4 * HH, x->f(p.Wf_lo) + (size_t)l * p.cmax * 4 * HH,
-                            x->param(lname(l, "b_U")), x->f(p.X[l]), x->f(p.X_lo));
+                            x->param(lname(l, "b_U")), x->f(p.X[l]), x->f(p.X_lo[l]));
       else if (x->use_tc)
         launch_tc_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")),
                          x->param(lname(l, "b_U")), x->f(p.X[l]));
@@ -282,12 +306,19 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     });
   }
   phase(pr, HG_PHASE_HEAD_FWD, [&] {
-    if (fuse_head_bwd)
+    if (fuse_head_bwd) {
       launch_head_fused(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
                         x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
-                        x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZa),
-                        cls ? x->f(p.dZa_lo) : nullptr, pos);
-    else
+                        x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZ[c.layers - 1]),
+                        cls ? x->f(p.dZ_lo[c.layers - 1]) : nullptr, pos);
+      // the loss value is an output only: reduce it on the side stream (joined at the end of the backward)
+      const bool fork = !pr && x->side_stream != nullptr;
+      if (fork) {
+        cudaEventRecord(x->ev_head, st);
+        cudaStreamWaitEvent(x->side_stream, x->ev_head, 0);
+      }
+      launch_loss(fork ? x->side_stream : st, blob, x->f(p.sqerr), x->f(p.loss));
+    } else
       launch_head_fwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
                       x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
                       x->f(p.sqerr), x->f(p.loss));
@@ -300,17 +331,29 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
   float *amp = x->f(p.amp), *att = x->f(p.att);
-  float *dZ = x->f(p.dZa), *dZn = x->f(p.dZb);
   const bool cls = x->use_tc && p.cmax > 0;
-  float *dZl = cls ? x->f(p.dZa_lo) : nullptr, *dZnl = cls ? x->f(p.dZb_lo) : nullptr;
+  float *dZ = x->f(p.dZ[c.layers - 1]), *dZl = cls ? x->f(p.dZ_lo[c.layers - 1]) : nullptr;
   const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
   const size_t HH = (size_t)c.hidden * c.hidden;
+  const bool fork = !pr && x->side_stream != nullptr;
+  cudaStream_t side = fork ? x->side_stream : st;
+  auto rec = [&](cudaEvent_t ev, cudaStream_t s) { if (fork) cudaEventRecord(ev, s); };
+  auto wait = [&](cudaStream_t s, cudaEvent_t ev) { if (fork) cudaStreamWaitEvent(s, ev, 0); };
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
-    launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"), x->f(p.G),
-                    x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
-                    x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), head_done, dZl, pos);
+    if (!head_done) {  // dZ of the last layer on the main stream
+      launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"),
+                      x->f(p.G), x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
+                      x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), false, dZl, pos, false);
+    }
+    rec(x->ev_head, st);
+    wait(side, x->ev_head);
+    g_low_prio = fork;
+    // head parameter gradients: off the critical chain
+    launch_head_grads(side, x->caps, blob, x->f(p.G), x->f(p.hpre), x->f(p.dy), x->f(p.dhid), x->grad("head.W1"),
+                        x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
+    g_low_prio = false;
   });
-  if (overlap_allreduce) enqueue_bucket(x, st, 0);
+  if (overlap_allreduce) enqueue_bucket(x, side, 0);
   const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
   const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
   if (x->use_tc && !cls)
@@ -323,19 +366,18 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   // main stream walks the critical chain dA -> agg_bwd -> dX of each layer.
   // Hazards: dX_l overwrites the dZ buffer Gram_{l+1} read; agg_bwd_l overwrites
   // the dP dM_x(l+1) read -> the main stream waits for the side events first.
-  const bool fork = !pr && x->side_stream != nullptr;
-  cudaStream_t side = fork ? x->side_stream : st;
-  auto rec = [&](cudaEvent_t ev, cudaStream_t s) { if (fork) cudaEventRecord(ev, s); };
-  auto wait = [&](cudaStream_t s, cudaEvent_t ev) { if (fork) cudaStreamWaitEvent(s, ev, 0); };
-  float *part_agg = x->f(p.part), *part_dU = x->f(p.part2), *part_dMx = x->f(p.part3);
+  float *part_dU = x->f(p.part2), *part_dMx = x->f(p.part3);
   for (int l = c.layers - 1; l >= 0; --l) {
+    dZ = x->f(p.dZ[l]);
+    dZl = cls ? x->f(p.dZ_lo[l]) : nullptr;
+    float *dP = x->f(p.dPl[l]), *dPlo = cls ? x->f(p.dPl_lo[l]) : nullptr, *pagg = x->f(p.pagg[l]);
     // ---- side: Gram (dU, db_U) as soon as dZ_l is ready
     rec(x->ev_dz[l], st);
     wait(side, x->ev_dz[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DU, [&] {
       if (cls)
-        launch_tc_dU_cls(side, x->caps, p.cmax, blob, dZ, x->f(p.A[l]), nullptr /* rows pre-sorted */, dinfo,
+        launch_mn_dU_cls(side, x->caps, p.cmax, dZ, dZl, x->f(p.A[l]), x->f(p.A_lo[l]), x->f(p.ones), dinfo,
                          reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
                          x->grad(lname(l, "b_U")));
       else if (x->use_tc)
@@ -345,7 +387,6 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         launch_dU(side, x->caps, blob, dZ, x->f(p.A[l]), amp, att, part_dU, x->grad(lname(l, "U")),
                   x->grad(lname(l, "b_U")));
     });
-    rec(x->ev_gram[l], side);
     g_low_prio = false;
     // ---- main: dA, aggregation backward
     phase(pr, HG_PHASE_DA, [&] {
@@ -358,43 +399,41 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       else
         launch_dA(st, x->caps, blob, dZ, amp, att, x->param(lname(l, "U")), x->f(p.dA));
     });
-    if (l + 1 < c.layers) wait(st, x->ev_side[l + 1]);  // dM_x(l+1) finished reading dP
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), x->f(p.dP), part_agg, x->grad(lname(l, "M_e")),
-                     cls && l > 0 ? x->f(p.dP_lo) : nullptr, pos);
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, cls && l > 0 ? dPlo : nullptr, pos);
     });
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
-    // ---- side: dM_x, db_M once dP_l is ready; then layer l's gradients are complete
+    // ---- side: dM_e, dM_x, db_M once dP_l is ready; then layer l's gradients are complete
     rec(x->ev_dp[l], st);
     wait(side, x->ev_dp[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
-      if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
-        launch_tc_dMx(side, x->caps, blob, x->f(p.dP), Xl, F, part_dMx, x->grad(lname(l, "M_x")),
-                      x->grad(lname(l, "b_M")));
+      launch_reduce_dMe(side, x->caps, pagg, x->grad(lname(l, "M_e")));
+      if (cls && l > 0)
+        launch_mn_dMx(side, x->caps, blob, dP, dPlo, Xl, x->f(p.X_lo[l - 1]), F, x->f(p.ones), part_dMx,
+                      x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+      else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
+        launch_tc_dMx(side, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else
-        launch_dMx(side, x->caps, blob, x->f(p.dP), Xl, F, part_dMx, x->grad(lname(l, "M_x")),
-                   x->grad(lname(l, "b_M")));
+        launch_dMx(side, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
     });
     g_low_prio = false;
     if (overlap_allreduce) enqueue_bucket(x, side, c.layers - l);  // conv l gradients complete
     rec(x->ev_side[l], side);
-    // ---- main: dX into the other dZ buffer
+    // ---- main: dX into dZ[l-1]
     if (l > 0) {
-      if (l + 1 < c.layers) wait(st, x->ev_gram[l + 1]);  // Gram_{l+1} finished reading dZn
+      float *dZn = x->f(p.dZ[l - 1]), *dZnl = cls ? x->f(p.dZ_lo[l - 1]) : nullptr;
       phase(pr, HG_PHASE_DX, [&] {
         if (cls)
-          launch_d_dX(st, x->caps, blob, x->f(p.dP), x->f(p.dP_lo), x->f(p.MxT) + (size_t)(l - 1) * HH,
+          launch_d_dX(st, x->caps, blob, dP, dPlo, x->f(p.MxT) + (size_t)(l - 1) * HH,
                       x->f(p.MxT_lo) + (size_t)(l - 1) * HH, F, Xl, dZn, dZnl, pos);
         else if (x->use_tc && F % 64 == 0)
-          launch_tc_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn);
+          launch_tc_dX(st, x->caps, blob, dP, x->param(lname(l, "M_x")), F, Xl, dZn);
         else
-          launch_dX(st, x->caps, blob, x->f(p.dP), x->param(lname(l, "M_x")), F, Xl, dZn);
+          launch_dX(st, x->caps, blob, dP, x->param(lname(l, "M_x")), F, Xl, dZn);
       });
-      std::swap(dZ, dZn);
-      std::swap(dZl, dZnl);
     }
   }
   wait(st, x->ev_side[0]);  // join: every gradient is complete on the main stream
@@ -508,6 +547,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
+  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep})
+    if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
     for (int l = 0; l < c->layers; ++l) {
       cudaEvent_t ev;
@@ -541,6 +582,13 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     if ((e = cudaMemcpyAsync(x->b(plan.u_off), uo.data(), sizeof(int64_t) * uo.size(), cudaMemcpyHostToDevice,
                              x->stream)) != cudaSuccess)
       return bail(e, "cudaMemcpyAsync");
+    if (plan.cmax) {
+      std::vector<float> one((size_t)c->max_nodes * 32, 1.0f);
+      if ((e = cudaMemcpyAsync(x->b(plan.ones), one.data(), sizeof(float) * one.size(), cudaMemcpyHostToDevice,
+                               x->stream)) != cudaSuccess)
+        return bail(e, "cudaMemcpyAsync");
+      if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
+    }
     if (plan.mx_off) {
       std::vector<int64_t> mo;
       for (int l = 0; l < c->layers; ++l)
@@ -570,6 +618,8 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->side_stream) cudaStreamDestroy(x->side_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
     for (auto ev : *v) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep})
+    if (ev) cudaEventDestroy(ev);
   if (x->comm) ncclCommDestroy(x->comm);
   for (auto ev : x->bucket_ready) cudaEventDestroy(ev);
   if (x->comm_done) cudaEventDestroy(x->comm_done);
@@ -660,7 +710,7 @@ hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t st
   const size_t PB = sizeof(float) * (size_t)x->n_params;
   if (m && (st = copy_arena(x, x->f(x->plan.m), m, PB, on_device, true))) return st;
   if (v && (st = copy_arena(x, x->f(x->plan.v), v, PB, on_device, true))) return st;
-  AdamDev ad{step, 0.f, 0.f};
+  AdamDev ad{step, 0, 0};
   CK(x, cudaMemcpyAsync(x->b(x->plan.adam), &ad, sizeof(ad), cudaMemcpyHostToDevice, x->stream));
   CK(x, cudaStreamSynchronize(x->stream));
   return HG_OK;

@@ -25,7 +25,7 @@
 namespace hg {
 
 std::atomic<int64_t> g_launches{0};
-bool g_pdl = true;
+bool g_pdl = false;  // HG_PDL=1: early launch starves the side stream (measured slower)
 bool g_low_prio = false;
 int g_prio_lo = 0, g_prio_hi = 0;
 static inline void counted(int n = 1) { g_launches += n; }
@@ -645,8 +645,13 @@ void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
   else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
   else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
   counted();
+  if (dMe) launch_reduce_dMe(st, c, partial, dMe);
+}
+
+void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe) {
   const int count = c.H * c.Fe;
-  launch_ex(k_reduce_rows, std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st, partial, agg_bwd_blocks(c), count, dMe);
+  launch_ex(k_reduce_rows, std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st, partial, agg_bwd_blocks(c),
+            count, dMe);
   counted();
 }
 
@@ -819,6 +824,9 @@ void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, cons
                        const int *pos) {
   head_launch<true, true>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy, dhid, dZL, dZL_lo, pos);
   counted();
+}
+
+void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float *loss) {
   launch_ex(k_loss, 1, 256, 0, st, blob, sqerr, loss);
   counted();
 }
@@ -856,37 +864,43 @@ __global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__re
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
                      float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done,
-                     float *dZL_lo, const int *pos) {
+                     float *dZL_lo, const int *pos, bool with_grads) {
   if (!head_done) {
     head_launch<false, true>(st, c, blob, XL, W1, nullptr, W2, nullptr, nullptr, const_cast<float *>(hpre),
                              const_cast<float *>(yhat), nullptr, dy, dhid, dZL, dZL_lo, pos);
     counted();
   }
+  if (with_grads) launch_head_grads(st, c, blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2);
+}
+
+void launch_head_grads(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *G, const float *hpre,
+                       const float *dy, const float *dhid, float *gW1, float *gb1, float *gW2, float *gb2) {
   const int total = c.Hf * c.H + 2 * c.Hf + 1;
-  launch_ex(k_head_grads, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2,
-                                                                       c.H, c.Hf);
+  launch_ex(k_head_grads, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, blob, G, hpre, dy, dhid, gW1, gb1, gW2,
+            gb2, c.H, c.Hf);
   counted();
 }
 
 // ------------------------------------------------------------------ K10 AdamW
 // theta <- theta (1 - lr wd); m <- b1 m + (1-b1) g; v <- b2 v + (1-b2) g^2;
 // theta <- theta - (lr/bc1) m / (sqrt(v)/sqrt(bc2) + eps)
-__global__ void k_adam_prep(AdamDev *ad, float lr, float beta1, float beta2) {
-  pdl_enter();
-  const int64_t t = ad->step + 1;
-  ad->step = t;
-  const double bc1 = 1.0 - pow((double)beta1, (double)t);
-  const double bc2 = 1.0 - pow((double)beta2, (double)t);
-  ad->step_size = (float)((double)lr / bc1);
-  ad->inv_sqrt_bc2 = (float)(1.0 / sqrt(bc2));
-}
 
 __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const float4 *__restrict__ g,
                                                float4 *__restrict__ m, float4 *__restrict__ v, int64_t n4,
-                                               const AdamDev *__restrict__ ad, float lr, float beta1,
+                                               const AdamDev *ad, float lr, float beta1,
                                                float beta2, float eps, float wd) {
   pdl_enter();
-  const float ss = ad->step_size, ib = ad->inv_sqrt_bc2;
+  // bias corrections of step t = ad->step + 1 (fp64 as the oracle), once per block
+  __shared__ float s_ss, s_ib;
+  const int64_t t = ad->step + 1;
+  if (threadIdx.x == 0) {
+    const double bc1 = 1.0 - pow((double)beta1, (double)t);
+    const double bc2 = 1.0 - pow((double)beta2, (double)t);
+    s_ss = (float)((double)lr / bc1);
+    s_ib = (float)(1.0 / sqrt(bc2));
+  }
+  __syncthreads();
+  const float ss = s_ss, ib = s_ib;
   const float decay = 1.0f - lr * wd;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
     float4 P = p[i], Gv = g[i], Mv = m[i], Vv = v[i];
@@ -901,12 +915,19 @@ __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const flo
     }
     p[i] = P; m[i] = Mv; v[i] = Vv;
   }
+  // every block has read ad->step above; the last block to finish advances it
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    AdamDev *w = const_cast<AdamDev *>(ad);
+    if (atomicAdd(&w->ticket, 1) == (int)gridDim.x - 1) {
+      w->step = t;
+      w->ticket = 0;
+    }
+  }
 }
 
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
                   float lr, float beta1, float beta2, float eps, float wd) {
-  launch_ex(k_adam_prep, 1, 1, 0, st, ad, lr, beta1, beta2);
-  counted();
   const int64_t n4 = n / 4;
   const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, kSMs * 8);
   launch_ex(k_adamw, blocks, 256, 0, st, reinterpret_cast<float4 *>(p), reinterpret_cast<const float4 *>(g),

@@ -46,6 +46,8 @@ void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
                     float *partial, float *dMe, float *dP_lo = nullptr, const int *pos = nullptr);
+// dM_e = fixed-order sum of launch_agg_bwd's block partials (launch_agg_bwd does it when dMe != null)
+void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe);
 size_t agg_bwd_partial_floats(const Caps &c);
 size_t dU_partial_floats(const Caps &c);
 size_t dMx_partial_floats(const Caps &c, int F);
@@ -54,8 +56,8 @@ size_t dMx_partial_floats(const Caps &c, int F);
 void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
                      float *sqerr, float *loss);
-// K5+K6 fused (a training step): pool, head forward, loss terms and the head/pool
-// backward down to dZ of the last layer
+// K5+K6 fused (a training step): pool, head forward, per-graph loss terms and the
+// head/pool backward down to dZ of the last layer (the loss itself: launch_loss)
 void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                        const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
                        float *sqerr, float *loss, float *dy, float *dhid, float *dZL, float *dZL_lo = nullptr,
@@ -64,13 +66,18 @@ void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, cons
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
                      float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done,
-                     float *dZL_lo = nullptr, const int *pos = nullptr);
+                     float *dZL_lo = nullptr, const int *pos = nullptr, bool with_grads = true);
+// head parameter gradients only (the tail of launch_head_bwd)
+void launch_head_grads(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *G, const float *hpre,
+                       const float *dy, const float *dhid, float *gW1, float *gb1, float *gW2, float *gb2);
+// mean squared error over the batch from the per-graph terms (after launch_head_fused)
+void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float *loss);
 void head_configure(const Caps &c);
 
 // K10: AdamW over the flat arena
 struct AdamDev {
   int64_t step;
-  float step_size, inv_sqrt_bc2;
+  int32_t ticket, pad;  // blocks finished in the running k_adamw (the last one advances step)
 };
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
                   float lr, float beta1, float beta2, float eps, float wd);
@@ -119,6 +126,17 @@ void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const i
                     float *Mx_lo, float *MxT, float *MxT_lo);
 void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
                     const DegInfo *info, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo);
+
+// TMA-fed MN-major Grams (tcmn.cu): per-class-split dU / db_U and per-split dM_x / db_M,
+// partials reduced in fixed order (class path; rows of dZ / A degree-sorted)
+size_t mn_gram_partial_floats(const Caps &c, int cmax);
+size_t mn_dmx_partial_floats(const Caps &c, int F);
+void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const float *A,
+                      const float *A_lo, const float *ones, const DegInfo *info, const int4 *splits, float *partial,
+                      float *dU, float *dbU);
+void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
+                   const float *X, const float *X_lo, int F, const float *ones, float *partial, float *dMx,
+                   float *dbM);
 
 // tcgen05 3xTF32 GEMMs (tcgemm.cu); require H % 128 == 0
 bool tc_supported(const Caps &c);

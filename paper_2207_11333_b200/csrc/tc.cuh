@@ -99,6 +99,16 @@ __device__ __forceinline__ uint64_t desc_sw128_mn(uint32_t saddr, uint32_t lbo, 
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1u << 46) | ((uint64_t)2u << 61);
 }
 
+// shared-memory descriptor: MN-major, SWIZZLE_128B_BASE32B (layout type 1) -- the
+// tf32 MN-major layout: atom = 4 k-rows x 128 bytes (32 fp32 along MN) with 32-byte
+// granules XOR (k-row % 4) (TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B writes exactly
+// this). LBO = byte stride between 32-element MN blocks, SBO = between 4-row k groups.
+// Verified bit-exact on B200 by tools/exp/mn_major.cu.
+__device__ __forceinline__ uint64_t desc_mn32(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | ((uint64_t)1u << 46) | ((uint64_t)1u << 61);
+}
+
 // byte offset of the 16-byte chunk holding MN elements [4c, 4c+4) of MN block b at
 // k-row kr (0..31 within a 32-k stage) in an MN-major SW128 tile with nblk MN blocks
 __device__ __forceinline__ uint32_t sw128_mn_off(int b, int c, int kr, int nblk) {

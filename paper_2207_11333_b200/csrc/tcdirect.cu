@@ -31,16 +31,13 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "tc.cuh"
+#include "tma.h"
 
 namespace hg {
 
 extern std::atomic<int64_t> g_launches;
 int g_tma_bn = 64;  // output-tile width of the TMA GEMMs (HG_TMA_BN=128 for A/B runs)
 
-// the four operand tensor maps of one launch (kernel parameter, __grid_constant__)
-struct TmaMaps {
-  CUtensorMap ah, al, bh, bl;
-};
 
 // experiments only: per-CTA %globaltimer trace of one Op type (hg_debug_set_trace)
 __device__ unsigned long long *g_trace = nullptr;
@@ -440,24 +437,28 @@ struct MapEntry {
   const void *p;
   uint64_t rows, cols;
   uint32_t box;
+  bool mn;
   CUtensorMap m;
 };
 std::vector<MapEntry> g_maps;
+}  // namespace
 
 // row-major fp32 [rows][cols] (cols contiguous, rows 16-byte aligned); box = box_rows x 32
-// fp32 (one 128-byte swizzle row), SWIZZLE_128B, out-of-range elements read as zero.
-// Encoded on the host once per (pointer, shape, box) and cached.
-CUtensorMap map2d(const float *p, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+// fp32 (one 128-byte row), out-of-range elements read as zero. Swizzle: SWIZZLE_128B
+// for K-major operand tiles, SWIZZLE_128B_ATOM_32B for MN-major ones (the only tf32
+// MN-major layout tcgen05 accepts). Encoded on the host once per argument set and cached.
+CUtensorMap tma_map2d(const float *p, uint64_t rows, uint64_t cols, uint32_t box_rows, bool mn_major) {
   std::lock_guard<std::mutex> g(g_map_mu);
   for (const auto &e : g_maps)
-    if (e.p == p && e.rows == rows && e.cols == cols && e.box == box_rows) return e.m;
-  MapEntry e{p, rows, cols, box_rows, {}};
+    if (e.p == p && e.rows == rows && e.cols == cols && e.box == box_rows && e.mn == mn_major) return e.m;
+  MapEntry e{p, rows, cols, box_rows, mn_major, {}};
   const cuuint64_t dims[2] = {cols, std::max<uint64_t>(rows, 1)};
   const cuuint64_t strides[1] = {cols * sizeof(float)};
   const cuuint32_t box[2] = {32, box_rows};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = g_encode(&e.m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(p), dims, strides, box, es,
-                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {  // shapes are validated at context creation: this is an internal invariant
     fprintf(stderr, "hgnn: cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%u\n", (int)r,
@@ -467,6 +468,11 @@ CUtensorMap map2d(const float *p, uint64_t rows, uint64_t cols, uint32_t box_row
   if (g_maps.size() > 4096) g_maps.clear();
   g_maps.push_back(e);
   return e.m;
+}
+
+namespace {
+CUtensorMap map2d(const float *p, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+  return tma_map2d(p, rows, cols, box_rows, false);
 }
 
 template <class Op>
@@ -527,18 +533,19 @@ void dX_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP,
 }  // namespace
 
 cudaError_t tcd_configure() {
+  cudaError_t e;
   if (!g_encode) {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
     if (e != cudaSuccess) return e;
     if (q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   if (const char *v = getenv("HG_TMA_BN")) g_tma_bn = atoi(v) == 128 ? 128 : 64;
-  cudaError_t e;
   if ((e = tconfigure_bn<64>()) != cudaSuccess) return e;
-  return tconfigure_bn<128>();
+  if ((e = tconfigure_bn<128>()) != cudaSuccess) return e;
+  return tmn_configure();
 }
 
 void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,

@@ -1,0 +1,343 @@
+// tcmn.cu — TMA-fed 3xTF32 tcgen05 GEMMs with BOTH operands MN-major: the
+// weight-gradient Grams that contract over nodes,
+//   G_c = dZ_c^T A_c  (per degree class split, SURVEY §8(a9) / reassociation G3)
+//   dM_x = dP^T X     (per node split)
+// Operands are node-row tensors read as-is: a TMA box {32 features, 32 nodes}
+// lands as one MN-major SWIZZLE_128B_BASE32B block (CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B),
+// so there is no transpose or transform stage. Column sums (db_U, db_M) come from
+// an extra N=32 tile whose B operand is a ones matrix: D = sum_k a[k][m] * 1.
+// K (node) ranges end inside a 32-row chunk: the MMA skips whole 8-row k-steps
+// past the end and the MMA warp zeroes the (<= 7) trailing rows of the last one.
+//   warps 0-3 epilogue (TMEM -> staging -> coalesced partial stores)
+//   warp 4    TMA producer      warp 5  TMEM alloc, tail fix-up, MMA issue
+// Persistent over (split, m-tile, n-tile) items; double-buffered accumulators.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <atomic>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+#include "tma.h"
+
+namespace hg {
+
+extern std::atomic<int64_t> g_launches;
+
+namespace {
+
+constexpr int N_BM = 128;          // output rows (features of the A operand) per tile
+constexpr int N_BK = 32;           // nodes per chunk
+constexpr int N_BOX = N_BK * 128;  // one MN block: 32 k-rows x 128 bytes
+constexpr int N_TMA_WARP = 4, N_MMA_WARP = 5, N_THREADS = 192;
+constexpr int N_STG_LD = 36;
+constexpr int N_STG_BYTES = 4 * 32 * N_STG_LD * 4;
+
+template <class Op>
+constexpr int n_stage_bytes() { return 2 * 4 * N_BOX + 2 * (Op::BN / 32) * N_BOX; }
+template <class Op>
+constexpr int n_stages() {
+  return (224 * 1024 - N_STG_BYTES) / n_stage_bytes<Op>() < 6 ? (224 * 1024 - N_STG_BYTES) / n_stage_bytes<Op>() : 6;
+}
+template <class Op>
+constexpr int n_smem_bytes() {
+  return n_stages<Op>() * n_stage_bytes<Op>() + N_STG_BYTES + 1024 + 8 * (3 * n_stages<Op>() + 4) + 16;
+}
+
+struct MnItem {
+  int m0, n0, k0, len, sp, cs;  // cs: column-sum tile (B = ones, MMA N = 32)
+};
+
+}  // namespace
+
+// maps: ah/al = A operand (rows = nodes, cols = M features), bh/bl = B operand
+// (cols = N features); ones map rides in a second parameter.
+template <class Op>
+__global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ TmaMaps mp,
+                                                      const __grid_constant__ CUtensorMap ones, Op op_in) {
+  constexpr int BN = Op::BN, ST = n_stages<Op>(), NB = BN / 32;
+  constexpr int A_BYTES = 4 * N_BOX, B_BYTES = NB * N_BOX, STAGE = n_stage_bytes<Op>();
+  constexpr int TCOLS = 2 * BN <= 256 ? 256 : 512;
+  static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256 && ST >= 2, "tile");
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  float *stg_all = reinterpret_cast<float *>(smem + ST * STAGE);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE + N_STG_BYTES);
+  uint64_t *empty = full + ST;
+  uint64_t *accf = empty + ST;
+  uint64_t *acce = accf + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acce + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == N_MMA_WARP) tc::tmem_alloc<TCOLS>(tmem_holder);
+  if (threadIdx.x == N_TMA_WARP * 32) {
+    tc::tma_prefetch_desc(&mp.ah);
+    tc::tma_prefetch_desc(&mp.al);
+    tc::tma_prefetch_desc(&mp.bh);
+    tc::tma_prefetch_desc(&mp.bl);
+    tc::tma_prefetch_desc(&ones);
+    for (int s = 0; s < ST; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&accf[b], 1);
+      tc::mbar_init(&acce[b], 4);
+    }
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_holder;
+  pdl_enter();
+
+  Op op = op_in;
+  const int items = op.items_cap;
+  if (warp == N_TMA_WARP) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      int it = 0;
+      for (int t = blockIdx.x; t < items; t += gridDim.x) {
+        MnItem w;
+        if (!op.item(t, w)) continue;
+        const int nch = (w.len + N_BK - 1) / N_BK;
+        for (int c = 0; c < nch; ++c, ++it) {
+          const int s = it % ST;
+          if (it >= ST) tc::mbar_wait(&empty[s], ((it / ST) - 1) & 1);
+          uint8_t *sa = smem + s * STAGE;
+          const int k = w.k0 + c * N_BK;
+          tc::mbar_expect_tx(&full[s], 2 * A_BYTES + (w.cs ? N_BOX : 2 * B_BYTES));
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            tc::tma_load_2d(sa + b * N_BOX, &mp.ah, w.m0 + 32 * b, k, &full[s]);
+            tc::tma_load_2d(sa + A_BYTES + b * N_BOX, &mp.al, w.m0 + 32 * b, k, &full[s]);
+          }
+          uint8_t *sb = sa + 2 * A_BYTES;
+          if (w.cs) {
+            tc::tma_load_2d(sb, &ones, 0, k, &full[s]);
+          } else {
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+              tc::tma_load_2d(sb + b * N_BOX, &mp.bh, w.n0 + 32 * b, k, &full[s]);
+              tc::tma_load_2d(sb + B_BYTES + b * N_BOX, &mp.bl, w.n0 + 32 * b, k, &full[s]);
+            }
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == N_MMA_WARP) {
+    // ---------------- MMA issuer (warp-wide loop; lane 0 issues). A partial last chunk
+    // is fixed in place first: the warp zeroes its k-rows [rem, ceil8(rem)) in every
+    // box loaded (rows past ceil8(rem) are skipped as whole k-steps) and makes the
+    // generic-proxy writes visible to the tensor core with fence.proxy.async.
+    constexpr uint32_t idesc = tc::idesc_tf32(N_BM, BN, true, true);
+    constexpr uint32_t idesc_cs = tc::idesc_tf32(N_BM, 32, true, true);
+    int it = 0, tcount = 0;
+    for (int t = blockIdx.x; t < items; t += gridDim.x) {
+      MnItem w;
+      if (!op.item(t, w)) continue;
+      const int buf = tcount & 1;
+      if (tcount >= 2) tc::mbar_wait(&acce[buf], ((tcount >> 1) - 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t d = tmem + (uint32_t)(buf * BN);
+      const int nch = (w.len + N_BK - 1) / N_BK;
+      for (int c = 0; c < nch; ++c, ++it) {
+        const int s = it % ST;
+        const int rem = w.len - c * N_BK;
+        const int nks = rem >= N_BK ? N_BK / 8 : (rem + 7) / 8;
+        tc::mbar_wait(&full[s], (it / ST) & 1);
+        uint8_t *sa = smem + s * STAGE;
+        if (rem < N_BK && (rem & 7)) {
+          const int nrow = ((rem + 7) & ~7) - rem;
+          const int nbox = 8 + (w.cs ? 1 : 2 * NB);  // A hi/lo + B boxes actually loaded
+          for (int e = lane; e < nbox * nrow * 8; e += 32) {
+            const int bx = e / (nrow * 8), r = rem + (e / 8) % nrow, ch = e % 8;
+            *reinterpret_cast<float4 *>(sa + bx * N_BOX + r * 128 + ch * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          tc::fence_proxy_async_smem();
+        }
+        __syncwarp();
+        tc::fence_after_sync();
+        if (lane == 0) {
+          const uint32_t aH = tc::smem_u32(sa), aL = aH + A_BYTES;
+          const uint32_t bH = aL + A_BYTES, bL = bH + B_BYTES;
+          for (int ks = 0; ks < nks; ++ks) {
+            const uint32_t off = ks * 1024;  // 8 k-rows = two 4-row groups
+            const uint64_t dah = tc::desc_mn32(aH + off, N_BOX, 512), dal = tc::desc_mn32(aL + off, N_BOX, 512);
+            const uint64_t dbh = tc::desc_mn32(bH + off, N_BOX, 512);
+            const uint32_t acc = (c | ks) != 0;
+            if (w.cs) {
+              tc::mma_tf32(d, dah, dbh, idesc_cs, acc);
+              tc::mma_tf32(d, dal, dbh, idesc_cs, 1u);
+            } else {
+              const uint64_t dbl = tc::desc_mn32(bL + off, N_BOX, 512);
+              tc::mma_tf32(d, dah, dbh, idesc, acc);
+              tc::mma_tf32(d, dah, dbl, idesc, 1u);
+              tc::mma_tf32(d, dal, dbh, idesc, 1u);
+            }
+          }
+          tc::mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) tc::mma_commit(&accf[buf]);
+      __syncwarp();
+      ++tcount;
+    }
+  } else {
+    // ---------------- epilogue
+    float *stg = stg_all + warp * 32 * N_STG_LD;
+    int tcount = 0;
+    for (int t = blockIdx.x; t < items; t += gridDim.x) {
+      MnItem w;
+      if (!op.item(t, w)) continue;
+      const int buf = tcount & 1;
+      tc::mbar_wait(&accf[buf], (tcount >> 1) & 1);
+      tc::fence_after_sync();
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * BN);
+      if (w.cs) {  // column sums: every column of the N=32 tile holds the same value
+        float acc[32];
+        tc::tmem_ld32(trow, acc);
+        op.emit_cs(w, w.m0 + warp * 32 + lane, acc[0]);
+      } else {
+#pragma unroll 1
+        for (int q = 0; q < BN / 32; ++q) {
+          float acc[32];
+          tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4 *>(stg + lane * N_STG_LD + 4 * j) =
+                make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = 4 * j + (lane >> 3), cc = 4 * (lane & 7);
+            op.emit(w, w.m0 + warp * 32 + r, w.n0 + q * 32 + cc,
+                    *reinterpret_cast<const float4 *>(stg + r * N_STG_LD + cc));
+          }
+          __syncwarp();
+        }
+      }
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acce[buf]);
+      ++tcount;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == N_MMA_WARP) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<TCOLS>(tmem);
+  }
+}
+
+// ---------------------------------------------------------------- ops
+// per-class-split Gram: part[sp][h][n] = sum_{k in split} dZ[k][h] A[k][n] (rows
+// degree-sorted, so a split is a contiguous row range), cs[sp][h] = sum_k dZ[k][h]
+struct MnGram {
+  static constexpr int BN = 128;
+  const DegInfo *info; const int4 *splits; float *part, *cs; int H; int items_cap;
+  __device__ bool item(int t, MnItem &w) const {
+    const int NT = 4 * H / BN + 1, MT = H / N_BM;
+    const int nt = t % NT, mt = (t / NT) % MT, sp = t / (NT * MT);
+    if (sp >= info->S) return false;
+    const int4 s = splits[sp];
+    w = MnItem{mt * N_BM, nt * BN, s.y, s.z, sp, nt == NT - 1};
+    return true;
+  }
+  __device__ void emit(const MnItem &w, int m, int n, float4 v) const {
+    *reinterpret_cast<float4 *>(part + ((size_t)w.sp * H + m) * 4 * H + n) = v;
+  }
+  __device__ void emit_cs(const MnItem &w, int m, float v) const { cs[(size_t)w.sp * H + m] = v; }
+};
+
+// dM_x partials over node splits: part[sp][h][f] = sum_{k in split} dP[k][h] X[k][f]; cs = sum_k dP[k][h]
+constexpr int kMnDMxSplits = 32;
+struct MnDMx {
+  static constexpr int BN = 128;
+  const uint8_t *blob; float *part, *cs; int H, F; int items_cap;
+  __device__ bool item(int t, MnItem &w) const {
+    const int NT = F / BN + 1, MT = H / N_BM;
+    const int nt = t % NT, mt = (t / NT) % MT, sp = t / (NT * MT);
+    const int N = batch_N(blob);
+    int kc = (N + kMnDMxSplits - 1) / kMnDMxSplits;
+    kc = (kc + N_BK - 1) / N_BK * N_BK;
+    const int k0 = sp * kc, len = min(N - k0, kc);
+    w = MnItem{mt * N_BM, nt * BN, k0, len, sp, nt == NT - 1};
+    return sp < kMnDMxSplits && len > 0;
+  }
+  __device__ void emit(const MnItem &w, int m, int n, float4 v) const {
+    *reinterpret_cast<float4 *>(part + ((size_t)w.sp * H + m) * F + n) = v;
+  }
+  __device__ void emit_cs(const MnItem &w, int m, float v) const { cs[(size_t)w.sp * H + m] = v; }
+};
+
+// reductions (tcgemm.cu / kernels.cu)
+__global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInfo *__restrict__ info,
+                                    const int4 *__restrict__ splits, int H, float *__restrict__ dU);
+__global__ void k_reduce_splits_rows(const float *__restrict__ cs, const DegInfo *__restrict__ info, int H,
+                                     float *__restrict__ out);
+__global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
+__global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
+
+namespace {
+template <class Op>
+void nrun(cudaStream_t st, const TmaMaps &mp, const CUtensorMap &ones, Op op, int items) {
+  op.items_cap = items;
+  launch_ex(k_tmn<Op>, std::max(1, std::min(items, kSMs)), N_THREADS, n_smem_bytes<Op>(), st, mp, ones, op);
+  g_launches += 1;
+}
+}  // namespace
+
+cudaError_t tmn_configure() {
+  cudaError_t e = cudaFuncSetAttribute(k_tmn<MnGram>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       n_smem_bytes<MnGram>());
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_tmn<MnDMx>, cudaFuncAttributeMaxDynamicSharedMemorySize, n_smem_bytes<MnDMx>());
+}
+
+size_t mn_gram_partial_floats(const Caps &c, int cmax) {
+  const size_t S = (size_t)tc_max_splits(c, cmax);
+  return S * c.H * 4 * c.H + S * c.H;
+}
+size_t mn_dmx_partial_floats(const Caps &c, int F) { return (size_t)kMnDMxSplits * c.H * (F + 1); }
+
+void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const float *A,
+                      const float *A_lo, const float *ones, const DegInfo *info, const int4 *splits, float *partial,
+                      float *dU, float *dbU) {
+  const int smax = tc_max_splits(c, cmax);
+  const int total = c.H * 4 * c.H;
+  float *cs = partial + (size_t)smax * total;
+  const TmaMaps mp{tma_map2d(dZ, c.maxN, c.H, N_BK, true), tma_map2d(dZ_lo, c.maxN, c.H, N_BK, true),
+                   tma_map2d(A, c.maxN, 4 * c.H, N_BK, true), tma_map2d(A_lo, c.maxN, 4 * c.H, N_BK, true)};
+  const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
+  MnGram op{info, splits, partial, cs, c.H, 0};
+  nrun(st, mp, om, op, smax * (c.H / N_BM) * (4 * c.H / MnGram::BN + 1));
+  launch_ex(k_reduce_dU_classes, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, info, splits, c.H, dU);
+  launch_ex(k_reduce_splits_rows, cdiv(c.H, 8), 256, 0, st, cs, info, c.H, dbU);
+  g_launches += 2;
+}
+
+void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
+                   const float *X, const float *X_lo, int F, const float *ones, float *partial, float *dMx,
+                   float *dbM) {
+  const int count = c.H * F;
+  float *cs = partial + (size_t)kMnDMxSplits * count;
+  const TmaMaps mp{tma_map2d(dP, c.maxN, c.H, N_BK, true), tma_map2d(dP_lo, c.maxN, c.H, N_BK, true),
+                   tma_map2d(X, c.maxN, F, N_BK, true), tma_map2d(X_lo, c.maxN, F, N_BK, true)};
+  const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
+  MnDMx op{blob, partial, cs, c.H, F, 0};
+  nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * (F / MnDMx::BN + 1));
+  launch_ex(k_reduce_parts, std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st, partial, kMnDMxSplits, count, dMx);
+  launch_ex(k_reduce_rows, cdiv(c.H, 8), 256, 0, st, cs, kMnDMxSplits, c.H, dbM);
+  g_launches += 2;
+}
+
+}  // namespace hg
