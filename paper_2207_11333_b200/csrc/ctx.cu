@@ -146,7 +146,7 @@ struct hg_ctx {
   cudaStream_t comm_stream = nullptr;           // bucketed allreduce overlapping the backward
   std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
   cudaEvent_t comm_done = nullptr;
-  cudaStream_t side_stream = nullptr;            // weight-gradient GEMMs beside the critical chain
+  cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side;  // per layer fork / join points
   cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr;
   int64_t launches = 0;
@@ -336,7 +336,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
   const size_t HH = (size_t)c.hidden * c.hidden;
   const bool fork = !pr && x->side_stream != nullptr;
-  cudaStream_t side = fork ? x->side_stream : st;
+  cudaStream_t side = fork ? x->side_stream : st, side2 = fork ? x->side2_stream : st;
   auto rec = [&](cudaEvent_t ev, cudaStream_t s) { if (fork) cudaEventRecord(ev, s); };
   auto wait = [&](cudaStream_t s, cudaEvent_t ev) { if (fork) cudaStreamWaitEvent(s, ev, 0); };
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
@@ -366,7 +366,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   // main stream walks the critical chain dA -> agg_bwd -> dX of each layer.
   // Hazards: dX_l overwrites the dZ buffer Gram_{l+1} read; agg_bwd_l overwrites
   // the dP dM_x(l+1) read -> the main stream waits for the side events first.
-  float *part_dU = x->f(p.part2), *part_dMx = x->f(p.part3);
+  float *part_dU = x->f(p.part2), *part_dMx = x->f(p.part3);  // (one per side stream)
   for (int l = c.layers - 1; l >= 0; --l) {
     dZ = x->f(p.dZ[l]);
     dZl = cls ? x->f(p.dZ_lo[l]) : nullptr;
@@ -375,7 +375,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     rec(x->ev_dz[l], st);
     wait(side, x->ev_dz[l]);
     g_low_prio = fork;
-    phase(pr, HG_PHASE_DU, [&] {
+    phase(pr, HG_PHASE_DU, [&] {  // (side stream 1)
       if (cls)
         launch_mn_dU_cls(side, x->caps, p.cmax, dZ, dZl, x->f(p.A[l]), x->f(p.A_lo[l]), x->f(p.ones), dinfo,
                          reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
@@ -387,6 +387,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         launch_dU(side, x->caps, blob, dZ, x->f(p.A[l]), amp, att, part_dU, x->grad(lname(l, "U")),
                   x->grad(lname(l, "b_U")));
     });
+    rec(x->ev_gram[l], side);
     g_low_prio = false;
     // ---- main: dA, aggregation backward
     phase(pr, HG_PHASE_DA, [&] {
@@ -405,23 +406,29 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     });
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
-    // ---- side: dM_e, dM_x, db_M once dP_l is ready; then layer l's gradients are complete
+    // ---- side stream 2: dM_e, dM_x, db_M once dP_l is ready; with Gram_l done, layer l is complete
     rec(x->ev_dp[l], st);
-    wait(side, x->ev_dp[l]);
+    wait(side2, x->ev_dp[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
-      launch_reduce_dMe(side, x->caps, pagg, x->grad(lname(l, "M_e")));
+      launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
       if (cls && l > 0)
-        launch_mn_dMx(side, x->caps, blob, dP, dPlo, Xl, x->f(p.X_lo[l - 1]), F, x->f(p.ones), part_dMx,
+        launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xl, x->f(p.X_lo[l - 1]), F, x->f(p.ones), part_dMx,
                       x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
-        launch_tc_dMx(side, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+        launch_tc_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+      else if (l == 0 && dmx_small_ok(x->caps, F))
+        launch_dMx_small(side2, x->caps, blob, dP, Xl /* null: node features from the batch */, F, part_dMx,
+                         x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else
-        launch_dMx(side, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+        launch_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
     });
     g_low_prio = false;
-    if (overlap_allreduce) enqueue_bucket(x, side, c.layers - l);  // conv l gradients complete
-    rec(x->ev_side[l], side);
+    if (overlap_allreduce) {  // conv l gradients complete
+      wait(side2, x->ev_gram[l]);
+      enqueue_bucket(x, side2, c.layers - l);
+    }
+    rec(x->ev_side[l], side2);
     // ---- main: dX into dZ[l-1]
     if (l > 0) {
       float *dZn = x->f(p.dZ[l - 1]), *dZnl = cls ? x->f(p.dZ_lo[l - 1]) : nullptr;
@@ -436,7 +443,8 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       });
     }
   }
-  wait(st, x->ev_side[0]);  // join: every gradient is complete on the main stream
+  wait(st, x->ev_gram[0]);  // join: every gradient is complete on the main stream
+  wait(st, x->ev_side[0]);
 }
 
 // gradient buckets in backward order: head first, then conv L-1 ... conv 0 (each a
@@ -545,6 +553,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   if ((e = cudaStreamCreateWithPriority(&x->side_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
     return bail(e, "cudaStreamCreate");
+  if ((e = cudaStreamCreateWithPriority(&x->side2_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
+    return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
   for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep})
@@ -616,6 +626,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
   if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
   if (x->side_stream) cudaStreamDestroy(x->side_stream);
+  if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
     for (auto ev : *v) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep})

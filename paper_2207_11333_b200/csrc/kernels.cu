@@ -247,6 +247,7 @@ __global__ void k_reduce_split(const float *__restrict__ part, int splits, int M
 
 constexpr int kDUSplits = 8;
 constexpr int kDMxSplits = 16;
+constexpr int kSmallSplits = 64;
 
 // dU[h, s*4H+k] = sum_i s_i dZ[i,h] A[i,k]; column 12H = ones -> db_U
 struct OpDU {
@@ -290,7 +291,60 @@ struct OpDMx {
     part[(size_t)sp * H * (F + 1) + (size_t)m * (F + 1) + n] = v;
   }
 };
-size_t dMx_partial_floats(const Caps &c, int F) { return (size_t)kDMxSplits * c.H * (F + 1); }
+size_t dMx_partial_floats(const Caps &c, int F) {
+  return (size_t)std::max(kDMxSplits, kSmallSplits) * c.H * (F + 1);
+}
+
+// dM_x / db_M partials for a narrow layer input (F <= 16, i.e. the node features of
+// layer 0): block b sums its contiguous node range; 256/H row groups per block,
+// combined in fixed order. part[b][h][f] (f = F: column sum of dP -> db_M).
+template <int FMAX>
+__global__ void __launch_bounds__(256) k_dmx_small(const uint8_t *__restrict__ blob, const float *__restrict__ dP,
+                                                   const float *__restrict__ X, int H, int F,
+                                                   float *__restrict__ part) {
+  pdl_enter();
+  __shared__ float red[256 * (FMAX + 1)];
+  const int N = batch_N(blob);
+  if (!X) X = load_batch(blob).x;
+  const int G = blockDim.x / H, g = threadIdx.x / H, h = threadIdx.x - g * H;
+  const int chunk = (N + gridDim.x - 1) / gridDim.x;
+  const int i0 = blockIdx.x * chunk, i1 = min(N, i0 + chunk);
+  float acc[FMAX + 1];
+#pragma unroll
+  for (int f = 0; f <= FMAX; ++f) acc[f] = 0.f;
+  for (int i = i0 + g; i < i1; i += G) {
+    const float d = dP[(size_t)i * H + h];
+    const float *xi = X + (size_t)i * F;
+#pragma unroll
+    for (int f = 0; f < FMAX; ++f)
+      if (f < F) acc[f] = fmaf(d, xi[f], acc[f]);
+    acc[FMAX] += d;
+  }
+#pragma unroll
+  for (int f = 0; f <= FMAX; ++f) red[(size_t)f * blockDim.x + threadIdx.x] = acc[f];
+  __syncthreads();
+  float *out = part + (size_t)blockIdx.x * H * (F + 1);
+  for (int e = threadIdx.x; e < H * (F + 1); e += blockDim.x) {
+    const int hh = e / (F + 1), f = e - hh * (F + 1), fs = f == F ? FMAX : f;
+    float s = 0.f;
+    for (int q = 0; q < G; ++q) s += red[(size_t)fs * blockDim.x + q * H + hh];
+    out[e] = s;
+  }
+}
+
+bool dmx_small_ok(const Caps &c, int F) { return F <= 16 && c.H <= 256 && 256 % c.H == 0; }
+
+void launch_dMx_small(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
+                      float *partial, float *dMx, float *dbM) {
+  if (F <= 8)
+    launch_ex(k_dmx_small<8>, kSmallSplits, 256, 0, st, blob, dP, X, c.H, F, partial);
+  else
+    launch_ex(k_dmx_small<16>, kSmallSplits, 256, 0, st, blob, dP, X, c.H, F, partial);
+  const int total = c.H * (F + 1);
+  launch_ex(k_reduce_split, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, kSmallSplits, c.H, F + 1, dMx,
+            dbM);
+  counted(2);
+}
 void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
                 float *partial, float *dMx, float *dbM) {
   OpDMx op{blob, dP, X, partial, c.H, F};
