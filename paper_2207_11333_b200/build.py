@@ -85,7 +85,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         f.write("\n".join(logs))
     tmp = LIB + f".tmp{os.getpid()}"
     link = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", tmp] + [o for _, o in jobs] + \
-        [f"-L{nccl_lib}", "-lnccl", "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
+        [f"-L{nccl_lib}", "-lnccl", "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-Xlinker", "--no-undefined",
          "-lpthread"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:

@@ -148,7 +148,7 @@ struct hg_ctx {
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side;  // per layer fork / join points
-  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr;
+  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr;
   int64_t launches = 0;
   bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
   hg_status sticky = HG_OK;
@@ -247,22 +247,24 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
   float *amp = x->f(p.amp), *att = x->f(p.att);
-  phase(pr, HG_PHASE_SCALERS, [&] {
-    launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
-                   reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
-                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)));
-  });
   const bool cls = x->use_tc && p.cmax > 0;
   const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
   const size_t HH = (size_t)c.hidden * c.hidden;
-  // class weights (needs the degree classes) and M_x splits: on the side stream,
-  // concurrent with layer 0's projection and aggregation; joined before layer 0's update
+  // Degree sort and the class / M_x weight preparation run on the side stream,
+  // concurrent with layer 0's projection; joined before layer 0's aggregation
+  // (needs pos) and update (needs the class weights).
   const bool fork = cls && !pr && x->side_stream != nullptr;
   cudaStream_t pst = fork ? x->side_stream : st;
   if (fork) {
-    cudaEventRecord(x->ev_deg, st);
-    cudaStreamWaitEvent(pst, x->ev_deg, 0);
+    cudaEventRecord(x->ev_start, st);
+    cudaStreamWaitEvent(pst, x->ev_start, 0);
   }
+  phase(pr, HG_PHASE_SCALERS, [&] {
+    launch_degsort(pst, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
+                   reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
+                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)));
+  });
+  if (fork) cudaEventRecord(x->ev_deg, pst);
   if (cls)
     phase(pr, HG_PHASE_UPDATE, [&] {
       launch_prep_W2(pst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
@@ -284,6 +286,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
       else
         launch_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
     });
+    if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_deg, 0);
     phase(pr, HG_PHASE_AGG_FWD, [&] {
       launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
                      c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), cls ? x->f(p.A_lo[l]) : nullptr, pos);
@@ -417,9 +420,6 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
                       x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
         launch_tc_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
-      else if (l == 0 && dmx_small_ok(x->caps, F))
-        launch_dMx_small(side2, x->caps, blob, dP, Xl /* null: node features from the batch */, F, part_dMx,
-                         x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else
         launch_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
     });
@@ -557,7 +557,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
-  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep})
+  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
     for (int l = 0; l < c->layers; ++l) {
@@ -629,7 +629,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
     for (auto ev : *v) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep})
+  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start})
     if (ev) cudaEventDestroy(ev);
   if (x->comm) ncclCommDestroy(x->comm);
   for (auto ev : x->bucket_ready) cudaEventDestroy(ev);

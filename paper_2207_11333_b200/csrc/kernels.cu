@@ -246,8 +246,7 @@ __global__ void k_reduce_split(const float *__restrict__ part, int splits, int M
 }
 
 constexpr int kDUSplits = 8;
-constexpr int kDMxSplits = 16;
-constexpr int kSmallSplits = 64;
+constexpr int kDMxSplits = 64;
 
 // dU[h, s*4H+k] = sum_i s_i dZ[i,h] A[i,k]; column 12H = ones -> db_U
 struct OpDU {
@@ -291,60 +290,8 @@ struct OpDMx {
     part[(size_t)sp * H * (F + 1) + (size_t)m * (F + 1) + n] = v;
   }
 };
-size_t dMx_partial_floats(const Caps &c, int F) {
-  return (size_t)std::max(kDMxSplits, kSmallSplits) * c.H * (F + 1);
-}
+size_t dMx_partial_floats(const Caps &c, int F) { return (size_t)kDMxSplits * c.H * (F + 1); }
 
-// dM_x / db_M partials for a narrow layer input (F <= 16, i.e. the node features of
-// layer 0): block b sums its contiguous node range; 256/H row groups per block,
-// combined in fixed order. part[b][h][f] (f = F: column sum of dP -> db_M).
-template <int FMAX>
-__global__ void __launch_bounds__(256) k_dmx_small(const uint8_t *__restrict__ blob, const float *__restrict__ dP,
-                                                   const float *__restrict__ X, int H, int F,
-                                                   float *__restrict__ part) {
-  pdl_enter();
-  __shared__ float red[256 * (FMAX + 1)];
-  const int N = batch_N(blob);
-  if (!X) X = load_batch(blob).x;
-  const int G = blockDim.x / H, g = threadIdx.x / H, h = threadIdx.x - g * H;
-  const int chunk = (N + gridDim.x - 1) / gridDim.x;
-  const int i0 = blockIdx.x * chunk, i1 = min(N, i0 + chunk);
-  float acc[FMAX + 1];
-#pragma unroll
-  for (int f = 0; f <= FMAX; ++f) acc[f] = 0.f;
-  for (int i = i0 + g; i < i1; i += G) {
-    const float d = dP[(size_t)i * H + h];
-    const float *xi = X + (size_t)i * F;
-#pragma unroll
-    for (int f = 0; f < FMAX; ++f)
-      if (f < F) acc[f] = fmaf(d, xi[f], acc[f]);
-    acc[FMAX] += d;
-  }
-#pragma unroll
-  for (int f = 0; f <= FMAX; ++f) red[(size_t)f * blockDim.x + threadIdx.x] = acc[f];
-  __syncthreads();
-  float *out = part + (size_t)blockIdx.x * H * (F + 1);
-  for (int e = threadIdx.x; e < H * (F + 1); e += blockDim.x) {
-    const int hh = e / (F + 1), f = e - hh * (F + 1), fs = f == F ? FMAX : f;
-    float s = 0.f;
-    for (int q = 0; q < G; ++q) s += red[(size_t)fs * blockDim.x + q * H + hh];
-    out[e] = s;
-  }
-}
-
-bool dmx_small_ok(const Caps &c, int F) { return F <= 16 && c.H <= 256 && 256 % c.H == 0; }
-
-void launch_dMx_small(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
-                      float *partial, float *dMx, float *dbM) {
-  if (F <= 8)
-    launch_ex(k_dmx_small<8>, kSmallSplits, 256, 0, st, blob, dP, X, c.H, F, partial);
-  else
-    launch_ex(k_dmx_small<16>, kSmallSplits, 256, 0, st, blob, dP, X, c.H, F, partial);
-  const int total = c.H * (F + 1);
-  launch_ex(k_reduce_split, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, kSmallSplits, c.H, F + 1, dMx,
-            dbM);
-  counted(2);
-}
 void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
                 float *partial, float *dMx, float *dbM) {
   OpDMx op{blob, dP, X, partial, c.H, F};
@@ -830,6 +777,191 @@ __global__ void __launch_bounds__(256) k_head(const uint8_t *__restrict__ blob, 
   }
 }
 
+// Latency-optimised head for H = 128*CH, Hf = 8*RW (one block of 8 warps per
+// graph): every global operand of the graph (its X_L rows, the W1 rows a warp
+// owns, b1, W2, b2, y) is requested up front, so the whole head costs about one
+// memory round trip plus shared-memory reductions. Warp w owns node rows
+// n0+w, n0+w+8, ... (kept in registers for the ReLU mask of the backward) and W1
+// rows w, w+8, ... (reused by the backward). Reductions are fixed-order
+// (per-warp in row order, then warps 0..7; xor-shuffle trees), so deterministic.
+template <bool FWD, bool BWD, int CH, int RW>
+__global__ void __launch_bounds__(256) k_head_fast(const uint8_t *__restrict__ blob, const float *__restrict__ XL,
+                                                   const float *__restrict__ W1, const float *__restrict__ b1,
+                                                   const float *__restrict__ W2, const float *__restrict__ b2,
+                                                   float *__restrict__ G, float *__restrict__ hpre,
+                                                   float *__restrict__ yhat, float *__restrict__ sqerr,
+                                                   float *__restrict__ dy, float *__restrict__ dhid,
+                                                   float *__restrict__ dZL, float *__restrict__ dZL_lo,
+                                                   const int *__restrict__ pos) {
+  constexpr int H = 128 * CH, Hf = 8 * RW, RMAX = 8;
+  __shared__ float4 red[8][H / 4];
+  __shared__ float Gs[H], hs[Hf], dh[Hf];
+  __shared__ float s_yh;
+  pdl_enter();
+  const BatchView b = load_batch(blob);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // this warp's W1 rows (lane owns channels [4*(lane + 32*q), +4) for q < CH)
+  float4 w1r[RW][CH];
+#pragma unroll
+  for (int k = 0; k < RW; ++k)
+#pragma unroll
+    for (int q = 0; q < CH; ++q) w1r[k][q] = ldg4(W1 + (size_t)(warp + 8 * k) * H + 4 * (lane + 32 * q));
+  for (int g = blockIdx.x; g < b.B; g += gridDim.x) {
+    const int n0 = b.gp[g], n1 = b.gp[g + 1], n = n1 - n0;
+    const float ng = (float)n;
+    const bool regs = n <= 8 * RMAX;
+    float4 xr[RMAX][CH];
+    if (regs) {
+#pragma unroll
+      for (int j = 0; j < RMAX; ++j) {
+        const int i = n0 + warp + 8 * j;
+#pragma unroll
+        for (int q = 0; q < CH; ++q)
+          xr[j][q] = i < n1 ? ldg4(XL + (size_t)i * H + 4 * (lane + 32 * q)) : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    float yh;
+    if (FWD) {
+      // ---- mean pool
+      float4 ps[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) ps[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (regs) {
+#pragma unroll
+        for (int j = 0; j < RMAX; ++j)
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            ps[q].x += xr[j][q].x; ps[q].y += xr[j][q].y; ps[q].z += xr[j][q].z; ps[q].w += xr[j][q].w;
+          }
+      } else {
+        for (int i = n0 + warp; i < n1; i += 8)
+#pragma unroll
+          for (int q = 0; q < CH; ++q) {
+            const float4 v = ldg4(XL + (size_t)i * H + 4 * (lane + 32 * q));
+            ps[q].x += v.x; ps[q].y += v.y; ps[q].z += v.z; ps[q].w += v.w;
+          }
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) red[warp][lane + 32 * q] = ps[q];
+      __syncthreads();
+      if (threadIdx.x < H) {
+        const float *rf = reinterpret_cast<const float *>(red);
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += rf[w * H + threadIdx.x];
+        const float v = s / ng;
+        Gs[threadIdx.x] = v;
+        G[(size_t)g * H + threadIdx.x] = v;
+      }
+      __syncthreads();
+      // ---- hidden pre-activations: warp-owned W1 rows . G
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        float acc = 0.f;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const float4 gv = reinterpret_cast<const float4 *>(Gs)[lane + 32 * q];
+          acc = fmaf(w1r[k][q].x, gv.x, acc);
+          acc = fmaf(w1r[k][q].y, gv.y, acc);
+          acc = fmaf(w1r[k][q].z, gv.z, acc);
+          acc = fmaf(w1r[k][q].w, gv.w, acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+          const int r = warp + 8 * k;
+          acc += b1[r];
+          hs[r] = acc;
+          hpre[(size_t)g * Hf + r] = acc;
+        }
+      }
+      __syncthreads();
+      // ---- output + squared error (warp 0)
+      if (warp == 0) {
+        float part = 0.f;
+        for (int r = lane; r < Hf; r += 32) part = fmaf(W2[r], fmaxf(hs[r], 0.f), part);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (lane == 0) {
+          const float y = part + b2[0];
+          s_yh = y;
+          yhat[g] = y;
+          const float e = y - b.y[g];
+          sqerr[g] = e * e;
+        }
+      }
+      __syncthreads();
+      yh = s_yh;
+    } else {
+      for (int r = threadIdx.x; r < Hf; r += blockDim.x) hs[r] = hpre[(size_t)g * Hf + r];
+      yh = yhat[g];
+      __syncthreads();
+    }
+    if (BWD) {
+      const float d = 2.0f * (yh - b.y[g]) / (float)b.B;
+      if (threadIdx.x == 0) dy[g] = d;
+      for (int r = threadIdx.x; r < Hf; r += blockDim.x) {
+        const float v = hs[r] > 0.f ? d * W2[r] : 0.f;
+        dh[r] = v;
+        dhid[(size_t)g * Hf + r] = v;
+      }
+      __syncthreads();
+      // ---- dG = W1^T dh / n: warp partials over its rows, then warps 0..7
+      float4 acc[CH];
+#pragma unroll
+      for (int q = 0; q < CH; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int k = 0; k < RW; ++k) {
+        const float dv = dh[warp + 8 * k];
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          acc[q].x = fmaf(w1r[k][q].x, dv, acc[q].x);
+          acc[q].y = fmaf(w1r[k][q].y, dv, acc[q].y);
+          acc[q].z = fmaf(w1r[k][q].z, dv, acc[q].z);
+          acc[q].w = fmaf(w1r[k][q].w, dv, acc[q].w);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < CH; ++q) red[warp][lane + 32 * q] = acc[q];
+      __syncthreads();
+      if (threadIdx.x < H) {
+        const float *rf = reinterpret_cast<const float *>(red);
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) s += rf[w * H + threadIdx.x];
+        Gs[threadIdx.x] = s / ng;
+      }
+      __syncthreads();
+      // ---- dZ_L rows = [X_L > 0] * dG (degree-sorted rows when pos is given)
+      for (int j = 0; j < (n + 7) / 8; ++j) {
+        const int i = n0 + warp + 8 * j;
+        if (i >= n1) break;
+        const size_t od = (size_t)(pos ? pos[i] : i) * H;
+#pragma unroll
+        for (int q = 0; q < CH; ++q) {
+          const int cc = 4 * (lane + 32 * q);
+          float4 x;
+          if (regs) {
+#pragma unroll
+            for (int jj = 0; jj < RMAX; ++jj)
+              if (jj == j) x = xr[jj][q];
+          } else {
+            x = ldg4(XL + (size_t)i * H + cc);
+          }
+          const float4 gv = reinterpret_cast<const float4 *>(Gs)[cc / 4];
+          const float4 v = make_float4(x.x > 0.f ? gv.x : 0.f, x.y > 0.f ? gv.y : 0.f, x.z > 0.f ? gv.z : 0.f,
+                                       x.w > 0.f ? gv.w : 0.f);
+          *reinterpret_cast<float4 *>(dZL + od + cc) = v;
+          if (dZL_lo)
+            *reinterpret_cast<float4 *>(dZL_lo + od + cc) =
+                make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void __launch_bounds__(256) k_loss(const uint8_t *__restrict__ blob, const float *__restrict__ sqerr,
                                               float *__restrict__ loss) {
   pdl_enter();
@@ -850,6 +982,15 @@ static void head_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, con
   const size_t w1 = sizeof(float) * (size_t)c.Hf * c.H;
   const int in_smem = base + w1 <= 200 * 1024 ? 1 : 0;  // attribute set once by head_configure
   const size_t smem = base + (in_smem ? w1 : 0);
+  if (c.H == 128 && (c.Hf == 128 || c.Hf == 64)) {  // latency-optimised kernel
+    if (c.Hf == 128)
+      launch_ex(k_head_fast<FWD, BWD, 1, 16>, std::min(c.maxB, kSMs), 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre,
+                yhat, sqerr, dy, dhid, dZL, dZL_lo, pos);
+    else
+      launch_ex(k_head_fast<FWD, BWD, 1, 8>, std::min(c.maxB, kSMs), 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre,
+                yhat, sqerr, dy, dhid, dZL, dZL_lo, pos);
+    return;
+  }
   launch_ex(k_head<FWD, BWD>, std::min(c.maxB, kSMs), 256, smem, st, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
             dhid, dZL, c.H, c.Hf, in_smem, dZL_lo, pos);
 }

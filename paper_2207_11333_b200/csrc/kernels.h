@@ -34,10 +34,6 @@ void launch_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float 
 // dM_x[H,F] = dP^T X ; db_M = sum_i dP_i
 void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
                 float *partial, float *dMx, float *dbM);
-// narrow-input variant (F <= 16, 256 % H == 0): node-split SIMT partials, fixed-order reduce
-bool dmx_small_ok(const Caps &c, int F);
-void launch_dMx_small(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
-                      float *partial, float *dMx, float *dbM);
 // dZprev[N,F] = (dP Mx) * [Xl > 0]
 void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
                const float *Xl, float *dZprev);

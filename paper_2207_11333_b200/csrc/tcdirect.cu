@@ -36,7 +36,8 @@
 namespace hg {
 
 extern std::atomic<int64_t> g_launches;
-int g_tma_bn = 64;  // output-tile width of the TMA GEMMs (HG_TMA_BN=128 for A/B runs)
+// output-tile width per TMA GEMM (update, dA, proj, dX); HG_BN_<OP>=64|128 for A/B runs
+int g_bn_upd = 64, g_bn_da = 128, g_bn_proj = 64, g_bn_dx = 64;
 
 
 // experiments only: per-CTA %globaltimer trace of one Op type (hg_debug_set_trace)
@@ -542,7 +543,13 @@ cudaError_t tcd_configure() {
     if (q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  if (const char *v = getenv("HG_TMA_BN")) g_tma_bn = atoi(v) == 128 ? 128 : 64;
+  auto env_bn = [](const char *n, int &v) {
+    if (const char *s = getenv(n)) v = atoi(s) == 128 ? 128 : 64;
+  };
+  env_bn("HG_BN_UPD", g_bn_upd);
+  env_bn("HG_BN_DA", g_bn_da);
+  env_bn("HG_BN_PROJ", g_bn_proj);
+  env_bn("HG_BN_DX", g_bn_dx);
   if ((e = tconfigure_bn<64>()) != cudaSuccess) return e;
   if ((e = tconfigure_bn<128>()) != cudaSuccess) return e;
   return tmn_configure();
@@ -551,26 +558,26 @@ cudaError_t tcd_configure() {
 void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
                          float *X1, float *X1_lo) {
-  if (g_tma_bn == 128) update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
+  if (g_bn_upd == 128) update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
   else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
 }
 
 void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
                      const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
-  if (g_tma_bn == 128) dA_bn<128>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
+  if (g_bn_da == 128) dA_bn<128>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
   else dA_bn<64>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
 }
 
 void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
                    const float *Mx, const float *Mx_lo, float *P) {
-  if (g_tma_bn == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+  if (g_bn_proj == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
   else proj_bn<64>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
 }
 
 void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
                  const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
                  const int *pos) {
-  if (g_tma_bn == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+  if (g_bn_dx == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
   else dX_bn<64>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
 }
 
