@@ -38,6 +38,7 @@ namespace hg {
 extern std::atomic<int64_t> g_launches;
 // output-tile width per TMA GEMM (update, dA, proj, dX); HG_BN_<OP>=64|128 for A/B runs
 int g_bn_upd = 64, g_bn_da = 128, g_bn_proj = 64, g_bn_dx = 64;
+bool g_update_sk = false;  // split-K cluster update (HG_UPDATE_SK=1): measured slower, see DESIGN.md
 
 
 // experiments only: per-CTA %globaltimer trace of one Op type (hg_debug_set_trace)
@@ -366,6 +367,207 @@ struct TDX {
   }
 };
 
+// ---------------------------------------------------------------- split-K update
+// G1 with K = 4H split over a cluster of KS = 4 CTAs (one aggregator block of
+// the class weights each), so a 128-row tile is served by 4 SMs instead of 1:
+// CTA r of the cluster accumulates A[:, rH:(r+1)H] W_c[:, rH:(r+1)H]^T (H x H,
+// 3xTF32) in TMEM; after a cluster barrier every CTA writes the column quarters
+// it does not own into the owner's shared memory (distributed shared memory,
+// st.shared::cluster), and after a second barrier CTA r sums the four partials
+// of its quarter in fixed rank order (deterministic) and applies the epilogue
+// (b_U, ReLU, X1 and its lo term, scattered to node order through perm).
+constexpr int SK_KS = 4;
+constexpr int SK_H = 128;  // H handled by this kernel (output tile = all H columns)
+constexpr int SK_ST = 3;
+constexpr int SK_STAGE = 4 * SK_H * 128;  // A hi/lo (128 rows) + B hi/lo (128 rows), one 32-wide K chunk
+constexpr int SK_SMEM = SK_ST * SK_STAGE + 1024 + 8 * (2 * SK_ST + 1) + 16;
+static_assert(SK_KS * SK_H * (SK_H / SK_KS) * 4 <= SK_ST * SK_STAGE, "receive buffer fits the stage ring");
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float4 v) {
+  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
+               "f"(v.w)
+               : "memory");
+}
+
+struct SkTraceOp {
+  static constexpr int ID = 4;
+};
+__global__ void __launch_bounds__(T_THREADS, 1) k_update_sk(const __grid_constant__ TmaMaps mp, const int *perm,
+                                                            const DegInfo *info, const int4 *tiles, const float *bU,
+                                                            float *X1, float *X1_lo) {
+  constexpr int H = SK_H, Q = H / SK_KS;  // Q: columns owned per CTA
+  constexpr int A_BYTES = T_BM * 128, B_BYTES = H * 128;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + SK_ST * SK_STAGE);
+  uint64_t *empty = full + SK_ST;
+  uint64_t *accf = empty + SK_ST;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(accf + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  using Op = SkTraceOp;
+  if (threadIdx.x == 0) TTRACE(0);
+  if (warp == T_MMA_WARP) tc::tmem_alloc<H>(tmem_holder);
+  if (threadIdx.x == T_TMA_WARP * 32) {
+    tc::tma_prefetch_desc(&mp.ah);
+    tc::tma_prefetch_desc(&mp.al);
+    tc::tma_prefetch_desc(&mp.bh);
+    tc::tma_prefetch_desc(&mp.bl);
+    for (int s = 0; s < SK_ST; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    tc::mbar_init(accf, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_holder;
+  pdl_enter();
+  if (threadIdx.x == 0) TTRACE(1);
+  const int ti = blockIdx.x / SK_KS;
+  const bool valid = ti < info->T;  // uniform over the cluster
+  int4 tl = make_int4(0, 0, 0, 0);
+  if (valid) tl = tiles[ti];
+  const int kbase = (int)rank * H;  // this CTA's K range [kbase, kbase + H)
+  constexpr int NCH = H / T_BK;
+  if (valid) {
+    if (warp == T_TMA_WARP) {
+      if (lane == 0) {
+        for (int c = 0; c < NCH; ++c) {
+          const int s = c % SK_ST;
+          if (c >= SK_ST) tc::mbar_wait(&empty[s], ((c / SK_ST) - 1) & 1);
+          uint8_t *sa = smem + s * SK_STAGE;
+          tc::mbar_expect_tx(&full[s], SK_STAGE);
+          const int k = kbase + c * T_BK;
+          tc::tma_load_2d(sa, &mp.ah, k, tl.y, &full[s]);
+          tc::tma_load_2d(sa + A_BYTES, &mp.al, k, tl.y, &full[s]);
+          tc::tma_load_2d(sa + 2 * A_BYTES, &mp.bh, k, tl.x * H, &full[s]);
+          tc::tma_load_2d(sa + 2 * A_BYTES + B_BYTES, &mp.bl, k, tl.x * H, &full[s]);
+        }
+      }
+      __syncwarp();
+    } else if (warp == T_MMA_WARP) {
+      if (lane == 0) {
+        constexpr uint32_t idesc = tc::idesc_tf32(T_BM, H);
+        for (int c = 0; c < NCH; ++c) {
+          const int s = c % SK_ST;
+          tc::mbar_wait(&full[s], (c / SK_ST) & 1);
+          tc::fence_after_sync();
+          const uint32_t aH = tc::smem_u32(smem + s * SK_STAGE);
+          const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < T_BK / 8; ++ks) {
+            const uint32_t off = ks * 32;
+            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
+            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+            tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
+            tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
+            tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+          }
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(accf);
+      }
+      __syncwarp();
+    }
+  }
+  // epilogue warps hold the full partial in registers across the exchange
+  float own[Q];
+  const int row = warp * 32 + lane;  // accumulator lane (epilogue warps)
+  if (valid && warp < 4) {
+    tc::mbar_wait(accf, 0);
+    tc::fence_after_sync();
+  }
+  if (threadIdx.x == 0) TTRACE(2);
+  // barrier 1: every CTA's MMAs are complete, so all stage rings are free to receive
+  tc::fence_before_sync();
+  cluster_sync_all();
+  if (valid && warp < 4) {
+    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+    // receive layout in each owner: slot[src][row][Q] fp32 at the start of the ring
+    const uint32_t slot0 = tc::smem_u32(smem);
+#pragma unroll 1
+    for (int q = 0; q < SK_KS; ++q) {
+      float acc[32];
+      tc::tmem_ld32(trow + (uint32_t)(q * Q), acc);
+      if (q == (int)rank) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) own[i] = acc[i];
+      } else {
+        const uint32_t dst = map_peer(slot0 + (uint32_t)(((rank * T_BM) + row) * Q * 4), (uint32_t)q);
+#pragma unroll
+        for (int i = 0; i < Q; i += 4) st_cluster_v4(dst + i * 4, make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
+      }
+    }
+  }
+  if (threadIdx.x == 0) TTRACE(3);
+  // barrier 2: all partial quarters have landed in their owners
+  cluster_sync_all();
+  if (threadIdx.x == 0) TTRACE(4);
+  if (valid && warp < 4) {
+    const float *slot = reinterpret_cast<const float *>(smem);
+    float sum[Q];
+#pragma unroll
+    for (int i = 0; i < Q; ++i) sum[i] = 0.f;
+    for (int src = 0; src < SK_KS; ++src) {  // fixed rank order
+      if (src == (int)rank) {
+#pragma unroll
+        for (int i = 0; i < Q; ++i) sum[i] += own[i];
+      } else {
+        const float *p = slot + ((size_t)src * T_BM + row) * Q;
+#pragma unroll
+        for (int i = 0; i < Q; i += 4) {
+          const float4 v = *reinterpret_cast<const float4 *>(p + i);
+          sum[i] += v.x; sum[i + 1] += v.y; sum[i + 2] += v.z; sum[i + 3] += v.w;
+        }
+      }
+    }
+    const int m = tl.y + row;
+    if (m < tl.y + tl.z) {
+      const int n0 = (int)rank * Q;
+      const size_t o = (size_t)perm[m] * H + n0;
+#pragma unroll
+      for (int i = 0; i < Q; i += 4) {
+        const float4 b = ldg4(bU + n0 + i);
+        const float4 z = make_float4(fmaxf(sum[i] + b.x, 0.f), fmaxf(sum[i + 1] + b.y, 0.f),
+                                     fmaxf(sum[i + 2] + b.z, 0.f), fmaxf(sum[i + 3] + b.w, 0.f));
+        *reinterpret_cast<float4 *>(X1 + o + i) = z;
+        *reinterpret_cast<float4 *>(X1_lo + o + i) = lo4(z);
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    TTRACE(5);
+    if (g_trace && g_trace_id == 4) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+      g_trace[blockIdx.x * 8 + 7] = smid;
+      g_trace[blockIdx.x * 8 + 6] = valid;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == T_MMA_WARP) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<H>(tmem);
+  }
+}
+
 // ---------------------------------------------------------------- weight preparation
 // per layer l >= 1: Mx_lo = lo(M_x) [H][F]; MxT = M_x^T [F][H] and its lo
 __global__ void k_prep_Mx(const float *__restrict__ params, const int64_t *__restrict__ mx_off, int L, int H, int F,
@@ -550,6 +752,9 @@ cudaError_t tcd_configure() {
   env_bn("HG_BN_DA", g_bn_da);
   env_bn("HG_BN_PROJ", g_bn_proj);
   env_bn("HG_BN_DX", g_bn_dx);
+  if (const char *v = getenv("HG_UPDATE_SK")) g_update_sk = atoi(v) != 0;
+  if ((e = cudaFuncSetAttribute(k_update_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM)) != cudaSuccess)
+    return e;
   if ((e = tconfigure_bn<64>()) != cudaSuccess) return e;
   if ((e = tconfigure_bn<128>()) != cudaSuccess) return e;
   return tmn_configure();
@@ -558,6 +763,30 @@ cudaError_t tcd_configure() {
 void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
                          float *X1, float *X1_lo) {
+  if (g_update_sk && c.H == SK_H) {
+    const int K = 4 * c.H;
+    const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, SK_H),
+                     map2d(Wf_lo, (uint64_t)cmax * c.H, K, SK_H)};
+    cudaLaunchAttribute attr[3];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = SK_KS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[2].id = cudaLaunchAttributePriority;
+    attr[2].val.priority = g_low_prio ? g_prio_lo : g_prio_hi;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(tc_max_tiles(c, cmax) * SK_KS);
+    cfg.blockDim = dim3(T_THREADS);
+    cfg.dynamicSmemBytes = SK_SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 3;
+    cudaLaunchKernelEx(&cfg, k_update_sk, mp, perm, info, tiles, bU, X1, X1_lo);
+    g_launches += 1;
+    return;
+  }
   if (g_bn_upd == 128) update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
   else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
 }
