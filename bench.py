@@ -330,22 +330,26 @@ def main():
             a = phases.setdefault(k, [0.0, 0])
             a[0] += ms / reps
             a[1] = nl
-    # algorithmic work per phase
+    # algorithmic work per phase:
+    # bytes = compulsory fp32 traffic of the method per node-layer, flops = fp32 MACs x 2
     Ns, Es = [], []
     for r in range(reps):
         hdr = blobs[r % n_res][:64].view(np.int32)
         Ns.append(int(hdr[1]))
         Es.append(int(hdr[2]))
     Nn, Ee = float(np.mean(Ns)), float(np.mean(Es))
+    eb = Ee / Nn  # mean in-degree
     F0 = data["f_node"]
-    flops = {
-        "update": 24.0 * Nn * H * H * L, "dA": 24.0 * Nn * H * H * L, "dU": 24.0 * Nn * H * H * L,
-        "proj": 2.0 * Nn * H * (F0 + H * (L - 1)), "dMx": 2.0 * Nn * H * (F0 + H * (L - 1)) + 2.0 * Nn * H * L,
-        "dX": 2.0 * Nn * H * H * (L - 1),
-    }
-    hbm_bytes = {
-        "agg_fwd": L * (Nn * (22 * H + 4) + 20 * Ee),
-        "agg_bwd": L * (Nn * (34 * H + 4) + 20 * Ee),
+    NL, NL1 = Nn * L, Nn * (L - 1)  # node-layers, node-layers with F = H
+    work = {  # phase -> (algorithmic bytes, algorithmic flops)
+        "proj": (Nn * (4 * F0 + 4 * H) + NL1 * 8 * H, 2.0 * Nn * H * F0 + 2.0 * NL1 * H * H),
+        "agg_fwd": (NL * (22 * H + 4 + 20 * eb), 0.0),
+        "update": (NL * (20 * H + 8), 8.0 * NL * H * H),
+        "dA": (NL * 20 * H, 8.0 * NL * H * H),
+        "dU": (NL * 20 * H, 8.0 * NL * H * H + NL * H),
+        "agg_bwd": (NL * (34 * H + 4 + 20 * eb), 0.0),
+        "dMx": (Nn * (4 * H + 4 * F0) + NL1 * 8 * H, 2.0 * Nn * H * (F0 + 1) + 2.0 * NL1 * H * (H + 1)),
+        "dX": (NL1 * 12 * H, 2.0 * NL1 * H * H),
     }
     peaks = {}
     try:
@@ -354,29 +358,41 @@ def main():
     except OSError:
         pass
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
-    ffma_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # fp32 FFMA TFLOP/s
-    dom = max((k for k in phases if k != "allreduce"), key=lambda k: phases[k][0])
+    bf16_peak = float(peaks.get("bf16_tflops", 2250.0))
+    # 3xTF32: three tf32 MMAs per fp32 MAC; tf32 dense = bf16 dense x 0.5 (nominal ratio, B200_PROFILING.md)
+    tc_peak = bf16_peak * 0.5 / 3.0
+    ridge = tc_peak * 1e12 / (hbm_peak * 1e9)  # flop / byte
     step_ms_prof = sum(v[0] for v in phases.values())
-    if dom in flops:
-        ach = flops[dom] / (phases[dom][0] / 1e3) / 1e12
-        prof = {"bound": "alu", "kernel": dom, "achieved": ach, "peak": ffma_peak, "unit": "TFLOP/s",
-                "frac": ach / ffma_peak, "traffic": None,
-                "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x sm_max_mhz (SIMT fp32 FFMA path)",
-                "share_of_step": phases[dom][0] / step_ms_prof}
-    else:
-        ach = hbm_bytes[dom] / (phases[dom][0] / 1e3) / 1e9
-        prof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm_peak, "unit": "GB/s",
-                "frac": ach / hbm_peak, "traffic": None, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                "share_of_step": phases[dom][0] / step_ms_prof}
-    agg = {}
-    for k in ("agg_fwd", "agg_bwd"):
-        a = hbm_bytes[k] / (phases[k][0] / 1e3) / 1e9
-        agg[k] = {"achieved_gbs": a, "frac_of_measured_hbm": a / hbm_peak, "ms": phases[k][0]}
-    gemm = {}
-    for k in ("update", "dA", "dU"):
-        a = flops[k] / (phases[k][0] / 1e3) / 1e12
-        gemm[k] = {"achieved_tflops": a, "frac_of_ffma": a / ffma_peak, "ms": phases[k][0]}
+    traffic_db = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic_per_launch.json")) as f:
+            traffic_db = json.load(f)
+    except (OSError, ValueError):
+        pass
+
+    def roof(k):
+        byt, fl = work[k]
+        t = phases[k][0] / 1e3
+        launches_k = max(1, phases[k][1])
+        if fl > 0 and fl / byt >= ridge:
+            ach = fl / t / 1e12
+            r = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak,
+                 "peak_source": "MEASURED_PEAKS.json bf16_tflops x 0.5 (tf32) / 3 (3xTF32 passes)"}
+        else:
+            ach = byt / t / 1e9
+            r = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
+                 "peak_source": "MEASURED_PEAKS.json hbm_gbs"}
+        r.update({"kernel": k, "ms": phases[k][0], "launches": phases[k][1],
+                  "algorithmic_bytes_per_launch": byt / launches_k, "algorithmic_flops_per_launch": fl / launches_k,
+                  "intensity_flop_per_byte": fl / byt, "share_of_step": phases[k][0] / step_ms_prof,
+                  "traffic": traffic_db.get(k)})
+        return r
+
+    dom = max((k for k in phases if k in work), key=lambda k: phases[k][0])
+    prof = roof(dom)
+    phase_roof = {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in roof(k).items()
+                      if kk in ("bound", "achieved", "frac", "ms", "intensity_flop_per_byte")}
+                  for k in work if k in phases}
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
     cpu = None
@@ -398,8 +414,8 @@ def main():
                    "layers": L, "hidden": H, "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
                    "parallelism": f"dp{world}", "resident_batches": n_res,
                    "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
-                   "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs"},
-        "roofline": prof, "roofline_agg": agg, "gemm": gemm,
+                   "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs, TMA-fed"},
+        "roofline": prof, "phase_roofline": phase_roof,
         "phases_ms": {k: round(v[0], 4) for k, v in phases.items()},
         "phase_launches": {k: v[1] for k, v in phases.items()},
         "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,

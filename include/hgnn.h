@@ -226,10 +226,12 @@ hg_status hg_train_step(hg_ctx *x, int32_t slot, const hg_adamw *h, int32_t grap
 /* Capture (without running) the CUDA graph hg_train_step replays for `slot`. */
 hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h);
 
-/* Instrumented step (no graph): runs forward + backward + allreduce + AdamW
- * eagerly with CUDA events around every kernel class and returns, per phase,
- * the summed device milliseconds (ms[HG_PHASE_COUNT]) and kernel launches
- * (launches[HG_PHASE_COUNT], nullable). Synchronises. (SPEC.md:429-432 PhaseTimings) */
+/* Instrumented step: forward + backward + allreduce + AdamW captured on ONE
+ * stream (no side-stream overlap) with CUDA timing events around every kernel
+ * class, replayed once as a graph; returns, per phase, the summed device
+ * milliseconds (ms[HG_PHASE_COUNT]) and kernel launches (launches[HG_PHASE_COUNT],
+ * nullable). Advances the training state like hg_train_step. Synchronises.
+ * (SPEC.md:429-432 PhaseTimings) */
 enum {
   HG_PHASE_SCALERS = 0, HG_PHASE_PROJ = 1, HG_PHASE_AGG_FWD = 2, HG_PHASE_UPDATE = 3, HG_PHASE_HEAD_FWD = 4,
   HG_PHASE_HEAD_BWD = 5, HG_PHASE_DA = 6, HG_PHASE_DU = 7, HG_PHASE_AGG_BWD = 8, HG_PHASE_DMX = 9,

@@ -231,11 +231,12 @@ void phase(Prof *pr, int ph, F &&fn) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  cudaEventRecord(a, pr->st);
+  // external event nodes: the graph replay records them, so they can be timed
+  cudaEventRecordWithFlags(a, pr->st, cudaEventRecordExternal);
   const int64_t l0 = launches_so_far();
   fn();
   pr->launches[ph] += launches_so_far() - l0;
-  cudaEventRecord(b, pr->st);
+  cudaEventRecordWithFlags(b, pr->st, cudaEventRecordExternal);
   pr->marks.push_back({ph, {a, b}});
 }
 
@@ -414,11 +415,14 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     wait(side2, x->ev_dp[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
-      launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
-      if (cls && l > 0)
+      if (cls && l > 0) {  // the MN-major Gram also reduces dM_e
         launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xl, x->f(p.X_lo[l - 1]), F, x->f(p.ones), part_dMx,
-                      x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
-      else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
+                      x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")), pagg, agg_bwd_partials(x->caps),
+                      x->grad(lname(l, "M_e")));
+        return;
+      }
+      launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
+      if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
         launch_tc_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else
         launch_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
@@ -920,19 +924,36 @@ hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms,
   hg_status st = usable(x);
   if (st || (st = check_slot(x, slot))) return st;
   if (!h || !ms) return fail(HG_E_INVALID, "null argument");
-  CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
-  Prof pr(x->stream);
+  // The step is captured with timing events between phases (single stream, no
+  // side-stream overlap) and replayed as one graph, so each phase's time is its
+  // kernels' device time without host launch gaps.
+  Prof pr(x->cap_stream);
+  CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
-  enqueue_forward(x, x->stream, slot, &pr, true);
-  enqueue_backward(x, x->stream, slot, &pr, true);
+  enqueue_forward(x, x->cap_stream, slot, &pr, true);
+  enqueue_backward(x, x->cap_stream, slot, &pr, true);
   hg_status ar = HG_OK;
-  phase(&pr, HG_PHASE_ALLREDUCE, [&] { ar = enqueue_allreduce(x, x->stream); });
-  if (ar) return ar;
-  enqueue_step(x, x->stream, *h, &pr);
-  x->launches += launches_so_far() - l0;
-  if ((st = after_enqueue(x, "profile launch"))) return st;
-  CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
-  CK(x, cudaStreamSynchronize(x->stream));
+  phase(&pr, HG_PHASE_ALLREDUCE, [&] { ar = enqueue_allreduce(x, x->cap_stream); });
+  enqueue_step(x, x->cap_stream, *h, &pr);
+  const int64_t nk = launches_so_far() - l0;
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
+  if (ar) {
+    if (g) cudaGraphDestroy(g);
+    return ar;
+  }
+  if (e != cudaSuccess) return cuda_fail(x, e, "cudaStreamEndCapture");
+  cudaGraphExec_t ex = nullptr;
+  e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) return cuda_fail(x, e, "cudaGraphInstantiate");
+  x->launches += nk;
+  CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
+  e = cudaGraphLaunch(ex, x->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(x->compute_done[slot], x->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
+  cudaGraphExecDestroy(ex);
+  if (e != cudaSuccess) return cuda_fail(x, e, "profile graph");
   for (int i = 0; i < HG_PHASE_COUNT; ++i) ms[i] = 0.f;
   for (auto &m : pr.marks) {
     float t = 0.f;

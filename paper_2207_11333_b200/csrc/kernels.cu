@@ -627,6 +627,7 @@ __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int co
 
 static int agg_bwd_blocks(const Caps &c) { return std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 2)); }
 size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * c.Fe; }
+int agg_bwd_partials(const Caps &c) { return agg_bwd_blocks(c); }
 
 template <int CPL, int FE>
 static void agg_bwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,

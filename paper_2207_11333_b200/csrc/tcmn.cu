@@ -279,6 +279,98 @@ struct MnDMx {
   __device__ void emit_cs(const MnItem &w, int m, float v) const { cs[(size_t)w.sp * H + m] = v; }
 };
 
+// ---------------------------------------------------------------- reductions
+// Block = RW warps x 32 float4 outputs: lane l of warp w sums parts w, w+RW, ...
+// of output float4 (32*block + l) -- coalesced rows -- then warp 0 adds the RW
+// warp sums in order (deterministic for a given partial count).
+constexpr int RW = 32;
+struct RJob {
+  const float *part;  // [nparts][count]
+  int nparts, count;  // count % 4 == 0
+  float *out;
+};
+__device__ __forceinline__ void add4(float4 &s, float4 v) {
+  s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
+}
+// up to three independent sums in one launch (dM_x, db_M, dM_e of a layer)
+__global__ void __launch_bounds__(32 * RW) k_reduce_jobs(RJob j0, RJob j1, RJob j2) {
+  pdl_enter();
+  __shared__ float4 red[RW][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int b0 = (j0.count / 4 + 31) / 32, b1 = (j1.count / 4 + 31) / 32;
+  int blk = blockIdx.x;
+  const RJob &j = blk < b0 ? j0 : (blk < b0 + b1 ? j1 : j2);
+  blk = blk < b0 ? blk : (blk < b0 + b1 ? blk - b0 : blk - b0 - b1);
+  const int e = 4 * (blk * 32 + lane);
+  const bool ok = e < j.count;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ok) {
+#pragma unroll 4
+    for (int p = warp; p < j.nparts; p += RW) add4(s, ldg4(j.part + (size_t)p * j.count + e));
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int w = 1; w < RW; ++w) add4(t, red[w][lane]);
+    *reinterpret_cast<float4 *>(j.out + e) = t;
+  }
+}
+static int reduce_blocks(const RJob &j) { return (j.count / 4 + 31) / 32; }
+
+// dU[h][s*4H + n] = sum_sp s(class(sp)) part[sp][h][n] for the three scalers
+// (blocks over the H x 4H partial), db_U[h] = sum_sp cs[sp][h] (trailing blocks);
+// S = info->S splits (device-side)
+__global__ void __launch_bounds__(256) k_reduce_gram(const float *__restrict__ part, const float *__restrict__ cs,
+                                                     const DegInfo *__restrict__ info, const int4 *__restrict__ splits,
+                                                     int H, float *__restrict__ dU, float *__restrict__ dbU) {
+  pdl_enter();
+  __shared__ float4 red[3][8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int S = info->S, K = 4 * H, bU = H * K / 128;
+  const bool gram = (int)blockIdx.x < bU;
+  const int e = 4 * (((int)blockIdx.x - (gram ? 0 : bU)) * 32 + lane);
+  const bool ok = gram || e < H;
+  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
+  if (ok) {
+    for (int sp = warp; sp < S; sp += 8) {
+      if (gram) {
+        const int c = splits[sp].x;
+        const float a = info->amp[c], t = info->att[c];
+        const float4 v = ldg4(part + (size_t)sp * H * K + e);
+        add4(s0, v);
+        s1.x = fmaf(a, v.x, s1.x); s1.y = fmaf(a, v.y, s1.y); s1.z = fmaf(a, v.z, s1.z); s1.w = fmaf(a, v.w, s1.w);
+        s2.x = fmaf(t, v.x, s2.x); s2.y = fmaf(t, v.y, s2.y); s2.z = fmaf(t, v.z, s2.z); s2.w = fmaf(t, v.w, s2.w);
+      } else {
+        add4(s0, ldg4(cs + (size_t)sp * H + e));
+      }
+    }
+  }
+  red[0][warp][lane] = s0;
+  red[1][warp][lane] = s1;
+  red[2][warp][lane] = s2;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float4 t0 = red[0][0][lane], t1 = red[1][0][lane], t2 = red[2][0][lane];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      add4(t0, red[0][w][lane]);
+      add4(t1, red[1][w][lane]);
+      add4(t2, red[2][w][lane]);
+    }
+    if (gram) {
+      const int h = e / K, n = e - h * K;
+      float *row = dU + (size_t)h * 3 * K + n;
+      *reinterpret_cast<float4 *>(row) = t0;
+      *reinterpret_cast<float4 *>(row + K) = t1;
+      *reinterpret_cast<float4 *>(row + 2 * K) = t2;
+    } else {
+      *reinterpret_cast<float4 *>(dbU + e) = t0;
+    }
+  }
+}
+
 // reductions (tcgemm.cu / kernels.cu)
 __global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInfo *__restrict__ info,
                                     const int4 *__restrict__ splits, int H, float *__restrict__ dU);
@@ -320,14 +412,13 @@ void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ,
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
   MnGram op{info, splits, partial, cs, c.H, 0};
   nrun(st, mp, om, op, smax * (c.H / N_BM) * (4 * c.H / MnGram::BN + 1));
-  launch_ex(k_reduce_dU_classes, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, info, splits, c.H, dU);
-  launch_ex(k_reduce_splits_rows, cdiv(c.H, 8), 256, 0, st, cs, info, c.H, dbU);
-  g_launches += 2;
+  launch_ex(k_reduce_gram, total / 128 + cdiv(c.H, 128), 256, 0, st, partial, cs, info, splits, c.H, dU, dbU);
+  g_launches += 1;
 }
 
 void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
                    const float *X, const float *X_lo, int F, const float *ones, float *partial, float *dMx,
-                   float *dbM) {
+                   float *dbM, const float *pagg, int nagg, float *dMe) {
   const int count = c.H * F;
   float *cs = partial + (size_t)kMnDMxSplits * count;
   const TmaMaps mp{tma_map2d(dP, c.maxN, c.H, N_BK, true), tma_map2d(dP_lo, c.maxN, c.H, N_BK, true),
@@ -335,9 +426,11 @@ void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
   MnDMx op{blob, partial, cs, c.H, F, 0};
   nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * (F / MnDMx::BN + 1));
-  launch_ex(k_reduce_parts, std::min(cdiv(count / 4, 256), kSMs * 4), 256, 0, st, partial, kMnDMxSplits, count, dMx);
-  launch_ex(k_reduce_rows, cdiv(c.H, 8), 256, 0, st, cs, kMnDMxSplits, c.H, dbM);
-  g_launches += 2;
+  // dM_x, db_M and (when given) the dM_e block partials of the aggregation backward
+  const RJob j0{partial, kMnDMxSplits, count, dMx}, j1{cs, kMnDMxSplits, c.H, dbM};
+  const RJob j2{pagg, pagg ? nagg : 0, pagg ? c.H * c.Fe : 0, dMe};
+  launch_ex(k_reduce_jobs, reduce_blocks(j0) + reduce_blocks(j1) + reduce_blocks(j2), 32 * RW, 0, st, j0, j1, j2);
+  g_launches += 1;
 }
 
 }  // namespace hg
