@@ -231,6 +231,8 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h);
  * class, replayed once as a graph; returns, per phase, the summed device
  * milliseconds (ms[HG_PHASE_COUNT]) and kernel launches (launches[HG_PHASE_COUNT],
  * nullable). Advances the training state like hg_train_step. Synchronises.
+ * HG_PHASE_SCALERS covers the degree sort, scalers and the degree-class weight
+ * preparation; HG_PHASE_DMX also covers the dM_e reduction.
  * (SPEC.md:429-432 PhaseTimings) */
 enum {
   HG_PHASE_SCALERS = 0, HG_PHASE_PROJ = 1, HG_PHASE_AGG_FWD = 2, HG_PHASE_UPDATE = 3, HG_PHASE_HEAD_FWD = 4,

@@ -267,7 +267,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   });
   if (fork) cudaEventRecord(x->ev_deg, pst);
   if (cls)
-    phase(pr, HG_PHASE_UPDATE, [&] {
+    phase(pr, HG_PHASE_SCALERS, [&] {  // (degree-class weights belong with the scalers)
       launch_prep_W2(pst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
                      reinterpret_cast<const DegInfo *>(x->b(p.deginfo)), x->f(p.Wf), x->f(p.Wf_lo), x->f(p.WbT),
                      x->f(p.WbT_lo));
