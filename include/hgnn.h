@@ -243,6 +243,14 @@ hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms,
 
 /* Read the loss of the last forward (synchronises the compute stream). */
 hg_status hg_loss_get(hg_ctx *x, float *loss);
+/* Pipelined loss read-back: hg_loss_enqueue copies the loss of the last enqueued
+ * forward into entry `i` (0 <= i < HG_LOSS_RING) of a pinned host ring owned by
+ * the ctx, on the compute stream, without synchronising; hg_loss_fetch waits for
+ * that copy only and returns the value. Lets a training loop read step k's loss
+ * after step k+1 has been launched. HG_E_RANGE for a bad index. */
+#define HG_LOSS_RING 4
+hg_status hg_loss_enqueue(hg_ctx *x, int32_t i);
+hg_status hg_loss_fetch(hg_ctx *x, int32_t i, float *loss);
 /* Synchronise the ctx's streams; surfaces sticky CUDA/NCCL errors. */
 hg_status hg_sync(hg_ctx *x);
 /* Number of kernels this ctx has launched (graph replays count their kernel nodes). */

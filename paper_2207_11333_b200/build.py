@@ -66,7 +66,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         jobs.append((cmd, obj))
     for f in CPP_SOURCES:
         obj = os.path.join(OBJDIR, f + ".o")
-        cmd = ["g++", "-fPIC", "-Wall", "-pthread"] + common + ["-c", os.path.join(CSRC, f), "-o", obj]
+        cmd = ["g++", "-fPIC", "-Wall", "-pthread", "-fopenmp"] + common + ["-c", os.path.join(CSRC, f), "-o", obj]
         jobs.append((cmd, obj))
 
     def run(job):
@@ -86,7 +86,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB + f".tmp{os.getpid()}"
     link = [NVCC] + ARCH + ["-shared", "-cudart", "shared", "-o", tmp] + [o for _, o in jobs] + \
         [f"-L{nccl_lib}", "-lnccl", "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", "-rpath,/usr/local/cuda/lib64", "-Xlinker", "--no-undefined",
-         "-lpthread"]
+         "-lpthread", "-lgomp"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("link failed:\n" + " ".join(link) + "\n" + r.stdout + r.stderr)

@@ -149,6 +149,8 @@ struct hg_ctx {
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side;  // per layer fork / join points
   cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr;
+  float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
+  cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
   bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
   hg_status sticky = HG_OK;
@@ -563,6 +565,11 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   g_prio_hi = prio_hi;
   for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
+  if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocDefault)) != cudaSuccess)
+    return bail(e, "cudaHostAlloc");
+  for (int i = 0; i < HG_LOSS_RING; ++i)
+    if ((e = cudaEventCreateWithFlags(&x->loss_ev[i], cudaEventDisableTiming)) != cudaSuccess)
+      return bail(e, "cudaEventCreate");
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
     for (int l = 0; l < c->layers; ++l) {
       cudaEvent_t ev;
@@ -635,6 +642,9 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
     for (auto ev : *v) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start})
     if (ev) cudaEventDestroy(ev);
+  for (cudaEvent_t ev : x->loss_ev)
+    if (ev) cudaEventDestroy(ev);
+  if (x->loss_ring) cudaFreeHost(x->loss_ring);
   if (x->comm) ncclCommDestroy(x->comm);
   for (auto ev : x->bucket_ready) cudaEventDestroy(ev);
   if (x->comm_done) cudaEventDestroy(x->comm_done);
@@ -962,6 +972,25 @@ hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms,
   }
   if (launches)
     for (int i = 0; i < HG_PHASE_COUNT; ++i) launches[i] = pr.launches[i];
+  return HG_OK;
+}
+
+hg_status hg_loss_enqueue(hg_ctx *x, int32_t i) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (i < 0 || i >= HG_LOSS_RING) return fail(HG_E_RANGE, "loss ring index %d out of range", i);
+  CK(x, cudaMemcpyAsync(x->loss_ring + i, x->f(x->plan.loss), sizeof(float), cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaEventRecord(x->loss_ev[i], x->stream));
+  return HG_OK;
+}
+
+hg_status hg_loss_fetch(hg_ctx *x, int32_t i, float *loss) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (i < 0 || i >= HG_LOSS_RING) return fail(HG_E_RANGE, "loss ring index %d out of range", i);
+  if (!loss) return fail(HG_E_INVALID, "null output");
+  CK(x, cudaEventSynchronize(x->loss_ev[i]));
+  *loss = x->loss_ring[i];
   return HG_OK;
 }
 

@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -29,6 +30,16 @@ hg_status fail(hg_status st, const char *fmt, ...) {
   va_end(ap);
   t_err = buf;
   return st;
+}
+
+// threads of one collation (hg_pack / hg_pack_host): HG_PACK_THREADS, default 4
+static int hg_pack_threads() {
+  static const int n = [] {
+    const char *e = std::getenv("HG_PACK_THREADS");
+    const int v = e ? std::atoi(e) : 4;
+    return v > 0 ? v : 1;
+  }();
+  return n;
 }
 
 static int hw_threads(int32_t t) {
@@ -176,6 +187,15 @@ hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads,
       if (n < 1) { st[t] = HG_E_EMPTY; bad[t] = g; break; }
       if (e1 < e0 || n1 < n0) { st[t] = HG_E_SHAPE; bad[t] = g; break; }
       mxn[t] = std::max<int32_t>(mxn[t], (int32_t)n);
+      {  // fault in this graph's node-feature pages now (a borrowed, memory-mapped store would
+         // otherwise page-fault inside every later collation)
+        volatile float sink = 0.f;
+        const float *xa = s->x + n0 * s->F0;
+        const int64_t nx = n * s->F0;
+        for (int64_t q = 0; q < nx; q += 1024) sink = sink + xa[q];
+        sink = sink + xa[nx - 1];
+        (void)sink;
+      }
       rs.assign((size_t)n + 1, 0);
       for (int64_t k = e0; k < e1; ++k) {
         const int32_t a = s->src[k], b = s->dst[k];
@@ -318,12 +338,27 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
   float *x = (float *)(base + o.x);
   float *ea = (float *)(base + o.eattr);
   uint8_t *sl = base + o.slot;
-  int64_t nb = 0, eb = 0;
   const int maxdeg = cfg->max_degree > 0 ? cfg->max_degree : HG_MAX_DEGREE;
-  gp[0] = 0;
-  rp[0] = 0;
+  // graph b's node / edge offsets in the batch (prefix sums), then the graphs are
+  // collated independently (in parallel: hg_pack_threads()); the bytes do not
+  // depend on the thread count
+  thread_local std::vector<int64_t> nbo, ebo;
+  nbo.resize((size_t)B + 1);
+  ebo.resize((size_t)B + 1);
+  nbo[0] = ebo[0] = 0;
   for (int32_t b = 0; b < B; ++b) {
     const int64_t g = ids[b];
+    nbo[b + 1] = nbo[b] + (s->no[g + 1] - s->no[g]);
+    ebo[b + 1] = ebo[b] + (s->eo[g + 1] - s->eo[g]);
+  }
+  gp[0] = 0;
+  rp[0] = 0;
+  int32_t bad_b = -1;  // first offending graph in batch order
+  int64_t bad_deg = 0;
+  const int64_t *nbp = nbo.data(), *ebp = ebo.data();
+#pragma omp parallel for num_threads(hg_pack_threads()) schedule(static) if (B >= 32)
+  for (int32_t b = 0; b < B; ++b) {
+    const int64_t g = ids[b], nb = nbp[b], eb = ebp[b];
     const int64_t n0 = s->no[g], n = s->no[g + 1] - n0, e0 = s->eo[g], e = s->eo[g + 1] - e0;
     y[b] = s->y[g];
     std::memcpy(x + nb * s->F0, s->x + n0 * s->F0, sizeof(float) * n * s->F0);
@@ -338,15 +373,17 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
         col[eb + k] = (int32_t)(s->dst[e0 + k] + nb);
         ++k;
       }
-      if (k - kstart > maxdeg)
-        return fail(HG_E_CAPACITY, "graph %lld has a node of degree %lld > max_degree %d", (long long)g,
-                    (long long)(k - kstart), maxdeg);
+      if (k - kstart > maxdeg) {
+#pragma omp critical
+        if (bad_b < 0 || b < bad_b) { bad_b = b; bad_deg = k - kstart; }
+      }
       rp[nb + i + 1] = (int32_t)(eb + k);
     }
-    nb += n;
-    eb += e;
-    gp[b + 1] = (int32_t)nb;
+    gp[b + 1] = (int32_t)(nb + n);
   }
+  if (bad_b >= 0)
+    return fail(HG_E_CAPACITY, "graph %lld has a node of degree %lld > max_degree %d", (long long)ids[bad_b],
+                (long long)bad_deg, maxdeg);
   if (used) *used = (size_t)o.total;
   return HG_OK;
 }

@@ -107,6 +107,8 @@ SIGNATURES = {
     "hg_capture_step": [_P, _I32, ctypes.POINTER(hg_adamw)],
     "hg_profile_step": [_P, _I32, ctypes.POINTER(hg_adamw), _P, _P],
     "hg_loss_get": [_P, ctypes.POINTER(ctypes.c_float)],
+    "hg_loss_enqueue": [_P, ctypes.c_int32],
+    "hg_loss_fetch": [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_float)],
     "hg_sync": [_P],
     "hg_launch_count": [_P, _I64P],
 }
@@ -417,6 +419,16 @@ class Context:
     def loss(self) -> float:
         out = ctypes.c_float()
         _check(_lib.hg_loss_get(self.handle, ctypes.byref(out)))
+        return out.value
+
+    def loss_enqueue(self, i: int):
+        """Start the D2H copy of the last loss into pinned ring entry i (no sync)."""
+        _check(_lib.hg_loss_enqueue(self.handle, i))
+
+    def loss_fetch(self, i: int) -> float:
+        """Wait for ring entry i's copy and return the loss it holds."""
+        out = ctypes.c_float()
+        _check(_lib.hg_loss_fetch(self.handle, i, ctypes.byref(out)))
         return out.value
 
     def sync(self):
