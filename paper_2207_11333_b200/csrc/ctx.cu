@@ -147,8 +147,8 @@ struct hg_ctx {
   std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
-  std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side;  // per layer fork / join points
-  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr;
+  std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx;  // per layer fork / join points
+  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_hgrad = nullptr;
   float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
@@ -243,6 +243,7 @@ void phase(Prof *pr, int ph, F &&fn) {
 }
 
 hg_status enqueue_bucket(hg_ctx *x, cudaStream_t st, int b);
+std::pair<int64_t, int64_t> bucket_range(hg_ctx *x, int b);
 
 // ---- the step's kernel sequence (enqueue only) ----
 void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool fuse_head_bwd = false) {
@@ -332,7 +333,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
 }
 
 void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false,
-                      bool overlap_allreduce = false) {
+                      bool overlap_allreduce = false, const hg_adamw *fuse_adamw = nullptr) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
@@ -360,6 +361,26 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     g_low_prio = false;
   });
   if (overlap_allreduce) enqueue_bucket(x, side, 0);
+  // Fused optimizer: AdamW of each gradient bucket as soon as the bucket is final
+  // (allreduced when W > 1) and nothing later in this step reads its parameters,
+  // all on one stream in bucket order (the last launch advances the step counter).
+  const bool fused = fuse_adamw && fork;
+  cudaStream_t ast = (x->world > 1 && x->comm) ? x->comm_stream : side2;
+  auto adamw_bucket = [&](int bk) {
+    auto r = bucket_range(x, bk);
+    launch_adamw(ast, x->f(p.params) + r.first, x->f(p.grads) + r.first, x->f(p.m) + r.first, x->f(p.v) + r.first,
+                 r.second - r.first, reinterpret_cast<AdamDev *>(x->b(p.adam)), fuse_adamw->lr, fuse_adamw->beta1,
+                 fuse_adamw->beta2, fuse_adamw->eps, fuse_adamw->weight_decay, bk == c.layers);
+  };
+  if (fused) {
+    if (ast == side2) {
+      rec(x->ev_hgrad, side);
+      wait(side2, x->ev_hgrad);
+    }
+    g_low_prio = true;
+    adamw_bucket(0);
+    g_low_prio = false;
+  }
   const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
   const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
   if (x->use_tc && !cls)
@@ -433,8 +454,10 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     if (overlap_allreduce) {  // conv l gradients complete
       wait(side2, x->ev_gram[l]);
       enqueue_bucket(x, side2, c.layers - l);
+    } else if (fused) {
+      wait(side2, x->ev_gram[l]);
     }
-    rec(x->ev_side[l], side2);
+    if (!fused) rec(x->ev_side[l], side2);
     // ---- main: dX into dZ[l-1]
     if (l > 0) {
       float *dZn = x->f(p.dZ[l - 1]), *dZnl = cls ? x->f(p.dZ_lo[l - 1]) : nullptr;
@@ -447,6 +470,14 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         else
           launch_dX(st, x->caps, blob, dP, x->param(lname(l, "M_x")), F, Xl, dZn);
       });
+    }
+    if (fused) {  // layer l's parameters are no longer read by this step (dX_l was the last reader)
+      rec(x->ev_dx[l], st);
+      wait(ast, x->ev_dx[l]);
+      g_low_prio = true;
+      adamw_bucket(c.layers - l);
+      g_low_prio = false;
+      rec(x->ev_side[l], ast);
     }
   }
   wait(st, x->ev_gram[0]);  // join: every gradient is complete on the main stream
@@ -563,14 +594,14 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
-  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start})
+  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
   if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocDefault)) != cudaSuccess)
     return bail(e, "cudaHostAlloc");
   for (int i = 0; i < HG_LOSS_RING; ++i)
     if ((e = cudaEventCreateWithFlags(&x->loss_ev[i], cudaEventDisableTiming)) != cudaSuccess)
       return bail(e, "cudaEventCreate");
-  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
+  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
     for (int l = 0; l < c->layers; ++l) {
       cudaEvent_t ev;
       if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
@@ -638,9 +669,9 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
   if (x->side_stream) cudaStreamDestroy(x->side_stream);
   if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
-  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side})
+  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
     for (auto ev : *v) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start})
+  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : x->loss_ev)
     if (ev) cudaEventDestroy(ev);
@@ -910,9 +941,14 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->cap_stream, slot, nullptr, true);
-  enqueue_backward(x, x->cap_stream, slot, nullptr, true, true);  // bucketed, overlapped allreduce
+  // bucketed, overlapped allreduce and (HG_FUSE_ADAMW=1) per-bucket AdamW inside the backward
+  static const bool fuse = [] {
+    const char *v = getenv("HG_FUSE_ADAMW");
+    return v && atoi(v) != 0;
+  }();
+  enqueue_backward(x, x->cap_stream, slot, nullptr, true, true, fuse ? h : nullptr);
   hg_status ar = join_buckets(x, x->cap_stream);
-  enqueue_step(x, x->cap_stream, *h);
+  if (!fuse) enqueue_step(x, x->cap_stream, *h);
   const int64_t nk = launches_so_far() - l0;
   cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
   if (ar) {

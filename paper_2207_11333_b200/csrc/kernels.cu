@@ -1084,7 +1084,7 @@ void launch_head_grads(cudaStream_t st, const Caps &c, const uint8_t *blob, cons
 __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const float4 *__restrict__ g,
                                                float4 *__restrict__ m, float4 *__restrict__ v, int64_t n4,
                                                const AdamDev *ad, float lr, float beta1,
-                                               float beta2, float eps, float wd) {
+                                               float beta2, float eps, float wd, int advance) {
   pdl_enter();
   // bias corrections of step t = ad->step + 1 (fp64 as the oracle), once per block
   __shared__ float s_ss, s_ib;
@@ -1112,6 +1112,8 @@ __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const flo
     p[i] = P; m[i] = Mv; v[i] = Vv;
   }
   // every block has read ad->step above; the last block to finish advances it
+  // (only in the launch that updates the last parameter range of the step)
+  if (!advance) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     AdamDev *w = const_cast<AdamDev *>(ad);
@@ -1123,12 +1125,12 @@ __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const flo
 }
 
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
-                  float lr, float beta1, float beta2, float eps, float wd) {
+                  float lr, float beta1, float beta2, float eps, float wd, bool advance) {
   const int64_t n4 = n / 4;
-  const int blocks = (int)std::min<int64_t>((n4 + 255) / 256, kSMs * 8);
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, kSMs * 8));
   launch_ex(k_adamw, blocks, 256, 0, st, reinterpret_cast<float4 *>(p), reinterpret_cast<const float4 *>(g),
-                                  reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, ad, lr, beta1,
-                                  beta2, eps, wd);
+            reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, ad, lr, beta1, beta2, eps, wd,
+            advance ? 1 : 0);
   counted();
 }
 

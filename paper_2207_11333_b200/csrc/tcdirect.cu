@@ -746,7 +746,7 @@ cudaError_t tcd_configure() {
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
   auto env_bn = [](const char *n, int &v) {
-    if (const char *s = getenv(n)) v = atoi(s) == 128 ? 128 : 64;
+    if (const char *s = getenv(n)) v = atoi(s) == 128 ? 128 : atoi(s) == 32 ? 32 : 64;
   };
   env_bn("HG_BN_UPD", g_bn_upd);
   env_bn("HG_BN_DA", g_bn_da);
@@ -755,6 +755,7 @@ cudaError_t tcd_configure() {
   if (const char *v = getenv("HG_UPDATE_SK")) g_update_sk = atoi(v) != 0;
   if ((e = cudaFuncSetAttribute(k_update_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM)) != cudaSuccess)
     return e;
+  if ((e = tconfigure_bn<32>()) != cudaSuccess) return e;
   if ((e = tconfigure_bn<64>()) != cudaSuccess) return e;
   if ((e = tconfigure_bn<128>()) != cudaSuccess) return e;
   return tmn_configure();
@@ -787,26 +788,30 @@ void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *
     g_launches += 1;
     return;
   }
-  if (g_bn_upd == 128) update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
+  if (g_bn_upd == 32) update_bn<32>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
+  else if (g_bn_upd == 128) update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
   else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
 }
 
 void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
                      const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
-  if (g_bn_da == 128) dA_bn<128>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
+  if (g_bn_da == 32) dA_bn<32>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
+  else if (g_bn_da == 128) dA_bn<128>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
   else dA_bn<64>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
 }
 
 void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
                    const float *Mx, const float *Mx_lo, float *P) {
-  if (g_bn_proj == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+  if (g_bn_proj == 32) proj_bn<32>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+  else if (g_bn_proj == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
   else proj_bn<64>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
 }
 
 void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
                  const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
                  const int *pos) {
-  if (g_bn_dx == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+  if (g_bn_dx == 32) dX_bn<32>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+  else if (g_bn_dx == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
   else dX_bn<64>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
 }
 

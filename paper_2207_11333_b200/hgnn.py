@@ -153,6 +153,7 @@ DEFAULT_ADAMW = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0
 
 
 HG_FLAG_SIMT_GEMM = 1
+HG_LOSS_RING = 4  # include/hgnn.h
 
 
 def make_config(f_node, f_edge, hidden, layers, max_graphs, max_nodes, max_edges, delta, fc_hidden=None,

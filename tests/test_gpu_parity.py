@@ -173,3 +173,23 @@ def test_errors_surface_through_the_abi(torch_cuda):
     ctx.train_step(0)
     ctx.sync()
     assert ctx.launch_count() > 0
+
+
+@pytest.mark.gpu
+def test_pipelined_loss_readback_matches_sync_read(torch_cuda):
+    """hg_loss_enqueue / hg_loss_fetch return exactly what hg_loss_get reads, one step later."""
+    data = PT.generate("tiny", 300, 4)
+    ctx, cfg, delta = PT.make_ctx(data, 16, 128, 2)
+    hyper = dict(hgnn.DEFAULT_ADAMW)
+    ids = list(range(16))
+    ctx.pack(ctx._store, ids, 0)
+    sync_losses, ring = [], []
+    for k in range(5):
+        ctx.train_step(0, graph=True, **hyper)
+        ctx.loss_enqueue(k % hgnn.HG_LOSS_RING)
+        sync_losses.append(ctx.loss())
+        ring.append(ctx.loss_fetch(k % hgnn.HG_LOSS_RING))
+    assert ring == sync_losses
+    with pytest.raises(hgnn.HgError) as e:
+        ctx.loss_enqueue(hgnn.HG_LOSS_RING)
+    assert e.value.name == "HG_E_RANGE"
