@@ -241,6 +241,21 @@ enum {
 };
 hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms, int64_t *launches);
 
+/* ---- Forward-only evaluation (SPEC.md:385-389 `evaluate`;
+ * PAPER.md:377-381 reports MAE). hg_eval_reset zeroes the device accumulators;
+ * hg_eval_batch runs the forward of the batch in `slot` (graph != 0: captured
+ * once per slot and replayed) and adds sum (yhat-y)^2, sum |yhat-y| and the
+ * graph count to fp64 device accumulators in a fixed order (deterministic);
+ * hg_eval_result synchronises and returns MSE = sum sq / n, MAE = sum abs / n
+ * over every graph since the reset (HG_E_EMPTY if none). hg_eval_pairs copies
+ * the (y, yhat) parity pairs of the last forward of `slot` to caller host
+ * buffers of capacity `cap` (HG_E_CAPACITY if the batch is larger), *n = B.
+ * Parameters are not modified. */
+hg_status hg_eval_reset(hg_ctx *x);
+hg_status hg_eval_batch(hg_ctx *x, int32_t slot, int32_t graph);
+hg_status hg_eval_result(hg_ctx *x, double *mse, double *mae, int64_t *count);
+hg_status hg_eval_pairs(hg_ctx *x, int32_t slot, float *y, float *yhat, int32_t cap, int32_t *n);
+
 /* Read the loss of the last forward (synchronises the compute stream). */
 hg_status hg_loss_get(hg_ctx *x, float *loss);
 /* Pipelined loss read-back: hg_loss_enqueue copies the loss of the last enqueued

@@ -515,3 +515,31 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
         by["head_relu"] += nb
         dec["head_relu"] = np.where(valid, g, own)
     return dec, {"overrides": n, "out_of_band": bad, "out_of_band_by": by}
+
+
+# ---------------------------------------------------------------- evaluation
+def regression_metrics(yhat, y) -> dict:
+    """MSE and MAE of predictions (SPEC.md:385-389 `evaluate`; "measured in mean
+    absolute error (MAE)"): MSE = (1/n) sum (yhat - y)^2, MAE = (1/n) sum |yhat - y|, n = #graphs."""
+    yhat = np.asarray(yhat, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    if yhat.shape != y.shape or yhat.size == 0:
+        raise ValueError("need equally long, non-empty prediction and target vectors")
+    e = yhat - y
+    return {"mse": float(np.mean(e * e)), "mae": float(np.mean(np.abs(e))), "count": int(y.size)}
+
+
+def evaluate(params: dict, store: dict, batches, cfg: dict, delta: float) -> dict:
+    """Forward-only evaluation over a list of batches: metrics over all
+    graphs of all batches plus the (y, yhat) parity pairs in batch order."""
+    ys, yh = [], []
+    for ids in batches:
+        batch = pack(store, ids)
+        _, yhat, _ = forward(params, batch, cfg, delta)
+        ys.append(batch["y"])
+        yh.append(yhat)
+    y = np.concatenate(ys)
+    yhat = np.concatenate(yh)
+    out = regression_metrics(yhat, y)
+    out["pairs"] = np.stack([y, yhat], axis=1)
+    return out

@@ -32,7 +32,8 @@ struct Plan {
   // readers never hold up the main chain (no write-after-read waits)
   std::vector<size_t> dZ, dZ_lo, dPl, dPl_lo, pagg;
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
-  size_t part = 0, part2 = 0, part3 = 0;  // scratch: agg_bwd (dM_e), Gram (dU), dM_x partials
+  size_t part = 0, part2 = 0, part3 = 0;
+  size_t eval_acc = 0;  // scratch: agg_bwd (dM_e), Gram (dU), dM_x partials
   size_t UT = 0, u_off = 0;
   int cmax = 0;  // degree-class slots (0 = class GEMMs off)
   size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
@@ -60,6 +61,7 @@ Plan make_plan(const hg_config &c) {
   p.v = take(PB);
   p.adam = take(sizeof(AdamDev));
   p.loss = take(sizeof(float) * 4);
+  p.eval_acc = take(sizeof(double) * 4);  // evaluation sums: sq err, abs err, graphs
   p.blob_max = (size_t)batch_offsets(c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge).total;
   for (int s = 0; s < c.n_slots; ++s) p.slot.push_back(take(p.blob_max));
   p.amp = take(sizeof(float) * N);
@@ -141,6 +143,8 @@ struct hg_ctx {
   std::vector<cudaGraphExec_t> graphs;
   std::vector<int64_t> graph_kernels;
   std::vector<hg_adamw> graph_hyper;
+  std::vector<cudaGraphExec_t> eval_graphs;  // forward + metric accumulation per slot
+  std::vector<int64_t> eval_kernels;
   ncclComm_t comm = nullptr;
   int rank = 0, world = 1;
   cudaStream_t comm_stream = nullptr;           // bucketed allreduce overlapping the backward
@@ -618,6 +622,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     x->compute_done.push_back(b2);
     x->graphs.push_back(nullptr);
     x->graph_kernels.push_back(0);
+    x->eval_graphs.push_back(nullptr);
+    x->eval_kernels.push_back(0);
     x->graph_hyper.push_back(hg_adamw{});
   }
   if ((e = cudaMemsetAsync(workspace, 0, plan.total, x->stream)) != cudaSuccess) return bail(e, "cudaMemsetAsync");
@@ -661,6 +667,8 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (!x) return HG_OK;
   if (x->stream || x->copy_stream) cudaDeviceSynchronize();
   for (auto g : x->graphs)
+    if (g) cudaGraphExecDestroy(g);
+  for (auto g : x->eval_graphs)
     if (g) cudaGraphExecDestroy(g);
   for (auto h : x->staging) cudaFreeHost(h);
   for (auto ev : x->copy_done) cudaEventDestroy(ev);
@@ -841,6 +849,81 @@ hg_status hg_forward(hg_ctx *x, int32_t slot) {
   enqueue_forward(x, x->stream, slot);
   x->launches += launches_so_far() - l0;
   return after_enqueue(x, "forward launch");
+}
+
+// ---- evaluation path
+hg_status hg_eval_reset(hg_ctx *x) {
+  hg_status st = usable(x);
+  if (st) return st;
+  CK(x, cudaMemsetAsync(x->b(x->plan.eval_acc), 0, sizeof(double) * 4, x->stream));
+  return HG_OK;
+}
+
+hg_status hg_eval_batch(hg_ctx *x, int32_t slot, int32_t graph) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
+  const uint8_t *blob = x->b(x->plan.slot[slot]);
+  double *acc = reinterpret_cast<double *>(x->b(x->plan.eval_acc));
+  if (!graph) {
+    const int64_t l0 = launches_so_far();
+    enqueue_forward(x, x->stream, slot);
+    launch_eval_accum(x->stream, blob, x->f(x->plan.yhat), acc);
+    x->launches += launches_so_far() - l0;
+    if ((st = after_enqueue(x, "eval launch"))) return st;
+  } else {
+    if (!x->eval_graphs[slot]) {
+      cudaGraph_t g = nullptr;
+      CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
+      const int64_t l0 = launches_so_far();
+      enqueue_forward(x, x->cap_stream, slot);
+      launch_eval_accum(x->cap_stream, blob, x->f(x->plan.yhat), acc);
+      const int64_t nk = launches_so_far() - l0;
+      cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
+      if (e != cudaSuccess) return cuda_fail(x, e, "cudaStreamEndCapture");
+      cudaGraphExec_t ex = nullptr;
+      e = cudaGraphInstantiate(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
+      cudaGraphDestroy(g);
+      if (e != cudaSuccess) return cuda_fail(x, e, "cudaGraphInstantiate");
+      x->eval_graphs[slot] = ex;
+      x->eval_kernels[slot] = nk;
+    }
+    CK(x, cudaGraphLaunch(x->eval_graphs[slot], x->stream));
+    x->launches += x->eval_kernels[slot];
+  }
+  CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
+  return HG_OK;
+}
+
+hg_status hg_eval_result(hg_ctx *x, double *mse, double *mae, int64_t *count) {
+  hg_status st = usable(x);
+  if (st) return st;
+  double h[4] = {0, 0, 0, 0};
+  CK(x, cudaMemcpyAsync(h, x->b(x->plan.eval_acc), sizeof(h), cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  const int64_t n = (int64_t)h[2];
+  if (count) *count = n;
+  if (n == 0) return fail(HG_E_EMPTY, "no graphs evaluated since hg_eval_reset");
+  if (mse) *mse = h[0] / (double)n;
+  if (mae) *mae = h[1] / (double)n;
+  return HG_OK;
+}
+
+hg_status hg_eval_pairs(hg_ctx *x, int32_t slot, float *y, float *yhat, int32_t cap, int32_t *n) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  if (!y || !yhat || !n) return fail(HG_E_INVALID, "null argument");
+  int32_t hdr[kHeaderInts];
+  CK(x, cudaMemcpyAsync(hdr, x->b(x->plan.slot[slot]), sizeof(hdr), cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  const int32_t B = hdr[0];
+  if (B > cap) return fail(HG_E_CAPACITY, "batch has %d graphs > cap %d", B, cap);
+  const BatchOffsets o = batch_offsets(hdr[0], hdr[1], hdr[2], hdr[3], hdr[4]);
+  CK(x, cudaMemcpyAsync(y, x->b(x->plan.slot[slot]) + o.y, sizeof(float) * B, cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaMemcpyAsync(yhat, x->f(x->plan.yhat), sizeof(float) * B, cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  *n = B;
+  return HG_OK;
 }
 
 hg_status hg_backward(hg_ctx *x, int32_t slot) {

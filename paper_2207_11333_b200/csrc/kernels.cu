@@ -1027,6 +1027,41 @@ void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float
   counted();
 }
 
+// evaluation sums: acc[0] += sum (yhat-y)^2, acc[1] += sum |yhat-y|,
+// acc[2] += B, in fp64 with a fixed-order block tree (deterministic)
+__global__ void __launch_bounds__(256) k_eval_accum(const uint8_t *__restrict__ blob, const float *__restrict__ yhat,
+                                                    double *__restrict__ acc) {
+  pdl_enter();
+  __shared__ double rs[256], ra[256];
+  const BatchView b = load_batch(blob);
+  double s = 0.0, a = 0.0;
+  for (int g = threadIdx.x; g < b.B; g += blockDim.x) {
+    const double e = (double)yhat[g] - (double)b.y[g];
+    s += e * e;
+    a += fabs(e);
+  }
+  rs[threadIdx.x] = s;
+  ra[threadIdx.x] = a;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      rs[threadIdx.x] += rs[threadIdx.x + w];
+      ra[threadIdx.x] += ra[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    acc[0] += rs[0];
+    acc[1] += ra[0];
+    acc[2] += (double)b.B;
+  }
+}
+
+void launch_eval_accum(cudaStream_t st, const uint8_t *blob, const float *yhat, double *acc) {
+  launch_ex(k_eval_accum, 1, 256, 0, st, blob, yhat, acc);
+  counted();
+}
+
 // head parameter gradients: thread per output element, fixed order over graphs
 __global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__restrict__ G,
                              const float *__restrict__ hpre, const float *__restrict__ dy,

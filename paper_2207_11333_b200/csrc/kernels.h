@@ -70,6 +70,8 @@ void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const 
 // head parameter gradients only (the tail of launch_head_bwd)
 void launch_head_grads(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *G, const float *hpre,
                        const float *dy, const float *dhid, float *gW1, float *gb1, float *gW2, float *gb2);
+// evaluation sums of one batch into acc[0..2] (fp64: squared error, absolute error, graphs)
+void launch_eval_accum(cudaStream_t st, const uint8_t *blob, const float *yhat, double *acc);
 // mean squared error over the batch from the per-graph terms (after launch_head_fused)
 void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float *loss);
 void head_configure(const Caps &c);

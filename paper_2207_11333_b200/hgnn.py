@@ -108,6 +108,11 @@ SIGNATURES = {
     "hg_profile_step": [_P, _I32, ctypes.POINTER(hg_adamw), _P, _P],
     "hg_loss_get": [_P, ctypes.POINTER(ctypes.c_float)],
     "hg_loss_enqueue": [_P, ctypes.c_int32],
+    "hg_eval_reset": [_P],
+    "hg_eval_batch": [_P, ctypes.c_int32, ctypes.c_int32],
+    "hg_eval_result": [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                       ctypes.POINTER(ctypes.c_int64)],
+    "hg_eval_pairs": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
     "hg_loss_fetch": [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_float)],
     "hg_sync": [_P],
     "hg_launch_count": [_P, _I64P],
@@ -421,6 +426,26 @@ class Context:
         out = ctypes.c_float()
         _check(_lib.hg_loss_get(self.handle, ctypes.byref(out)))
         return out.value
+
+    # ---- forward-only evaluation (hg_eval_*)
+    def eval_reset(self):
+        _check(_lib.hg_eval_reset(self.handle))
+
+    def eval_batch(self, slot: int, graph: bool = True):
+        _check(_lib.hg_eval_batch(self.handle, slot, 1 if graph else 0))
+
+    def eval_result(self) -> dict:
+        mse, mae, n = ctypes.c_double(), ctypes.c_double(), ctypes.c_int64()
+        _check(_lib.hg_eval_result(self.handle, ctypes.byref(mse), ctypes.byref(mae), ctypes.byref(n)))
+        return {"mse": mse.value, "mae": mae.value, "count": n.value}
+
+    def eval_pairs(self, slot: int) -> np.ndarray:
+        """(y, yhat) parity pairs of the last forward of `slot`, shape [B, 2]."""
+        cap = self.cfg.max_graphs
+        y, yh = np.zeros(cap, np.float32), np.zeros(cap, np.float32)
+        n = ctypes.c_int32()
+        _check(_lib.hg_eval_pairs(self.handle, slot, _ptr(y), _ptr(yh), cap, ctypes.byref(n)))
+        return np.stack([y[:n.value], yh[:n.value]], axis=1)
 
     def loss_enqueue(self, i: int):
         """Start the D2H copy of the last loss into pinned ring entry i (no sync)."""

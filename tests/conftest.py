@@ -1,3 +1,4 @@
+import pytest
 import os
 import sys
 
@@ -9,3 +10,12 @@ if ROOT not in sys.path:
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a B200 (runs the CUDA path through the C-ABI)")
     config.addinivalue_line("markers", "slow: longer CPU test")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    """The torch module with a CUDA device (skips the test without one)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch

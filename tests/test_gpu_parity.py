@@ -12,14 +12,6 @@ from tests._util import make_store
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def torch_cuda():
-    torch = pytest.importorskip("torch")
-    if not torch.cuda.is_available():
-        pytest.skip("no CUDA device")
-    return torch
-
-
 def test_device_pack_bit_exact(torch_cuda):
     data = PT.generate("pcqm", 2000, 11)
     ctx, cfg, delta = PT.make_ctx(data, 128, 128, 6)
