@@ -283,6 +283,30 @@ def main():
     value = world * K * B / (total_ms / 1e3)
     loss_now = ctx.loss()
 
+    # ---- forward-only evaluation over the resident batches: device-timed
+    ctx.eval_reset()
+    for s in range(n_res):  # capture the eval graphs, warm
+        ctx.eval_batch(s)
+    ctx.eval_reset()
+    barrier()
+    torch.cuda.synchronize()
+    ev_a, ev_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev_a.record(stream)
+    for k in range(K):
+        ctx.eval_batch(k % n_res)
+    ev_b.record(stream)
+    torch.cuda.synchronize()
+    em = ev_a.elapsed_time(ev_b)
+    tm = torch.tensor([em], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    em = float(tm.item())
+    er = ctx.eval_result()
+    eval_out = {"value": world * K * B / (em / 1e3), "unit": "graphs/s", "ms_per_batch": em / K,
+                "mse": er["mse"], "mae": er["mae"], "graphs": er["count"],
+                "note": "hg_eval_batch (forward + fp64 MSE/MAE accumulation, graph replay) over the resident "
+                        "batches, device-timed, no L2 flush; metrics of the trained-for-a-few-steps model"}
+
     # ---- e2e through the public API from host buffers
     e2e = None
     if not args.no_e2e:
@@ -423,7 +447,7 @@ def main():
         "roofline": prof, "phase_roofline": phase_roof,
         "phases_ms": {k: round(v[0], 4) for k, v in phases.items()},
         "phase_launches": {k: v[1] for k, v in phases.items()},
-        "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clk,
+        "cpu_baseline": cpu, "e2e": e2e, "eval": eval_out, "gpu_launches": launches, "clocks": clk,
         "loss_after_timed": loss_now,
     }
     sys.stdout.flush()
