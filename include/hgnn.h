@@ -46,7 +46,8 @@ typedef enum {
   HG_E_CUDA = 8,       /* CUDA runtime failure */
   HG_E_NCCL = 9,       /* NCCL failure (TransportFailure) */
   HG_E_STATE = 10,     /* ctx unusable after a sticky failure, or call out of order */
-  HG_E_UNSORTED = 11   /* per-graph edges not sorted by (src, dst) */
+  HG_E_UNSORTED = 11,  /* per-graph edges not sorted by (src, dst) */
+  HG_E_IO = 12         /* container / object file missing, truncated, bad magic or checksum */
 } hg_status;
 
 /* Largest supported node degree: argmin/argmax positions are stored as u8
@@ -240,6 +241,30 @@ enum {
   HG_PHASE_DX = 10, HG_PHASE_ALLREDUCE = 11, HG_PHASE_ADAMW = 12, HG_PHASE_COUNT = 13
 };
 hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms, int64_t *launches);
+
+/* ---- On-disk packed container with subfiles: the ADIOS
+ * stand-in of PAPER.md:183-192 — the Table-1 variables as
+ * global arrays with per-graph offsets, split over `n_subfiles` files that hold
+ * contiguous graph ranges ("control the number of subfiles").
+ * Format (little-endian, version 1): `dir`/meta.idx = header {"HGPK", version,
+ * G, N, E, F0, Fe, n_sub}, node_offset[G+1], edge_offset[G+1] (int64),
+ * sub_graph[n_sub+1], CRC-32C; `dir`/data.<k> = header {"HGPD", version, global
+ * graph/node/edge ranges} then x, src, dst, edge_attr, y blocks each followed by
+ * its CRC-32C. The index is written last.
+ * hg_container_write: writes the store (threads: one per subfile). Creates `dir`
+ *   if needed and overwrites its files. HG_E_IO on any write failure.
+ * hg_container_open: reads every subfile straight into owned global arrays
+ *   (parallel), validates CRCs and index consistency (HG_E_IO: missing subfile,
+ *   bad magic/version, truncation, checksum), then validates the graphs exactly
+ *   like hg_store_create; the returned store owns its memory (hg_store_destroy).
+ * hg_container_info: header counts only (no data read).
+ * hg_objfiles_write / hg_objfiles_open: the comparison backend of PAPER.md:341-347
+ *   (one object file per graph, `dir`/g<id>.obj), same store result. */
+hg_status hg_container_write(const hg_store *s, const char *dir, int32_t n_subfiles, int32_t threads);
+hg_status hg_container_open(const char *dir, int32_t threads, hg_store **out);
+hg_status hg_container_info(const char *dir, int64_t *graphs, int64_t *nodes, int64_t *edges, int32_t *subfiles);
+hg_status hg_objfiles_write(const hg_store *s, const char *dir, int32_t threads);
+hg_status hg_objfiles_open(const char *dir, int64_t num_graphs, int32_t threads, hg_store **out);
 
 /* ---- Forward-only evaluation (SPEC.md:385-389 `evaluate`;
  * PAPER.md:377-381 reports MAE). hg_eval_reset zeroes the device accumulators;

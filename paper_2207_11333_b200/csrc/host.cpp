@@ -139,41 +139,12 @@ void init_params_host(const hg_config &c, uint64_t seed, float *dst) {
 
 }  // namespace hg
 
-using namespace hg;
-
-extern "C" {
-
-const char *hg_last_error(void) { return hg::t_err.c_str(); }
-int32_t hg_abi_version(void) { return HG_ABI_VERSION; }
-
-hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads, hg_store **out) {
-  if (!d || !out) return fail(HG_E_INVALID, "null argument");
-  *out = nullptr;
-  if (d->num_graphs < 1) return fail(HG_E_EMPTY, "store has no graphs");
-  if (d->num_nodes < 0 || d->num_edges < 0 || d->f_node < 1 || d->f_edge < 1)
-    return fail(HG_E_INVALID, "bad sizes");
-  if (!d->node_offset || !d->edge_offset || !d->x || !d->y || (d->num_edges && (!d->edge_index || !d->edge_attr)))
-    return fail(HG_E_INVALID, "null array");
-  const int64_t G = d->num_graphs;
-  if (d->node_offset[0] != 0 || d->edge_offset[0] != 0 || d->node_offset[G] != d->num_nodes ||
-      d->edge_offset[G] != d->num_edges)
-    return fail(HG_E_SHAPE, "offsets must start at 0 and end at the totals");
-  hg_store *s = new hg_store();
-  s->G = G; s->N = d->num_nodes; s->E = d->num_edges; s->F0 = d->f_node; s->Fe = d->f_edge;
-  if (copy) {
-    s->own_no.assign(d->node_offset, d->node_offset + G + 1);
-    s->own_eo.assign(d->edge_offset, d->edge_offset + G + 1);
-    s->own_x.assign(d->x, d->x + s->N * s->F0);
-    s->own_ea.assign(d->edge_attr, d->edge_attr + s->E * s->Fe);
-    s->own_y.assign(d->y, d->y + G);
-    s->own_ei.assign(d->edge_index, d->edge_index + 2 * s->E);
-    s->no = s->own_no.data(); s->eo = s->own_eo.data(); s->x = s->own_x.data();
-    s->ea = s->own_ea.data(); s->y = s->own_y.data();
-    s->src = s->own_ei.data(); s->dst = s->own_ei.data() + s->E;
-  } else {
-    s->no = d->node_offset; s->eo = d->edge_offset; s->x = d->x; s->ea = d->edge_attr; s->y = d->y;
-    s->src = d->edge_index; s->dst = d->edge_index + s->E;
-  }
+namespace hg {
+// validate a store whose array pointers are set and compute slot / max stats
+// (shared by hg_store_create and the container readers); on failure the caller
+// deletes s.
+hg_status store_finish(hg_store *s, int32_t threads) {
+  const int64_t G = s->G;
   s->slot.assign((size_t)s->E, 0);
   const int nt = hw_threads(threads);
   std::vector<hg_status> st(nt, HG_OK);
@@ -230,7 +201,6 @@ hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads,
   for (int t = 0; t < nt; ++t) {
     if (st[t] != HG_OK) {
       int64_t g = bad[t];
-      delete s;
       const char *what = st[t] == HG_E_EMPTY ? "empty graph (SPEC.md:356)"
                          : st[t] == HG_E_RANGE ? "edge endpoint out of range"
                          : st[t] == HG_E_UNSORTED ? "edges not sorted by (src,dst)"
@@ -241,6 +211,50 @@ hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads,
     }
     s->max_nodes = std::max(s->max_nodes, mxn[t]);
     s->max_deg = std::max(s->max_deg, mxd[t]);
+  }
+  return HG_OK;
+}
+}  // namespace hg
+
+using namespace hg;
+
+extern "C" {
+
+const char *hg_last_error(void) { return hg::t_err.c_str(); }
+int32_t hg_abi_version(void) { return HG_ABI_VERSION; }
+
+hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads, hg_store **out) {
+  if (!d || !out) return fail(HG_E_INVALID, "null argument");
+  *out = nullptr;
+  if (d->num_graphs < 1) return fail(HG_E_EMPTY, "store has no graphs");
+  if (d->num_nodes < 0 || d->num_edges < 0 || d->f_node < 1 || d->f_edge < 1)
+    return fail(HG_E_INVALID, "bad sizes");
+  if (!d->node_offset || !d->edge_offset || !d->x || !d->y || (d->num_edges && (!d->edge_index || !d->edge_attr)))
+    return fail(HG_E_INVALID, "null array");
+  const int64_t G = d->num_graphs;
+  if (d->node_offset[0] != 0 || d->edge_offset[0] != 0 || d->node_offset[G] != d->num_nodes ||
+      d->edge_offset[G] != d->num_edges)
+    return fail(HG_E_SHAPE, "offsets must start at 0 and end at the totals");
+  hg_store *s = new hg_store();
+  s->G = G; s->N = d->num_nodes; s->E = d->num_edges; s->F0 = d->f_node; s->Fe = d->f_edge;
+  if (copy) {
+    s->own_no.assign(d->node_offset, d->node_offset + G + 1);
+    s->own_eo.assign(d->edge_offset, d->edge_offset + G + 1);
+    s->own_x.assign(d->x, d->x + s->N * s->F0);
+    s->own_ea.assign(d->edge_attr, d->edge_attr + s->E * s->Fe);
+    s->own_y.assign(d->y, d->y + G);
+    s->own_ei.assign(d->edge_index, d->edge_index + 2 * s->E);
+    s->no = s->own_no.data(); s->eo = s->own_eo.data(); s->x = s->own_x.data();
+    s->ea = s->own_ea.data(); s->y = s->own_y.data();
+    s->src = s->own_ei.data(); s->dst = s->own_ei.data() + s->E;
+  } else {
+    s->no = d->node_offset; s->eo = d->edge_offset; s->x = d->x; s->ea = d->edge_attr; s->y = d->y;
+    s->src = d->edge_index; s->dst = d->edge_index + s->E;
+  }
+  hg_status fst = store_finish(s, threads);
+  if (fst != HG_OK) {
+    delete s;
+    return fst;
   }
   *out = s;
   return HG_OK;

@@ -27,6 +27,10 @@ void init_params_host(const hg_config &c, uint64_t seed, float *dst);
 
 // Table-1 store: global arrays + per-graph offsets, plus the
 // derived per-edge slot (position of src inside dst's neighbour row).
+struct hg_store;
+namespace hg {
+hg_status store_finish(hg_store *s, int32_t threads);  // host.cpp
+}
 struct hg_store {
   int64_t G = 0, N = 0, E = 0;
   int32_t F0 = 0, Fe = 0;

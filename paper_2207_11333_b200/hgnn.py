@@ -23,7 +23,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 
 HG_OK = 0
 STATUS = {0: "HG_OK", 1: "HG_E_INVALID", 2: "HG_E_SHAPE", 3: "HG_E_RANGE", 4: "HG_E_EMPTY", 5: "HG_E_ASYMMETRIC",
-          6: "HG_E_DEGREE", 7: "HG_E_CAPACITY", 8: "HG_E_CUDA", 9: "HG_E_NCCL", 10: "HG_E_STATE", 11: "HG_E_UNSORTED"}
+          6: "HG_E_DEGREE", 7: "HG_E_CAPACITY", 8: "HG_E_CUDA", 9: "HG_E_NCCL", 10: "HG_E_STATE", 11: "HG_E_UNSORTED",
+          12: "HG_E_IO"}
 HG_MAX_DEGREE = 127
 
 PHASES = ["scalers", "proj", "agg_fwd", "update", "head_fwd", "head_bwd", "dA", "dU", "agg_bwd", "dMx", "dX",
@@ -109,6 +110,12 @@ SIGNATURES = {
     "hg_loss_get": [_P, ctypes.POINTER(ctypes.c_float)],
     "hg_loss_enqueue": [_P, ctypes.c_int32],
     "hg_eval_reset": [_P],
+    "hg_container_write": [_P, ctypes.c_char_p, ctypes.c_int32, ctypes.c_int32],
+    "hg_container_open": [ctypes.c_char_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)],
+    "hg_container_info": [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int64),
+                          ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_int32)],
+    "hg_objfiles_write": [_P, ctypes.c_char_p, ctypes.c_int32],
+    "hg_objfiles_open": [ctypes.c_char_p, ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(ctypes.c_void_p)],
     "hg_eval_batch": [_P, ctypes.c_int32, ctypes.c_int32],
     "hg_eval_result": [_P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                        ctypes.POINTER(ctypes.c_int64)],
@@ -204,6 +211,38 @@ class Store:
         if copy:
             self._arrays = None
 
+    @classmethod
+    def _adopt(cls, handle):
+        s = cls.__new__(cls)
+        s.handle = handle
+        s._arrays = None
+        g, n, e, mn, md = _I64(), _I64(), _I64(), _I32(), _I32()
+        _check(_lib.hg_store_stats(handle, ctypes.byref(g), ctypes.byref(n), ctypes.byref(e), ctypes.byref(mn),
+                                   ctypes.byref(md)))
+        return s
+
+    @classmethod
+    def from_container(cls, path: str, threads: int = 0) -> "Store":
+        """Open an on-disk packed container (hg_container_open); the store owns its memory."""
+        load()
+        h = ctypes.c_void_p()
+        _check(_lib.hg_container_open(path.encode(), int(threads), ctypes.byref(h)))
+        return cls._adopt(h)
+
+    @classmethod
+    def from_objfiles(cls, path: str, num_graphs: int, threads: int = 0) -> "Store":
+        """Load the object-per-graph comparison backend (hg_objfiles_open)."""
+        load()
+        h = ctypes.c_void_p()
+        _check(_lib.hg_objfiles_open(path.encode(), int(num_graphs), int(threads), ctypes.byref(h)))
+        return cls._adopt(h)
+
+    def write_container(self, path: str, n_subfiles: int, threads: int = 0):
+        _check(_lib.hg_container_write(self.handle, path.encode(), int(n_subfiles), int(threads)))
+
+    def write_objfiles(self, path: str, threads: int = 0):
+        _check(_lib.hg_objfiles_write(self.handle, path.encode(), int(threads)))
+
     def __del__(self):
         if getattr(self, "handle", None) and _lib is not None:
             _lib.hg_store_destroy(self.handle)
@@ -244,6 +283,15 @@ def hg_batch_offsets(B, N, E, f_node, f_edge) -> dict:
     o = hg_batch_offsets_t()
     _check(_lib.hg_batch_offsets_get(B, N, E, f_node, f_edge, ctypes.byref(o)))
     return {k: getattr(o, k) for k, _ in hg_batch_offsets_t._fields_}
+
+
+def container_info(path: str) -> dict:
+    """Counts from a container's index (hg_container_info), no data read."""
+    load()
+    g, n, e, k = _I64(), _I64(), _I64(), _I32()
+    _check(_lib.hg_container_info(path.encode(), ctypes.byref(g), ctypes.byref(n), ctypes.byref(e), ctypes.byref(k)))
+    return {"graphs": g.value, "nodes": n.value, "edges": e.value, "subfiles": k.value,
+            "avg_nodes_per_graph": n.value / g.value}
 
 
 def hg_pack_host(store: Store, ids, cfg: hg_config) -> np.ndarray:
