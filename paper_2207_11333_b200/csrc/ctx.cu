@@ -116,7 +116,7 @@ Plan make_plan(const hg_config &c) {
     p.MxT = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
     p.MxT_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
     p.mx_off = take(sizeof(int64_t) * (size_t)c.layers);
-    pf = std::max({pf, tc_gram_partial_floats(caps, p.cmax), mn_gram_partial_floats(caps, p.cmax),
+    pf = std::max({pf, mn_gram_partial_floats(caps, p.cmax),
                    mn_dmx_partial_floats(caps, H)});
     p.part = take(sizeof(float) * pf);  // (re-take: the class partials are larger)
   }
@@ -152,7 +152,8 @@ struct hg_ctx {
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx;  // per layer fork / join points
-  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_hgrad = nullptr;
+  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_hgrad = nullptr,
+              ev_prepmx = nullptr, ev_prepw = nullptr;
   float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
@@ -258,33 +259,47 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   const bool cls = x->use_tc && p.cmax > 0;
   const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
   const size_t HH = (size_t)c.hidden * c.hidden;
-  // Degree sort and the class / M_x weight preparation run on the side stream,
-  // concurrent with layer 0's projection; joined before layer 0's aggregation
-  // (needs pos) and update (needs the class weights).
+  // Degree sort on side stream 1 and the degree-slot / M_x weight preparation on
+  // side stream 2 (they depend only on the batch resp. the parameters), concurrent
+  // with layer 0's projection; the main chain joins the sort before layer 0's
+  // aggregation (pos), W_d before layer 0's update and M_x before layer 1's projection.
   const bool fork = cls && !pr && x->side_stream != nullptr;
-  cudaStream_t pst = fork ? x->side_stream : st;
-  if (fork) {
-    cudaEventRecord(x->ev_start, st);
-    cudaStreamWaitEvent(pst, x->ev_start, 0);
-  }
+  cudaStream_t wst = fork ? x->side2_stream : st;
+  // The degree sort is the graph's single root (measured: with several root branches the
+  // main stream's first kernel started ~14 us late); the weight preparation forks after it.
   phase(pr, HG_PHASE_SCALERS, [&] {
-    launch_degsort(pst, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
+    launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
                    reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
                    reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)));
   });
-  if (fork) cudaEventRecord(x->ev_deg, pst);
+  if (fork) cudaEventRecord(x->ev_start, st);
+  // the prep branch is enqueued after layer 0's projection so that the main chain is
+  // the sort's first successor in the graph (measured: the other successor starts later)
+  auto enqueue_prep = [&] {
+  if (fork) cudaStreamWaitEvent(wst, x->ev_start, 0);
   if (cls)
-    phase(pr, HG_PHASE_SCALERS, [&] {  // (degree-class weights belong with the scalers)
-      launch_prep_W2(pst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers, p.cmax,
-                     reinterpret_cast<const DegInfo *>(x->b(p.deginfo)), x->f(p.Wf), x->f(p.Wf_lo), x->f(p.WbT),
-                     x->f(p.WbT_lo));
-      launch_prep_Mx(pst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
+    phase(pr, HG_PHASE_SCALERS, [&] {  // (degree-slot weights belong with the scalers)
+      // layer 0's weights first (needed soonest); low priority and narrow grids so the
+      // main chain's first kernels are not kept off the SMs
+      g_low_prio = fork;
+      const int64_t *uo = reinterpret_cast<const int64_t *>(x->b(p.u_off));
+      launch_prep_W2(wst, x->caps, x->f(p.params), uo, 0, 1, p.cmax, c.delta, x->f(p.Wf), x->f(p.Wf_lo),
+                     x->f(p.WbT), x->f(p.WbT_lo));
+      if (fork) cudaEventRecord(x->ev_prep, wst);
+      launch_prep_Mx(wst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
                      x->f(p.Mx_lo), x->f(p.MxT), x->f(p.MxT_lo));
+      if (fork) cudaEventRecord(x->ev_prepmx, wst);
+      if (c.layers > 1)
+        launch_prep_W2(wst, x->caps, x->f(p.params), uo, 1, c.layers, p.cmax, c.delta, x->f(p.Wf), x->f(p.Wf_lo),
+                       x->f(p.WbT), x->f(p.WbT_lo));
+      if (fork) cudaEventRecord(x->ev_prepw, wst);
+      g_low_prio = false;
     });
-  if (fork) cudaEventRecord(x->ev_prep, pst);
+  };
   for (int l = 0; l < c.layers; ++l) {
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
+    if (fork && l == 1) cudaStreamWaitEvent(st, x->ev_prepmx, 0);
     phase(pr, HG_PHASE_PROJ, [&] {
       if (cls && l > 0)
         launch_d_proj(st, x->caps, blob, Xl, x->f(p.X_lo[l - 1]), F, x->param(lname(l, "M_x")),
@@ -294,12 +309,13 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
       else
         launch_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
     });
-    if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_deg, 0);
+    if (l == 0) enqueue_prep();
     phase(pr, HG_PHASE_AGG_FWD, [&] {
       launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
                      c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), cls ? x->f(p.A_lo[l]) : nullptr, pos);
     });
     if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_prep, 0);
+    if (fork && l == 1) cudaStreamWaitEvent(st, x->ev_prepw, 0);
     phase(pr, HG_PHASE_UPDATE, [&] {
       if (cls)
         launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), x->f(p.A_lo[l]),
@@ -316,6 +332,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
                       x->f(p.X[l]));
     });
   }
+  if (fork && c.layers < 2) cudaStreamWaitEvent(st, x->ev_prepw, 0);  // join side stream 2
   phase(pr, HG_PHASE_HEAD_FWD, [&] {
     if (fuse_head_bwd) {
       launch_head_fused(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
@@ -598,7 +615,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
-  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad})
+  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad, &x->ev_prepmx, &x->ev_prepw})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
   if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocDefault)) != cudaSuccess)
     return bail(e, "cudaHostAlloc");
@@ -679,7 +696,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
     for (auto ev : *v) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad})
+  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad, x->ev_prepmx, x->ev_prepw})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : x->loss_ev)
     if (ev) cudaEventDestroy(ev);

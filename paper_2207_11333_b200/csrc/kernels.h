@@ -102,16 +102,6 @@ int tc_max_splits(const Caps &c, int cmax);
 // perm[r] = node at degree-sorted row r, pos = its inverse (pos may be null)
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
                     DegInfo *info, int4 *tiles, int4 *splits, int *pos = nullptr);
-void launch_prep_W(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
-                   const DegInfo *info, float *Wf, float *WbT);
-void launch_tc_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm,
-                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *bU, float *X1);
-void launch_tc_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const int *perm, const DegInfo *info,
-                      const int4 *tiles, const float *WbT, float *dA);
-size_t tc_gram_partial_floats(const Caps &c, int cmax);
-void launch_tc_dU_cls(cudaStream_t st, const Caps &c, int cmax, const uint8_t *blob, const float *dZ, const float *A,
-                      const int *perm, const DegInfo *info, const int4 *splits, float *partial, float *dU,
-                      float *dbU);
 
 // TMA-fed tcgen05 GEMMs over pre-split operands (tcdirect.cu). A / dZ operands of
 // the class GEMMs are stored in degree-sorted row order (row pos[i] for node i).
@@ -128,8 +118,9 @@ void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const floa
                  const int *pos);
 void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,
                     float *Mx_lo, float *MxT, float *MxT_lo);
-void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
-                    const DegInfo *info, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo);
+// layers [l0, l1) of the degree-slot weights
+void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int l0, int l1,
+                    int cmax, double delta, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo);
 
 // TMA-fed MN-major Grams (tcmn.cu): per-class-split dU / db_U and per-split dM_x / db_M,
 // partials reduced in fixed order (class path; rows of dZ / A degree-sorted)

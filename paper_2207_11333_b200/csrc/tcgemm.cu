@@ -483,46 +483,80 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
                                                   int4 *__restrict__ tiles, int4 *__restrict__ splits,
                                                   int *__restrict__ pos) {
   pdl_enter();
-  __shared__ int hist[kMaxClasses], bstart[kMaxClasses], run[kMaxClasses], cls_of[kMaxClasses];
-  __shared__ int wcnt[32][kMaxClasses];
+  __shared__ int hist[kMaxClasses], bstart[kMaxClasses];
+  __shared__ int wcnt[32][kMaxClasses];  // per-warp class counts, then per-warp class bases
+  __shared__ float tamp[kMaxClasses], tatt[kMaxClasses];
   const BatchView b = load_batch(blob);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < kMaxClasses) { hist[tid] = 0; run[tid] = 0; }
-  __syncthreads();
-  for (int i = tid; i < b.N; i += blockDim.x) {
-    const int d = b.rowptr[i + 1] - b.rowptr[i];
-    if (d == 0) {
-      amp[i] = 1.0f;
-      att[i] = 1.0f;
-    } else {
-      const double ld = log((double)d + 1.0);
-      amp[i] = (float)(ld / delta);
-      att[i] = (float)(delta / ld);
+  if (cmax <= 0) {  // scalers only (no class GEMMs)
+    for (int i = tid; i < b.N; i += blockDim.x) {
+      const int d = b.rowptr[i + 1] - b.rowptr[i];
+      if (d == 0) {
+        amp[i] = 1.0f;
+        att[i] = 1.0f;
+      } else {
+        const double ld = log((double)d + 1.0);
+        amp[i] = (float)(ld / delta);
+        att[i] = (float)(delta / ld);
+      }
     }
-    if (cmax > 0) atomicAdd(&hist[min(d, cmax - 1)], 1);  // integer counts: order-independent
+    return;
   }
-  if (cmax <= 0) return;
+  // per-degree scalers once (d < cmax = max_degree + 1), in the same fp64 arithmetic
+  if (tid < cmax) {
+    if (tid == 0) {
+      tamp[0] = 1.0f;
+      tatt[0] = 1.0f;
+    } else {
+      const double ld = log((double)tid + 1.0);
+      tamp[tid] = (float)(ld / delta);
+      tatt[tid] = (float)(delta / ld);
+    }
+  }
+  for (int e = tid; e < 32 * kMaxClasses; e += blockDim.x) wcnt[e / kMaxClasses][e % kMaxClasses] = 0;
   __syncthreads();
+  // stable counting sort: warp w owns the contiguous node range [w*per, (w+1)*per), in
+  // rounds of 32 nodes; ranks inside a round come from __match_any_sync
+  const int per = (b.N + 31) / 32;
+  const int w0 = warp * per, w1 = min(b.N, w0 + per);
+  for (int base = w0; base < w1; base += 32) {
+    const int i = base + lane;
+    const int d = i < w1 ? min(b.rowptr[i + 1] - b.rowptr[i], cmax - 1) : -1;
+    if (i < w1) {
+      amp[i] = tamp[d];
+      att[i] = tatt[d];
+    }
+    const unsigned mask = __match_any_sync(0xffffffffu, d);
+    const int rank = __popc(mask & ((1u << lane) - 1u));
+    if (d >= 0 && rank == 0) wcnt[warp][d] += __popc(mask);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (tid < cmax) {  // class totals and, per class, exclusive scan over warps in warp order
+    int acc = 0;
+    for (int w = 0; w < 32; ++w) {
+      const int c = wcnt[w][tid];
+      wcnt[w][tid] = acc;
+      acc += c;
+    }
+    hist[tid] = acc;
+  }
+  __syncthreads();
+  if (tid < cmax) {
+    info->amp[tid] = tamp[tid];  // per degree slot
+    info->att[tid] = tatt[tid];
+  }
   if (tid == 0) {
     int off = 0, C = 0, T = 0, S = 0;
     for (int d = 0; d < cmax; ++d) {
       bstart[d] = off;
-      cls_of[d] = -1;
       if (hist[d] > 0) {
-        cls_of[d] = C;
         info->deg[C] = d;
         info->start[C] = off;
         info->count[C] = hist[d];
-        float a = 1.0f, t = 1.0f;
-        if (d > 0) {
-          const double ld = log((double)d + 1.0);
-          a = (float)(ld / delta);
-          t = (float)(delta / ld);
-        }
-        info->amp[C] = a;
-        info->att[C] = t;
-        for (int r = 0; r < hist[d]; r += TC_BM) tiles[T++] = make_int4(C, off + r, min(TC_BM, hist[d] - r), 0);
-        for (int r = 0; r < hist[d]; r += ks) splits[S++] = make_int4(C, off + r, min(ks, hist[d] - r), 0);
+        // tiles and splits carry the degree slot d: weights and scalers are indexed by d
+        for (int r = 0; r < hist[d]; r += TC_BM) tiles[T++] = make_int4(d, off + r, min(TC_BM, hist[d] - r), 0);
+        for (int r = 0; r < hist[d]; r += ks) splits[S++] = make_int4(d, off + r, min(ks, hist[d] - r), 0);
         ++C;
       }
       off += hist[d];
@@ -532,221 +566,28 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
     info->S = S;
   }
   __syncthreads();
-  // stable scatter, 1024 nodes per round: rank inside the warp by __match_any,
-  // across warps by a per-bin prefix over warp counts
-  for (int base = 0; base < b.N; base += blockDim.x) {
-    for (int e = tid; e < 32 * kMaxClasses; e += blockDim.x) wcnt[e / kMaxClasses][e % kMaxClasses] = 0;
-    __syncthreads();
-    const int i = base + tid;
-    const int d = i < b.N ? min(b.rowptr[i + 1] - b.rowptr[i], cmax - 1) : -1;
+  // scatter: same rounds again, positions = class start + warp base + running rank
+  for (int base = w0; base < w1; base += 32) {
+    const int i = base + lane;
+    const int d = i < w1 ? min(b.rowptr[i + 1] - b.rowptr[i], cmax - 1) : -1;
     const unsigned mask = __match_any_sync(0xffffffffu, d);
     const int rank = __popc(mask & ((1u << lane) - 1u));
-    if (d >= 0 && rank == 0) wcnt[warp][d] = __popc(mask);
-    __syncthreads();
-    if (tid < cmax) {
-      int acc = run[tid];
-      for (int w = 0; w < 32; ++w) {
-        const int c = wcnt[w][tid];
-        wcnt[w][tid] = acc;
-        acc += c;
-      }
-      run[tid] = acc;
-    }
-    __syncthreads();
     if (d >= 0) {
       const int r = bstart[d] + wcnt[warp][d] + rank;
       perm[r] = i;
       if (pos) pos[i] = r;
     }
-    __syncthreads();
+    __syncwarp();
+    if (d >= 0 && rank == 0) wcnt[warp][d] += __popc(mask);
+    __syncwarp();
   }
 }
 
-// Wf[c][h][k] = W_d[h][k] and WbT[c][k][h] = W_d[h][k] for every class c present,
-// for all layers (32x32 tiles; the transposed copy goes through shared memory)
-__global__ void k_prep_W(const float *__restrict__ params, const int64_t *__restrict__ u_off, int L, int H, int cmax,
-                         const DegInfo *__restrict__ info, float *__restrict__ Wf, float *__restrict__ WbT) {
-  pdl_enter();
-  __shared__ float tile[32][33];
-  const int K = 4 * H, tk = K / 32, th = H / 32;
-  const int per_cls = tk * th;
-  const int C = info->C;
-  for (int t = blockIdx.x; t < L * cmax * per_cls; t += gridDim.x) {
-    const int l = t / (cmax * per_cls);
-    const int c = (t / per_cls) % cmax;
-    if (c >= C) continue;  // uniform per block
-    const int tt = t % per_cls, h0 = (tt / tk) * 32, k0 = (tt % tk) * 32;
-    const float *U = params + u_off[l];
-    const float a = info->amp[c], b = info->att[c];
-    float *wf = Wf + ((size_t)l * cmax + c) * H * K;
-    float *wb = WbT + ((size_t)l * cmax + c) * H * K;
-    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-      const float *u = U + (size_t)(h0 + r) * 3 * K + k0 + threadIdx.x;
-      const float w = u[0] + a * u[K] + b * u[2 * K];
-      wf[(size_t)(h0 + r) * K + k0 + threadIdx.x] = w;
-      tile[r][threadIdx.x] = w;
-    }
-    __syncthreads();
-    for (int r = threadIdx.y; r < 32; r += blockDim.y)
-      wb[(size_t)(k0 + r) * H + h0 + threadIdx.x] = tile[threadIdx.x][r];
-    __syncthreads();
-  }
-}
 
-// ---------------------------------------------------------------- G1 update, class tiles
-struct TcUpdC {
-  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
-  static constexpr bool A_MN = false, B_MN = false;
-  static constexpr bool COLSUM = false;
-  const float *A; const int *perm; const DegInfo *info; const int4 *tiles; const float *Wf; const float *bU;
-  float *X1; int H; int cmax; int row_end; const float *W;
-  __device__ void prepare() {}
-  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) {
-    const int nt = H / BN, ti = t / nt;
-    if (ti >= info->T) return false;
-    const int4 tl = tiles[ti];
-    m0 = tl.y;
-    row_end = tl.y + tl.z;
-    n0 = (t % nt) * BN;
-    W = Wf + (size_t)tl.x * H * 4 * H;
-    kb = 0;
-    ke = 4 * H;
-    return true;
-  }
-  __device__ const float *any_src() const { return bU; }
-  __device__ const float *a_src(int m, int k, int) const {
-    return m < row_end ? A + (size_t)perm[m] * 4 * H + k : nullptr;
-  }
-  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
-  __device__ const float *b_src(int n0, int r, int k, int) const { return W + (size_t)(n0 + r) * 4 * H + k; }
-  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
-  __device__ void store(int m, int n0, int q0, const float (&acc)[1][32]) const {
-    if (m >= row_end) return;
-    float *out = X1 + (size_t)perm[m] * H + n0 + q0;
-    const float *b = bU + n0 + q0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4 *>(out + i) =
-          make_float4(fmaxf(acc[0][i] + b[i], 0.f), fmaxf(acc[0][i + 1] + b[i + 1], 0.f),
-                      fmaxf(acc[0][i + 2] + b[i + 2], 0.f), fmaxf(acc[0][i + 3] + b[i + 3], 0.f));
-  }
-};
 
-// ---------------------------------------------------------------- G2 dA, class tiles
-struct TcDAC {
-  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
-  static constexpr bool A_MN = false, B_MN = false;
-  static constexpr bool COLSUM = false;
-  const float *dZ; const int *perm; const DegInfo *info; const int4 *tiles; const float *WbT; float *dA; int H;
-  int row_end; const float *W;
-  __device__ void prepare() {}
-  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) {
-    const int nt = 4 * H / BN, ti = t / nt;
-    if (ti >= info->T) return false;
-    const int4 tl = tiles[ti];
-    m0 = tl.y;
-    row_end = tl.y + tl.z;
-    n0 = (t % nt) * BN;
-    W = WbT + (size_t)tl.x * H * 4 * H;
-    kb = 0;
-    ke = H;
-    return true;
-  }
-  __device__ const float *any_src() const { return dZ; }
-  __device__ const float *a_src(int m, int k, int) const { return m < row_end ? dZ + (size_t)perm[m] * H + k : nullptr; }
-  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
-  __device__ const float *b_src(int n0, int r, int k, int) const { return W + (size_t)(n0 + r) * H + k; }
-  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
-  __device__ void store(int m, int n0, int q0, const float (&acc)[1][32]) const {
-    if (m >= row_end) return;
-    float *out = dA + (size_t)perm[m] * 4 * H + n0 + q0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[0][i], acc[0][i + 1], acc[0][i + 2], acc[0][i + 3]);
-  }
-};
 
-// ---------------------------------------------------------------- G3 per-class Gram partials
-// part[sp][h][n] = sum_{k in split sp} dZ[perm[k], h] A[perm[k], n]
-struct TcGramC {
-  static constexpr int BN = 64, NACC = 1, NMMA = 64, STAGES = 3, RAW = 3;
-  static constexpr bool A_MN = true, B_MN = true;
-  static constexpr bool COLSUM = true;
-  const float *dZ; const float *A; const int *perm; const DegInfo *info; const int4 *splits; float *part; int H;
-  int smax; float *cs_part; int sp; int s0;
-  __device__ void colsum(int m, int n0, float v) const {
-    if (n0 == 0) cs_part[(size_t)sp * H + m] = v;
-  }
-  __device__ void prepare() {}
-  __device__ bool tile(int t, int &m0, int &n0, int &kb, int &ke) {
-    const int nt = 4 * H / BN, mt = H / TC_BM;
-    sp = t % smax;
-    const int t2 = t / smax;
-    if (sp >= info->S) return false;
-    n0 = (t2 % nt) * BN;
-    m0 = (t2 / nt) * TC_BM;
-    if (m0 >= mt * TC_BM) return false;
-    const int4 s = splits[sp];
-    s0 = s.y;
-    kb = 0;
-    ke = s.z;
-    return true;
-  }
-  __device__ const float *any_src() const { return dZ; }
-  __device__ const float *a_src(int m, int k, int ke) const {
-    return k < ke ? dZ + (size_t)(perm ? perm[s0 + k] : s0 + k) * H + m : nullptr;  // perm null: rows pre-sorted
-  }
-  __device__ float4 a_fix(float4 v, int, int, int) const { return v; }
-  __device__ const float *b_src(int n0, int r, int k, int ke) const {
-    return k < ke ? A + (size_t)(perm ? perm[s0 + k] : s0 + k) * 4 * H + n0 + r : nullptr;
-  }
-  __device__ float4 b_fix(float4 v, int, int, int, int) const { return v; }
-  __device__ void store(int m, int n0, int q0, const float (&acc)[1][32]) const {
-    float *out = part + (size_t)sp * H * 4 * H + (size_t)m * 4 * H + n0 + q0;
-#pragma unroll
-    for (int i = 0; i < 32; i += 4)
-      *reinterpret_cast<float4 *>(out + i) = make_float4(acc[0][i], acc[0][i + 1], acc[0][i + 2], acc[0][i + 3]);
-  }
-};
 
-// db_U[h] = sum over the S (device-side) class splits of the fused column sums,
-// one warp per output, fixed xor-shuffle order
-__global__ void k_reduce_splits_rows(const float *__restrict__ cs, const DegInfo *__restrict__ info, int H,
-                                     float *__restrict__ out) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-  const int S = info->S;
-  for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < H; e += gridDim.x * wpb) {
-    float s = 0.f;
-    for (int p = lane; p < S; p += 32) s += cs[(size_t)p * H + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[e] = s;
-  }
-}
 
-// dU[h][s*4H + n] = sum_sp s(class(sp)) part[sp][h][n], fixed split order
-__global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInfo *__restrict__ info,
-                                    const int4 *__restrict__ splits, int H, float *__restrict__ dU) {
-  pdl_enter();
-  const int S = info->S;
-  const int K = 4 * H, total = H * K;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-    for (int sp = 0; sp < S; ++sp) {
-      const int c = splits[sp].x;
-      const float v = part[(size_t)sp * total + e];
-      s0 += v;
-      s1 = fmaf(info->amp[c], v, s1);
-      s2 = fmaf(info->att[c], v, s2);
-    }
-    const int h = e / K, n = e - h * K;
-    float *row = dU + (size_t)h * 3 * K;
-    row[n] = s0;
-    row[K + n] = s1;
-    row[2 * K + n] = s2;
-  }
-}
 
 // ---------------------------------------------------------------- K1 projection (F % 4 == 0)
 // P[N, H] = X[N, F] M_x^T : A = X rows (K = F), B = M_x rows
@@ -976,41 +817,10 @@ void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax
   g_launches += 1;
 }
 
-void launch_prep_W(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L, int cmax,
-                   const DegInfo *info, float *Wf, float *WbT) {
-  const int blocks = std::min(L * cmax * (4 * c.H / 32) * (c.H / 32), kSMs * 8);
-  launch_ex(k_prep_W, blocks, dim3(32, 8), 0, st, params, u_off_dev, L, c.H, cmax, info, Wf, WbT);
-  g_launches += 1;
-}
 
-void launch_tc_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm,
-                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *bU, float *X1) {
-  TcUpdC op{A, perm, info, tiles, Wf, bU, X1, c.H, cmax, 0, nullptr};
-  run_tc(st, op, tc_max_tiles(c, cmax) * (c.H / TcUpdC::BN));
-}
 
-void launch_tc_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const int *perm, const DegInfo *info,
-                      const int4 *tiles, const float *WbT, float *dA) {
-  TcDAC op{dZ, perm, info, tiles, WbT, dA, c.H, 0, nullptr};
-  run_tc(st, op, tc_max_tiles(c, cmax) * (4 * c.H / TcDAC::BN));
-}
 
-size_t tc_gram_partial_floats(const Caps &c, int cmax) {
-  return (size_t)tc_max_splits(c, cmax) * (c.H * 4 * c.H + c.H);
-}
 
-void launch_tc_dU_cls(cudaStream_t st, const Caps &c, int cmax, const uint8_t *blob, const float *dZ, const float *A,
-                      const int *perm, const DegInfo *info, const int4 *splits, float *partial, float *dU,
-                      float *dbU) {
-  const int smax = tc_max_splits(c, cmax);
-  const int total = c.H * 4 * c.H;
-  float *cs = partial + (size_t)smax * total;  // per-split column sums of dZ (db_U)
-  TcGramC op{dZ, A, perm, info, splits, partial, c.H, smax, cs, 0, 0};
-  run_tc(st, op, (c.H / TC_BM) * (4 * c.H / TcGramC::BN) * smax);
-  launch_ex(k_reduce_dU_classes, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, info, splits, c.H, dU);
-  launch_ex(k_reduce_splits_rows, cdiv(c.H, 8), 256, 0, st, cs, info, c.H, dbU);
-  g_launches += 2;
-}
 
 cudaError_t tc_configure() {
   cudaError_t e;
@@ -1019,9 +829,6 @@ cudaError_t tc_configure() {
   if ((e = configure_tc<TcProj>()) != cudaSuccess) return e;
   if ((e = configure_tc<TcDX>()) != cudaSuccess) return e;
   if ((e = configure_tc<TcDMx>()) != cudaSuccess) return e;
-  if ((e = configure_tc<TcUpdC>()) != cudaSuccess) return e;
-  if ((e = configure_tc<TcDAC>()) != cudaSuccess) return e;
-  if ((e = configure_tc<TcGramC>()) != cudaSuccess) return e;
   return configure_tc<TcDU>();
 }
 

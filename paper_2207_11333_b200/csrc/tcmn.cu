@@ -372,10 +372,6 @@ __global__ void __launch_bounds__(256) k_reduce_gram(const float *__restrict__ p
 }
 
 // reductions (tcgemm.cu / kernels.cu)
-__global__ void k_reduce_dU_classes(const float *__restrict__ part, const DegInfo *__restrict__ info,
-                                    const int4 *__restrict__ splits, int H, float *__restrict__ dU);
-__global__ void k_reduce_splits_rows(const float *__restrict__ cs, const DegInfo *__restrict__ info, int H,
-                                     float *__restrict__ out);
 __global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
 __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
 
