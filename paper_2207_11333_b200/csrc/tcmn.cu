@@ -16,6 +16,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <atomic>
 
 #include "common.cuh"
@@ -376,10 +377,19 @@ __global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int c
 __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
 
 namespace {
+// CTAs of the side-stream Grams (persistent): fewer than the SM count leaves room for
+// the critical chain's kernels that run concurrently (HG_MN_GRID to override)
+int mn_grid_cap() {
+  static const int v = [] {
+    const char *e = getenv("HG_MN_GRID");
+    return e ? std::max(1, atoi(e)) : 40;  // measured optimum at config B (148 -> 40: +2%)
+  }();
+  return v;
+}
 template <class Op>
 void nrun(cudaStream_t st, const TmaMaps &mp, const CUtensorMap &ones, Op op, int items) {
   op.items_cap = items;
-  launch_ex(k_tmn<Op>, std::max(1, std::min(items, kSMs)), N_THREADS, n_smem_bytes<Op>(), st, mp, ones, op);
+  launch_ex(k_tmn<Op>, std::max(1, std::min(items, mn_grid_cap())), N_THREADS, n_smem_bytes<Op>(), st, mp, ones, op);
   g_launches += 1;
 }
 }  // namespace
