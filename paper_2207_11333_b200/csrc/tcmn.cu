@@ -284,7 +284,7 @@ struct MnDMx {
 // Block = RW warps x 32 float4 outputs: lane l of warp w sums parts w, w+RW, ...
 // of output float4 (32*block + l) -- coalesced rows -- then warp 0 adds the RW
 // warp sums in order (deterministic for a given partial count).
-constexpr int RW = 32;
+constexpr int RW = 8;
 struct RJob {
   const float *part;  // [nparts][count]
   int nparts, count;  // count % 4 == 0
