@@ -249,6 +249,8 @@ void phase(Prof *pr, int ph, F &&fn) {
 
 hg_status enqueue_bucket(hg_ctx *x, cudaStream_t st, int b);
 std::pair<int64_t, int64_t> bucket_range(hg_ctx *x, int b);
+int bucket_count(const hg_ctx *x);
+int bucket_closed_by(const hg_ctx *x, int l);
 
 // ---- the step's kernel sequence (enqueue only) ----
 void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool fuse_head_bwd = false) {
@@ -354,7 +356,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
 }
 
 void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false,
-                      bool overlap_allreduce = false, const hg_adamw *fuse_adamw = nullptr) {
+                      bool overlap_allreduce = false) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
@@ -381,27 +383,6 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
                         x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
     g_low_prio = false;
   });
-  if (overlap_allreduce) enqueue_bucket(x, side, 0);
-  // Fused optimizer: AdamW of each gradient bucket as soon as the bucket is final
-  // (allreduced when W > 1) and nothing later in this step reads its parameters,
-  // all on one stream in bucket order (the last launch advances the step counter).
-  const bool fused = fuse_adamw && fork;
-  cudaStream_t ast = (x->world > 1 && x->comm) ? x->comm_stream : side2;
-  auto adamw_bucket = [&](int bk) {
-    auto r = bucket_range(x, bk);
-    launch_adamw(ast, x->f(p.params) + r.first, x->f(p.grads) + r.first, x->f(p.m) + r.first, x->f(p.v) + r.first,
-                 r.second - r.first, reinterpret_cast<AdamDev *>(x->b(p.adam)), fuse_adamw->lr, fuse_adamw->beta1,
-                 fuse_adamw->beta2, fuse_adamw->eps, fuse_adamw->weight_decay, bk == c.layers);
-  };
-  if (fused) {
-    if (ast == side2) {
-      rec(x->ev_hgrad, side);
-      wait(side2, x->ev_hgrad);
-    }
-    g_low_prio = true;
-    adamw_bucket(0);
-    g_low_prio = false;
-  }
   const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
   const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
   if (x->use_tc && !cls)
@@ -472,13 +453,12 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         launch_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
     });
     g_low_prio = false;
-    if (overlap_allreduce) {  // conv l gradients complete
+    const int bk = bucket_closed_by(x, l);
+    if (overlap_allreduce && bk >= 0) {  // conv l's gradients complete: its bucket may go
       wait(side2, x->ev_gram[l]);
-      enqueue_bucket(x, side2, c.layers - l);
-    } else if (fused) {
-      wait(side2, x->ev_gram[l]);
+      enqueue_bucket(x, side2, bk);
     }
-    if (!fused) rec(x->ev_side[l], side2);
+    rec(x->ev_side[l], side2);
     // ---- main: dX into dZ[l-1]
     if (l > 0) {
       float *dZn = x->f(p.dZ[l - 1]), *dZnl = cls ? x->f(p.dZ_lo[l - 1]) : nullptr;
@@ -492,14 +472,6 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
           launch_dX(st, x->caps, blob, dP, x->param(lname(l, "M_x")), F, Xl, dZn);
       });
     }
-    if (fused) {  // layer l's parameters are no longer read by this step (dX_l was the last reader)
-      rec(x->ev_dx[l], st);
-      wait(ast, x->ev_dx[l]);
-      g_low_prio = true;
-      adamw_bucket(c.layers - l);
-      g_low_prio = false;
-      rec(x->ev_side[l], ast);
-    }
   }
   wait(st, x->ev_gram[0]);  // join: every gradient is complete on the main stream
   wait(st, x->ev_side[0]);
@@ -507,6 +479,48 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
 
 // gradient buckets in backward order: head first, then conv L-1 ... conv 0 (each a
 // contiguous range of the flat gradient arena)
+// Gradient buckets in backward order. Bucket 0 holds the head and the first
+// groups[0] conv layers (L-1, L-2, ...), bucket k the next groups[k] layers; a
+// bucket is allreduced on the comm stream once its lowest layer's gradients are
+// final. Default: layer pairs, the last two layers alone (HG_BUCKETS=a,b,... layer
+// counts per bucket overrides).
+std::vector<int> bucket_groups(const hg_ctx *x) {
+  const int L = x->cfg.layers;
+  std::vector<int> g;
+  if (const char *e = getenv("HG_BUCKETS")) {
+    int tot = 0;
+    for (const char *p = e; *p;) {
+      const int v = atoi(p);
+      if (v > 0 && tot + v <= L) {
+        g.push_back(v);
+        tot += v;
+      }
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+    if (tot < L) g.push_back(L - tot);
+  } else {  // pairs of layers, the last two alone (measured best at 2 GPUs, config B)
+    int rest = L;
+    while (rest > 2) {
+      const int v = std::min(2, rest - 2);
+      g.push_back(v);
+      rest -= v;
+    }
+    while (rest-- > 0) g.push_back(1);
+  }
+  return g;
+}
+int bucket_count(const hg_ctx *x) { return (int)bucket_groups(x).size(); }
+// bucket that completes when layer l's gradients are final, or -1
+int bucket_closed_by(const hg_ctx *x, int l) {
+  const auto g = bucket_groups(x);
+  int top = x->cfg.layers;  // layers [top - g[k], top) belong to bucket k
+  for (int k = 0; k < (int)g.size(); ++k) {
+    top -= g[k];
+    if (l == top) return k;
+  }
+  return -1;
+}
 std::pair<int64_t, int64_t> bucket_range(hg_ctx *x, int b) {
   const int L = x->cfg.layers;
   auto off = [&](const std::string &name) {
@@ -514,10 +528,12 @@ std::pair<int64_t, int64_t> bucket_range(hg_ctx *x, int b) {
       if (t.name == name) return t.offset;
     return (int64_t)-1;
   };
-  if (b == 0) return {off("head.W1"), x->n_params};
-  const int l = L - b;
-  const int64_t beg = off(lname(l, "M_x"));
-  const int64_t end = l + 1 < L ? off(lname(l + 1, "M_x")) : off("head.W1");
+  const auto g = bucket_groups(x);
+  int top = L;
+  for (int k = 0; k < b; ++k) top -= g[k];
+  const int lo = top - g[b];
+  const int64_t beg = off(lname(lo, "M_x"));
+  const int64_t end = b == 0 ? x->n_params : off(lname(top, "M_x"));
   return {beg, end};
 }
 
@@ -977,7 +993,7 @@ hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world
   ncclResult_t r = ncclCommInitRank(&x->comm, world, id, rank);
   if (r != ncclSuccess) return nccl_fail(x, r, "ncclCommInitRank");
   CK(x, cudaStreamCreateWithFlags(&x->comm_stream, cudaStreamNonBlocking));
-  for (int b = 0; b <= x->cfg.layers; ++b) {
+  for (int b = 0; b < bucket_count(x); ++b) {
     cudaEvent_t ev;
     CK(x, cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     x->bucket_ready.push_back(ev);
@@ -1041,14 +1057,9 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->cap_stream, slot, nullptr, true);
-  // bucketed, overlapped allreduce and (HG_FUSE_ADAMW=1) per-bucket AdamW inside the backward
-  static const bool fuse = [] {
-    const char *v = getenv("HG_FUSE_ADAMW");
-    return v && atoi(v) != 0;
-  }();
-  enqueue_backward(x, x->cap_stream, slot, nullptr, true, true, fuse ? h : nullptr);
+  enqueue_backward(x, x->cap_stream, slot, nullptr, true, true);  // bucketed, overlapped allreduce
   hg_status ar = join_buckets(x, x->cap_stream);
-  if (!fuse) enqueue_step(x, x->cap_stream, *h);
+  enqueue_step(x, x->cap_stream, *h);
   const int64_t nk = launches_so_far() - l0;
   cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
   if (ar) {

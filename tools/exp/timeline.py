@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--graphs", type=int, default=20000)
 ap.add_argument("--B", type=int, default=128)
 ap.add_argument("--json", default="gpurun_out/timeline_trace.json")
+ap.add_argument("--nosync", action="store_true", help="launch the profiled steps back to back")
 args = ap.parse_args()
 
 d = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
@@ -32,11 +33,17 @@ B, H, L = args.B, 128, 6
 cfg = hgnn.make_config(data["f_node"], 4, H, L, B, B * st["max_nodes_per_graph"],
                        B * int(np.diff(np.asarray(data["edge_offset"])).max()), store.degree_stat(), n_slots=1,
                        max_degree=st["max_degree"])
-ctx = hgnn.Context(cfg, device=0)
+rank = int(os.environ.get("RANK", "0"))
+world = int(os.environ.get("WORLD_SIZE", "1"))
+torch.cuda.set_device(rank)
+if world > 1:
+    import torch.distributed as dist
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{rank}"))
+ctx = hgnn.Context(cfg, device=rank)
 ctx.params_init(1234)
-ctx.comm_init(0, 1)
+ctx.comm_init(rank, world)
 hyper = dict(hgnn.DEFAULT_ADAMW)
-ids = hgnn.hg_shard(13, 0, 0, 1, args.graphs)[:B]
+ids = hgnn.hg_shard(13, 0, rank, world, args.graphs)[:B]
 ctx.upload(hgnn.hg_pack_host(store, ids, cfg), 0)
 ctx.capture_step(0, **hyper)
 for _ in range(10):
@@ -44,26 +51,31 @@ for _ in range(10):
 torch.cuda.synchronize()
 from torch.profiler import ProfilerActivity, profile  # noqa: E402
 
+if world > 1:
+    dist.barrier()
 with profile(activities=[ProfilerActivity.CUDA]) as prof:
     for _ in range(3):
         ctx.train_step(0, graph=True, **hyper)
-        torch.cuda.synchronize()
+        if not args.nosync:
+            torch.cuda.synchronize()
+    torch.cuda.synchronize()
+if rank != 0:
+    sys.exit(0)
 os.makedirs(os.path.dirname(args.json) or ".", exist_ok=True)
 prof.export_chrome_trace(args.json)
 ev = json.load(open(args.json))["traceEvents"]
 k = [e for e in ev if e.get("cat") == "kernel"]
 k.sort(key=lambda e: e["ts"])
-# split into steps at gaps > 20 us
-steps, cur = [], [k[0]]
-for e in k[1:]:
-    prev_end = max(x["ts"] + x["dur"] for x in cur)
-    if e["ts"] - prev_end > 20:
+# split into steps at the optimizer kernel (last kernel of a step)
+steps, cur = [], []
+for e in k:
+    cur.append(e)
+    if "adamw" in e["name"]:
         steps.append(cur)
-        cur = [e]
-    else:
-        cur.append(e)
-steps.append(cur)
-s = steps[-1]
+        cur = []
+if cur:
+    steps.append(cur)
+s = steps[-1] if len(steps[-1]) > 10 else steps[-2]
 t0 = s[0]["ts"]
 t1 = max(e["ts"] + e["dur"] for e in s)
 print(f"{len(steps)} steps profiled; last step: {len(s)} kernels, span {t1 - t0:.1f} us")
