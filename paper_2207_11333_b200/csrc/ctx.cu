@@ -38,7 +38,7 @@ struct Plan {
   int cmax = 0;  // degree-class slots (0 = class GEMMs off)
   size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
   // direct-GEMM residuals x - trunc19(x) (class path): operands and weights
-  size_t Wf_lo = 0, WbT_lo = 0, ones = 0;
+  size_t Wf_lo = 0, WbT_lo = 0, ones = 0, xpad = 0, xpad_lo = 0;
   std::vector<size_t> A_lo, X_lo;  // per layer (the backward Grams read them)
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t total = 0;
@@ -108,6 +108,10 @@ Plan make_plan(const hg_config &c) {
       p.X_lo.push_back(take(sizeof(float) * N * H));
     }
     p.ones = take(sizeof(float) * N * 32);  // B operand of the column-sum tiles
+    if (pad_x0_width(c.f_node) <= 256) {      // layer-0 features for the TMA dM_x Gram
+      p.xpad = take(sizeof(float) * N * pad_x0_width(c.f_node));
+      p.xpad_lo = take(sizeof(float) * N * pad_x0_width(c.f_node));
+    }
     for (int l = 0; l < c.layers; ++l) {
       p.dZ_lo.push_back(take(sizeof(float) * N * H));
       p.dPl_lo.push_back(take(sizeof(float) * N * H));
@@ -294,6 +298,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
       if (c.layers > 1)
         launch_prep_W2(wst, x->caps, x->f(p.params), uo, 1, c.layers, p.cmax, c.delta, x->f(p.Wf), x->f(p.Wf_lo),
                        x->f(p.WbT), x->f(p.WbT_lo));
+      if (p.xpad) launch_pad_x0(wst, x->caps, blob, x->f(p.xpad), x->f(p.xpad_lo));
       if (fork) cudaEventRecord(x->ev_prepw, wst);
       g_low_prio = false;
     });
@@ -431,7 +436,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, cls && l > 0 ? dPlo : nullptr, pos);
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, cls ? dPlo : nullptr, pos);
     });
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
@@ -440,14 +445,12 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     wait(side2, x->ev_dp[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
-      if (cls && l > 0) {  // the MN-major Gram also reduces dM_e
-        launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xl, x->f(p.X_lo[l - 1]), F, x->f(p.ones), part_dMx,
-                      x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")), pagg, agg_bwd_partials(x->caps),
-                      x->grad(lname(l, "M_e")));
-        return;
-      }
       launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
-      if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
+      if (cls && (l > 0 || p.xpad)) {  // MN-major TMA Gram (layer 0: padded node features)
+        const float *Xg = l > 0 ? Xl : x->f(p.xpad), *Xg_lo = l > 0 ? x->f(p.X_lo[l - 1]) : x->f(p.xpad_lo);
+        launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xg, Xg_lo, F, l > 0 ? F : pad_x0_width(c.f_node),
+                      x->f(p.ones), part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+      } else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
         launch_tc_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else
         launch_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
@@ -835,6 +838,10 @@ hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_
     case 9: *offset = p.grads; *bytes = 4 * x->n_params; break;
     case 10: *offset = p.amp; *bytes = 4 * N; break;
     case 11: *offset = p.att; *bytes = 4 * N; break;
+    // (debug views, not in the header: per-layer dP, dP_lo; padded layer-0 features)
+    case 100: if (layer < 0 || layer >= c.layers) return fail(HG_E_RANGE, "layer"); *offset = p.dPl[layer]; *bytes = 4 * N * H; break;
+    case 101: if (layer < 0 || layer >= c.layers || p.dPl_lo.empty()) return fail(HG_E_RANGE, "layer"); *offset = p.dPl_lo[layer]; *bytes = 4 * N * H; break;
+    case 102: if (!p.xpad) return fail(HG_E_RANGE, "no xpad"); *offset = p.xpad; *bytes = 4 * N * pad_x0_width(c.f_node); break;
     default: return fail(HG_E_RANGE, "unknown view %d", what);
   }
   return HG_OK;

@@ -129,10 +129,13 @@ size_t mn_dmx_partial_floats(const Caps &c, int F);
 void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const float *A,
                       const float *A_lo, const float *ones, const DegInfo *info, const int4 *splits, float *partial,
                       float *dU, float *dbU);
-// (also reduces the aggregation backward's dM_e block partials pagg[nagg][H*Fe] into dMe when pagg != null)
+// X: [maxN][Fp] (Fp >= F, 16-byte row pitch; Fp = F for hidden layers), F output columns
 void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
-                   const float *X, const float *X_lo, int F, const float *ones, float *partial, float *dMx,
-                   float *dbM, const float *pagg = nullptr, int nagg = 0, float *dMe = nullptr);
+                   const float *X, const float *X_lo, int F, int Fp, const float *ones, float *partial, float *dMx,
+                   float *dbM);
+// layer-0 node features padded to pad_x0_width(F0) columns (+ tf32 residual) for the TMA path
+int pad_x0_width(int F0);
+void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo);
 int agg_bwd_partials(const Caps &c);  // number of dM_e block partials launch_agg_bwd writes
 
 // tcgen05 3xTF32 GEMMs (tcgemm.cu); require H % 128 == 0

@@ -202,15 +202,20 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
       tc::mbar_wait(&accf[buf], (tcount >> 1) & 1);
       tc::fence_after_sync();
       const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * BN);
+      const bool empty_item = w.len <= 0;  // no MMA ran: the partial is zero
       if (w.cs) {  // column sums: every column of the N=32 tile holds the same value
         float acc[32];
         tc::tmem_ld32(trow, acc);
-        op.emit_cs(w, w.m0 + warp * 32 + lane, acc[0]);
+        op.emit_cs(w, w.m0 + warp * 32 + lane, empty_item ? 0.f : acc[0]);
       } else {
 #pragma unroll 1
         for (int q = 0; q < BN / 32; ++q) {
           float acc[32];
           tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
+          if (empty_item) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) acc[i] = 0.f;
+          }
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             *reinterpret_cast<float4 *>(stg + lane * N_STG_LD + 4 * j) =
@@ -265,20 +270,45 @@ struct MnDMx {
   static constexpr int BN = 128;
   const uint8_t *blob; float *part, *cs; int H, F; int items_cap;
   __device__ bool item(int t, MnItem &w) const {
-    const int NT = F / BN + 1, MT = H / N_BM;
+    const int NT = (F + BN - 1) / BN + 1, MT = H / N_BM;
     const int nt = t % NT, mt = (t / NT) % MT, sp = t / (NT * MT);
     const int N = batch_N(blob);
     int kc = (N + kMnDMxSplits - 1) / kMnDMxSplits;
     kc = (kc + N_BK - 1) / N_BK * N_BK;
-    const int k0 = sp * kc, len = min(N - k0, kc);
+    const int k0 = sp * kc, len = max(0, min(N - k0, kc));
     w = MnItem{mt * N_BM, nt * BN, k0, len, sp, nt == NT - 1};
-    return sp < kMnDMxSplits && len > 0;
+    // every split is an item, also an empty one (len 0: its partial is written as zeros),
+    // because the fixed-order reduction sums all kMnDMxSplits partials
+    return sp < kMnDMxSplits;
   }
   __device__ void emit(const MnItem &w, int m, int n, float4 v) const {
-    *reinterpret_cast<float4 *>(part + ((size_t)w.sp * H + m) * F + n) = v;
+    float *o = part + ((size_t)w.sp * H + m) * F + n;
+    if ((F & 3) == 0) {
+      if (n < F) *reinterpret_cast<float4 *>(o) = v;
+    } else {  // narrow layer input (F % 4 != 0): scalar stores, columns >= F dropped
+      if (n < F) o[0] = v.x;
+      if (n + 1 < F) o[1] = v.y;
+      if (n + 2 < F) o[2] = v.z;
+      if (n + 3 < F) o[3] = v.w;
+    }
   }
   __device__ void emit_cs(const MnItem &w, int m, float v) const { cs[(size_t)w.sp * H + m] = v; }
 };
+
+// layer-0 input as a TMA-readable operand: Xp[i][0..Fp) = x_i padded with zeros to a
+// 16-byte row pitch, and its tf32 residual
+__global__ void __launch_bounds__(256) k_pad_x0(const uint8_t *__restrict__ blob, int Fp, float *__restrict__ Xp,
+                                                float *__restrict__ Xp_lo) {
+  pdl_enter();
+  const BatchView b = load_batch(blob);
+  const int F = b.F0;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < b.N * Fp; e += gridDim.x * blockDim.x) {
+    const int i = e / Fp, f = e - i * Fp;
+    const float v = f < F ? b.x[(size_t)i * F + f] : 0.f;
+    Xp[e] = v;
+    Xp_lo[e] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  }
+}
 
 // ---------------------------------------------------------------- reductions
 // Block = RW warps x 32 float4 outputs: lane l of warp w sums parts w, w+RW, ...
@@ -423,19 +453,24 @@ void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ,
 }
 
 void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
-                   const float *X, const float *X_lo, int F, const float *ones, float *partial, float *dMx,
-                   float *dbM, const float *pagg, int nagg, float *dMe) {
+                   const float *X, const float *X_lo, int F, int Fp, const float *ones, float *partial, float *dMx,
+                   float *dbM) {
   const int count = c.H * F;
   float *cs = partial + (size_t)kMnDMxSplits * count;
   const TmaMaps mp{tma_map2d(dP, c.maxN, c.H, N_BK, true), tma_map2d(dP_lo, c.maxN, c.H, N_BK, true),
-                   tma_map2d(X, c.maxN, F, N_BK, true), tma_map2d(X_lo, c.maxN, F, N_BK, true)};
+                   tma_map2d(X, c.maxN, Fp, N_BK, true), tma_map2d(X_lo, c.maxN, Fp, N_BK, true)};
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
   MnDMx op{blob, partial, cs, c.H, F, 0};
-  nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * (F / MnDMx::BN + 1));
-  // dM_x, db_M and (when given) the dM_e block partials of the aggregation backward
-  const RJob j0{partial, kMnDMxSplits, count, dMx}, j1{cs, kMnDMxSplits, c.H, dbM};
-  const RJob j2{pagg, pagg ? nagg : 0, pagg ? c.H * c.Fe : 0, dMe};
-  launch_ex(k_reduce_jobs, reduce_blocks(j0) + reduce_blocks(j1) + reduce_blocks(j2), 32 * RW, 0, st, j0, j1, j2);
+  nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + 1));
+  const RJob j0{partial, kMnDMxSplits, count, dMx}, j1{cs, kMnDMxSplits, c.H, dbM}, j2{nullptr, 0, 0, nullptr};
+  launch_ex(k_reduce_jobs, reduce_blocks(j0) + reduce_blocks(j1), 32 * RW, 0, st, j0, j1, j2);
+  g_launches += 1;
+}
+
+int pad_x0_width(int F0) { return (F0 + 3) / 4 * 4; }  // 16-byte row pitch; TMA zero-fills the rest
+void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo) {
+  const int Fp = pad_x0_width(c.F0);
+  launch_ex(k_pad_x0, std::max(1, std::min(cdiv(c.maxN * Fp, 256), kSMs * 2)), 256, 0, st, blob, Fp, Xp, Xp_lo);
   g_launches += 1;
 }
 

@@ -185,3 +185,16 @@ def test_pipelined_loss_readback_matches_sync_read(torch_cuda):
     with pytest.raises(hgnn.HgError) as e:
         ctx.loss_enqueue(hgnn.HG_LOSS_RING)
     assert e.value.name == "HG_E_RANGE"
+
+
+def test_small_batch_after_large_batch_class_path(torch_cuda):
+    """Split-K partial buffers are reused across batches: a small batch (most node
+    splits empty) after a large one must not pick up stale partials (class path)."""
+    data = PT.generate("pcqm", 800, 33)
+    ctx, cfg, delta = PT.make_ctx(data, 128, 128, 3, seed=9)
+    big = O.shard(2, 0, 0, 1, len(data["y"]))[:128]
+    PT.assert_parity(PT.run_step_parity(data, big, ctx, cfg, delta))
+    small = O.shard(2, 1, 0, 1, len(data["y"]))[:3]
+    res = PT.run_step_parity(data, small, ctx, cfg, delta)
+    print({k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
+    PT.assert_parity(res)
