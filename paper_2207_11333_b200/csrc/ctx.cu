@@ -446,7 +446,8 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
       launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
-      if (cls && (l > 0 || p.xpad)) {  // MN-major TMA Gram (layer 0: padded node features)
+      static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
+      if (cls && (l > 0 || (p.xpad && !dmx0_simt))) {  // MN-major TMA Gram (layer 0: padded features)
         const float *Xg = l > 0 ? Xl : x->f(p.xpad), *Xg_lo = l > 0 ? x->f(p.X_lo[l - 1]) : x->f(p.xpad_lo);
         launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xg, Xg_lo, F, l > 0 ? F : pad_x0_width(c.f_node),
                       x->f(p.ones), part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
