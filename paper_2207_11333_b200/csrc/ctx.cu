@@ -157,7 +157,7 @@ struct hg_ctx {
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx;  // per layer fork / join points
   cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_hgrad = nullptr,
-              ev_prepmx = nullptr, ev_prepw = nullptr;
+              ev_prepmx = nullptr, ev_prepw = nullptr, ev_ar1 = nullptr;
   float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
@@ -360,8 +360,10 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   });
 }
 
+void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr, int64_t b, int64_t e, bool advance);
+int64_t layer1_offset(const hg_ctx *x);
 void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false,
-                      bool overlap_allreduce = false) {
+                      bool overlap_allreduce = false, const hg_adamw *early_adamw = nullptr) {
   const hg_config &c = x->cfg;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
@@ -449,8 +451,11 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
       if (cls && (l > 0 || (p.xpad && !dmx0_simt))) {  // MN-major TMA Gram (layer 0: padded features)
         const float *Xg = l > 0 ? Xl : x->f(p.xpad), *Xg_lo = l > 0 ? x->f(p.X_lo[l - 1]) : x->f(p.xpad_lo);
+        // layer 0's dM_x runs after the last main-chain kernel: it may use every SM
+        g_mn_grid_override = l == 0 ? 148 : 0;  // (kSMs)
         launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xg, Xg_lo, F, l > 0 ? F : pad_x0_width(c.f_node),
                       x->f(p.ones), part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+        g_mn_grid_override = 0;
       } else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
         launch_tc_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
       else
@@ -461,6 +466,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     if (overlap_allreduce && bk >= 0) {  // conv l's gradients complete: its bucket may go
       wait(side2, x->ev_gram[l]);
       enqueue_bucket(x, side2, bk);
+      if (x->world > 1 && x->comm && l == 1) rec(x->ev_ar1, x->comm_stream);  // layers >= 1 averaged
     }
     rec(x->ev_side[l], side2);
     // ---- main: dX into dZ[l-1]
@@ -475,6 +481,18 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         else
           launch_dX(st, x->caps, blob, dP, x->param(lname(l, "M_x")), F, Xl, dZn);
       });
+      if (early_adamw && fork && l == 1) {
+        // every parameter of layers >= 1 and the head is final (and allreduced) and no longer
+        // read by this step (dX_1 was the last reader): update them now, off the critical
+        // chain; conv0's parameters follow after the backward (that launch advances the step)
+        rec(x->ev_dx[1], st);
+        wait(side2, x->ev_dx[1]);
+        wait(side2, x->ev_gram[1]);
+        if (x->world > 1 && x->comm) wait(side2, x->ev_ar1);  // (early_adamw_ok: layer 1 closes a bucket)
+        g_low_prio = true;
+        enqueue_step(x, side2, *early_adamw, nullptr, layer1_offset(x), -1, false);
+        g_low_prio = false;
+      }
     }
   }
   wait(st, x->ev_gram[0]);  // join: every gradient is complete on the main stream
@@ -572,12 +590,21 @@ hg_status enqueue_allreduce(hg_ctx *x, cudaStream_t st) {
   return HG_OK;
 }
 
-void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr = nullptr) {
+// AdamW over parameters [b, e) of the flat arena (default: all); `advance` = this launch
+// is the step's last and advances the step counter
+void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr = nullptr, int64_t b = 0, int64_t e = -1,
+                  bool advance = true) {
   const Plan &p = x->plan;
+  if (e < 0) e = x->n_params;
   phase(pr, HG_PHASE_ADAMW, [&] {
-    launch_adamw(st, x->f(p.params), x->f(p.grads), x->f(p.m), x->f(p.v), x->n_params,
-                 reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay);
+    launch_adamw(st, x->f(p.params) + b, x->f(p.grads) + b, x->f(p.m) + b, x->f(p.v) + b, e - b,
+                 reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay, advance);
   });
+}
+int64_t layer1_offset(const hg_ctx *x) {  // start of conv1's parameters (conv0's come first)
+  for (auto &t : x->lay)
+    if (t.name == lname(1, "M_x")) return t.offset;
+  return x->n_params;
 }
 
 hg_status after_enqueue(hg_ctx *x, const char *what) {
@@ -635,7 +662,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
-  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad, &x->ev_prepmx, &x->ev_prepw})
+  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad, &x->ev_prepmx, &x->ev_prepw, &x->ev_ar1})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
   if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocDefault)) != cudaSuccess)
     return bail(e, "cudaHostAlloc");
@@ -716,7 +743,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
     for (auto ev : *v) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad, x->ev_prepmx, x->ev_prepw})
+  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad, x->ev_prepmx, x->ev_prepw, x->ev_ar1})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : x->loss_ev)
     if (ev) cudaEventDestroy(ev);
@@ -1065,9 +1092,15 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->cap_stream, slot, nullptr, true);
-  enqueue_backward(x, x->cap_stream, slot, nullptr, true, true);  // bucketed, overlapped allreduce
+  // bucketed, overlapped allreduce; AdamW of layers >= 1 and the head inside the backward
+  const bool split_adamw = x->cfg.layers > 1 && x->side_stream != nullptr && getenv("HG_ADAMW_END") == nullptr &&
+                           (x->world <= 1 || !x->comm || bucket_closed_by(x, 1) >= 0);
+  enqueue_backward(x, x->cap_stream, slot, nullptr, true, true, split_adamw ? h : nullptr);
   hg_status ar = join_buckets(x, x->cap_stream);
-  enqueue_step(x, x->cap_stream, *h);
+  if (split_adamw)
+    enqueue_step(x, x->cap_stream, *h, nullptr, 0, layer1_offset(x), true);  // conv0: advances the step
+  else
+    enqueue_step(x, x->cap_stream, *h);
   const int64_t nk = launches_so_far() - l0;
   cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
   if (ar) {

@@ -122,6 +122,7 @@ void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const i
 void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int l0, int l1,
                     int cmax, double delta, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo);
 
+extern int g_mn_grid_override;  // tcmn.cu: grid cap override for MN Grams (0 = default)
 // TMA-fed MN-major Grams (tcmn.cu): per-class-split dU / db_U and per-split dM_x / db_M,
 // partials reduced in fixed order (class path; rows of dZ / A degree-sorted)
 size_t mn_gram_partial_floats(const Caps &c, int cmax);

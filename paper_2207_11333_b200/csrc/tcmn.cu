@@ -27,6 +27,7 @@
 namespace hg {
 
 extern std::atomic<int64_t> g_launches;
+int g_mn_grid_override = 0;  // > 0: grid cap for the next MN launches (set by the step builder)
 
 namespace {
 
@@ -410,6 +411,7 @@ namespace {
 // CTAs of the side-stream Grams (persistent): fewer than the SM count leaves room for
 // the critical chain's kernels that run concurrently (HG_MN_GRID to override)
 int mn_grid_cap() {
+  if (g_mn_grid_override > 0) return g_mn_grid_override;
   static const int v = [] {
     const char *e = getenv("HG_MN_GRID");
     return e ? std::max(1, atoi(e)) : 40;  // measured optimum at config B (148 -> 40: +2%)

@@ -66,13 +66,13 @@ prof.export_chrome_trace(args.json)
 ev = json.load(open(args.json))["traceEvents"]
 k = [e for e in ev if e.get("cat") == "kernel"]
 k.sort(key=lambda e: e["ts"])
-# split into steps at the optimizer kernel (last kernel of a step)
+# split into steps at the degree sort (first kernel of every step)
 steps, cur = [], []
 for e in k:
-    cur.append(e)
-    if "adamw" in e["name"]:
+    if "degsort" in e["name"] and cur:
         steps.append(cur)
         cur = []
+    cur.append(e)
 if cur:
     steps.append(cur)
 s = steps[-1] if len(steps[-1]) > 10 else steps[-2]
