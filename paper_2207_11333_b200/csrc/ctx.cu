@@ -40,6 +40,7 @@ struct Plan {
   // direct-GEMM residuals x - trunc19(x) (class path): operands and weights
   size_t Wf_lo = 0, WbT_lo = 0, ones = 0, xpad = 0, xpad_lo = 0;
   std::vector<size_t> A_lo, X_lo;  // per layer (the backward Grams read them)
+  std::vector<size_t> Xs, Xs_lo;   // per layer: X_l in degree-sorted rows (fused dX->dA path)
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t total = 0;
 };
@@ -106,6 +107,8 @@ Plan make_plan(const hg_config &c) {
     for (int l = 0; l < c.layers; ++l) {
       p.A_lo.push_back(take(sizeof(float) * N * 4 * H));
       p.X_lo.push_back(take(sizeof(float) * N * H));
+      p.Xs.push_back(take(sizeof(float) * N * H));
+      p.Xs_lo.push_back(take(sizeof(float) * N * H));
     }
     p.ones = take(sizeof(float) * N * 32);  // B operand of the column-sum tiles
     if (pad_x0_width(c.f_node) <= 256) {      // layer-0 features for the TMA dM_x Gram
@@ -162,6 +165,7 @@ struct hg_ctx {
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
   bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
+  bool dxda = false;    // fused dX -> dA backward kernel (class path, H == 128; opt-in HG_DXDA=1)
   hg_status sticky = HG_OK;
   std::string sticky_msg;
 
@@ -298,7 +302,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
       if (c.layers > 1)
         launch_prep_W2(wst, x->caps, x->f(p.params), uo, 1, c.layers, p.cmax, c.delta, x->f(p.Wf), x->f(p.Wf_lo),
                        x->f(p.WbT), x->f(p.WbT_lo));
-      if (p.xpad) launch_pad_x0(wst, x->caps, blob, x->f(p.xpad), x->f(p.xpad_lo));
+      if (p.xpad) launch_pad_x0(wst, x->caps, blob, x->f(p.xpad), x->f(p.xpad_lo), x->dxda ? pos : nullptr);
       if (fork) cudaEventRecord(x->ev_prepw, wst);
       g_low_prio = false;
     });
@@ -330,7 +334,9 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
                             reinterpret_cast<const DegInfo *>(x->b(p.deginfo)),
                             reinterpret_cast<const int4 *>(x->b(p.tiles)),
                             x->f(p.Wf) + (size_t)l * p.cmax * 4 * HH, x->f(p.Wf_lo) + (size_t)l * p.cmax * 4 * HH,
-                            x->param(lname(l, "b_U")), x->f(p.X[l]), x->f(p.X_lo[l]));
+                            x->param(lname(l, "b_U")), x->f(p.X[l]), x->f(p.X_lo[l]),
+                            x->dxda && l + 1 < c.layers ? x->f(p.Xs[l]) : nullptr,
+                            x->dxda && l + 1 < c.layers ? x->f(p.Xs_lo[l]) : nullptr);
       else if (x->use_tc)
         launch_tc_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")),
                          x->param(lname(l, "b_U")), x->f(p.X[l]));
@@ -426,8 +432,11 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     rec(x->ev_gram[l], side);
     g_low_prio = false;
     // ---- main: dA, aggregation backward
+    const bool dxda = x->dxda && cls;
     phase(pr, HG_PHASE_DA, [&] {
-      if (cls)
+      if (dxda && l + 1 < c.layers) {
+        // dA_l was produced with dZ_l by layer l+1's fused dX -> dA kernel
+      } else if (cls)
         launch_d_dA_cls(st, x->caps, p.cmax, dZ, dZl, perm, dinfo, reinterpret_cast<const int4 *>(x->b(p.tiles)),
                         x->f(p.WbT) + (size_t)l * p.cmax * 4 * HH, x->f(p.WbT_lo) + (size_t)l * p.cmax * 4 * HH,
                         x->f(p.dA));
@@ -438,7 +447,8 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, cls ? dPlo : nullptr, pos);
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, cls ? dPlo : nullptr, pos,
+                     dxda ? pos : nullptr);
     });
     const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
@@ -450,7 +460,9 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
       static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
       if (cls && (l > 0 || (p.xpad && !dmx0_simt))) {  // MN-major TMA Gram (layer 0: padded features)
-        const float *Xg = l > 0 ? Xl : x->f(p.xpad), *Xg_lo = l > 0 ? x->f(p.X_lo[l - 1]) : x->f(p.xpad_lo);
+        // (fused path: dP rows are degree-sorted, so X comes in sorted rows too)
+        const float *Xg = l > 0 ? (dxda ? x->f(p.Xs[l - 1]) : Xl) : x->f(p.xpad);
+        const float *Xg_lo = l > 0 ? x->f(dxda ? p.Xs_lo[l - 1] : p.X_lo[l - 1]) : x->f(p.xpad_lo);
         // layer 0's dM_x runs after the last main-chain kernel: it may use every SM
         g_mn_grid_override = l == 0 ? 148 : 0;  // (kSMs)
         launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xg, Xg_lo, F, l > 0 ? F : pad_x0_width(c.f_node),
@@ -473,7 +485,12 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     if (l > 0) {
       float *dZn = x->f(p.dZ[l - 1]), *dZnl = cls ? x->f(p.dZ_lo[l - 1]) : nullptr;
       phase(pr, HG_PHASE_DX, [&] {
-        if (cls)
+        if (dxda)
+          launch_dxda(st, x->caps, p.cmax, dP, dPlo, x->f(p.MxT) + (size_t)(l - 1) * HH,
+                      x->f(p.MxT_lo) + (size_t)(l - 1) * HH, x->f(p.WbT) + (size_t)(l - 1) * p.cmax * 4 * HH,
+                      x->f(p.WbT_lo) + (size_t)(l - 1) * p.cmax * 4 * HH, perm, dinfo,
+                      reinterpret_cast<const int4 *>(x->b(p.tiles)), x->f(p.Xs[l - 1]), dZn, dZnl, x->f(p.dA));
+        else if (cls)
           launch_d_dX(st, x->caps, blob, dP, dPlo, x->f(p.MxT) + (size_t)(l - 1) * HH,
                       x->f(p.MxT_lo) + (size_t)(l - 1) * HH, F, Xl, dZn, dZnl, pos);
         else if (x->use_tc && F % 64 == 0)
@@ -695,6 +712,9 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   head_configure(x->caps);
   if (x->use_tc && (e = tc_configure()) != cudaSuccess) return bail(e, "tc_configure");
   if (x->use_tc && (e = tcd_configure()) != cudaSuccess) return bail(e, "tcd_configure");
+  // fused dX -> dA backward: opt-in (HG_DXDA=1); measured 7% slower at config B than the
+  // separate TMA dX and dA kernels (its two chained GEMMs and epilogues run serially per CTA)
+  x->dxda = x->use_tc && plan.cmax > 0 && dxda_supported(x->caps) && getenv("HG_DXDA") != nullptr;
   if (const char *pe = getenv("HG_PDL")) g_pdl = atoi(pe) != 0;  // A/B switch for launch overlap
   {
     std::vector<int64_t> uo;

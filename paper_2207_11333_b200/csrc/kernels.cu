@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
                                                     const float *__restrict__ A, const uint8_t *__restrict__ arg,
                                                     const float *__restrict__ dA, float *__restrict__ dP,
                                                     float *__restrict__ partial, int H, float *__restrict__ dP_lo,
-                                                    const int *__restrict__ pos) {
+                                                    const int *__restrict__ pos, const int *__restrict__ dp_pos) {
   pdl_enter();
   __shared__ float red[kAggBwdWarps][32][CPL * FE];
   const BatchView b = load_batch(blob);
@@ -590,8 +590,9 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
         for (int f = 0; f < FE; ++f) acc[c][f] = fmaf(g, ef[f], acc[c][f]);
       }
     }
-    store_vec<CPL>(dP + (size_t)j * H + ch, dp);
-    if (dP_lo) store_vec_lo<CPL>(dP_lo + (size_t)j * H + ch, dp);
+    const size_t prow = (size_t)(dp_pos ? dp_pos[j] : j) * H + ch;  // degree-sorted row when dp_pos is given
+    store_vec<CPL>(dP + prow, dp);
+    if (dP_lo) store_vec_lo<CPL>(dP_lo + prow, dp);
   }
   // block reduction of dM_e partials in fixed warp order
 #pragma unroll
@@ -632,20 +633,20 @@ int agg_bwd_partials(const Caps &c) { return agg_bwd_blocks(c); }
 template <int CPL, int FE>
 static void agg_bwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                            const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                           float *partial, float *dP_lo, const int *pos) {
+                           float *partial, float *dP_lo, const int *pos, const int *dp_pos) {
   const dim3 grid(agg_bwd_blocks(c), c.H / (32 * CPL));
   launch_ex(k_agg_bwd<CPL, FE>, grid, 32 * kAggBwdWarps, 0, st, blob, P, Me, bM, A, arg, dA, dP, partial, c.H, dP_lo,
-            pos);
+            pos, dp_pos);
 }
 
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe, float *dP_lo, const int *pos) {
+                    float *partial, float *dMe, float *dP_lo, const int *pos, const int *dp_pos) {
   const int cpl = agg_cpl(c.H);
-  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
-  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
-  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
-  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos);
+  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
+  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
+  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
+  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
   counted();
   if (dMe) launch_reduce_dMe(st, c, partial, dMe);
 }

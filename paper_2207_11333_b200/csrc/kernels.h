@@ -45,7 +45,8 @@ void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
 // K8: aggregation backward + scatter to sources; dM_e via block partials
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe, float *dP_lo = nullptr, const int *pos = nullptr);
+                    float *partial, float *dMe, float *dP_lo = nullptr, const int *pos = nullptr,
+                    const int *dp_pos = nullptr);  // dp_pos: write dP row j at dp_pos[j]
 // dM_e = fixed-order sum of launch_agg_bwd's block partials (launch_agg_bwd does it when dMe != null)
 void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe);
 size_t agg_bwd_partial_floats(const Caps &c);
@@ -106,9 +107,10 @@ void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax
 // TMA-fed tcgen05 GEMMs over pre-split operands (tcdirect.cu). A / dZ operands of
 // the class GEMMs are stored in degree-sorted row order (row pos[i] for node i).
 cudaError_t tcd_configure();
+// (X1s, X1s_lo optional: also write the output rows in degree-sorted order)
 void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
-                         float *X1, float *X1_lo);
+                         float *X1, float *X1_lo, float *X1s = nullptr, float *X1s_lo = nullptr);
 void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
                      const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA);
 void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
@@ -116,6 +118,12 @@ void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
 void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
                  const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
                  const int *pos);
+// fused backward (H == 128): dZ_{l-1} = (dP_l M_x) * [X_{l-1} > 0] (sorted rows, + lo) and
+// dA_{l-1} = dZ_{l-1} W_c per degree-class tile; dP_s / Xs in degree-sorted row order
+bool dxda_supported(const Caps &c);
+void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *dP_s_lo, const float *MxT,
+                 const float *MxT_lo, const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info,
+                 const int4 *tiles, const float *Xs, float *dZ, float *dZ_lo, float *dA);
 void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,
                     float *Mx_lo, float *MxT, float *MxT_lo);
 // layers [l0, l1) of the degree-slot weights
@@ -136,7 +144,8 @@ void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
                    float *dbM);
 // layer-0 node features padded to pad_x0_width(F0) columns (+ tf32 residual) for the TMA path
 int pad_x0_width(int F0);
-void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo);
+void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo,
+                   const int *pos = nullptr);  // pos: write row i at pos[i]
 int agg_bwd_partials(const Caps &c);  // number of dM_e block partials launch_agg_bwd writes
 
 // tcgen05 3xTF32 GEMMs (tcgemm.cu); require H % 128 == 0

@@ -266,6 +266,7 @@ template <int BN_>
 struct TUpdC {
   static constexpr int BN = BN_, ID = 0;
   const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1, *X1_lo; int H; int items_cap;
+  float *X1s, *X1s_lo;  // optional: the same rows in degree-sorted order (backward dX/dM_x operands)
   int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     const int nt = H / BN, ti = t / nt;
@@ -287,7 +288,13 @@ struct TUpdC {
     const float4 z = make_float4(fmaxf(v.x + b.x, 0.f), fmaxf(v.y + b.y, 0.f), fmaxf(v.z + b.z, 0.f),
                                  fmaxf(v.w + b.w, 0.f));
     *reinterpret_cast<float4 *>(X1 + o) = z;
-    *reinterpret_cast<float4 *>(X1_lo + o) = lo4(z);
+    const float4 zl = lo4(z);
+    *reinterpret_cast<float4 *>(X1_lo + o) = zl;
+    if (X1s) {
+      const size_t os = (size_t)m * H + n;
+      *reinterpret_cast<float4 *>(X1s + os) = z;
+      *reinterpret_cast<float4 *>(X1s_lo + os) = zl;
+    }
   }
 };
 
@@ -366,6 +373,214 @@ struct TDX {
     *reinterpret_cast<float4 *>(dZ_lo + od) = lo4(z);
   }
 };
+
+// ---------------------------------------------------------------- fused dX -> dA
+// Backward of layer l's projection chained into layer l-1's update backward, per
+// 128-row degree-class tile (rows degree-sorted) and 128-column slice of dA:
+//   stage 1  T   = dP_l[rows] M_x                     (K = H,  N = F = H)
+//   epi 1    dZ  = T * [X_{l-1}[rows] > 0]  -> smem (K-major SW128, hi + lo) as stage 2's A;
+//                                              slice 0 also stores dZ_{l-1} (+ lo) for the Gram
+//   stage 2  dA  = dZ W_c^T...               (K = F,  N = 128 of 4H) -> dA[perm[m]]
+// Every operand row range is contiguous (dP_l and X_{l-1} are kept in sorted order for this).
+// The stage-1 ring (2 x 64 KB) is reused for the 128 KB dZ tile once stage 1's MMAs are done.
+// warps 0-3 epilogues, warp 4 TMA, warp 5 TMEM + MMA; one tile per CTA.
+struct DxDaMaps {
+  CUtensorMap ah, al;  // dP_l sorted rows [maxN][H]
+  CUtensorMap bh, bl;  // M_x^T [F][H]
+  CUtensorMap wh, wl;  // W_c^T rows of layer l-1 [cmax*4H][F]
+};
+constexpr int XD_ST1 = 2, XD_ST2 = 2;
+constexpr int XD_STAGE1 = 4 * 128 * 128;  // A hi/lo + B hi/lo: 64 KB
+constexpr int XD_STAGE2 = 2 * 128 * 128;  // W hi/lo: 32 KB
+constexpr int XD_SMEM = XD_ST1 * XD_STAGE1 + XD_ST2 * XD_STAGE2 + T_STG_BYTES + 1024 + 8 * 16 + 16;
+
+struct SkTraceOp5 {
+  static constexpr int ID = 5;
+};
+__global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ DxDaMaps mp, const int *perm,
+                                                       const DegInfo *info, const int4 *tiles, const float *Xs,
+                                                       float *dZ, float *dZ_lo, float *dA, int H) {
+  using Op = SkTraceOp5;
+  constexpr int F = 128;  // dZ width (= H, checked by the launcher)
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t *ring1 = smem;                                   // stage-1 ring, later the dZ tile
+  uint8_t *ring2 = smem + XD_ST1 * XD_STAGE1;              // stage-2 W ring
+  float *stg_all = reinterpret_cast<float *>(ring2 + XD_ST2 * XD_STAGE2);
+  uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(stg_all) + T_STG_BYTES);
+  uint64_t *full1 = bar, *empty1 = bar + 2, *full2 = bar + 4, *empty2 = bar + 6, *acc1 = bar + 8, *acc2 = bar + 9,
+           *zrdy = bar + 10;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 12);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) TTRACE(0);
+  if (warp == T_MMA_WARP) tc::tmem_alloc<256>(tmem_holder);
+  if (threadIdx.x == T_TMA_WARP * 32) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full1[i], 1);
+      tc::mbar_init(&empty1[i], 1);
+      tc::mbar_init(&full2[i], 1);
+      tc::mbar_init(&empty2[i], 1);
+    }
+    tc::mbar_init(acc1, 1);
+    tc::mbar_init(acc2, 1);
+    tc::mbar_init(zrdy, 4);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_holder;  // cols [0,128): T, [128,256): dA slice
+  pdl_enter();
+  const int NT2 = 4 * H / 128, ti = blockIdx.x / NT2, n2 = (blockIdx.x % NT2) * 128;
+  if (ti < info->T) {  // uniform per CTA
+    const int4 tl = tiles[ti];
+    const int row_end = tl.y + tl.z;
+    constexpr int KC1 = 4;          // H / 32 (H = 128)
+    constexpr int KC2 = F / T_BK;   // 4
+    if (warp == T_TMA_WARP) {
+      if (lane == 0) {
+        for (int c = 0; c < KC1; ++c) {
+          const int s = c & 1;
+          if (c >= 2) tc::mbar_wait(&empty1[s], 0);
+          uint8_t *sa = ring1 + s * XD_STAGE1;
+          tc::mbar_expect_tx(&full1[s], XD_STAGE1);
+          tc::tma_load_2d(sa, &mp.ah, c * T_BK, tl.y, &full1[s]);
+          tc::tma_load_2d(sa + 16384, &mp.al, c * T_BK, tl.y, &full1[s]);
+          tc::tma_load_2d(sa + 32768, &mp.bh, c * T_BK, 0, &full1[s]);
+          tc::tma_load_2d(sa + 49152, &mp.bl, c * T_BK, 0, &full1[s]);
+        }
+        const int wrow = tl.x * 4 * H + n2;  // rows of W_c^T for this dA slice
+        for (int c = 0; c < KC2; ++c) {
+          const int s = c & 1;
+          if (c >= 2) tc::mbar_wait(&empty2[s], 0);
+          uint8_t *sw = ring2 + s * XD_STAGE2;
+          tc::mbar_expect_tx(&full2[s], XD_STAGE2);
+          tc::tma_load_2d(sw, &mp.wh, c * T_BK, wrow, &full2[s]);
+          tc::tma_load_2d(sw + 16384, &mp.wl, c * T_BK, wrow, &full2[s]);
+        }
+      }
+      __syncwarp();
+    } else if (warp == T_MMA_WARP) {
+      if (lane == 0) {
+        constexpr uint32_t idesc = tc::idesc_tf32(T_BM, 128);
+        for (int c = 0; c < KC1; ++c) {
+          const int s = c & 1;
+          tc::mbar_wait(&full1[s], (c >> 1) & 1);
+          tc::fence_after_sync();
+          const uint32_t aH = tc::smem_u32(ring1 + s * XD_STAGE1), aL = aH + 16384, bH = aH + 32768, bL = aH + 49152;
+#pragma unroll
+          for (int ks = 0; ks < T_BK / 8; ++ks) {
+            const uint32_t off = ks * 32;
+            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
+            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+            tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
+            tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
+            tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+          }
+          tc::mma_commit(&empty1[s]);
+        }
+        tc::mma_commit(acc1);
+        // stage 2: A = the dZ tile the epilogue wrote into ring1 (chunk c: hi 16 KB | lo 16 KB)
+        tc::mbar_wait(zrdy, 0);
+        tc::fence_after_sync();
+        for (int c = 0; c < KC2; ++c) {
+          const int s = c & 1;
+          tc::mbar_wait(&full2[s], (c >> 1) & 1);
+          tc::fence_after_sync();
+          const uint32_t aH = tc::smem_u32(ring1 + c * 32768), aL = aH + 16384;
+          const uint32_t bH = tc::smem_u32(ring2 + s * XD_STAGE2), bL = bH + 16384;
+#pragma unroll
+          for (int ks = 0; ks < T_BK / 8; ++ks) {
+            const uint32_t off = ks * 32;
+            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
+            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+            tc::mma_tf32(tmem + 128, dah, dbh, idesc, (c | ks) != 0);
+            tc::mma_tf32(tmem + 128, dah, dbl, idesc, 1u);
+            tc::mma_tf32(tmem + 128, dal, dbh, idesc, 1u);
+          }
+          tc::mma_commit(&empty2[s]);
+        }
+        tc::mma_commit(acc2);
+      }
+      __syncwarp();
+    } else {
+      // ---------------- epilogue 1: mask, dZ tile into smem (+ global for slice 0)
+      const int row = warp * 32 + lane, m = tl.y + row;
+      float *stg = stg_all + warp * 32 * T_STG_LD;
+      tc::mbar_wait(acc1, 0);
+      tc::fence_after_sync();
+      const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+      for (int q = 0; q < F / 32; ++q) {
+        float t[32];
+        tc::tmem_ld32(trow + (uint32_t)(q * 32), t);
+        const float *xr = Xs + (size_t)(m < row_end ? m : tl.y) * F + q * 32;  // (rows past the tile: unused)
+        uint8_t *ch = ring1 + q * 32768;  // dZ chunk q: hi, then lo
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float4 x = ldg4(xr + 4 * j);
+          const float4 z = make_float4(x.x > 0.f ? t[4 * j] : 0.f, x.y > 0.f ? t[4 * j + 1] : 0.f,
+                                       x.z > 0.f ? t[4 * j + 2] : 0.f, x.w > 0.f ? t[4 * j + 3] : 0.f);
+          const uint32_t o = tc::sw128_off(row, j);
+          *reinterpret_cast<float4 *>(ch + o) = z;
+          *reinterpret_cast<float4 *>(ch + 16384 + o) = lo4(z);
+          *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) = z;
+        }
+        __syncwarp();
+        if (n2 == 0) {  // coalesced store of dZ_{l-1} (sorted rows of this class tile only)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int r = 4 * j + (lane >> 3), cc = 4 * (lane & 7), mr = tl.y + warp * 32 + r;
+            if (mr < row_end) {
+              const float4 z = *reinterpret_cast<const float4 *>(stg + r * T_STG_LD + cc);
+              *reinterpret_cast<float4 *>(dZ + (size_t)mr * F + q * 32 + cc) = z;
+              *reinterpret_cast<float4 *>(dZ_lo + (size_t)mr * F + q * 32 + cc) = lo4(z);
+            }
+          }
+        }
+        __syncwarp();
+      }
+      tc::fence_proxy_async_smem();  // generic smem writes -> visible to the tensor core
+      tc::fence_before_sync();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(zrdy);
+      // ---------------- epilogue 2: dA rows (node order)
+      tc::mbar_wait(acc2, 0);
+      tc::fence_after_sync();
+#pragma unroll 1
+      for (int q = 0; q < 128 / 32; ++q) {
+        float a[32];
+        tc::tmem_ld32(trow + 128u + (uint32_t)(q * 32), a);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) =
+              make_float4(a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
+        __syncwarp();
+        int node[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int mr = tl.y + warp * 32 + 4 * j + (lane >> 3);
+          node[j] = mr < row_end ? perm[mr] : -1;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int r = 4 * j + (lane >> 3), cc = 4 * (lane & 7);
+          if (node[j] >= 0)
+            *reinterpret_cast<float4 *>(dA + (size_t)node[j] * 4 * H + n2 + q * 32 + cc) =
+                *reinterpret_cast<const float4 *>(stg + r * T_STG_LD + cc);
+        }
+        __syncwarp();
+      }
+      if (threadIdx.x == 0) TTRACE(6);
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == T_MMA_WARP) {
+    tc::fence_after_sync();
+    tc::tmem_dealloc<256>(tmem);
+  }
+}
 
 // ---------------------------------------------------------------- split-K update
 // G1 with K = 4H split over a cluster of KS = 4 CTAs (one aggregator block of
@@ -706,11 +921,11 @@ cudaError_t tconfigure_bn() {
 template <int BN>
 void update_bn(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU, float *X1,
-               float *X1_lo) {
+               float *X1_lo, float *X1s, float *X1s_lo) {
   const int K = 4 * c.H;
   const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, BN),
                    map2d(Wf_lo, (uint64_t)cmax * c.H, K, BN)};
-  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0, 0};
+  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0, X1s, X1s_lo, 0};
   trun(st, mp, op, tc_max_tiles(c, cmax) * (c.H / BN));
 }
 template <int BN>
@@ -759,6 +974,8 @@ cudaError_t tcd_configure() {
   if (const char *v = getenv("HG_UPDATE_SK")) g_update_sk = atoi(v) != 0;
   if ((e = cudaFuncSetAttribute(k_update_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM)) != cudaSuccess)
     return e;
+  if ((e = cudaFuncSetAttribute(k_dxda, cudaFuncAttributeMaxDynamicSharedMemorySize, XD_SMEM)) != cudaSuccess)
+    return e;
   if ((e = tconfigure_bn<32>()) != cudaSuccess) return e;
   if ((e = tconfigure_bn<64>()) != cudaSuccess) return e;
   if ((e = tconfigure_bn<128>()) != cudaSuccess) return e;
@@ -767,8 +984,8 @@ cudaError_t tcd_configure() {
 
 void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
-                         float *X1, float *X1_lo) {
-  if (g_update_sk && c.H == SK_H) {
+                         float *X1, float *X1_lo, float *X1s, float *X1s_lo) {
+  if (g_update_sk && c.H == SK_H && !X1s) {
     const int K = 4 * c.H;
     const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, SK_H),
                      map2d(Wf_lo, (uint64_t)cmax * c.H, K, SK_H)};
@@ -792,9 +1009,10 @@ void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *
     g_launches += 1;
     return;
   }
-  if (g_bn_upd == 32) update_bn<32>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
-  else if (g_bn_upd == 128) update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
-  else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo);
+  if (g_bn_upd == 32) update_bn<32>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo);
+  else if (g_bn_upd == 128)
+    update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo);
+  else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo);
 }
 
 void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
@@ -817,6 +1035,19 @@ void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const floa
   if (g_bn_dx == 32) dX_bn<32>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
   else if (g_bn_dx == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
   else dX_bn<64>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+}
+
+bool dxda_supported(const Caps &c) { return c.H == 128; }
+
+void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *dP_s_lo, const float *MxT,
+                 const float *MxT_lo, const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info,
+                 const int4 *tiles, const float *Xs, float *dZ, float *dZ_lo, float *dA) {
+  const DxDaMaps mp{map2d(dP_s, c.maxN, c.H, 128), map2d(dP_s_lo, c.maxN, c.H, 128), map2d(MxT, 128, c.H, 128),
+                    map2d(MxT_lo, 128, c.H, 128), map2d(WbT, (uint64_t)cmax * 4 * c.H, 128, 128),
+                    map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, 128, 128)};
+  const int grid = tc_max_tiles(c, cmax) * (4 * c.H / 128);
+  launch_ex(k_dxda, grid, T_THREADS, XD_SMEM, st, mp, perm, info, tiles, Xs, dZ, dZ_lo, dA, c.H);
+  g_launches += 1;
 }
 
 void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,

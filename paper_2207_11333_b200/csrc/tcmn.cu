@@ -299,15 +299,16 @@ struct MnDMx {
 // layer-0 input as a TMA-readable operand: Xp[i][0..Fp) = x_i padded with zeros to a
 // 16-byte row pitch, and its tf32 residual
 __global__ void __launch_bounds__(256) k_pad_x0(const uint8_t *__restrict__ blob, int Fp, float *__restrict__ Xp,
-                                                float *__restrict__ Xp_lo) {
+                                                float *__restrict__ Xp_lo, const int *__restrict__ pos) {
   pdl_enter();
   const BatchView b = load_batch(blob);
   const int F = b.F0;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < b.N * Fp; e += gridDim.x * blockDim.x) {
     const int i = e / Fp, f = e - i * Fp;
     const float v = f < F ? b.x[(size_t)i * F + f] : 0.f;
-    Xp[e] = v;
-    Xp_lo[e] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    const size_t o = pos ? (size_t)pos[i] * Fp + f : (size_t)e;  // degree-sorted rows when pos is given
+    Xp[o] = v;
+    Xp_lo[o] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
   }
 }
 
@@ -470,9 +471,10 @@ void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
 }
 
 int pad_x0_width(int F0) { return (F0 + 3) / 4 * 4; }  // 16-byte row pitch; TMA zero-fills the rest
-void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo) {
+void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo, const int *pos) {
   const int Fp = pad_x0_width(c.F0);
-  launch_ex(k_pad_x0, std::max(1, std::min(cdiv(c.maxN * Fp, 256), kSMs * 2)), 256, 0, st, blob, Fp, Xp, Xp_lo);
+  launch_ex(k_pad_x0, std::max(1, std::min(cdiv(c.maxN * Fp, 256), kSMs * 2)), 256, 0, st, blob, Fp, Xp, Xp_lo,
+            pos);
   g_launches += 1;
 }
 

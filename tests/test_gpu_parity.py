@@ -198,3 +198,14 @@ def test_small_batch_after_large_batch_class_path(torch_cuda):
     res = PT.run_step_parity(data, small, ctx, cfg, delta)
     print({k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     PT.assert_parity(res)
+
+
+def test_fused_dx_da_path(torch_cuda, monkeypatch):
+    """The opt-in fused dX -> dA backward kernel (HG_DXDA=1) computes the same step."""
+    monkeypatch.setenv("HG_DXDA", "1")
+    data = PT.generate("pcqm", 600, 21)
+    ctx, cfg, delta = PT.make_ctx(data, 128, 128, 4, seed=5)
+    ids = O.shard(23, 1, 0, 1, len(data["y"]))[:128]
+    res = PT.run_step_parity(data, ids, ctx, cfg, delta)
+    print({k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
+    PT.assert_parity(res)
