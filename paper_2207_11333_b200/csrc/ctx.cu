@@ -280,7 +280,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   phase(pr, HG_PHASE_SCALERS, [&] {
     launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
                    reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
-                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)));
+                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)),
+                   gram_ks(x->caps));
   });
   if (fork) cudaEventRecord(x->ev_start, st);
   // the prep branch is enqueued after layer 0's projection so that the main chain is

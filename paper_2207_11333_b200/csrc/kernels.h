@@ -89,7 +89,13 @@ void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v,
 
 // degree classes (tcgemm.cu): one class per distinct degree present in the batch
 constexpr int kMaxClasses = 16;
-constexpr int kGramKS = 256;  // nodes per K-split of the per-class Gram GEMM
+constexpr int kGramKS = 256;  // minimum nodes per K-split of the per-class Gram GEMM
+// nodes per Gram K-split for a capacity: >= kGramKS, about 64 splits at large capacities
+// (the split partials are reduced afterwards, so their number bounds that traffic)
+inline int gram_ks(const Caps &c) {
+  const int k = (c.maxN + 63) / 64;
+  return k <= kGramKS ? kGramKS : (k + 31) / 32 * 32;
+}
 constexpr int HG_MAX_DEGREE_DEV = 127;
 struct DegInfo {
   int C, T, S, pad;
@@ -102,7 +108,7 @@ int tc_max_splits(const Caps &c, int cmax);
 // stable degree sort + per-node scalers (+ class table / tiles / splits when cmax > 0)
 // perm[r] = node at degree-sorted row r, pos = its inverse (pos may be null)
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
-                    DegInfo *info, int4 *tiles, int4 *splits, int *pos = nullptr);
+                    DegInfo *info, int4 *tiles, int4 *splits, int *pos = nullptr, int ks = 0);
 
 // TMA-fed tcgen05 GEMMs over pre-split operands (tcdirect.cu). A / dZ operands of
 // the class GEMMs are stored in degree-sorted row order (row pos[i] for node i).

@@ -809,11 +809,12 @@ int tc_num_classes(const Caps &c, int max_degree) {
   return (tc_supported(c) && cm <= kMaxClasses) ? cm : 0;
 }
 int tc_max_tiles(const Caps &c, int cmax) { return mtiles(c.maxN) + cmax; }
-int tc_max_splits(const Caps &c, int cmax) { return (c.maxN + kGramKS - 1) / kGramKS + cmax; }
+int tc_max_splits(const Caps &c, int cmax) { return (c.maxN + gram_ks(c) - 1) / gram_ks(c) + cmax; }
 
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
-                    DegInfo *info, int4 *tiles, int4 *splits, int *pos) {
-  launch_ex(k_degsort, 1, 1024, 0, st, blob, delta, cmax, kGramKS, amp, att, perm, info, tiles, splits, pos);
+                    DegInfo *info, int4 *tiles, int4 *splits, int *pos, int ks) {
+  launch_ex(k_degsort, 1, 1024, 0, st, blob, delta, cmax, ks > 0 ? ks : kGramKS, amp, att, perm, info, tiles, splits,
+            pos);
   g_launches += 1;
 }
 

@@ -411,18 +411,23 @@ __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int co
 namespace {
 // CTAs of the side-stream Grams (persistent): fewer than the SM count leaves room for
 // the critical chain's kernels that run concurrently (HG_MN_GRID to override)
-int mn_grid_cap() {
+// Small steps (config B: ~150 Gram items) run the Grams beside the latency-bound main chain,
+// where fewer CTAs interfere less (148 -> 40 measured +2%); large ones (config D/E: thousands
+// of items) need every SM. Cap = clamp(items / 4, 40, 148) unless HG_MN_GRID overrides.
+int mn_grid_cap(int items) {
   if (g_mn_grid_override > 0) return g_mn_grid_override;
   static const int v = [] {
     const char *e = getenv("HG_MN_GRID");
-    return e ? std::max(1, atoi(e)) : 40;  // measured optimum at config B (148 -> 40: +2%)
+    return e ? std::max(1, atoi(e)) : 0;
   }();
-  return v;
+  if (v > 0) return v;
+  return std::max(40, std::min(kSMs, items / 4));
 }
 template <class Op>
 void nrun(cudaStream_t st, const TmaMaps &mp, const CUtensorMap &ones, Op op, int items) {
   op.items_cap = items;
-  launch_ex(k_tmn<Op>, std::max(1, std::min(items, mn_grid_cap())), N_THREADS, n_smem_bytes<Op>(), st, mp, ones, op);
+  launch_ex(k_tmn<Op>, std::max(1, std::min(items, mn_grid_cap(items))), N_THREADS, n_smem_bytes<Op>(), st, mp, ones,
+            op);
   g_launches += 1;
 }
 }  // namespace
