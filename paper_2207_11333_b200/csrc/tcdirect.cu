@@ -390,6 +390,7 @@ struct DxDaMaps {
   CUtensorMap wh, wl;  // W_c^T rows of layer l-1 [cmax*4H][F]
 };
 constexpr int XD_ST1 = 2, XD_ST2 = 2;
+constexpr int XD_NS = 2;  // dA slices (of 128 columns) per CTA: stage 1 is recomputed 4H/(128*XD_NS) times per tile
 constexpr int XD_STAGE1 = 4 * 128 * 128;  // A hi/lo + B hi/lo: 64 KB
 constexpr int XD_STAGE2 = 2 * 128 * 128;  // W hi/lo: 32 KB
 constexpr int XD_SMEM = XD_ST1 * XD_STAGE1 + XD_ST2 * XD_STAGE2 + T_STG_BYTES + 1024 + 8 * 16 + 16;
@@ -413,7 +414,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 12);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) TTRACE(0);
-  if (warp == T_MMA_WARP) tc::tmem_alloc<256>(tmem_holder);
+  if (warp == T_MMA_WARP) tc::tmem_alloc<512>(tmem_holder);
   if (threadIdx.x == T_TMA_WARP * 32) {
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&full1[i], 1);
@@ -423,20 +424,21 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
     }
     tc::mbar_init(acc1, 1);
     tc::mbar_init(acc2, 1);
+    tc::mbar_init(acc2 + 2, 1);  // second dA slice (bar[11])
     tc::mbar_init(zrdy, 4);
     tc::fence_mbar_init();
   }
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
-  const uint32_t tmem = *tmem_holder;  // cols [0,128): T, [128,256): dA slice
+  const uint32_t tmem = *tmem_holder;  // cols [0,128): T, [128 + 128 s, ...): dA slice s
   pdl_enter();
-  const int NT2 = 4 * H / 128, ti = blockIdx.x / NT2, n2 = (blockIdx.x % NT2) * 128;
+  const int NG = 4 * H / (128 * XD_NS), ti = blockIdx.x / NG, n2 = (blockIdx.x % NG) * 128 * XD_NS;
   if (ti < info->T) {  // uniform per CTA
     const int4 tl = tiles[ti];
     const int row_end = tl.y + tl.z;
     constexpr int KC1 = 4;          // H / 32 (H = 128)
-    constexpr int KC2 = F / T_BK;   // 4
+    constexpr int KC2 = F / T_BK;   // 4 chunks per dA slice
     if (warp == T_TMA_WARP) {
       if (lane == 0) {
         for (int c = 0; c < KC1; ++c) {
@@ -449,14 +451,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
           tc::tma_load_2d(sa + 32768, &mp.bh, c * T_BK, 0, &full1[s]);
           tc::tma_load_2d(sa + 49152, &mp.bl, c * T_BK, 0, &full1[s]);
         }
-        const int wrow = tl.x * 4 * H + n2;  // rows of W_c^T for this dA slice
-        for (int c = 0; c < KC2; ++c) {
+        for (int c = 0; c < KC2 * XD_NS; ++c) {  // slice c / KC2, K chunk c % KC2
           const int s = c & 1;
-          if (c >= 2) tc::mbar_wait(&empty2[s], 0);
+          if (c >= 2) tc::mbar_wait(&empty2[s], ((c >> 1) - 1) & 1);
           uint8_t *sw = ring2 + s * XD_STAGE2;
+          const int wrow = tl.x * 4 * H + n2 + (c / KC2) * 128;  // rows of W_c^T for this dA slice
           tc::mbar_expect_tx(&full2[s], XD_STAGE2);
-          tc::tma_load_2d(sw, &mp.wh, c * T_BK, wrow, &full2[s]);
-          tc::tma_load_2d(sw + 16384, &mp.wl, c * T_BK, wrow, &full2[s]);
+          tc::tma_load_2d(sw, &mp.wh, (c % KC2) * T_BK, wrow, &full2[s]);
+          tc::tma_load_2d(sw + 16384, &mp.wl, (c % KC2) * T_BK, wrow, &full2[s]);
         }
       }
       __syncwarp();
@@ -483,30 +485,47 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
         // stage 2: A = the dZ tile the epilogue wrote into ring1 (chunk c: hi 16 KB | lo 16 KB)
         tc::mbar_wait(zrdy, 0);
         tc::fence_after_sync();
-        for (int c = 0; c < KC2; ++c) {
-          const int s = c & 1;
+        for (int c = 0; c < KC2 * XD_NS; ++c) {
+          const int s = c & 1, sl = c / KC2, kc = c % KC2;
           tc::mbar_wait(&full2[s], (c >> 1) & 1);
           tc::fence_after_sync();
-          const uint32_t aH = tc::smem_u32(ring1 + c * 32768), aL = aH + 16384;
+          const uint32_t aH = tc::smem_u32(ring1 + kc * 32768), aL = aH + 16384;
           const uint32_t bH = tc::smem_u32(ring2 + s * XD_STAGE2), bL = bH + 16384;
+          const uint32_t d = tmem + 128u + (uint32_t)(sl * 128);
 #pragma unroll
           for (int ks = 0; ks < T_BK / 8; ++ks) {
             const uint32_t off = ks * 32;
             const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
             const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
-            tc::mma_tf32(tmem + 128, dah, dbh, idesc, (c | ks) != 0);
-            tc::mma_tf32(tmem + 128, dah, dbl, idesc, 1u);
-            tc::mma_tf32(tmem + 128, dal, dbh, idesc, 1u);
+            tc::mma_tf32(d, dah, dbh, idesc, (kc | ks) != 0);
+            tc::mma_tf32(d, dah, dbl, idesc, 1u);
+            tc::mma_tf32(d, dal, dbh, idesc, 1u);
           }
           tc::mma_commit(&empty2[s]);
+          if (kc == KC2 - 1) tc::mma_commit(sl == 0 ? acc2 : acc2 + 2);
         }
-        tc::mma_commit(acc2);
       }
       __syncwarp();
     } else {
       // ---------------- epilogue 1: mask, dZ tile into smem (+ global for slice 0)
       const int row = warp * 32 + lane, m = tl.y + row;
       float *stg = stg_all + warp * 32 * T_STG_LD;
+      // the ReLU mask of X_{l-1} for this row as 128 bits, loaded while stage 1 runs
+      uint32_t mbits[F / 32];
+      {
+        const float *xr = Xs + (size_t)(m < row_end ? m : tl.y) * F;  // (rows past the tile: unused)
+#pragma unroll
+        for (int q = 0; q < F / 32; ++q) {
+          uint32_t w = 0;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float4 x = ldg4(xr + q * 32 + 4 * j);
+            w |= (x.x > 0.f ? 1u : 0u) << (4 * j) | (x.y > 0.f ? 2u : 0u) << (4 * j) |
+                 (x.z > 0.f ? 4u : 0u) << (4 * j) | (x.w > 0.f ? 8u : 0u) << (4 * j);
+          }
+          mbits[q] = w;
+        }
+      }
       tc::mbar_wait(acc1, 0);
       tc::fence_after_sync();
       const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
@@ -514,13 +533,13 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
       for (int q = 0; q < F / 32; ++q) {
         float t[32];
         tc::tmem_ld32(trow + (uint32_t)(q * 32), t);
-        const float *xr = Xs + (size_t)(m < row_end ? m : tl.y) * F + q * 32;  // (rows past the tile: unused)
         uint8_t *ch = ring1 + q * 32768;  // dZ chunk q: hi, then lo
+        const uint32_t mb = mbits[q];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-          const float4 x = ldg4(xr + 4 * j);
-          const float4 z = make_float4(x.x > 0.f ? t[4 * j] : 0.f, x.y > 0.f ? t[4 * j + 1] : 0.f,
-                                       x.z > 0.f ? t[4 * j + 2] : 0.f, x.w > 0.f ? t[4 * j + 3] : 0.f);
+          const uint32_t b4 = mb >> (4 * j);
+          const float4 z = make_float4((b4 & 1u) ? t[4 * j] : 0.f, (b4 & 2u) ? t[4 * j + 1] : 0.f,
+                                       (b4 & 4u) ? t[4 * j + 2] : 0.f, (b4 & 8u) ? t[4 * j + 3] : 0.f);
           const uint32_t o = tc::sw128_off(row, j);
           *reinterpret_cast<float4 *>(ch + o) = z;
           *reinterpret_cast<float4 *>(ch + 16384 + o) = lo4(z);
@@ -544,11 +563,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(zrdy);
-      // ---------------- epilogue 2: dA rows (node order)
-      tc::mbar_wait(acc2, 0);
-      tc::fence_after_sync();
+      // ---------------- epilogue 2: dA rows (node order), slice by slice
 #pragma unroll 1
-      for (int q = 0; q < 128 / 32; ++q) {
+      for (int q = 0; q < XD_NS * 4; ++q) {
+        const int sl = q / 4;
+        if ((q & 3) == 0) {
+          tc::mbar_wait(sl == 0 ? acc2 : acc2 + 2, 0);
+          tc::fence_after_sync();
+        }
         float a[32];
         tc::tmem_ld32(trow + 128u + (uint32_t)(q * 32), a);
 #pragma unroll
@@ -578,7 +600,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
   __syncthreads();
   if (warp == T_MMA_WARP) {
     tc::fence_after_sync();
-    tc::tmem_dealloc<256>(tmem);
+    tc::tmem_dealloc<512>(tmem);
   }
 }
 
@@ -1045,7 +1067,7 @@ void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, co
   const DxDaMaps mp{map2d(dP_s, c.maxN, c.H, 128), map2d(dP_s_lo, c.maxN, c.H, 128), map2d(MxT, 128, c.H, 128),
                     map2d(MxT_lo, 128, c.H, 128), map2d(WbT, (uint64_t)cmax * 4 * c.H, 128, 128),
                     map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, 128, 128)};
-  const int grid = tc_max_tiles(c, cmax) * (4 * c.H / 128);
+  const int grid = tc_max_tiles(c, cmax) * (4 * c.H / (128 * XD_NS));
   launch_ex(k_dxda, grid, T_THREADS, XD_SMEM, st, mp, perm, info, tiles, Xs, dZ, dZ_lo, dA, c.H);
   g_launches += 1;
 }
