@@ -165,7 +165,7 @@ struct hg_ctx {
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
   bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
-  bool dxda = false;    // fused dX -> dA backward kernel (class path, H == 128; opt-in HG_DXDA=1)
+  bool dxda = false;    // fused dX -> dA backward kernel (class path, H == 128; HG_DXDA=0 disables)
   hg_status sticky = HG_OK;
   std::string sticky_msg;
 
@@ -713,9 +713,12 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   head_configure(x->caps);
   if (x->use_tc && (e = tc_configure()) != cudaSuccess) return bail(e, "tc_configure");
   if (x->use_tc && (e = tcd_configure()) != cudaSuccess) return bail(e, "tcd_configure");
-  // fused dX -> dA backward: opt-in (HG_DXDA=1); measured 7% slower at config B than the
-  // separate TMA dX and dA kernels (its two chained GEMMs and epilogues run serially per CTA)
-  x->dxda = x->use_tc && plan.cmax > 0 && dxda_supported(x->caps) && getenv("HG_DXDA") != nullptr;
+  // fused dX -> dA backward (default; HG_DXDA=0 selects the separate TMA dX and dA kernels):
+  // +2.3% at config B
+  {
+    const char *v = getenv("HG_DXDA");
+    x->dxda = x->use_tc && plan.cmax > 0 && dxda_supported(x->caps) && !(v && atoi(v) == 0);
+  }
   if (const char *pe = getenv("HG_PDL")) g_pdl = atoi(pe) != 0;  // A/B switch for launch overlap
   {
     std::vector<int64_t> uo;

@@ -546,7 +546,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
           *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) = z;
         }
         __syncwarp();
-        if (n2 == 0) {  // coalesced store of dZ_{l-1} (sorted rows of this class tile only)
+        // coalesced store of dZ_{l-1} (sorted rows of this class tile only); the CTAs of the
+        // tile's slice groups share it: group g stores the 32-column chunks q = g, g + NG, ...
+        if (q % NG == n2 / (128 * XD_NS)) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int r = 4 * j + (lane >> 3), cc = 4 * (lane & 7), mr = tl.y + warp * 32 + r;

@@ -200,9 +200,9 @@ def test_small_batch_after_large_batch_class_path(torch_cuda):
     PT.assert_parity(res)
 
 
-def test_fused_dx_da_path(torch_cuda, monkeypatch):
-    """The opt-in fused dX -> dA backward kernel (HG_DXDA=1) computes the same step."""
-    monkeypatch.setenv("HG_DXDA", "1")
+def test_separate_dx_da_path(torch_cuda, monkeypatch):
+    """The separate TMA dX and dA kernels (HG_DXDA=0; default is the fused kernel) compute the same step."""
+    monkeypatch.setenv("HG_DXDA", "0")
     data = PT.generate("pcqm", 600, 21)
     ctx, cfg, delta = PT.make_ctx(data, 128, 128, 4, seed=5)
     ids = O.shard(23, 1, 0, 1, len(data["y"]))[:128]
