@@ -41,6 +41,7 @@ struct Plan {
   size_t Wf_lo = 0, WbT_lo = 0, ones = 0, xpad = 0, xpad_lo = 0;
   std::vector<size_t> A_lo, X_lo;  // per layer (the backward Grams read them)
   std::vector<size_t> Xs, Xs_lo;   // per layer: X_l in degree-sorted rows (fused dX->dA path)
+  std::vector<size_t> Xmask;       // per layer: ReLU mask bits of X_l, sorted rows, [N][H/32]
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t total = 0;
 };
@@ -109,6 +110,7 @@ Plan make_plan(const hg_config &c) {
       p.X_lo.push_back(take(sizeof(float) * N * H));
       p.Xs.push_back(take(sizeof(float) * N * H));
       p.Xs_lo.push_back(take(sizeof(float) * N * H));
+      p.Xmask.push_back(take(sizeof(uint32_t) * N * ((H + 31) / 32)));
     }
     p.ones = take(sizeof(float) * N * 32);  // B operand of the column-sum tiles
     if (pad_x0_width(c.f_node) <= 256) {      // layer-0 features for the TMA dM_x Gram
@@ -337,7 +339,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
                             x->f(p.Wf) + (size_t)l * p.cmax * 4 * HH, x->f(p.Wf_lo) + (size_t)l * p.cmax * 4 * HH,
                             x->param(lname(l, "b_U")), x->f(p.X[l]), x->f(p.X_lo[l]),
                             x->dxda && l + 1 < c.layers ? x->f(p.Xs[l]) : nullptr,
-                            x->dxda && l + 1 < c.layers ? x->f(p.Xs_lo[l]) : nullptr);
+                            x->dxda && l + 1 < c.layers ? x->f(p.Xs_lo[l]) : nullptr,
+                            x->dxda && l + 1 < c.layers ? reinterpret_cast<uint32_t *>(x->b(p.Xmask[l])) : nullptr);
       else if (x->use_tc)
         launch_tc_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")),
                          x->param(lname(l, "b_U")), x->f(p.X[l]));
@@ -490,7 +493,8 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
           launch_dxda(st, x->caps, p.cmax, dP, dPlo, x->f(p.MxT) + (size_t)(l - 1) * HH,
                       x->f(p.MxT_lo) + (size_t)(l - 1) * HH, x->f(p.WbT) + (size_t)(l - 1) * p.cmax * 4 * HH,
                       x->f(p.WbT_lo) + (size_t)(l - 1) * p.cmax * 4 * HH, perm, dinfo,
-                      reinterpret_cast<const int4 *>(x->b(p.tiles)), x->f(p.Xs[l - 1]), dZn, dZnl, x->f(p.dA));
+                      reinterpret_cast<const int4 *>(x->b(p.tiles)),
+                      reinterpret_cast<const uint32_t *>(x->b(p.Xmask[l - 1])), dZn, dZnl, x->f(p.dA));
         else if (cls)
           launch_d_dX(st, x->caps, blob, dP, dPlo, x->f(p.MxT) + (size_t)(l - 1) * HH,
                       x->f(p.MxT_lo) + (size_t)(l - 1) * HH, F, Xl, dZn, dZnl, pos);

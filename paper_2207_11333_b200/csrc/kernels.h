@@ -116,7 +116,8 @@ cudaError_t tcd_configure();
 // (X1s, X1s_lo optional: also write the output rows in degree-sorted order)
 void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
-                         float *X1, float *X1_lo, float *X1s = nullptr, float *X1s_lo = nullptr);
+                         float *X1, float *X1_lo, float *X1s = nullptr, float *X1s_lo = nullptr,
+                         uint32_t *X1mask = nullptr);
 void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
                      const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA);
 void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
@@ -129,7 +130,7 @@ void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const floa
 bool dxda_supported(const Caps &c);
 void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *dP_s_lo, const float *MxT,
                  const float *MxT_lo, const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info,
-                 const int4 *tiles, const float *Xs, float *dZ, float *dZ_lo, float *dA);
+                 const int4 *tiles, const uint32_t *Xmask, float *dZ, float *dZ_lo, float *dA);
 void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,
                     float *Mx_lo, float *MxT, float *MxT_lo);
 // layers [l0, l1) of the degree-slot weights

@@ -267,6 +267,7 @@ struct TUpdC {
   static constexpr int BN = BN_, ID = 0;
   const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1, *X1_lo; int H; int items_cap;
   float *X1s, *X1s_lo;  // optional: the same rows in degree-sorted order (backward dX/dM_x operands)
+  uint32_t *X1mask;     // optional: ReLU mask bits of the sorted rows, [rows][H/32] words
   int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     const int nt = H / BN, ti = t / nt;
@@ -282,11 +283,20 @@ struct TUpdC {
   struct Pre { int node; float4 b; };
   __device__ Pre pre(int m, int n) const { return Pre{m < row_end ? perm[m] : 0, ldg4(bU + n)}; }
   __device__ void emit(int m, int n, float4 v, const Pre &p) const {
-    if (m >= row_end) return;
-    const size_t o = (size_t)p.node * H + n;
     const float4 b = p.b;
     const float4 z = make_float4(fmaxf(v.x + b.x, 0.f), fmaxf(v.y + b.y, 0.f), fmaxf(v.z + b.z, 0.f),
                                  fmaxf(v.w + b.w, 0.f));
+    if (X1mask) {  // the 8 lanes of a row hold 32 consecutive columns: gather their 4-bit nibbles
+      const int lane = threadIdx.x & 31;
+      uint32_t w = ((z.x > 0.f ? 1u : 0u) | (z.y > 0.f ? 2u : 0u) | (z.z > 0.f ? 4u : 0u) | (z.w > 0.f ? 8u : 0u))
+                   << (4 * (lane & 7));
+      w |= __shfl_xor_sync(0xffffffffu, w, 1);
+      w |= __shfl_xor_sync(0xffffffffu, w, 2);
+      w |= __shfl_xor_sync(0xffffffffu, w, 4);
+      if ((lane & 7) == 0 && m < row_end) X1mask[(size_t)m * (H / 32) + n / 32] = w;
+    }
+    if (m >= row_end) return;
+    const size_t o = (size_t)p.node * H + n;
     *reinterpret_cast<float4 *>(X1 + o) = z;
     const float4 zl = lo4(z);
     *reinterpret_cast<float4 *>(X1_lo + o) = zl;
@@ -399,8 +409,9 @@ struct SkTraceOp5 {
   static constexpr int ID = 5;
 };
 __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ DxDaMaps mp, const int *perm,
-                                                       const DegInfo *info, const int4 *tiles, const float *Xs,
-                                                       float *dZ, float *dZ_lo, float *dA, int H) {
+                                                       const DegInfo *info, const int4 *tiles,
+                                                       const uint32_t *Xmask, float *dZ, float *dZ_lo, float *dA,
+                                                       int H) {
   using Op = SkTraceOp5;
   constexpr int F = 128;  // dZ width (= H, checked by the launcher)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -433,6 +444,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_holder;  // cols [0,128): T, [128 + 128 s, ...): dA slice s
   pdl_enter();
+  if (threadIdx.x == 0) TTRACE(1);
   const int NG = 4 * H / (128 * XD_NS), ti = blockIdx.x / NG, n2 = (blockIdx.x % NG) * 128 * XD_NS;
   if (ti < info->T) {  // uniform per CTA
     const int4 tl = tiles[ti];
@@ -510,24 +522,19 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
       // ---------------- epilogue 1: mask, dZ tile into smem (+ global for slice 0)
       const int row = warp * 32 + lane, m = tl.y + row;
       float *stg = stg_all + warp * 32 * T_STG_LD;
-      // the ReLU mask of X_{l-1} for this row as 128 bits, loaded while stage 1 runs
+      // the ReLU mask of X_{l-1} for this row: 128 bits written by layer l-1's update epilogue
       uint32_t mbits[F / 32];
       {
-        const float *xr = Xs + (size_t)(m < row_end ? m : tl.y) * F;  // (rows past the tile: unused)
-#pragma unroll
-        for (int q = 0; q < F / 32; ++q) {
-          uint32_t w = 0;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const float4 x = ldg4(xr + q * 32 + 4 * j);
-            w |= (x.x > 0.f ? 1u : 0u) << (4 * j) | (x.y > 0.f ? 2u : 0u) << (4 * j) |
-                 (x.z > 0.f ? 4u : 0u) << (4 * j) | (x.w > 0.f ? 8u : 0u) << (4 * j);
-          }
-          mbits[q] = w;
-        }
+        const uint4 mw = __ldg(reinterpret_cast<const uint4 *>(Xmask) + (m < row_end ? m : tl.y));
+        mbits[0] = mw.x;
+        mbits[1] = mw.y;
+        mbits[2] = mw.z;
+        mbits[3] = mw.w;
       }
+      if (threadIdx.x == 0) TTRACE(2);
       tc::mbar_wait(acc1, 0);
       tc::fence_after_sync();
+      if (threadIdx.x == 0) TTRACE(3);
       const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
       for (int q = 0; q < F / 32; ++q) {
@@ -565,13 +572,21 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(zrdy);
+      if (threadIdx.x == 0) TTRACE(4);
       // ---------------- epilogue 2: dA rows (node order), slice by slice
+      int node[8];  // the 8 rows this lane stores, resolved once for every column chunk
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int mr = tl.y + warp * 32 + 4 * j + (lane >> 3);
+        node[j] = mr < row_end ? perm[mr] : -1;
+      }
 #pragma unroll 1
       for (int q = 0; q < XD_NS * 4; ++q) {
         const int sl = q / 4;
         if ((q & 3) == 0) {
           tc::mbar_wait(sl == 0 ? acc2 : acc2 + 2, 0);
           tc::fence_after_sync();
+          if (threadIdx.x == 0 && sl == 0) TTRACE(5);
         }
         float a[32];
         tc::tmem_ld32(trow + 128u + (uint32_t)(q * 32), a);
@@ -580,12 +595,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
           *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) =
               make_float4(a[4 * j], a[4 * j + 1], a[4 * j + 2], a[4 * j + 3]);
         __syncwarp();
-        int node[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int mr = tl.y + warp * 32 + 4 * j + (lane >> 3);
-          node[j] = mr < row_end ? perm[mr] : -1;
-        }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
           const int r = 4 * j + (lane >> 3), cc = 4 * (lane & 7);
@@ -595,7 +604,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
         }
         __syncwarp();
       }
-      if (threadIdx.x == 0) TTRACE(6);
+      if (threadIdx.x == 0) {
+        TTRACE(6);
+        if (g_trace && g_trace_id == Op::ID) g_trace[blockIdx.x * 8 + 7] = 1;  // (valid CTA)
+      }
     }
   }
   tc::fence_before_sync();
@@ -945,11 +957,11 @@ cudaError_t tconfigure_bn() {
 template <int BN>
 void update_bn(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU, float *X1,
-               float *X1_lo, float *X1s, float *X1s_lo) {
+               float *X1_lo, float *X1s, float *X1s_lo, uint32_t *X1mask) {
   const int K = 4 * c.H;
   const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, BN),
                    map2d(Wf_lo, (uint64_t)cmax * c.H, K, BN)};
-  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0, X1s, X1s_lo, 0};
+  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0, X1s, X1s_lo, X1mask, 0};
   trun(st, mp, op, tc_max_tiles(c, cmax) * (c.H / BN));
 }
 template <int BN>
@@ -1008,7 +1020,7 @@ cudaError_t tcd_configure() {
 
 void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
-                         float *X1, float *X1_lo, float *X1s, float *X1s_lo) {
+                         float *X1, float *X1_lo, float *X1s, float *X1s_lo, uint32_t *X1mask) {
   if (g_update_sk && c.H == SK_H && !X1s) {
     const int K = 4 * c.H;
     const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, SK_H),
@@ -1033,10 +1045,11 @@ void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *
     g_launches += 1;
     return;
   }
-  if (g_bn_upd == 32) update_bn<32>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo);
+  if (g_bn_upd == 32)
+    update_bn<32>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
   else if (g_bn_upd == 128)
-    update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo);
-  else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo);
+    update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
+  else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
 }
 
 void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
@@ -1065,12 +1078,12 @@ bool dxda_supported(const Caps &c) { return c.H == 128; }
 
 void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *dP_s_lo, const float *MxT,
                  const float *MxT_lo, const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info,
-                 const int4 *tiles, const float *Xs, float *dZ, float *dZ_lo, float *dA) {
+                 const int4 *tiles, const uint32_t *Xmask, float *dZ, float *dZ_lo, float *dA) {
   const DxDaMaps mp{map2d(dP_s, c.maxN, c.H, 128), map2d(dP_s_lo, c.maxN, c.H, 128), map2d(MxT, 128, c.H, 128),
                     map2d(MxT_lo, 128, c.H, 128), map2d(WbT, (uint64_t)cmax * 4 * c.H, 128, 128),
                     map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, 128, 128)};
   const int grid = tc_max_tiles(c, cmax) * (4 * c.H / (128 * XD_NS));
-  launch_ex(k_dxda, grid, T_THREADS, XD_SMEM, st, mp, perm, info, tiles, Xs, dZ, dZ_lo, dA, c.H);
+  launch_ex(k_dxda, grid, T_THREADS, XD_SMEM, st, mp, perm, info, tiles, Xmask, dZ, dZ_lo, dA, c.H);
   g_launches += 1;
 }
 
