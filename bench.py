@@ -45,6 +45,13 @@ WORKLOADS = {
           "D: AISD HOMO-LUMO-shaped 10.5M synthetic molecules, 6 conv layers hidden 128, batch 512/GPU"),
     "E256": ("aisd", 10_500_000, 512, 256, 8, "E: AISD-shaped, 8 conv layers hidden 256, batch 512/GPU"),
     "E512": ("aisd", 10_500_000, 512, 512, 8, "E: AISD-shaped, 8 conv layers hidden 512, batch 512/GPU"),
+    # the paper's own model widths (channel-padded internally, include/hgnn.h hg_config_internal)
+    "P55": ("pcqm", 3_400_000, 128, 55, 6,
+            "paper scalability model (PAPER.md:315): PCQM4Mv2-shaped 3.4M molecules, 6 PNA layers of 55 neurons, "
+            "local batch 128"),
+    "P200": ("pcqm", 3_400_000, 128, 200, 6,
+             "paper convergence-test width (PAPER.md:318): PCQM4Mv2-shaped 3.4M molecules, 6 PNA layers of 200 "
+             "neurons, local batch 128"),
 }
 
 
@@ -380,6 +387,12 @@ def main():
         "dMx": (Nn * (4 * H + 4 * F0) + NL1 * 8 * H, 2.0 * Nn * H * (F0 + 1) + 2.0 * NL1 * H * (H + 1)),
         "dX": (NL1 * 12 * H, 2.0 * NL1 * H * H),
     }
+    # fused dX -> dA kernel (k_dxda): the dA of layers < L-1 runs inside the dX phase
+    n_da = phases.get("dA", [0.0, L])[1]
+    if "dA" in phases and 0 < n_da < L:
+        (ba, fa), (bx, fx) = work["dA"], work["dX"]
+        work["dA"] = (ba * n_da / L, fa * n_da / L)
+        work["dX"] = (bx + ba * (L - n_da) / L, fx + fa * (L - n_da) / L)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -440,7 +453,8 @@ def main():
         "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "data": "synthetic (molgen seeded molecules, Table-2 calibrated; random-init weights)",
         "config": {"workload": desc, "graphs_in_store": n_graphs, "global_batch": B * world, "batch_per_gpu": B,
-                   "layers": L, "hidden": H, "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
+                   "layers": L, "hidden": H, "hidden_internal": int(ctx.internal_cfg.hidden),
+                   "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
                    "parallelism": f"dp{world}", "resident_batches": n_res,
                    "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
                    "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs, TMA-fed"},

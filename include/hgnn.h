@@ -106,7 +106,8 @@ hg_status hg_shard(uint64_t seed, int64_t epoch, int32_t rank, int32_t world, in
  * ====================================================================== */
 typedef struct {
   int32_t f_node, f_edge;            /* input widths F0, Fe */
-  int32_t hidden;                    /* H: multiple of 32 */
+  int32_t hidden;                    /* H in [1, 1024]; not a multiple of 32 => channel-padded
+                                        internally (hg_config_internal) */
   int32_t layers;                    /* L >= 1 conv layers */
   int32_t fc_hidden;                 /* Hf: head hidden width (= H) */
   int32_t max_graphs;                /* capacity: graphs per batch */
@@ -123,6 +124,20 @@ typedef struct {
 /* hg_config.flags: force the SIMT fp32 GEMMs instead of the tcgen05 3xTF32
  * tensor-core GEMMs (which are used whenever hidden % 128 == 0). */
 #define HG_FLAG_SIMT_GEMM 1
+
+/* Channel padding for widths that are not a multiple of 32, e.g. the paper's
+ * H = 55 and H = 200 (SURVEY §8(d) "Padding hazard").
+ * Writes to *out the configuration the kernels actually run: hidden rounded up
+ * to a multiple of 128 (the tensor-core tile; 32 with HG_FLAG_SIMT_GEMM) and
+ * fc_hidden padded alike when it equals hidden; *out = *c when hidden % 32 == 0.
+ * The padded channels compute exact zeros: padded parameter entries start at
+ * zero, the std aggregator of a padded channel is forced to 0 (not
+ * sqrt(var_floor)), so every padded gradient is exactly zero and AdamW keeps
+ * the padding at zero. Everything public stays logical: hg_param_info, the
+ * params / grads / optimizer-state arenas of get/set are in the layout of *c
+ * (hg_param_layout(c)); only hg_workspace_view buffers are internal-width.
+ * Host-only. Errors: HG_E_INVALID as hg_workspace_bytes. */
+hg_status hg_config_internal(const hg_config *c, hg_config *out);
 
 typedef struct {
   float lr, beta1, beta2, eps, weight_decay;  /* 1e-3, 0.9, 0.999, 1e-8, 0.01 */

@@ -453,9 +453,15 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
     legitimately resolved either way); invalid ones are counted and the
     oracle keeps its own decision, so they show up in the gradient error too.
     tau defaults to the forward tolerance 1e-4 (reading R-replay).
-    Returns (decisions, {'overrides', 'out_of_band', 'out_of_band_by'})."""
-    dec, n, bad = {}, 0, 0
+    Overrides whose two candidates are equal to float64 rounding (|gap| <= 1e-12 of
+    the layer's max, i.e. algebraic ties such as automorphic atoms, where the
+    oracle's own summation order decides) are counted apart as 'tie_overrides'.
+    Returns (decisions, {'overrides', 'tie_overrides', 'overrides_by', 'out_of_band',
+    'out_of_band_by'})."""
+    dec, n, bad, nt = {}, 0, 0, 0
+    TIE = 1e-12
     by = {"relu": 0, "argmax": 0, "argmin": 0, "varflag": 0, "head_relu": 0}
+    ov = dict(by)  # overrides per decision kind (diagnostic)
     for l, (c, gdec) in enumerate(zip(cache["layers"], gpu)):
         zs = np.abs(c["Z"]).max() if c["Z"].size else 0.0
         msg = c["msg"]
@@ -469,7 +475,10 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
             g = np.asarray(gdec["relu"])
             valid = np.where(g, c["Z"] >= -tau * zs, c["Z"] <= tau * zs)
             diff = g != own["relu"]
-            n += int((valid & diff).sum())
+            tie = np.abs(c["Z"]) <= TIE * zs
+            n += int((valid & diff & ~tie).sum())
+            nt += int((valid & diff & tie).sum())
+            ov["relu"] += int((valid & diff).sum())
             nb = int((~valid & diff).sum())
             bad += nb
             by["relu"] += nb
@@ -487,7 +496,10 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
             valid = (sign * (gval - ext) >= -tau * ms) & (g < np.maximum(deg, 1)[:, None])
             valid |= ~has
             diff = (g != own[k]) & has
-            n += int((valid & diff).sum())
+            tie = np.abs(gval - ext) <= TIE * ms
+            n += int((valid & diff & ~tie).sum())
+            nt += int((valid & diff & tie).sum())
+            ov[k] += int((valid & diff).sum())
             nb = int((~valid & diff).sum())
             bad += nb
             by[k] += nb
@@ -497,6 +509,7 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
             band = np.abs(c["var"] - VAR_FLOOR) < 0.5 * VAR_FLOOR
             diff = (g != own["varflag"]) & has
             n += int((band & diff).sum())
+            ov["varflag"] += int((band & diff).sum())
             nb = int((~band & diff).sum())
             bad += nb
             by["varflag"] += nb
@@ -509,12 +522,16 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
         own = hp > 0
         valid = np.where(g, hp >= -tau * hs, hp <= tau * hs)
         diff = g != own
-        n += int((valid & diff).sum())
+        tie = np.abs(hp) <= TIE * hs
+        n += int((valid & diff & ~tie).sum())
+        nt += int((valid & diff & tie).sum())
+        ov["head_relu"] += int((valid & diff).sum())
         nb = int((~valid & diff).sum())
         bad += nb
         by["head_relu"] += nb
         dec["head_relu"] = np.where(valid, g, own)
-    return dec, {"overrides": n, "out_of_band": bad, "out_of_band_by": by}
+    return dec, {"overrides": n, "tie_overrides": nt, "overrides_by": ov, "out_of_band": bad,
+                 "out_of_band_by": by}
 
 
 # ---------------------------------------------------------------- evaluation

@@ -139,11 +139,13 @@ Plan make_plan(const hg_config &c) {
 }  // namespace
 
 struct hg_ctx {
-  hg_config cfg{};
+  hg_config cfg{};    // internal (padded) configuration the kernels run
+  hg_config cfg_l{};  // the caller's configuration (logical widths)
+  bool padded = false;
   Caps caps{};
   Plan plan;
-  std::vector<TensorInfo> lay;
-  int64_t n_params = 0;
+  std::vector<TensorInfo> lay, lay_l;  // device arena layout / public (logical) layout
+  int64_t n_params = 0, n_params_l = 0;
   int device = 0;
   uint8_t *ws = nullptr;
   cudaStream_t stream = nullptr, copy_stream = nullptr, cap_stream = nullptr;
@@ -643,7 +645,7 @@ hg_status hg_workspace_bytes(const hg_config *c, size_t *bytes) {
   hg_status st = check_config(c);
   if (st) return st;
   if (!bytes) return fail(HG_E_INVALID, "null output");
-  *bytes = make_plan(*c).total;
+  *bytes = make_plan(padded_config(*c)).total;
   return HG_OK;
 }
 
@@ -653,6 +655,9 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   if (st) return st;
   if (!out || !workspace) return fail(HG_E_INVALID, "null argument");
   *out = nullptr;
+  const hg_config cl = *c;
+  const hg_config pc = padded_config(cl);
+  c = &pc;
   Plan plan = make_plan(*c);
   if (bytes < plan.total) return fail(HG_E_CAPACITY, "workspace too small: %zu < %zu", bytes, plan.total);
   if (((uintptr_t)workspace & 255) != 0) return fail(HG_E_INVALID, "workspace must be 256-byte aligned");
@@ -660,10 +665,14 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   if (e != cudaSuccess) return cuda_fail(nullptr, e, "cudaSetDevice");
   hg_ctx *x = new hg_ctx();
   x->cfg = *c;
-  x->caps = Caps{c->max_graphs, c->max_nodes, c->max_edges, c->f_node, c->f_edge, c->hidden, c->fc_hidden};
+  x->cfg_l = cl;
+  x->padded = config_is_padded(cl);
+  x->caps = Caps{c->max_graphs, c->max_nodes, c->max_edges, c->f_node, c->f_edge, c->hidden, c->fc_hidden, cl.hidden};
   x->plan = plan;
   x->lay = param_layout(*c);
   x->n_params = param_total(x->lay);
+  x->lay_l = param_layout(cl);
+  x->n_params_l = param_total(x->lay_l);
   x->device = device;
   x->ws = (uint8_t *)workspace;
   x->stream = (cudaStream_t)stream;
@@ -786,19 +795,19 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
 
 hg_status hg_param_count(const hg_ctx *x, int32_t *n_tensors, int64_t *n_elems) {
   if (!x) return fail(HG_E_INVALID, "null ctx");
-  if (n_tensors) *n_tensors = (int32_t)x->lay.size();
-  if (n_elems) *n_elems = x->n_params;
+  if (n_tensors) *n_tensors = (int32_t)x->lay_l.size();
+  if (n_elems) *n_elems = x->n_params_l;
   return HG_OK;
 }
 
 hg_status hg_param_info(const hg_ctx *x, int32_t i, const char **name, int64_t *offset, int32_t *rows,
                         int32_t *cols) {
   if (!x) return fail(HG_E_INVALID, "null ctx");
-  if (i < 0 || i >= (int32_t)x->lay.size()) return fail(HG_E_RANGE, "tensor index out of range");
-  if (name) *name = x->lay[i].name.c_str();
-  if (offset) *offset = x->lay[i].offset;
-  if (rows) *rows = x->lay[i].rows;
-  if (cols) *cols = x->lay[i].cols;
+  if (i < 0 || i >= (int32_t)x->lay_l.size()) return fail(HG_E_RANGE, "tensor index out of range");
+  if (name) *name = x->lay_l[i].name.c_str();
+  if (offset) *offset = x->lay_l[i].offset;
+  if (rows) *rows = x->lay_l[i].rows;
+  if (cols) *cols = x->lay_l[i].cols;
   return HG_OK;
 }
 
@@ -809,11 +818,44 @@ static hg_status copy_arena(hg_ctx *x, void *dst, const void *src, size_t bytes,
   return HG_OK;
 }
 
+// public (logical) arena -> device arena / device arena -> public arena; a padded
+// configuration goes through host copies (parameter I/O is not on the step path)
+static hg_status arena_in(hg_ctx *x, float *dev, const float *src, int on_device) {
+  if (!x->padded) return copy_arena(x, dev, src, sizeof(float) * (size_t)x->n_params, on_device, true);
+  std::vector<float> hl((size_t)x->n_params_l), hp((size_t)x->n_params, 0.f);
+  if (on_device) {
+    hg_status st = copy_arena(x, hl.data(), src, sizeof(float) * hl.size(), 0, false);
+    if (st) return st;
+  } else {
+    std::memcpy(hl.data(), src, sizeof(float) * hl.size());
+  }
+  arena_pad(x->cfg_l, hl.data(), hp.data());
+  return copy_arena(x, dev, hp.data(), sizeof(float) * hp.size(), 0, true);
+}
+static hg_status arena_out(hg_ctx *x, float *dst, const float *dev, int on_device) {
+  if (!x->padded) return copy_arena(x, dst, dev, sizeof(float) * (size_t)x->n_params, on_device, false);
+  std::vector<float> hl((size_t)x->n_params_l), hp((size_t)x->n_params);
+  hg_status st = copy_arena(x, hp.data(), dev, sizeof(float) * hp.size(), 0, false);
+  if (st) return st;
+  arena_unpad(x->cfg_l, hp.data(), hl.data());
+  if (!on_device) {
+    std::memcpy(dst, hl.data(), sizeof(float) * hl.size());
+    return HG_OK;
+  }
+  return copy_arena(x, dst, hl.data(), sizeof(float) * hl.size(), 0, true);
+}
+
 hg_status hg_params_init(hg_ctx *x, uint64_t seed) {
   hg_status st = usable(x);
   if (st) return st;
-  std::vector<float> h((size_t)x->n_params);
-  init_params_host(x->cfg, seed, h.data());
+  std::vector<float> h((size_t)x->n_params, 0.f);
+  if (x->padded) {
+    std::vector<float> hl((size_t)x->n_params_l);
+    init_params_host(x->cfg_l, seed, hl.data());
+    arena_pad(x->cfg_l, hl.data(), h.data());
+  } else {
+    init_params_host(x->cfg, seed, h.data());
+  }
   const size_t PB = sizeof(float) * (size_t)x->n_params;
   CK(x, cudaMemcpyAsync(x->f(x->plan.params), h.data(), PB, cudaMemcpyHostToDevice, x->stream));
   CK(x, cudaMemsetAsync(x->f(x->plan.m), 0, PB, x->stream));
@@ -828,29 +870,28 @@ hg_status hg_params_set(hg_ctx *x, const float *src, int32_t on_device) {
   hg_status st = usable(x);
   if (st) return st;
   if (!src) return fail(HG_E_INVALID, "null source");
-  return copy_arena(x, x->f(x->plan.params), src, sizeof(float) * (size_t)x->n_params, on_device, true);
+  return arena_in(x, x->f(x->plan.params), src, on_device);
 }
 
 hg_status hg_params_get(hg_ctx *x, float *dst, int32_t on_device) {
   hg_status st = usable(x);
   if (st) return st;
   if (!dst) return fail(HG_E_INVALID, "null destination");
-  return copy_arena(x, dst, x->f(x->plan.params), sizeof(float) * (size_t)x->n_params, on_device, false);
+  return arena_out(x, dst, x->f(x->plan.params), on_device);
 }
 
 hg_status hg_grads_get(hg_ctx *x, float *dst, int32_t on_device) {
   hg_status st = usable(x);
   if (st) return st;
   if (!dst) return fail(HG_E_INVALID, "null destination");
-  return copy_arena(x, dst, x->f(x->plan.grads), sizeof(float) * (size_t)x->n_params, on_device, false);
+  return arena_out(x, dst, x->f(x->plan.grads), on_device);
 }
 
 hg_status hg_opt_state_get(hg_ctx *x, float *m, float *v, int64_t *step, int32_t on_device) {
   hg_status st = usable(x);
   if (st) return st;
-  const size_t PB = sizeof(float) * (size_t)x->n_params;
-  if (m && (st = copy_arena(x, m, x->f(x->plan.m), PB, on_device, false))) return st;
-  if (v && (st = copy_arena(x, v, x->f(x->plan.v), PB, on_device, false))) return st;
+  if (m && (st = arena_out(x, m, x->f(x->plan.m), on_device))) return st;
+  if (v && (st = arena_out(x, v, x->f(x->plan.v), on_device))) return st;
   if (step) {
     AdamDev ad;
     CK(x, cudaMemcpyAsync(&ad, x->b(x->plan.adam), sizeof(ad), cudaMemcpyDeviceToHost, x->stream));
@@ -863,9 +904,8 @@ hg_status hg_opt_state_get(hg_ctx *x, float *m, float *v, int64_t *step, int32_t
 hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t step, int32_t on_device) {
   hg_status st = usable(x);
   if (st) return st;
-  const size_t PB = sizeof(float) * (size_t)x->n_params;
-  if (m && (st = copy_arena(x, x->f(x->plan.m), m, PB, on_device, true))) return st;
-  if (v && (st = copy_arena(x, x->f(x->plan.v), v, PB, on_device, true))) return st;
+  if (m && (st = arena_in(x, x->f(x->plan.m), m, on_device))) return st;
+  if (v && (st = arena_in(x, x->f(x->plan.v), v, on_device))) return st;
   AdamDev ad{step, 0, 0};
   CK(x, cudaMemcpyAsync(x->b(x->plan.adam), &ad, sizeof(ad), cudaMemcpyHostToDevice, x->stream));
   CK(x, cudaStreamSynchronize(x->stream));

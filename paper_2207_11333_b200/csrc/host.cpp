@@ -108,8 +108,8 @@ hg_status check_config(const hg_config *c) {
   if (!c) return fail(HG_E_INVALID, "null config");
   if (c->f_node < 1 || c->f_edge < 1 || c->layers < 1 || c->fc_hidden < 1)
     return fail(HG_E_INVALID, "config widths must be positive");
-  if (c->hidden < 32 || c->hidden % 32 != 0 || c->hidden > 1024)
-    return fail(HG_E_INVALID, "hidden must be a multiple of 32 in [32, 1024] (got %d)", c->hidden);
+  if (c->hidden < 1 || c->hidden > 1024)
+    return fail(HG_E_INVALID, "hidden must be in [1, 1024] (got %d)", c->hidden);
   if (c->fc_hidden > 1024) return fail(HG_E_INVALID, "fc_hidden must be <= 1024");
   if (c->f_edge > 8) return fail(HG_E_INVALID, "f_edge must be <= 8");
   if (c->max_graphs < 1 || c->max_nodes < 1 || c->max_edges < 0 || c->n_slots < 1)
@@ -119,6 +119,39 @@ hg_status check_config(const hg_config *c) {
   if (c->max_degree < 0 || c->max_degree > HG_MAX_DEGREE) return fail(HG_E_INVALID, "max_degree out of range");
   return HG_OK;
 }
+
+bool config_is_padded(const hg_config &c) { return c.hidden % 32 != 0; }
+
+hg_config padded_config(const hg_config &c) {
+  if (!config_is_padded(c)) return c;
+  hg_config p = c;
+  const int q = (c.flags & HG_FLAG_SIMT_GEMM) ? 32 : 128;
+  p.hidden = (c.hidden + q - 1) / q * q;
+  if (c.fc_hidden == c.hidden) p.fc_hidden = p.hidden;
+  return p;
+}
+
+// Per tensor: logical [R, nb*W] -> padded [Rp, nb*Wp]; column j = q*W + c maps to
+// q*Wp + c (nb = 12 column blocks for U: (s*4+a)*H + c), rows r -> r.
+static void arena_map(const hg_config &logical, const float *src, float *dst, bool to_padded) {
+  const hg_config pc = padded_config(logical);
+  const auto ll = param_layout(logical), lp = param_layout(pc);
+  for (size_t t = 0; t < ll.size(); ++t) {
+    const TensorInfo &a = ll[t], &b = lp[t];
+    const int nb = a.name.size() >= 2 && a.name.compare(a.name.size() - 2, 2, ".U") == 0 ? 12 : 1;
+    const int W = a.cols / nb, Wp = b.cols / nb;
+    for (int r = 0; r < a.rows; ++r)
+      for (int q = 0; q < nb; ++q)
+        for (int c = 0; c < W; ++c) {
+          const int64_t li = a.offset + (int64_t)r * a.cols + (int64_t)q * W + c;
+          const int64_t pi = b.offset + (int64_t)r * b.cols + (int64_t)q * Wp + c;
+          if (to_padded) dst[pi] = src[li];
+          else dst[li] = src[pi];
+        }
+  }
+}
+void arena_pad(const hg_config &logical, const float *src, float *dst) { arena_map(logical, src, dst, true); }
+void arena_unpad(const hg_config &logical, const float *src, float *dst) { arena_map(logical, src, dst, false); }
 
 void init_params_host(const hg_config &c, uint64_t seed, float *dst) {
   auto lay = param_layout(c);
@@ -399,6 +432,14 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
     return fail(HG_E_CAPACITY, "graph %lld has a node of degree %lld > max_degree %d", (long long)ids[bad_b],
                 (long long)bad_deg, maxdeg);
   if (used) *used = (size_t)o.total;
+  return HG_OK;
+}
+
+hg_status hg_config_internal(const hg_config *c, hg_config *out) {
+  hg_status st = check_config(c);
+  if (st) return st;
+  if (!out) return fail(HG_E_INVALID, "null output");
+  *out = padded_config(*c);
   return HG_OK;
 }
 

@@ -23,6 +23,20 @@ int64_t param_total(const std::vector<TensorInfo> &v);
 hg_status check_config(const hg_config *c);
 void init_params_host(const hg_config &c, uint64_t seed, float *dst);
 
+// Channel padding (SURVEY §8(d) "Padding hazard"; paper widths H = 55, 200 at
+// PAPER.md:315, 318). A hidden width that is not a multiple of 32 runs internally
+// at Hp = roundup(H, 128) (tensor-core path; roundup(H, 32) with HG_FLAG_SIMT_GEMM),
+// fc_hidden == H padded alike. The padded parameter entries are zero and stay zero
+// (their gradients are exactly zero: the aggregation kernel writes zero aggregates
+// for padded channels, see launch_agg_fwd), so the padded model computes the
+// logical one exactly. The public arena (hg_param_info, get/set) stays logical.
+hg_config padded_config(const hg_config &c);
+bool config_is_padded(const hg_config &c);
+// scatter a logical arena (layout of `logical`) into a zeroed padded arena
+// (layout of padded_config(logical)), or gather it back
+void arena_pad(const hg_config &logical, const float *src, float *dst);
+void arena_unpad(const hg_config &logical, const float *src, float *dst);
+
 }  // namespace hg
 
 // Table-1 store: global arrays + per-graph offsets, plus the

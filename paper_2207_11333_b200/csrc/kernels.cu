@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
                                                     const float *__restrict__ Me, const float *__restrict__ bM,
                                                     float var_floor, float *__restrict__ A,
                                                     uint8_t *__restrict__ arg, int H, float *__restrict__ A_lo,
-                                                    const int *__restrict__ pos) {
+                                                    const int *__restrict__ pos, int Hl) {
   pdl_enter();
   const BatchView b = load_batch(blob);
   const int lane = threadIdx.x & 31;
@@ -455,7 +455,10 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
       for (int c = 0; c < CPL; ++c) {
         const float var = ss[c] / fd;
         flag[c] = var > var_floor;
-        sd[c] = sqrtf(fmaxf(var, var_floor));
+        // channels >= Hl are padding (internal width H > logical Hl): their messages are
+        // exactly 0, and their std is forced to 0 instead of sqrt(var_floor) so that no
+        // gradient reaches the zero padded parameters (SURVEY §8(d) padding hazard)
+        sd[c] = ch + c < Hl ? sqrtf(fmaxf(var, var_floor)) : 0.f;
       }
     }
     const size_t arow = (size_t)(pos ? pos[i] : i) * 4 * H + ch;  // degree-sorted row when pos is given
@@ -495,7 +498,8 @@ template <int CPL, int FE>
 static void agg_fwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                            const float *bM, float var_floor, float *A, uint8_t *arg, float *A_lo, const int *pos) {
   const dim3 grid(std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 4)), c.H / (32 * CPL));
-  launch_ex(k_agg_fwd<CPL, FE>, grid, 256, 0, st, blob, P, Me, bM, var_floor, A, arg, c.H, A_lo, pos);
+  launch_ex(k_agg_fwd<CPL, FE>, grid, 256, 0, st, blob, P, Me, bM, var_floor, A, arg, c.H, A_lo, pos,
+            c.Hl > 0 ? c.Hl : c.H);
 }
 
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,

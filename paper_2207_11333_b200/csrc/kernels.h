@@ -14,6 +14,7 @@ extern int g_prio_lo, g_prio_hi;  // launch kernels with programmatic dependent 
 struct Caps {
   int maxB, maxN, maxE;
   int F0, Fe, H, Hf;
+  int Hl = 0;  // logical hidden width (< H when the configuration is channel-padded; 0 = H)
 };
 
 // per-node degree scalers amp = ln(d+1)/delta, att = delta/ln(d+1) (1 for d=0)

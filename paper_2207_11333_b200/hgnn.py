@@ -81,6 +81,7 @@ SIGNATURES = {
     "hg_shard": [_U64, _I64, _I32, _I32, _I64, _P, _I64P],
     "hg_batch_offsets_get": [_I32, _I32, _I32, _I32, _I32, ctypes.POINTER(hg_batch_offsets_t)],
     "hg_pack_host": [_P, _P, _I32, ctypes.POINTER(hg_config), _P, _SZ, _SZP],
+    "hg_config_internal": [ctypes.POINTER(hg_config), ctypes.POINTER(hg_config)],
     "hg_param_layout": [ctypes.POINTER(hg_config), _I32P, _I64P],
     "hg_param_layout_info": [ctypes.POINTER(hg_config), _I32, _CP, _I64P, _I32P, _I32P],
     "hg_params_init_host": [ctypes.POINTER(hg_config), _U64, _P],
@@ -334,6 +335,14 @@ def hg_param_layout(cfg: hg_config):
     return out, ne.value
 
 
+def hg_config_internal(cfg: hg_config) -> hg_config:
+    """The configuration the kernels run (channel-padded when hidden % 32 != 0)."""
+    load()
+    out = hg_config()
+    _check(_lib.hg_config_internal(ctypes.byref(cfg), ctypes.byref(out)))
+    return out
+
+
 def hg_params_init_host(cfg: hg_config, seed: int) -> np.ndarray:
     load()
     _, total = hg_param_layout(cfg)
@@ -379,6 +388,7 @@ class Context:
                                   ctypes.c_void_p(self.stream.cuda_stream), ctypes.byref(h)))
         self.handle = h
         self.layout, self.n_params = hg_param_layout(cfg)
+        self.internal_cfg = hg_config_internal(cfg)  # widths of the workspace views
 
     def __del__(self):
         if getattr(self, "handle", None) and _lib is not None:

@@ -32,14 +32,21 @@ def oracle_cfg(cfg):
             "fc_hidden": cfg.fc_hidden, "var_floor": float(np.float32(cfg.var_floor))}
 
 
+def gpu_X(ctx, l, N, H):
+    """X_{l+1} [N, H] (the logical channels of the internal-width workspace view)."""
+    Hp = ctx.internal_cfg.hidden
+    return ctx.view_f32(hgnn.VIEW_X, l)[:N * Hp].cpu().numpy().reshape(N, Hp)[:, :H]
+
+
 def gpu_decisions(ctx, N, H, L):
     dec = []
+    Hp = ctx.internal_cfg.hidden
     for l in range(L):
-        arg = ctx.view(hgnn.VIEW_ARG, l)[:N * 2 * H].cpu().numpy().reshape(N, 2 * H)
-        X = ctx.view_f32(hgnn.VIEW_X, l)[:N * H].cpu().numpy().reshape(N, H)
+        arg = ctx.view(hgnn.VIEW_ARG, l)[:N * 2 * Hp].cpu().numpy().reshape(N, 2 * Hp)
+        X = gpu_X(ctx, l, N, H)
         amn = arg[:, :H].astype(np.int64)
-        amx = (arg[:, H:] & 0x7F).astype(np.int64)
-        flag = (arg[:, H:] & 0x80) != 0
+        amx = (arg[:, Hp:Hp + H] & 0x7F).astype(np.int64)
+        flag = (arg[:, Hp:Hp + H] & 0x80) != 0
         dec.append(dict(relu=X > 0, argmax=amx, argmin=amn, varflag=flag))
     return dec
 
@@ -80,13 +87,16 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
         res["loss"] = abs(gl - loss) / max(abs(loss), 1e-30)
     xs = []
     for l in range(L):
-        X = ctx.view_f32(hgnn.VIEW_X, l)[:N * H].cpu().numpy().reshape(N, H)
+        X = gpu_X(ctx, l, N, H)
         ref = np.maximum(cache["layers"][l]["Z"], 0)
         xs.append(float(np.abs(X - ref).max() / max(np.abs(ref).max(), 1e-30)))
     res["X"] = max(xs)
-    hpre = ctx.view_f32(hgnn.VIEW_HPRE)[:B * cfg.fc_hidden].cpu().numpy().reshape(B, cfg.fc_hidden)
+    Hfp = ctx.internal_cfg.fc_hidden
+    hpre = ctx.view_f32(hgnn.VIEW_HPRE)[:B * Hfp].cpu().numpy().reshape(B, Hfp)[:, :cfg.fc_hidden]
     dec, counts = O.replay(cache, gpu_decisions(ctx, N, H, L), head_relu_gpu=hpre > 0)
     res["overrides"] = counts["overrides"]
+    res["overrides_by"] = counts["overrides_by"]
+    res["tie_overrides"] = counts["tie_overrides"]
     res["out_of_band"] = counts["out_of_band"]
     res["out_of_band_by"] = counts["out_of_band_by"]
     res["cells"] = int(sum(c["Z"].size * 4 for c in cache["layers"]))
@@ -135,7 +145,9 @@ def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
         bad.append(("X", res["X"]))
     # GPU discrete decisions (ReLU masks, argmin/argmax, std floor) must agree with the
     # oracle wherever the oracle's margin exceeds tau; in-band
-    # overrides are equally valid choices and only bounded loosely.
+    # overrides are equally valid choices and only bounded loosely; overrides at
+    # algebraic ties (tie_overrides: candidates equal to float64 rounding, where the
+    # oracle's own summation order picks the position) are not bounded.
     if res["out_of_band"] > max(2, 1e-5 * res["cells"]):
         bad.append(("out_of_band", res["out_of_band"], res["out_of_band_by"]))
     if res["overrides"] > 1e-3 * res["cells"]:

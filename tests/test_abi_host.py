@@ -138,6 +138,35 @@ def test_store_stats_and_degree_stat(pcqm):
     assert abs(store.degree_stat(ids) - O.degree_stat(pcqm, ids)) <= 1e-13
 
 
+@pytest.mark.parametrize("H,Hf,flags,Hp,Hfp", [
+    (55, 55, 0, 128, 128),     # paper width -> tensor-core tile
+    (200, 200, 0, 256, 256),   # paper width
+    (55, 55, 1, 64, 64),       # SIMT path pads to the warp width
+    (55, 40, 0, 128, 40),      # fc_hidden != hidden is left as given
+    (128, 128, 0, 128, 128),   # multiples of 32 are not padded
+    (96, 96, 0, 96, 96),
+])
+def test_config_internal_padding(H, Hf, flags, Hp, Hfp):
+    cfg = hgnn.make_config(34, 4, H, 2, 4, 100, 400, 1.0, fc_hidden=Hf, flags=flags)
+    ic = hgnn.hg_config_internal(cfg)
+    assert (ic.hidden, ic.fc_hidden) == (Hp, Hfp)
+    assert (ic.layers, ic.max_nodes, ic.flags) == (cfg.layers, cfg.max_nodes, cfg.flags)
+    # the public arena stays logical: init matches the oracle at the logical width
+    lay, _ = hgnn.hg_param_layout(cfg)
+    flat = hgnn.hg_params_init_host(cfg, 3)
+    ref = O.init_params({"f_node": 34, "f_edge": 4, "hidden": H, "layers": 2, "fc_hidden": Hf}, 3)
+    for name, off, r, c in lay:
+        np.testing.assert_array_equal(flat[off:off + r * c], ref[name].reshape(-1).astype(np.float32), err_msg=name)
+
+
+@pytest.mark.parametrize("H", [0, -3, 1025])
+def test_config_hidden_range(H):
+    cfg = hgnn.make_config(34, 4, H, 2, 4, 100, 400, 1.0, fc_hidden=32)
+    with pytest.raises(hgnn.HgError) as e:
+        hgnn.hg_config_internal(cfg)
+    assert e.value.name == "HG_E_INVALID"
+
+
 @pytest.mark.parametrize("F0,H,L,Hf", [(34, 32, 2, 32), (9, 128, 6, 128), (1, 32, 1, 8)])
 def test_param_init_bit_exact_vs_oracle(F0, H, L, Hf):
     cfg = hgnn.make_config(F0, 4, H, L, 4, 100, 400, 1.0, fc_hidden=Hf)

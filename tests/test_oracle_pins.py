@@ -504,7 +504,7 @@ def test_decision_replay_is_identity_on_own_decisions(pcqm_small):
     _, _, cache = O.forward(p, b, cfg, delta)
     own = [dict(relu=c["Z"] > 0, argmax=c["argmax"], argmin=c["argmin"]) for c in cache["layers"]]
     dec, n = O.replay(cache, own)
-    assert n["overrides"] == 0 and n["out_of_band"] == 0
+    assert n["overrides"] == 0 and n["tie_overrides"] == 0 and n["out_of_band"] == 0
     g0 = O.backward(p, b, cfg, cache)
     g1 = O.backward(p, b, cfg, cache, dec)
     for k in g0:
@@ -527,7 +527,8 @@ def test_replay_accepts_exact_ties_and_rejects_wrong_choices():
     g = dict(argmax=c["argmax"].copy(), argmin=c["argmin"].copy())
     g["argmax"][0, 0] = 1  # the other tied leaf: valid
     _, cnt = O.replay(cache, [g])
-    assert cnt["overrides"] == 1 and cnt["out_of_band"] == 0
+    # an exact tie: counted as a tie override (unbounded), not a near-tie override
+    assert cnt["tie_overrides"] == 1 and cnt["overrides"] == 0 and cnt["out_of_band"] == 0
     g["argmax"][0, 0] = 2  # leaf with x = 1: not a maximum
     _, cnt = O.replay(cache, [g])
     assert cnt["out_of_band"] == 1 and cnt["out_of_band_by"]["argmax"] == 1
