@@ -36,8 +36,11 @@
 namespace hg {
 
 extern std::atomic<int64_t> g_launches;
-// output-tile width per TMA GEMM (update, dA, proj, dX); HG_BN_<OP>=64|128 for A/B runs
-int g_bn_upd = 64, g_bn_da = 128, g_bn_proj = 64, g_bn_dx = 64;
+// output-tile width per TMA GEMM (update, dA, proj, dX); HG_BN_<OP>=32|64|128 for A/B runs.
+// 0 = by width: 64 for H = 128 (more tiles for the small config-B batches), 128 for
+// H >= 256 (measured: E512 +14%, E256 +9%; N = 64 MMAs are shared-memory-read bound)
+int g_bn_upd = 0, g_bn_da = 128, g_bn_proj = 0, g_bn_dx = 0;
+int bn_auto(int v, const Caps &c) { return v ? v : (c.H >= 256 ? 128 : 64); }
 bool g_update_sk = false;  // split-K cluster update (HG_UPDATE_SK=1): measured slower, see DESIGN.md
 
 
@@ -1045,9 +1048,10 @@ void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *
     g_launches += 1;
     return;
   }
-  if (g_bn_upd == 32)
+  const int bn_upd = bn_auto(g_bn_upd, c);
+  if (bn_upd == 32)
     update_bn<32>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
-  else if (g_bn_upd == 128)
+  else if (bn_upd == 128)
     update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
   else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
 }
@@ -1061,16 +1065,18 @@ void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, 
 
 void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
                    const float *Mx, const float *Mx_lo, float *P) {
-  if (g_bn_proj == 32) proj_bn<32>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
-  else if (g_bn_proj == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+  const int bn = bn_auto(g_bn_proj, c);
+  if (bn == 32) proj_bn<32>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+  else if (bn == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
   else proj_bn<64>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
 }
 
 void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
                  const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
                  const int *pos) {
-  if (g_bn_dx == 32) dX_bn<32>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
-  else if (g_bn_dx == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+  const int bn = bn_auto(g_bn_dx, c);
+  if (bn == 32) dX_bn<32>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+  else if (bn == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
   else dX_bn<64>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
 }
 
