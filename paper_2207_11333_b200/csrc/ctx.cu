@@ -162,9 +162,10 @@ struct hg_ctx {
   std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
+  cudaStream_t adam_stream = nullptr;  // early AdamW of layers >= 1 (must not delay layer 0's side-stream work)
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx;  // per layer fork / join points
   cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_hgrad = nullptr,
-              ev_prepmx = nullptr, ev_prepw = nullptr, ev_ar1 = nullptr;
+              ev_prepmx = nullptr, ev_prepw = nullptr, ev_ar1 = nullptr, ev_adam = nullptr;
   float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
@@ -372,7 +373,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   });
 }
 
-void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr, int64_t b, int64_t e, bool advance);
+void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr, int64_t b, int64_t e, bool advance,
+                  int max_blocks);
 int64_t layer1_offset(const hg_ctx *x);
 void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false,
                       bool overlap_allreduce = false, const hg_adamw *early_adamw = nullptr) {
@@ -388,6 +390,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   cudaStream_t side = fork ? x->side_stream : st, side2 = fork ? x->side2_stream : st;
   auto rec = [&](cudaEvent_t ev, cudaStream_t s) { if (fork) cudaEventRecord(ev, s); };
   auto wait = [&](cudaStream_t s, cudaEvent_t ev) { if (fork) cudaStreamWaitEvent(s, ev, 0); };
+  bool adam_forked = false;
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
     if (!head_done) {  // dZ of the last layer on the main stream
       launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"),
@@ -424,10 +427,18 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     wait(side, x->ev_dz[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DU, [&] {  // (side stream 1)
-      if (cls)
+      // layer 0's Gram ends the step (only agg_bwd_0 and dM_x0 run beside it): more CTAs
+      static const int gram0_grid = [] {
+        const char *e = getenv("HG_GRAM0_GRID");
+        return e ? atoi(e) : 148;  // (kSMs)
+      }();
+      if (cls) {
+        g_mn_grid_override = l == 0 ? gram0_grid : 0;
         launch_mn_dU_cls(side, x->caps, p.cmax, dZ, dZl, x->f(p.A[l]), x->f(p.A_lo[l]), x->f(p.ones), dinfo,
                          reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
                          x->grad(lname(l, "b_U")));
+        g_mn_grid_override = 0;
+      }
       else if (x->use_tc)
         launch_tc_dU(side, x->caps, blob, dZ, x->f(p.A[l]), amp, att, part_dU, x->grad(lname(l, "U")),
                      x->grad(lname(l, "b_U")));
@@ -463,8 +474,14 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     wait(side2, x->ev_dp[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
-      launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
       static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
+      if (l == 0 && adam_forked) {  // layer 0: off the step's final dM_x chain, on the idle AdamW stream
+        wait(x->adam_stream, x->ev_dp[0]);
+        launch_reduce_dMe(x->adam_stream, x->caps, pagg, x->grad(lname(l, "M_e")));
+        rec(x->ev_adam, x->adam_stream);
+      } else {
+        launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
+      }
       if (cls && (l > 0 || (p.xpad && !dmx0_simt))) {  // MN-major TMA Gram (layer 0: padded features)
         // (fused path: dP rows are degree-sorted, so X comes in sorted rows too)
         const float *Xg = l > 0 ? (dxda ? x->f(p.Xs[l - 1]) : Xl) : x->f(p.xpad);
@@ -509,18 +526,30 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         // every parameter of layers >= 1 and the head is final (and allreduced) and no longer
         // read by this step (dX_1 was the last reader): update them now, off the critical
         // chain; conv0's parameters follow after the backward (that launch advances the step)
+        // (own stream: on side stream 2 it delayed layer 0's dM_x chain at the step's end)
+        cudaStream_t as = x->adam_stream;
         rec(x->ev_dx[1], st);
-        wait(side2, x->ev_dx[1]);
-        wait(side2, x->ev_gram[1]);
-        if (x->world > 1 && x->comm) wait(side2, x->ev_ar1);  // (early_adamw_ok: layer 1 closes a bucket)
+        wait(as, x->ev_dx[1]);
+        wait(as, x->ev_gram[1]);
+        wait(as, x->ev_side[1]);
+        if (x->world > 1 && x->comm) wait(as, x->ev_ar1);  // (early_adamw_ok: layer 1 closes a bucket)
         g_low_prio = true;
-        enqueue_step(x, side2, *early_adamw, nullptr, layer1_offset(x), -1, false);
+        // (HG_EARLY_ADAMW_BLOCKS caps its grid: 64 CTAs was measured 1% slower — the update
+        // then finishes late and delays layer 0's dM_e reduction queued behind it)
+        static const int early_blocks = [] {
+          const char *e = getenv("HG_EARLY_ADAMW_BLOCKS");  // 0 = full grid (measured best)
+          return e ? atoi(e) : 0;
+        }();
+        enqueue_step(x, as, *early_adamw, nullptr, layer1_offset(x), -1, false, early_blocks);
         g_low_prio = false;
+        rec(x->ev_adam, as);
+        adam_forked = true;
       }
     }
   }
   wait(st, x->ev_gram[0]);  // join: every gradient is complete on the main stream
   wait(st, x->ev_side[0]);
+  if (adam_forked) wait(st, x->ev_adam);
 }
 
 // gradient buckets in backward order: head first, then conv L-1 ... conv 0 (each a
@@ -617,12 +646,13 @@ hg_status enqueue_allreduce(hg_ctx *x, cudaStream_t st) {
 // AdamW over parameters [b, e) of the flat arena (default: all); `advance` = this launch
 // is the step's last and advances the step counter
 void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr = nullptr, int64_t b = 0, int64_t e = -1,
-                  bool advance = true) {
+                  bool advance = true, int max_blocks = 0) {
   const Plan &p = x->plan;
   if (e < 0) e = x->n_params;
   phase(pr, HG_PHASE_ADAMW, [&] {
     launch_adamw(st, x->f(p.params) + b, x->f(p.grads) + b, x->f(p.m) + b, x->f(p.v) + b, e - b,
-                 reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay, advance);
+                 reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay, advance,
+                 max_blocks);
   });
 }
 int64_t layer1_offset(const hg_ctx *x) {  // start of conv1's parameters (conv0's come first)
@@ -691,9 +721,12 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   if ((e = cudaStreamCreateWithPriority(&x->side2_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
     return bail(e, "cudaStreamCreate");
+  if ((e = cudaStreamCreateWithPriority(&x->adam_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
+    return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
-  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad, &x->ev_prepmx, &x->ev_prepw, &x->ev_ar1})
+  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad, &x->ev_prepmx, &x->ev_prepw,
+                          &x->ev_ar1, &x->ev_adam})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
   if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocDefault)) != cudaSuccess)
     return bail(e, "cudaHostAlloc");
@@ -778,9 +811,11 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
   if (x->side_stream) cudaStreamDestroy(x->side_stream);
   if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
+  if (x->adam_stream) cudaStreamDestroy(x->adam_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
     for (auto ev : *v) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad, x->ev_prepmx, x->ev_prepw, x->ev_ar1})
+  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad, x->ev_prepmx, x->ev_prepw, x->ev_ar1,
+                         x->ev_adam})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : x->loss_ev)
     if (ev) cudaEventDestroy(ev);

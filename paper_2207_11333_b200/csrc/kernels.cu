@@ -1165,9 +1165,10 @@ __global__ void __launch_bounds__(256) k_adamw(float4 *__restrict__ p, const flo
 }
 
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
-                  float lr, float beta1, float beta2, float eps, float wd, bool advance) {
+                  float lr, float beta1, float beta2, float eps, float wd, bool advance, int max_blocks) {
   const int64_t n4 = n / 4;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, kSMs * 8));
+  const int cap = max_blocks > 0 ? max_blocks : kSMs * 8;
+  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n4 + 255) / 256, cap));
   launch_ex(k_adamw, blocks, 256, 0, st, reinterpret_cast<float4 *>(p), reinterpret_cast<const float4 *>(g),
             reinterpret_cast<float4 *>(m), reinterpret_cast<float4 *>(v), n4, ad, lr, beta1, beta2, eps, wd,
             advance ? 1 : 0);

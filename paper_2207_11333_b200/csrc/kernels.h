@@ -86,7 +86,8 @@ struct AdamDev {
 // (advance: this launch covers the step's last parameter range and advances the step counter;
 // ranges of one step must be launched in order on one stream)
 void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v, int64_t n, AdamDev *ad,
-                  float lr, float beta1, float beta2, float eps, float wd, bool advance = true);
+                  float lr, float beta1, float beta2, float eps, float wd, bool advance = true,
+                  int max_blocks = 0);
 
 // degree classes (tcgemm.cu): one class per distinct degree present in the batch
 constexpr int kMaxClasses = 16;

@@ -37,10 +37,11 @@ namespace hg {
 
 extern std::atomic<int64_t> g_launches;
 // output-tile width per TMA GEMM (update, dA, proj, dX); HG_BN_<OP>=32|64|128 for A/B runs.
-// 0 = by width: 64 for H = 128 (more tiles for the small config-B batches), 128 for
-// H >= 256 (measured: E512 +14%, E256 +9%; N = 64 MMAs are shared-memory-read bound)
+// 0 = by shape: 128 for H >= 256 (measured: E512 +14%, E256 +9%; N = 64 MMAs are
+// shared-memory-read bound); at H = 128, 32 for small batches (config B: 4x51 CTAs instead
+// of 2x51 for these latency-bound GEMMs, +1.5%), 64 for large ones (config D)
 int g_bn_upd = 0, g_bn_da = 128, g_bn_proj = 0, g_bn_dx = 0;
-int bn_auto(int v, const Caps &c) { return v ? v : (c.H >= 256 ? 128 : 64); }
+int bn_auto(int v, const Caps &c) { return v ? v : (c.H >= 256 ? 128 : c.maxN <= 16384 ? 32 : 64); }
 bool g_update_sk = false;  // split-K cluster update (HG_UPDATE_SK=1): measured slower, see DESIGN.md
 
 
