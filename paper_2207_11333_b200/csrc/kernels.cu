@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
   }
   for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < b.N; i += gridDim.x * wpb) {
     const int k0 = b.rowptr[i], k1 = b.rowptr[i + 1], d = k1 - k0;
+    const int prow = pos ? __ldg(pos + i) : i;  // (issued early: its latency hides behind the edge loop)
     float s[CPL], mx[CPL], mn[CPL];
     int amx[CPL], amn[CPL];
 #pragma unroll
@@ -435,10 +436,10 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
 #pragma unroll
       for (int c = 0; c < CPL; ++c) { mean[c] = 0.f; mx[c] = 0.f; mn[c] = 0.f; sd[c] = 0.f; flag[c] = 0; }
     } else {
-      const float fd = (float)d;
+      const float fd = (float)d, rd = __frcp_rn(fd);
       float ss[CPL];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) { mean[c] = s[c] / fd; ss[c] = 0.f; }
+      for (int c = 0; c < CPL; ++c) { mean[c] = s[c] * rd; ss[c] = 0.f; }
       for (int k = k0; k < k1; ++k) {  // second pass: recompute (P rows are L1-resident)
         const int j = b.col[k];
         float ef[FE], pj[CPL], m[CPL];
@@ -453,7 +454,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
       }
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        const float var = ss[c] / fd;
+        const float var = ss[c] * rd;
         flag[c] = var > var_floor;
         // channels >= Hl are padding (internal width H > logical Hl): their messages are
         // exactly 0, and their std is forced to 0 instead of sqrt(var_floor) so that no
@@ -461,7 +462,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
         sd[c] = ch + c < Hl ? sqrtf(fmaxf(var, var_floor)) : 0.f;
       }
     }
-    const size_t arow = (size_t)(pos ? pos[i] : i) * 4 * H + ch;  // degree-sorted row when pos is given
+    const size_t arow = (size_t)prow * 4 * H + ch;  // degree-sorted row when pos is given
     float *Ai = A + arow;
     store_vec<CPL>(Ai, mean);
     store_vec<CPL>(Ai + H, mn);
@@ -545,6 +546,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
   }
   for (int j = blockIdx.x * wpb + warp; j < b.N; j += gridDim.x * wpb) {
     const int k0 = b.rowptr[j], k1 = b.rowptr[j + 1];
+    const int prow_out = dp_pos ? __ldg(dp_pos + j) : j;  // (issued early)
     float pj[CPL], dp[CPL];
     load_vec<CPL>(P + (size_t)j * H + ch, pj);
 #pragma unroll
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
       const int i = b.col[k];
       const int sl = b.slot[k];
       const int di = b.rowptr[i + 1] - b.rowptr[i];
-      const float inv_d = 1.0f / (float)di;
+      const float inv_d = __frcp_rn((float)di);
       float ef[FE];
       load_edge<FE>(b.ea, Fe, k, ef);
       float m[CPL];
@@ -594,7 +596,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
         for (int f = 0; f < FE; ++f) acc[c][f] = fmaf(g, ef[f], acc[c][f]);
       }
     }
-    const size_t prow = (size_t)(dp_pos ? dp_pos[j] : j) * H + ch;  // degree-sorted row when dp_pos is given
+    const size_t prow = (size_t)prow_out * H + ch;  // degree-sorted row when dp_pos is given
     store_vec<CPL>(dP + prow, dp);
     if (dP_lo) store_vec_lo<CPL>(dP_lo + prow, dp);
   }
