@@ -75,6 +75,8 @@ def parse():
     ap.add_argument("--store-dir", default="")
     ap.add_argument("--seed", type=int, default=11)
     ap.add_argument("--tc-mode", type=int, default=0, help="pipeline experiment switch (timing only)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 gradient exchange: fused peer-memory reduce/AdamW/all-gather kernel or bucketed NCCL")
     return ap.parse_args()
 
 
@@ -244,6 +246,8 @@ def main():
         hgnn.load().hg_debug_set_tc_mode(args.tc_mode)
     ctx.params_init(1234)
     ctx.comm_init(rank, world)
+    if world > 1 and args.exchange == "p2p":
+        ctx.p2p_init(rank, world)
     hyper = dict(hgnn.DEFAULT_ADAMW)
 
     ids = hgnn.hg_shard(13, 0, rank, world, n_graphs)
@@ -456,6 +460,7 @@ def main():
                    "layers": L, "hidden": H, "hidden_internal": int(ctx.internal_cfg.hidden),
                    "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
                    "parallelism": f"dp{world}", "resident_batches": n_res,
+                   "grad_exchange": (args.exchange if world > 1 else "none"),
                    "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
                    "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs, TMA-fed"},
         "roofline": prof, "phase_roofline": phase_roof,

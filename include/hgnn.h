@@ -232,6 +232,26 @@ hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world
 /* Mean over ranks of the gradient arena; no-op when world == 1. */
 hg_status hg_allreduce_grads(hg_ctx *x);
 
+/* Gradient exchange over NVLink peer memory (reduce-scatter ->
+ * sharded fused AdamW -> all-gather, as ONE kernel; PAPER.md:206-212 DDP averaging).
+ * hg_p2p_handle writes this rank's HG_P2P_HANDLE_BYTES record (CUDA IPC handle of the
+ * workspace allocation + the workspace's byte offset in it; the workspace must be a
+ * cudaMalloc-backed allocation, e.g. torch's default caching allocator, not
+ * expandable segments -> HG_E_CUDA). After every rank's records are gathered (rank
+ * order, world x HG_P2P_HANDLE_BYTES bytes) hg_p2p_open maps the peers' workspaces
+ * (requires hg_comm_init with 2 <= world <= 8; all ranks use the same config).
+ * From then on hg_train_step / hg_capture_step end every step with: this rank's
+ * gradients ready -> flag in every rank; each rank sums the W gradient copies of its
+ * 1/W shard of the flat arena in rank order over peer loads, divides by W, applies
+ * AdamW and stores the new parameters into every rank's arena; a done flag per rank
+ * closes the step. Deterministic; parameters stay bitwise identical across ranks.
+ * The Adam moments become sharded: rank r's m, v are valid on its shard only
+ * (hg_opt_state_get returns the local arrays). The eager hg_allreduce_grads / hg_step
+ * path keeps using NCCL. Every rank must run the same sequence of steps. */
+#define HG_P2P_HANDLE_BYTES 72
+hg_status hg_p2p_handle(hg_ctx *x, void *out);
+hg_status hg_p2p_open(hg_ctx *x, const void *all);
+
 /* Fused AdamW over the whole parameter arena. */
 hg_status hg_step(hg_ctx *x, const hg_adamw *h);
 

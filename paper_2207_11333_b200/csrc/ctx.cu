@@ -2,6 +2,8 @@
 // async H2D ring, the per-step kernel sequence (forward / backward / step),
 // NCCL gradient averaging and CUDA-graph capture of a
 // whole training step.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -43,6 +45,7 @@ struct Plan {
   std::vector<size_t> Xs, Xs_lo;   // per layer: X_l in degree-sorted rows (fused dX->dA path)
   std::vector<size_t> Xmask;       // per layer: ReLU mask bits of X_l, sorted rows, [N][H/32]
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
+  size_t p2p = 0;  // P2PDev flags of the peer-memory gradient exchange
   size_t total = 0;
 };
 
@@ -62,6 +65,7 @@ Plan make_plan(const hg_config &c) {
   p.m = take(PB);
   p.v = take(PB);
   p.adam = take(sizeof(AdamDev));
+  p.p2p = take(sizeof(P2PDev));
   p.loss = take(sizeof(float) * 4);
   p.eval_acc = take(sizeof(double) * 4);  // evaluation sums: sq err, abs err, graphs
   p.blob_max = (size_t)batch_offsets(c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge).total;
@@ -162,7 +166,10 @@ struct hg_ctx {
   std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
-  cudaStream_t adam_stream = nullptr;  // early AdamW of layers >= 1 (must not delay layer 0's side-stream work)
+  cudaStream_t adam_stream = nullptr;
+  bool p2p = false;                        // gradient exchange over peer memory (hg_p2p_open)
+  uint8_t *peer_ws[kP2PMaxWorld] = {};     // every rank's workspace ([rank] = ws)
+  void *peer_base[kP2PMaxWorld] = {};      // opened IPC mappings (closed at destroy)  // early AdamW of layers >= 1 (must not delay layer 0's side-stream work)
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx;  // per layer fork / join points
   cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_hgrad = nullptr,
               ev_prepmx = nullptr, ev_prepw = nullptr, ev_ar1 = nullptr, ev_adam = nullptr;
@@ -475,7 +482,9 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
       static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
-      if (l == 0 && adam_forked) {  // layer 0: off the step's final dM_x chain, on the idle AdamW stream
+      // layer 0 on one GPU: off the step's final dM_x chain, on the idle AdamW stream (with W > 1
+      // the conv0 bucket's allreduce is enqueued on side stream 2 and must follow dM_e)
+      if (l == 0 && adam_forked && !(overlap_allreduce && x->world > 1 && x->comm)) {
         wait(x->adam_stream, x->ev_dp[0]);
         launch_reduce_dMe(x->adam_stream, x->caps, pagg, x->grad(lname(l, "M_e")));
         rec(x->ev_adam, x->adam_stream);
@@ -655,6 +664,23 @@ void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr = null
                  max_blocks);
   });
 }
+P2PArgs p2p_args(hg_ctx *x, const hg_adamw &h) {
+  P2PArgs a{};
+  const Plan &p = x->plan;
+  for (int q = 0; q < x->world; ++q) {
+    a.params[q] = reinterpret_cast<float *>(x->peer_ws[q] + p.params);
+    a.grads[q] = reinterpret_cast<const float *>(x->peer_ws[q] + p.grads);
+    a.dev[q] = reinterpret_cast<P2PDev *>(x->peer_ws[q] + p.p2p);
+  }
+  a.m = x->f(p.m);
+  a.v = x->f(p.v);
+  a.ad = reinterpret_cast<AdamDev *>(x->b(p.adam));
+  a.world = x->world;
+  a.rank = x->rank;
+  a.n4 = x->n_params / 4;
+  a.lr = h.lr; a.beta1 = h.beta1; a.beta2 = h.beta2; a.eps = h.eps; a.wd = h.weight_decay;
+  return a;
+}
 int64_t layer1_offset(const hg_ctx *x) {  // start of conv1's parameters (conv0's come first)
   for (auto &t : x->lay)
     if (t.name == lname(1, "M_x")) return t.offset;
@@ -821,6 +847,8 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
     if (ev) cudaEventDestroy(ev);
   if (x->loss_ring) cudaFreeHost(x->loss_ring);
   if (x->comm) ncclCommDestroy(x->comm);
+  for (void *b : x->peer_base)
+    if (b) cudaIpcCloseMemHandle(b);
   for (auto ev : x->bucket_ready) cudaEventDestroy(ev);
   if (x->comm_done) cudaEventDestroy(x->comm_done);
   if (x->comm_stream) cudaStreamDestroy(x->comm_stream);
@@ -1146,6 +1174,63 @@ hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world
   return HG_OK;
 }
 
+hg_status hg_p2p_handle(hg_ctx *x, void *out) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!out) return fail(HG_E_INVALID, "null output");
+  static PFN_cuMemGetAddressRange_v3020 get_range = nullptr;
+  if (!get_range) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return fail(HG_E_CUDA, "cuMemGetAddressRange unavailable");
+    get_range = reinterpret_cast<PFN_cuMemGetAddressRange_v3020>(fn);
+  }
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (get_range(&base, &size, (CUdeviceptr)x->ws) != CUDA_SUCCESS)
+    return fail(HG_E_CUDA, "cuMemGetAddressRange failed on the workspace");
+  cudaIpcMemHandle_t h;
+  CK(x, cudaIpcGetMemHandle(&h, (void *)base));
+  const int64_t off = (int64_t)((uintptr_t)x->ws - (uintptr_t)base);
+  std::memcpy(out, &h, sizeof(h));
+  std::memcpy((uint8_t *)out + sizeof(h), &off, sizeof(off));
+  return HG_OK;
+}
+
+hg_status hg_p2p_open(hg_ctx *x, const void *all) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!all) return fail(HG_E_INVALID, "null handles");
+  if (x->world < 2 || x->world > kP2PMaxWorld) return fail(HG_E_INVALID, "p2p needs 2..8 ranks (hg_comm_init first)");
+  static_assert(sizeof(cudaIpcMemHandle_t) + 8 == HG_P2P_HANDLE_BYTES, "handle size");
+  CK(x, cudaSetDevice(x->device));
+  for (int q = 0; q < x->world; ++q) {
+    if (q == x->rank) {
+      x->peer_ws[q] = x->ws;
+      continue;
+    }
+    if (x->peer_base[q]) continue;  // already open
+    cudaIpcMemHandle_t h;
+    int64_t off = 0;
+    const uint8_t *rec = (const uint8_t *)all + (size_t)q * HG_P2P_HANDLE_BYTES;
+    std::memcpy(&h, rec, sizeof(h));
+    std::memcpy(&off, rec + sizeof(h), sizeof(off));
+    void *b = nullptr;
+    CK(x, cudaIpcOpenMemHandle(&b, h, cudaIpcMemLazyEnablePeerAccess));
+    x->peer_base[q] = b;
+    x->peer_ws[q] = (uint8_t *)b + off;
+  }
+  x->p2p = true;
+  for (auto &g : x->graphs)  // captured graphs hold the NCCL exchange
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  return HG_OK;
+}
+
 hg_status hg_allreduce_grads(hg_ctx *x) {
   hg_status st = usable(x);
   if (st) return st;
@@ -1195,6 +1280,22 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->cap_stream, slot, nullptr, true);
+  if (x->p2p && x->world > 1) {
+    // gradient average + sharded AdamW + parameter all-gather in one kernel over peer memory
+    enqueue_backward(x, x->cap_stream, slot, nullptr, true, false, nullptr);
+    launch_p2p_step(x->cap_stream, p2p_args(x, *h));
+    const int64_t nk = launches_so_far() - l0;
+    cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
+    if (e != cudaSuccess) return cuda_fail(x, e, "cudaStreamEndCapture");
+    cudaGraphExec_t ex = nullptr;
+    e = cudaGraphInstantiate(&ex, g, cudaGraphInstantiateFlagUseNodePriority);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return cuda_fail(x, e, "cudaGraphInstantiate");
+    x->graphs[slot] = ex;
+    x->graph_kernels[slot] = nk;
+    x->graph_hyper[slot] = *h;
+    return HG_OK;
+  }
   // bucketed, overlapped allreduce; AdamW of layers >= 1 and the head inside the backward
   const bool split_adamw = x->cfg.layers > 1 && x->side_stream != nullptr && getenv("HG_ADAMW_END") == nullptr &&
                            (x->world <= 1 || !x->comm || bucket_closed_by(x, 1) >= 0);

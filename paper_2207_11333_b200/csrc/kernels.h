@@ -89,6 +89,26 @@ void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v,
                   float lr, float beta1, float beta2, float eps, float wd, bool advance = true,
                   int max_blocks = 0);
 
+// fused gradient average + sharded AdamW + parameter all-gather over peer memory (p2p.cu)
+constexpr int kP2PMaxWorld = 8;
+struct P2PDev {                     // in every rank's workspace; zero at ctx creation
+  unsigned ready[kP2PMaxWorld];     // ready[q] = epoch: rank q's gradients of that step are complete
+  unsigned done[kP2PMaxWorld];      // done[q] = epoch: rank q's parameter shard is written everywhere
+  unsigned epoch;                   // steps taken through the p2p path
+  unsigned ticket;                  // k_p2p_adamw's finished-block counter
+};
+struct P2PArgs {
+  float *params[kP2PMaxWorld];       // every rank's parameter arena ([rank] = local)
+  const float *grads[kP2PMaxWorld];  // every rank's gradient arena
+  P2PDev *dev[kP2PMaxWorld];         // every rank's flags
+  float *m, *v;                      // local Adam moments (the owned shard is used)
+  AdamDev *ad;
+  int world, rank;
+  int64_t n4;                        // float4s in the flat arena
+  float lr, beta1, beta2, eps, wd;
+};
+void launch_p2p_step(cudaStream_t st, const P2PArgs &a);
+
 // degree classes (tcgemm.cu): one class per distinct degree present in the batch
 constexpr int kMaxClasses = 16;
 constexpr int kGramKS = 256;  // minimum nodes per K-split of the per-class Gram GEMM

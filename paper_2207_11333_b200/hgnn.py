@@ -30,6 +30,7 @@ HG_MAX_DEGREE = 127
 PHASES = ["scalers", "proj", "agg_fwd", "update", "head_fwd", "head_bwd", "dA", "dU", "agg_bwd", "dMx", "dX",
           "allreduce", "adamw"]
 
+P2P_HANDLE_BYTES = 72  # include/hgnn.h HG_P2P_HANDLE_BYTES
 VIEW_P, VIEW_A, VIEW_ARG, VIEW_X, VIEW_SLOT, VIEW_YHAT, VIEW_LOSS, VIEW_HPRE, VIEW_PARAMS, VIEW_GRADS, \
     VIEW_AMP, VIEW_ATT = range(12)
 
@@ -104,6 +105,8 @@ SIGNATURES = {
     "hg_nccl_unique_id": [_P],
     "hg_comm_init": [_P, _P, _I32, _I32],
     "hg_allreduce_grads": [_P],
+    "hg_p2p_handle": [_P, _P],
+    "hg_p2p_open": [_P, _P],
     "hg_step": [_P, ctypes.POINTER(hg_adamw)],
     "hg_train_step": [_P, _I32, ctypes.POINTER(hg_adamw), _I32],
     "hg_capture_step": [_P, _I32, ctypes.POINTER(hg_adamw)],
@@ -456,6 +459,21 @@ class Context:
         """Create the NCCL communicator; the 128-byte id travels over torch.distributed."""
         buf = nccl_unique_id_broadcast(rank, world, group, device=self.device)
         _check(_lib.hg_comm_init(self.handle, _ptr(buf), rank, world))
+
+    def p2p_init(self, rank: int, world: int, group=None):
+        """Map every rank's workspace (CUDA IPC) for the fused peer-memory gradient
+        exchange (include/hgnn.h hg_p2p_open); call after comm_init on every rank."""
+        import torch
+        import torch.distributed as dist
+        rec = np.zeros(P2P_HANDLE_BYTES, np.uint8)
+        _check(_lib.hg_p2p_handle(self.handle, _ptr(rec)))
+        backend = dist.get_backend(group)
+        dev = f"cuda:{self.device}" if backend == "nccl" else "cpu"
+        t = torch.from_numpy(rec).to(dev)
+        allt = [torch.zeros_like(t) for _ in range(world)]
+        dist.all_gather(allt, t, group=group)
+        allh = np.ascontiguousarray(np.concatenate([a.cpu().numpy() for a in allt]))
+        _check(_lib.hg_p2p_open(self.handle, _ptr(allh)))
 
     def allreduce_grads(self):
         _check(_lib.hg_allreduce_grads(self.handle))

@@ -39,3 +39,27 @@ def test_ddp_nccl_matches_oracle_full_batch(tmp_path, world):
     print(res)
     assert res["params_identical"]
     assert res["grad_maxscaled"] <= 1e-3 and res["grad_normwise"] <= 1e-3
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_ddp_p2p_fused_exchange(tmp_path, world):
+    """Peer-memory reduce -> sharded AdamW -> all-gather (hg_p2p_open) against the
+    NCCL path and the oracle's full-batch step (tests/ddp_p2p_worker.py)."""
+    torch = pytest.importorskip("torch")
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    out = tmp_path / "res.json"
+    for attempt in range(3):
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+               "--master-addr=127.0.0.1", f"--master-port={_port()}",
+               os.path.join(ROOT, "tests", "ddp_p2p_worker.py"), str(out)]
+        r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
+        if r.returncode == 0 or "EADDRINUSE" not in r.stderr:
+            break
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    res = json.loads(out.read_text())
+    print(res)
+    assert res["nccl_identical"] and res["p2p_identical"]
+    # same arithmetic up to the order of the W-term gradient sum (NCCL's ring vs rank order)
+    assert res["p2p_vs_nccl_normwise"] <= 1e-5
+    assert res["p2p_step1_vs_oracle_normwise"] <= 1e-3
