@@ -383,6 +383,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
 void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr, int64_t b, int64_t e, bool advance,
                   int max_blocks);
 int64_t layer1_offset(const hg_ctx *x);
+P2PArgs p2p_args(hg_ctx *x, const hg_adamw &h);
 void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false,
                       bool overlap_allreduce = false, const hg_adamw *early_adamw = nullptr) {
   const hg_config &c = x->cfg;
@@ -484,7 +485,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
       // layer 0 on one GPU: off the step's final dM_x chain, on the idle AdamW stream (with W > 1
       // the conv0 bucket's allreduce is enqueued on side stream 2 and must follow dM_e)
-      if (l == 0 && adam_forked && !(overlap_allreduce && x->world > 1 && x->comm)) {
+      if (l == 0 && adam_forked && x->world == 1) {
         wait(x->adam_stream, x->ev_dp[0]);
         launch_reduce_dMe(x->adam_stream, x->caps, pagg, x->grad(lname(l, "M_e")));
         rec(x->ev_adam, x->adam_stream);
@@ -541,7 +542,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         wait(as, x->ev_dx[1]);
         wait(as, x->ev_gram[1]);
         wait(as, x->ev_side[1]);
-        if (x->world > 1 && x->comm) wait(as, x->ev_ar1);  // (early_adamw_ok: layer 1 closes a bucket)
+        if (x->world > 1 && x->comm && !x->p2p) wait(as, x->ev_ar1);  // (layer 1 closes a bucket)
         g_low_prio = true;
         // (HG_EARLY_ADAMW_BLOCKS caps its grid: 64 CTAs was measured 1% slower — the update
         // then finishes late and delays layer 0's dM_e reduction queued behind it)
@@ -549,7 +550,10 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
           const char *e = getenv("HG_EARLY_ADAMW_BLOCKS");  // 0 = full grid (measured best)
           return e ? atoi(e) : 0;
         }();
-        enqueue_step(x, as, *early_adamw, nullptr, layer1_offset(x), -1, false, early_blocks);
+        if (x->p2p && x->world > 1)  // peer-memory exchange of layers >= 1 and the head (part 1)
+          launch_p2p_part(as, p2p_args(x, *early_adamw), 1, layer1_offset(x) / 4, x->n_params / 4, true, false);
+        else
+          enqueue_step(x, as, *early_adamw, nullptr, layer1_offset(x), -1, false, early_blocks);
         g_low_prio = false;
         rec(x->ev_adam, as);
         adam_forked = true;
@@ -1281,9 +1285,17 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->cap_stream, slot, nullptr, true);
   if (x->p2p && x->world > 1) {
-    // gradient average + sharded AdamW + parameter all-gather in one kernel over peer memory
-    enqueue_backward(x, x->cap_stream, slot, nullptr, true, false, nullptr);
-    launch_p2p_step(x->cap_stream, p2p_args(x, *h));
+    // gradient average + sharded AdamW + parameter all-gather in one kernel over peer memory:
+    // layers >= 1 and the head during layer 0's backward (part 1), conv0 at the end (part 0)
+    // (HG_P2P_SPLIT=1: measured slower at 2 and 4 GPUs — part 1's grid competes with layer 0's
+    // backward, a capped grid puts it on the critical path; the default exchanges at the end)
+    static const bool split_env = getenv("HG_P2P_SPLIT") != nullptr && atoi(getenv("HG_P2P_SPLIT")) != 0;
+    const bool split = split_env && x->cfg.layers > 1 && x->side_stream != nullptr;
+    enqueue_backward(x, x->cap_stream, slot, nullptr, true, false, split ? h : nullptr);
+    const P2PArgs a = p2p_args(x, *h);
+    launch_p2p_part(x->cap_stream, a, 0, 0, split ? layer1_offset(x) / 4 : x->n_params / 4, !split, true);
+    launch_p2p_wait_done(x->cap_stream, a, 0);
+    if (split) launch_p2p_wait_done(x->cap_stream, a, 1);
     const int64_t nk = launches_so_far() - l0;
     cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
     if (e != cudaSuccess) return cuda_fail(x, e, "cudaStreamEndCapture");

@@ -91,11 +91,11 @@ void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v,
 
 // fused gradient average + sharded AdamW + parameter all-gather over peer memory (p2p.cu)
 constexpr int kP2PMaxWorld = 8;
-struct P2PDev {                     // in every rank's workspace; zero at ctx creation
-  unsigned ready[kP2PMaxWorld];     // ready[q] = epoch: rank q's gradients of that step are complete
-  unsigned done[kP2PMaxWorld];      // done[q] = epoch: rank q's parameter shard is written everywhere
-  unsigned epoch;                   // steps taken through the p2p path
-  unsigned ticket;                  // k_p2p_adamw's finished-block counter
+struct P2PDev {                        // in every rank's workspace; zero at ctx creation
+  unsigned ready[2][kP2PMaxWorld];     // ready[part][q] = epoch: rank q's gradients of that part are complete
+  unsigned done[2][kP2PMaxWorld];      // done[part][q] = epoch: rank q's shard of that part is written everywhere
+  unsigned epoch;                      // steps taken through the p2p path
+  unsigned ticket[2];                  // k_p2p_adamw's finished-block counters
 };
 struct P2PArgs {
   float *params[kP2PMaxWorld];       // every rank's parameter arena ([rank] = local)
@@ -107,7 +107,13 @@ struct P2PArgs {
   int64_t n4;                        // float4s in the flat arena
   float lr, beta1, beta2, eps, wd;
 };
-void launch_p2p_step(cudaStream_t st, const P2PArgs &a);
+// one exchange part (0: conv0 at the step's end, 1: layers >= 1 + head, overlapped with layer
+// 0's backward) over float4 range [b4, e4): signal ready, wait for every rank's ready, fused
+// reduce + AdamW + all-gather of this rank's shard (bump: first part of the step; advance:
+// last part, advances the AdamW step counter); launch_p2p_wait_done: wait for every rank's
+// done flag of `part` (before parameters or gradients are touched again)
+void launch_p2p_part(cudaStream_t st, const P2PArgs &a, int part, int64_t b4, int64_t e4, bool bump, bool advance);
+void launch_p2p_wait_done(cudaStream_t st, const P2PArgs &a, int part);
 
 // degree classes (tcgemm.cu): one class per distinct degree present in the batch
 constexpr int kMaxClasses = 16;

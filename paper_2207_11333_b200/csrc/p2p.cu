@@ -14,6 +14,7 @@
 // No float atomics; flags are monotonic epochs (no resets).
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <atomic>
@@ -36,27 +37,40 @@ __device__ __forceinline__ void spin_until_geq(const unsigned *p, unsigned e) {
   while ((int)(ld_acquire_sys(p) - e) < 0) __nanosleep(64);
 }
 
-__global__ void k_p2p_signal(P2PArgs a) {
+// ready / done flags and the finished-block ticket of exchange part `part` (0 = conv0's
+// parameters at the step's end, 1 = layers >= 1 and the head, during layer 0's backward)
+__device__ __forceinline__ unsigned *flags(P2PDev *d, int part, int which) {
+  return which == 0 ? d->ready[part] : d->done[part];
+}
+
+// this rank's gradients of `part` are complete: ready[part][rank] = epoch on every rank
+// (bump: first exchange of the step, advances the epoch)
+__global__ void k_p2p_signal(P2PArgs a, int part, int bump) {
   pdl_enter();
   __shared__ unsigned e;
   if (threadIdx.x == 0) {
-    e = a.dev[a.rank]->epoch + 1;
+    e = a.dev[a.rank]->epoch + (bump ? 1u : 0u);
     a.dev[a.rank]->epoch = e;
     __threadfence_system();  // this rank's gradients (earlier kernels) before the flags
   }
   __syncthreads();
-  if ((int)threadIdx.x < a.world) st_release_sys(&a.dev[threadIdx.x]->ready[a.rank], e);
+  if ((int)threadIdx.x < a.world) st_release_sys(&flags(a.dev[threadIdx.x], part, 0)[a.rank], e);
 }
 
-__global__ void __launch_bounds__(256) k_p2p_adamw(P2PArgs a) {
+// one warp waits until every rank's ready (which = 0) or done (which = 1) flag of `part`
+// reached this step's epoch (a single small CTA spins, so no SM is held by a waiting grid)
+__global__ void k_p2p_wait(P2PArgs a, int part, int which) {
+  pdl_enter();
+  P2PDev *me = a.dev[a.rank];
+  const unsigned e = *reinterpret_cast<volatile unsigned *>(&me->epoch);
+  if ((int)threadIdx.x < a.world) spin_until_geq(&flags(me, part, which)[threadIdx.x], e);
+}
+
+// float4 range [b4, e4) of the flat arena; this rank owns 1/W of it
+__global__ void __launch_bounds__(256) k_p2p_adamw(P2PArgs a, int part, int64_t b4, int64_t e4, int advance) {
   pdl_enter();
   __shared__ float s_ss, s_ib;
-  __shared__ unsigned s_e;
   P2PDev *me = a.dev[a.rank];
-  if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile unsigned *>(&me->epoch);
-  __syncthreads();
-  const unsigned e = s_e;
-  if ((int)threadIdx.x < a.world) spin_until_geq(&me->ready[threadIdx.x], e);
   const int64_t t = a.ad->step + 1;
   if (threadIdx.x == 0) {  // bias corrections of step t (fp64, as k_adamw and the oracle)
     const double bc1 = 1.0 - pow((double)a.beta1, (double)t);
@@ -67,7 +81,7 @@ __global__ void __launch_bounds__(256) k_p2p_adamw(P2PArgs a) {
   __syncthreads();
   const float ss = s_ss, ib = s_ib, decay = 1.0f - a.lr * a.wd, invw = 1.0f / (float)a.world;
   const float b1 = a.beta1, b2 = a.beta2, eps = a.eps;
-  const int64_t s0 = a.n4 * a.rank / a.world, s1 = a.n4 * (a.rank + 1) / a.world;
+  const int64_t n = e4 - b4, s0 = b4 + n * a.rank / a.world, s1 = b4 + n * (a.rank + 1) / a.world;
   float4 *p4 = reinterpret_cast<float4 *>(a.params[a.rank]);
   float4 *m4 = reinterpret_cast<float4 *>(a.m), *v4 = reinterpret_cast<float4 *>(a.v);
   for (int64_t i = s0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < s1; i += (int64_t)gridDim.x * blockDim.x) {
@@ -90,33 +104,41 @@ __global__ void __launch_bounds__(256) k_p2p_adamw(P2PArgs a) {
     v4[i] = V;
     for (int q = 0; q < a.world; ++q) reinterpret_cast<float4 *>(a.params[q])[i] = P;  // all-gather
   }
-  // completion: the last block advances the step and raises done[rank] on every rank
+  // completion: the last block (advances the step and) raises done[part][rank] on every rank
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence_system();
-    if (atomicAdd(&me->ticket, 1u) == gridDim.x - 1) {
-      me->ticket = 0;
-      a.ad->step = t;
+    if (atomicAdd(&me->ticket[part], 1u) == gridDim.x - 1) {
+      me->ticket[part] = 0;
+      if (advance) a.ad->step = t;
       __threadfence_system();
-      for (int q = 0; q < a.world; ++q) st_release_sys(&a.dev[q]->done[a.rank], e);
+      const unsigned e = *reinterpret_cast<volatile unsigned *>(&me->epoch);
+      for (int q = 0; q < a.world; ++q) st_release_sys(&flags(a.dev[q], part, 1)[a.rank], e);
     }
   }
 }
 
-__global__ void k_p2p_wait(P2PArgs a) {
-  pdl_enter();
-  P2PDev *me = a.dev[a.rank];
-  const unsigned e = *reinterpret_cast<volatile unsigned *>(&me->epoch);
-  if ((int)threadIdx.x < a.world) spin_until_geq(&me->done[threadIdx.x], e);
+static int p2p_blocks(int64_t n4, int world) {
+  const int64_t shard4 = (n4 + world - 1) / world;
+  return (int)std::max<int64_t>(1, std::min<int64_t>((shard4 + 255) / 256, kSMs * 8));
 }
 
-void launch_p2p_step(cudaStream_t st, const P2PArgs &a) {
-  launch_ex(k_p2p_signal, 1, 32, 0, st, a);
-  const int64_t shard4 = (a.n4 + a.world - 1) / a.world;
-  const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((shard4 + 255) / 256, kSMs * 8));
-  launch_ex(k_p2p_adamw, blocks, 256, 0, st, a);
-  launch_ex(k_p2p_wait, 1, 32, 0, st, a);
+void launch_p2p_part(cudaStream_t st, const P2PArgs &a, int part, int64_t b4, int64_t e4, bool bump, bool advance) {
+  launch_ex(k_p2p_signal, 1, 32, 0, st, a, part, bump ? 1 : 0);
+  launch_ex(k_p2p_wait, 1, 32, 0, st, a, part, 0);
+  // part 1 runs beside layer 0's backward: a capped grid leaves it the SMs (HG_P2P1_BLOCKS)
+  static const int p1_cap = [] {
+    const char *e = getenv("HG_P2P1_BLOCKS");
+    return e ? atoi(e) : 0;
+  }();
+  int blocks = p2p_blocks(e4 - b4, a.world);
+  if (part == 1 && p1_cap > 0) blocks = std::min(blocks, p1_cap);
+  launch_ex(k_p2p_adamw, blocks, 256, 0, st, a, part, b4, e4, advance ? 1 : 0);
   g_launches += 3;
+}
+void launch_p2p_wait_done(cudaStream_t st, const P2PArgs &a, int part) {
+  launch_ex(k_p2p_wait, 1, 32, 0, st, a, part, 1);
+  g_launches += 1;
 }
 
 }  // namespace hg
