@@ -532,7 +532,12 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
                                                     const int *__restrict__ pos, const int *__restrict__ dp_pos) {
   pdl_enter();
   __shared__ float red[kAggBwdWarps][32][CPL * FE];
-  const BatchView b = load_batch(blob);
+  // the batch view lives in shared memory: under register pressure the compiler reloads its
+  // pointers (one LDS) instead of recomputing the blob offsets on every edge
+  __shared__ BatchView sb;
+  if (threadIdx.x == 0) sb = load_batch(blob);
+  __syncthreads();
+  const BatchView &b = sb;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int wpb = blockDim.x >> 5;
   const int ch = blockIdx.y * 32 * CPL + lane * CPL;
@@ -560,8 +565,9 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
       load_edge<FE>(b.ea, Fe, k, ef);
       float m[CPL];
       message<CPL, FE>(pj, bm, me, ef, m);
-      const float *dAi = dA + (size_t)i * 4 * H + ch;
-      const float *Ai = A + (size_t)(pos ? pos[i] : i) * 4 * H + ch;
+      // (32-bit row offsets from per-lane bases: N * 4H < 2^31)
+      const float *dAi = dA + ch + i * (4 * H);
+      const float *Ai = A + ch + (pos ? __ldg(pos + i) : i) * (4 * H);
       float gmean[CPL], gmin[CPL], gmax[CPL], gstd[CPL], mu[CPL], sg[CPL];
       load_vec<CPL>(dAi, gmean);
       load_vec<CPL>(dAi + H, gmin);
@@ -570,7 +576,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
       load_vec<CPL>(Ai, mu);
       load_vec<CPL>(Ai + 3 * H, sg);
       uint8_t amn[CPL], amx[CPL];
-      const uint8_t *ai = arg + (size_t)i * 2 * H + ch;
+      const uint8_t *ai = arg + ch + i * (2 * H);
       if constexpr (CPL == 4) {
         const uchar4 t0 = *reinterpret_cast<const uchar4 *>(ai);
         const uchar4 t1 = *reinterpret_cast<const uchar4 *>(ai + H);
