@@ -420,7 +420,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
       const int j = b.col[k];
       float ef[FE], pj[CPL], m[CPL];
       load_edge<FE>(b.ea, Fe, k, ef);
-      load_vec<CPL>(P + (size_t)j * H + ch, pj);
+      load_vec<CPL>(P + ch + j * H, pj);
       message<CPL, FE>(pj, bm, me, ef, m);
       const int p = k - k0;
 #pragma unroll
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
         const int j = b.col[k];
         float ef[FE], pj[CPL], m[CPL];
         load_edge<FE>(b.ea, Fe, k, ef);
-        load_vec<CPL>(P + (size_t)j * H + ch, pj);
+        load_vec<CPL>(P + ch + j * H, pj);
         message<CPL, FE>(pj, bm, me, ef, m);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
         sd[c] = ch + c < Hl ? sqrtf(fmaxf(var, var_floor)) : 0.f;
       }
     }
-    const size_t arow = (size_t)prow * 4 * H + ch;  // degree-sorted row when pos is given
+    const int arow = prow * (4 * H) + ch;  // degree-sorted row when pos is given (N * 4H < 2^31)
     float *Ai = A + arow;
     store_vec<CPL>(Ai, mean);
     store_vec<CPL>(Ai + H, mn);
@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
       store_vec_lo<CPL>(Li + 2 * H, mx);
       store_vec_lo<CPL>(Li + 3 * H, sd);
     }
-    uint8_t *ai = arg + (size_t)i * 2 * H + ch;
+    uint8_t *ai = arg + ch + i * (2 * H);
     if constexpr (CPL == 4) {
       *reinterpret_cast<uchar4 *>(ai) = make_uchar4(amn[0], amn[1], amn[2], amn[3]);
       *reinterpret_cast<uchar4 *>(ai + H) =
