@@ -1104,7 +1104,11 @@ void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const i
 
 void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int l0, int l1,
                     int cmax, double delta, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo) {
-  const int blocks = std::min((l1 - l0) * cmax * (4 * c.H / 32) * (c.H / 32), kSMs * 2);
+  static const int cap = [] {  // A/B switch: grid of the (side-stream) weight preparation
+    const char *e = getenv("HG_PREP_BLOCKS");
+    return e ? atoi(e) : kSMs * 2;
+  }();
+  const int blocks = std::max(1, std::min((l1 - l0) * cmax * (4 * c.H / 32) * (c.H / 32), cap));
   launch_ex(k_prep_W2, blocks, dim3(32, 8), 0, st, params, u_off_dev, l0, l1, c.H, cmax, delta, Wf, Wf_lo, WbT,
             WbT_lo);
   g_launches += 1;
