@@ -209,6 +209,11 @@ hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t st
  * pre-activation [B,Hf], 8 = params, 9 = grads, 10 = amp [N], 11 = att [N]. */
 hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_t *offset, int64_t *bytes);
 
+/* Debug: copy batch slot `slot`'s packed blob (layout above; its header gives B, N, E) to
+ * host memory dst (capacity cap bytes), after the slot's pending H2D copy and the compute
+ * stream's work. *used = blob bytes. HG_E_RANGE bad slot, HG_E_CAPACITY cap too small. */
+hg_status hg_batch_get(hg_ctx *x, int32_t slot, void *dst, size_t cap, size_t *used);
+
 /* Collate `ids` from the store on the host (pinned staging buffer of `slot`)
  * and enqueue the H2D copy on the ctx's copy stream; later device work on
  * that slot waits for it. The staging buffer is reused only after its

@@ -979,6 +979,22 @@ hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t st
   return HG_OK;
 }
 
+hg_status hg_batch_get(hg_ctx *x, int32_t slot, void *dst, size_t cap, size_t *used) {
+  hg_status st = usable(x);
+  if (st || (st = check_slot(x, slot))) return st;
+  if (!dst) return fail(HG_E_INVALID, "null destination");
+  CK(x, cudaStreamWaitEvent(x->stream, x->copy_done[slot], 0));
+  int32_t hdr[5];
+  CK(x, cudaMemcpyAsync(hdr, x->b(x->plan.slot[slot]), sizeof(hdr), cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  const size_t bytes = (size_t)batch_offsets(hdr[0], hdr[1], hdr[2], hdr[3], hdr[4]).total;
+  if (used) *used = bytes;
+  if (bytes > cap) return fail(HG_E_CAPACITY, "destination too small (%zu bytes needed)", bytes);
+  CK(x, cudaMemcpyAsync(dst, x->b(x->plan.slot[slot]), bytes, cudaMemcpyDeviceToHost, x->stream));
+  CK(x, cudaStreamSynchronize(x->stream));
+  return HG_OK;
+}
+
 hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_t *offset, int64_t *bytes) {
   if (!x || !offset || !bytes) return fail(HG_E_INVALID, "null argument");
   const hg_config &c = x->cfg;

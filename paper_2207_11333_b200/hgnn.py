@@ -98,6 +98,7 @@ SIGNATURES = {
     "hg_opt_state_get": [_P, _P, _P, _I64P, _I32],
     "hg_opt_state_set": [_P, _P, _P, _I64, _I32],
     "hg_workspace_view": [_P, _I32, _I32, _I64P, _I64P],
+    "hg_batch_get": [_P, _I32, _P, _SZ, _SZP],
     "hg_pack": [_P, _P, _P, _I32, _I32],
     "hg_upload_packed": [_P, _P, _SZ, _I32],
     "hg_forward": [_P, _I32],
@@ -404,6 +405,14 @@ class Context:
         _check(_lib.hg_workspace_view(self.handle, what, layer, ctypes.byref(off), ctypes.byref(nb)))
         o = self._ws_off + off.value
         return self.workspace[o:o + nb.value]
+
+    def batch_get(self, slot: int) -> dict:
+        """The packed batch of `slot`, copied to the host and unpacked (hg_batch_get)."""
+        cap = self.view(VIEW_SLOT, slot).numel()
+        out = np.zeros(cap, np.uint8)
+        used = _SZ()
+        _check(_lib.hg_batch_get(self.handle, slot, _ptr(out), cap, ctypes.byref(used)))
+        return unpack_blob(out[:used.value])
 
     def view_f32(self, what: int, layer: int = 0):
         import torch

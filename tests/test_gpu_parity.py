@@ -24,6 +24,9 @@ def test_device_pack_bit_exact(torch_cuda):
     got = hgnn.unpack_blob(blob)
     for k in ("graph_ptr", "y", "rowptr", "col", "x", "eattr", "slot"):
         np.testing.assert_array_equal(np.asarray(got[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8), err_msg=k)
+    got2 = ctx.batch_get(1)  # the same blob through hg_batch_get
+    for k in ("graph_ptr", "y", "rowptr", "col", "x", "eattr", "slot"):
+        np.testing.assert_array_equal(np.asarray(got2[k]).view(np.uint8), np.asarray(ref[k]).view(np.uint8), err_msg=k)
 
 
 def test_config_a_every_step_of_an_epoch(torch_cuda):
