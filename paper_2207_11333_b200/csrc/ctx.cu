@@ -485,21 +485,24 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
       // layer 0 on one GPU: off the step's final dM_x chain, on the idle AdamW stream (with W > 1
       // the conv0 bucket's allreduce is enqueued on side stream 2 and must follow dM_e)
+      // the MN-major dM_x Gram takes db_M from the aggregation partials (no column-sum tiles)
+      const bool mn_dmx = cls && (l > 0 || (p.xpad && !dmx0_simt));
+      float *dbM_agg = mn_dmx ? x->grad(lname(l, "b_M")) : nullptr;
       if (l == 0 && adam_forked && x->world == 1) {
         wait(x->adam_stream, x->ev_dp[0]);
-        launch_reduce_dMe(x->adam_stream, x->caps, pagg, x->grad(lname(l, "M_e")));
+        launch_reduce_dMe(x->adam_stream, x->caps, pagg, x->grad(lname(l, "M_e")), dbM_agg);
         rec(x->ev_adam, x->adam_stream);
       } else {
-        launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")));
+        launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")), dbM_agg);
       }
-      if (cls && (l > 0 || (p.xpad && !dmx0_simt))) {  // MN-major TMA Gram (layer 0: padded features)
+      if (mn_dmx) {  // MN-major TMA Gram (layer 0: padded features)
         // (fused path: dP rows are degree-sorted, so X comes in sorted rows too)
         const float *Xg = l > 0 ? (dxda ? x->f(p.Xs[l - 1]) : Xl) : x->f(p.xpad);
         const float *Xg_lo = l > 0 ? x->f(dxda ? p.Xs_lo[l - 1] : p.X_lo[l - 1]) : x->f(p.xpad_lo);
         // layer 0's dM_x runs after the last main-chain kernel: it may use every SM
         g_mn_grid_override = l == 0 ? 148 : 0;  // (kSMs)
         launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xg, Xg_lo, F, l > 0 ? F : pad_x0_width(c.f_node),
-                      x->f(p.ones), part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+                      x->f(p.ones), part_dMx, x->grad(lname(l, "M_x")), nullptr);
         g_mn_grid_override = 0;
       } else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
         launch_tc_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));

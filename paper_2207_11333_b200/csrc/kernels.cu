@@ -532,6 +532,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
                                                     const int *__restrict__ pos, const int *__restrict__ dp_pos) {
   pdl_enter();
   __shared__ float red[kAggBwdWarps][32][CPL * FE];
+  __shared__ float redb[kAggBwdWarps][32][CPL];
   // the batch view lives in shared memory: under register pressure the compiler reloads its
   // pointers (one LDS) instead of recomputing the blob offsets on every edge
   __shared__ BatchView sb;
@@ -542,10 +543,11 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
   const int wpb = blockDim.x >> 5;
   const int ch = blockIdx.y * 32 * CPL + lane * CPL;
   const int Fe = b.Fe;
-  float me[CPL][FE], bm[CPL], acc[CPL][FE];
+  float me[CPL][FE], bm[CPL], acc[CPL][FE], bsum[CPL];  // bsum: db_M = sum_j dP_j
 #pragma unroll
   for (int c = 0; c < CPL; ++c) {
     bm[c] = bM[ch + c];
+    bsum[c] = 0.f;
 #pragma unroll
     for (int f = 0; f < FE; ++f) { me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f; acc[c][f] = 0.f; }
   }
@@ -605,21 +607,53 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
     const size_t prow = (size_t)prow_out * H + ch;  // degree-sorted row when dp_pos is given
     store_vec<CPL>(dP + prow, dp);
     if (dP_lo) store_vec_lo<CPL>(dP_lo + prow, dp);
-  }
-  // block reduction of dM_e partials in fixed warp order
 #pragma unroll
-  for (int c = 0; c < CPL; ++c)
+    for (int c = 0; c < CPL; ++c) bsum[c] += dp[c];
+  }
+  // block reduction of the dM_e and db_M partials in fixed warp order
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    redb[warp][lane][c] = bsum[c];
 #pragma unroll
     for (int f = 0; f < FE; ++f) red[warp][lane][c * FE + f] = acc[c][f];
+  }
   __syncthreads();
   const int chunkC = 32 * CPL;
-  for (int t = threadIdx.x; t < chunkC * Fe; t += blockDim.x) {
-    const int cc = t / Fe, f = t - cc * Fe;   // channel within chunk, feature
-    const int l = cc / CPL, c = cc - l * CPL;
+  // partial layout: [block][H * Fe + H] = M_e's layout [H][Fe], then b_M's [H]
+  float *pb = partial + (size_t)blockIdx.x * H * (Fe + 1);
+  for (int t = threadIdx.x; t < chunkC * (Fe + 1); t += blockDim.x) {
+    if (t < chunkC * Fe) {
+      const int cc = t / Fe, f = t - cc * Fe;  // channel within chunk, feature
+      const int l = cc / CPL, c = cc - l * CPL;
+      float s = 0.f;
+      for (int w = 0; w < wpb; ++w) s += red[w][l][c * FE + f];
+      pb[(size_t)(blockIdx.y * chunkC + cc) * Fe + f] = s;
+    } else {
+      const int cc = t - chunkC * Fe, l = cc / CPL, c = cc - l * CPL;
+      float s = 0.f;
+      for (int w = 0; w < wpb; ++w) s += redb[w][l][c];
+      pb[(size_t)H * Fe + blockIdx.y * chunkC + cc] = s;
+    }
+  }
+}
+
+// fixed-order reduction of launch_agg_bwd's block partials (stride H * (Fe + 1)): dM_e
+// ([H][Fe]) and, when dbM is given, db_M ([H]); one warp per output element, lanes stride
+// over the blocks, then a fixed xor-shuffle tree (deterministic)
+__global__ void k_reduce_agg(const float *__restrict__ part, int nparts, int stride, int cnt_e,
+                             float *__restrict__ dMe, int cnt_b, float *__restrict__ dbM) {
+  pdl_enter();
+  const int lane = threadIdx.x & 31;
+  const int wpb = blockDim.x >> 5;
+  for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < cnt_e + cnt_b; e += gridDim.x * wpb) {
     float s = 0.f;
-    for (int w = 0; w < wpb; ++w) s += red[w][l][c * FE + f];
-    // partial layout: [block][H][Fe] (M_e layout)
-    partial[(size_t)blockIdx.x * H * Fe + (size_t)(blockIdx.y * chunkC + cc) * Fe + f] = s;
+    for (int p = lane; p < nparts; p += 32) s += part[(size_t)p * stride + e];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) {
+      if (e < cnt_e) dMe[e] = s;
+      else dbM[e - cnt_e] = s;
+    }
   }
 }
 
@@ -639,7 +673,7 @@ __global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int co
 }
 
 static int agg_bwd_blocks(const Caps &c) { return std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 2)); }
-size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * c.Fe; }
+size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * (c.Fe + 1); }
 int agg_bwd_partials(const Caps &c) { return agg_bwd_blocks(c); }
 
 template <int CPL, int FE>
@@ -663,10 +697,10 @@ void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
   if (dMe) launch_reduce_dMe(st, c, partial, dMe);
 }
 
-void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe) {
-  const int count = c.H * c.Fe;
-  launch_ex(k_reduce_rows, std::max(1, std::min(cdiv(count, 8), kSMs * 4)), 256, 0, st, partial, agg_bwd_blocks(c),
-            count, dMe);
+void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe, float *dbM) {
+  const int ce = c.H * c.Fe, cb = dbM ? c.H : 0;
+  launch_ex(k_reduce_agg, std::max(1, std::min(cdiv(ce + cb, 8), kSMs * 4)), 256, 0, st, partial, agg_bwd_blocks(c),
+            c.H * (c.Fe + 1), ce, dMe, cb, dbM);
   counted();
 }
 

@@ -49,7 +49,8 @@ void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const f
                     float *partial, float *dMe, float *dP_lo = nullptr, const int *pos = nullptr,
                     const int *dp_pos = nullptr);  // dp_pos: write dP row j at dp_pos[j]
 // dM_e = fixed-order sum of launch_agg_bwd's block partials (launch_agg_bwd does it when dMe != null)
-void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe);
+// (dbM != null: also db_M = sum_j dP_j from the same partials)
+void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe, float *dbM = nullptr);
 size_t agg_bwd_partial_floats(const Caps &c);
 size_t dU_partial_floats(const Caps &c);
 size_t dMx_partial_floats(const Caps &c, int F);
@@ -176,7 +177,7 @@ void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ,
 // X: [maxN][Fp] (Fp >= F, 16-byte row pitch; Fp = F for hidden layers), F output columns
 void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
                    const float *X, const float *X_lo, int F, int Fp, const float *ones, float *partial, float *dMx,
-                   float *dbM);
+                   float *dbM);  // dbM == null: no column-sum tiles (db_M comes from launch_reduce_dMe)
 // layer-0 node features padded to pad_x0_width(F0) columns (+ tf32 residual) for the TMA path
 int pad_x0_width(int F0);
 void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo,

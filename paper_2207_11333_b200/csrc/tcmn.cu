@@ -270,14 +270,15 @@ constexpr int kMnDMxSplits = 32;
 struct MnDMx {
   static constexpr int BN = 128;
   const uint8_t *blob; float *part, *cs; int H, F; int items_cap;
+  int with_cs;  // 1: a trailing ones tile per (m, split) gives cs = sum_k dP[k][h] (db_M)
   __device__ bool item(int t, MnItem &w) const {
-    const int NT = (F + BN - 1) / BN + 1, MT = H / N_BM;
+    const int NT = (F + BN - 1) / BN + with_cs, MT = H / N_BM;
     const int nt = t % NT, mt = (t / NT) % MT, sp = t / (NT * MT);
     const int N = batch_N(blob);
     int kc = (N + kMnDMxSplits - 1) / kMnDMxSplits;
     kc = (kc + N_BK - 1) / N_BK * N_BK;
     const int k0 = sp * kc, len = max(0, min(N - k0, kc));
-    w = MnItem{mt * N_BM, nt * BN, k0, len, sp, nt == NT - 1};
+    w = MnItem{mt * N_BM, nt * BN, k0, len, sp, with_cs && nt == NT - 1};
     // every split is an item, also an empty one (len 0: its partial is written as zeros),
     // because the fixed-order reduction sums all kMnDMxSplits partials
     return sp < kMnDMxSplits;
@@ -468,10 +469,12 @@ void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
   const TmaMaps mp{tma_map2d(dP, c.maxN, c.H, N_BK, true), tma_map2d(dP_lo, c.maxN, c.H, N_BK, true),
                    tma_map2d(X, c.maxN, Fp, N_BK, true), tma_map2d(X_lo, c.maxN, Fp, N_BK, true)};
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
-  MnDMx op{blob, partial, cs, c.H, F, 0};
-  nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + 1));
-  const RJob j0{partial, kMnDMxSplits, count, dMx}, j1{cs, kMnDMxSplits, c.H, dbM}, j2{nullptr, 0, 0, nullptr};
-  launch_ex(k_reduce_jobs, reduce_blocks(j0) + reduce_blocks(j1), 32 * RW, 0, st, j0, j1, j2);
+  const int with_cs = dbM ? 1 : 0;
+  MnDMx op{blob, partial, cs, c.H, F, 0, with_cs};
+  nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + with_cs));
+  const RJob j0{partial, kMnDMxSplits, count, dMx}, j1{cs, kMnDMxSplits, with_cs ? c.H : 0, dbM},
+      j2{nullptr, 0, 0, nullptr};
+  launch_ex(k_reduce_jobs, reduce_blocks(j0) + (with_cs ? reduce_blocks(j1) : 0), 32 * RW, 0, st, j0, j1, j2);
   g_launches += 1;
 }
 
