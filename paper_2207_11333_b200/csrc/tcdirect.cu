@@ -97,7 +97,12 @@ template <class Op>
 __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ TmaMaps mp, Op op_in) {
   constexpr int BN = Op::BN, ST = t_stages<Op>();
   constexpr int A_BYTES = T_BM * 128, B_BYTES = BN * 128, STAGE = t_stage_bytes<Op>();
-  constexpr int TCOLS = TCols<2 * BN>::v;
+  // TMEM: two buffers of the main accumulator (hi*hi) at columns [0, 2BN) and two of the
+  // correction accumulator (hi*lo + lo*hi) at [2BN, 4BN). Accumulating the small correction
+  // terms apart keeps the main accumulator's additions to K/8 (the tensor pipe's fp32
+  // accumulation error grows with the number of additions: measured max-scaled forward error
+  // at H = 512 x 8 layers 1.2e-4 with one accumulator, vs 3e-7 for a plain fp32 evaluation)
+  constexpr int TCOLS = TCols<4 * BN>::v;
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256, "BN");
   static_assert(ST >= 2, "stages");
 
@@ -179,7 +184,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
         const int buf = tcount & 1;
         if (tcount >= 2) tc::mbar_wait(&acce[buf], ((tcount >> 1) - 1) & 1);
         tc::fence_after_sync();
-        const uint32_t d = tmem + (uint32_t)(buf * BN);
+        const uint32_t d = tmem + (uint32_t)(buf * BN), dc = d + (uint32_t)(2 * BN);
         const int nchunks = (ke + T_BK - 1) / T_BK;
         for (int c = 0; c < nchunks; ++c, ++it) {
           const int s = it % ST;
@@ -194,8 +199,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
             const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
             const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
             tc::mma_tf32(d, dah, dbh, idesc, (c | ks) != 0);
-            tc::mma_tf32(d, dah, dbl, idesc, 1u);
-            tc::mma_tf32(d, dal, dbh, idesc, 1u);
+            tc::mma_tf32(dc, dah, dbl, idesc, (c | ks) != 0);
+            tc::mma_tf32(dc, dal, dbh, idesc, 1u);
           }
           tc::mma_commit(&empty[s]);
         }
@@ -219,12 +224,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
       const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
       for (int q = 0; q < BN / 32; ++q) {
-        float acc[32];
+        float acc[32], cor[32];
         tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
+        tc::tmem_ld32(trow + (uint32_t)(2 * BN + q * 32), cor);
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) =
-              make_float4(acc[4 * j], acc[4 * j + 1], acc[4 * j + 2], acc[4 * j + 3]);
+              make_float4(acc[4 * j] + cor[4 * j], acc[4 * j + 1] + cor[4 * j + 1], acc[4 * j + 2] + cor[4 * j + 2],
+                          acc[4 * j + 3] + cor[4 * j + 3]);
         __syncwarp();
         // all global loads of the 8 rows first (emit's stores may alias them), then the stores
         const int cc = 4 * (lane & 7), n = n0 + q * 32 + cc;

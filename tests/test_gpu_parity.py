@@ -80,11 +80,7 @@ def test_one_step_parity(torch_cuda, preset, B, H, L):
     ids = O.shard(23, 1, 0, 1, len(data["y"]))[:B]
     res = PT.run_step_parity(data, ids, ctx, cfg, delta)
     print(preset, B, H, L, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
-    # DESIGN.md reading R-fp32-depth: the forward error of any fp32 evaluation grows like
-    # sqrt(K) (measured X error 2.7e-5 / 6.4e-5 / 1.2e-4 at H = 128 / 256 / 512; a fourth
-    # 3xTF32 product changed nothing), so the 1e-4 bar holds to H = 256; H = 512 x 8 layers
-    # is checked at 2e-4
-    PT.assert_parity(res, fwd_tol=2e-4 if H >= 512 else PT.FWD_TOL)
+    PT.assert_parity(res)
 
 
 @pytest.mark.parametrize("mode", ["simt", "tc_3acc", "tc_classes"])
