@@ -246,8 +246,14 @@ def main():
         hgnn.load().hg_debug_set_tc_mode(args.tc_mode)
     ctx.params_init(1234)
     ctx.comm_init(rank, world)
-    if world > 1 and args.exchange == "p2p":
-        ctx.p2p_init(rank, world)
+    exchange = args.exchange if world > 1 else "none"
+    if exchange == "p2p":
+        try:
+            ctx.p2p_init(rank, world)
+        except hgnn.HgError as e:  # e.g. a workspace that is not cudaMalloc-backed: NCCL buckets
+            log(f"rank {rank}: peer-memory exchange unavailable ({e}); using the NCCL exchange")
+            exchange = f"nccl (p2p unavailable: {e})"
+        # (p2p_init agrees across ranks: all take the peer-memory path or none)
     hyper = dict(hgnn.DEFAULT_ADAMW)
 
     ids = hgnn.hg_shard(13, 0, rank, world, n_graphs)
@@ -460,7 +466,7 @@ def main():
                    "layers": L, "hidden": H, "hidden_internal": int(ctx.internal_cfg.hidden),
                    "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
                    "parallelism": f"dp{world}", "resident_batches": n_res,
-                   "grad_exchange": (args.exchange if world > 1 else "none"),
+                   "grad_exchange": exchange,
                    "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
                    "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs, TMA-fed"},
         "roofline": prof, "phase_roofline": phase_roof,

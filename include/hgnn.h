@@ -252,7 +252,9 @@ hg_status hg_allreduce_grads(hg_ctx *x);
  * closes the step. Deterministic; parameters stay bitwise identical across ranks.
  * The Adam moments become sharded: rank r's m, v are valid on its shard only
  * (hg_opt_state_get returns the local arrays). The eager hg_allreduce_grads / hg_step
- * path keeps using NCCL. Every rank must run the same sequence of steps. */
+ * path keeps using NCCL. Every rank must run the same sequence of steps.
+ * hg_p2p_open(x, NULL) returns this ctx to the NCCL exchange (captured graphs are
+ * rebuilt on their next use). */
 #define HG_P2P_HANDLE_BYTES 72
 hg_status hg_p2p_handle(hg_ctx *x, void *out);
 hg_status hg_p2p_open(hg_ctx *x, const void *all);

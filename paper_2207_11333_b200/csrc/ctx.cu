@@ -1215,7 +1215,13 @@ hg_status hg_p2p_handle(hg_ctx *x, void *out) {
   if (get_range(&base, &size, (CUdeviceptr)x->ws) != CUDA_SUCCESS)
     return fail(HG_E_CUDA, "cuMemGetAddressRange failed on the workspace");
   cudaIpcMemHandle_t h;
-  CK(x, cudaIpcGetMemHandle(&h, (void *)base));
+  // (not sticky: an allocation without IPC support, e.g. expandable segments, only means
+  // the caller keeps the NCCL exchange)
+  const cudaError_t ie = cudaIpcGetMemHandle(&h, (void *)base);
+  if (ie != cudaSuccess) {
+    cudaGetLastError();
+    return fail(HG_E_CUDA, "cudaIpcGetMemHandle: %s (workspace not IPC-capable)", cudaGetErrorString(ie));
+  }
   const int64_t off = (int64_t)((uintptr_t)x->ws - (uintptr_t)base);
   std::memcpy(out, &h, sizeof(h));
   std::memcpy((uint8_t *)out + sizeof(h), &off, sizeof(off));
@@ -1225,7 +1231,16 @@ hg_status hg_p2p_handle(hg_ctx *x, void *out) {
 hg_status hg_p2p_open(hg_ctx *x, const void *all) {
   hg_status st = usable(x);
   if (st) return st;
-  if (!all) return fail(HG_E_INVALID, "null handles");
+  if (!all) {  // back to the NCCL exchange (mappings stay open until destroy)
+    if (x->p2p)
+      for (auto &g : x->graphs)
+        if (g) {
+          cudaGraphExecDestroy(g);
+          g = nullptr;
+        }
+    x->p2p = false;
+    return HG_OK;
+  }
   if (x->world < 2 || x->world > kP2PMaxWorld) return fail(HG_E_INVALID, "p2p needs 2..8 ranks (hg_comm_init first)");
   static_assert(sizeof(cudaIpcMemHandle_t) + 8 == HG_P2P_HANDLE_BYTES, "handle size");
   CK(x, cudaSetDevice(x->device));

@@ -474,15 +474,33 @@ class Context:
         exchange (include/hgnn.h hg_p2p_open); call after comm_init on every rank."""
         import torch
         import torch.distributed as dist
-        rec = np.zeros(P2P_HANDLE_BYTES, np.uint8)
-        _check(_lib.hg_p2p_handle(self.handle, _ptr(rec)))
         backend = dist.get_backend(group)
         dev = f"cuda:{self.device}" if backend == "nccl" else "cpu"
+
+        def all_ok(ok: bool) -> bool:  # every rank takes the same path
+            f = torch.tensor([1 if ok else 0], device=dev)
+            dist.all_reduce(f, op=dist.ReduceOp.MIN, group=group)
+            return bool(f.item())
+
+        rec = np.zeros(P2P_HANDLE_BYTES, np.uint8)
+        err = None
+        try:
+            _check(_lib.hg_p2p_handle(self.handle, _ptr(rec)))
+        except HgError as e:
+            err = e
+        if not all_ok(err is None):
+            raise err or HgError(8, "peer-memory exchange unavailable on another rank")  # HG_E_CUDA
         t = torch.from_numpy(rec).to(dev)
         allt = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(allt, t, group=group)
         allh = np.ascontiguousarray(np.concatenate([a.cpu().numpy() for a in allt]))
-        _check(_lib.hg_p2p_open(self.handle, _ptr(allh)))
+        try:
+            _check(_lib.hg_p2p_open(self.handle, _ptr(allh)))
+        except HgError as e:
+            err = e
+        if not all_ok(err is None):
+            _lib.hg_p2p_open(self.handle, None)  # back to NCCL everywhere
+            raise err or HgError(8, "peer-memory exchange unavailable on another rank")  # HG_E_CUDA
 
     def allreduce_grads(self):
         _check(_lib.hg_allreduce_grads(self.handle))
