@@ -62,7 +62,9 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
                                                       const __grid_constant__ CUtensorMap ones, Op op_in) {
   constexpr int BN = Op::BN, ST = n_stages<Op>(), NB = BN / 32;
   constexpr int A_BYTES = 4 * N_BOX, B_BYTES = NB * N_BOX, STAGE = n_stage_bytes<Op>();
-  constexpr int TCOLS = 2 * BN <= 256 ? 256 : 512;
+  // two buffers of the main accumulator at [0, 2BN), two of the correction accumulator
+  // (hi*lo + lo*hi) at [2BN, 4BN) -- see tcdirect.cu k_tma (DESIGN.md F-accumulate)
+  constexpr int TCOLS = 4 * BN <= 256 ? 256 : 512;
   static_assert(BN % 32 == 0 && BN >= 32 && BN <= 256 && ST >= 2, "tile");
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -147,7 +149,7 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
       const int buf = tcount & 1;
       if (tcount >= 2) tc::mbar_wait(&acce[buf], ((tcount >> 1) - 1) & 1);
       tc::fence_after_sync();
-      const uint32_t d = tmem + (uint32_t)(buf * BN);
+      const uint32_t d = tmem + (uint32_t)(buf * BN), dc = d + (uint32_t)(2 * BN);
       const int nch = (w.len + N_BK - 1) / N_BK;
       for (int c = 0; c < nch; ++c, ++it) {
         const int s = it % ST;
@@ -180,8 +182,8 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
             } else {
               const uint64_t dbl = tc::desc_mn32(bL + off, N_BOX, 512);
               tc::mma_tf32(d, dah, dbh, idesc, acc);
-              tc::mma_tf32(d, dah, dbl, idesc, 1u);
-              tc::mma_tf32(d, dal, dbh, idesc, 1u);
+              tc::mma_tf32(dc, dah, dbl, idesc, acc);
+              tc::mma_tf32(dc, dal, dbh, idesc, 1u);
             }
           }
           tc::mma_commit(&empty[s]);
@@ -211,12 +213,11 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
       } else {
 #pragma unroll 1
         for (int q = 0; q < BN / 32; ++q) {
-          float acc[32];
+          float acc[32], cor[32];
           tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
-          if (empty_item) {
+          tc::tmem_ld32(trow + (uint32_t)(2 * BN + q * 32), cor);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) acc[i] = 0.f;
-          }
+          for (int i = 0; i < 32; ++i) acc[i] = empty_item ? 0.f : acc[i] + cor[i];
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             *reinterpret_cast<float4 *>(stg + lane * N_STG_LD + 4 * j) =
