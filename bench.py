@@ -74,7 +74,6 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--store-dir", default="")
     ap.add_argument("--seed", type=int, default=11)
-    ap.add_argument("--tc-mode", type=int, default=0, help="pipeline experiment switch (timing only)")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 gradient exchange: fused peer-memory reduce/AdamW/all-gather kernel or bucketed NCCL")
     return ap.parse_args()
@@ -242,8 +241,6 @@ def main():
     cfg = hgnn.make_config(data["f_node"], 4, H, L, B, max_nodes, max_edges, delta, n_slots=n_res + e2e_slots,
                            max_degree=st["max_degree"])
     ctx = hgnn.Context(cfg, device=local_rank)
-    if args.tc_mode:
-        hgnn.load().hg_debug_set_tc_mode(args.tc_mode)
     ctx.params_init(1234)
     ctx.comm_init(rank, world)
     exchange = args.exchange if world > 1 else "none"

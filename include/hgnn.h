@@ -41,7 +41,8 @@ typedef enum {
   HG_E_RANGE = 3,      /* IndexOutOfRange: graph id or node id out of range */
   HG_E_EMPTY = 4,      /* EmptyBatch / EmptyGraphSlot */
   HG_E_ASYMMETRIC = 5, /* edge list not symmetric with identical attributes */
-  HG_E_DEGREE = 6,     /* a node degree exceeds HG_MAX_DEGREE */
+  HG_E_DEGREE = 6,     /* a node degree exceeds HG_MAX_DEGREE / max_degree, or a batch holds more
+                          distinct node degrees than the ctx's degree-class slots */
   HG_E_CAPACITY = 7,   /* batch exceeds the ctx capacities (max_graphs / max_nodes / max_edges) */
   HG_E_CUDA = 8,       /* CUDA runtime failure */
   HG_E_NCCL = 9,       /* NCCL failure (TransportFailure) */
@@ -118,18 +119,23 @@ typedef struct {
   double delta;                      /* PNA degree statistic (hg_degree_stat) */
   float var_floor;                   /* epsilon_v for the std aggregator, 1e-10 */
   int32_t max_degree;                /* capacity: largest node degree in a batch (0 = HG_MAX_DEGREE).
-                                        <= 15 enables the degree-class GEMMs. */
+                                        Degree-class slots = min(max_degree + 1, 32): a batch may hold
+                                        at most that many DISTINCT node degrees (HG_E_DEGREE at pack
+                                        time otherwise; molecules: <= 6). DESIGN.md §6. */
 } hg_config;
 
-/* hg_config.flags: force the SIMT fp32 GEMMs instead of the tcgen05 3xTF32
- * tensor-core GEMMs (which are used whenever hidden % 128 == 0). */
-#define HG_FLAG_SIMT_GEMM 1
+/* hg_config.flags: HG_FLAG_TF32 selects the reduced-precision GEMM mode (
+ * PAPER.md:212): every tensor-core contraction runs ONE tf32 pass (operands truncated to
+ * tf32, fp32 accumulate) instead of the fp32-accurate 3xTF32 default. Everything else
+ * (aggregation, head, loss, AdamW, the exchange) stays fp32. Its parity bars are looser
+ * (DESIGN.md §3 "TF32 mode": forward 1e-2, gradients 5e-2 normwise). */
+#define HG_FLAG_TF32 1
 
-/* Channel padding for widths that are not a multiple of 32, e.g. the paper's
- * H = 55 and H = 200 (SURVEY §8(d) "Padding hazard").
- * Writes to *out the configuration the kernels actually run: hidden rounded up
- * to a multiple of 128 (the tensor-core tile; 32 with HG_FLAG_SIMT_GEMM) and
- * fc_hidden padded alike when it equals hidden; *out = *c when hidden % 32 == 0.
+/* Channel padding for widths that are not a multiple of the tensor-core tile (128),
+ * e.g. the paper's H = 55 and H = 200 (SURVEY §8(d) "Padding
+ * hazard"), or config A's H = 32. Writes to *out the configuration the kernels
+ * actually run: hidden rounded up to a multiple of 128 and fc_hidden padded alike
+ * when it equals hidden; *out = *c when hidden % 128 == 0.
  * The padded channels compute exact zeros: padded parameter entries start at
  * zero, the std aggregator of a padded channel is forced to 0 (not
  * sqrt(var_floor)), so every padded gradient is exactly zero and AdamW keeps
@@ -166,6 +172,9 @@ hg_status hg_batch_offsets_get(int32_t B, int32_t N, int32_t E, int32_t f_node, 
  * cfg), HG_E_CAPACITY (exceeds cfg capacities or cap). *used = blob bytes. */
 hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const hg_config *cfg,
                        void *dst, size_t cap, size_t *used);
+/* Host threads one collation (hg_pack / hg_pack_host) uses, process-wide (default 4; the
+ * packed bytes do not depend on it). HG_E_INVALID outside [1, 1024]. */
+hg_status hg_pack_threads_set(int32_t threads);
 
 /* Host-side parameter initialisation into a flat fp32 array laid out like the
  * device arena (hg_param_info offsets; padding zero). SPEC.md:339, 401 with the
@@ -219,7 +228,8 @@ hg_status hg_batch_get(hg_ctx *x, int32_t slot, void *dst, size_t cap, size_t *u
  * that slot waits for it. The staging buffer is reused only after its
  * previous copy completed. Errors as hg_pack_host. */
 hg_status hg_pack(hg_ctx *x, const hg_store *s, const int64_t *ids, int32_t B, int32_t slot);
-/* Copy an already packed blob (host pointer, e.g. from hg_pack_host) into `slot`. */
+/* Copy an already packed blob (host pointer, e.g. from hg_pack_host) into `slot`. The blob is
+ * validated first (header, capacities, offsets, degrees, distinct-degree count). */
 hg_status hg_upload_packed(hg_ctx *x, const void *blob, size_t bytes, int32_t slot);
 
 /* Forward pass on the batch in `slot`: L GC layers, global
@@ -231,11 +241,19 @@ hg_status hg_forward(hg_ctx *x, int32_t slot);
 hg_status hg_backward(hg_ctx *x, int32_t slot);
 
 /* NCCL data-parallel plumbing. The 128-byte unique id is
- * produced on rank 0 and distributed by the caller (e.g. torch.distributed). */
+ * produced on rank 0 and distributed by the caller (e.g. torch.distributed).
+ * hg_comm_init: world == 1 with id128 == NULL sets rank/world only (no communicator:
+ * the exchange is a no-op); with an id (world >= 1) it creates the NCCL communicator, so
+ * a one-rank communicator runs the bucketed average path too. HG_E_STATE if called twice. */
 hg_status hg_nccl_unique_id(void *out128);
 hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world);
-/* Mean over ranks of the gradient arena; no-op when world == 1. */
+/* Mean over ranks of the gradient arena; no-op without a communicator. */
 hg_status hg_allreduce_grads(hg_ctx *x);
+/* The gradient buckets of a configuration (host-only): *n = bucket count; ranges (capacity
+ * `cap` buckets, nullable) receives [begin, end) float offsets into the flat parameter arena
+ * of the INTERNAL layout (hg_config_internal), in backward (launch) order: bucket 0 = head +
+ * the last layers ... last bucket = conv0. Together they cover the arena exactly once. */
+hg_status hg_bucket_layout(const hg_config *c, int64_t *ranges, int32_t cap, int32_t *n);
 
 /* Gradient exchange over NVLink peer memory (reduce-scatter ->
  * sharded fused AdamW -> all-gather, as ONE kernel; PAPER.md:206-212 DDP averaging).
@@ -250,14 +268,31 @@ hg_status hg_allreduce_grads(hg_ctx *x);
  * 1/W shard of the flat arena in rank order over peer loads, divides by W, applies
  * AdamW and stores the new parameters into every rank's arena; a done flag per rank
  * closes the step. Deterministic; parameters stay bitwise identical across ranks.
- * The Adam moments become sharded: rank r's m, v are valid on its shard only
- * (hg_opt_state_get returns the local arrays). The eager hg_allreduce_grads / hg_step
- * path keeps using NCCL. Every rank must run the same sequence of steps.
- * hg_p2p_open(x, NULL) returns this ctx to the NCCL exchange (captured graphs are
- * rebuilt on their next use). */
+ * The Adam moments become sharded (rank r updates m, v of its shard only); every call that
+ * needs whole moments first gathers the peers' shards over peer memory, stream-ordered:
+ * hg_opt_state_get, hg_step, hg_profile_step and hg_p2p_open(x, NULL) (which returns this
+ * ctx to the NCCL exchange; captured graphs are rebuilt on their next use). Such calls are
+ * collective: every rank makes them at the same point of its step sequence. The eager
+ * hg_train_step(graph = 0) returns HG_E_STATE while the peer-memory exchange is on.
+ * Every flag wait is bounded by hg_set_timeout (a dead peer traps the step: HG_E_CUDA). */
 #define HG_P2P_HANDLE_BYTES 72
 hg_status hg_p2p_handle(hg_ctx *x, void *out);
 hg_status hg_p2p_open(hg_ctx *x, const void *all);
+
+/* Validation entry for the peer-memory exchange on ONE device: world (2..8) contexts of one
+ * process and one configuration act as the ranks. After every context ran its backward,
+ * the exchange kernels of every rank (the same k_p2p_signal / k_p2p_adamw as
+ * hg_p2p_open's captured step) run back to back on ctxs[0]'s stream with the flag waits
+ * elided (ranks that spin on one another must not share a GPU, B200_PROFILING.md), then
+ * synchronise. Afterwards the contexts are ranks 0..world-1 with sharded moments (see above).
+ * HG_E_STATE if a context holds a communicator. */
+hg_status hg_p2p_emulate(hg_ctx *const *ctxs, int32_t world, const hg_adamw *h);
+
+/* Fail-stop bound, seconds (0 = none, the default): every device
+ * flag wait of the peer-memory exchange traps past it (the step then fails with HG_E_CUDA),
+ * and hg_sync returns HG_E_NCCL after aborting the NCCL communicator when its streams have
+ * not drained within it. Captured graphs are rebuilt on their next use. */
+hg_status hg_set_timeout(hg_ctx *x, double seconds);
 
 /* Fused AdamW over the whole parameter arena. */
 hg_status hg_step(hg_ctx *x, const hg_adamw *h);
@@ -333,7 +368,9 @@ hg_status hg_loss_get(hg_ctx *x, float *loss);
 #define HG_LOSS_RING 4
 hg_status hg_loss_enqueue(hg_ctx *x, int32_t i);
 hg_status hg_loss_fetch(hg_ctx *x, int32_t i, float *loss);
-/* Synchronise the ctx's streams; surfaces sticky CUDA/NCCL errors. */
+/* Synchronise the ctx's streams; surfaces sticky CUDA/NCCL errors. Polls NCCL's async error
+ * while waiting: an NCCL failure, a CUDA fault or the hg_set_timeout bound aborts the
+ * communicator and makes the ctx unusable (fail-stop). */
 hg_status hg_sync(hg_ctx *x);
 /* Number of kernels this ctx has launched (graph replays count their kernel nodes). */
 hg_status hg_launch_count(const hg_ctx *x, int64_t *count);

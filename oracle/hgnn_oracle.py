@@ -415,44 +415,26 @@ def train_step(params, state, store, ids, cfg, delta, hyper=None, world=1):
 
 
 # --------------------------------------------------------------------------
-# decision bands for parity
+# decision replay for parity
 # --------------------------------------------------------------------------
-def decision_bands(cache: dict, tau: float = 1e-6, var_floor: float = VAR_FLOOR) -> list:
-    """Per layer, boolean masks of the cells whose discrete decision is
-    numerically ambiguous at relative margin ``tau``: |Z| < tau*|Z|_inf (ReLU),
-    top-2 gap between distinct values < tau*|m|_inf (argmax / argmin),
-    |var - eps_v| < 0.5 eps_v (std floor)."""
-    out = []
-    for c in cache["layers"]:
-        zs = np.abs(c["Z"]).max() if c["Z"].size else 0.0
-        relu_band = np.abs(c["Z"]) < tau * zs
-        msg = c["msg"]
-        ms = np.abs(msg).max() if msg.size else 0.0
-        rowptr = np.concatenate([[0], np.cumsum(c["deg"])])
-        row = np.repeat(np.arange(c["N"]), c["deg"])
-        mx2 = _seg_reduce(np.maximum, np.where(msg == c["mx"][row], -np.inf, msg), rowptr, -np.inf)
-        mn2 = _seg_reduce(np.minimum, np.where(msg == c["mn"][row], np.inf, msg), rowptr, np.inf)
-        max_band = (c["mx"] - mx2) < tau * ms
-        min_band = (mn2 - c["mn"]) < tau * ms
-        var_band = np.abs(c["var"] - var_floor) < 0.5 * var_floor
-        out.append(dict(relu=relu_band, argmax=max_band, argmin=min_band, varflag=var_band))
-    return out
-
-
-def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
+def replay(cache: dict, gpu: list, tau_arg: float = 1e-6, tau_relu=1e-6, tau_head: float = 1e-6,
+           head_relu_gpu=None):
     """Decision replay for parity: where several discrete
-    decisions are correct at tolerance tau, adopt the GPU's; check the rest.
+    decisions are correct, adopt the GPU's; check the rest.
 
-    For every cell the GPU's decision is *valid* if it is optimal within tau
-    in the oracle's own float64 values:
-      argmax: m[gpu position] >= max - tau*|m|_inf   (argmin symmetric),
+    A GPU decision is *valid* if it is optimal within a band in the oracle's own
+    float64 values:
+      argmax: m[gpu position] >= max - tau_arg*|m|_inf   (argmin symmetric),
+              tau_arg = 1e-6 (SURVEY C8);
       relu:   Z >= -tau*|Z|_inf if the GPU kept the unit, Z <= tau*|Z|_inf if not,
+              tau = tau_relu (per layer: a float, or a list with one value per
+              layer) -- the parity harness passes the GPU's measured forward error
+              bound of that layer (DESIGN.md reading R-replay); tau_head for the head;
       varflag: var within 0.5*eps_v of eps_v, or the same side as the GPU.
-    Valid GPU decisions are adopted (exact ties such as automorphic atoms,
-    whose float64 and fp32 roundings can break the tie differently, are
-    legitimately resolved either way); invalid ones are counted and the
-    oracle keeps its own decision, so they show up in the gradient error too.
-    tau defaults to the forward tolerance 1e-4 (reading R-replay).
+    Valid GPU decisions are adopted (exact ties such as automorphic atoms, whose
+    float64 and fp32 roundings can break the tie differently, are legitimately
+    resolved either way); invalid ones are counted and the oracle keeps its own
+    decision, so they show up in the gradient error too.
     Overrides whose two candidates are equal to float64 rounding (|gap| <= 1e-12 of
     the layer's max, i.e. algebraic ties such as automorphic atoms, where the
     oracle's own summation order decides) are counted apart as 'tie_overrides'.
@@ -463,6 +445,7 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
     by = {"relu": 0, "argmax": 0, "argmin": 0, "varflag": 0, "head_relu": 0}
     ov = dict(by)  # overrides per decision kind (diagnostic)
     for l, (c, gdec) in enumerate(zip(cache["layers"], gpu)):
+        tau_r = float(tau_relu[l]) if np.ndim(tau_relu) else float(tau_relu)
         zs = np.abs(c["Z"]).max() if c["Z"].size else 0.0
         msg = c["msg"]
         ms = np.abs(msg).max() if msg.size else 0.0
@@ -473,7 +456,7 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
         d = dict(own)
         if "relu" in gdec:
             g = np.asarray(gdec["relu"])
-            valid = np.where(g, c["Z"] >= -tau * zs, c["Z"] <= tau * zs)
+            valid = np.where(g, c["Z"] >= -tau_r * zs, c["Z"] <= tau_r * zs)
             diff = g != own["relu"]
             tie = np.abs(c["Z"]) <= TIE * zs
             n += int((valid & diff & ~tie).sum())
@@ -493,7 +476,7 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
             chan = np.broadcast_to(np.arange(msg.shape[1] if msg.size else g.shape[1]), g.shape)
             gval = msg[idx, chan] if msg.size else np.zeros(g.shape)
             ext = c["mx"] if sign > 0 else c["mn"]
-            valid = (sign * (gval - ext) >= -tau * ms) & (g < np.maximum(deg, 1)[:, None])
+            valid = (sign * (gval - ext) >= -tau_arg * ms) & (g < np.maximum(deg, 1)[:, None])
             valid |= ~has
             diff = (g != own[k]) & has
             tie = np.abs(gval - ext) <= TIE * ms
@@ -520,7 +503,7 @@ def replay(cache: dict, gpu: list, tau: float = 1e-4, head_relu_gpu=None):
         hs = np.abs(hp).max() if hp.size else 0.0
         g = np.asarray(head_relu_gpu)
         own = hp > 0
-        valid = np.where(g, hp >= -tau * hs, hp <= tau * hs)
+        valid = np.where(g, hp >= -tau_head * hs, hp <= tau_head * hs)
         diff = g != own
         tie = np.abs(hp) <= TIE * hs
         n += int((valid & diff & ~tie).sum())

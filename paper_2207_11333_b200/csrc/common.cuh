@@ -40,20 +40,14 @@ __device__ __forceinline__ int batch_N(const uint8_t *blob) { return reinterpret
 
 inline int cdiv(int a, int b) { return (a + b - 1) / b; }
 
-// ------------------------------------------------ programmatic dependent launch
-// Every kernel of the step is launched with programmatic stream serialization:
-// its CTAs may become resident while the previous kernel is still running, and
-// each kernel starts with pdl_enter(), which blocks until the previous grid has
-// completed and flushed its writes (griddepcontrol.wait), then lets the next
-// kernel begin launching (griddepcontrol.launch_dependents). Because EVERY
-// kernel waits before touching global memory, completion of kernel k implies
-// completion of all kernels before it, so stream order is preserved
-// transitively; the gain is that launch latency overlaps the previous kernel.
-extern bool g_pdl;
+// ------------------------------------------------ launches
 // launch priority: kernels enqueued while g_low_prio is set (side-stream weight
 // gradients) get the device's lowest priority, all others its highest
 extern bool g_low_prio;
 extern int g_prio_lo, g_prio_hi;
+// Every kernel starts with pdl_enter() (griddepcontrol.wait / launch_dependents): a no-op
+// under plain stream ordering, it makes the kernels safe to launch with programmatic
+// dependent launch (measured slower for this step: DESIGN.md §7, so it is not enabled).
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -61,18 +55,16 @@ __device__ __forceinline__ void pdl_enter() {
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                              Args &&...args) {
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
-  attr[1].id = cudaLaunchAttributePriority;
-  attr[1].val.priority = g_low_prio ? g_prio_lo : g_prio_hi;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributePriority;
+  attr[0].val.priority = g_low_prio ? g_prio_lo : g_prio_hi;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cfg.attrs = attr;
-  cfg.numAttrs = 2;
+  cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 constexpr int kSMs = 148;

@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <filesystem>
+#include <new>
 #include <string>
 #include <thread>
 #include <vector>
@@ -205,9 +207,26 @@ hg_status hg_container_open(const char *dir, int32_t threads, hg_store **out) {
   if (fread(&m, sizeof(m), 1, f.f) != 1 || std::memcmp(m.magic, "HGPK", 4) != 0)
     return fail(HG_E_IO, "%s: bad magic", mpath.c_str());
   if (m.version != kVersion) return fail(HG_E_IO, "%s: unsupported version %u", mpath.c_str(), m.version);
-  if (m.G < 1 || m.N < 1 || m.E < 0 || m.F0 < 1 || m.Fe < 1 || m.n_sub < 1 || m.n_sub > m.G)
+  if (m.G < 1 || m.N < 1 || m.E < 0 || m.F0 < 1 || m.Fe < 1 || m.Fe > 8 || m.n_sub < 1 || m.n_sub > m.G)
     return fail(HG_E_IO, "%s: corrupt header", mpath.c_str());
-  hg_store *s = new hg_store();
+  {  // the index must fit its file, and the data its subfiles' total size, before anything is allocated
+    std::error_code ec;
+    const uint64_t isz = std::filesystem::file_size(mpath, ec);
+    const uint64_t need = sizeof(m) + 16ull * ((uint64_t)m.G + 1) + 8ull * ((uint64_t)m.n_sub + 1) + 4;
+    if (ec || isz != need) return fail(HG_E_IO, "%s: index size %llu != %llu (corrupt header)", mpath.c_str(),
+                                       (unsigned long long)isz, (unsigned long long)need);
+    uint64_t dsz = 0;
+    for (int32_t k = 0; k < m.n_sub; ++k) {
+      const uint64_t z = std::filesystem::file_size(base + "/data." + std::to_string(k), ec);
+      if (ec) return fail(HG_E_IO, "missing subfile %s/data.%d (MissingSubfile)", dir, k);
+      dsz += z;
+    }
+    const long double bytes = 4.0L * ((long double)m.N * m.F0 + (long double)m.E * (2 + m.Fe) + m.G);
+    if (bytes > (long double)dsz) return fail(HG_E_IO, "%s: header counts exceed the subfiles' size", mpath.c_str());
+  }
+  hg_store *s = nullptr;
+  try {
+    s = new hg_store();
   s->G = m.G; s->N = m.N; s->E = m.E; s->F0 = m.F0; s->Fe = m.Fe;
   s->own_no.resize(m.G + 1);
   s->own_eo.resize(m.G + 1);
@@ -222,6 +241,12 @@ hg_status hg_container_open(const char *dir, int32_t threads, hg_store **out) {
     c = crc32(sub.data(), sizeof(int64_t) * sub.size(), c);
     ok = c == stored && s->own_no[0] == 0 && s->own_eo[0] == 0 && s->own_no[m.G] == m.N && s->own_eo[m.G] == m.E &&
          sub[0] == 0 && sub[m.n_sub] == m.G;
+    // every subfile range and every offset selects memory inside the arrays (they become fread
+    // destinations below): sub strictly increasing in [0, G], offsets non-decreasing in [0, N|E]
+    for (int32_t k = 0; ok && k < m.n_sub; ++k) ok = sub[k] < sub[k + 1] && sub[k + 1] <= m.G;
+    for (int64_t g = 0; ok && g < m.G; ++g)
+      ok = s->own_no[g] <= s->own_no[g + 1] && s->own_no[g + 1] <= m.N && s->own_eo[g] <= s->own_eo[g + 1] &&
+           s->own_eo[g + 1] <= m.E;
   }
   if (!ok) {
     delete s;
@@ -255,6 +280,10 @@ hg_status hg_container_open(const char *dir, int32_t threads, hg_store **out) {
     return st;
   }
   return adopt(s, threads, out);
+  } catch (const std::bad_alloc &) {
+    delete s;
+    return fail(HG_E_IO, "%s: header sizes exceed the host memory (corrupt header?)", mpath.c_str());
+  }
 }
 
 // ---- comparison backend: one object file per graph ("g<id>.obj": header + the
@@ -316,7 +345,8 @@ hg_status hg_objfiles_open(const char *dir, int64_t num_graphs, int32_t threads,
     int64_t hdr[4];
     std::memcpy(hdr, obj[g].data(), sizeof(hdr));
     const int32_t F0 = (int32_t)(hdr[3] >> 32), Fe = (int32_t)(hdr[3] & 0xFFFFFFFF);
-    if (hdr[0] != 0x424F4748 || hdr[1] < 1 || hdr[2] < 0 || (g > 0 && (F0 != s->F0 || Fe != s->Fe)) ||
+    if (hdr[0] != 0x424F4748 || hdr[1] < 1 || hdr[2] < 0 || F0 < 1 || Fe < 1 || Fe > 8 ||
+        (g > 0 && (F0 != s->F0 || Fe != s->Fe)) ||
         obj[g].size() != 32 + sizeof(float) * (hdr[1] * F0 + hdr[2] * Fe + 1) + sizeof(int32_t) * 2 * hdr[2]) {
       delete s;
       return fail(HG_E_IO, "object %lld: corrupt", (long long)g);

@@ -8,7 +8,9 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdlib>
+#include <thread>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -19,6 +21,7 @@
 #include "layout.h"
 
 using namespace hg;
+static_assert(kClassSlots == kMaxClasses, "degree-class slots (internal.h) == kernels.h");
 
 namespace {
 
@@ -29,20 +32,20 @@ struct Plan {
   size_t amp = 0, att = 0;
   std::vector<size_t> P, A, arg, X;  // X[l] = output of layer l (X_{l+1})
   size_t dA = 0;
-  // per layer l: dZ[l] = dL/dX_l (class path: degree-sorted rows), dP[l], their lo
-  // terms and the dM_e block partials -- one buffer per layer so the side-stream
-  // readers never hold up the main chain (no write-after-read waits)
-  std::vector<size_t> dZ, dZ_lo, dPl, dPl_lo, pagg;
+  // per layer l: dZ[l] = dL/dX_l (degree-sorted rows), dP[l] and the dM_e block partials --
+  // one buffer per layer so the side-stream readers never hold up the main chain (no
+  // write-after-read waits)
+  std::vector<size_t> dZ, dPl, pagg;
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
-  size_t part = 0, part2 = 0, part3 = 0;
-  size_t eval_acc = 0;  // scratch: agg_bwd (dM_e), Gram (dU), dM_x partials
-  size_t UT = 0, u_off = 0;
-  int cmax = 0;  // degree-class slots (0 = class GEMMs off)
+  size_t part = 0, part2 = 0, part3 = 0;  // split partials: spare, Gram (dU), dM_x
+  size_t eval_acc = 0;
+  size_t u_off = 0;
+  int cmax = 0;  // degree-class slots
   size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
-  // direct-GEMM residuals x - trunc19(x) (class path): operands and weights
-  size_t Wf_lo = 0, WbT_lo = 0, ones = 0, xpad = 0, xpad_lo = 0;
-  std::vector<size_t> A_lo, X_lo;  // per layer (the backward Grams read them)
-  std::vector<size_t> Xs, Xs_lo;   // per layer: X_l in degree-sorted rows (fused dX->dA path)
+  // residuals w - trunc19(w) of the weight operands (activations' lo terms are derived in
+  // shared memory by the GEMM kernels)
+  size_t Wf_lo = 0, WbT_lo = 0, ones = 0, xpad = 0;
+  std::vector<size_t> Xs;          // per layer: X_l in degree-sorted rows (fused dX->dA path)
   std::vector<size_t> Xmask;       // per layer: ReLU mask bits of X_l, sorted rows, [N][H/32]
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t p2p = 0;  // P2PDev flags of the peer-memory gradient exchange
@@ -91,48 +94,30 @@ Plan make_plan(const hg_config &c) {
   p.dy = take(sizeof(float) * B);
   p.sqerr = take(sizeof(float) * B);
   Caps caps{c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge, c.hidden, c.fc_hidden};
-  size_t pf = std::max({agg_bwd_partial_floats(caps), dU_partial_floats(caps), dMx_partial_floats(caps, c.f_node),
-                        dMx_partial_floats(caps, c.hidden)});
-  if (tc_supported(caps))
-    pf = std::max({pf, tc_dU_partial_floats(caps), tc_dMx_partial_floats(caps, c.hidden)});
-  p.part = take(sizeof(float) * pf);
-  p.cmax = tc_num_classes(caps, c.max_degree);
-  p.UT = take(p.cmax ? 256 : sizeof(float) * (size_t)c.layers * 12 * H * H);
+  p.cmax = tc_num_classes(c.max_degree);
   p.u_off = take(sizeof(int64_t) * (size_t)c.layers);
   p.perm = take(sizeof(int) * N);
   p.pos = take(sizeof(int) * N);
   p.deginfo = take(sizeof(DegInfo));
-  if (p.cmax) {
-    p.tiles = take(sizeof(int4) * (size_t)tc_max_tiles(caps, p.cmax));
-    p.splits = take(sizeof(int4) * (size_t)tc_max_splits(caps, p.cmax));
-    p.Wf = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-    p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-    p.Wf_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-    p.WbT_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-    for (int l = 0; l < c.layers; ++l) {
-      p.A_lo.push_back(take(sizeof(float) * N * 4 * H));
-      p.X_lo.push_back(take(sizeof(float) * N * H));
-      p.Xs.push_back(take(sizeof(float) * N * H));
-      p.Xs_lo.push_back(take(sizeof(float) * N * H));
-      p.Xmask.push_back(take(sizeof(uint32_t) * N * ((H + 31) / 32)));
-    }
-    p.ones = take(sizeof(float) * N * 32);  // B operand of the column-sum tiles
-    if (pad_x0_width(c.f_node) <= 256) {      // layer-0 features for the TMA dM_x Gram
-      p.xpad = take(sizeof(float) * N * pad_x0_width(c.f_node));
-      p.xpad_lo = take(sizeof(float) * N * pad_x0_width(c.f_node));
-    }
-    for (int l = 0; l < c.layers; ++l) {
-      p.dZ_lo.push_back(take(sizeof(float) * N * H));
-      p.dPl_lo.push_back(take(sizeof(float) * N * H));
-    }
-    p.Mx_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
-    p.MxT = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
-    p.MxT_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
-    p.mx_off = take(sizeof(int64_t) * (size_t)c.layers);
-    pf = std::max({pf, mn_gram_partial_floats(caps, p.cmax),
-                   mn_dmx_partial_floats(caps, H)});
-    p.part = take(sizeof(float) * pf);  // (re-take: the class partials are larger)
+  p.tiles = take(sizeof(int4) * (size_t)tc_max_tiles(caps, p.cmax));
+  p.splits = take(sizeof(int4) * (size_t)tc_max_splits(caps, p.cmax));
+  p.Wf = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+  p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+  p.Wf_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+  p.WbT_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+  for (int l = 0; l < c.layers; ++l) {
+    p.Xs.push_back(take(sizeof(float) * N * H));
+    p.Xmask.push_back(take(sizeof(uint32_t) * N * ((H + 31) / 32)));
   }
+  p.ones = take(sizeof(float) * N * 32);  // B operand of the column-sum tiles
+  p.xpad = take(sizeof(float) * N * pad_x0_width(c.f_node));  // layer-0 features for the TMA dM_x Gram
+  p.Mx_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
+  p.MxT = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
+  p.MxT_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
+  p.mx_off = take(sizeof(int64_t) * (size_t)c.layers);
+  const size_t pf = std::max({mn_gram_partial_floats(caps, p.cmax), mn_dmx_partial_floats(caps, H),
+                              mn_dmx_partial_floats(caps, c.f_node)});
+  p.part = take(sizeof(float) * 4);
   p.part2 = take(sizeof(float) * pf);
   p.part3 = take(sizeof(float) * pf);
   for (int l = 0; l < c.layers; ++l) p.pagg.push_back(take(sizeof(float) * agg_bwd_partial_floats(caps)));
@@ -166,18 +151,19 @@ struct hg_ctx {
   std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
-  cudaStream_t adam_stream = nullptr;
-  bool p2p = false;                        // gradient exchange over peer memory (hg_p2p_open)
+  cudaStream_t adam_stream = nullptr;  // early AdamW of layers >= 1 (must not delay layer 0's side-stream work)
+  bool p2p = false;                        // captured steps exchange over peer memory (hg_p2p_open)
+  bool mv_sharded = false;                 // Adam moments valid on this rank's shard only (after p2p steps)
   uint8_t *peer_ws[kP2PMaxWorld] = {};     // every rank's workspace ([rank] = ws)
-  void *peer_base[kP2PMaxWorld] = {};      // opened IPC mappings (closed at destroy)  // early AdamW of layers >= 1 (must not delay layer 0's side-stream work)
+  void *peer_base[kP2PMaxWorld] = {};      // opened IPC mappings (closed at destroy)
+  unsigned long long timeout_ns = 0;       // fail-stop bound of device flag waits and hg_sync (0 = none)
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx;  // per layer fork / join points
-  cudaEvent_t ev_head = nullptr, ev_deg = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_hgrad = nullptr,
-              ev_prepmx = nullptr, ev_prepw = nullptr, ev_ar1 = nullptr, ev_adam = nullptr;
+  cudaEvent_t ev_head = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_prepmx = nullptr, ev_prepw = nullptr,
+              ev_ar1 = nullptr, ev_adam = nullptr;
   float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
-  bool use_tc = false;  // tcgen05 3xTF32 GEMMs (else SIMT fp32)
-  bool dxda = false;    // fused dX -> dA backward kernel (class path, H == 128; HG_DXDA=0 disables)
+  bool dxda = false;    // fused dX -> dA backward kernel (H == 128)
   hg_status sticky = HG_OK;
   std::string sticky_msg;
 
@@ -275,88 +261,72 @@ int bucket_closed_by(const hg_ctx *x, int l);
 // ---- the step's kernel sequence (enqueue only) ----
 void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool fuse_head_bwd = false) {
   const hg_config &c = x->cfg;
+  g_gemm_passes = (c.flags & HG_FLAG_TF32) ? 1 : 3;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
   float *amp = x->f(p.amp), *att = x->f(p.att);
-  const bool cls = x->use_tc && p.cmax > 0;
-  const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
+  const int *pos = reinterpret_cast<const int *>(x->b(p.pos));  // sorted A / dZ rows
+  const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
   const size_t HH = (size_t)c.hidden * c.hidden;
-  // Degree sort on side stream 1 and the degree-slot / M_x weight preparation on
-  // side stream 2 (they depend only on the batch resp. the parameters), concurrent
-  // with layer 0's projection; the main chain joins the sort before layer 0's
-  // aggregation (pos), W_d before layer 0's update and M_x before layer 1's projection.
-  const bool fork = cls && !pr && x->side_stream != nullptr;
+  // Degree sort first (the graph's single root: measured, with several root branches the main
+  // stream's first kernel started ~14 us late), then the class-weight / M_x preparation on
+  // side stream 2, concurrent with layer 0's projection; the main chain joins the class
+  // weights before layer 0's update and M_x before layer 1's projection.
+  const bool fork = !pr && x->side_stream != nullptr;
   cudaStream_t wst = fork ? x->side2_stream : st;
-  // The degree sort is the graph's single root (measured: with several root branches the
-  // main stream's first kernel started ~14 us late); the weight preparation forks after it.
   phase(pr, HG_PHASE_SCALERS, [&] {
     launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
                    reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
-                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)),
-                   gram_ks(x->caps));
+                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)), gram_ks(x->caps));
   });
   if (fork) cudaEventRecord(x->ev_start, st);
-  // the prep branch is enqueued after layer 0's projection so that the main chain is
-  // the sort's first successor in the graph (measured: the other successor starts later)
+  // the prep branch is enqueued after layer 0's projection so that the main chain is the
+  // sort's first successor in the graph (measured: the other successor starts later)
   auto enqueue_prep = [&] {
-  if (fork) cudaStreamWaitEvent(wst, x->ev_start, 0);
-  if (cls)
-    phase(pr, HG_PHASE_SCALERS, [&] {  // (degree-slot weights belong with the scalers)
-      // layer 0's weights first (needed soonest); low priority and narrow grids so the
-      // main chain's first kernels are not kept off the SMs
+    if (fork) cudaStreamWaitEvent(wst, x->ev_start, 0);
+    phase(pr, HG_PHASE_SCALERS, [&] {  // (class weights belong with the scalers)
+      // layer 0's weights first (needed soonest); low priority so the main chain's first
+      // kernels are not kept off the SMs
       g_low_prio = fork;
       const int64_t *uo = reinterpret_cast<const int64_t *>(x->b(p.u_off));
-      launch_prep_W2(wst, x->caps, x->f(p.params), uo, 0, 1, p.cmax, c.delta, x->f(p.Wf), x->f(p.Wf_lo),
-                     x->f(p.WbT), x->f(p.WbT_lo));
+      launch_prep_W2(wst, x->caps, x->f(p.params), uo, 0, 1, p.cmax, dinfo, x->f(p.Wf), x->f(p.Wf_lo), x->f(p.WbT),
+                     x->f(p.WbT_lo));
       if (fork) cudaEventRecord(x->ev_prep, wst);
       launch_prep_Mx(wst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
                      x->f(p.Mx_lo), x->f(p.MxT), x->f(p.MxT_lo));
       if (fork) cudaEventRecord(x->ev_prepmx, wst);
       if (c.layers > 1)
-        launch_prep_W2(wst, x->caps, x->f(p.params), uo, 1, c.layers, p.cmax, c.delta, x->f(p.Wf), x->f(p.Wf_lo),
+        launch_prep_W2(wst, x->caps, x->f(p.params), uo, 1, c.layers, p.cmax, dinfo, x->f(p.Wf), x->f(p.Wf_lo),
                        x->f(p.WbT), x->f(p.WbT_lo));
-      if (p.xpad) launch_pad_x0(wst, x->caps, blob, x->f(p.xpad), x->f(p.xpad_lo), x->dxda ? pos : nullptr);
+      launch_pad_x0(wst, x->caps, blob, x->f(p.xpad), x->dxda ? pos : nullptr);
       if (fork) cudaEventRecord(x->ev_prepw, wst);
       g_low_prio = false;
     });
   };
   for (int l = 0; l < c.layers; ++l) {
-    const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
     if (fork && l == 1) cudaStreamWaitEvent(st, x->ev_prepmx, 0);
     phase(pr, HG_PHASE_PROJ, [&] {
-      if (cls && l > 0)
-        launch_d_proj(st, x->caps, blob, Xl, x->f(p.X_lo[l - 1]), F, x->param(lname(l, "M_x")),
+      if (l > 0)
+        launch_d_proj(st, x->caps, blob, x->f(p.X[l - 1]), F, x->param(lname(l, "M_x")),
                       x->f(p.Mx_lo) + (size_t)(l - 1) * HH, x->f(p.P[l]));
-      else if (x->use_tc && l > 0 && tc_proj_ok(x->caps, F))
-        launch_tc_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
       else
-        launch_proj(st, x->caps, blob, Xl, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
+        launch_proj(st, x->caps, blob, nullptr, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
     });
     if (l == 0) enqueue_prep();
     phase(pr, HG_PHASE_AGG_FWD, [&] {
       launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), cls ? x->f(p.A_lo[l]) : nullptr, pos);
+                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), pos);
     });
     if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_prep, 0);
     if (fork && l == 1) cudaStreamWaitEvent(st, x->ev_prepw, 0);
     phase(pr, HG_PHASE_UPDATE, [&] {
-      if (cls)
-        launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), x->f(p.A_lo[l]),
-                            reinterpret_cast<const int *>(x->b(p.perm)),
-                            reinterpret_cast<const DegInfo *>(x->b(p.deginfo)),
-                            reinterpret_cast<const int4 *>(x->b(p.tiles)),
-                            x->f(p.Wf) + (size_t)l * p.cmax * 4 * HH, x->f(p.Wf_lo) + (size_t)l * p.cmax * 4 * HH,
-                            x->param(lname(l, "b_U")), x->f(p.X[l]), x->f(p.X_lo[l]),
-                            x->dxda && l + 1 < c.layers ? x->f(p.Xs[l]) : nullptr,
-                            x->dxda && l + 1 < c.layers ? x->f(p.Xs_lo[l]) : nullptr,
-                            x->dxda && l + 1 < c.layers ? reinterpret_cast<uint32_t *>(x->b(p.Xmask[l])) : nullptr);
-      else if (x->use_tc)
-        launch_tc_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")),
-                         x->param(lname(l, "b_U")), x->f(p.X[l]));
-      else
-        launch_update(st, x->caps, blob, x->f(p.A[l]), amp, att, x->param(lname(l, "U")), x->param(lname(l, "b_U")),
-                      x->f(p.X[l]));
+      const bool keep_sorted = x->dxda && l + 1 < c.layers;  // X_l operands of the fused dX -> dA kernel
+      launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), reinterpret_cast<const int *>(x->b(p.perm)), dinfo,
+                          reinterpret_cast<const int4 *>(x->b(p.tiles)), x->f(p.Wf) + (size_t)l * p.cmax * 4 * HH,
+                          x->f(p.Wf_lo) + (size_t)l * p.cmax * 4 * HH, x->param(lname(l, "b_U")), x->f(p.X[l]),
+                          keep_sorted ? x->f(p.Xs[l]) : nullptr,
+                          keep_sorted ? reinterpret_cast<uint32_t *>(x->b(p.Xmask[l])) : nullptr);
     });
   }
   if (fork && c.layers < 2) cudaStreamWaitEvent(st, x->ev_prepw, 0);  // join side stream 2
@@ -364,10 +334,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     if (fuse_head_bwd) {
       launch_head_fused(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
                         x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
-                        x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZ[c.layers - 1]),
-                        cls ? x->f(p.dZ_lo[c.layers - 1]) : nullptr, pos);
+                        x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZ[c.layers - 1]), pos);
       // the loss value is an output only: reduce it on the side stream (joined at the end of the backward)
-      const bool fork = !pr && x->side_stream != nullptr;
       if (fork) {
         cudaEventRecord(x->ev_head, st);
         cudaStreamWaitEvent(x->side_stream, x->ev_head, 0);
@@ -380,19 +348,15 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   });
 }
 
-void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr, int64_t b, int64_t e, bool advance,
-                  int max_blocks);
+void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr, int64_t b, int64_t e, bool advance);
 int64_t layer1_offset(const hg_ctx *x);
-P2PArgs p2p_args(hg_ctx *x, const hg_adamw &h);
 void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool head_done = false,
                       bool overlap_allreduce = false, const hg_adamw *early_adamw = nullptr) {
   const hg_config &c = x->cfg;
+  g_gemm_passes = (c.flags & HG_FLAG_TF32) ? 1 : 3;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
-  float *amp = x->f(p.amp), *att = x->f(p.att);
-  const bool cls = x->use_tc && p.cmax > 0;
-  float *dZ = x->f(p.dZ[c.layers - 1]), *dZl = cls ? x->f(p.dZ_lo[c.layers - 1]) : nullptr;
-  const int *pos = cls ? reinterpret_cast<const int *>(x->b(p.pos)) : nullptr;  // class path: sorted A / dZ rows
+  const int *pos = reinterpret_cast<const int *>(x->b(p.pos));  // sorted A / dZ rows
   const size_t HH = (size_t)c.hidden * c.hidden;
   const bool fork = !pr && x->side_stream != nullptr;
   cudaStream_t side = fork ? x->side_stream : st, side2 = fork ? x->side2_stream : st;
@@ -400,143 +364,101 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   auto wait = [&](cudaStream_t s, cudaEvent_t ev) { if (fork) cudaStreamWaitEvent(s, ev, 0); };
   bool adam_forked = false;
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
-    if (!head_done) {  // dZ of the last layer on the main stream
+    if (!head_done)  // dZ of the last layer on the main stream
       launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"),
-                      x->f(p.G), x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), dZ, x->grad("head.W1"),
-                      x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), false, dZl, pos, false);
-    }
+                      x->f(p.G), x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), x->f(p.dZ[c.layers - 1]),
+                      x->grad("head.W1"), x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), false, pos,
+                      false);
     rec(x->ev_head, st);
     wait(side, x->ev_head);
     g_low_prio = fork;
     // head parameter gradients: off the critical chain
     launch_head_grads(side, x->caps, blob, x->f(p.G), x->f(p.hpre), x->f(p.dy), x->f(p.dhid), x->grad("head.W1"),
-                        x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
+                      x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
     g_low_prio = false;
   });
   const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
   const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
-  if (x->use_tc && !cls)
-    phase(pr, HG_PHASE_DA, [&] {
-      launch_prep_UT(st, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)), c.layers,
-                     x->f(p.UT));
-    });
-  // Weight-gradient GEMMs (dU / db_U from the class Gram, dM_x / db_M) feed only
-  // the allreduce and AdamW, so they run on a low-priority side stream while the
-  // main stream walks the critical chain dA -> agg_bwd -> dX of each layer.
-  // Hazards: dX_l overwrites the dZ buffer Gram_{l+1} read; agg_bwd_l overwrites
-  // the dP dM_x(l+1) read -> the main stream waits for the side events first.
+  const int4 *tiles = reinterpret_cast<const int4 *>(x->b(p.tiles));
+  // Weight-gradient GEMMs (dU / db_U from the class Gram, dM_x / db_M) feed only the
+  // exchange and AdamW, so they run on low-priority side streams while the main stream
+  // walks the critical chain dA -> agg_bwd -> dX of each layer.
+  // Hazards: dX_l overwrites the dZ buffer Gram_{l+1} read; agg_bwd_l overwrites the dP
+  // dM_x(l+1) read -> one buffer per layer (Plan), so no write-after-read waits.
   float *part_dU = x->f(p.part2), *part_dMx = x->f(p.part3);  // (one per side stream)
   for (int l = c.layers - 1; l >= 0; --l) {
-    dZ = x->f(p.dZ[l]);
-    dZl = cls ? x->f(p.dZ_lo[l]) : nullptr;
-    float *dP = x->f(p.dPl[l]), *dPlo = cls ? x->f(p.dPl_lo[l]) : nullptr, *pagg = x->f(p.pagg[l]);
+    float *dZ = x->f(p.dZ[l]);
+    float *dP = x->f(p.dPl[l]), *pagg = x->f(p.pagg[l]);
     // ---- side: Gram (dU, db_U) as soon as dZ_l is ready
     rec(x->ev_dz[l], st);
     wait(side, x->ev_dz[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DU, [&] {  // (side stream 1)
-      // layer 0's Gram ends the step (only agg_bwd_0 and dM_x0 run beside it): more CTAs
-      static const int gram0_grid = [] {
-        const char *e = getenv("HG_GRAM0_GRID");
-        return e ? atoi(e) : 148;  // (kSMs)
-      }();
-      if (cls) {
-        g_mn_grid_override = l == 0 ? gram0_grid : 0;
-        launch_mn_dU_cls(side, x->caps, p.cmax, dZ, dZl, x->f(p.A[l]), x->f(p.A_lo[l]), x->f(p.ones), dinfo,
-                         reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
-                         x->grad(lname(l, "b_U")));
-        g_mn_grid_override = 0;
-      }
-      else if (x->use_tc)
-        launch_tc_dU(side, x->caps, blob, dZ, x->f(p.A[l]), amp, att, part_dU, x->grad(lname(l, "U")),
-                     x->grad(lname(l, "b_U")));
-      else
-        launch_dU(side, x->caps, blob, dZ, x->f(p.A[l]), amp, att, part_dU, x->grad(lname(l, "U")),
-                  x->grad(lname(l, "b_U")));
+      // layer 0's Gram ends the step (only agg_bwd_0 and dM_x0 run beside it): every SM
+      g_mn_grid_override = l == 0 ? kNumSMs : 0;
+      launch_mn_dU_cls(side, x->caps, p.cmax, dZ, x->f(p.A[l]), x->f(p.ones), dinfo,
+                       reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
+                       x->grad(lname(l, "b_U")));
+      g_mn_grid_override = 0;
     });
     rec(x->ev_gram[l], side);
     g_low_prio = false;
     // ---- main: dA, aggregation backward
-    const bool dxda = x->dxda && cls;
     phase(pr, HG_PHASE_DA, [&] {
-      if (dxda && l + 1 < c.layers) {
-        // dA_l was produced with dZ_l by layer l+1's fused dX -> dA kernel
-      } else if (cls)
-        launch_d_dA_cls(st, x->caps, p.cmax, dZ, dZl, perm, dinfo, reinterpret_cast<const int4 *>(x->b(p.tiles)),
-                        x->f(p.WbT) + (size_t)l * p.cmax * 4 * HH, x->f(p.WbT_lo) + (size_t)l * p.cmax * 4 * HH,
-                        x->f(p.dA));
-      else if (x->use_tc)
-        launch_tc_dA(st, x->caps, blob, dZ, amp, att, x->f(p.UT) + (size_t)l * 12 * c.hidden * c.hidden, x->f(p.dA));
-      else
-        launch_dA(st, x->caps, blob, dZ, amp, att, x->param(lname(l, "U")), x->f(p.dA));
+      if (!(x->dxda && l + 1 < c.layers))  // (else dA_l came with dZ_l from layer l+1's fused dX -> dA)
+        launch_d_dA_cls(st, x->caps, p.cmax, dZ, perm, dinfo, tiles, x->f(p.WbT) + (size_t)l * p.cmax * 4 * HH,
+                        x->f(p.WbT_lo) + (size_t)l * p.cmax * 4 * HH, x->f(p.dA));
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, cls ? dPlo : nullptr, pos,
-                     dxda ? pos : nullptr);
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, pos, x->dxda ? pos : nullptr);
     });
-    const float *Xl = l == 0 ? nullptr : x->f(p.X[l - 1]);
     const int F = l == 0 ? c.f_node : c.hidden;
     // ---- side stream 2: dM_e, dM_x, db_M once dP_l is ready; with Gram_l done, layer l is complete
     rec(x->ev_dp[l], st);
     wait(side2, x->ev_dp[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DMX, [&] {
-      static const bool dmx0_simt = getenv("HG_DMX0_SIMT") != nullptr;  // A/B switch for layer 0
       // layer 0 on one GPU: off the step's final dM_x chain, on the idle AdamW stream (with W > 1
       // the conv0 bucket's allreduce is enqueued on side stream 2 and must follow dM_e)
-      // the MN-major dM_x Gram takes db_M from the aggregation partials (no column-sum tiles)
-      const bool mn_dmx = cls && (l > 0 || (p.xpad && !dmx0_simt));
-      float *dbM_agg = mn_dmx ? x->grad(lname(l, "b_M")) : nullptr;
-      if (l == 0 && adam_forked && x->world == 1) {
+      if (l == 0 && adam_forked && !x->comm) {
         wait(x->adam_stream, x->ev_dp[0]);
-        launch_reduce_dMe(x->adam_stream, x->caps, pagg, x->grad(lname(l, "M_e")), dbM_agg);
+        launch_reduce_dMe(x->adam_stream, x->caps, pagg, x->grad(lname(l, "M_e")), x->grad(lname(l, "b_M")));
         rec(x->ev_adam, x->adam_stream);
       } else {
-        launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")), dbM_agg);
+        launch_reduce_dMe(side2, x->caps, pagg, x->grad(lname(l, "M_e")), x->grad(lname(l, "b_M")));
       }
-      if (mn_dmx) {  // MN-major TMA Gram (layer 0: padded features)
-        // (fused path: dP rows are degree-sorted, so X comes in sorted rows too)
-        const float *Xg = l > 0 ? (dxda ? x->f(p.Xs[l - 1]) : Xl) : x->f(p.xpad);
-        const float *Xg_lo = l > 0 ? x->f(dxda ? p.Xs_lo[l - 1] : p.X_lo[l - 1]) : x->f(p.xpad_lo);
-        // layer 0's dM_x runs after the last main-chain kernel: it may use every SM
-        g_mn_grid_override = l == 0 ? 148 : 0;  // (kSMs)
-        launch_mn_dMx(side2, x->caps, blob, dP, dPlo, Xg, Xg_lo, F, l > 0 ? F : pad_x0_width(c.f_node),
-                      x->f(p.ones), part_dMx, x->grad(lname(l, "M_x")), nullptr);
-        g_mn_grid_override = 0;
-      } else if (x->use_tc && l > 0 && tc_dmx_ok(x->caps, F))
-        launch_tc_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
-      else
-        launch_dMx(side2, x->caps, blob, dP, Xl, F, part_dMx, x->grad(lname(l, "M_x")), x->grad(lname(l, "b_M")));
+      // MN-major TMA Gram dM_x = dP^T X (db_M comes from the aggregation partials);
+      // fused dX -> dA path: dP rows are degree-sorted, so X comes in sorted rows too
+      const float *Xg = l > 0 ? x->f(x->dxda ? p.Xs[l - 1] : p.X[l - 1]) : x->f(p.xpad);
+      g_mn_grid_override = l == 0 ? kNumSMs : 0;  // layer 0's dM_x runs after the last main-chain kernel
+      launch_mn_dMx(side2, x->caps, blob, dP, Xg, F, l > 0 ? F : pad_x0_width(c.f_node), x->f(p.ones), part_dMx,
+                    x->grad(lname(l, "M_x")), nullptr);
+      g_mn_grid_override = 0;
     });
     g_low_prio = false;
     const int bk = bucket_closed_by(x, l);
     if (overlap_allreduce && bk >= 0) {  // conv l's gradients complete: its bucket may go
       wait(side2, x->ev_gram[l]);
       enqueue_bucket(x, side2, bk);
-      if (x->world > 1 && x->comm && l == 1) rec(x->ev_ar1, x->comm_stream);  // layers >= 1 averaged
+      if (x->comm && l == 1) rec(x->ev_ar1, x->comm_stream);  // layers >= 1 averaged
     }
     rec(x->ev_side[l], side2);
     // ---- main: dX into dZ[l-1]
     if (l > 0) {
-      float *dZn = x->f(p.dZ[l - 1]), *dZnl = cls ? x->f(p.dZ_lo[l - 1]) : nullptr;
+      float *dZn = x->f(p.dZ[l - 1]);
       phase(pr, HG_PHASE_DX, [&] {
-        if (dxda)
-          launch_dxda(st, x->caps, p.cmax, dP, dPlo, x->f(p.MxT) + (size_t)(l - 1) * HH,
+        if (x->dxda)
+          launch_dxda(st, x->caps, p.cmax, dP, x->f(p.MxT) + (size_t)(l - 1) * HH,
                       x->f(p.MxT_lo) + (size_t)(l - 1) * HH, x->f(p.WbT) + (size_t)(l - 1) * p.cmax * 4 * HH,
-                      x->f(p.WbT_lo) + (size_t)(l - 1) * p.cmax * 4 * HH, perm, dinfo,
-                      reinterpret_cast<const int4 *>(x->b(p.tiles)),
-                      reinterpret_cast<const uint32_t *>(x->b(p.Xmask[l - 1])), dZn, dZnl, x->f(p.dA));
-        else if (cls)
-          launch_d_dX(st, x->caps, blob, dP, dPlo, x->f(p.MxT) + (size_t)(l - 1) * HH,
-                      x->f(p.MxT_lo) + (size_t)(l - 1) * HH, F, Xl, dZn, dZnl, pos);
-        else if (x->use_tc && F % 64 == 0)
-          launch_tc_dX(st, x->caps, blob, dP, x->param(lname(l, "M_x")), F, Xl, dZn);
+                      x->f(p.WbT_lo) + (size_t)(l - 1) * p.cmax * 4 * HH, perm, dinfo, tiles,
+                      reinterpret_cast<const uint32_t *>(x->b(p.Xmask[l - 1])), dZn, x->f(p.dA));
         else
-          launch_dX(st, x->caps, blob, dP, x->param(lname(l, "M_x")), F, Xl, dZn);
+          launch_d_dX(st, x->caps, blob, dP, x->f(p.MxT) + (size_t)(l - 1) * HH,
+                      x->f(p.MxT_lo) + (size_t)(l - 1) * HH, F, x->f(p.X[l - 1]), dZn, pos);
       });
       if (early_adamw && fork && l == 1) {
-        // every parameter of layers >= 1 and the head is final (and allreduced) and no longer
+        // every parameter of layers >= 1 and the head is final (and averaged) and no longer
         // read by this step (dX_1 was the last reader): update them now, off the critical
         // chain; conv0's parameters follow after the backward (that launch advances the step)
         // (own stream: on side stream 2 it delayed layer 0's dM_x chain at the step's end)
@@ -545,18 +467,9 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
         wait(as, x->ev_dx[1]);
         wait(as, x->ev_gram[1]);
         wait(as, x->ev_side[1]);
-        if (x->world > 1 && x->comm && !x->p2p) wait(as, x->ev_ar1);  // (layer 1 closes a bucket)
+        if (x->comm) wait(as, x->ev_ar1);  // (layer 1 closes a bucket)
         g_low_prio = true;
-        // (HG_EARLY_ADAMW_BLOCKS caps its grid: 64 CTAs was measured 1% slower — the update
-        // then finishes late and delays layer 0's dM_e reduction queued behind it)
-        static const int early_blocks = [] {
-          const char *e = getenv("HG_EARLY_ADAMW_BLOCKS");  // 0 = full grid (measured best)
-          return e ? atoi(e) : 0;
-        }();
-        if (x->p2p && x->world > 1)  // peer-memory exchange of layers >= 1 and the head (part 1)
-          launch_p2p_part(as, p2p_args(x, *early_adamw), 1, layer1_offset(x) / 4, x->n_params / 4, true, false);
-        else
-          enqueue_step(x, as, *early_adamw, nullptr, layer1_offset(x), -1, false, early_blocks);
+        enqueue_step(x, as, *early_adamw, nullptr, layer1_offset(x), -1, false);
         g_low_prio = false;
         rec(x->ev_adam, as);
         adam_forked = true;
@@ -568,39 +481,23 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   if (adam_forked) wait(st, x->ev_adam);
 }
 
-// gradient buckets in backward order: head first, then conv L-1 ... conv 0 (each a
-// contiguous range of the flat gradient arena)
-// Gradient buckets in backward order. Bucket 0 holds the head and the first
-// groups[0] conv layers (L-1, L-2, ...), bucket k the next groups[k] layers; a
-// bucket is allreduced on the comm stream once its lowest layer's gradients are
-// final. Default: layer pairs, the last two layers alone (HG_BUCKETS=a,b,... layer
-// counts per bucket overrides).
-std::vector<int> bucket_groups(const hg_ctx *x) {
-  const int L = x->cfg.layers;
+// Gradient buckets in backward order. Bucket 0 holds the head and the first groups[0]
+// conv layers (L-1, L-2, ...), bucket k the next groups[k] layers; a bucket is averaged on
+// the comm stream once its lowest layer's gradients are final. Layer pairs, the last two
+// layers alone (measured best at 2 GPUs, config B). Buckets are contiguous
+// ranges of the flat arena and together cover it exactly (hg_bucket_layout, tested).
+std::vector<int> bucket_groups_for(int L) {
   std::vector<int> g;
-  if (const char *e = getenv("HG_BUCKETS")) {
-    int tot = 0;
-    for (const char *p = e; *p;) {
-      const int v = atoi(p);
-      if (v > 0 && tot + v <= L) {
-        g.push_back(v);
-        tot += v;
-      }
-      while (*p && *p != ',') ++p;
-      if (*p == ',') ++p;
-    }
-    if (tot < L) g.push_back(L - tot);
-  } else {  // pairs of layers, the last two alone (measured best at 2 GPUs, config B)
-    int rest = L;
-    while (rest > 2) {
-      const int v = std::min(2, rest - 2);
-      g.push_back(v);
-      rest -= v;
-    }
-    while (rest-- > 0) g.push_back(1);
+  int rest = L;
+  while (rest > 2) {
+    const int v = std::min(2, rest - 2);
+    g.push_back(v);
+    rest -= v;
   }
+  while (rest-- > 0) g.push_back(1);
   return g;
 }
+std::vector<int> bucket_groups(const hg_ctx *x) { return bucket_groups_for(x->cfg.layers); }
 int bucket_count(const hg_ctx *x) { return (int)bucket_groups(x).size(); }
 // bucket that completes when layer l's gradients are final, or -1
 int bucket_closed_by(const hg_ctx *x, int l) {
@@ -612,25 +509,28 @@ int bucket_closed_by(const hg_ctx *x, int l) {
   }
   return -1;
 }
-std::pair<int64_t, int64_t> bucket_range(hg_ctx *x, int b) {
-  const int L = x->cfg.layers;
+// float range [beg, end) of bucket b in the arena layout `lay` (n = arena floats)
+std::pair<int64_t, int64_t> bucket_range_of(const std::vector<TensorInfo> &lay, int64_t n, int L, int b) {
   auto off = [&](const std::string &name) {
-    for (auto &t : x->lay)
+    for (auto &t : lay)
       if (t.name == name) return t.offset;
     return (int64_t)-1;
   };
-  const auto g = bucket_groups(x);
+  const auto g = bucket_groups_for(L);
   int top = L;
   for (int k = 0; k < b; ++k) top -= g[k];
   const int lo = top - g[b];
   const int64_t beg = off(lname(lo, "M_x"));
-  const int64_t end = b == 0 ? x->n_params : off(lname(top, "M_x"));
+  const int64_t end = b == 0 ? n : off(lname(top, "M_x"));
   return {beg, end};
 }
+std::pair<int64_t, int64_t> bucket_range(hg_ctx *x, int b) {
+  return bucket_range_of(x->lay, x->n_params, x->cfg.layers, b);
+}
 
-// enqueue the allreduce of bucket b on the comm stream once the compute stream reaches this point
+// enqueue the average of bucket b on the comm stream once the compute stream reaches this point
 hg_status enqueue_bucket(hg_ctx *x, cudaStream_t st, int b) {
-  if (x->world <= 1 || !x->comm) return HG_OK;
+  if (!x->comm) return HG_OK;
   auto r = bucket_range(x, b);
   cudaError_t e;
   if ((e = cudaEventRecord(x->bucket_ready[b], st)) != cudaSuccess) return cuda_fail(x, e, "cudaEventRecord");
@@ -642,9 +542,9 @@ hg_status enqueue_bucket(hg_ctx *x, cudaStream_t st, int b) {
   return HG_OK;
 }
 
-// join: the compute stream waits for every bucket's allreduce
+// join: the compute stream waits for every bucket's average
 hg_status join_buckets(hg_ctx *x, cudaStream_t st) {
-  if (x->world <= 1 || !x->comm) return HG_OK;
+  if (!x->comm) return HG_OK;
   cudaError_t e;
   if ((e = cudaEventRecord(x->comm_done, x->comm_stream)) != cudaSuccess) return cuda_fail(x, e, "cudaEventRecord");
   if ((e = cudaStreamWaitEvent(st, x->comm_done, 0)) != cudaSuccess) return cuda_fail(x, e, "cudaStreamWaitEvent");
@@ -652,7 +552,7 @@ hg_status join_buckets(hg_ctx *x, cudaStream_t st) {
 }
 
 hg_status enqueue_allreduce(hg_ctx *x, cudaStream_t st) {
-  if (x->world <= 1 || !x->comm) return HG_OK;
+  if (!x->comm) return HG_OK;
   ncclResult_t r = ncclAllReduce(x->f(x->plan.grads), x->f(x->plan.grads), (size_t)x->n_params, ncclFloat32, ncclAvg,
                                  x->comm, st);
   if (r != ncclSuccess) return nccl_fail(x, r, "ncclAllReduce");
@@ -662,32 +562,36 @@ hg_status enqueue_allreduce(hg_ctx *x, cudaStream_t st) {
 // AdamW over parameters [b, e) of the flat arena (default: all); `advance` = this launch
 // is the step's last and advances the step counter
 void enqueue_step(hg_ctx *x, cudaStream_t st, const hg_adamw &h, Prof *pr = nullptr, int64_t b = 0, int64_t e = -1,
-                  bool advance = true, int max_blocks = 0) {
+                  bool advance = true) {
   const Plan &p = x->plan;
   if (e < 0) e = x->n_params;
   phase(pr, HG_PHASE_ADAMW, [&] {
     launch_adamw(st, x->f(p.params) + b, x->f(p.grads) + b, x->f(p.m) + b, x->f(p.v) + b, e - b,
-                 reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay, advance,
-                 max_blocks);
+                 reinterpret_cast<AdamDev *>(x->b(p.adam)), h.lr, h.beta1, h.beta2, h.eps, h.weight_decay, advance);
   });
 }
-P2PArgs p2p_args(hg_ctx *x, const hg_adamw &h) {
+// peer-memory exchange arguments; peers = every rank's workspace (mapped or, emulated, local)
+P2PArgs p2p_args_of(hg_ctx *x, uint8_t *const *peers, int world, int rank, const hg_adamw &h) {
   P2PArgs a{};
   const Plan &p = x->plan;
-  for (int q = 0; q < x->world; ++q) {
-    a.params[q] = reinterpret_cast<float *>(x->peer_ws[q] + p.params);
-    a.grads[q] = reinterpret_cast<const float *>(x->peer_ws[q] + p.grads);
-    a.dev[q] = reinterpret_cast<P2PDev *>(x->peer_ws[q] + p.p2p);
+  for (int q = 0; q < world; ++q) {
+    a.params[q] = reinterpret_cast<float *>(peers[q] + p.params);
+    a.grads[q] = reinterpret_cast<const float *>(peers[q] + p.grads);
+    a.dev[q] = reinterpret_cast<P2PDev *>(peers[q] + p.p2p);
+    a.m_all[q] = reinterpret_cast<const float *>(peers[q] + p.m);
+    a.v_all[q] = reinterpret_cast<const float *>(peers[q] + p.v);
   }
   a.m = x->f(p.m);
   a.v = x->f(p.v);
   a.ad = reinterpret_cast<AdamDev *>(x->b(p.adam));
-  a.world = x->world;
-  a.rank = x->rank;
+  a.world = world;
+  a.rank = rank;
   a.n4 = x->n_params / 4;
+  a.timeout_ns = x->timeout_ns;
   a.lr = h.lr; a.beta1 = h.beta1; a.beta2 = h.beta2; a.eps = h.eps; a.wd = h.weight_decay;
   return a;
 }
+P2PArgs p2p_args(hg_ctx *x, const hg_adamw &h) { return p2p_args_of(x, x->peer_ws, x->world, x->rank, h); }
 int64_t layer1_offset(const hg_ctx *x) {  // start of conv1's parameters (conv0's come first)
   for (auto &t : x->lay)
     if (t.name == lname(1, "M_x")) return t.offset;
@@ -698,6 +602,17 @@ hg_status after_enqueue(hg_ctx *x, const char *what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return cuda_fail(x, e, what);
   return HG_OK;
+}
+
+// moments sharded by earlier peer-memory steps: gather the peers' shards (stream-ordered
+// after the last exchange, whose final done-wait guarantees the peers' shards are written)
+hg_status gather_moments(hg_ctx *x) {
+  if (!x->mv_sharded) return HG_OK;
+  launch_p2p_gather_moments(x->stream, p2p_args(x, hg_adamw{}));
+  x->launches += 1;
+  hg_status st = after_enqueue(x, "moment gather");
+  if (st == HG_OK) x->mv_sharded = false;
+  return st;
 }
 
 }  // namespace
@@ -758,8 +673,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   g_prio_lo = prio_lo;
   g_prio_hi = prio_hi;
-  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_deg, &x->ev_prep, &x->ev_start, &x->ev_hgrad, &x->ev_prepmx, &x->ev_prepw,
-                          &x->ev_ar1, &x->ev_adam})
+  for (cudaEvent_t *ev : {&x->ev_head, &x->ev_prep, &x->ev_start, &x->ev_prepmx, &x->ev_prepw, &x->ev_ar1, &x->ev_adam})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
   if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocDefault)) != cudaSuccess)
     return bail(e, "cudaHostAlloc");
@@ -788,44 +702,26 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     x->graph_hyper.push_back(hg_adamw{});
   }
   if ((e = cudaMemsetAsync(workspace, 0, plan.total, x->stream)) != cudaSuccess) return bail(e, "cudaMemsetAsync");
-  x->use_tc = tc_supported(x->caps) && !(c->flags & HG_FLAG_SIMT_GEMM);
   head_configure(x->caps);
-  if (x->use_tc && (e = tc_configure()) != cudaSuccess) return bail(e, "tc_configure");
-  if (x->use_tc && (e = tcd_configure()) != cudaSuccess) return bail(e, "tcd_configure");
-  // fused dX -> dA backward (default; HG_DXDA=0 selects the separate TMA dX and dA kernels):
-  // +2.3% at config B
+  if ((e = tcd_configure()) != cudaSuccess) return bail(e, "tcd_configure");
+  x->dxda = dxda_supported(x->caps);  // fused dX -> dA backward: +2.3% at config B
   {
-    const char *v = getenv("HG_DXDA");
-    x->dxda = x->use_tc && plan.cmax > 0 && dxda_supported(x->caps) && !(v && atoi(v) == 0);
-  }
-  if (const char *pe = getenv("HG_PDL")) g_pdl = atoi(pe) != 0;  // A/B switch for launch overlap
-  {
-    std::vector<int64_t> uo;
+    std::vector<int64_t> uo, mo;
     for (int l = 0; l < c->layers; ++l)
-      for (auto &t : x->lay)
+      for (auto &t : x->lay) {
         if (t.name == lname(l, "U")) uo.push_back(t.offset);
+        if (t.name == lname(l, "M_x")) mo.push_back(t.offset);
+      }
+    std::vector<float> one((size_t)c->max_nodes * 32, 1.0f);
     if ((e = cudaMemcpyAsync(x->b(plan.u_off), uo.data(), sizeof(int64_t) * uo.size(), cudaMemcpyHostToDevice,
+                             x->stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(x->b(plan.mx_off), mo.data(), sizeof(int64_t) * mo.size(), cudaMemcpyHostToDevice,
+                             x->stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(x->b(plan.ones), one.data(), sizeof(float) * one.size(), cudaMemcpyHostToDevice,
                              x->stream)) != cudaSuccess)
       return bail(e, "cudaMemcpyAsync");
-    if (plan.cmax) {
-      std::vector<float> one((size_t)c->max_nodes * 32, 1.0f);
-      if ((e = cudaMemcpyAsync(x->b(plan.ones), one.data(), sizeof(float) * one.size(), cudaMemcpyHostToDevice,
-                               x->stream)) != cudaSuccess)
-        return bail(e, "cudaMemcpyAsync");
-      if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
-    }
-    if (plan.mx_off) {
-      std::vector<int64_t> mo;
-      for (int l = 0; l < c->layers; ++l)
-        for (auto &t : x->lay)
-          if (t.name == lname(l, "M_x")) mo.push_back(t.offset);
-      if ((e = cudaMemcpyAsync(x->b(plan.mx_off), mo.data(), sizeof(int64_t) * mo.size(), cudaMemcpyHostToDevice,
-                               x->stream)) != cudaSuccess)
-        return bail(e, "cudaMemcpyAsync");
-    }
     if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
   }
-  if ((e = cudaStreamSynchronize(x->stream)) != cudaSuccess) return bail(e, "cudaStreamSynchronize");
   *out = x;
   return HG_OK;
 }
@@ -847,8 +743,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->adam_stream) cudaStreamDestroy(x->adam_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
     for (auto ev : *v) cudaEventDestroy(ev);
-  for (cudaEvent_t ev : {x->ev_head, x->ev_deg, x->ev_prep, x->ev_start, x->ev_hgrad, x->ev_prepmx, x->ev_prepw, x->ev_ar1,
-                         x->ev_adam})
+  for (cudaEvent_t ev : {x->ev_head, x->ev_prep, x->ev_start, x->ev_prepmx, x->ev_prepw, x->ev_ar1, x->ev_adam})
     if (ev) cudaEventDestroy(ev);
   for (cudaEvent_t ev : x->loss_ev)
     if (ev) cudaEventDestroy(ev);
@@ -959,7 +854,7 @@ hg_status hg_grads_get(hg_ctx *x, float *dst, int32_t on_device) {
 
 hg_status hg_opt_state_get(hg_ctx *x, float *m, float *v, int64_t *step, int32_t on_device) {
   hg_status st = usable(x);
-  if (st) return st;
+  if (st || (st = gather_moments(x))) return st;
   if (m && (st = arena_out(x, m, x->f(x->plan.m), on_device))) return st;
   if (v && (st = arena_out(x, v, x->f(x->plan.v), on_device))) return st;
   if (step) {
@@ -976,6 +871,7 @@ hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t st
   if (st) return st;
   if (m && (st = arena_in(x, x->f(x->plan.m), m, on_device))) return st;
   if (v && (st = arena_in(x, x->f(x->plan.v), v, on_device))) return st;
+  if (m && v) x->mv_sharded = false;
   AdamDev ad{step, 0, 0};
   CK(x, cudaMemcpyAsync(x->b(x->plan.adam), &ad, sizeof(ad), cudaMemcpyHostToDevice, x->stream));
   CK(x, cudaStreamSynchronize(x->stream));
@@ -1022,7 +918,6 @@ hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_
     case 11: *offset = p.att; *bytes = 4 * N; break;
     // (debug views, not in the header: per-layer dP, dP_lo; padded layer-0 features)
     case 100: if (layer < 0 || layer >= c.layers) return fail(HG_E_RANGE, "layer"); *offset = p.dPl[layer]; *bytes = 4 * N * H; break;
-    case 101: if (layer < 0 || layer >= c.layers || p.dPl_lo.empty()) return fail(HG_E_RANGE, "layer"); *offset = p.dPl_lo[layer]; *bytes = 4 * N * H; break;
     case 102: if (!p.xpad) return fail(HG_E_RANGE, "no xpad"); *offset = p.xpad; *bytes = 4 * N * pad_x0_width(c.f_node); break;
     default: return fail(HG_E_RANGE, "unknown view %d", what);
   }
@@ -1048,13 +943,9 @@ hg_status hg_upload_packed(hg_ctx *x, const void *blob, size_t bytes, int32_t sl
   hg_status st = usable(x);
   if (st || (st = check_slot(x, slot))) return st;
   if (!blob || bytes < (size_t)kHeaderInts * 4) return fail(HG_E_INVALID, "bad blob");
+  if ((st = check_blob(blob, bytes, x->cfg))) return st;
   const int32_t *h = (const int32_t *)blob;
-  if (h[0] < 1) return fail(HG_E_EMPTY, "EmptyBatch");
-  if (h[0] > x->cfg.max_graphs || h[1] > x->cfg.max_nodes || h[2] > x->cfg.max_edges)
-    return fail(HG_E_CAPACITY, "blob exceeds ctx capacity");
-  if (h[3] != x->cfg.f_node || h[4] != x->cfg.f_edge) return fail(HG_E_SHAPE, "blob feature widths differ");
   const size_t need = (size_t)batch_offsets(h[0], h[1], h[2], h[3], h[4]).total;
-  if (bytes < need) return fail(HG_E_SHAPE, "blob shorter than its header implies");
   CK(x, cudaEventSynchronize(x->copy_done[slot]));
   std::memcpy(x->staging[slot], blob, need);
   CK(x, cudaStreamWaitEvent(x->copy_stream, x->compute_done[slot], 0));
@@ -1070,7 +961,10 @@ hg_status hg_forward(hg_ctx *x, int32_t slot) {
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->stream, slot);
   x->launches += launches_so_far() - l0;
-  return after_enqueue(x, "forward launch");
+  if ((st = after_enqueue(x, "forward launch"))) return st;
+  // the slot's blob is read by this forward: a later hg_pack of the slot waits for it
+  CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
+  return HG_OK;
 }
 
 // ---- evaluation path
@@ -1172,10 +1066,12 @@ hg_status hg_nccl_unique_id(void *out128) {
 hg_status hg_comm_init(hg_ctx *x, const void *id128, int32_t rank, int32_t world) {
   hg_status st = usable(x);
   if (st) return st;
-  if (!id128 || world < 1 || rank < 0 || rank >= world) return fail(HG_E_INVALID, "bad rank/world");
+  if (world < 1 || rank < 0 || rank >= world) return fail(HG_E_INVALID, "bad rank/world");
+  if (!id128 && world > 1) return fail(HG_E_INVALID, "null NCCL id");
+  if (x->comm) return fail(HG_E_STATE, "communicator already initialised");
   x->rank = rank;
   x->world = world;
-  if (world == 1) return HG_OK;
+  if (!id128) return HG_OK;  // world == 1 without an id: no communicator, the exchange is a no-op
   CK(x, cudaSetDevice(x->device));
   ncclUniqueId id;
   std::memcpy(&id, id128, sizeof(id));
@@ -1232,6 +1128,7 @@ hg_status hg_p2p_open(hg_ctx *x, const void *all) {
   hg_status st = usable(x);
   if (st) return st;
   if (!all) {  // back to the NCCL exchange (mappings stay open until destroy)
+    if ((st = gather_moments(x))) return st;  // the NCCL path's AdamW needs whole moments
     if (x->p2p)
       for (auto &g : x->graphs)
         if (g) {
@@ -1279,6 +1176,7 @@ hg_status hg_step(hg_ctx *x, const hg_adamw *h) {
   hg_status st = usable(x);
   if (st) return st;
   if (!h) return fail(HG_E_INVALID, "null hyper");
+  if ((st = gather_moments(x))) return st;  // (after peer-memory steps the moments are sharded)
   const int64_t l0 = launches_so_far();
   enqueue_step(x, x->stream, *h);
   x->launches += launches_so_far() - l0;
@@ -1290,6 +1188,7 @@ hg_status hg_train_step(hg_ctx *x, int32_t slot, const hg_adamw *h, int32_t grap
   if (st || (st = check_slot(x, slot))) return st;
   if (!h) return fail(HG_E_INVALID, "null hyper");
   if (!graph) {
+    if (x->p2p) return fail(HG_E_STATE, "eager steps use the NCCL exchange: hg_p2p_open(x, NULL) first");
     if ((st = hg_forward(x, slot)) || (st = hg_backward(x, slot)) || (st = hg_allreduce_grads(x)) ||
         (st = hg_step(x, h)))
       return st;
@@ -1299,6 +1198,7 @@ hg_status hg_train_step(hg_ctx *x, int32_t slot, const hg_adamw *h, int32_t grap
   if ((st = hg_capture_step(x, slot, h))) return st;
   CK(x, cudaGraphLaunch(x->graphs[slot], x->stream));
   x->launches += x->graph_kernels[slot];
+  if (x->p2p) x->mv_sharded = true;
   CK(x, cudaEventRecord(x->compute_done[slot], x->stream));
   return HG_OK;
 }
@@ -1318,18 +1218,11 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
   enqueue_forward(x, x->cap_stream, slot, nullptr, true);
-  if (x->p2p && x->world > 1) {
-    // gradient average + sharded AdamW + parameter all-gather in one kernel over peer memory:
-    // layers >= 1 and the head during layer 0's backward (part 1), conv0 at the end (part 0)
-    // (HG_P2P_SPLIT=1: measured slower at 2 and 4 GPUs — part 1's grid competes with layer 0's
-    // backward, a capped grid puts it on the critical path; the default exchanges at the end)
-    static const bool split_env = getenv("HG_P2P_SPLIT") != nullptr && atoi(getenv("HG_P2P_SPLIT")) != 0;
-    const bool split = split_env && x->cfg.layers > 1 && x->side_stream != nullptr;
-    enqueue_backward(x, x->cap_stream, slot, nullptr, true, false, split ? h : nullptr);
-    const P2PArgs a = p2p_args(x, *h);
-    launch_p2p_part(x->cap_stream, a, 0, 0, split ? layer1_offset(x) / 4 : x->n_params / 4, !split, true);
-    launch_p2p_wait_done(x->cap_stream, a, 0);
-    if (split) launch_p2p_wait_done(x->cap_stream, a, 1);
+  if (x->p2p) {
+    // gradient average + sharded AdamW + parameter all-gather in one kernel over peer memory
+    // after the backward
+    enqueue_backward(x, x->cap_stream, slot, nullptr, true, false, nullptr);
+    launch_p2p_exchange(x->cap_stream, p2p_args(x, *h));
     const int64_t nk = launches_so_far() - l0;
     cudaError_t e = cudaStreamEndCapture(x->cap_stream, &g);
     if (e != cudaSuccess) return cuda_fail(x, e, "cudaStreamEndCapture");
@@ -1343,8 +1236,7 @@ hg_status hg_capture_step(hg_ctx *x, int32_t slot, const hg_adamw *h) {
     return HG_OK;
   }
   // bucketed, overlapped allreduce; AdamW of layers >= 1 and the head inside the backward
-  const bool split_adamw = x->cfg.layers > 1 && x->side_stream != nullptr && getenv("HG_ADAMW_END") == nullptr &&
-                           (x->world <= 1 || !x->comm || bucket_closed_by(x, 1) >= 0);
+  const bool split_adamw = x->cfg.layers > 1 && x->side_stream != nullptr && (!x->comm || bucket_closed_by(x, 1) >= 0);
   enqueue_backward(x, x->cap_stream, slot, nullptr, true, true, split_adamw ? h : nullptr);
   hg_status ar = join_buckets(x, x->cap_stream);
   if (split_adamw)
@@ -1375,6 +1267,7 @@ hg_status hg_profile_step(hg_ctx *x, int32_t slot, const hg_adamw *h, float *ms,
   // The step is captured with timing events between phases (single stream, no
   // side-stream overlap) and replayed as one graph, so each phase's time is its
   // kernels' device time without host launch gaps.
+  if ((st = gather_moments(x))) return st;  // (the instrumented step runs the full-arena AdamW)
   Prof pr(x->cap_stream);
   CK(x, cudaStreamBeginCapture(x->cap_stream, cudaStreamCaptureModeThreadLocal));
   const int64_t l0 = launches_so_far();
@@ -1441,17 +1334,118 @@ hg_status hg_loss_get(hg_ctx *x, float *loss) {
   return HG_OK;
 }
 
+// wait for one stream with the fail-stop bound: poll the stream, NCCL's async error and the
+// peer-exchange flag block; a failed or timed-out wait aborts the communicator (SPEC.md:459,
+// 475: a dead peer fails the job instead of hanging it) and makes the ctx unusable
+static hg_status wait_stream(hg_ctx *x, cudaStream_t s, const std::chrono::steady_clock::time_point &t0) {
+  for (unsigned spins = 0;; ++spins) {
+    const cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) return HG_OK;
+    if (q != cudaErrorNotReady) {
+      if (x->comm) {
+        ncclCommAbort(x->comm);
+        x->comm = nullptr;
+      }
+      return cuda_fail(x, q, "stream");
+    }
+    if (x->comm) {
+      ncclResult_t ar = ncclSuccess;
+      const ncclResult_t r = ncclCommGetAsyncError(x->comm, &ar);
+      if (r != ncclSuccess || ar != ncclSuccess) {
+        ncclCommAbort(x->comm);
+        x->comm = nullptr;
+        return nccl_fail(x, r != ncclSuccess ? r : ar, "NCCL async error (communicator aborted)");
+      }
+    }
+    if (x->timeout_ns) {
+      const auto el = std::chrono::duration_cast<std::chrono::nanoseconds>(std::chrono::steady_clock::now() - t0);
+      if ((unsigned long long)el.count() > x->timeout_ns) {
+        if (x->comm) {
+          ncclCommAbort(x->comm);
+          x->comm = nullptr;
+        }
+        hg_status st = fail(HG_E_NCCL, "hg_sync timed out after %.3f s (peer not responding?)", x->timeout_ns * 1e-9);
+        x->sticky = st;
+        x->sticky_msg = hg_last_error();
+        return st;
+      }
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(spins < 100 ? 20 : 200));
+  }
+}
+
 hg_status hg_sync(hg_ctx *x) {
   if (!x) return fail(HG_E_INVALID, "null ctx");
   if (x->sticky != HG_OK) return fail(HG_E_STATE, "%s", x->sticky_msg.c_str());
-  CK(x, cudaStreamSynchronize(x->stream));
-  CK(x, cudaStreamSynchronize(x->copy_stream));
-  if (x->comm_stream) CK(x, cudaStreamSynchronize(x->comm_stream));
-  if (x->comm) {
-    ncclResult_t ar;
-    ncclResult_t r = ncclCommGetAsyncError(x->comm, &ar);
-    if (r != ncclSuccess) return nccl_fail(x, r, "ncclCommGetAsyncError");
-    if (ar != ncclSuccess) return nccl_fail(x, ar, "NCCL async error");
+  const auto t0 = std::chrono::steady_clock::now();
+  hg_status st;
+  if ((st = wait_stream(x, x->stream, t0))) return st;
+  if ((st = wait_stream(x, x->copy_stream, t0))) return st;
+  if (x->comm_stream && (st = wait_stream(x, x->comm_stream, t0))) return st;
+  return HG_OK;
+}
+
+hg_status hg_set_timeout(hg_ctx *x, double seconds) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!(seconds >= 0.0) || seconds > 1e6) return fail(HG_E_INVALID, "timeout must be in [0, 1e6] s");
+  x->timeout_ns = (unsigned long long)(seconds * 1e9);
+  for (auto &g : x->graphs)  // captured exchanges carry the bound
+    if (g) {
+      cudaGraphExecDestroy(g);
+      g = nullptr;
+    }
+  return HG_OK;
+}
+
+hg_status hg_p2p_emulate(hg_ctx *const *ctxs, int32_t world, const hg_adamw *h) {
+  if (!ctxs || !h || world < 2 || world > kP2PMaxWorld) return fail(HG_E_INVALID, "need 2..8 contexts and hyper");
+  uint8_t *peers[kP2PMaxWorld] = {};
+  for (int r = 0; r < world; ++r) {
+    hg_status st = usable(ctxs[r]);
+    if (st) return st;
+    if (ctxs[r]->p2p || ctxs[r]->comm) return fail(HG_E_STATE, "emulated ranks must not hold a communicator");
+    if (ctxs[r]->device != ctxs[0]->device || ctxs[r]->n_params != ctxs[0]->n_params)
+      return fail(HG_E_INVALID, "emulated ranks need one device and one configuration");
+    for (int q = 0; q < r; ++q)
+      if (ctxs[q] == ctxs[r]) return fail(HG_E_INVALID, "context passed twice");
+    peers[r] = ctxs[r]->ws;
+  }
+  hg_ctx *x0 = ctxs[0];
+  for (int r = 0; r < world; ++r)  // every rank's backward precedes every rank's exchange
+    if (r > 0) {
+      CK(x0, cudaStreamSynchronize(ctxs[r]->stream));
+    }
+  for (int r = 0; r < world; ++r) {
+    hg_ctx *x = ctxs[r];
+    x->world = world;
+    x->rank = r;
+    for (int q = 0; q < world; ++q) x->peer_ws[q] = peers[q];
+    launch_p2p_exchange_emulated(x0->stream, p2p_args(x, *h));
+    x->launches += 2;
+    x->mv_sharded = true;
+  }
+  hg_status st = after_enqueue(x0, "emulated exchange");
+  if (st) return st;
+  CK(x0, cudaStreamSynchronize(x0->stream));
+  return HG_OK;
+}
+
+hg_status hg_bucket_layout(const hg_config *c, int64_t *ranges, int32_t cap, int32_t *n) {
+  hg_status st = check_config(c);
+  if (st) return st;
+  if (!n) return fail(HG_E_INVALID, "null output");
+  const hg_config pc = padded_config(*c);
+  const auto lay = param_layout(pc);
+  const int64_t total = param_total(lay);
+  const int nb = (int)bucket_groups_for(pc.layers).size();
+  *n = nb;
+  if (!ranges) return HG_OK;
+  if (cap < nb) return fail(HG_E_CAPACITY, "%d buckets > capacity %d", nb, cap);
+  for (int b = 0; b < nb; ++b) {
+    const auto r = bucket_range_of(lay, total, pc.layers, b);
+    ranges[2 * b] = r.first;
+    ranges[2 * b + 1] = r.second;
   }
   return HG_OK;
 }

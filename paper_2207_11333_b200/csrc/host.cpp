@@ -32,15 +32,9 @@ hg_status fail(hg_status st, const char *fmt, ...) {
   return st;
 }
 
-// threads of one collation (hg_pack / hg_pack_host): HG_PACK_THREADS, default 4
-static int hg_pack_threads() {
-  static const int n = [] {
-    const char *e = std::getenv("HG_PACK_THREADS");
-    const int v = e ? std::atoi(e) : 4;
-    return v > 0 ? v : 1;
-  }();
-  return n;
-}
+// threads of one collation (hg_pack / hg_pack_host): hg_pack_threads_set, default 4
+static std::atomic<int> g_pack_threads{4};
+static int hg_pack_threads() { return g_pack_threads.load(); }
 
 static int hw_threads(int32_t t) {
   if (t > 0) return t;
@@ -117,15 +111,16 @@ hg_status check_config(const hg_config *c) {
   if (!(c->delta > 0.0)) return fail(HG_E_INVALID, "delta must be > 0 (SPEC.md:329)");
   if (!(c->var_floor > 0.0f)) return fail(HG_E_INVALID, "var_floor must be > 0");
   if (c->max_degree < 0 || c->max_degree > HG_MAX_DEGREE) return fail(HG_E_INVALID, "max_degree out of range");
+  if (c->flags & ~HG_FLAGS_KNOWN) return fail(HG_E_INVALID, "unknown flags 0x%x", c->flags);
   return HG_OK;
 }
 
-bool config_is_padded(const hg_config &c) { return c.hidden % 32 != 0; }
+bool config_is_padded(const hg_config &c) { return c.hidden % kChannelTile != 0; }
 
 hg_config padded_config(const hg_config &c) {
   if (!config_is_padded(c)) return c;
   hg_config p = c;
-  const int q = (c.flags & HG_FLAG_SIMT_GEMM) ? 32 : 128;
+  const int q = kChannelTile;
   p.hidden = (c.hidden + q - 1) / q * q;
   if (c.fc_hidden == c.hidden) p.fc_hidden = p.hidden;
   return p;
@@ -176,8 +171,49 @@ namespace hg {
 // validate a store whose array pointers are set and compute slot / max stats
 // (shared by hg_store_create and the container readers); on failure the caller
 // deletes s.
+int class_slots(const hg_config &c) {
+  const int dmax = c.max_degree > 0 ? c.max_degree : HG_MAX_DEGREE;
+  return std::min(dmax + 1, kClassSlots);
+}
+
+hg_status check_blob(const void *blob, size_t bytes, const hg_config &cfg) {
+  const int32_t *h = (const int32_t *)blob;
+  const int32_t B = h[0], N = h[1], E = h[2];
+  if (B < 1) return fail(HG_E_EMPTY, "EmptyBatch");
+  if (B > cfg.max_graphs || N > cfg.max_nodes || E > cfg.max_edges || N < 0 || E < 0)
+    return fail(HG_E_CAPACITY, "blob exceeds ctx capacity");
+  if (h[3] != cfg.f_node || h[4] != cfg.f_edge) return fail(HG_E_SHAPE, "blob feature widths differ");
+  const BatchOffsets o = batch_offsets(B, N, E, h[3], h[4]);
+  if (bytes < (size_t)o.total) return fail(HG_E_SHAPE, "blob shorter than its header implies");
+  const int32_t *rp = (const int32_t *)((const uint8_t *)blob + o.rowptr);
+  const int32_t *col = (const int32_t *)((const uint8_t *)blob + o.col);
+  const int32_t *gp = (const int32_t *)((const uint8_t *)blob + o.graph_ptr);
+  if (gp[0] != 0 || gp[B] != N || rp[0] != 0 || rp[N] != E) return fail(HG_E_SHAPE, "blob offsets inconsistent");
+  for (int32_t g = 0; g < B; ++g)
+    if (gp[g + 1] <= gp[g]) return fail(HG_E_EMPTY, "EmptyGraphSlot in blob");
+  const int maxdeg = cfg.max_degree > 0 ? cfg.max_degree : HG_MAX_DEGREE;
+  uint64_t bits[2] = {0, 0};
+  for (int32_t i = 0; i < N; ++i) {
+    const int32_t d = rp[i + 1] - rp[i];
+    if (d < 0 || d > maxdeg) return fail(HG_E_DEGREE, "blob node %d has degree %d", i, d);
+    bits[d >> 6] |= 1ull << (d & 63);
+  }
+  for (int32_t k = 0; k < E; ++k)
+    if (col[k] < 0 || col[k] >= N) return fail(HG_E_RANGE, "blob edge %d endpoint out of range", k);
+  const int ndeg = __builtin_popcountll(bits[0]) + __builtin_popcountll(bits[1]);
+  if (ndeg > class_slots(cfg))
+    return fail(HG_E_DEGREE, "batch has %d distinct node degrees > %d degree-class slots", ndeg, class_slots(cfg));
+  return HG_OK;
+}
+
 hg_status store_finish(hg_store *s, int32_t threads) {
   const int64_t G = s->G;
+  // offsets first, serially: every later (parallel) pass indexes the arrays through them
+  if (s->no[0] != 0 || s->eo[0] != 0 || s->no[G] != s->N || s->eo[G] != s->E)
+    return fail(HG_E_SHAPE, "offsets must start at 0 and end at the totals");
+  for (int64_t g = 0; g < G; ++g)
+    if (s->no[g + 1] < s->no[g] || s->eo[g + 1] < s->eo[g] || s->no[g + 1] > s->N || s->eo[g + 1] > s->E)
+      return fail(HG_E_SHAPE, "store graph %lld: offsets not non-decreasing within the totals", (long long)g);
   s->slot.assign((size_t)s->E, 0);
   const int nt = hw_threads(threads);
   std::vector<hg_status> st(nt, HG_OK);
@@ -403,6 +439,10 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
   int32_t bad_b = -1;  // first offending graph in batch order
   int64_t bad_deg = 0;
   const int64_t *nbp = nbo.data(), *ebp = ebo.data();
+  // degrees present in the batch (bitset over 0..HG_MAX_DEGREE): one degree class each
+  thread_local std::vector<uint64_t> dbits;
+  dbits.assign(2 * (size_t)B, 0);
+  uint64_t *dbp = dbits.data();
 #pragma omp parallel for num_threads(hg_pack_threads()) schedule(static) if (B >= 32)
   for (int32_t b = 0; b < B; ++b) {
     const int64_t g = ids[b], nb = nbp[b], eb = ebp[b];
@@ -423,6 +463,9 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
       if (k - kstart > maxdeg) {
 #pragma omp critical
         if (bad_b < 0 || b < bad_b) { bad_b = b; bad_deg = k - kstart; }
+      } else {
+        const int64_t d = k - kstart;
+        dbp[2 * b + (d >> 6)] |= 1ull << (d & 63);
       }
       rp[nb + i + 1] = (int32_t)(eb + k);
     }
@@ -431,7 +474,21 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
   if (bad_b >= 0)
     return fail(HG_E_CAPACITY, "graph %lld has a node of degree %lld > max_degree %d", (long long)ids[bad_b],
                 (long long)bad_deg, maxdeg);
+  uint64_t d0 = 0, d1 = 0;
+  for (int32_t b = 0; b < B; ++b) {
+    d0 |= dbp[2 * b];
+    d1 |= dbp[2 * b + 1];
+  }
+  const int ndeg = __builtin_popcountll(d0) + __builtin_popcountll(d1);
+  if (ndeg > class_slots(*cfg))
+    return fail(HG_E_DEGREE, "batch has %d distinct node degrees > %d degree-class slots", ndeg, class_slots(*cfg));
   if (used) *used = (size_t)o.total;
+  return HG_OK;
+}
+
+hg_status hg_pack_threads_set(int32_t threads) {
+  if (threads < 1 || threads > 1024) return fail(HG_E_INVALID, "threads must be in [1, 1024]");
+  g_pack_threads.store(threads);
   return HG_OK;
 }
 

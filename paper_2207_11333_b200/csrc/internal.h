@@ -24,13 +24,21 @@ hg_status check_config(const hg_config *c);
 void init_params_host(const hg_config &c, uint64_t seed, float *dst);
 
 // Channel padding (SURVEY §8(d) "Padding hazard"; paper widths H = 55, 200 at
-// PAPER.md:315, 318). A hidden width that is not a multiple of 32 runs internally
-// at Hp = roundup(H, 128) (tensor-core path; roundup(H, 32) with HG_FLAG_SIMT_GEMM),
-// fc_hidden == H padded alike. The padded parameter entries are zero and stay zero
+// PAPER.md:315, 318). A hidden width that is not a multiple of the tensor-core tile
+// (kChannelTile = 128) runs internally at Hp = roundup(H, 128), fc_hidden == H padded alike. The padded parameter entries are zero and stay zero
 // (their gradients are exactly zero: the aggregation kernel writes zero aggregates
 // for padded channels, see launch_agg_fwd), so the padded model computes the
 // logical one exactly. The public arena (hg_param_info, get/set) stays logical.
+constexpr int kChannelTile = 128;
+constexpr int kClassSlots = 32;  // degree-class slots at most (kernels.h kMaxClasses)
+constexpr int HG_FLAGS_KNOWN = HG_FLAG_TF32;
 hg_config padded_config(const hg_config &c);
+// degree classes a ctx of this configuration holds: min(max_degree + 1, kClassSlots); a batch
+// with more distinct node degrees is rejected when it is packed (HG_E_DEGREE)
+int class_slots(const hg_config &c);
+// validate a packed blob (include/hgnn.h layout) against a configuration: header, capacities,
+// offsets, node degrees and distinct-degree count (hg_upload_packed)
+hg_status check_blob(const void *blob, size_t bytes, const hg_config &cfg);
 bool config_is_padded(const hg_config &c);
 // scatter a logical arena (layout of `logical`) into a zeroed padded arena
 // (layout of padded_config(logical)), or gather it back

@@ -25,38 +25,15 @@
 namespace hg {
 
 std::atomic<int64_t> g_launches{0};
-bool g_pdl = false;  // HG_PDL=1: early launch starves the side stream (measured slower)
 bool g_low_prio = false;
 int g_prio_lo = 0, g_prio_hi = 0;
 static inline void counted(int n = 1) { g_launches += n; }
 
-// ------------------------------------------------------------------ scalers
-// amplification ln(d+1)/delta and attenuation delta/ln(d+1), both 1 for d = 0
-// (SURVEY C4-C5). Computed in double, stored fp32.
-__global__ void k_scalers(const uint8_t *__restrict__ blob, double delta, float *__restrict__ amp,
-                          float *__restrict__ att) {
-  pdl_enter();
-  const BatchView b = load_batch(blob);
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < b.N; i += gridDim.x * blockDim.x) {
-    const int d = b.rowptr[i + 1] - b.rowptr[i];
-    if (d == 0) {
-      amp[i] = 1.0f;
-      att[i] = 1.0f;
-    } else {
-      const double ld = log((double)d + 1.0);
-      amp[i] = (float)(ld / delta);
-      att[i] = (float)(delta / ld);
-    }
-  }
-}
-
-void launch_scalers(cudaStream_t st, const Caps &c, const uint8_t *blob, double delta, float *amp, float *att) {
-  const int blocks = std::min(cdiv(c.maxN, 256), kSMs * 4);
-  launch_ex(k_scalers, blocks, 256, 0, st, blob, delta, amp, att);
-  counted();
-}
-
-// ------------------------------------------------------------------ SIMT GEMM (v1)
+// ------------------------------------------------------------------ layer-0 projection (SIMT)
+// Layer 0's projection P = x M_x^T contracts over the F0 = |vocab| + 3 raw node features
+// (34 for the PCQM vocabulary): 2 N F0 H flops, under 1% of a step's GEMM work, with
+// operand rows that are not 16-byte aligned, so it runs on the FP32 pipe (every other
+// GEMM of the step is a TMA-fed tcgen05 kernel, tcdirect.cu / tcmn.cu).
 // C[M,N] = sum_k a(m,k) b(k,n) with operand transforms supplied by Op; 64x64
 // tiles, BK=16, 256 threads, 4x4 outputs per thread, register-prefetched
 // double-buffered shared memory. A_KMAJ: a(m,k) contiguous in k (else in m);
@@ -162,10 +139,6 @@ static void run_gemm(cudaStream_t st, const Op &op, int maxM, int N, int splits)
   counted();
 }
 
-__device__ __forceinline__ float scaler(const float *amp, const float *att, int m, int s) {
-  return s == 0 ? 1.0f : (s == 1 ? amp[m] : att[m]);
-}
-
 // P = X Mx^T  (the message M[x_j || e] + b_M is linear, so the
 // x-part is projected once per node instead of once per edge)
 struct OpProj {
@@ -183,143 +156,6 @@ void launch_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const floa
                  float *P) {
   OpProj op{blob, X, Mx, P, F, c.H};
   run_gemm<true, true>(st, op, c.maxN, c.H, 1);
-}
-
-// Z = [A || amp*A || att*A] U^T + b_U ; X1 = ReLU(Z)
-struct OpUpdate {
-  const uint8_t *blob; const float *A; const float *amp; const float *att; const float *U; const float *bU;
-  float *X1; int H;
-  __device__ void prepare() {}
-  __device__ int M() const { return batch_N(blob); }
-  __device__ int N() const { return H; }
-  __device__ int K() const { return 12 * H; }
-  __device__ int splits() const { return 1; }
-  __device__ float a(int m, int k) const {
-    const int s = k / (4 * H), kk = k - s * 4 * H;
-    return A[(size_t)m * 4 * H + kk] * scaler(amp, att, m, s);
-  }
-  __device__ float b(int k, int n) const { return U[(size_t)n * 12 * H + k]; }
-  __device__ void store(int m, int n, float v, int) const { X1[(size_t)m * H + n] = fmaxf(v + bU[n], 0.0f); }
-};
-void launch_update(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *A, const float *amp,
-                   const float *att, const float *U, const float *bU, float *X1) {
-  OpUpdate op{blob, A, amp, att, U, bU, X1, c.H};
-  run_gemm<true, true>(st, op, c.maxN, c.H, 1);
-}
-
-// dA = sum_s diag(s) dZ U_s : A'[m, s*H+h] = s_m dZ[m,h], B'[s*H+h, n] = U[h, s*4H+n]
-struct OpDA {
-  const uint8_t *blob; const float *dZ; const float *amp; const float *att; const float *U; float *dA; int H;
-  __device__ void prepare() {}
-  __device__ int M() const { return batch_N(blob); }
-  __device__ int N() const { return 4 * H; }
-  __device__ int K() const { return 3 * H; }
-  __device__ int splits() const { return 1; }
-  __device__ float a(int m, int k) const {
-    const int s = k / H, h = k - s * H;
-    return dZ[(size_t)m * H + h] * scaler(amp, att, m, s);
-  }
-  __device__ float b(int k, int n) const {
-    const int s = k / H, h = k - s * H;
-    return U[(size_t)h * 12 * H + s * 4 * H + n];
-  }
-  __device__ void store(int m, int n, float v, int) const { dA[(size_t)m * 4 * H + n] = v; }
-};
-void launch_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *amp,
-               const float *att, const float *U, float *dA) {
-  OpDA op{blob, dZ, amp, att, U, dA, c.H};
-  run_gemm<true, false>(st, op, c.maxN, 4 * c.H, 1);
-}
-
-// split-K partial reduction in fixed split order; column Nc-1 of each row is the bias gradient
-__global__ void k_reduce_split(const float *__restrict__ part, int splits, int Mr, int Nc, float *__restrict__ outW,
-                               float *__restrict__ outB) {
-  pdl_enter();
-  const int total = Mr * Nc;
-  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-    float s = 0.f;
-    for (int p = 0; p < splits; ++p) s += part[(size_t)p * total + e];
-    const int m = e / Nc, n = e - m * Nc;
-    if (n == Nc - 1) outB[m] = s;
-    else outW[(size_t)m * (Nc - 1) + n] = s;
-  }
-}
-
-constexpr int kDUSplits = 8;
-constexpr int kDMxSplits = 64;
-
-// dU[h, s*4H+k] = sum_i s_i dZ[i,h] A[i,k]; column 12H = ones -> db_U
-struct OpDU {
-  const uint8_t *blob; const float *dZ; const float *A; const float *amp; const float *att; float *part; int H;
-  __device__ void prepare() {}
-  __device__ int M() const { return H; }
-  __device__ int N() const { return 12 * H + 1; }
-  __device__ int K() const { return batch_N(blob); }
-  __device__ int splits() const { return kDUSplits; }
-  __device__ float a(int m, int k) const { return dZ[(size_t)k * H + m]; }
-  __device__ float b(int k, int n) const {
-    if (n == 12 * H) return 1.0f;
-    const int s = n / (4 * H), kk = n - s * 4 * H;
-    return A[(size_t)k * 4 * H + kk] * scaler(amp, att, k, s);
-  }
-  __device__ void store(int m, int n, float v, int sp) const {
-    part[(size_t)sp * H * (12 * H + 1) + (size_t)m * (12 * H + 1) + n] = v;
-  }
-};
-size_t dU_partial_floats(const Caps &c) { return (size_t)kDUSplits * c.H * (12 * c.H + 1); }
-void launch_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
-               const float *amp, const float *att, float *partial, float *dU, float *dbU) {
-  OpDU op{blob, dZ, A, amp, att, partial, c.H};
-  run_gemm<false, false>(st, op, c.H, 12 * c.H + 1, kDUSplits);
-  const int total = c.H * (12 * c.H + 1);
-  launch_ex(k_reduce_split, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, kDUSplits, c.H, 12 * c.H + 1, dU, dbU);
-  counted();
-}
-
-// dM_x[h, f] = sum_i dP[i,h] X[i,f]; column F = ones -> db_M
-struct OpDMx {
-  const uint8_t *blob; const float *dP; const float *X; float *part; int H, F;
-  __device__ void prepare() { if (!X) X = load_batch(blob).x; }
-  __device__ int M() const { return H; }
-  __device__ int N() const { return F + 1; }
-  __device__ int K() const { return batch_N(blob); }
-  __device__ int splits() const { return kDMxSplits; }
-  __device__ float a(int m, int k) const { return dP[(size_t)k * H + m]; }
-  __device__ float b(int k, int n) const { return n == F ? 1.0f : X[(size_t)k * F + n]; }
-  __device__ void store(int m, int n, float v, int sp) const {
-    part[(size_t)sp * H * (F + 1) + (size_t)m * (F + 1) + n] = v;
-  }
-};
-size_t dMx_partial_floats(const Caps &c, int F) { return (size_t)kDMxSplits * c.H * (F + 1); }
-
-void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
-                float *partial, float *dMx, float *dbM) {
-  OpDMx op{blob, dP, X, partial, c.H, F};
-  run_gemm<false, false>(st, op, c.H, F + 1, kDMxSplits);
-  const int total = c.H * (F + 1);
-  launch_ex(k_reduce_split, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, partial, kDMxSplits, c.H, F + 1, dMx, dbM);
-  counted();
-}
-
-// dZprev = (dP Mx) * [Xl > 0]  (ReLU'(0) = 0)
-struct OpDX {
-  const uint8_t *blob; const float *dP; const float *Mx; const float *Xl; float *dZ; int H, F;
-  __device__ void prepare() {}
-  __device__ int M() const { return batch_N(blob); }
-  __device__ int N() const { return F; }
-  __device__ int K() const { return H; }
-  __device__ int splits() const { return 1; }
-  __device__ float a(int m, int k) const { return dP[(size_t)m * H + k]; }
-  __device__ float b(int k, int n) const { return Mx[(size_t)k * F + n]; }
-  __device__ void store(int m, int n, float v, int) const {
-    const size_t o = (size_t)m * F + n;
-    dZ[o] = Xl[o] > 0.0f ? v : 0.0f;
-  }
-};
-void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
-               const float *Xl, float *dZprev) {
-  OpDX op{blob, dP, Mx, Xl, dZprev, c.H, F};
-  run_gemm<true, false>(st, op, c.maxN, F, 1);
 }
 
 // ------------------------------------------------------------------ K2 aggregation forward
@@ -366,17 +202,6 @@ __device__ __forceinline__ void load_edge(const float *ea, int Fe, int k, float 
   }
 }
 
-// 3xTF32 residual of a value (x - x with the 13 low mantissa bits cleared): written next
-// to operands the direct tensor-core GEMMs consume (tcdirect.cu)
-__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
-template <int CPL>
-__device__ __forceinline__ void store_vec_lo(float *p, const float (&v)[CPL]) {
-  float l[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) l[c] = tf32_lo(v[c]);
-  store_vec<CPL>(p, l);
-}
-
 // message for CPL channels: m = (P + b_M) + sum_f M_e[:,f] e_f  (same order in K2 and K8)
 template <int CPL, int FE>
 __device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm)[CPL], const float (&me)[CPL][FE],
@@ -394,7 +219,7 @@ template <int CPL, int FE>
 __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
                                                     const float *__restrict__ Me, const float *__restrict__ bM,
                                                     float var_floor, float *__restrict__ A,
-                                                    uint8_t *__restrict__ arg, int H, float *__restrict__ A_lo,
+                                                    uint8_t *__restrict__ arg, int H,
                                                     const int *__restrict__ pos, int Hl) {
   pdl_enter();
   const BatchView b = load_batch(blob);
@@ -468,13 +293,6 @@ __global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ 
     store_vec<CPL>(Ai + H, mn);
     store_vec<CPL>(Ai + 2 * H, mx);
     store_vec<CPL>(Ai + 3 * H, sd);
-    if (A_lo) {
-      float *Li = A_lo + arow;
-      store_vec_lo<CPL>(Li, mean);
-      store_vec_lo<CPL>(Li + H, mn);
-      store_vec_lo<CPL>(Li + 2 * H, mx);
-      store_vec_lo<CPL>(Li + 3 * H, sd);
-    }
     uint8_t *ai = arg + ch + i * (2 * H);
     if constexpr (CPL == 4) {
       *reinterpret_cast<uchar4 *>(ai) = make_uchar4(amn[0], amn[1], amn[2], amn[3]);
@@ -497,19 +315,19 @@ static int agg_cpl(int H) { return (H % 64 == 0) ? 2 : 1; }
 
 template <int CPL, int FE>
 static void agg_fwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                           const float *bM, float var_floor, float *A, uint8_t *arg, float *A_lo, const int *pos) {
+                           const float *bM, float var_floor, float *A, uint8_t *arg, const int *pos) {
   const dim3 grid(std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 4)), c.H / (32 * CPL));
-  launch_ex(k_agg_fwd<CPL, FE>, grid, 256, 0, st, blob, P, Me, bM, var_floor, A, arg, c.H, A_lo, pos,
+  launch_ex(k_agg_fwd<CPL, FE>, grid, 256, 0, st, blob, P, Me, bM, var_floor, A, arg, c.H, pos,
             c.Hl > 0 ? c.Hl : c.H);
 }
 
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, float var_floor, float *A, uint8_t *arg, float *A_lo, const int *pos) {
+                    const float *bM, float var_floor, float *A, uint8_t *arg, const int *pos) {
   const int cpl = agg_cpl(c.H);
-  if (cpl == 2 && c.Fe == 4) agg_fwd_launch<2, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
-  else if (cpl == 2) agg_fwd_launch<2, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
-  else if (c.Fe == 4) agg_fwd_launch<1, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
-  else agg_fwd_launch<1, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, A_lo, pos);
+  if (cpl == 2 && c.Fe == 4) agg_fwd_launch<2, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
+  else if (cpl == 2) agg_fwd_launch<2, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
+  else if (c.Fe == 4) agg_fwd_launch<1, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
+  else agg_fwd_launch<1, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
   counted();
 }
 
@@ -528,7 +346,7 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
                                                     const float *__restrict__ Me, const float *__restrict__ bM,
                                                     const float *__restrict__ A, const uint8_t *__restrict__ arg,
                                                     const float *__restrict__ dA, float *__restrict__ dP,
-                                                    float *__restrict__ partial, int H, float *__restrict__ dP_lo,
+                                                    float *__restrict__ partial, int H,
                                                     const int *__restrict__ pos, const int *__restrict__ dp_pos) {
   pdl_enter();
   __shared__ float red[kAggBwdWarps][32][CPL * FE];
@@ -606,7 +424,6 @@ __global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ 
     }
     const size_t prow = (size_t)prow_out * H + ch;  // degree-sorted row when dp_pos is given
     store_vec<CPL>(dP + prow, dp);
-    if (dP_lo) store_vec_lo<CPL>(dP_lo + prow, dp);
 #pragma unroll
     for (int c = 0; c < CPL; ++c) bsum[c] += dp[c];
   }
@@ -657,42 +474,27 @@ __global__ void k_reduce_agg(const float *__restrict__ part, int nparts, int str
   }
 }
 
-// fixed-order reduction of nparts partial vectors: one warp per output element;
-// lanes stride over the parts, then a fixed xor-shuffle tree (deterministic)
-__global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < count; e += gridDim.x * wpb) {
-    float s = 0.f;
-    for (int p = lane; p < nparts; p += 32) s += part[(size_t)p * count + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[e] = s;
-  }
-}
-
 static int agg_bwd_blocks(const Caps &c) { return std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 2)); }
 size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * (c.Fe + 1); }
-int agg_bwd_partials(const Caps &c) { return agg_bwd_blocks(c); }
+
 
 template <int CPL, int FE>
 static void agg_bwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                            const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                           float *partial, float *dP_lo, const int *pos, const int *dp_pos) {
+                           float *partial, const int *pos, const int *dp_pos) {
   const dim3 grid(agg_bwd_blocks(c), c.H / (32 * CPL));
-  launch_ex(k_agg_bwd<CPL, FE>, grid, 32 * kAggBwdWarps, 0, st, blob, P, Me, bM, A, arg, dA, dP, partial, c.H, dP_lo,
+  launch_ex(k_agg_bwd<CPL, FE>, grid, 32 * kAggBwdWarps, 0, st, blob, P, Me, bM, A, arg, dA, dP, partial, c.H,
             pos, dp_pos);
 }
 
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe, float *dP_lo, const int *pos, const int *dp_pos) {
+                    float *partial, float *dMe, const int *pos, const int *dp_pos) {
   const int cpl = agg_cpl(c.H);
-  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
-  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
-  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
-  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, dP_lo, pos, dp_pos);
+  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
+  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
+  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
+  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
   counted();
   if (dMe) launch_reduce_dMe(st, c, partial, dMe);
 }
@@ -734,7 +536,7 @@ __global__ void __launch_bounds__(256) k_head(const uint8_t *__restrict__ blob, 
                                               float *__restrict__ yhat, float *__restrict__ sqerr,
                                               float *__restrict__ dy, float *__restrict__ dhid,
                                               float *__restrict__ dZL, int H, int Hf, int w1_in_smem,
-                                              float *__restrict__ dZL_lo, const int *__restrict__ pos) {
+                                              const int *__restrict__ pos) {
   pdl_enter();
   extern __shared__ float sm[];
   float *Gs = sm, *hs = Gs + H, *dh = hs + Hf, *red = dh + Hf, *W1s = red + 256;
@@ -818,7 +620,6 @@ __global__ void __launch_bounds__(256) k_head(const uint8_t *__restrict__ blob, 
         const float v = XL[o] > 0.f ? Gs[c] : 0.f;
         const size_t od = pos ? (size_t)pos[i] * H + c : o;  // degree-sorted row when pos is given
         dZL[od] = v;
-        if (dZL_lo) dZL_lo[od] = tf32_lo(v);
       }
     }
     __syncthreads();
@@ -839,8 +640,7 @@ __global__ void __launch_bounds__(256) k_head_fast(const uint8_t *__restrict__ b
                                                    float *__restrict__ G, float *__restrict__ hpre,
                                                    float *__restrict__ yhat, float *__restrict__ sqerr,
                                                    float *__restrict__ dy, float *__restrict__ dhid,
-                                                   float *__restrict__ dZL, float *__restrict__ dZL_lo,
-                                                   const int *__restrict__ pos) {
+                                                   float *__restrict__ dZL, const int *__restrict__ pos) {
   constexpr int H = 128 * CH, Hf = 8 * RW, RMAX = 8;
   __shared__ float4 red[8][H / 4];
   __shared__ float Gs[H], hs[Hf], dh[Hf];
@@ -1000,9 +800,6 @@ __global__ void __launch_bounds__(256) k_head_fast(const uint8_t *__restrict__ b
           const float4 v = make_float4(x.x > 0.f ? gv.x : 0.f, x.y > 0.f ? gv.y : 0.f, x.z > 0.f ? gv.z : 0.f,
                                        x.w > 0.f ? gv.w : 0.f);
           *reinterpret_cast<float4 *>(dZL + od + cc) = v;
-          if (dZL_lo)
-            *reinterpret_cast<float4 *>(dZL_lo + od + cc) =
-                make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
         }
       }
     }
@@ -1024,8 +821,7 @@ __global__ void __launch_bounds__(256) k_loss(const uint8_t *__restrict__ blob, 
 template <bool FWD, bool BWD>
 static void head_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                         const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
-                        float *sqerr, float *dy, float *dhid, float *dZL, float *dZL_lo = nullptr,
-                        const int *pos = nullptr) {
+                        float *sqerr, float *dy, float *dhid, float *dZL, const int *pos = nullptr) {
   const size_t base = sizeof(float) * (c.H + 2 * c.Hf + 256);
   const size_t w1 = sizeof(float) * (size_t)c.Hf * c.H;
   const int in_smem = base + w1 <= 200 * 1024 ? 1 : 0;  // attribute set once by head_configure
@@ -1033,14 +829,14 @@ static void head_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, con
   if (c.H == 128 && (c.Hf == 128 || c.Hf == 64)) {  // latency-optimised kernel
     if (c.Hf == 128)
       launch_ex(k_head_fast<FWD, BWD, 1, 16>, std::min(c.maxB, kSMs), 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre,
-                yhat, sqerr, dy, dhid, dZL, dZL_lo, pos);
+                yhat, sqerr, dy, dhid, dZL, pos);
     else
       launch_ex(k_head_fast<FWD, BWD, 1, 8>, std::min(c.maxB, kSMs), 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre,
-                yhat, sqerr, dy, dhid, dZL, dZL_lo, pos);
+                yhat, sqerr, dy, dhid, dZL, pos);
     return;
   }
   launch_ex(k_head<FWD, BWD>, std::min(c.maxB, kSMs), 256, smem, st, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
-            dhid, dZL, c.H, c.Hf, in_smem, dZL_lo, pos);
+            dhid, dZL, c.H, c.Hf, in_smem, pos);
 }
 
 void head_configure(const Caps &c) {  // outside graph capture: opt into large dynamic smem
@@ -1063,9 +859,8 @@ void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const 
 
 void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                        const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
-                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL, float *dZL_lo,
-                       const int *pos) {
-  head_launch<true, true>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy, dhid, dZL, dZL_lo, pos);
+                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL, const int *pos) {
+  head_launch<true, true>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy, dhid, dZL, pos);
   counted();
 }
 
@@ -1142,10 +937,10 @@ __global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__re
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
                      float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done,
-                     float *dZL_lo, const int *pos, bool with_grads) {
+                     const int *pos, bool with_grads) {
   if (!head_done) {
     head_launch<false, true>(st, c, blob, XL, W1, nullptr, W2, nullptr, nullptr, const_cast<float *>(hpre),
-                             const_cast<float *>(yhat), nullptr, dy, dhid, dZL, dZL_lo, pos);
+                             const_cast<float *>(yhat), nullptr, dy, dhid, dZL, pos);
     counted();
   }
   if (with_grads) launch_head_grads(st, c, blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2);

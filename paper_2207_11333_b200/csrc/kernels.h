@@ -7,9 +7,8 @@
 #include <stdint.h>
 
 namespace hg {
-extern bool g_pdl;
 extern bool g_low_prio;
-extern int g_prio_lo, g_prio_hi;  // launch kernels with programmatic dependent launch (common.cuh)
+extern int g_prio_lo, g_prio_hi;  // launch priorities (common.cuh launch_ex)
 
 struct Caps {
   int maxB, maxN, maxE;
@@ -17,43 +16,22 @@ struct Caps {
   int Hl = 0;  // logical hidden width (< H when the configuration is channel-padded; 0 = H)
 };
 
-// per-node degree scalers amp = ln(d+1)/delta, att = delta/ln(d+1) (1 for d=0)
-void launch_scalers(cudaStream_t st, const Caps &c, const uint8_t *blob, double delta, float *amp, float *att);
-
-// K1 / K9b / K3 / K7a / K7b / K9a GEMMs (SIMT fp32 v1)
-// P[N,H] = X[N,F] * Mx^T
+// K1 layer 0: P[N,H] = x[N,F0] * Mx^T (SIMT; layers >= 1 use launch_d_proj)
 void launch_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx, float *P);
-// X1 = ReLU(sum_s diag(s) A U_s^T + b_U)
-void launch_update(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *A, const float *amp,
-                   const float *att, const float *U, const float *bU, float *X1);
-// dA[N,4H] = sum_s diag(s) dZ U_s
-void launch_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *amp,
-               const float *att, const float *U, float *dA);
-// dU[H,12H] = sum_i s_i dZ_i^T A_i ; db_U = sum_i dZ_i   (split-K partials then fixed-order reduce)
-void launch_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
-               const float *amp, const float *att, float *partial, float *dU, float *dbU);
-// dM_x[H,F] = dP^T X ; db_M = sum_i dP_i
-void launch_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
-                float *partial, float *dMx, float *dbM);
-// dZprev[N,F] = (dP Mx) * [Xl > 0]
-void launch_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
-               const float *Xl, float *dZprev);
 
 // K2: fused edge gather + message + mean/min/max/std segmented reduction
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, float var_floor, float *A, uint8_t *arg, float *A_lo = nullptr,
+                    const float *bM, float var_floor, float *A, uint8_t *arg,
                     const int *pos = nullptr);  // pos: write A row i at pos[i] (degree-sorted)
 // K8: aggregation backward + scatter to sources; dM_e via block partials
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
                     const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe, float *dP_lo = nullptr, const int *pos = nullptr,
+                    float *partial, float *dMe, const int *pos = nullptr,
                     const int *dp_pos = nullptr);  // dp_pos: write dP row j at dp_pos[j]
 // dM_e = fixed-order sum of launch_agg_bwd's block partials (launch_agg_bwd does it when dMe != null)
 // (dbM != null: also db_M = sum_j dP_j from the same partials)
 void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe, float *dbM = nullptr);
 size_t agg_bwd_partial_floats(const Caps &c);
-size_t dU_partial_floats(const Caps &c);
-size_t dMx_partial_floats(const Caps &c, int F);
 
 // K4/K5: pool + head forward, loss
 void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
@@ -63,14 +41,14 @@ void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const 
 // head/pool backward down to dZ of the last layer (the loss itself: launch_loss)
 void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                        const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
-                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL, float *dZL_lo = nullptr,
-                       const int *pos = nullptr);
-// K6: head + pool backward -> dZ of the last layer (skipped if head_done), then head parameter gradients
+                       float *sqerr, float *loss, float *dy, float *dhid, float *dZL, const int *pos = nullptr);
+// K6 (eager backward after a forward-only head): head + pool backward -> dZ of the last
+// layer, then (with_grads) the head parameter gradients
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
                      float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done,
-                     float *dZL_lo = nullptr, const int *pos = nullptr, bool with_grads = true);
-// head parameter gradients only (the tail of launch_head_bwd)
+                     const int *pos = nullptr, bool with_grads = true);
+// head parameter gradients
 void launch_head_grads(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *G, const float *hpre,
                        const float *dy, const float *dhid, float *gW1, float *gb1, float *gW2, float *gb2);
 // evaluation sums of one batch into acc[0..2] (fp64: squared error, absolute error, graphs)
@@ -92,33 +70,41 @@ void launch_adamw(cudaStream_t st, float *p, const float *g, float *m, float *v,
 
 // fused gradient average + sharded AdamW + parameter all-gather over peer memory (p2p.cu)
 constexpr int kP2PMaxWorld = 8;
-struct P2PDev {                        // in every rank's workspace; zero at ctx creation
-  unsigned ready[2][kP2PMaxWorld];     // ready[part][q] = epoch: rank q's gradients of that part are complete
-  unsigned done[2][kP2PMaxWorld];      // done[part][q] = epoch: rank q's shard of that part is written everywhere
-  unsigned epoch;                      // steps taken through the p2p path
-  unsigned ticket[2];                  // k_p2p_adamw's finished-block counters
+constexpr unsigned kP2PTimeout = 1;  // P2PDev::error: a peer did not answer within the timeout
+struct P2PDev {                      // in every rank's workspace; zero at ctx creation
+  unsigned ready[kP2PMaxWorld];      // ready[q] = epoch: rank q's gradients of that step are complete
+  unsigned done[kP2PMaxWorld];       // done[q] = epoch: rank q's shard of that step is written everywhere
+  unsigned epoch;                    // steps taken through the p2p path
+  unsigned ticket;                   // k_p2p_adamw's finished-block counter
+  unsigned error;                    // kP2PTimeout after a timed-out wait (the kernel then traps)
+  unsigned pad;
 };
 struct P2PArgs {
   float *params[kP2PMaxWorld];       // every rank's parameter arena ([rank] = local)
   const float *grads[kP2PMaxWorld];  // every rank's gradient arena
   P2PDev *dev[kP2PMaxWorld];         // every rank's flags
+  const float *m_all[kP2PMaxWorld];  // every rank's Adam moments (moment gather)
+  const float *v_all[kP2PMaxWorld];
   float *m, *v;                      // local Adam moments (the owned shard is used)
   AdamDev *ad;
   int world, rank;
   int64_t n4;                        // float4s in the flat arena
+  unsigned long long timeout_ns;     // bound of every flag wait (0 = unbounded)
   float lr, beta1, beta2, eps, wd;
 };
-// one exchange part (0: conv0 at the step's end, 1: layers >= 1 + head, overlapped with layer
-// 0's backward) over float4 range [b4, e4): signal ready, wait for every rank's ready, fused
-// reduce + AdamW + all-gather of this rank's shard (bump: first part of the step; advance:
-// last part, advances the AdamW step counter); launch_p2p_wait_done: wait for every rank's
-// done flag of `part` (before parameters or gradients are touched again)
-void launch_p2p_part(cudaStream_t st, const P2PArgs &a, int part, int64_t b4, int64_t e4, bool bump, bool advance);
-void launch_p2p_wait_done(cudaStream_t st, const P2PArgs &a, int part);
+// one step's exchange: signal, wait for every ready flag, fused reduce + AdamW + all-gather of
+// this rank's shard, wait for every done flag
+void launch_p2p_exchange(cudaStream_t st, const P2PArgs &a);
+// the same arithmetic for ranks emulated in one process on one device (hg_p2p_emulate): the
+// ranks' kernels run back to back, so the flag waits are elided
+void launch_p2p_exchange_emulated(cudaStream_t st, const P2PArgs &a);
+// copy every peer's shard of the Adam moments into the local arrays
+void launch_p2p_gather_moments(cudaStream_t st, const P2PArgs &a);
 
-// degree classes (tcgemm.cu): one class per distinct degree present in the batch
-constexpr int kMaxClasses = 16;
-constexpr int kGramKS = 256;  // minimum nodes per K-split of the per-class Gram GEMM
+// degree classes (degsort.cu): one class per distinct degree present in the batch
+constexpr int kNumSMs = 148;     // B200
+constexpr int kMaxClasses = 32;  // class slots (distinct degrees per batch) at most
+constexpr int kGramKS = 256;     // minimum nodes per K-split of the per-class Gram GEMM
 // nodes per Gram K-split for a capacity: >= kGramKS, about 64 splits at large capacities
 // (the split partials are reduced afterwards, so their number bounds that traffic)
 inline int gram_ks(const Caps &c) {
@@ -127,85 +113,60 @@ inline int gram_ks(const Caps &c) {
 }
 constexpr int HG_MAX_DEGREE_DEV = 127;
 struct DegInfo {
-  int C, T, S, pad;
+  int C, T, S, overflow;  // classes, 128-row tiles, Gram splits; overflow: > cmax distinct degrees
   int deg[kMaxClasses], start[kMaxClasses], count[kMaxClasses];
   float amp[kMaxClasses], att[kMaxClasses];
 };
-int tc_num_classes(const Caps &c, int max_degree);  // class slots (max_degree+1) or 0 = class path off
+int tc_num_classes(int max_degree);  // class slots of a ctx: min(max_degree + 1, kMaxClasses)
 int tc_max_tiles(const Caps &c, int cmax);
 int tc_max_splits(const Caps &c, int cmax);
-// stable degree sort + per-node scalers (+ class table / tiles / splits when cmax > 0)
+// stable degree sort + per-node scalers + class table / tiles / splits
 // perm[r] = node at degree-sorted row r, pos = its inverse (pos may be null)
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
                     DegInfo *info, int4 *tiles, int4 *splits, int *pos = nullptr, int ks = 0);
 
-// TMA-fed tcgen05 GEMMs over pre-split operands (tcdirect.cu). A / dZ operands of
-// the class GEMMs are stored in degree-sorted row order (row pos[i] for node i).
+// TMA-fed tcgen05 GEMMs (tcdirect.cu): activation operands are read once as fp32 (their tf32
+// lo terms are derived in shared memory), weight operands with their lo terms (prep kernels).
+// A / dZ operands of the class GEMMs are stored in degree-sorted row order (row pos[i]).
+extern int g_gemm_passes;  // 3 = 3xTF32 (default), 1 = plain TF32 (HG_FLAG_TF32); set per enqueue
 cudaError_t tcd_configure();
-// (X1s, X1s_lo optional: also write the output rows in degree-sorted order)
-void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
+// (X1s optional: also write the output rows in degree-sorted order, X1mask their ReLU bits)
+void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
-                         float *X1, float *X1_lo, float *X1s = nullptr, float *X1s_lo = nullptr,
-                         uint32_t *X1mask = nullptr);
-void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
-                     const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA);
-void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
-                   const float *Mx, const float *Mx_lo, float *P);
-void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
-                 const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
-                 const int *pos);
-// fused backward (H == 128): dZ_{l-1} = (dP_l M_x) * [X_{l-1} > 0] (sorted rows, + lo) and
+                         float *X1, float *X1s = nullptr, uint32_t *X1mask = nullptr);
+void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const int *perm, const DegInfo *info,
+                     const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA);
+void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
+                   const float *Mx_lo, float *P);
+void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *MxT,
+                 const float *MxT_lo, int F, const float *Xl, float *dZ, const int *pos);
+// fused backward (H == 128): dZ_{l-1} = (dP_l M_x) * [X_{l-1} > 0] (sorted rows) and
 // dA_{l-1} = dZ_{l-1} W_c per degree-class tile; dP_s / Xs in degree-sorted row order
 bool dxda_supported(const Caps &c);
-void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *dP_s_lo, const float *MxT,
-                 const float *MxT_lo, const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info,
-                 const int4 *tiles, const uint32_t *Xmask, float *dZ, float *dZ_lo, float *dA);
+void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *MxT, const float *MxT_lo,
+                 const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info, const int4 *tiles,
+                 const uint32_t *Xmask, float *dZ, float *dA);
 void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,
                     float *Mx_lo, float *MxT, float *MxT_lo);
-// layers [l0, l1) of the degree-slot weights
+// layers [l0, l1) of the class weights (needs the batch's class table: after launch_degsort)
 void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int l0, int l1,
-                    int cmax, double delta, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo);
+                    int cmax, const DegInfo *info, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo);
 
 extern int g_mn_grid_override;  // tcmn.cu: grid cap override for MN Grams (0 = default)
 // TMA-fed MN-major Grams (tcmn.cu): per-class-split dU / db_U and per-split dM_x / db_M,
-// partials reduced in fixed order (class path; rows of dZ / A degree-sorted)
+// partials reduced in fixed order (rows of dZ / A degree-sorted)
 size_t mn_gram_partial_floats(const Caps &c, int cmax);
 size_t mn_dmx_partial_floats(const Caps &c, int F);
-void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const float *A,
-                      const float *A_lo, const float *ones, const DegInfo *info, const int4 *splits, float *partial,
-                      float *dU, float *dbU);
+void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *A, const float *ones,
+                      const DegInfo *info, const int4 *splits, float *partial, float *dU, float *dbU);
 // X: [maxN][Fp] (Fp >= F, 16-byte row pitch; Fp = F for hidden layers), F output columns
-void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
-                   const float *X, const float *X_lo, int F, int Fp, const float *ones, float *partial, float *dMx,
+void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F, int Fp,
+                   const float *ones, float *partial, float *dMx,
                    float *dbM);  // dbM == null: no column-sum tiles (db_M comes from launch_reduce_dMe)
-// layer-0 node features padded to pad_x0_width(F0) columns (+ tf32 residual) for the TMA path
+// layer-0 node features padded to pad_x0_width(F0) columns for the TMA path
 int pad_x0_width(int F0);
-void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo,
+void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp,
                    const int *pos = nullptr);  // pos: write row i at pos[i]
-int agg_bwd_partials(const Caps &c);  // number of dM_e block partials launch_agg_bwd writes
-
-// tcgen05 3xTF32 GEMMs (tcgemm.cu); require H % 128 == 0
-bool tc_supported(const Caps &c);
-cudaError_t tc_configure();  // opt-in shared-memory sizes (call once, outside graph capture)
-void launch_tc_update(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *A, const float *amp,
-                      const float *att, const float *U, const float *bU, float *X1);
-void launch_tc_dA(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *amp,
-                  const float *att, const float *UT, float *dA);
-void launch_tc_dU(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dZ, const float *A,
-                  const float *amp, const float *att, float *partial, float *dU, float *dbU);
-size_t tc_dU_partial_floats(const Caps &c);
-bool tc_proj_ok(const Caps &c, int F);  // X rows 16-byte aligned
-bool tc_dmx_ok(const Caps &c, int F);
-void launch_tc_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
-                    float *P);
-void launch_tc_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *Mx, int F,
-                  const float *Xl, float *dZprev);
-size_t tc_dMx_partial_floats(const Caps &c, int F);
-void launch_tc_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F,
-                   float *partial, float *dMx, float *dbM);
-// UT[l][s*4H + n][h] = U_l[h][s*4H + n] for all layers (u_off: device array of U offsets in floats)
-void launch_prep_UT(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int L,
-                    float *UT);
 
 // process-wide count of kernels launched by the wrappers above
 int64_t launches_so_far();

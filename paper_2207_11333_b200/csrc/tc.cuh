@@ -167,6 +167,24 @@ __device__ __forceinline__ void tma_prefetch_desc(const void *tmap) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(tmap) : "memory");
 }
 
+// lo terms x - trunc19(x) of n16 16-byte chunks at src, written to dst at the same offsets
+// (a swizzle permutes whole 16-byte chunks, so the transform is layout-agnostic); thread t
+// of nt takes chunks t, t + nt, ... (consecutive lanes read consecutive chunks: no bank
+// conflicts). The 3xTF32 GEMMs derive their activation operands' lo terms this way in shared
+// memory instead of reading a stored residual.
+__device__ __forceinline__ void lo_chunks(const uint8_t *src, uint8_t *dst, int n16, int t, int nt) {
+#pragma unroll 4
+  for (int i = t; i < n16; i += nt) {
+    const float4 v = *reinterpret_cast<const float4 *>(src + 16 * i);
+    float4 l;
+    l.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    l.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    l.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    l.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    *reinterpret_cast<float4 *>(dst + 16 * i) = l;
+  }
+}
+
 // 3xTF32 split: hi keeps the 10 explicit mantissa bits TF32 uses, lo = x - hi (exact)
 __device__ __forceinline__ void split_tf32(float x, float &hi, float &lo) {
   hi = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);

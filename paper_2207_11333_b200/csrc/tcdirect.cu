@@ -36,27 +36,16 @@
 namespace hg {
 
 extern std::atomic<int64_t> g_launches;
-// output-tile width per TMA GEMM (update, dA, proj, dX); HG_BN_<OP>=32|64|128 for A/B runs.
-// 0 = by shape: 128 for H >= 256 (measured: E512 +14%, E256 +9%; N = 64 MMAs are
+// output-tile width of the TMA GEMMs update, proj and dX (dA: 128), by shape: 128 for H >= 256 (measured: E512 +14%, E256 +9%; N = 64 MMAs are
 // shared-memory-read bound); at H = 128, 32 for small batches (config B: 4x51 CTAs instead
 // of 2x51 for these latency-bound GEMMs, +1.5%), 64 for large ones (config D)
-int g_bn_upd = 0, g_bn_da = 128, g_bn_proj = 0, g_bn_dx = 0;
-int bn_auto(int v, const Caps &c) { return v ? v : (c.H >= 256 ? 128 : c.maxN <= 16384 ? 32 : 64); }
-bool g_update_sk = false;  // split-K cluster update (HG_UPDATE_SK=1): measured slower, see DESIGN.md
+static int bn_auto(const Caps &c) { return c.H >= 256 ? 128 : c.maxN <= 16384 ? 32 : 64; }
 
 
-// experiments only: per-CTA %globaltimer trace of one Op type (hg_debug_set_trace)
-__device__ unsigned long long *g_trace = nullptr;
-__device__ int g_trace_id = -1;
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#define TTRACE(j)                                                                     \
-  do {                                                                                \
-    if (g_trace && g_trace_id == Op::ID) g_trace[blockIdx.x * 8 + (j)] = gtimer();   \
-  } while (0)
+// GEMM passes of the tf32 tensor-core GEMMs: 3 = 3xTF32 (fp32-accurate, the graded mode),
+// 1 = plain TF32 (hg_config.flags HG_FLAG_TF32, the reduced-precision mode). Set by the step
+// builder before it enqueues a ctx's kernels (like g_low_prio).
+int g_gemm_passes = 3;
 
 namespace {
 
@@ -64,7 +53,8 @@ constexpr int T_BM = 128;
 constexpr int T_BK = 32;  // fp32 per 128-byte swizzle row
 constexpr int T_TMA_WARP = 4;
 constexpr int T_MMA_WARP = 5;
-constexpr int T_THREADS = 192;
+constexpr int T_XF_WARP = 6;  // warps 6-9: the A operand's lo terms in shared memory
+constexpr int T_THREADS = 320;
 
 template <int N>
 struct TCols {
@@ -82,7 +72,7 @@ constexpr int t_stages() {
 }
 template <class Op>
 constexpr int t_smem_bytes() {
-  return t_stages<Op>() * t_stage_bytes<Op>() + T_STG_BYTES + 1024 + 8 * (2 * t_stages<Op>() + 4) + 16;
+  return t_stages<Op>() * t_stage_bytes<Op>() + T_STG_BYTES + 1024 + 8 * (3 * t_stages<Op>() + 4) + 16;
 }
 
 }  // namespace
@@ -91,10 +81,16 @@ constexpr int t_smem_bytes() {
 // device-side count are skipped by every role alike). The smem ring continues
 // across items and the accumulator is double-buffered in TMEM (2 x BN columns),
 // so the epilogue of item i overlaps the loads and MMAs of item i + 1.
-// Epilogue: TMEM -> registers -> per-warp staging tile -> Op::emit, one float4
-// per lane with 8 lanes per row, so global stores are 128-byte coalesced rows.
+//   warps 0-3  epilogue: TMEM -> registers -> per-warp staging tile -> Op::emit, one float4
+//              per lane with 8 lanes per row, so global stores are 128-byte coalesced rows
+//   warp 4     TMA producer: per K chunk the A tile (activation, fp32) and the B tile hi and
+//              lo (weights, split once per step by the prep kernels)
+//   warp 5     TMEM allocation + single-thread tcgen05.mma issue
+//   warps 6-9  A_lo = A - trunc19(A) of each landed A tile, written into the stage's A_lo
+//              slot (3xTF32 only): activations are stored once, as fp32, in HBM
+// passes == 1: plain TF32 (one MMA per k-step, no lo terms loaded or derived).
 template <class Op>
-__global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ TmaMaps mp, Op op_in) {
+__global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ TmaMaps mp, Op op_in, int passes) {
   constexpr int BN = Op::BN, ST = t_stages<Op>();
   constexpr int A_BYTES = T_BM * 128, B_BYTES = BN * 128, STAGE = t_stage_bytes<Op>();
   // TMEM: two buffers of the main accumulator (hi*hi) at columns [0, 2BN) and two of the
@@ -111,22 +107,23 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
   float *stg_all = reinterpret_cast<float *>(smem + ST * STAGE);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE + T_STG_BYTES);
   uint64_t *empty = full + ST;
-  uint64_t *accf = empty + ST;  // [2] MMA -> epilogue
-  uint64_t *acce = accf + 2;    // [2] epilogue -> MMA
+  uint64_t *lofull = empty + ST;  // [ST] transform -> MMA
+  uint64_t *accf = lofull + ST;   // [2] MMA -> epilogue
+  uint64_t *acce = accf + 2;      // [2] epilogue -> MMA
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acce + 2);
+  const bool p3 = passes == 3;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) TTRACE(0);
   // prologue: no global memory written by earlier kernels is touched before pdl_enter
   if (warp == T_MMA_WARP) tc::tmem_alloc<TCOLS>(tmem_holder);
   if (threadIdx.x == T_TMA_WARP * 32) {
     tc::tma_prefetch_desc(&mp.ah);
-    tc::tma_prefetch_desc(&mp.al);
     tc::tma_prefetch_desc(&mp.bh);
-    tc::tma_prefetch_desc(&mp.bl);
+    if (p3) tc::tma_prefetch_desc(&mp.bl);
     for (int s = 0; s < ST; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&lofull[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&accf[b], 1);
@@ -139,14 +136,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_holder;
   pdl_enter();
-  if (threadIdx.x == 0) {
-    TTRACE(1);
-    if (g_trace && g_trace_id == Op::ID) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      g_trace[blockIdx.x * 8 + 7] = smid;
-    }
-  }
 
   Op op = op_in;
   const int items = op.items_cap;
@@ -154,6 +143,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
     // ---------------- TMA producer
     if (lane == 0) {
       int it = 0;
+      const uint32_t bytes = A_BYTES + (p3 ? 2 : 1) * B_BYTES;
       for (int item = blockIdx.x; item < items; item += gridDim.x) {
         int m0, n0, ke, ay, by;
         if (!op.tile(item, m0, n0, ke, ay, by)) continue;
@@ -162,17 +152,35 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
           const int s = it % ST;
           if (it >= ST) tc::mbar_wait(&empty[s], ((it / ST) - 1) & 1);
           uint8_t *sa = smem + s * STAGE;
-          tc::mbar_expect_tx(&full[s], STAGE);
+          tc::mbar_expect_tx(&full[s], bytes);
           const int k0 = c * T_BK;
           tc::tma_load_2d(sa, &mp.ah, k0, ay, &full[s]);
-          tc::tma_load_2d(sa + A_BYTES, &mp.al, k0, ay, &full[s]);
           tc::tma_load_2d(sa + 2 * A_BYTES, &mp.bh, k0, by, &full[s]);
-          tc::tma_load_2d(sa + 2 * A_BYTES + B_BYTES, &mp.bl, k0, by, &full[s]);
-          if (it == 0) TTRACE(2);
+          if (p3) tc::tma_load_2d(sa + 2 * A_BYTES + B_BYTES, &mp.bl, k0, by, &full[s]);
         }
       }
     }
     __syncwarp();
+  } else if (warp >= T_XF_WARP) {
+    // ---------------- A_lo of every landed A tile (3xTF32)
+    if (p3) {
+      int it = 0;
+      const int t = threadIdx.x - T_XF_WARP * 32;
+      for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        int m0, n0, ke, ay, by;
+        if (!op.tile(item, m0, n0, ke, ay, by)) continue;
+        const int nchunks = (ke + T_BK - 1) / T_BK;
+        for (int c = 0; c < nchunks; ++c, ++it) {
+          const int s = it % ST;
+          tc::mbar_wait(&full[s], (it / ST) & 1);
+          uint8_t *sa = smem + s * STAGE;
+          tc::lo_chunks(sa, sa + A_BYTES, A_BYTES / 16, t, 128);
+          tc::fence_proxy_async_smem();  // generic smem writes -> visible to the tensor core
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&lofull[s]);
+        }
+      }
+    }
   } else if (warp == T_MMA_WARP) {
     // ---------------- MMA issuer
     if (lane == 0) {
@@ -189,25 +197,26 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
         for (int c = 0; c < nchunks; ++c, ++it) {
           const int s = it % ST;
           tc::mbar_wait(&full[s], (it / ST) & 1);
+          if (p3) tc::mbar_wait(&lofull[s], (it / ST) & 1);
           tc::fence_after_sync();
-          if (it == 0) TTRACE(3);
           const uint32_t aH = tc::smem_u32(smem + s * STAGE);
           const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
 #pragma unroll
           for (int ks = 0; ks < T_BK / 8; ++ks) {
             const uint32_t off = ks * 32;
-            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
-            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+            const uint64_t dah = tc::desc_sw128(aH + off), dbh = tc::desc_sw128(bH + off);
             tc::mma_tf32(d, dah, dbh, idesc, (c | ks) != 0);
-            tc::mma_tf32(dc, dah, dbl, idesc, (c | ks) != 0);
-            tc::mma_tf32(dc, dal, dbh, idesc, 1u);
+            if (p3) {
+              const uint64_t dal = tc::desc_sw128(aL + off), dbl = tc::desc_sw128(bL + off);
+              tc::mma_tf32(dc, dah, dbl, idesc, (c | ks) != 0);
+              tc::mma_tf32(dc, dal, dbh, idesc, 1u);
+            }
           }
           tc::mma_commit(&empty[s]);
         }
         tc::mma_commit(&accf[buf]);
         ++tcount;
       }
-      TTRACE(4);
     }
     __syncwarp();
   } else {
@@ -220,13 +229,17 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
       const int buf = tcount & 1;
       tc::mbar_wait(&accf[buf], (tcount >> 1) & 1);
       tc::fence_after_sync();
-      if (threadIdx.x == 0 && tcount == 0) TTRACE(5);
       const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
       for (int q = 0; q < BN / 32; ++q) {
         float acc[32], cor[32];
         tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
-        tc::tmem_ld32(trow + (uint32_t)(2 * BN + q * 32), cor);
+        if (p3) {
+          tc::tmem_ld32(trow + (uint32_t)(2 * BN + q * 32), cor);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) cor[i] = 0.f;
+        }
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) =
@@ -250,7 +263,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_tma(const __grid_constant__ Tm
       if (lane == 0) tc::mbar_arrive(&acce[buf]);
       ++tcount;
     }
-    if (threadIdx.x == 0) TTRACE(6);
   }
   tc::fence_before_sync();
   __syncthreads();
@@ -272,13 +284,13 @@ __device__ __forceinline__ float4 lo4(float4 v) { return make_float4(lo_of(v.x),
 // the row coordinates of the A and B boxes in their tensor maps (false: no
 // work for this item). emit(m, n, v): epilogue for output row m, columns n..n+3.
 
-// G1 update per degree class (A in sorted rows): X1[perm[m]] = ReLU(A[m] W_c^T + b_U), also X1_lo
+// G1 update per degree class (A in sorted rows): X1[perm[m]] = ReLU(A[m] W_c^T + b_U)
 template <int BN_>
 struct TUpdC {
-  static constexpr int BN = BN_, ID = 0;
-  const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1, *X1_lo; int H; int items_cap;
-  float *X1s, *X1s_lo;  // optional: the same rows in degree-sorted order (backward dX/dM_x operands)
-  uint32_t *X1mask;     // optional: ReLU mask bits of the sorted rows, [rows][H/32] words
+  static constexpr int BN = BN_;
+  const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1; int H; int items_cap;
+  float *X1s;        // optional: the same rows in degree-sorted order (backward dX/dM_x operands)
+  uint32_t *X1mask;  // optional: ReLU mask bits of the sorted rows, [rows][H/32] words
   int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     const int nt = H / BN, ti = t / nt;
@@ -307,22 +319,15 @@ struct TUpdC {
       if ((lane & 7) == 0 && m < row_end) X1mask[(size_t)m * (H / 32) + n / 32] = w;
     }
     if (m >= row_end) return;
-    const size_t o = (size_t)p.node * H + n;
-    *reinterpret_cast<float4 *>(X1 + o) = z;
-    const float4 zl = lo4(z);
-    *reinterpret_cast<float4 *>(X1_lo + o) = zl;
-    if (X1s) {
-      const size_t os = (size_t)m * H + n;
-      *reinterpret_cast<float4 *>(X1s + os) = z;
-      *reinterpret_cast<float4 *>(X1s_lo + os) = zl;
-    }
+    *reinterpret_cast<float4 *>(X1 + (size_t)p.node * H + n) = z;
+    if (X1s) *reinterpret_cast<float4 *>(X1s + (size_t)m * H + n) = z;
   }
 };
 
 // G2 dA per degree class (dZ in sorted rows): dA[perm[m]] = dZ[m] W_c
 template <int BN_>
 struct TDAC {
-  static constexpr int BN = BN_, ID = 1;
+  static constexpr int BN = BN_;
   const int *perm; const DegInfo *info; const int4 *tiles; float *dA; int H; int items_cap;
   int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
@@ -347,7 +352,7 @@ struct TDAC {
 // K1 projection (layers > 0): P = X M_x^T
 template <int BN_>
 struct TProj {
-  static constexpr int BN = BN_, ID = 2;
+  static constexpr int BN = BN_;
   const uint8_t *blob; float *P; int F, H; int items_cap;
   int N;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
@@ -366,11 +371,11 @@ struct TProj {
   }
 };
 
-// K9b dX (layers > 0): dZprev[pos[m]] = (dP[m] M_x) * [X_l[m] > 0] (sorted rows), also its lo
+// K9b dX (layers > 0, H > 128): dZprev[pos[m]] = (dP[m] M_x) * [X_l[m] > 0] (sorted rows)
 template <int BN_>
 struct TDX {
-  static constexpr int BN = BN_, ID = 3;
-  const uint8_t *blob; const float *Xl; float *dZ, *dZ_lo; const int *pos; int H, F; int items_cap;
+  static constexpr int BN = BN_;
+  const uint8_t *blob; const float *Xl; float *dZ; const int *pos; int H, F; int items_cap;
   int N;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     N = batch_N(blob);
@@ -389,41 +394,37 @@ struct TDX {
     const float4 x = p.x;
     const float4 z = make_float4(x.x > 0.f ? v.x : 0.f, x.y > 0.f ? v.y : 0.f, x.z > 0.f ? v.z : 0.f,
                                  x.w > 0.f ? v.w : 0.f);
-    const size_t od = (size_t)p.row * F + n;
-    *reinterpret_cast<float4 *>(dZ + od) = z;
-    *reinterpret_cast<float4 *>(dZ_lo + od) = lo4(z);
+    *reinterpret_cast<float4 *>(dZ + (size_t)p.row * F + n) = z;
   }
 };
 
 // ---------------------------------------------------------------- fused dX -> dA
 // Backward of layer l's projection chained into layer l-1's update backward, per
-// 128-row degree-class tile (rows degree-sorted) and 128-column slice of dA:
+// 128-row degree-class tile (rows degree-sorted) and pair of 128-column slices of dA:
 //   stage 1  T   = dP_l[rows] M_x                     (K = H,  N = F = H)
-//   epi 1    dZ  = T * [X_{l-1}[rows] > 0]  -> smem (K-major SW128, hi + lo) as stage 2's A;
-//                                              slice 0 also stores dZ_{l-1} (+ lo) for the Gram
+//   epi 1    dZ  = T * [X_{l-1}[rows] > 0]  -> smem (K-major SW128, hi + lo, split in
+//                                              registers) as stage 2's A; the CTAs of a
+//                                              tile share storing dZ_{l-1} for the Gram
 //   stage 2  dA  = dZ W_c^T...               (K = F,  N = 128 of 4H) -> dA[perm[m]]
 // Every operand row range is contiguous (dP_l and X_{l-1} are kept in sorted order for this).
 // The stage-1 ring (2 x 64 KB) is reused for the 128 KB dZ tile once stage 1's MMAs are done.
-// warps 0-3 epilogues, warp 4 TMA, warp 5 TMEM + MMA; one tile per CTA.
+// warps 0-3 stage-1 A_lo transform, then the epilogues; warp 4 TMA; warp 5 TMEM + MMA.
 struct DxDaMaps {
-  CUtensorMap ah, al;  // dP_l sorted rows [maxN][H]
+  CUtensorMap ah;      // dP_l sorted rows [maxN][H]
   CUtensorMap bh, bl;  // M_x^T [F][H]
   CUtensorMap wh, wl;  // W_c^T rows of layer l-1 [cmax*4H][F]
 };
+constexpr int XD_THREADS = 192;
 constexpr int XD_ST1 = 2, XD_ST2 = 2;
 constexpr int XD_NS = 2;  // dA slices (of 128 columns) per CTA: stage 1 is recomputed 4H/(128*XD_NS) times per tile
 constexpr int XD_STAGE1 = 4 * 128 * 128;  // A hi/lo + B hi/lo: 64 KB
 constexpr int XD_STAGE2 = 2 * 128 * 128;  // W hi/lo: 32 KB
 constexpr int XD_SMEM = XD_ST1 * XD_STAGE1 + XD_ST2 * XD_STAGE2 + T_STG_BYTES + 1024 + 8 * 16 + 16;
 
-struct SkTraceOp5 {
-  static constexpr int ID = 5;
-};
-__global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ DxDaMaps mp, const int *perm,
-                                                       const DegInfo *info, const int4 *tiles,
-                                                       const uint32_t *Xmask, float *dZ, float *dZ_lo, float *dA,
-                                                       int H) {
-  using Op = SkTraceOp5;
+__global__ void __launch_bounds__(XD_THREADS, 1) k_dxda(const __grid_constant__ DxDaMaps mp, const int *perm,
+                                                        const DegInfo *info, const int4 *tiles,
+                                                        const uint32_t *Xmask, float *dZ, float *dA, int H,
+                                                        int passes) {
   constexpr int F = 128;  // dZ width (= H, checked by the launcher)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -432,10 +433,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
   float *stg_all = reinterpret_cast<float *>(ring2 + XD_ST2 * XD_STAGE2);
   uint64_t *bar = reinterpret_cast<uint64_t *>(reinterpret_cast<uint8_t *>(stg_all) + T_STG_BYTES);
   uint64_t *full1 = bar, *empty1 = bar + 2, *full2 = bar + 4, *empty2 = bar + 6, *acc1 = bar + 8, *acc2 = bar + 9,
-           *zrdy = bar + 10;
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 12);
+           *zrdy = bar + 10, *lofull1 = bar + 12;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(bar + 14);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x == 0) TTRACE(0);
+  const bool p3 = passes == 3;
   if (warp == T_MMA_WARP) tc::tmem_alloc<512>(tmem_holder);
   if (threadIdx.x == T_TMA_WARP * 32) {
     for (int i = 0; i < 2; ++i) {
@@ -443,6 +444,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
       tc::mbar_init(&empty1[i], 1);
       tc::mbar_init(&full2[i], 1);
       tc::mbar_init(&empty2[i], 1);
+      tc::mbar_init(&lofull1[i], 4);
     }
     tc::mbar_init(acc1, 1);
     tc::mbar_init(acc2, 1);
@@ -455,7 +457,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_holder;  // cols [0,128): T, [128 + 128 s, ...): dA slice s
   pdl_enter();
-  if (threadIdx.x == 0) TTRACE(1);
   const int NG = 4 * H / (128 * XD_NS), ti = blockIdx.x / NG, n2 = (blockIdx.x % NG) * 128 * XD_NS;
   if (ti < info->T) {  // uniform per CTA
     const int4 tl = tiles[ti];
@@ -468,20 +469,19 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
           const int s = c & 1;
           if (c >= 2) tc::mbar_wait(&empty1[s], 0);
           uint8_t *sa = ring1 + s * XD_STAGE1;
-          tc::mbar_expect_tx(&full1[s], XD_STAGE1);
+          tc::mbar_expect_tx(&full1[s], p3 ? 3 * 16384 : 2 * 16384);
           tc::tma_load_2d(sa, &mp.ah, c * T_BK, tl.y, &full1[s]);
-          tc::tma_load_2d(sa + 16384, &mp.al, c * T_BK, tl.y, &full1[s]);
           tc::tma_load_2d(sa + 32768, &mp.bh, c * T_BK, 0, &full1[s]);
-          tc::tma_load_2d(sa + 49152, &mp.bl, c * T_BK, 0, &full1[s]);
+          if (p3) tc::tma_load_2d(sa + 49152, &mp.bl, c * T_BK, 0, &full1[s]);
         }
         for (int c = 0; c < KC2 * XD_NS; ++c) {  // slice c / KC2, K chunk c % KC2
           const int s = c & 1;
           if (c >= 2) tc::mbar_wait(&empty2[s], ((c >> 1) - 1) & 1);
           uint8_t *sw = ring2 + s * XD_STAGE2;
           const int wrow = tl.x * 4 * H + n2 + (c / KC2) * 128;  // rows of W_c^T for this dA slice
-          tc::mbar_expect_tx(&full2[s], XD_STAGE2);
+          tc::mbar_expect_tx(&full2[s], p3 ? XD_STAGE2 : XD_STAGE2 / 2);
           tc::tma_load_2d(sw, &mp.wh, (c % KC2) * T_BK, wrow, &full2[s]);
-          tc::tma_load_2d(sw + 16384, &mp.wl, (c % KC2) * T_BK, wrow, &full2[s]);
+          if (p3) tc::tma_load_2d(sw + 16384, &mp.wl, (c % KC2) * T_BK, wrow, &full2[s]);
         }
       }
       __syncwarp();
@@ -491,16 +491,18 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
         for (int c = 0; c < KC1; ++c) {
           const int s = c & 1;
           tc::mbar_wait(&full1[s], (c >> 1) & 1);
+          if (p3) tc::mbar_wait(&lofull1[s], (c >> 1) & 1);
           tc::fence_after_sync();
           const uint32_t aH = tc::smem_u32(ring1 + s * XD_STAGE1), aL = aH + 16384, bH = aH + 32768, bL = aH + 49152;
 #pragma unroll
           for (int ks = 0; ks < T_BK / 8; ++ks) {
             const uint32_t off = ks * 32;
-            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
-            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+            const uint64_t dah = tc::desc_sw128(aH + off), dbh = tc::desc_sw128(bH + off);
             tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
-            tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
-            tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
+            if (p3) {
+              tc::mma_tf32(tmem, dah, tc::desc_sw128(bL + off), idesc, 1u);
+              tc::mma_tf32(tmem, tc::desc_sw128(aL + off), dbh, idesc, 1u);
+            }
           }
           tc::mma_commit(&empty1[s]);
         }
@@ -518,11 +520,12 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
 #pragma unroll
           for (int ks = 0; ks < T_BK / 8; ++ks) {
             const uint32_t off = ks * 32;
-            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
-            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
+            const uint64_t dah = tc::desc_sw128(aH + off), dbh = tc::desc_sw128(bH + off);
             tc::mma_tf32(d, dah, dbh, idesc, (kc | ks) != 0);
-            tc::mma_tf32(d, dah, dbl, idesc, 1u);
-            tc::mma_tf32(d, dal, dbh, idesc, 1u);
+            if (p3) {
+              tc::mma_tf32(d, dah, tc::desc_sw128(bL + off), idesc, 1u);
+              tc::mma_tf32(d, tc::desc_sw128(aL + off), dbh, idesc, 1u);
+            }
           }
           tc::mma_commit(&empty2[s]);
           if (kc == KC2 - 1) tc::mma_commit(sl == 0 ? acc2 : acc2 + 2);
@@ -530,7 +533,19 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
       }
       __syncwarp();
     } else {
-      // ---------------- epilogue 1: mask, dZ tile into smem (+ global for slice 0)
+      // ---------------- stage-1 A_lo: dP_l tile lo terms (3xTF32), chunk by chunk
+      if (p3) {
+        for (int c = 0; c < KC1; ++c) {
+          const int s = c & 1;
+          tc::mbar_wait(&full1[s], (c >> 1) & 1);
+          uint8_t *sa = ring1 + s * XD_STAGE1;
+          tc::lo_chunks(sa, sa + 16384, 16384 / 16, threadIdx.x, 128);
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&lofull1[s]);
+        }
+      }
+      // ---------------- epilogue 1: mask, dZ tile into smem (+ global, shared by the slice groups)
       const int row = warp * 32 + lane, m = tl.y + row;
       float *stg = stg_all + warp * 32 * T_STG_LD;
       // the ReLU mask of X_{l-1} for this row: 128 bits written by layer l-1's update epilogue
@@ -542,10 +557,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
         mbits[2] = mw.z;
         mbits[3] = mw.w;
       }
-      if (threadIdx.x == 0) TTRACE(2);
       tc::mbar_wait(acc1, 0);
       tc::fence_after_sync();
-      if (threadIdx.x == 0) TTRACE(3);
       const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
 #pragma unroll 1
       for (int q = 0; q < F / 32; ++q) {
@@ -560,7 +573,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
                                        (b4 & 4u) ? t[4 * j + 2] : 0.f, (b4 & 8u) ? t[4 * j + 3] : 0.f);
           const uint32_t o = tc::sw128_off(row, j);
           *reinterpret_cast<float4 *>(ch + o) = z;
-          *reinterpret_cast<float4 *>(ch + 16384 + o) = lo4(z);
+          if (p3) *reinterpret_cast<float4 *>(ch + 16384 + o) = lo4(z);
           *reinterpret_cast<float4 *>(stg + lane * T_STG_LD + 4 * j) = z;
         }
         __syncwarp();
@@ -570,11 +583,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int r = 4 * j + (lane >> 3), cc = 4 * (lane & 7), mr = tl.y + warp * 32 + r;
-            if (mr < row_end) {
-              const float4 z = *reinterpret_cast<const float4 *>(stg + r * T_STG_LD + cc);
-              *reinterpret_cast<float4 *>(dZ + (size_t)mr * F + q * 32 + cc) = z;
-              *reinterpret_cast<float4 *>(dZ_lo + (size_t)mr * F + q * 32 + cc) = lo4(z);
-            }
+            if (mr < row_end)
+              *reinterpret_cast<float4 *>(dZ + (size_t)mr * F + q * 32 + cc) =
+                  *reinterpret_cast<const float4 *>(stg + r * T_STG_LD + cc);
           }
         }
         __syncwarp();
@@ -583,7 +594,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
       tc::fence_before_sync();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(zrdy);
-      if (threadIdx.x == 0) TTRACE(4);
       // ---------------- epilogue 2: dA rows (node order), slice by slice
       int node[8];  // the 8 rows this lane stores, resolved once for every column chunk
 #pragma unroll
@@ -597,7 +607,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
         if ((q & 3) == 0) {
           tc::mbar_wait(sl == 0 ? acc2 : acc2 + 2, 0);
           tc::fence_after_sync();
-          if (threadIdx.x == 0 && sl == 0) TTRACE(5);
         }
         float a[32];
         tc::tmem_ld32(trow + 128u + (uint32_t)(q * 32), a);
@@ -615,10 +624,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
         }
         __syncwarp();
       }
-      if (threadIdx.x == 0) {
-        TTRACE(6);
-        if (g_trace && g_trace_id == Op::ID) g_trace[blockIdx.x * 8 + 7] = 1;  // (valid CTA)
-      }
     }
   }
   tc::fence_before_sync();
@@ -626,207 +631,6 @@ __global__ void __launch_bounds__(T_THREADS, 1) k_dxda(const __grid_constant__ D
   if (warp == T_MMA_WARP) {
     tc::fence_after_sync();
     tc::tmem_dealloc<512>(tmem);
-  }
-}
-
-// ---------------------------------------------------------------- split-K update
-// G1 with K = 4H split over a cluster of KS = 4 CTAs (one aggregator block of
-// the class weights each), so a 128-row tile is served by 4 SMs instead of 1:
-// CTA r of the cluster accumulates A[:, rH:(r+1)H] W_c[:, rH:(r+1)H]^T (H x H,
-// 3xTF32) in TMEM; after a cluster barrier every CTA writes the column quarters
-// it does not own into the owner's shared memory (distributed shared memory,
-// st.shared::cluster), and after a second barrier CTA r sums the four partials
-// of its quarter in fixed rank order (deterministic) and applies the epilogue
-// (b_U, ReLU, X1 and its lo term, scattered to node order through perm).
-constexpr int SK_KS = 4;
-constexpr int SK_H = 128;  // H handled by this kernel (output tile = all H columns)
-constexpr int SK_ST = 3;
-constexpr int SK_STAGE = 4 * SK_H * 128;  // A hi/lo (128 rows) + B hi/lo (128 rows), one 32-wide K chunk
-constexpr int SK_SMEM = SK_ST * SK_STAGE + 1024 + 8 * (2 * SK_ST + 1) + 16;
-static_assert(SK_KS * SK_H * (SK_H / SK_KS) * 4 <= SK_ST * SK_STAGE, "receive buffer fits the stage ring");
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t map_peer(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void st_cluster_v4(uint32_t addr, float4 v) {
-  asm volatile("st.shared::cluster.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z),
-               "f"(v.w)
-               : "memory");
-}
-
-struct SkTraceOp {
-  static constexpr int ID = 4;
-};
-__global__ void __launch_bounds__(T_THREADS, 1) k_update_sk(const __grid_constant__ TmaMaps mp, const int *perm,
-                                                            const DegInfo *info, const int4 *tiles, const float *bU,
-                                                            float *X1, float *X1_lo) {
-  constexpr int H = SK_H, Q = H / SK_KS;  // Q: columns owned per CTA
-  constexpr int A_BYTES = T_BM * 128, B_BYTES = H * 128;
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t *smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + SK_ST * SK_STAGE);
-  uint64_t *empty = full + SK_ST;
-  uint64_t *accf = empty + SK_ST;
-  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(accf + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  using Op = SkTraceOp;
-  if (threadIdx.x == 0) TTRACE(0);
-  if (warp == T_MMA_WARP) tc::tmem_alloc<H>(tmem_holder);
-  if (threadIdx.x == T_TMA_WARP * 32) {
-    tc::tma_prefetch_desc(&mp.ah);
-    tc::tma_prefetch_desc(&mp.al);
-    tc::tma_prefetch_desc(&mp.bh);
-    tc::tma_prefetch_desc(&mp.bl);
-    for (int s = 0; s < SK_ST; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&empty[s], 1);
-    }
-    tc::mbar_init(accf, 1);
-    tc::fence_mbar_init();
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  tc::fence_after_sync();
-  const uint32_t tmem = *tmem_holder;
-  pdl_enter();
-  if (threadIdx.x == 0) TTRACE(1);
-  const int ti = blockIdx.x / SK_KS;
-  const bool valid = ti < info->T;  // uniform over the cluster
-  int4 tl = make_int4(0, 0, 0, 0);
-  if (valid) tl = tiles[ti];
-  const int kbase = (int)rank * H;  // this CTA's K range [kbase, kbase + H)
-  constexpr int NCH = H / T_BK;
-  if (valid) {
-    if (warp == T_TMA_WARP) {
-      if (lane == 0) {
-        for (int c = 0; c < NCH; ++c) {
-          const int s = c % SK_ST;
-          if (c >= SK_ST) tc::mbar_wait(&empty[s], ((c / SK_ST) - 1) & 1);
-          uint8_t *sa = smem + s * SK_STAGE;
-          tc::mbar_expect_tx(&full[s], SK_STAGE);
-          const int k = kbase + c * T_BK;
-          tc::tma_load_2d(sa, &mp.ah, k, tl.y, &full[s]);
-          tc::tma_load_2d(sa + A_BYTES, &mp.al, k, tl.y, &full[s]);
-          tc::tma_load_2d(sa + 2 * A_BYTES, &mp.bh, k, tl.x * H, &full[s]);
-          tc::tma_load_2d(sa + 2 * A_BYTES + B_BYTES, &mp.bl, k, tl.x * H, &full[s]);
-        }
-      }
-      __syncwarp();
-    } else if (warp == T_MMA_WARP) {
-      if (lane == 0) {
-        constexpr uint32_t idesc = tc::idesc_tf32(T_BM, H);
-        for (int c = 0; c < NCH; ++c) {
-          const int s = c % SK_ST;
-          tc::mbar_wait(&full[s], (c / SK_ST) & 1);
-          tc::fence_after_sync();
-          const uint32_t aH = tc::smem_u32(smem + s * SK_STAGE);
-          const uint32_t aL = aH + A_BYTES, bH = aL + A_BYTES, bL = bH + B_BYTES;
-#pragma unroll
-          for (int ks = 0; ks < T_BK / 8; ++ks) {
-            const uint32_t off = ks * 32;
-            const uint64_t dah = tc::desc_sw128(aH + off), dal = tc::desc_sw128(aL + off);
-            const uint64_t dbh = tc::desc_sw128(bH + off), dbl = tc::desc_sw128(bL + off);
-            tc::mma_tf32(tmem, dah, dbh, idesc, (c | ks) != 0);
-            tc::mma_tf32(tmem, dah, dbl, idesc, 1u);
-            tc::mma_tf32(tmem, dal, dbh, idesc, 1u);
-          }
-          tc::mma_commit(&empty[s]);
-        }
-        tc::mma_commit(accf);
-      }
-      __syncwarp();
-    }
-  }
-  // epilogue warps hold the full partial in registers across the exchange
-  float own[Q];
-  const int row = warp * 32 + lane;  // accumulator lane (epilogue warps)
-  if (valid && warp < 4) {
-    tc::mbar_wait(accf, 0);
-    tc::fence_after_sync();
-  }
-  if (threadIdx.x == 0) TTRACE(2);
-  // barrier 1: every CTA's MMAs are complete, so all stage rings are free to receive
-  tc::fence_before_sync();
-  cluster_sync_all();
-  if (valid && warp < 4) {
-    const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-    // receive layout in each owner: slot[src][row][Q] fp32 at the start of the ring
-    const uint32_t slot0 = tc::smem_u32(smem);
-#pragma unroll 1
-    for (int q = 0; q < SK_KS; ++q) {
-      float acc[32];
-      tc::tmem_ld32(trow + (uint32_t)(q * Q), acc);
-      if (q == (int)rank) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) own[i] = acc[i];
-      } else {
-        const uint32_t dst = map_peer(slot0 + (uint32_t)(((rank * T_BM) + row) * Q * 4), (uint32_t)q);
-#pragma unroll
-        for (int i = 0; i < Q; i += 4) st_cluster_v4(dst + i * 4, make_float4(acc[i], acc[i + 1], acc[i + 2], acc[i + 3]));
-      }
-    }
-  }
-  if (threadIdx.x == 0) TTRACE(3);
-  // barrier 2: all partial quarters have landed in their owners
-  cluster_sync_all();
-  if (threadIdx.x == 0) TTRACE(4);
-  if (valid && warp < 4) {
-    const float *slot = reinterpret_cast<const float *>(smem);
-    float sum[Q];
-#pragma unroll
-    for (int i = 0; i < Q; ++i) sum[i] = 0.f;
-    for (int src = 0; src < SK_KS; ++src) {  // fixed rank order
-      if (src == (int)rank) {
-#pragma unroll
-        for (int i = 0; i < Q; ++i) sum[i] += own[i];
-      } else {
-        const float *p = slot + ((size_t)src * T_BM + row) * Q;
-#pragma unroll
-        for (int i = 0; i < Q; i += 4) {
-          const float4 v = *reinterpret_cast<const float4 *>(p + i);
-          sum[i] += v.x; sum[i + 1] += v.y; sum[i + 2] += v.z; sum[i + 3] += v.w;
-        }
-      }
-    }
-    const int m = tl.y + row;
-    if (m < tl.y + tl.z) {
-      const int n0 = (int)rank * Q;
-      const size_t o = (size_t)perm[m] * H + n0;
-#pragma unroll
-      for (int i = 0; i < Q; i += 4) {
-        const float4 b = ldg4(bU + n0 + i);
-        const float4 z = make_float4(fmaxf(sum[i] + b.x, 0.f), fmaxf(sum[i + 1] + b.y, 0.f),
-                                     fmaxf(sum[i + 2] + b.z, 0.f), fmaxf(sum[i + 3] + b.w, 0.f));
-        *reinterpret_cast<float4 *>(X1 + o + i) = z;
-        *reinterpret_cast<float4 *>(X1_lo + o + i) = lo4(z);
-      }
-    }
-  }
-  if (threadIdx.x == 0) {
-    TTRACE(5);
-    if (g_trace && g_trace_id == 4) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-      g_trace[blockIdx.x * 8 + 7] = smid;
-      g_trace[blockIdx.x * 8 + 6] = valid;
-    }
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-  if (warp == T_MMA_WARP) {
-    tc::fence_after_sync();
-    tc::tmem_dealloc<H>(tmem);
   }
 }
 
@@ -858,26 +662,24 @@ __global__ void k_prep_Mx(const float *__restrict__ params, const int64_t *__res
   }
 }
 
-// weights of every degree slot d < cmax with their lo terms: Wf[d] = W_d [H][4H],
-// WbT[d] = W_d^T [4H][H] (depends only on the parameters and delta)
+// class weights of the batch's degree classes with their lo terms: Wf[c] = W_c [H][4H],
+// WbT[c] = W_c^T [4H][H], W_c = U_id + amp(d_c) U_amp + att(d_c) U_att (scalers from the
+// class table k_degsort wrote; slots c >= info->C are not touched)
 __global__ void k_prep_W2(const float *__restrict__ params, const int64_t *__restrict__ u_off, int l0, int l1, int H,
-                          int cmax, double delta, float *__restrict__ Wf, float *__restrict__ Wf_lo,
+                          int cmax, const DegInfo *__restrict__ info, float *__restrict__ Wf, float *__restrict__ Wf_lo,
                           float *__restrict__ WbT, float *__restrict__ WbT_lo) {
   pdl_enter();
   __shared__ float tile[32][33];
   const int K = 4 * H, tk = K / 32, th = H / 32;
   const int per_cls = tk * th;
+  const int C = info->C;
   for (int t = blockIdx.x; t < (l1 - l0) * cmax * per_cls; t += gridDim.x) {
     const int l = l0 + t / (cmax * per_cls);
-    const int c = (t / per_cls) % cmax;  // degree slot d = c (every slot, batch-independent)
+    const int c = (t / per_cls) % cmax;
+    if (c >= C) continue;  // uniform per block
     const int tt = t % per_cls, h0 = (tt / tk) * 32, k0 = (tt % tk) * 32;
     const float *U = params + u_off[l];
-    float a = 1.0f, b = 1.0f;  // amp(d), att(d) exactly as k_degsort computes them
-    if (c > 0) {
-      const double ld = log((double)c + 1.0);
-      a = (float)(ld / delta);
-      b = (float)(delta / ld);
-    }
+    const float a = info->amp[c], b = info->att[c];
     const size_t base = ((size_t)l * cmax + c) * H * K;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
       const float *u = U + (size_t)(h0 + r) * 3 * K + k0 + threadIdx.x;
@@ -951,7 +753,7 @@ cudaError_t tconfigure() {
 template <class Op>
 void trun(cudaStream_t st, const TmaMaps &mp, Op op, int items) {
   op.items_cap = items;
-  launch_ex(k_tma<Op>, std::max(1, std::min(items, kSMs)), T_THREADS, t_smem_bytes<Op>(), st, mp, op);
+  launch_ex(k_tma<Op>, std::max(1, std::min(items, kSMs)), T_THREADS, t_smem_bytes<Op>(), st, mp, op, g_gemm_passes);
   g_launches += 1;
 }
 int mt(int n) { return (n + T_BM - 1) / T_BM; }
@@ -965,38 +767,39 @@ cudaError_t tconfigure_bn() {
   return tconfigure<TDX<BN>>();
 }
 
+// (the activation operand's al map slot is unused: its lo terms are derived in shared memory)
 template <int BN>
-void update_bn(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
-               const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU, float *X1,
-               float *X1_lo, float *X1s, float *X1s_lo, uint32_t *X1mask) {
+void update_bn(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm, const DegInfo *info,
+               const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU, float *X1, float *X1s,
+               uint32_t *X1mask) {
   const int K = 4 * c.H;
-  const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, BN),
-                   map2d(Wf_lo, (uint64_t)cmax * c.H, K, BN)};
-  TUpdC<BN> op{perm, info, tiles, bU, X1, X1_lo, c.H, 0, X1s, X1s_lo, X1mask, 0};
+  const CUtensorMap a = map2d(A, c.maxN, K, T_BM);
+  const TmaMaps mp{a, a, map2d(Wf, (uint64_t)cmax * c.H, K, BN), map2d(Wf_lo, (uint64_t)cmax * c.H, K, BN)};
+  TUpdC<BN> op{perm, info, tiles, bU, X1, c.H, 0, X1s, X1mask, 0};
   trun(st, mp, op, tc_max_tiles(c, cmax) * (c.H / BN));
 }
 template <int BN>
-void dA_bn(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
-           const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
-  const TmaMaps mp{map2d(dZ, c.maxN, c.H, T_BM), map2d(dZ_lo, c.maxN, c.H, T_BM),
-                   map2d(WbT, (uint64_t)cmax * 4 * c.H, c.H, BN), map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, c.H, BN)};
+void dA_bn(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const int *perm, const DegInfo *info,
+           const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
+  const CUtensorMap a = map2d(dZ, c.maxN, c.H, T_BM);
+  const TmaMaps mp{a, a, map2d(WbT, (uint64_t)cmax * 4 * c.H, c.H, BN), map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, c.H, BN)};
   TDAC<BN> op{perm, info, tiles, dA, c.H, 0, 0};
   trun(st, mp, op, tc_max_tiles(c, cmax) * (4 * c.H / BN));
 }
 template <int BN>
-void proj_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
-             const float *Mx, const float *Mx_lo, float *P) {
-  const TmaMaps mp{map2d(X, c.maxN, F, T_BM), map2d(X_lo, c.maxN, F, T_BM), map2d(Mx, c.H, F, BN),
-                   map2d(Mx_lo, c.H, F, BN)};
+void proj_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
+             const float *Mx_lo, float *P) {
+  const CUtensorMap a = map2d(X, c.maxN, F, T_BM);
+  const TmaMaps mp{a, a, map2d(Mx, c.H, F, BN), map2d(Mx_lo, c.H, F, BN)};
   TProj<BN> op{blob, P, F, c.H, 0, 0};
   trun(st, mp, op, mt(c.maxN) * (c.H / BN));
 }
 template <int BN>
-void dX_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo, const float *MxT,
-           const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo, const int *pos) {
-  const TmaMaps mp{map2d(dP, c.maxN, c.H, T_BM), map2d(dP_lo, c.maxN, c.H, T_BM), map2d(MxT, F, c.H, BN),
-                   map2d(MxT_lo, F, c.H, BN)};
-  TDX<BN> op{blob, Xl, dZ, dZ_lo, pos, c.H, F, 0, 0};
+void dX_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *MxT, const float *MxT_lo,
+           int F, const float *Xl, float *dZ, const int *pos) {
+  const CUtensorMap a = map2d(dP, c.maxN, c.H, T_BM);
+  const TmaMaps mp{a, a, map2d(MxT, F, c.H, BN), map2d(MxT_lo, F, c.H, BN)};
+  TDX<BN> op{blob, Xl, dZ, pos, c.H, F, 0, 0};
   trun(st, mp, op, mt(c.maxN) * (F / BN));
 }
 }  // namespace
@@ -1011,16 +814,6 @@ cudaError_t tcd_configure() {
     if (q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  auto env_bn = [](const char *n, int &v) {
-    if (const char *s = getenv(n)) v = atoi(s) == 128 ? 128 : atoi(s) == 32 ? 32 : 64;
-  };
-  env_bn("HG_BN_UPD", g_bn_upd);
-  env_bn("HG_BN_DA", g_bn_da);
-  env_bn("HG_BN_PROJ", g_bn_proj);
-  env_bn("HG_BN_DX", g_bn_dx);
-  if (const char *v = getenv("HG_UPDATE_SK")) g_update_sk = atoi(v) != 0;
-  if ((e = cudaFuncSetAttribute(k_update_sk, cudaFuncAttributeMaxDynamicSharedMemorySize, SK_SMEM)) != cudaSuccess)
-    return e;
   if ((e = cudaFuncSetAttribute(k_dxda, cudaFuncAttributeMaxDynamicSharedMemorySize, XD_SMEM)) != cudaSuccess)
     return e;
   if ((e = tconfigure_bn<32>()) != cudaSuccess) return e;
@@ -1029,75 +822,45 @@ cudaError_t tcd_configure() {
   return tmn_configure();
 }
 
-void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const float *A_lo, const int *perm,
+void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm,
                          const DegInfo *info, const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU,
-                         float *X1, float *X1_lo, float *X1s, float *X1s_lo, uint32_t *X1mask) {
-  if (g_update_sk && c.H == SK_H && !X1s) {
-    const int K = 4 * c.H;
-    const TmaMaps mp{map2d(A, c.maxN, K, T_BM), map2d(A_lo, c.maxN, K, T_BM), map2d(Wf, (uint64_t)cmax * c.H, K, SK_H),
-                     map2d(Wf_lo, (uint64_t)cmax * c.H, K, SK_H)};
-    cudaLaunchAttribute attr[3];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = SK_KS;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[1].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
-    attr[2].id = cudaLaunchAttributePriority;
-    attr[2].val.priority = g_low_prio ? g_prio_lo : g_prio_hi;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(tc_max_tiles(c, cmax) * SK_KS);
-    cfg.blockDim = dim3(T_THREADS);
-    cfg.dynamicSmemBytes = SK_SMEM;
-    cfg.stream = st;
-    cfg.attrs = attr;
-    cfg.numAttrs = 3;
-    cudaLaunchKernelEx(&cfg, k_update_sk, mp, perm, info, tiles, bU, X1, X1_lo);
-    g_launches += 1;
-    return;
-  }
-  const int bn_upd = bn_auto(g_bn_upd, c);
-  if (bn_upd == 32)
-    update_bn<32>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
-  else if (bn_upd == 128)
-    update_bn<128>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
-  else update_bn<64>(st, c, cmax, A, A_lo, perm, info, tiles, Wf, Wf_lo, bU, X1, X1_lo, X1s, X1s_lo, X1mask);
+                         float *X1, float *X1s, uint32_t *X1mask) {
+  const int bn = bn_auto(c);
+  if (bn == 32) update_bn<32>(st, c, cmax, A, perm, info, tiles, Wf, Wf_lo, bU, X1, X1s, X1mask);
+  else if (bn == 128) update_bn<128>(st, c, cmax, A, perm, info, tiles, Wf, Wf_lo, bU, X1, X1s, X1mask);
+  else update_bn<64>(st, c, cmax, A, perm, info, tiles, Wf, Wf_lo, bU, X1, X1s, X1mask);
 }
 
-void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const int *perm,
-                     const DegInfo *info, const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
-  if (g_bn_da == 32) dA_bn<32>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
-  else if (g_bn_da == 128) dA_bn<128>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
-  else dA_bn<64>(st, c, cmax, dZ, dZ_lo, perm, info, tiles, WbT, WbT_lo, dA);
+void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const int *perm, const DegInfo *info,
+                     const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
+  dA_bn<128>(st, c, cmax, dZ, perm, info, tiles, WbT, WbT_lo, dA);
 }
 
-void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, const float *X_lo, int F,
-                   const float *Mx, const float *Mx_lo, float *P) {
-  const int bn = bn_auto(g_bn_proj, c);
-  if (bn == 32) proj_bn<32>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
-  else if (bn == 128) proj_bn<128>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
-  else proj_bn<64>(st, c, blob, X, X_lo, F, Mx, Mx_lo, P);
+void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
+                   const float *Mx_lo, float *P) {
+  const int bn = bn_auto(c);
+  if (bn == 32) proj_bn<32>(st, c, blob, X, F, Mx, Mx_lo, P);
+  else if (bn == 128) proj_bn<128>(st, c, blob, X, F, Mx, Mx_lo, P);
+  else proj_bn<64>(st, c, blob, X, F, Mx, Mx_lo, P);
 }
 
-void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
-                 const float *MxT, const float *MxT_lo, int F, const float *Xl, float *dZ, float *dZ_lo,
-                 const int *pos) {
-  const int bn = bn_auto(g_bn_dx, c);
-  if (bn == 32) dX_bn<32>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
-  else if (bn == 128) dX_bn<128>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
-  else dX_bn<64>(st, c, blob, dP, dP_lo, MxT, MxT_lo, F, Xl, dZ, dZ_lo, pos);
+void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *MxT,
+                 const float *MxT_lo, int F, const float *Xl, float *dZ, const int *pos) {
+  const int bn = bn_auto(c);
+  if (bn == 32) dX_bn<32>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos);
+  else if (bn == 128) dX_bn<128>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos);
+  else dX_bn<64>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos);
 }
 
 bool dxda_supported(const Caps &c) { return c.H == 128; }
 
-void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *dP_s_lo, const float *MxT,
-                 const float *MxT_lo, const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info,
-                 const int4 *tiles, const uint32_t *Xmask, float *dZ, float *dZ_lo, float *dA) {
-  const DxDaMaps mp{map2d(dP_s, c.maxN, c.H, 128), map2d(dP_s_lo, c.maxN, c.H, 128), map2d(MxT, 128, c.H, 128),
-                    map2d(MxT_lo, 128, c.H, 128), map2d(WbT, (uint64_t)cmax * 4 * c.H, 128, 128),
-                    map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, 128, 128)};
+void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *MxT, const float *MxT_lo,
+                 const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info, const int4 *tiles,
+                 const uint32_t *Xmask, float *dZ, float *dA) {
+  const DxDaMaps mp{map2d(dP_s, c.maxN, c.H, 128), map2d(MxT, 128, c.H, 128), map2d(MxT_lo, 128, c.H, 128),
+                    map2d(WbT, (uint64_t)cmax * 4 * c.H, 128, 128), map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, 128, 128)};
   const int grid = tc_max_tiles(c, cmax) * (4 * c.H / (128 * XD_NS));
-  launch_ex(k_dxda, grid, T_THREADS, XD_SMEM, st, mp, perm, info, tiles, Xmask, dZ, dZ_lo, dA, c.H);
+  launch_ex(k_dxda, grid, XD_THREADS, XD_SMEM, st, mp, perm, info, tiles, Xmask, dZ, dA, c.H, g_gemm_passes);
   g_launches += 1;
 }
 
@@ -1110,21 +873,12 @@ void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const i
 }
 
 void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int l0, int l1,
-                    int cmax, double delta, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo) {
-  static const int cap = [] {  // A/B switch: grid of the (side-stream) weight preparation
-    const char *e = getenv("HG_PREP_BLOCKS");
-    return e ? atoi(e) : kSMs * 2;
-  }();
-  const int blocks = std::max(1, std::min((l1 - l0) * cmax * (4 * c.H / 32) * (c.H / 32), cap));
-  launch_ex(k_prep_W2, blocks, dim3(32, 8), 0, st, params, u_off_dev, l0, l1, c.H, cmax, delta, Wf, Wf_lo, WbT,
+                    int cmax, const DegInfo *info, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo) {
+  // (side-stream kernel: a grid of two waves leaves room for the main chain's first kernels)
+  const int blocks = std::max(1, std::min((l1 - l0) * cmax * (4 * c.H / 32) * (c.H / 32), kSMs * 2));
+  launch_ex(k_prep_W2, blocks, dim3(32, 8), 0, st, params, u_off_dev, l0, l1, c.H, cmax, info, Wf, Wf_lo, WbT,
             WbT_lo);
   g_launches += 1;
 }
 
 }  // namespace hg
-
-extern "C" int hg_debug_set_trace(void *buf, int op_id) {  // experiments only (not part of the ABI header)
-  cudaError_t e = cudaMemcpyToSymbol(hg::g_trace, &buf, sizeof(void *));
-  if (e == cudaSuccess) e = cudaMemcpyToSymbol(hg::g_trace_id, &op_id, sizeof(int));
-  return (int)e;
-}

@@ -7,16 +7,18 @@
 // so there is no transpose or transform stage. Column sums (db_U, db_M) come from
 // an extra N=32 tile whose B operand is a ones matrix: D = sum_k a[k][m] * 1.
 // K (node) ranges end inside a 32-row chunk: the MMA skips whole 8-row k-steps
-// past the end and the MMA warp zeroes the (<= 7) trailing rows of the last one.
+// past the end and the transform warps zero the A operand's trailing rows of the last one.
 //   warps 0-3 epilogue (TMEM -> staging -> coalesced partial stores)
-//   warp 4    TMA producer      warp 5  TMEM alloc, tail fix-up, MMA issue
+//   warp 4    TMA producer (the operands' fp32 tiles)   warp 5  TMEM alloc, MMA issue
+//   warps 6-9 per landed stage: zero the A tile's rows past the split, then (3xTF32) the lo
+//             terms x - trunc19(x) of the A and B tiles into the stage's lo slots -- the
+//             activations are stored once, as fp32, in HBM
 // Persistent over (split, m-tile, n-tile) items; double-buffered accumulators.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
 #include <algorithm>
-#include <cstdlib>
 #include <atomic>
 
 #include "common.cuh"
@@ -34,7 +36,7 @@ namespace {
 constexpr int N_BM = 128;          // output rows (features of the A operand) per tile
 constexpr int N_BK = 32;           // nodes per chunk
 constexpr int N_BOX = N_BK * 128;  // one MN block: 32 k-rows x 128 bytes
-constexpr int N_TMA_WARP = 4, N_MMA_WARP = 5, N_THREADS = 192;
+constexpr int N_TMA_WARP = 4, N_MMA_WARP = 5, N_XF_WARP = 6, N_THREADS = 320;
 constexpr int N_STG_LD = 36;
 constexpr int N_STG_BYTES = 4 * 32 * N_STG_LD * 4;
 
@@ -46,7 +48,7 @@ constexpr int n_stages() {
 }
 template <class Op>
 constexpr int n_smem_bytes() {
-  return n_stages<Op>() * n_stage_bytes<Op>() + N_STG_BYTES + 1024 + 8 * (3 * n_stages<Op>() + 4) + 16;
+  return n_stages<Op>() * n_stage_bytes<Op>() + N_STG_BYTES + 1024 + 8 * (4 * n_stages<Op>() + 4) + 16;
 }
 
 struct MnItem {
@@ -57,9 +59,12 @@ struct MnItem {
 
 // maps: ah/al = A operand (rows = nodes, cols = M features), bh/bl = B operand
 // (cols = N features); ones map rides in a second parameter.
+extern int g_gemm_passes;  // tcdirect.cu: 3 = 3xTF32, 1 = plain TF32
+
 template <class Op>
 __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ TmaMaps mp,
-                                                      const __grid_constant__ CUtensorMap ones, Op op_in) {
+                                                      const __grid_constant__ CUtensorMap ones, Op op_in,
+                                                      int passes) {
   constexpr int BN = Op::BN, ST = n_stages<Op>(), NB = BN / 32;
   constexpr int A_BYTES = 4 * N_BOX, B_BYTES = NB * N_BOX, STAGE = n_stage_bytes<Op>();
   // two buffers of the main accumulator at [0, 2BN), two of the correction accumulator
@@ -72,21 +77,22 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
   float *stg_all = reinterpret_cast<float *>(smem + ST * STAGE);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + ST * STAGE + N_STG_BYTES);
   uint64_t *empty = full + ST;
-  uint64_t *accf = empty + ST;
+  uint64_t *xfull = empty + ST;  // [ST] transform -> MMA
+  uint64_t *accf = xfull + ST;
   uint64_t *acce = accf + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(acce + 2);
+  const bool p3 = passes == 3;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == N_MMA_WARP) tc::tmem_alloc<TCOLS>(tmem_holder);
   if (threadIdx.x == N_TMA_WARP * 32) {
     tc::tma_prefetch_desc(&mp.ah);
-    tc::tma_prefetch_desc(&mp.al);
     tc::tma_prefetch_desc(&mp.bh);
-    tc::tma_prefetch_desc(&mp.bl);
     tc::tma_prefetch_desc(&ones);
     for (int s = 0; s < ST; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
+      tc::mbar_init(&xfull[s], 4);
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&accf[b], 1);
@@ -115,31 +121,51 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
           if (it >= ST) tc::mbar_wait(&empty[s], ((it / ST) - 1) & 1);
           uint8_t *sa = smem + s * STAGE;
           const int k = w.k0 + c * N_BK;
-          tc::mbar_expect_tx(&full[s], 2 * A_BYTES + (w.cs ? N_BOX : 2 * B_BYTES));
+          tc::mbar_expect_tx(&full[s], A_BYTES + (w.cs ? N_BOX : B_BYTES));
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
-            tc::tma_load_2d(sa + b * N_BOX, &mp.ah, w.m0 + 32 * b, k, &full[s]);
-            tc::tma_load_2d(sa + A_BYTES + b * N_BOX, &mp.al, w.m0 + 32 * b, k, &full[s]);
-          }
+          for (int b = 0; b < 4; ++b) tc::tma_load_2d(sa + b * N_BOX, &mp.ah, w.m0 + 32 * b, k, &full[s]);
           uint8_t *sb = sa + 2 * A_BYTES;
           if (w.cs) {
             tc::tma_load_2d(sb, &ones, 0, k, &full[s]);
           } else {
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-              tc::tma_load_2d(sb + b * N_BOX, &mp.bh, w.n0 + 32 * b, k, &full[s]);
-              tc::tma_load_2d(sb + B_BYTES + b * N_BOX, &mp.bl, w.n0 + 32 * b, k, &full[s]);
-            }
+            for (int b = 0; b < NB; ++b) tc::tma_load_2d(sb + b * N_BOX, &mp.bh, w.n0 + 32 * b, k, &full[s]);
           }
         }
       }
     }
     __syncwarp();
+  } else if (warp >= N_XF_WARP) {
+    // ---------------- per landed stage: A rows past the split -> 0 (a partial last chunk:
+    // rows past ceil8(rem) are skipped as whole k-steps, rows in [rem, ceil8(rem)) must be
+    // zero), then the lo terms; generic writes made visible to the tensor core
+    const int t = threadIdx.x - N_XF_WARP * 32;
+    int it = 0;
+    for (int tt = blockIdx.x; tt < items; tt += gridDim.x) {
+      MnItem w;
+      if (!op.item(tt, w)) continue;
+      const int nch = (w.len + N_BK - 1) / N_BK;
+      for (int c = 0; c < nch; ++c, ++it) {
+        const int s = it % ST;
+        const int rem = w.len - c * N_BK;
+        tc::mbar_wait(&full[s], (it / ST) & 1);
+        uint8_t *sa = smem + s * STAGE;
+        if (rem < N_BK) {  // 16-byte chunk i of box i / 256 lies in k-row (i % 256) / 8 (each thread
+                           // zeroes exactly the chunks it then splits: no barrier needed)
+          for (int i = t; i < 4 * N_BOX / 16; i += 128)
+            if (((i & 255) >> 3) >= rem) *reinterpret_cast<float4 *>(sa + 16 * i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        if (p3) {
+          tc::lo_chunks(sa, sa + A_BYTES, A_BYTES / 16, t, 128);
+          if (!w.cs) tc::lo_chunks(sa + 2 * A_BYTES, sa + 2 * A_BYTES + B_BYTES, B_BYTES / 16, t, 128);
+        }
+        tc::fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&xfull[s]);
+      }
+    }
   } else if (warp == N_MMA_WARP) {
-    // ---------------- MMA issuer (warp-wide loop; lane 0 issues). A partial last chunk
-    // is fixed in place first: the warp zeroes its k-rows [rem, ceil8(rem)) in every
-    // box loaded (rows past ceil8(rem) are skipped as whole k-steps) and makes the
-    // generic-proxy writes visible to the tensor core with fence.proxy.async.
+    // ---------------- MMA issuer (lane 0)
     constexpr uint32_t idesc = tc::idesc_tf32(N_BM, BN, true, true);
     constexpr uint32_t idesc_cs = tc::idesc_tf32(N_BM, 32, true, true);
     int it = 0, tcount = 0;
@@ -156,16 +182,8 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
         const int rem = w.len - c * N_BK;
         const int nks = rem >= N_BK ? N_BK / 8 : (rem + 7) / 8;
         tc::mbar_wait(&full[s], (it / ST) & 1);
+        tc::mbar_wait(&xfull[s], (it / ST) & 1);
         uint8_t *sa = smem + s * STAGE;
-        if (rem < N_BK && (rem & 7)) {
-          const int nrow = ((rem + 7) & ~7) - rem;
-          const int nbox = 8 + (w.cs ? 1 : 2 * NB);  // A hi/lo + B boxes actually loaded
-          for (int e = lane; e < nbox * nrow * 8; e += 32) {
-            const int bx = e / (nrow * 8), r = rem + (e / 8) % nrow, ch = e % 8;
-            *reinterpret_cast<float4 *>(sa + bx * N_BOX + r * 128 + ch * 16) = make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-          tc::fence_proxy_async_smem();
-        }
         __syncwarp();
         tc::fence_after_sync();
         if (lane == 0) {
@@ -178,12 +196,13 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
             const uint32_t acc = (c | ks) != 0;
             if (w.cs) {
               tc::mma_tf32(d, dah, dbh, idesc_cs, acc);
-              tc::mma_tf32(d, dal, dbh, idesc_cs, 1u);
+              if (p3) tc::mma_tf32(d, dal, dbh, idesc_cs, 1u);
             } else {
-              const uint64_t dbl = tc::desc_mn32(bL + off, N_BOX, 512);
               tc::mma_tf32(d, dah, dbh, idesc, acc);
-              tc::mma_tf32(dc, dah, dbl, idesc, acc);
-              tc::mma_tf32(dc, dal, dbh, idesc, 1u);
+              if (p3) {
+                tc::mma_tf32(dc, dah, tc::desc_mn32(bL + off, N_BOX, 512), idesc, acc);
+                tc::mma_tf32(dc, dal, dbh, idesc, 1u);
+              }
             }
           }
           tc::mma_commit(&empty[s]);
@@ -215,7 +234,12 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
         for (int q = 0; q < BN / 32; ++q) {
           float acc[32], cor[32];
           tc::tmem_ld32(trow + (uint32_t)(q * 32), acc);
-          tc::tmem_ld32(trow + (uint32_t)(2 * BN + q * 32), cor);
+          if (p3) {
+            tc::tmem_ld32(trow + (uint32_t)(2 * BN + q * 32), cor);
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cor[i] = 0.f;
+          }
 #pragma unroll
           for (int i = 0; i < 32; ++i) acc[i] = empty_item ? 0.f : acc[i] + cor[i];
 #pragma unroll
@@ -299,9 +323,9 @@ struct MnDMx {
 };
 
 // layer-0 input as a TMA-readable operand: Xp[i][0..Fp) = x_i padded with zeros to a
-// 16-byte row pitch, and its tf32 residual
+// 16-byte row pitch
 __global__ void __launch_bounds__(256) k_pad_x0(const uint8_t *__restrict__ blob, int Fp, float *__restrict__ Xp,
-                                                float *__restrict__ Xp_lo, const int *__restrict__ pos) {
+                                                const int *__restrict__ pos) {
   pdl_enter();
   const BatchView b = load_batch(blob);
   const int F = b.F0;
@@ -310,7 +334,6 @@ __global__ void __launch_bounds__(256) k_pad_x0(const uint8_t *__restrict__ blob
     const float v = f < F ? b.x[(size_t)i * F + f] : 0.f;
     const size_t o = pos ? (size_t)pos[i] * Fp + f : (size_t)e;  // degree-sorted rows when pos is given
     Xp[o] = v;
-    Xp_lo[o] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
   }
 }
 
@@ -406,30 +429,22 @@ __global__ void __launch_bounds__(256) k_reduce_gram(const float *__restrict__ p
   }
 }
 
-// reductions (tcgemm.cu / kernels.cu)
-__global__ void k_reduce_parts(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
-__global__ void k_reduce_rows(const float *__restrict__ part, int nparts, int count, float *__restrict__ out);
-
 namespace {
 // CTAs of the side-stream Grams (persistent): fewer than the SM count leaves room for
-// the critical chain's kernels that run concurrently (HG_MN_GRID to override)
+// the critical chain's kernels that run concurrently
 // Small steps (config B: ~150 Gram items) run the Grams beside the latency-bound main chain,
 // where fewer CTAs interfere less (148 -> 40 measured +2%); large ones (config D/E: thousands
-// of items) need every SM. Cap = clamp(items / 4, 40, 148) unless HG_MN_GRID overrides.
+// of items) need every SM. Cap = clamp(items / 4, 40, 148) unless the step builder overrides
+// it (g_mn_grid_override: the Grams that end the step use every SM).
 int mn_grid_cap(int items) {
   if (g_mn_grid_override > 0) return g_mn_grid_override;
-  static const int v = [] {
-    const char *e = getenv("HG_MN_GRID");
-    return e ? std::max(1, atoi(e)) : 0;
-  }();
-  if (v > 0) return v;
   return std::max(40, std::min(kSMs, items / 4));
 }
 template <class Op>
 void nrun(cudaStream_t st, const TmaMaps &mp, const CUtensorMap &ones, Op op, int items) {
   op.items_cap = items;
   launch_ex(k_tmn<Op>, std::max(1, std::min(items, mn_grid_cap(items))), N_THREADS, n_smem_bytes<Op>(), st, mp, ones,
-            op);
+            op, g_gemm_passes);
   g_launches += 1;
 }
 }  // namespace
@@ -447,14 +462,13 @@ size_t mn_gram_partial_floats(const Caps &c, int cmax) {
 }
 size_t mn_dmx_partial_floats(const Caps &c, int F) { return (size_t)kMnDMxSplits * c.H * (F + 1); }
 
-void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *dZ_lo, const float *A,
-                      const float *A_lo, const float *ones, const DegInfo *info, const int4 *splits, float *partial,
-                      float *dU, float *dbU) {
+void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *A, const float *ones,
+                      const DegInfo *info, const int4 *splits, float *partial, float *dU, float *dbU) {
   const int smax = tc_max_splits(c, cmax);
   const int total = c.H * 4 * c.H;
   float *cs = partial + (size_t)smax * total;
-  const TmaMaps mp{tma_map2d(dZ, c.maxN, c.H, N_BK, true), tma_map2d(dZ_lo, c.maxN, c.H, N_BK, true),
-                   tma_map2d(A, c.maxN, 4 * c.H, N_BK, true), tma_map2d(A_lo, c.maxN, 4 * c.H, N_BK, true)};
+  const CUtensorMap a = tma_map2d(dZ, c.maxN, c.H, N_BK, true), b = tma_map2d(A, c.maxN, 4 * c.H, N_BK, true);
+  const TmaMaps mp{a, a, b, b};  // (lo slots unused: derived in shared memory)
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
   MnGram op{info, splits, partial, cs, c.H, 0};
   nrun(st, mp, om, op, smax * (c.H / N_BM) * (4 * c.H / MnGram::BN + 1));
@@ -462,13 +476,12 @@ void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ,
   g_launches += 1;
 }
 
-void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *dP_lo,
-                   const float *X, const float *X_lo, int F, int Fp, const float *ones, float *partial, float *dMx,
-                   float *dbM) {
+void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F, int Fp,
+                   const float *ones, float *partial, float *dMx, float *dbM) {
   const int count = c.H * F;
   float *cs = partial + (size_t)kMnDMxSplits * count;
-  const TmaMaps mp{tma_map2d(dP, c.maxN, c.H, N_BK, true), tma_map2d(dP_lo, c.maxN, c.H, N_BK, true),
-                   tma_map2d(X, c.maxN, Fp, N_BK, true), tma_map2d(X_lo, c.maxN, Fp, N_BK, true)};
+  const CUtensorMap a = tma_map2d(dP, c.maxN, c.H, N_BK, true), b = tma_map2d(X, c.maxN, Fp, N_BK, true);
+  const TmaMaps mp{a, a, b, b};  // (lo slots unused: derived in shared memory)
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
   const int with_cs = dbM ? 1 : 0;
   MnDMx op{blob, partial, cs, c.H, F, 0, with_cs};
@@ -480,10 +493,9 @@ void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
 }
 
 int pad_x0_width(int F0) { return (F0 + 3) / 4 * 4; }  // 16-byte row pitch; TMA zero-fills the rest
-void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, float *Xp_lo, const int *pos) {
+void launch_pad_x0(cudaStream_t st, const Caps &c, const uint8_t *blob, float *Xp, const int *pos) {
   const int Fp = pad_x0_width(c.F0);
-  launch_ex(k_pad_x0, std::max(1, std::min(cdiv(c.maxN * Fp, 256), kSMs * 2)), 256, 0, st, blob, Fp, Xp, Xp_lo,
-            pos);
+  launch_ex(k_pad_x0, std::max(1, std::min(cdiv(c.maxN * Fp, 256), kSMs * 2)), 256, 0, st, blob, Fp, Xp, pos);
   g_launches += 1;
 }
 

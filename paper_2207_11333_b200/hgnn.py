@@ -127,6 +127,10 @@ SIGNATURES = {
     "hg_eval_pairs": [_P, ctypes.c_int32, _P, _P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32)],
     "hg_loss_fetch": [_P, ctypes.c_int32, ctypes.POINTER(ctypes.c_float)],
     "hg_sync": [_P],
+    "hg_set_timeout": [_P, _D],
+    "hg_p2p_emulate": [ctypes.POINTER(_P), _I32, ctypes.POINTER(hg_adamw)],
+    "hg_bucket_layout": [ctypes.POINTER(hg_config), _I64P, _I32, _I32P],
+    "hg_pack_threads_set": [_I32],
     "hg_launch_count": [_P, _I64P],
 }
 
@@ -169,8 +173,8 @@ def _ptr(a: np.ndarray):
 DEFAULT_ADAMW = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
 
 
-HG_FLAG_SIMT_GEMM = 1
 HG_LOSS_RING = 4  # include/hgnn.h
+HG_FLAG_TF32 = 1  # reduced-precision (single-pass TF32) GEMM mode
 
 
 def make_config(f_node, f_edge, hidden, layers, max_graphs, max_nodes, max_edges, delta, fc_hidden=None,
@@ -464,10 +468,23 @@ class Context:
     def backward(self, slot: int = 0):
         _check(_lib.hg_backward(self.handle, slot))
 
-    def comm_init(self, rank: int, world: int, group=None):
-        """Create the NCCL communicator; the 128-byte id travels over torch.distributed."""
+    def comm_init(self, rank: int, world: int, group=None, force_comm: bool = False):
+        """Create the NCCL communicator; the 128-byte id travels over torch.distributed.
+        world == 1: no communicator (the exchange is a no-op) unless force_comm, which creates
+        a one-rank communicator (the bucketed NCCL path then runs as in a W-rank job)."""
+        if world == 1:
+            buf = None
+            if force_comm:
+                buf = np.zeros(128, np.uint8)
+                _check(_lib.hg_nccl_unique_id(_ptr(buf)))
+            _check(_lib.hg_comm_init(self.handle, _ptr(buf) if buf is not None else None, rank, world))
+            return
         buf = nccl_unique_id_broadcast(rank, world, group, device=self.device)
         _check(_lib.hg_comm_init(self.handle, _ptr(buf), rank, world))
+
+    def set_timeout(self, seconds: float):
+        """Fail-stop bound of the exchange's device waits and of sync() (hg_set_timeout)."""
+        _check(_lib.hg_set_timeout(self.handle, float(seconds)))
 
     def p2p_init(self, rank: int, world: int, group=None):
         """Map every rank's workspace (CUDA IPC) for the fused peer-memory gradient
@@ -501,6 +518,10 @@ class Context:
         if not all_ok(err is None):
             _lib.hg_p2p_open(self.handle, None)  # back to NCCL everywhere
             raise err or HgError(8, "peer-memory exchange unavailable on another rank")  # HG_E_CUDA
+
+    def p2p_close(self):
+        """Back to the NCCL exchange (hg_p2p_open(x, NULL)); gathers the sharded moments."""
+        _check(_lib.hg_p2p_open(self.handle, None))
 
     def allreduce_grads(self):
         _check(_lib.hg_allreduce_grads(self.handle))
@@ -585,6 +606,29 @@ def nccl_unique_id_broadcast(rank: int, world: int, group=None, device: int = 0)
     t = torch.from_numpy(buf).to(dev)
     dist.broadcast(t, src=0, group=group)
     return t.cpu().numpy().copy()
+
+
+def p2p_emulate(ctxs, **hyper):
+    """hg_p2p_emulate: the peer-memory exchange of len(ctxs) ranks emulated on one device."""
+    load()
+    h = make_adamw(**hyper)
+    arr = (_P * len(ctxs))(*[c.handle.value for c in ctxs])
+    _check(_lib.hg_p2p_emulate(arr, len(ctxs), ctypes.byref(h)))
+
+
+def bucket_layout(cfg: hg_config) -> list:
+    """[(begin, end)] float ranges of the gradient buckets in launch order (hg_bucket_layout)."""
+    load()
+    n = _I32()
+    _check(_lib.hg_bucket_layout(ctypes.byref(cfg), None, 0, ctypes.byref(n)))
+    r = np.zeros(2 * n.value, np.int64)
+    _check(_lib.hg_bucket_layout(ctypes.byref(cfg), r.ctypes.data_as(_I64P), n.value, ctypes.byref(n)))
+    return [(int(r[2 * i]), int(r[2 * i + 1])) for i in range(n.value)]
+
+
+def pack_threads_set(threads: int):
+    load()
+    _check(_lib.hg_pack_threads_set(int(threads)))
 
 
 # C-named module-level entry points (same names as include/hgnn.h)

@@ -5,9 +5,17 @@ float64 oracle on the same seeded inputs and parameters, and returns the
 comparison metrics of SURVEY §8(c) C19:
   forward (yhat, loss, per-layer X): max |diff| / max |ref|    (bar 1e-4)
   gradients: per tensor max-scaled and normwise                (bar 1e-3)
-  one-step params: per tensor normwise                         (bar 1e-3)
-  decision replay (C8): oracle decisions inside the ambiguity band are
+  one-step Adam moments m1, v1: per tensor normwise            (bar 1e-3)
+  one-step params: per tensor normwise over the components whose oracle
+  gradient is >= 100 eps (bar 1e-3); the others -- where Adam's first step
+  lr*g/(|g|+eps) is ill-conditioned -- are counted and checked against the
+  step bound |theta1 - theta0 (1 - lr wd)| <= lr (reading R-adam-eps)
+  decision replay (C8): oracle decisions inside the ambiguity band (argmin /
+  argmax 1e-6, ReLU the GPU's measured forward error of that layer) are
   replaced by the GPU's; the override count is reported.
+Every oracle input is the oracle's own (or the GPU's parameters / moments it
+re-syncs to before the step, SURVEY §8(d) "Per-step re-sync"); no GPU output
+enters the oracle's arithmetic.
 """
 import numpy as np
 
@@ -93,7 +101,14 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
     res["X"] = max(xs)
     Hfp = ctx.internal_cfg.fc_hidden
     hpre = ctx.view_f32(hgnn.VIEW_HPRE)[:B * Hfp].cpu().numpy().reshape(B, Hfp)[:, :cfg.fc_hidden]
-    dec, counts = O.replay(cache, gpu_decisions(ctx, N, H, L), head_relu_gpu=hpre > 0)
+    # ReLU replay band per layer: the GPU's measured forward error of that layer (x2), at least
+    # C8's 1e-6 -- a unit whose |Z| exceeds the demonstrated error cannot legitimately flip
+    tau_relu = [max(1e-6, 2.0 * e) for e in xs]
+    hp_ref = cache["head"]["hpre"]
+    tau_head = max(1e-6, 2.0 * float(np.abs(hpre - hp_ref).max() / max(np.abs(hp_ref).max(), 1e-30)))
+    res["tau_relu"] = max(tau_relu)
+    dec, counts = O.replay(cache, gpu_decisions(ctx, N, H, L), tau_arg=1e-6, tau_relu=tau_relu, tau_head=tau_head,
+                           head_relu_gpu=hpre > 0)
     res["overrides"] = counts["overrides"]
     res["overrides_by"] = counts["overrides_by"]
     res["tie_overrides"] = counts["tie_overrides"]
@@ -109,32 +124,38 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
         if not graph:
             ctx.step(**hyper)
             torch.cuda.synchronize()
-        # DESIGN.md reading R-adam-eps: Adam's first step lr*g/(|g|+eps) is ill-conditioned for
-        # |g| near eps (d step/d g = lr/eps at g = 0), so for components whose oracle gradient is
-        # below 100*eps -- cancellation residues, where fp32 rounding of O(1) terms is ~1e-8 -- the
-        # oracle's optimizer takes the GPU's gradient (itself checked by the gradient bar above)
-        ggs = gg if gg is not None else hgnn.arena_to_dict(ctx.grads_get(), layout)
-        floor = 100.0 * hyper["eps"]
-        g_opt, nrep = {}, 0
-        for k in g:
-            small = np.abs(g[k]) < floor
-            gk = np.asarray(ggs[k], np.float64).reshape(g[k].shape)
-            nrep += int((small & (gk != g[k])).sum())
-            g_opt[k] = np.where(small, gk, g[k])
-        res["adam_replayed"] = nrep
-        newp, _ = O.adamw_step(params, g_opt, st, **{k: hyper[k] for k in ("lr", "beta1", "beta2", "eps", "weight_decay")})
+        newp, newst = O.adamw_step(params, g, st, **{k: hyper[k] for k in ("lr", "beta1", "beta2", "eps",
+                                                                            "weight_decay")})
         gp = hgnn.arena_to_dict(ctx.params_get(), layout)
-        # the stated bar: one-step parameters, per tensor normwise
-        res["param_normwise"] = {k: normwise(gp[k], newp[k]) for k in g}
-        # stricter diagnostic: the update theta1 - theta0 itself (Adam step 1 ~ lr*sign(g), so
-        # sign-ambiguous tiny gradients move by 2 lr; reported, not asserted)
-        res["update_normwise"] = {k: normwise(np.asarray(gp[k], np.float64) - params[k], newp[k] - params[k])
-                                  for k in g}
+        m1, v1, step1 = ctx.opt_state_get()
+        gm, gv = hgnn.arena_to_dict(m1, layout), hgnn.arena_to_dict(v1, layout)
+        res["step"] = (step1, newst["step"])
+        # the moments are well-conditioned functions of the gradient
+        res["m_normwise"] = {k: normwise(gm[k], newst["m"][k]) for k in g}
+        res["v_normwise"] = {k: normwise(gv[k], newst["v"][k]) for k in g}
+        # DESIGN.md reading R-adam-eps: theta1 = theta0 (1 - lr wd) - lr m^/(sqrt(v^) + eps) has
+        # sensitivity lr/eps = 1e5 to g at g = 0, so theta1 is compared only where the oracle
+        # gradient is >= 100 eps; elsewhere the GPU's step must respect |m^/(sqrt(v^)+eps)| <= 1
+        floor = 100.0 * hyper["eps"]
+        pn, n_ill, bound_bad = {}, 0, 0
+        decay = 1.0 - hyper["lr"] * hyper["weight_decay"]
+        for k in g:
+            ok = np.abs(g[k]) >= floor
+            a_ = np.asarray(gp[k], np.float64).reshape(g[k].shape)
+            n_ill += int((~ok).sum())
+            if ok.any():
+                pn[k] = normwise(a_[ok], newp[k][ok])
+            step_ = np.abs(a_[~ok] - params[k][~ok] * decay)
+            bound_bad += int((step_ > hyper["lr"] * (1 + 1e-3) + 1e-7).sum())
+        res["param_normwise"] = pn
+        res["adam_ill_conditioned"] = n_ill
+        res["adam_step_bound_violations"] = bound_bad
     res["oracle_loss"] = loss
     return res
 
 
 def make_ctx(data, B, H, L, seed=2, n_slots=2, Hf=None, flags=0, max_degree=None):
+    """A ctx sized for the B largest graphs of `data`, parameters from the C12 init."""
     delta = O.degree_stat(data)
     maxn, maxe = capacity_for(data, B)
     store = hgnn.Store(data)
@@ -163,7 +184,7 @@ def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
     # oracle's own summation order picks the position) are not bounded.
     if res["out_of_band"] > max(2, 1e-5 * res["cells"]):
         bad.append(("out_of_band", res["out_of_band"], res["out_of_band_by"]))
-    if res["overrides"] > 1e-3 * res["cells"]:
+    if res["overrides"] > 1e-4 * res["cells"]:  # overrides < 1e-4 of the cells
         bad.append(("overrides", res["overrides"], res["cells"]))
     if "grad_maxscaled" in res:
         for k, v in res["grad_maxscaled"].items():
@@ -173,9 +194,14 @@ def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
             if v > grad_tol:
                 bad.append(("grad_normwise", k, v))
     if "param_normwise" in res:
-        for k, v in res["param_normwise"].items():
-            if v > param_tol:
-                bad.append(("param_normwise", k, v))
+        for key in ("param_normwise", "m_normwise", "v_normwise"):
+            for k, v in res[key].items():
+                if v > param_tol:
+                    bad.append((key, k, v))
+        if res["adam_step_bound_violations"]:
+            bad.append(("adam_step_bound_violations", res["adam_step_bound_violations"]))
+        if res["step"][0] != res["step"][1]:
+            bad.append(("adam step counter", res["step"]))
     assert not bad, bad
 
 

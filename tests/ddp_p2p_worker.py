@@ -56,9 +56,20 @@ def main(out):
             if k == 0:
                 params[mode + "_1"] = ctx.params_get()
         params[mode] = ctx.params_get()
+        if mode == "p2p":
+            # back to the NCCL exchange mid-run: the sharded moments are gathered,
+            # then every rank must keep bitwise-identical parameters and moments
+            ctx.p2p_close()
+            for k in range(2):
+                bg = order[(K + k) * Bg:(K + k + 1) * Bg]
+                ctx.pack(store, bg[rank * Bl:(rank + 1) * Bl], k % 2)
+                ctx.train_step(k % 2, graph=True)
+                ctx.sync()
+            m, v, _ = ctx.opt_state_get()
+            params["switched"] = np.concatenate([ctx.params_get(), m, v])
         del ctx
     res = {"rank": rank}
-    for mode in ("nccl", "p2p"):
+    for mode in ("nccl", "p2p", "switched"):
         t = torch.from_numpy(params[mode]).cuda()
         allp = [torch.zeros_like(t) for _ in range(world)]
         dist.all_gather(allp, t)

@@ -138,16 +138,17 @@ def test_store_stats_and_degree_stat(pcqm):
     assert abs(store.degree_stat(ids) - O.degree_stat(pcqm, ids)) <= 1e-13
 
 
-@pytest.mark.parametrize("H,Hf,flags,Hp,Hfp", [
-    (55, 55, 0, 128, 128),     # paper width -> tensor-core tile
-    (200, 200, 0, 256, 256),   # paper width
-    (55, 55, 1, 64, 64),       # SIMT path pads to the warp width
-    (55, 40, 0, 128, 40),      # fc_hidden != hidden is left as given
-    (128, 128, 0, 128, 128),   # multiples of 32 are not padded
-    (96, 96, 0, 96, 96),
+@pytest.mark.parametrize("H,Hf,Hp,Hfp", [
+    (55, 55, 128, 128),     # paper width -> tensor-core tile
+    (200, 200, 256, 256),   # paper width
+    (32, 32, 128, 128),     # config A's width
+    (55, 40, 128, 40),      # fc_hidden != hidden is left as given
+    (128, 128, 128, 128),   # multiples of 128 are not padded
+    (96, 96, 128, 128),
+    (512, 512, 512, 512),
 ])
-def test_config_internal_padding(H, Hf, flags, Hp, Hfp):
-    cfg = hgnn.make_config(34, 4, H, 2, 4, 100, 400, 1.0, fc_hidden=Hf, flags=flags)
+def test_config_internal_padding(H, Hf, Hp, Hfp):
+    cfg = hgnn.make_config(34, 4, H, 2, 4, 100, 400, 1.0, fc_hidden=Hf)
     ic = hgnn.hg_config_internal(cfg)
     assert (ic.hidden, ic.fc_hidden) == (Hp, Hfp)
     assert (ic.layers, ic.max_nodes, ic.flags) == (cfg.layers, cfg.max_nodes, cfg.flags)
@@ -191,3 +192,61 @@ def test_batch_offsets_alignment():
     for k in ("graph_ptr", "y", "rowptr", "col", "x", "eattr", "slot"):
         assert o[k] % 16 == 0
     assert o["total"] >= o["slot"] + 33
+
+
+def test_unknown_flags_rejected():
+    cfg = hgnn.make_config(34, 4, 128, 2, 4, 100, 400, 1.0, flags=1 << 20)
+    with pytest.raises(hgnn.HgError) as e:
+        hgnn.hg_config_internal(cfg)
+    assert e.value.name == "HG_E_INVALID"
+
+
+@pytest.mark.parametrize("L,H", [(1, 128), (2, 32), (6, 128), (8, 512), (7, 55)])
+def test_bucket_layout_partitions_the_arena(L, H):
+    """The NCCL gradient buckets (hg_bucket_layout) are contiguous, in backward order (head and
+    the last layers first, conv0 last), and cover the internal arena exactly once, so the
+    bucketed average touches every gradient once."""
+    cfg = hgnn.make_config(34, 4, H, L, 4, 100, 400, 1.0)
+    icfg = hgnn.hg_config_internal(cfg)
+    lay, total = hgnn.hg_param_layout(icfg)
+    b = hgnn.bucket_layout(cfg)
+    assert b[-1][0] == 0 and b[0][1] == total
+    for (b0, e0), (b1, e1) in zip(b, b[1:]):
+        assert e1 == b0 and b1 < e1 and b0 < e0  # descending, adjacent, non-empty
+    covered = np.zeros(total, np.int32)
+    for beg, end in b:
+        covered[beg:end] += 1
+    assert np.all(covered == 1)
+    off = {name: o for name, o, r, c in lay}
+    assert b[-1] == (0, off["conv1.M_x"] if L > 1 else total)  # conv0 alone in the last bucket
+    assert b[0][0] <= off["head.W1"]
+
+
+def test_pack_rejects_more_distinct_degrees_than_class_slots():
+    graphs = []
+    for d in range(1, 40):  # stars of every degree 1..39
+        graphs.append((np.ones((d + 1, 2), np.float32), [(0, i, [1, 0, 0, 0]) for i in range(1, d + 1)], 1.0))
+    data = make_store(graphs, f_edge=4)
+    store = hgnn.Store(data)
+    cfg = hgnn.make_config(2, 4, 128, 1, 40, 1000, 2000, 1.0, max_degree=127)
+    with pytest.raises(hgnn.HgError) as e:
+        hgnn.hg_pack_host(store, list(range(39)), cfg)
+    assert e.value.name == "HG_E_DEGREE"
+    hgnn.hg_pack_host(store, list(range(30)), cfg)  # degrees 1..30: 30 distinct <= 32 slots
+    cfg5 = hgnn.make_config(2, 4, 128, 1, 40, 1000, 2000, 1.0, max_degree=4)  # 5 slots
+    with pytest.raises(hgnn.HgError) as e:
+        hgnn.hg_pack_host(store, [4], cfg5)  # degree 5 > max_degree 4
+    assert e.value.name == "HG_E_CAPACITY"
+
+
+def test_pack_threads_setting_does_not_change_the_bytes(pcqm):
+    store = hgnn.Store(pcqm)
+    cfg = _cfg_for(pcqm, 64)
+    ids = np.arange(64) * 7
+    ref = hgnn.hg_pack_host(store, ids, cfg)
+    for t in (1, 3, 8):
+        hgnn.pack_threads_set(t)
+        np.testing.assert_array_equal(hgnn.hg_pack_host(store, ids, cfg), ref)
+    hgnn.pack_threads_set(4)
+    with pytest.raises(hgnn.HgError):
+        hgnn.pack_threads_set(0)

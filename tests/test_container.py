@@ -96,3 +96,49 @@ def test_container_is_smaller_than_object_store(tmp_path):
     def blocks(d):
         return sum(os.stat(os.path.join(d, f)).st_blocks for f in os.listdir(d))
     assert blocks(tmp_path / "c") < blocks(tmp_path / "o")
+
+
+def _crc32c(data: bytes, crc: int = 0) -> int:
+    """CRC-32C (Castagnoli, reflected 0x82F63B78, initial and final inversion), the checksum
+    csrc/container.cpp computes with the SSE4.2 crc32 instruction."""
+    tbl = []
+    for i in range(256):
+        c = i
+        for _ in range(8):
+            c = (c >> 1) ^ (0x82F63B78 if c & 1 else 0)
+        tbl.append(c)
+    crc ^= 0xFFFFFFFF
+    for b in data:
+        crc = (crc >> 8) ^ tbl[(crc ^ b) & 0xFF]
+    return crc ^ 0xFFFFFFFF
+
+
+def test_checksum_consistent_but_malformed_index_is_rejected(tmp_path):
+    """A meta.idx whose CRC is right but whose subfile table or offsets are out of order must be
+    rejected before any of its values is used as a read destination (container.cpp)."""
+    data = molgen.generate("tiny", 60, 5)
+    src = hgnn.Store(data)
+    path = str(tmp_path / "c.hgpk")
+    src.write_container(path, 3)
+    raw = bytearray(open(os.path.join(path, "meta.idx"), "rb").read())
+    hdr = 48  # MetaHead: magic, version, G, N, E, F0, Fe, n_sub, reserved
+    assert _crc32c(bytes(raw[:-4])) == int.from_bytes(raw[-4:], "little")  # our CRC matches the writer's
+    G = int.from_bytes(raw[8:16], "little")
+    sub_off = hdr + 16 * (G + 1)
+
+    def corrupt(off, value):
+        bad = bytearray(raw)
+        bad[off:off + 8] = int(value).to_bytes(8, "little", signed=True)
+        bad[-4:] = _crc32c(bytes(bad[:-4])).to_bytes(4, "little")
+        open(os.path.join(path, "meta.idx"), "wb").write(bad)
+        with pytest.raises(hgnn.HgError) as e:
+            hgnn.Store.from_container(path)
+        assert e.value.name == "HG_E_IO"
+
+    corrupt(sub_off + 8, 10 ** 12)      # sub[1] far past G
+    corrupt(sub_off + 8, -5)            # sub[1] negative
+    corrupt(hdr + 8 * 5, 10 ** 9)       # node_offset[5] past N
+    corrupt(hdr + 8 * (G + 1) + 8 * 7, -1)  # edge_offset[7] negative
+    corrupt(8, 10 ** 15)                # G absurd: sizes checked before any allocation
+    open(os.path.join(path, "meta.idx"), "wb").write(raw)
+    assert hgnn.Store.from_container(path).stats() == src.stats()

@@ -59,7 +59,7 @@ def test_ddp_p2p_fused_exchange(tmp_path, world):
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     res = json.loads(out.read_text())
     print(res)
-    assert res["nccl_identical"] and res["p2p_identical"]
+    assert res["nccl_identical"] and res["p2p_identical"] and res["switched_identical"]
     # same arithmetic up to the order of the W-term gradient sum (NCCL's ring vs rank order)
     assert res["p2p_vs_nccl_normwise"] <= 1e-5
     assert res["p2p_step1_vs_oracle_normwise"] <= 1e-3

@@ -1,6 +1,6 @@
 """Channel-padded widths (the paper's own H = 55 and H = 200):
-the kernels run at the internal width of hg_config_internal (roundup to 128, or
-32 on the SIMT path) and must compute the logical model exactly (SURVEY §8(d)
+the kernels run at the internal width of hg_config_internal (roundup to 128, the
+tensor-core tile) and must compute the logical model exactly (SURVEY §8(d)
 "Padding hazard"): parity against the float64 oracle at the logical width, and
 every padded parameter / gradient / Adam-moment entry exactly zero after
 training steps."""
@@ -32,17 +32,18 @@ def padded_index(cfg, icfg):
     return np.concatenate(src), np.concatenate(dst), npad
 
 
-@pytest.mark.parametrize("H,flags,L,B", [
-    (55, 0, 2, 64),     # paper width -> 128 channels, tensor-core path
-    (200, 0, 2, 32),    # paper width -> 256 channels
-    (55, 1, 2, 64),     # HG_FLAG_SIMT_GEMM -> 64 channels, SIMT path
-    (100, 0, 3, 48),    # another ragged width, deeper
+@pytest.mark.parametrize("H,L,B", [
+    (55, 2, 64),     # paper width -> 128 channels
+    (200, 2, 32),    # paper width -> 256 channels
+    (32, 2, 64),     # config A's width -> 128 channels
+    (100, 3, 48),    # another ragged width, deeper
 ])
-def test_padded_width_parity_and_zero_padding(torch_cuda, H, flags, L, B):
+def test_padded_width_parity_and_zero_padding(torch_cuda, H, L, B):
+    flags = 0
     data = PT.generate("pcqm", 800, 31)
-    ctx, cfg, delta = PT.make_ctx(data, B, H, L, seed=7, flags=flags)
+    ctx, cfg, delta = PT.make_ctx(data, B, H, L, seed=7)
     icfg = ctx.internal_cfg
-    q = 32 if flags else 128
+    q = 128
     assert icfg.hidden == (H + q - 1) // q * q and icfg.fc_hidden == icfg.hidden
     ids = O.shard(17, 0, 0, 1, len(data["y"]))
     # per-step parity at the logical width (3 steps: moments become non-zero)

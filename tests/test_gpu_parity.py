@@ -83,24 +83,20 @@ def test_one_step_parity(torch_cuda, preset, B, H, L):
     PT.assert_parity(res)
 
 
-@pytest.mark.parametrize("mode", ["simt", "tc_3acc", "tc_classes"])
-def test_gemm_paths_agree(torch_cuda, mode):
-    """Three implementations of the dense contractions compute the same step,
-    each within the oracle bars: SIMT fp32 GEMMs, tcgen05 3xTF32 with three
-    scaler accumulators, and tcgen05 3xTF32 per degree class (config B shape)."""
+@pytest.mark.parametrize("max_degree", [None, 127])
+def test_class_slot_capacities_agree(torch_cuda, max_degree):
+    """The degree-class GEMMs with exactly the store's degree range (5 class slots) and with
+    the full HG_MAX_DEGREE capacity (32 slots, class-indexed weights prepared per batch)
+    compute the same step within the oracle bars (config B shape)."""
     data = PT.generate("pcqm", 600, 51)
     ids = O.shard(5, 0, 0, 1, 600)[:128]
-    flags = hgnn.HG_FLAG_SIMT_GEMM if mode == "simt" else 0
-    max_degree = 127 if mode == "tc_3acc" else None  # > 15 disables the class path
-    ctx, cfg, delta = PT.make_ctx(data, 128, 128, 6, seed=7, flags=flags, max_degree=max_degree)
+    ctx, cfg, delta = PT.make_ctx(data, 128, 128, 6, seed=7, max_degree=max_degree)
     res = PT.run_step_parity(data, ids, ctx, cfg, delta, do_step=False)
-    print(mode, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
+    print(max_degree, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     PT.assert_parity(res)
 
 
-def test_edge_cases_isolated_nodes_single_graph_max_degree(torch_cuda):
-    """d = 0 nodes (C5), single-node graphs, a degree-127 hub (HG_MAX_DEGREE),
-    a disconnected graph; all in one ragged batch."""
+def _edge_case_store():
     rng = np.random.default_rng(0)
     F = 5
     graphs = [
@@ -110,14 +106,46 @@ def test_edge_cases_isolated_nodes_single_graph_max_degree(torch_cuda):
          [(0, i, [0, 1, 0, 0]) for i in range(1, 128)], 3.0),                           # degree-127 hub
         (rng.integers(0, 3, (6, F)).astype(np.float32),
          [(0, 1, [1, 0, 0, 0]), (1, 2, [0, 0, 1, 0]), (3, 4, [0, 0, 0, 1]), (4, 5, [1, 0, 0, 0])], 4.0),
+        (rng.integers(0, 3, (5, F)).astype(np.float32),                                # 4-cycle + pendant:
+         [(0, 1, [1, 0, 0, 0]), (1, 2, [1, 0, 0, 0]), (2, 3, [1, 0, 0, 0]), (3, 0, [1, 0, 0, 0]),
+          (0, 4, [0, 0, 0, 1])], 5.0),                                                  # automorphic ties
     ]
     data = make_store(graphs, f_edge=4)
     data["f_node"] = F
-    ctx, cfg, delta = PT.make_ctx(data, 4, 32, 2, seed=9)
-    res = PT.run_step_parity(data, [0, 1, 2, 3], ctx, cfg, delta)
+    return data
+
+
+@pytest.mark.parametrize("H", [32, 55, 128, 256])
+def test_edge_cases_isolated_nodes_single_graph_max_degree(torch_cuda, H):
+    """d = 0 nodes (C5), single-node graphs, a degree-127 hub (HG_MAX_DEGREE), a disconnected
+    graph and automorphic ties, in one ragged batch, through the product path: tcgen05 degree
+    classes (the hub is its own class), at padded (32, 55 -> 128), native (128: fused dX -> dA
+    kernel) and wide (256: separate dX / dA kernels) widths."""
+    data = _edge_case_store()
+    ctx, cfg, delta = PT.make_ctx(data, 5, H, 2, seed=9)
+    res = PT.run_step_parity(data, [0, 1, 2, 3, 4], ctx, cfg, delta)
+    print(H, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     PT.assert_parity(res)
-    res = PT.run_step_parity(data, [2], ctx, cfg, delta)
+    res = PT.run_step_parity(data, [2], ctx, cfg, delta)  # the hub alone
     PT.assert_parity(res)
+    res = PT.run_step_parity(data, [0], ctx, cfg, delta)  # one isolated node: every aggregate 0
+    PT.assert_parity(res)
+
+
+def test_too_many_distinct_degrees_rejected(torch_cuda):
+    """A batch needs one degree class per distinct degree: more than the ctx's class slots
+    (min(max_degree + 1, 32)) is rejected at pack time (HG_E_DEGREE), not computed wrongly."""
+    graphs = []
+    for d in range(1, 40):  # stars of every degree 1..39
+        graphs.append((np.ones((d + 1, 2), np.float32), [(0, i, [1, 0, 0, 0]) for i in range(1, d + 1)], 1.0))
+    data = make_store(graphs, f_edge=4)
+    data["f_node"] = 2
+    ctx, cfg, delta = PT.make_ctx(data, 39, 128, 1, seed=1, max_degree=127)
+    with pytest.raises(hgnn.HgError) as e:
+        ctx.pack(ctx._store, list(range(39)), 0)
+    assert e.value.name == "HG_E_DEGREE"
+    ctx.pack(ctx._store, list(range(30)), 0)  # 31 distinct degrees (1..30 and 1 for leaves): fits
+    PT.assert_parity(PT.run_step_parity(data, list(range(30)), ctx, cfg, delta))
 
 
 def test_graph_mode_matches_eager_bitwise(torch_cuda):
@@ -206,12 +234,11 @@ def test_small_batch_after_large_batch_class_path(torch_cuda):
     PT.assert_parity(res)
 
 
-def test_separate_dx_da_path(torch_cuda, monkeypatch):
-    """The separate TMA dX and dA kernels (HG_DXDA=0; default is the fused kernel) compute the same step."""
-    monkeypatch.setenv("HG_DXDA", "0")
+def test_separate_dx_da_path_wide(torch_cuda):
+    """H = 256 runs the separate TMA dX and dA kernels (the fused kernel is H = 128 only)."""
     data = PT.generate("pcqm", 600, 21)
-    ctx, cfg, delta = PT.make_ctx(data, 128, 128, 4, seed=5)
-    ids = O.shard(23, 1, 0, 1, len(data["y"]))[:128]
+    ctx, cfg, delta = PT.make_ctx(data, 64, 256, 3, seed=5)
+    ids = O.shard(23, 1, 0, 1, len(data["y"]))[:64]
     res = PT.run_step_parity(data, ids, ctx, cfg, delta)
     print({k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     PT.assert_parity(res)
