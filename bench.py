@@ -169,6 +169,46 @@ def oracle_rate(data, ids_list, cfg, delta, seconds, max_steps=None):
     return graphs / dt, graphs, steps, dt
 
 
+def cpu_info() -> dict:
+    """CPU model (/proc/cpuinfo) and the BLAS numpy runs on (threadpoolctl)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    blas = "unknown"
+    try:
+        from threadpoolctl import threadpool_info
+        b = [i for i in threadpool_info() if i.get("user_api") == "blas"]
+        if b:
+            blas = f"{b[0].get('internal_api')} {b[0].get('version')} ({b[0].get('num_threads')} threads)"
+    except Exception:
+        pass
+    return {"cpu_model": model, "blas": blas}
+
+
+def oracle_config_a_epoch() -> dict:
+    """the oracle over one full config-A epoch (1,000 molecules <= 20 atoms, L=2,
+    H=32, batch 64: 15 steps, drop-last)."""
+    import molgen
+    import oracle as O
+    data = molgen.generate("tiny", 1000, 1)
+    delta = O.degree_stat(data)
+    cfg = {"f_node": data["f_node"], "f_edge": 4, "hidden": 32, "layers": 2, "fc_hidden": 32}
+    params = O.init_params(cfg, 2)
+    st = O.zero_state(params)
+    ids = O.shard(3, 0, 0, 1, 1000)
+    t0 = time.perf_counter()
+    for k in range(len(ids) // 64):
+        params, st, _, _ = O.train_step(params, st, data, ids[k * 64:(k + 1) * 64], cfg, delta)
+    dt = time.perf_counter() - t0
+    return {"steps": len(ids) // 64, "seconds": dt, "graphs_per_s": (len(ids) // 64) * 64 / dt}
+
+
 def blas_threads() -> int:
     try:
         from threadpoolctl import threadpool_info
@@ -252,6 +292,9 @@ def main():
             exchange = f"nccl (p2p unavailable: {e})"
         # (p2p_init agrees across ranks: all take the peer-memory path or none)
     hyper = dict(hgnn.DEFAULT_ADAMW)
+    # host collation threads: 4 on one GPU; with W ranks sharing the host, cores / W each
+    pack_threads = max(1, len(os.sched_getaffinity(0)) // world) if world > 1 else 4
+    hgnn.pack_threads_set(pack_threads)
 
     ids = hgnn.hg_shard(13, 0, rank, world, n_graphs)
     nb = len(ids) // B
@@ -394,12 +437,21 @@ def main():
         "dMx": (Nn * (4 * H + 4 * F0) + NL1 * 8 * H, 2.0 * Nn * H * (F0 + 1) + 2.0 * NL1 * H * (H + 1)),
         "dX": (NL1 * 12 * H, 2.0 * NL1 * H * H),
     }
+    # SURVEY §8(d)'s counting of the same phases: the update and its backward as the 12H-wide
+    # scaler concatenation would compute them (24H^2 FLOPs per node-layer each for update, dA, dU);
+    # the kernels execute the exact degree-class reassociation (8H^2 each), so "executed" is
+    # the work the tensor pipe does and "s8" the method's nominal work
+    work_s8 = dict(work)
+    work_s8["update"] = (work["update"][0], 24.0 * NL * H * H)
+    work_s8["dA"] = (work["dA"][0], 24.0 * NL * H * H)
+    work_s8["dU"] = (work["dU"][0], 24.0 * NL * H * H + NL * H)
     # fused dX -> dA kernel (k_dxda): the dA of layers < L-1 runs inside the dX phase
     n_da = phases.get("dA", [0.0, L])[1]
     if "dA" in phases and 0 < n_da < L:
-        (ba, fa), (bx, fx) = work["dA"], work["dX"]
-        work["dA"] = (ba * n_da / L, fa * n_da / L)
-        work["dX"] = (bx + ba * (L - n_da) / L, fx + fa * (L - n_da) / L)
+        for w in (work, work_s8):
+            (ba, fa), (bx, fx) = w["dA"], w["dX"]
+            w["dA"] = (ba * n_da / L, fa * n_da / L)
+            w["dX"] = (bx + ba * (L - n_da) / L, fx + fa * (L - n_da) / L)
     peaks = {}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -435,13 +487,65 @@ def main():
                   "algorithmic_bytes_per_launch": byt / launches_k, "algorithmic_flops_per_launch": fl / launches_k,
                   "intensity_flop_per_byte": fl / byt, "share_of_step": phases[k][0] / step_ms_prof,
                   "traffic": traffic_db.get(k)})
+        if r["bound"] == "tensor":
+            fl8 = work_s8[k][1]
+            r.update({"flops_counting": "executed: degree-class form (8H^2 per node-layer per update/dA/dU GEMM)",
+                      "achieved_s8": fl8 / t / 1e12, "frac_s8": fl8 / t / 1e12 / tc_peak,
+                      "flops_counting_s8": "SURVEY §8(d): 24H^2 per node-layer per update/dA/dU GEMM",
+                      "algorithmic_flops_per_launch_s8": fl8 / launches_k})
         return r
 
     dom = max((k for k in phases if k in work), key=lambda k: phases[k][0])
     prof = roof(dom)
     phase_roof = {k: {kk: (round(vv, 4) if isinstance(vv, float) else vv) for kk, vv in roof(k).items()
-                      if kk in ("bound", "achieved", "frac", "ms", "intensity_flop_per_byte")}
+                      if kk in ("bound", "achieved", "frac", "frac_s8", "ms", "intensity_flop_per_byte")}
                   for k in work if k in phases}
+    # the north_star's aggregation bar (>= 60% of HBM): algorithmic bytes / time
+    agg = {k: {"algorithmic_GBps": round(work[k][0] / (phases[k][0] / 1e3) / 1e9, 1),
+               "frac_of_hbm": round(work[k][0] / (phases[k][0] / 1e3) / 1e9 / hbm_peak, 4),
+               "us_per_launch": round(1e3 * phases[k][0] / max(1, phases[k][1]), 2),
+               "bytes_per_node_layer": f"{'22' if k == 'agg_fwd' else '34'}H + 4 + 20*ebar"}
+           for k in ("agg_fwd", "agg_bwd") if k in phases}
+
+    # ---- host-only collation rate (SURVEY §8(d) timing protocol (3)): hg_pack_host from the store
+    nb_pack = min(nb, 200)
+    t0 = time.perf_counter()
+    for k in range(nb_pack):
+        hgnn.hg_pack_host(store, batches[k], cfg)
+    dtp = time.perf_counter() - t0
+    pack_rate = {"graphs_per_s_per_rank": nb_pack * B / dtp, "threads": pack_threads, "batches": nb_pack,
+                 "note": "hg_pack_host (C++ collate of B graphs from the Table-1 store), host only"}
+
+    # ---- exchange alone (N > 1): peer-memory exchange or NCCL bucketed path, bus GB/s
+    exch = None
+    if world > 1:
+        import torch.distributed as tdist
+        P4 = ctx.n_params * 4
+        busf = 2.0 * (world - 1) / world
+        exch = {"grad_bytes": P4, "bus_factor": busf, "nvlink_ref_GBps": 770.0,
+                "nvlink_ref_source": "B200_PROFILING.md peer copy per direction (900 nominal)"}
+        barrier()
+        t_ex = ctx.exchange_time(20, **hyper)
+        barrier()
+        exch["step_exchange"] = {"kind": exchange, "ms": t_ex, "busbw_GBps": P4 * busf / (t_ex / 1e3) / 1e9}
+        sweep = {}
+        for sz in [64 << 10, 256 << 10, 1 << 20, 4 << 20, 16 << 20, 64 << 20, 128 << 20]:
+            tsw = torch.empty(sz // 4, dtype=torch.float32, device="cuda")
+            for _ in range(3):
+                tdist.all_reduce(tsw)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(10):
+                tdist.all_reduce(tsw)
+            e1.record()
+            torch.cuda.synchronize()
+            tt = e0.elapsed_time(e1) / 10
+            sweep[str(sz)] = {"ms": tt, "busbw_GBps": sz * busf / (tt / 1e3) / 1e9}
+            del tsw
+        exch["nccl_allreduce_sweep"] = sweep
+        bucket_sizes = [4 * (e - b0) for b0, e in hgnn.bucket_layout(cfg)]
+        exch["nccl_bucket_bytes"] = bucket_sizes
 
     # ---- CPU baseline: the oracle on a bounded sample (rank 0, N = 1)
     cpu = None
@@ -454,6 +558,8 @@ def main():
         cpu = {"value": rate, "unit": "graphs/s", "cores": blas_threads(), "kind": "oracle",
                "sample": f"{s} oracle train steps (f64 numpy forward+backward+AdamW) on batches of {B} graphs of "
                          f"this workload, {dt:.1f} s", "host_cores": len(os.sched_getaffinity(0))}
+        cpu.update(cpu_info())
+        cpu["config_A_epoch"] = oracle_config_a_epoch()
 
     out = {
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
@@ -466,7 +572,8 @@ def main():
                    "grad_exchange": exchange,
                    "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
                    "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs, TMA-fed"},
-        "roofline": prof, "phase_roofline": phase_roof,
+        "roofline": prof, "phase_roofline": phase_roof, "aggregation": agg, "pack_rate": pack_rate,
+        "exchange": exch,
         "phases_ms": {k: round(v[0], 4) for k, v in phases.items()},
         "phase_launches": {k: v[1] for k, v in phases.items()},
         "cpu_baseline": cpu, "e2e": e2e, "eval": eval_out, "gpu_launches": launches, "clocks": clk,

@@ -288,6 +288,13 @@ hg_status hg_p2p_open(hg_ctx *x, const void *all);
  * HG_E_STATE if a context holds a communicator. */
 hg_status hg_p2p_emulate(hg_ctx *const *ctxs, int32_t world, const hg_adamw *h);
 
+/* Measurement: run this ctx's gradient exchange alone `iters` times back to back on the
+ * compute stream (peer-memory reduce + AdamW + all-gather when hg_p2p_open is on, else the
+ * NCCL average of the whole arena) and return the mean device milliseconds per exchange.
+ * Collective (every rank calls it); the peer-memory variant applies AdamW to the current
+ * gradients, so it advances the optimizer state. HG_E_STATE without an exchange. */
+hg_status hg_exchange_time(hg_ctx *x, const hg_adamw *h, int32_t iters, float *ms);
+
 /* Fail-stop bound, seconds (0 = none, the default): every device
  * flag wait of the peer-memory exchange traps past it (the step then fails with HG_E_CUDA),
  * and hg_sync returns HG_E_NCCL after aborting the NCCL communicator when its streams have

@@ -55,24 +55,51 @@ def _mul64(a: int, b: np.ndarray) -> np.ndarray:
 # --------------------------------------------------------------------------
 # model configuration and parameters
 # --------------------------------------------------------------------------
+SCALERS = ("identity", "amplification", "attenuation", "linear", "inverse_linear")
+DEFAULT_SCALERS = ("identity", "amplification", "attenuation")
+
+
+def model_scalers(cfg: dict) -> tuple:
+    """The configured scaler list (SPEC.md:326 'scalers subset of {identity, amplification,
+    attenuation}', identity present; SURVEY C2 default: all three). Model variant (SURVEY §8(f)
+    row 3, reading R-scalers): PNA's linear d/delta_lin and inverse_linear delta_lin/d scalers."""
+    sc = tuple(cfg.get("scalers", DEFAULT_SCALERS))
+    if not sc or sc[0] != "identity" or len(set(sc)) != len(sc) or any(x not in SCALERS for x in sc):
+        raise ValueError("scalers: identity first, then distinct names from %s" % (SCALERS,))
+    return sc
+
+
 def param_specs(cfg: dict) -> list:
     """Ordered (name, shape, fan_in, fan_out) list; the order is tensor_idx.
 
     Per conv layer l: message matrix M = [M_x | M_e]
     of shape [H, F_l + Fe] stored as two tensors (same init scale, fan of the
-    whole M), bias b_M [H]; update matrix U [H, 12H] with column index
-    (s*4 + a)*H + c, s in (identity, amplification, attenuation), a in (mean,
-    min, max, std); bias b_U [H]. Head: W1 [Hf, H], b1, W2 [1, Hf], b2.
+    whole M), bias b_M [H]; update matrix U [H, 4SH] with column index
+    (s*4 + a)*H + c, s over the configured scalers (default identity,
+    amplification, attenuation: 12H), a in (mean, min, max, std); bias b_U [H].
+    Self-term variant (cfg['self_term'], reading R-self):
+    M = [M_x | M_s | M_e] (M_s [H, F_l] multiplies the destination's own x_i) and the update
+    matrix [U | U_x] (U_x [H, F_l] multiplies x_i), each stored as separate tensors with the
+    whole matrix's fan; order M_x, M_s, M_e, b_M, U, U_x, b_U.
+    Head: W1 [Hf, H], b1, W2 [1, Hf], b2.
     """
     H, L, F0, Fe = cfg["hidden"], cfg["layers"], cfg["f_node"], cfg["f_edge"]
     Hf = cfg.get("fc_hidden", H)
+    S = len(model_scalers(cfg))
+    st = bool(cfg.get("self_term", False))
     out = []
     for l in range(L):
         Fl = F0 if l == 0 else H
-        out.append((f"conv{l}.M_x", (H, Fl), Fl + Fe, H))
-        out.append((f"conv{l}.M_e", (H, Fe), Fl + Fe, H))
+        fm = (2 * Fl if st else Fl) + Fe
+        fu = 4 * S * H + (Fl if st else 0)
+        out.append((f"conv{l}.M_x", (H, Fl), fm, H))
+        if st:
+            out.append((f"conv{l}.M_s", (H, Fl), fm, H))
+        out.append((f"conv{l}.M_e", (H, Fe), fm, H))
         out.append((f"conv{l}.b_M", (H,), 0, 0))
-        out.append((f"conv{l}.U", (H, 12 * H), 12 * H, H))
+        out.append((f"conv{l}.U", (H, 4 * S * H), fu, H))
+        if st:
+            out.append((f"conv{l}.U_x", (H, Fl), fu, H))
         out.append((f"conv{l}.b_U", (H,), 0, 0))
     out.append(("head.W1", (Hf, H), H, Hf))
     out.append(("head.b1", (Hf,), 0, 0))
@@ -137,6 +164,18 @@ def degree_stat(store: dict, ids=None) -> float:
         tot += float(np.log(d.astype(np.float64) + 1.0).sum())
         cnt += n
     return tot / cnt
+
+
+def degree_stat_linear(store: dict, ids=None) -> float:
+    """delta_lin = mean in-degree over all nodes of the (training) graphs: the normaliser of
+    PNA's linear / inverse_linear scalers (model variant, reading R-scalers; C4's convention
+    of the global training set)."""
+    no, eo = store["node_offset"], store["edge_offset"]
+    if ids is None:
+        ids = np.arange(len(no) - 1)
+    ne = sum(int(eo[g + 1] - eo[g]) for g in np.asarray(ids))
+    nn = sum(int(no[g + 1] - no[g]) for g in np.asarray(ids))
+    return ne / nn  # symmetric edge lists: sum of in-degrees = number of directed edges
 
 
 # --------------------------------------------------------------------------
@@ -227,7 +266,32 @@ def scalers(deg: np.ndarray, delta: float):
     return amp, att
 
 
-def conv_forward(Xl: np.ndarray, batch: dict, p: dict, l: int, delta: float, var_floor: float = VAR_FLOOR):
+def scaler_values(deg: np.ndarray, delta: float, names=DEFAULT_SCALERS, delta_lin: float = None) -> list:
+    """Per-node value of each configured scaler (reading
+    R-scalers for the PNA variants): identity 1, amplification ln(d+1)/delta, attenuation
+    delta/ln(d+1), linear d/delta_lin, inverse_linear delta_lin/d; every scaler is 1 at d = 0."""
+    amp, att = scalers(deg, delta)
+    d = deg.astype(np.float64)
+    has = deg > 0
+    out = []
+    for nm in names:
+        if nm == "identity":
+            out.append(np.ones(len(deg)))
+        elif nm == "amplification":
+            out.append(amp)
+        elif nm == "attenuation":
+            out.append(att)
+        elif nm == "linear":
+            out.append(np.where(has, d / delta_lin, 1.0))
+        elif nm == "inverse_linear":
+            out.append(np.where(has, delta_lin / np.where(has, d, 1.0), 1.0))
+        else:
+            raise ValueError(nm)
+    return out
+
+
+def conv_forward(Xl: np.ndarray, batch: dict, p: dict, l: int, delta: float, var_floor: float = VAR_FLOOR,
+                 cfg: dict = None):
     """One PNA-style GC layer.
 
     m_{j->i} = M [x_j || e_ji] + b_M over in-neighbours j of i;
@@ -235,13 +299,22 @@ def conv_forward(Xl: np.ndarray, batch: dict, p: dict, l: int, delta: float, var
     sqrt(max(var, eps_v)) with the population variance computed two-pass
     (SURVEY C6); d = 0 rows are all zero (C5); S = [A || amp*A || att*A]
     (scaler-major, C3); Z = S U^T + b_U; X_{l+1} = max(Z, 0).
+    Variants (cfg): other scaler lists (S = [s_1 A || s_2 A || ...]); self_term: the message
+    is M [x_j || x_i || e_ji] + b_M and Z = [S || x_i] [U | U_x]^T + b_U.
     """
+    cfg = cfg or {}
+    names = model_scalers(cfg)
+    self_t = bool(cfg.get("self_term", False))
     rowptr = batch["rowptr"].astype(np.int64)
     col = batch["col"].astype(np.int64)
     row, pos = batch["row"], batch["pos"]
     deg = np.diff(rowptr)
-    M = np.concatenate([p[f"conv{l}.M_x"], p[f"conv{l}.M_e"]], axis=1)
-    cat = np.concatenate([Xl[col], batch["eattr"].astype(np.float64)], axis=1)
+    if self_t:
+        M = np.concatenate([p[f"conv{l}.M_x"], p[f"conv{l}.M_s"], p[f"conv{l}.M_e"]], axis=1)
+        cat = np.concatenate([Xl[col], Xl[row], batch["eattr"].astype(np.float64)], axis=1)
+    else:
+        M = np.concatenate([p[f"conv{l}.M_x"], p[f"conv{l}.M_e"]], axis=1)
+        cat = np.concatenate([Xl[col], batch["eattr"].astype(np.float64)], axis=1)
     msg = cat @ M.T + p[f"conv{l}.b_M"]
     N = len(deg)
     dd = np.maximum(deg, 1).astype(np.float64)[:, None]
@@ -259,11 +332,16 @@ def conv_forward(Xl: np.ndarray, batch: dict, p: dict, l: int, delta: float, var
     std[empty] = 0.0
     A = np.concatenate([mean, mn, mx, std], axis=1)
     amp, att = scalers(deg, delta)
-    S = np.concatenate([A, amp[:, None] * A, att[:, None] * A], axis=1)
-    Z = S @ p[f"conv{l}.U"].T + p[f"conv{l}.b_U"]
+    sv = scaler_values(deg, delta, names, cfg.get("delta_lin"))
+    S = np.concatenate([s[:, None] * A for s in sv], axis=1)
+    Uf = p[f"conv{l}.U"]
+    if self_t:
+        S = np.concatenate([S, Xl], axis=1)
+        Uf = np.concatenate([Uf, p[f"conv{l}.U_x"]], axis=1)
+    Z = S @ Uf.T + p[f"conv{l}.b_U"]
     X1 = np.maximum(Z, 0.0)
     cache = dict(Xl=Xl, cat=cat, msg=msg, mean=mean, mn=mn, mx=mx, argmax=argmax, argmin=argmin,
-                 var=var, std=std, A=A, S=S, Z=Z, amp=amp, att=att, deg=deg, N=N)
+                 var=var, std=std, A=A, S=S, Z=Z, amp=amp, att=att, sv=sv, deg=deg, N=N)
     return X1, cache
 
 
@@ -273,7 +351,7 @@ def forward(params: dict, batch: dict, cfg: dict, delta: float):
     X = batch["x"].astype(np.float64)
     caches = []
     for l in range(cfg["layers"]):
-        X, c = conv_forward(X, batch, params, l, delta, cfg.get("var_floor", VAR_FLOOR))
+        X, c = conv_forward(X, batch, params, l, delta, cfg.get("var_floor", VAR_FLOOR), cfg)
         caches.append(c)
     gp = batch["graph_ptr"].astype(np.int64)
     ng = np.diff(gp)
@@ -323,16 +401,24 @@ def backward(params: dict, batch: dict, cfg: dict, cache: dict, decisions: dict 
     col = batch["col"].astype(np.int64)
     row, pos = batch["row"], batch["pos"]
     H = cfg["hidden"]
+    self_t = bool(cfg.get("self_term", False))
+    nS = len(model_scalers(cfg))
     for l in reversed(range(cfg["layers"])):
         c = cache["layers"][l]
         dec = decisions.get(l, {})
         relu = dec.get("relu", c["Z"] > 0)
         dZ = dX * relu
-        g[f"conv{l}.U"] = dZ.T @ c["S"]
+        F = c["Xl"].shape[1]
+        dUf = dZ.T @ c["S"]
+        g[f"conv{l}.U"] = dUf[:, :4 * nS * H]
+        Uf = params[f"conv{l}.U"]
+        if self_t:
+            g[f"conv{l}.U_x"] = dUf[:, 4 * nS * H:]
+            Uf = np.concatenate([Uf, params[f"conv{l}.U_x"]], axis=1)
         g[f"conv{l}.b_U"] = dZ.sum(0)
-        dS = dZ @ params[f"conv{l}.U"]
-        amp, att = c["amp"][:, None], c["att"][:, None]
-        dA = dS[:, :4 * H] + amp * dS[:, 4 * H:8 * H] + att * dS[:, 8 * H:]
+        dS = dZ @ Uf
+        dA = sum(s[:, None] * dS[:, k * 4 * H:(k + 1) * 4 * H] for k, s in enumerate(c["sv"]))
+        dX_self = dS[:, 4 * nS * H:] if self_t else None
         dmean, dmin, dmax, dstd = (dA[:, a * H:(a + 1) * H] for a in range(4))
         argmax = dec.get("argmax", c["argmax"])
         argmin = dec.get("argmin", c["argmin"])
@@ -345,14 +431,19 @@ def backward(params: dict, batch: dict, cfg: dict, cache: dict, decisions: dict 
               + (p2 == argmin[row]) * dmin[row]
               + varflag[row] * dstd[row] * (c["msg"] - c["mean"][row]) / (dr * np.where(c["std"][row] > 0, c["std"][row], 1.0)))
         dM = dm.T @ c["cat"]
-        F = c["Xl"].shape[1]
         g[f"conv{l}.M_x"] = dM[:, :F]
-        g[f"conv{l}.M_e"] = dM[:, F:]
+        if self_t:
+            g[f"conv{l}.M_s"] = dM[:, F:2 * F]
+            g[f"conv{l}.M_e"] = dM[:, 2 * F:]
+        else:
+            g[f"conv{l}.M_e"] = dM[:, F:]
         g[f"conv{l}.b_M"] = dm.sum(0)
         if l > 0:
-            dcat = dm @ np.concatenate([params[f"conv{l}.M_x"], params[f"conv{l}.M_e"]], axis=1)
             dX = np.zeros_like(c["Xl"])
-            np.add.at(dX, col, dcat[:, :F])
+            np.add.at(dX, col, dm @ params[f"conv{l}.M_x"])  # through the sources x_j
+            if self_t:
+                np.add.at(dX, row, dm @ params[f"conv{l}.M_s"])  # through the destinations x_i
+                dX = dX + dX_self  # through the update's x_i block
     return g
 
 

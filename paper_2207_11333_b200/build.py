@@ -20,7 +20,7 @@ OBJDIR = os.path.join(HERE, "build")
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["kernels.cu", "degsort.cu", "tcdirect.cu", "tcmn.cu", "p2p.cu", "ctx.cu"]
+CU_SOURCES = ["kernels.cu", "agg.cu", "degsort.cu", "tcdirect.cu", "tcmn.cu", "p2p.cu", "ctx.cu"]
 CPP_SOURCES = ["host.cpp", "container.cpp"]
 
 

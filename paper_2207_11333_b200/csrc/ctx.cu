@@ -49,6 +49,7 @@ struct Plan {
   std::vector<size_t> Xmask;       // per layer: ReLU mask bits of X_l, sorted rows, [N][H/32]
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t p2p = 0;  // P2PDev flags of the peer-memory gradient exchange
+  size_t dm_scratch = 0;
   size_t total = 0;
 };
 
@@ -121,6 +122,7 @@ Plan make_plan(const hg_config &c) {
   p.part2 = take(sizeof(float) * pf);
   p.part3 = take(sizeof(float) * pf);
   for (int l = 0; l < c.layers; ++l) p.pagg.push_back(take(sizeof(float) * agg_bwd_partial_floats(caps)));
+  p.dm_scratch = take(sizeof(float) * agg_bwd_dm_floats(caps));  // graphs too large to stage (agg.cu)
   p.total = off;
   return p;
 }
@@ -411,7 +413,8 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
       launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, nullptr, pos, x->dxda ? pos : nullptr);
+                     x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, pos, x->dxda ? pos : nullptr,
+                     x->f(p.dm_scratch));
     });
     const int F = l == 0 ? c.f_node : c.hidden;
     // ---- side stream 2: dM_e, dM_x, db_M once dP_l is ready; with Gram_l done, layer l is complete
@@ -704,6 +707,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   if ((e = cudaMemsetAsync(workspace, 0, plan.total, x->stream)) != cudaSuccess) return bail(e, "cudaMemsetAsync");
   head_configure(x->caps);
   if ((e = tcd_configure()) != cudaSuccess) return bail(e, "tcd_configure");
+  if ((e = agg_configure()) != cudaSuccess) return bail(e, "agg_configure");
   x->dxda = dxda_supported(x->caps);  // fused dX -> dA backward: +2.3% at config B
   {
     std::vector<int64_t> uo, mo;
@@ -1428,6 +1432,36 @@ hg_status hg_p2p_emulate(hg_ctx *const *ctxs, int32_t world, const hg_adamw *h) 
   hg_status st = after_enqueue(x0, "emulated exchange");
   if (st) return st;
   CK(x0, cudaStreamSynchronize(x0->stream));
+  return HG_OK;
+}
+
+hg_status hg_exchange_time(hg_ctx *x, const hg_adamw *h, int32_t iters, float *ms) {
+  hg_status st = usable(x);
+  if (st) return st;
+  if (!h || !ms || iters < 1) return fail(HG_E_INVALID, "bad arguments");
+  if (!x->p2p && !x->comm) return fail(HG_E_STATE, "no exchange configured (hg_comm_init / hg_p2p_open)");
+  cudaEvent_t a, b;
+  CK(x, cudaEventCreate(&a));
+  CK(x, cudaEventCreate(&b));
+  CK(x, cudaStreamSynchronize(x->stream));
+  CK(x, cudaEventRecord(a, x->stream));
+  for (int i = 0; i < iters; ++i) {
+    if (x->p2p) {
+      launch_p2p_exchange(x->stream, p2p_args(x, *h));
+      x->launches += 4;
+      x->mv_sharded = true;
+    } else if ((st = enqueue_allreduce(x, x->stream))) {
+      return st;
+    }
+  }
+  CK(x, cudaEventRecord(b, x->stream));
+  if ((st = after_enqueue(x, "exchange"))) return st;
+  CK(x, cudaEventSynchronize(b));
+  float t = 0.f;
+  CK(x, cudaEventElapsedTime(&t, a, b));
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  *ms = t / (float)iters;
   return HG_OK;
 }
 

@@ -158,354 +158,6 @@ void launch_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const floa
   run_gemm<true, true>(st, op, c.maxN, c.H, 1);
 }
 
-// ------------------------------------------------------------------ K2 aggregation forward
-// One warp per destination node i, lane owns CPL consecutive channels of a
-// 32*CPL-channel chunk (blockIdx.y). Messages m = P[j] + b_M + M_e e_ji are
-// recomputed, never stored. First pass: sum, min, max with
-// first-position argmin/argmax; second pass: centred sum of squares (two-pass
-// variance) over recomputed messages. d = 0 -> all aggregates 0 (C5).
-// FE: compile-time edge-feature width (4 for the molecular encoding; 8 = generic <= 8).
-
-template <int CPL>
-__device__ __forceinline__ void load_vec(const float *p, float (&v)[CPL]) {
-  if constexpr (CPL == 4) {
-    const float4 t = __ldg(reinterpret_cast<const float4 *>(p));
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  } else if constexpr (CPL == 2) {
-    const float2 t = __ldg(reinterpret_cast<const float2 *>(p));
-    v[0] = t.x; v[1] = t.y;
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) v[c] = __ldg(p + c);
-  }
-}
-template <int CPL>
-__device__ __forceinline__ void store_vec(float *p, const float (&v)[CPL]) {
-  if constexpr (CPL == 4) {
-    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  } else if constexpr (CPL == 2) {
-    *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
-  } else {
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) p[c] = v[c];
-  }
-}
-
-template <int FE>
-__device__ __forceinline__ void load_edge(const float *ea, int Fe, int k, float (&ef)[FE]) {
-  if constexpr (FE == 4) {
-    const float4 t = __ldg(reinterpret_cast<const float4 *>(ea + (size_t)k * 4));
-    ef[0] = t.x; ef[1] = t.y; ef[2] = t.z; ef[3] = t.w;
-  } else {
-#pragma unroll
-    for (int f = 0; f < FE; ++f) ef[f] = f < Fe ? __ldg(ea + (size_t)k * Fe + f) : 0.f;
-  }
-}
-
-// message for CPL channels: m = (P + b_M) + sum_f M_e[:,f] e_f  (same order in K2 and K8)
-template <int CPL, int FE>
-__device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm)[CPL], const float (&me)[CPL][FE],
-                                        const float (&ef)[FE], float (&m)[CPL]) {
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    float v = pj[c] + bm[c];
-#pragma unroll
-    for (int f = 0; f < FE; ++f) v = fmaf(me[c][f], ef[f], v);
-    m[c] = v;
-  }
-}
-
-template <int CPL, int FE>
-__global__ void __launch_bounds__(256, 4) k_agg_fwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
-                                                    const float *__restrict__ Me, const float *__restrict__ bM,
-                                                    float var_floor, float *__restrict__ A,
-                                                    uint8_t *__restrict__ arg, int H,
-                                                    const int *__restrict__ pos, int Hl) {
-  pdl_enter();
-  const BatchView b = load_batch(blob);
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  const int ch = blockIdx.y * 32 * CPL + lane * CPL;
-  const int Fe = b.Fe;
-  float me[CPL][FE], bm[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    bm[c] = bM[ch + c];
-#pragma unroll
-    for (int f = 0; f < FE; ++f) me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f;
-  }
-  for (int i = blockIdx.x * wpb + (threadIdx.x >> 5); i < b.N; i += gridDim.x * wpb) {
-    const int k0 = b.rowptr[i], k1 = b.rowptr[i + 1], d = k1 - k0;
-    const int prow = pos ? __ldg(pos + i) : i;  // (issued early: its latency hides behind the edge loop)
-    float s[CPL], mx[CPL], mn[CPL];
-    int amx[CPL], amn[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) { s[c] = 0.f; mx[c] = -INFINITY; mn[c] = INFINITY; amx[c] = 0; amn[c] = 0; }
-    for (int k = k0; k < k1; ++k) {
-      const int j = b.col[k];
-      float ef[FE], pj[CPL], m[CPL];
-      load_edge<FE>(b.ea, Fe, k, ef);
-      load_vec<CPL>(P + ch + j * H, pj);
-      message<CPL, FE>(pj, bm, me, ef, m);
-      const int p = k - k0;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        s[c] += m[c];
-        if (m[c] > mx[c]) { mx[c] = m[c]; amx[c] = p; }
-        if (m[c] < mn[c]) { mn[c] = m[c]; amn[c] = p; }
-      }
-    }
-    float mean[CPL], sd[CPL];
-    int flag[CPL];
-    if (d == 0) {
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) { mean[c] = 0.f; mx[c] = 0.f; mn[c] = 0.f; sd[c] = 0.f; flag[c] = 0; }
-    } else {
-      const float fd = (float)d, rd = __frcp_rn(fd);
-      float ss[CPL];
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) { mean[c] = s[c] * rd; ss[c] = 0.f; }
-      for (int k = k0; k < k1; ++k) {  // second pass: recompute (P rows are L1-resident)
-        const int j = b.col[k];
-        float ef[FE], pj[CPL], m[CPL];
-        load_edge<FE>(b.ea, Fe, k, ef);
-        load_vec<CPL>(P + ch + j * H, pj);
-        message<CPL, FE>(pj, bm, me, ef, m);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const float t = m[c] - mean[c];
-          ss[c] = fmaf(t, t, ss[c]);
-        }
-      }
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        const float var = ss[c] * rd;
-        flag[c] = var > var_floor;
-        // channels >= Hl are padding (internal width H > logical Hl): their messages are
-        // exactly 0, and their std is forced to 0 instead of sqrt(var_floor) so that no
-        // gradient reaches the zero padded parameters (SURVEY §8(d) padding hazard)
-        sd[c] = ch + c < Hl ? sqrtf(fmaxf(var, var_floor)) : 0.f;
-      }
-    }
-    const int arow = prow * (4 * H) + ch;  // degree-sorted row when pos is given (N * 4H < 2^31)
-    float *Ai = A + arow;
-    store_vec<CPL>(Ai, mean);
-    store_vec<CPL>(Ai + H, mn);
-    store_vec<CPL>(Ai + 2 * H, mx);
-    store_vec<CPL>(Ai + 3 * H, sd);
-    uint8_t *ai = arg + ch + i * (2 * H);
-    if constexpr (CPL == 4) {
-      *reinterpret_cast<uchar4 *>(ai) = make_uchar4(amn[0], amn[1], amn[2], amn[3]);
-      *reinterpret_cast<uchar4 *>(ai + H) =
-          make_uchar4(amx[0] | (flag[0] << 7), amx[1] | (flag[1] << 7), amx[2] | (flag[2] << 7), amx[3] | (flag[3] << 7));
-    } else if constexpr (CPL == 2) {
-      *reinterpret_cast<uchar2 *>(ai) = make_uchar2(amn[0], amn[1]);
-      *reinterpret_cast<uchar2 *>(ai + H) = make_uchar2(amx[0] | (flag[0] << 7), amx[1] | (flag[1] << 7));
-    } else {
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        ai[c] = (uint8_t)amn[c];
-        ai[H + c] = (uint8_t)(amx[c] | (flag[c] << 7));
-      }
-    }
-  }
-}
-
-static int agg_cpl(int H) { return (H % 64 == 0) ? 2 : 1; }
-
-template <int CPL, int FE>
-static void agg_fwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                           const float *bM, float var_floor, float *A, uint8_t *arg, const int *pos) {
-  const dim3 grid(std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 4)), c.H / (32 * CPL));
-  launch_ex(k_agg_fwd<CPL, FE>, grid, 256, 0, st, blob, P, Me, bM, var_floor, A, arg, c.H, pos,
-            c.Hl > 0 ? c.Hl : c.H);
-}
-
-void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, float var_floor, float *A, uint8_t *arg, const int *pos) {
-  const int cpl = agg_cpl(c.H);
-  if (cpl == 2 && c.Fe == 4) agg_fwd_launch<2, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
-  else if (cpl == 2) agg_fwd_launch<2, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
-  else if (c.Fe == 4) agg_fwd_launch<1, 4>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
-  else agg_fwd_launch<1, 8>(st, c, blob, P, Me, bM, var_floor, A, arg, pos);
-  counted();
-}
-
-// ------------------------------------------------------------------ K8 aggregation backward
-// One warp per SOURCE node j over its CSR row: by symmetry row j
-// lists every i with an edge j -> i, and slot[k] is j's position inside row i,
-// i.e. where K2 saw message m_{j->i}. Per edge:
-//   dm = dA_mean[i]/d_i + [slot == argmax_i] dA_max[i] + [slot == argmin_i] dA_min[i]
-//        + [var_i > eps] dA_std[i] (m - mu_i)/(d_i sigma_i)
-// dP[j] = sum dm (written once, no atomics); dM_e per-block partials reduced in
-// fixed order by k_reduce_rows.
-constexpr int kAggBwdWarps = 8;
-
-template <int CPL, int FE>
-__global__ void __launch_bounds__(256, 4) k_agg_bwd(const uint8_t *__restrict__ blob, const float *__restrict__ P,
-                                                    const float *__restrict__ Me, const float *__restrict__ bM,
-                                                    const float *__restrict__ A, const uint8_t *__restrict__ arg,
-                                                    const float *__restrict__ dA, float *__restrict__ dP,
-                                                    float *__restrict__ partial, int H,
-                                                    const int *__restrict__ pos, const int *__restrict__ dp_pos) {
-  pdl_enter();
-  __shared__ float red[kAggBwdWarps][32][CPL * FE];
-  __shared__ float redb[kAggBwdWarps][32][CPL];
-  // the batch view lives in shared memory: under register pressure the compiler reloads its
-  // pointers (one LDS) instead of recomputing the blob offsets on every edge
-  __shared__ BatchView sb;
-  if (threadIdx.x == 0) sb = load_batch(blob);
-  __syncthreads();
-  const BatchView &b = sb;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int wpb = blockDim.x >> 5;
-  const int ch = blockIdx.y * 32 * CPL + lane * CPL;
-  const int Fe = b.Fe;
-  float me[CPL][FE], bm[CPL], acc[CPL][FE], bsum[CPL];  // bsum: db_M = sum_j dP_j
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    bm[c] = bM[ch + c];
-    bsum[c] = 0.f;
-#pragma unroll
-    for (int f = 0; f < FE; ++f) { me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f; acc[c][f] = 0.f; }
-  }
-  for (int j = blockIdx.x * wpb + warp; j < b.N; j += gridDim.x * wpb) {
-    const int k0 = b.rowptr[j], k1 = b.rowptr[j + 1];
-    const int prow_out = dp_pos ? __ldg(dp_pos + j) : j;  // (issued early)
-    float pj[CPL], dp[CPL];
-    load_vec<CPL>(P + (size_t)j * H + ch, pj);
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) dp[c] = 0.f;
-    for (int k = k0; k < k1; ++k) {
-      const int i = b.col[k];
-      const int sl = b.slot[k];
-      const int di = b.rowptr[i + 1] - b.rowptr[i];
-      const float inv_d = __frcp_rn((float)di);
-      float ef[FE];
-      load_edge<FE>(b.ea, Fe, k, ef);
-      float m[CPL];
-      message<CPL, FE>(pj, bm, me, ef, m);
-      // (32-bit row offsets from per-lane bases: N * 4H < 2^31)
-      const float *dAi = dA + ch + i * (4 * H);
-      const float *Ai = A + ch + (pos ? __ldg(pos + i) : i) * (4 * H);
-      float gmean[CPL], gmin[CPL], gmax[CPL], gstd[CPL], mu[CPL], sg[CPL];
-      load_vec<CPL>(dAi, gmean);
-      load_vec<CPL>(dAi + H, gmin);
-      load_vec<CPL>(dAi + 2 * H, gmax);
-      load_vec<CPL>(dAi + 3 * H, gstd);
-      load_vec<CPL>(Ai, mu);
-      load_vec<CPL>(Ai + 3 * H, sg);
-      uint8_t amn[CPL], amx[CPL];
-      const uint8_t *ai = arg + ch + i * (2 * H);
-      if constexpr (CPL == 4) {
-        const uchar4 t0 = *reinterpret_cast<const uchar4 *>(ai);
-        const uchar4 t1 = *reinterpret_cast<const uchar4 *>(ai + H);
-        amn[0] = t0.x; amn[1] = t0.y; amn[2] = t0.z; amn[3] = t0.w;
-        amx[0] = t1.x; amx[1] = t1.y; amx[2] = t1.z; amx[3] = t1.w;
-      } else if constexpr (CPL == 2) {
-        const uchar2 t0 = *reinterpret_cast<const uchar2 *>(ai);
-        const uchar2 t1 = *reinterpret_cast<const uchar2 *>(ai + H);
-        amn[0] = t0.x; amn[1] = t0.y;
-        amx[0] = t1.x; amx[1] = t1.y;
-      } else {
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) { amn[c] = ai[c]; amx[c] = ai[H + c]; }
-      }
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        float g = gmean[c] * inv_d;
-        if ((amx[c] & 0x7f) == sl) g += gmax[c];
-        if (amn[c] == sl) g += gmin[c];
-        if (amx[c] & 0x80) g += gstd[c] * (m[c] - mu[c]) * inv_d * __frcp_rn(sg[c]);
-        dp[c] += g;
-#pragma unroll
-        for (int f = 0; f < FE; ++f) acc[c][f] = fmaf(g, ef[f], acc[c][f]);
-      }
-    }
-    const size_t prow = (size_t)prow_out * H + ch;  // degree-sorted row when dp_pos is given
-    store_vec<CPL>(dP + prow, dp);
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) bsum[c] += dp[c];
-  }
-  // block reduction of the dM_e and db_M partials in fixed warp order
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    redb[warp][lane][c] = bsum[c];
-#pragma unroll
-    for (int f = 0; f < FE; ++f) red[warp][lane][c * FE + f] = acc[c][f];
-  }
-  __syncthreads();
-  const int chunkC = 32 * CPL;
-  // partial layout: [block][H * Fe + H] = M_e's layout [H][Fe], then b_M's [H]
-  float *pb = partial + (size_t)blockIdx.x * H * (Fe + 1);
-  for (int t = threadIdx.x; t < chunkC * (Fe + 1); t += blockDim.x) {
-    if (t < chunkC * Fe) {
-      const int cc = t / Fe, f = t - cc * Fe;  // channel within chunk, feature
-      const int l = cc / CPL, c = cc - l * CPL;
-      float s = 0.f;
-      for (int w = 0; w < wpb; ++w) s += red[w][l][c * FE + f];
-      pb[(size_t)(blockIdx.y * chunkC + cc) * Fe + f] = s;
-    } else {
-      const int cc = t - chunkC * Fe, l = cc / CPL, c = cc - l * CPL;
-      float s = 0.f;
-      for (int w = 0; w < wpb; ++w) s += redb[w][l][c];
-      pb[(size_t)H * Fe + blockIdx.y * chunkC + cc] = s;
-    }
-  }
-}
-
-// fixed-order reduction of launch_agg_bwd's block partials (stride H * (Fe + 1)): dM_e
-// ([H][Fe]) and, when dbM is given, db_M ([H]); one warp per output element, lanes stride
-// over the blocks, then a fixed xor-shuffle tree (deterministic)
-__global__ void k_reduce_agg(const float *__restrict__ part, int nparts, int stride, int cnt_e,
-                             float *__restrict__ dMe, int cnt_b, float *__restrict__ dbM) {
-  pdl_enter();
-  const int lane = threadIdx.x & 31;
-  const int wpb = blockDim.x >> 5;
-  for (int e = blockIdx.x * wpb + (threadIdx.x >> 5); e < cnt_e + cnt_b; e += gridDim.x * wpb) {
-    float s = 0.f;
-    for (int p = lane; p < nparts; p += 32) s += part[(size_t)p * stride + e];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) {
-      if (e < cnt_e) dMe[e] = s;
-      else dbM[e - cnt_e] = s;
-    }
-  }
-}
-
-static int agg_bwd_blocks(const Caps &c) { return std::max(1, std::min(cdiv(c.maxN, 8), kSMs * 2)); }
-size_t agg_bwd_partial_floats(const Caps &c) { return (size_t)agg_bwd_blocks(c) * c.H * (c.Fe + 1); }
-
-
-template <int CPL, int FE>
-static void agg_bwd_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                           const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                           float *partial, const int *pos, const int *dp_pos) {
-  const dim3 grid(agg_bwd_blocks(c), c.H / (32 * CPL));
-  launch_ex(k_agg_bwd<CPL, FE>, grid, 32 * kAggBwdWarps, 0, st, blob, P, Me, bM, A, arg, dA, dP, partial, c.H,
-            pos, dp_pos);
-}
-
-void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe, const int *pos, const int *dp_pos) {
-  const int cpl = agg_cpl(c.H);
-  if (cpl == 2 && c.Fe == 4) agg_bwd_launch<2, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
-  else if (cpl == 2) agg_bwd_launch<2, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
-  else if (c.Fe == 4) agg_bwd_launch<1, 4>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
-  else agg_bwd_launch<1, 8>(st, c, blob, P, Me, bM, A, arg, dA, dP, partial, pos, dp_pos);
-  counted();
-  if (dMe) launch_reduce_dMe(st, c, partial, dMe);
-}
-
-void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe, float *dbM) {
-  const int ce = c.H * c.Fe, cb = dbM ? c.H : 0;
-  launch_ex(k_reduce_agg, std::max(1, std::min(cdiv(ce + cb, 8), kSMs * 4)), 256, 0, st, partial, agg_bwd_blocks(c),
-            c.H * (c.Fe + 1), ce, dMe, cb, dbM);
-  counted();
-}
-
 // ------------------------------------------------------------------ head
 // Block per graph: G_g = mean of X_L rows, hpre = W1 G + b1,
 // yhat = W2 ReLU(hpre) + b2, sqerr = (yhat - y)^2.

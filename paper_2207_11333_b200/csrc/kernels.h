@@ -19,19 +19,23 @@ struct Caps {
 // K1 layer 0: P[N,H] = x[N,F0] * Mx^T (SIMT; layers >= 1 use launch_d_proj)
 void launch_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx, float *P);
 
-// K2: fused edge gather + message + mean/min/max/std segmented reduction
+// aggregation kernels (agg.cu): one CTA per graph and channel chunk, the graph staged in
+// shared memory (requires c.H % 128 == 0)
+cudaError_t agg_configure();  // opt-in shared memory (once, outside graph capture)
+// K2: fused edge gather + message + mean/min/max/std segmented reduction; A row i is written
+// at the degree-sorted row pos[i]
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, float var_floor, float *A, uint8_t *arg,
-                    const int *pos = nullptr);  // pos: write A row i at pos[i] (degree-sorted)
-// K8: aggregation backward + scatter to sources; dM_e via block partials
+                    const float *bM, float var_floor, float *A, uint8_t *arg, const int *pos);
+// K8: aggregation backward + scatter to sources (dP row j at pos[j] when dp_pos != null, else
+// j; dp_pos must be pos or null); dM_e / db_M per-graph partials (launch_reduce_dMe sums them);
+// dm_scratch: agg_bwd_dm_floats floats, used only by graphs too large to stage
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *P, const float *Me,
-                    const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
-                    float *partial, float *dMe, const int *pos = nullptr,
-                    const int *dp_pos = nullptr);  // dp_pos: write dP row j at dp_pos[j]
-// dM_e = fixed-order sum of launch_agg_bwd's block partials (launch_agg_bwd does it when dMe != null)
-// (dbM != null: also db_M = sum_j dP_j from the same partials)
-void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe, float *dbM = nullptr);
+                    const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP, float *partial,
+                    const int *pos, const int *dp_pos, float *dm_scratch);
+// dM_e and db_M = fixed-order sums of launch_agg_bwd's per-graph partials (tcmn.cu)
+void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe, float *dbM);
 size_t agg_bwd_partial_floats(const Caps &c);
+size_t agg_bwd_dm_floats(const Caps &c);
 
 // K4/K5: pool + head forward, loss
 void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,

@@ -343,9 +343,10 @@ __global__ void __launch_bounds__(256) k_pad_x0(const uint8_t *__restrict__ blob
 // warp sums in order (deterministic for a given partial count).
 constexpr int RW = 8;
 struct RJob {
-  const float *part;  // [nparts][count]
+  const float *part;  // [nparts][stride], the first count of each row summed
   int nparts, count;  // count % 4 == 0
   float *out;
+  int stride;         // floats between parts (0 = count)
 };
 __device__ __forceinline__ void add4(float4 &s, float4 v) {
   s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
@@ -363,8 +364,9 @@ __global__ void __launch_bounds__(32 * RW) k_reduce_jobs(RJob j0, RJob j1, RJob 
   const bool ok = e < j.count;
   float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
   if (ok) {
+    const size_t stride = j.stride > 0 ? j.stride : j.count;
 #pragma unroll 4
-    for (int p = warp; p < j.nparts; p += RW) add4(s, ldg4(j.part + (size_t)p * j.count + e));
+    for (int p = warp; p < j.nparts; p += RW) add4(s, ldg4(j.part + (size_t)p * stride + e));
   }
   red[warp][lane] = s;
   __syncthreads();
@@ -486,9 +488,45 @@ void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
   const int with_cs = dbM ? 1 : 0;
   MnDMx op{blob, partial, cs, c.H, F, 0, with_cs};
   nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + with_cs));
-  const RJob j0{partial, kMnDMxSplits, count, dMx}, j1{cs, kMnDMxSplits, with_cs ? c.H : 0, dbM},
-      j2{nullptr, 0, 0, nullptr};
+  const RJob j0{partial, kMnDMxSplits, count, dMx, 0}, j1{cs, kMnDMxSplits, with_cs ? c.H : 0, dbM, 0},
+      j2{nullptr, 0, 0, nullptr, 0};
   launch_ex(k_reduce_jobs, reduce_blocks(j0) + (with_cs ? reduce_blocks(j1) : 0), 32 * RW, 0, st, j0, j1, j2);
+  g_launches += 1;
+}
+
+// fixed-order sums of the aggregation backward's per-graph partials (agg.cu): rows of H*Fe
+// dM_e entries then H db_M entries, one row per graph slot (up to thousands of rows). Block =
+// 32 warps x 32 lanes over 32 float4 columns: warp w sums rows w, w + 32, ... of its lane's
+// column (coalesced 512-byte row segments, four loads in flight), then warp 0 adds the 32
+// warp sums in order (deterministic).
+__global__ void __launch_bounds__(1024) k_reduce_rows32(const float *__restrict__ part, int nparts, int stride,
+                                                         int cnt_e, float *__restrict__ dMe, int cnt_b,
+                                                         float *__restrict__ dbM) {
+  pdl_enter();
+  __shared__ float4 red[32][33];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = 4 * (blockIdx.x * 32 + lane);
+  const bool ok = e < cnt_e + cnt_b;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (ok) {
+#pragma unroll 4
+    for (int p = warp; p < nparts; p += 32) add4(s, ldg4(part + (size_t)p * stride + e));
+  }
+  red[warp][lane] = s;
+  __syncthreads();
+  if (warp == 0 && ok) {
+    float4 t = red[0][lane];
+#pragma unroll
+    for (int w = 1; w < 32; ++w) add4(t, red[w][lane]);
+    float *o = e < cnt_e ? dMe + e : dbM + (e - cnt_e);
+    *reinterpret_cast<float4 *>(o) = t;
+  }
+}
+
+void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, float *dMe, float *dbM) {
+  const int stride = c.H * (c.Fe + 1), cnt_e = c.H * c.Fe, cnt_b = c.H;  // (both % 4 == 0: H % 128 == 0)
+  launch_ex(k_reduce_rows32, (cnt_e + cnt_b + 127) / 128, 1024, 0, st, partial, c.maxB, stride, cnt_e, dMe, cnt_b,
+            dbM);
   g_launches += 1;
 }
 

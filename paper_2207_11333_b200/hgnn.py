@@ -131,6 +131,7 @@ SIGNATURES = {
     "hg_p2p_emulate": [ctypes.POINTER(_P), _I32, ctypes.POINTER(hg_adamw)],
     "hg_bucket_layout": [ctypes.POINTER(hg_config), _I64P, _I32, _I32P],
     "hg_pack_threads_set": [_I32],
+    "hg_exchange_time": [_P, ctypes.POINTER(hg_adamw), _I32, ctypes.POINTER(ctypes.c_float)],
     "hg_launch_count": [_P, _I64P],
 }
 
@@ -522,6 +523,13 @@ class Context:
     def p2p_close(self):
         """Back to the NCCL exchange (hg_p2p_open(x, NULL)); gathers the sharded moments."""
         _check(_lib.hg_p2p_open(self.handle, None))
+
+    def exchange_time(self, iters: int = 20, **hyper) -> float:
+        """Mean device ms of this ctx's gradient exchange alone (hg_exchange_time; collective)."""
+        h = make_adamw(**hyper)
+        out = ctypes.c_float()
+        _check(_lib.hg_exchange_time(self.handle, ctypes.byref(h), int(iters), ctypes.byref(out)))
+        return out.value
 
     def allreduce_grads(self):
         _check(_lib.hg_allreduce_grads(self.handle))

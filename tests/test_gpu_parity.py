@@ -109,7 +109,9 @@ def _edge_case_store():
         (rng.integers(0, 3, (5, F)).astype(np.float32),                                # 4-cycle + pendant:
          [(0, 1, [1, 0, 0, 0]), (1, 2, [1, 0, 0, 0]), (2, 3, [1, 0, 0, 0]), (3, 0, [1, 0, 0, 0]),
           (0, 4, [0, 0, 0, 1])], 5.0),                                                  # automorphic ties
-    ]
+        (rng.integers(0, 3, (200, F)).astype(np.float32),                              # 200-node ring with
+         [(i, (i + 1) % 200, [0, 0, 1, 0]) for i in range(200)] + [(0, 100, [1, 0, 0, 0])], 6.0),  # a chord: too
+    ]                                                                                   # large to stage
     data = make_store(graphs, f_edge=4)
     data["f_node"] = F
     return data
@@ -118,15 +120,18 @@ def _edge_case_store():
 @pytest.mark.parametrize("H", [32, 55, 128, 256])
 def test_edge_cases_isolated_nodes_single_graph_max_degree(torch_cuda, H):
     """d = 0 nodes (C5), single-node graphs, a degree-127 hub (HG_MAX_DEGREE), a disconnected
-    graph and automorphic ties, in one ragged batch, through the product path: tcgen05 degree
-    classes (the hub is its own class), at padded (32, 55 -> 128), native (128: fused dX -> dA
-    kernel) and wide (256: separate dX / dA kernels) widths."""
+    graph, automorphic ties and a 200-node graph (larger than the aggregation kernels' shared-
+    memory staging: their global-memory path) in one ragged batch, through the product path:
+    tcgen05 degree classes (the hub is its own class), at padded (32, 55 -> 128), native (128:
+    fused dX -> dA kernel) and wide (256: separate dX / dA kernels) widths."""
     data = _edge_case_store()
-    ctx, cfg, delta = PT.make_ctx(data, 5, H, 2, seed=9)
-    res = PT.run_step_parity(data, [0, 1, 2, 3, 4], ctx, cfg, delta)
+    ctx, cfg, delta = PT.make_ctx(data, 6, H, 2, seed=9)
+    res = PT.run_step_parity(data, [0, 1, 2, 3, 4, 5], ctx, cfg, delta)
     print(H, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     PT.assert_parity(res)
     res = PT.run_step_parity(data, [2], ctx, cfg, delta)  # the hub alone
+    PT.assert_parity(res)
+    res = PT.run_step_parity(data, [5, 3], ctx, cfg, delta)  # the large graph first
     PT.assert_parity(res)
     res = PT.run_step_parity(data, [0], ctx, cfg, delta)  # one isolated node: every aggregate 0
     PT.assert_parity(res)

@@ -74,6 +74,55 @@ def test_p2_star_graph_all_aggregators_and_scalers():
     assert c["argmax"][0, 0] == 2 and c["argmin"][0, 0] == 0
 
 
+def test_p1s_self_term_worked_example():
+    """Model variant: the PNA self-term (x_i into M and U), hand-derived (tests/golden)."""
+    g = _golden("p1s_two_node_self_term.json")
+    st = make_store([(g["graph"]["x"], [(a, b, e) for a, b, e in g["graph"]["bonds"]], g["graph"]["y"])])
+    cfg = g["model"]
+    p = _params_from(g["params"])
+    assert [n for n, *_ in O.param_specs(cfg)] == list(g["params"])  # tensor order (C12 init keys)
+    b = O.pack(st, [0])
+    loss, yhat, cache = O.forward(p, b, cfg, cfg["delta"])
+    ex = g["expected"]
+    np.testing.assert_allclose(cache["layers"][0]["Z"][:, 0], ex["Z"], atol=1e-12)
+    assert abs(loss - ex["loss"]) < 1e-12
+    np.testing.assert_allclose(yhat, ex["yhat"], atol=1e-12)
+    grads = O.backward(p, b, cfg, cache)
+    assert set(grads) == set(p)
+    for k, v in ex["grads"].items():
+        np.testing.assert_allclose(grads[k], np.asarray(v), rtol=1e-9, atol=1e-14, err_msg=k)
+
+
+def test_p2s_five_scalers_worked_example():
+    """Model variant: PNA's linear / inverse_linear scalers beside C2's three, hand-derived."""
+    g = _golden("p2s_star_five_scalers.json")
+    st = make_store([(g["graph"]["x"], [(a, b, e) for a, b, e in g["graph"]["bonds"]], g["graph"]["y"])])
+    cfg = g["model"]
+    assert abs(O.degree_stat_linear(st) - cfg["delta_lin"]) < 1e-15
+    p = _params_from(g["params"])
+    b = O.pack(st, [0])
+    loss, yhat, cache = O.forward(p, b, cfg, cfg["delta"])
+    c, ex = cache["layers"][0], g["expected"]
+    np.testing.assert_allclose([s[0] for s in c["sv"]], ex["centre_scalers"], atol=1e-15)
+    np.testing.assert_allclose([s[1] for s in c["sv"]], ex["leaf_scalers"], atol=1e-15)
+    assert abs(c["Z"][0, 0] - ex["Z_centre"]) < 1e-12 and abs(c["Z"][2, 0] - ex["Z_leaf"]) < 1e-12
+    assert abs(yhat[0] - ex["yhat"]) < 1e-12
+    grads = O.backward(p, b, cfg, cache)
+    np.testing.assert_allclose(grads["conv0.b_U"], ex["grads"]["conv0.b_U"], rtol=1e-12)
+
+
+def test_linear_scalers_closed_forms():
+    """linear(d) * inverse_linear(d) = 1 for d > 0; every scaler is 1 at d = 0 (C5); with
+    delta_lin = delta = ln 2 at d = 1 linear = 1/ln 2."""
+    deg = np.array([0, 1, 2, 5, 127])
+    sv = O.scaler_values(deg, math.log(2), O.SCALERS, delta_lin=1.7)
+    np.testing.assert_allclose(sv[3][1:] * sv[4][1:], 1.0, rtol=1e-15)
+    assert all(s[0] == 1.0 for s in sv)
+    np.testing.assert_allclose(sv[3], [1.0, 1 / 1.7, 2 / 1.7, 5 / 1.7, 127 / 1.7], rtol=1e-15)
+    with pytest.raises(ValueError):
+        O.model_scalers({"scalers": ("amplification", "identity")})  # identity must come first
+
+
 # ---------------------------------------------------------------- P3 delta by hand
 def _benzene():
     # 6 aromatic C ring + 6 H (each C: 2 ring neighbours + 1 H -> degree 3; H degree 1)
@@ -229,14 +278,27 @@ def _jitter_params(p, seed, scale=0.3):
     return {k: v + scale * rng.standard_normal(v.shape) for k, v in p.items()}
 
 
+VARIANTS = {
+    "default": {},
+    "self_term": {"self_term": True},
+    "five_scalers": {"scalers": O.SCALERS, "delta_lin": 1.9},
+    "self_five": {"self_term": True, "scalers": ("identity", "linear", "amplification", "inverse_linear"),
+                  "delta_lin": 2.1},
+}
+
+
+@pytest.mark.parametrize("variant", list(VARIANTS))
 @pytest.mark.parametrize("seed", range(20))
-def test_p5_finite_difference_gradients(seed):
+def test_p5_finite_difference_gradients(seed, variant):
     """central FD (h=1e-6, f64) vs hand-derived gradients,
-    per-tensor max-scaled error <= 1e-5, on 20 random small graphs."""
+    per-tensor max-scaled error <= 1e-5, on 20 random small graphs; for the
+    default model and the model variants (self-term, extra scalers)."""
     import molgen
+    if variant != "default" and seed % 4:
+        pytest.skip("variants: every 4th seed")
     st = molgen.generate("tiny", 3, seed=100 + seed, first_id=0)
     st = molgen.perturb_features(st, seed=200 + seed, scale=0.2)
-    cfg = small_cfg(st["f_node"], 4, 2, Hf=3)
+    cfg = dict(small_cfg(st["f_node"], 4, 2, Hf=3), **VARIANTS[variant])
     p = _jitter_params(O.init_params(cfg, seed), seed)
     delta = 0.8 + 0.05 * seed
     b = O.pack(st, [0, 1, 2])
@@ -348,12 +410,22 @@ def _torch_model_loss(torch, params, st, ids, cfg, delta):
     deg = torch.zeros(N, dtype=dt).index_add_(0, d, torch.ones(len(d), dtype=dt))
     has = deg > 0
     logd = torch.log(deg + 1)
-    amp = torch.where(has, logd / delta, torch.ones_like(deg))
-    att = torch.where(has, delta / torch.where(has, logd, torch.ones_like(deg)), torch.ones_like(deg))
+    one = torch.ones_like(deg)
+    safe = torch.where(has, deg, one)
+    dlin = cfg.get("delta_lin", 1.0)
+    scal = {"identity": one,  # PNA (Corso et al. 2020) degree scalers, 1 on isolated nodes
+            "amplification": torch.where(has, logd / delta, one),
+            "attenuation": torch.where(has, delta / torch.where(has, logd, one), one),
+            "linear": torch.where(has, deg / dlin, one),
+            "inverse_linear": torch.where(has, dlin / safe, one)}
+    names = cfg.get("scalers", ("identity", "amplification", "attenuation"))
+    self_t = cfg.get("self_term", False)
     for l in range(cfg["layers"]):
         Mx, Me, bM = params[f"conv{l}.M_x"], params[f"conv{l}.M_e"], params[f"conv{l}.b_M"]
         U, bU = params[f"conv{l}.U"], params[f"conv{l}.b_U"]
         m = X[s] @ Mx.T + e @ Me.T + bM
+        if self_t:  # PyG PNAConv: the pre-transform also sees the destination's x_i
+            m = m + X[d] @ params[f"conv{l}.M_s"].T
         idx = d[:, None].expand(-1, H)
         summ = torch.zeros(N, H, dtype=dt).index_add_(0, d, m)
         mean = summ / deg.clamp(min=1)[:, None]
@@ -364,8 +436,11 @@ def _torch_model_loss(torch, params, st, ids, cfg, delta):
         std = torch.sqrt(torch.clamp(var, min=1e-10))
         std = torch.where(has[:, None], std, torch.zeros_like(std))
         A = torch.cat([mean, mn, mx, std], 1)
-        Sx = torch.cat([A, amp[:, None] * A, att[:, None] * A], 1)
-        X = torch.relu(Sx @ U.T + bU)
+        Sx = torch.cat([scal[nm][:, None] * A for nm in names], 1)
+        Z = Sx @ U.T + bU
+        if self_t:  # ... and the post-transform x_i beside the scaled aggregates
+            Z = Z + X @ params[f"conv{l}.U_x"].T
+        X = torch.relu(Z)
     gidt = torch.cat(gid)
     B = len(ids)
     cnt = torch.zeros(B, dtype=dt).index_add_(0, gidt, torch.ones(N, dtype=dt))
@@ -375,10 +450,12 @@ def _torch_model_loss(torch, params, st, ids, cfg, delta):
     return torch.mean((yhat - torch.tensor(ys, dtype=dt)) ** 2), yhat
 
 
-def test_p9i_torch_autograd_crosscheck(pcqm_small):
+@pytest.mark.parametrize("variant", list(VARIANTS))
+def test_p9i_torch_autograd_crosscheck(pcqm_small, variant):
     torch = pytest.importorskip("torch")
     st, cfg, p, delta = pcqm_small
-    p = _jitter_params(p, 3, 0.2)
+    cfg = dict(cfg, **VARIANTS[variant])
+    p = _jitter_params(O.init_params(cfg, 9), 3, 0.2)
     ids = [0, 4, 9, 2]
     tp = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in p.items()}
     tl, ty = _torch_model_loss(torch, tp, st, ids, cfg, delta)
