@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define HG_ABI_VERSION 1
+#define HG_ABI_VERSION 2
 
 typedef enum {
   HG_OK = 0,
@@ -73,6 +73,7 @@ typedef struct {
                                         per graph sorted by (src, dst), each bond in both directions */
   const float *edge_attr;            /* [num_edges][f_edge] */
   const float *y;                    /* [num_graphs] target (eV) */
+  const float *y_node;               /* [num_nodes] node-level targets (node-level head), nullable = 0 */
 } hg_store_desc;
 
 /* Validate and adopt a store. copy != 0: arrays are copied (caller may free on
@@ -91,6 +92,9 @@ hg_status hg_store_stats(const hg_store *s, int64_t *graphs, int64_t *nodes, int
 /* PNA degree statistic delta = mean over the nodes of graphs `ids` of ln(d+1),
  * float64. ids == NULL: all graphs. */
 hg_status hg_degree_stat(const hg_store *s, const int64_t *ids, int64_t n, double *delta);
+/* delta_lin = mean in-degree over the nodes of graphs `ids` (NULL: all), float64: the
+ * normaliser of the linear scalers (hg_config.delta_lin). */
+hg_status hg_degree_stat_linear(const hg_store *s, const int64_t *ids, int64_t n, double *delta_lin);
 
 /* ======================================================================
  * Sharding ("shuffled and disjointed subsets")
@@ -122,7 +126,23 @@ typedef struct {
                                         Degree-class slots = min(max_degree + 1, 32): a batch may hold
                                         at most that many DISTINCT node degrees (HG_E_DEGREE at pack
                                         time otherwise; molecules: <= 6). DESIGN.md §6. */
+  int32_t scalers;                   /* PNA degree scalers, HG_SCALER_* bit set (0 = the default
+                                        IDENTITY | AMPLIFICATION | ATTENUATION); identity
+                                        required. U holds 4 * popcount(scalers) blocks of H columns,
+                                        scaler-major in bit order, aggregator-minor. */
+  double delta_lin;                  /* mean in-degree over the training set (hg_degree_stat_linear):
+                                        normaliser of the LINEAR / INVERSE_LINEAR scalers (> 0 if used) */
+  float node_weight;                 /* HG_FLAG_NODE_HEAD: weight of the node-level MSE in the loss (>= 0) */
 } hg_config;
+
+/* Degree scalers (SURVEY §8(f) row 3 adds PNA's linear pair, DESIGN.md
+ * reading R-scalers): identity 1, amplification ln(d+1)/delta, attenuation delta/ln(d+1),
+ * linear d/delta_lin, inverse_linear delta_lin/d; every scaler is 1 at d = 0. */
+#define HG_SCALER_IDENTITY 1
+#define HG_SCALER_AMPLIFICATION 2
+#define HG_SCALER_ATTENUATION 4
+#define HG_SCALER_LINEAR 8
+#define HG_SCALER_INVERSE_LINEAR 16
 
 /* hg_config.flags: HG_FLAG_TF32 selects the reduced-precision GEMM mode (
  * PAPER.md:212): every tensor-core contraction runs ONE tf32 pass (operands truncated to
@@ -130,6 +150,18 @@ typedef struct {
  * (aggregation, head, loss, AdamW, the exchange) stays fp32. Its parity bars are looser
  * (DESIGN.md §3 "TF32 mode": forward 1e-2, gradients 5e-2 normwise). */
 #define HG_FLAG_TF32 1
+/* hg_config.flags: HG_FLAG_SELF_TERM selects the PNA self-term variant (SURVEY C1 / §8(f)
+ * row 3, reading R-self): the message is M [x_j || x_i || e_ij] + b_M and the update
+ * [scaled aggregates || x_i] [U | U_x]^T + b_U, with the extra parameters conv<l>.M_s [H, F_l]
+ * (after M_x) and conv<l>.U_x [H, F_l] (after U). Requires f_node <= hidden. */
+#define HG_FLAG_SELF_TERM 2
+/* hg_config.flags: HG_FLAG_NODE_HEAD adds a node-level head beside the graph head (PAPER.md:77
+ * "multitask prediction of hybrid node-level and graph-level properties", PAPER.md:144 atom-level
+ * properties; reading R-node-head): per node yhat_i = W2n ReLU(W1n x_L,i + b1n) + b2n
+ * (parameters head_n.W1 [fc_hidden, H], head_n.b1, head_n.W2 [1, fc_hidden], head_n.b2 after the
+ * graph head's), and loss = graph MSE + node_weight * mean over the batch's nodes of
+ * (yhat_i - y_node,i)^2 with the store's y_node targets. */
+#define HG_FLAG_NODE_HEAD 4
 
 /* Channel padding for widths that are not a multiple of the tensor-core tile (128),
  * e.g. the paper's H = 55 and H = 200 (SURVEY §8(d) "Padding
@@ -154,6 +186,7 @@ typedef struct {
  *   header   int32[16]: B, N, E, F0, Fe, then zeros
  *   graph_ptr int32[B+1]   cumulative node counts
  *   y         float[B]
+ *   y_node    float[N]     node-level targets (zeros when the store has none)
  *   rowptr    int32[N+1]   CSR over destination nodes
  *   col       int32[E]     in-neighbour ids, ascending within a row
  *   x         float[N*F0]
@@ -161,7 +194,7 @@ typedef struct {
  *   slot      uint8[E]     position of row inside col's row
  * each array starting at a 16-byte aligned offset given by hg_batch_offsets. */
 typedef struct {
-  int64_t graph_ptr, y, rowptr, col, x, eattr, slot, total;  /* byte offsets; total = blob size */
+  int64_t graph_ptr, y, y_node, rowptr, col, x, eattr, slot, total;  /* byte offsets; total = blob size */
 } hg_batch_offsets;
 hg_status hg_batch_offsets_get(int32_t B, int32_t N, int32_t E, int32_t f_node, int32_t f_edge,
                                hg_batch_offsets *off);
@@ -212,10 +245,12 @@ hg_status hg_opt_state_get(hg_ctx *x, float *m, float *v, int64_t *step, int32_t
 hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t step, int32_t on_device);
 
 /* Debug / parity views into the workspace: byte offset and size of a named
- * buffer. what: 0 = P_l [N,H], 1 = A_l [N,4H] (mean|min|max|std), 2 = arg_l
+ * buffer. what: 0 = P_l [N,H] ([N,2H] = [P | Q] with the self-term), 1 = A_l [N,4H]
+ * (mean|min|max|std, degree-sorted rows; [N,5H] with the self-term's x_i block), 2 = arg_l
  * [N,2H] u8 (argmin | argmax with bit7 = var>floor), 3 = X_{l+1} [N,H],
  * 4 = batch slot `layer` blob, 5 = yhat [B], 6 = loss [1], 7 = head hidden
- * pre-activation [B,Hf], 8 = params, 9 = grads, 10 = amp [N], 11 = att [N]. */
+ * pre-activation [B,Hf], 8 = params, 9 = grads, 10 = amp [N], 11 = att [N], 12 = node-level
+ * head yhat [N], 13 = its hidden pre-activation [N,Hf] (HG_FLAG_NODE_HEAD). */
 hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_t *offset, int64_t *bytes);
 
 /* Debug: copy batch slot `slot`'s packed blob (layout above; its header gives B, N, E) to

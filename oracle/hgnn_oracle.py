@@ -105,6 +105,11 @@ def param_specs(cfg: dict) -> list:
     out.append(("head.b1", (Hf,), 0, 0))
     out.append(("head.W2", (1, Hf), Hf, 1))
     out.append(("head.b2", (1,), 0, 0))
+    if cfg.get("node_head", False):  # node-level head (reading R-node-head): same shape, per node
+        out.append(("head_n.W1", (Hf, H), H, Hf))
+        out.append(("head_n.b1", (Hf,), 0, 0))
+        out.append(("head_n.W2", (1, Hf), Hf, 1))
+        out.append(("head_n.b2", (1,), 0, 0))
     return out
 
 
@@ -194,7 +199,7 @@ def pack(store: dict, ids) -> dict:
     if len(ids) == 0:
         raise ValueError("EmptyBatch (SPEC.md:279)")
     no, eo = store["node_offset"], store["edge_offset"]
-    xs, eas, srcs, dsts, ys, counts = [], [], [], [], [], [0]
+    xs, eas, srcs, dsts, ys, yns, counts = [], [], [], [], [], [], [0]
     base = 0
     for g in ids:
         n0, n1, e0, e1 = int(no[g]), int(no[g + 1]), int(eo[g]), int(eo[g + 1])
@@ -207,6 +212,7 @@ def pack(store: dict, ids) -> dict:
         dsts.append(d + base)
         eas.append(store["edge_attr"][e0:e1])
         ys.append(store["y"][g])
+        yns.append(store["y_node"][n0:n1] if "y_node" in store else np.zeros(n1 - n0, np.float32))
         base += n1 - n0
         counts.append(base)
     N = base
@@ -233,6 +239,7 @@ def pack(store: dict, ids) -> dict:
         "graph_ptr": np.asarray(counts, np.int32),
         "x": np.concatenate(xs).astype(np.float32),
         "y": np.asarray(ys, np.float32),
+        "y_node": np.concatenate(yns).astype(np.float32),
         "rowptr": rowptr.astype(np.int32),
         "col": col.astype(np.int32),
         "eattr": eattr,
@@ -364,6 +371,16 @@ def forward(params: dict, batch: dict, cfg: dict, delta: float):
     y = batch["y"].astype(np.float64)
     loss = float(np.mean((yhat - y) ** 2))
     head = dict(XL=X, G=G, hpre=hpre, hid=hid, yhat=yhat, ng=ng, gp=gp)
+    if cfg.get("node_head", False):
+        # node-level head ("hybrid node-level and graph-level properties";
+        # reading R-node-head): per node ReLU(X_L W1n^T + b1n) W2n^T + b2n, node MSE over the
+        # batch's nodes, added to the graph MSE with weight node_weight
+        hn_pre = X @ params["head_n.W1"].T + params["head_n.b1"]
+        hn = np.maximum(hn_pre, 0.0)
+        yn = (hn @ params["head_n.W2"].T)[:, 0] + params["head_n.b2"][0]
+        loss_n = float(np.mean((yn - batch["y_node"].astype(np.float64)) ** 2))
+        loss = loss + cfg.get("node_weight", 1.0) * loss_n
+        head.update(hn_pre=hn_pre, hn=hn, yn=yn, loss_n=loss_n)
     return loss, yhat, dict(layers=caches, head=head)
 
 
@@ -398,6 +415,16 @@ def backward(params: dict, batch: dict, cfg: dict, cache: dict, decisions: dict 
     gp, ng = h["gp"], h["ng"]
     gid = np.repeat(np.arange(B), ng)
     dX = dG[gid] / ng[gid][:, None]
+    if cfg.get("node_head", False):
+        Nn = len(h["yn"])
+        dyn = 2.0 * cfg.get("node_weight", 1.0) * (h["yn"] - batch["y_node"].astype(np.float64)) / Nn
+        g["head_n.W2"] = (dyn @ h["hn"])[None, :]
+        g["head_n.b2"] = np.array([dyn.sum()])
+        nmask = decisions.get("node_relu", h["hn_pre"] > 0)
+        dhn = dyn[:, None] * params["head_n.W2"][0][None, :] * nmask
+        g["head_n.W1"] = dhn.T @ h["XL"]
+        g["head_n.b1"] = dhn.sum(0)
+        dX = dX + dhn @ params["head_n.W1"]
     col = batch["col"].astype(np.int64)
     row, pos = batch["row"], batch["pos"]
     H = cfg["hidden"]
@@ -509,7 +536,7 @@ def train_step(params, state, store, ids, cfg, delta, hyper=None, world=1):
 # decision replay for parity
 # --------------------------------------------------------------------------
 def replay(cache: dict, gpu: list, tau_arg: float = 1e-6, tau_relu=1e-6, tau_head: float = 1e-6,
-           head_relu_gpu=None):
+           head_relu_gpu=None, node_relu_gpu=None):
     """Decision replay for parity: where several discrete
     decisions are correct, adopt the GPU's; check the rest.
 
@@ -604,6 +631,21 @@ def replay(cache: dict, gpu: list, tau_arg: float = 1e-6, tau_relu=1e-6, tau_hea
         bad += nb
         by["head_relu"] += nb
         dec["head_relu"] = np.where(valid, g, own)
+    if node_relu_gpu is not None:  # the node-level head's hidden units (variant), same rule
+        hp = cache["head"]["hn_pre"]
+        hs = np.abs(hp).max() if hp.size else 0.0
+        g = np.asarray(node_relu_gpu)
+        own = hp > 0
+        valid = np.where(g, hp >= -tau_head * hs, hp <= tau_head * hs)
+        diff = g != own
+        tie = np.abs(hp) <= TIE * hs
+        n += int((valid & diff & ~tie).sum())
+        nt += int((valid & diff & tie).sum())
+        ov["head_relu"] += int((valid & diff).sum())
+        nb = int((~valid & diff).sum())
+        bad += nb
+        by["head_relu"] += nb
+        dec["node_relu"] = np.where(valid, g, own)
     return dec, {"overrides": n, "tie_overrides": nt, "overrides_by": ov, "out_of_band": bad,
                  "out_of_band_by": by}
 

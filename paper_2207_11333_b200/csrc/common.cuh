@@ -13,7 +13,7 @@ namespace hg {
 struct BatchView {
   int B, N, E, F0, Fe;
   const int *gp;
-  const float *y;
+  const float *y, *y_node;
   const int *rowptr;
   const int *col;
   const float *x;
@@ -28,6 +28,7 @@ __device__ __forceinline__ BatchView load_batch(const uint8_t *blob) {
   const BatchOffsets o = batch_offsets(v.B, v.N, v.E, v.F0, v.Fe);
   v.gp = reinterpret_cast<const int *>(blob + o.graph_ptr);
   v.y = reinterpret_cast<const float *>(blob + o.y);
+  v.y_node = reinterpret_cast<const float *>(blob + o.y_node);
   v.rowptr = reinterpret_cast<const int *>(blob + o.rowptr);
   v.col = reinterpret_cast<const int *>(blob + o.col);
   v.x = reinterpret_cast<const float *>(blob + o.x);

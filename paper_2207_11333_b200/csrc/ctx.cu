@@ -39,9 +39,9 @@ struct Plan {
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
   size_t part = 0, part2 = 0, part3 = 0;  // split partials: spare, Gram (dU), dM_x
   size_t eval_acc = 0;
-  size_t u_off = 0;
+  size_t u_off = 0, ux_off = 0;
   int cmax = 0;  // degree-class slots
-  size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0;
+  size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0, gslice = 0;
   // residuals w - trunc19(w) of the weight operands (activations' lo terms are derived in
   // shared memory by the GEMM kernels)
   size_t Wf_lo = 0, WbT_lo = 0, ones = 0, xpad = 0;
@@ -50,6 +50,7 @@ struct Plan {
   size_t Mx_lo = 0, MxT = 0, MxT_lo = 0, mx_off = 0;
   size_t p2p = 0;  // P2PDev flags of the peer-memory gradient exchange
   size_t dm_scratch = 0;
+  size_t nh_hpre = 0, nh_yn = 0, nh_sq = 0, nh_dyn = 0, nh_dhn = 0, nh_part = 0;  // node-level head
   size_t total = 0;
 };
 
@@ -64,6 +65,10 @@ Plan make_plan(const hg_config &c) {
   const auto lay = param_layout(c);
   const size_t PB = sizeof(float) * (size_t)param_total(lay);
   const size_t N = c.max_nodes, H = c.hidden, B = c.max_graphs, Hf = c.fc_hidden;
+  Caps caps{c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge, c.hidden, c.fc_hidden};
+  caps.S = n_scalers(c);
+  caps.self_t = self_term(c) ? 1 : 0;
+  const size_t KA = caps.KA(), PW = caps.PW();
   p.params = take(PB);
   p.grads = take(PB);
   p.m = take(PB);
@@ -77,47 +82,57 @@ Plan make_plan(const hg_config &c) {
   p.amp = take(sizeof(float) * N);
   p.att = take(sizeof(float) * N);
   for (int l = 0; l < c.layers; ++l) {
-    p.P.push_back(take(sizeof(float) * N * H));
-    p.A.push_back(take(sizeof(float) * N * 4 * H));
+    p.P.push_back(take(sizeof(float) * N * PW));
+    p.A.push_back(take(sizeof(float) * N * KA));
     p.arg.push_back(take(N * 2 * H));
     p.X.push_back(take(sizeof(float) * N * H));
   }
   const size_t Fmax = std::max<size_t>(H, c.f_node);
   for (int l = 0; l < c.layers; ++l) {
     p.dZ.push_back(take(sizeof(float) * N * Fmax));
-    p.dPl.push_back(take(sizeof(float) * N * H));
+    p.dPl.push_back(take(sizeof(float) * N * PW));
   }
-  p.dA = take(sizeof(float) * N * 4 * H);
+  p.dA = take(sizeof(float) * N * KA);
   p.G = take(sizeof(float) * B * H);
   p.hpre = take(sizeof(float) * B * Hf);
   p.dhid = take(sizeof(float) * B * Hf);
   p.yhat = take(sizeof(float) * B);
   p.dy = take(sizeof(float) * B);
   p.sqerr = take(sizeof(float) * B);
-  Caps caps{c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge, c.hidden, c.fc_hidden};
   p.cmax = tc_num_classes(c.max_degree);
   p.u_off = take(sizeof(int64_t) * (size_t)c.layers);
+  p.ux_off = take(sizeof(int64_t) * (size_t)c.layers);
   p.perm = take(sizeof(int) * N);
   p.pos = take(sizeof(int) * N);
   p.deginfo = take(sizeof(DegInfo));
+  p.gslice = take(sizeof(int4) * B);
   p.tiles = take(sizeof(int4) * (size_t)tc_max_tiles(caps, p.cmax));
   p.splits = take(sizeof(int4) * (size_t)tc_max_splits(caps, p.cmax));
-  p.Wf = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-  p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-  p.Wf_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
-  p.WbT_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * 4 * H);
+  p.Wf = take(sizeof(float) * (size_t)c.layers * p.cmax * H * KA);
+  p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * KA);
+  p.Wf_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * KA);
+  p.WbT_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * KA);
   for (int l = 0; l < c.layers; ++l) {
     p.Xs.push_back(take(sizeof(float) * N * H));
     p.Xmask.push_back(take(sizeof(uint32_t) * N * ((H + 31) / 32)));
   }
   p.ones = take(sizeof(float) * N * 32);  // B operand of the column-sum tiles
   p.xpad = take(sizeof(float) * N * pad_x0_width(c.f_node));  // layer-0 features for the TMA dM_x Gram
-  p.Mx_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
-  p.MxT = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
-  p.MxT_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * H * H);
+  p.Mx_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * PW * H);
+  p.MxT = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * PW * H);
+  p.MxT_lo = take(sizeof(float) * (size_t)std::max(1, c.layers - 1) * PW * H);
   p.mx_off = take(sizeof(int64_t) * (size_t)c.layers);
-  const size_t pf = std::max({mn_gram_partial_floats(caps, p.cmax), mn_dmx_partial_floats(caps, H),
-                              mn_dmx_partial_floats(caps, c.f_node)});
+  size_t pf = std::max({mn_gram_partial_floats(caps, p.cmax), mn_dmx_partial_floats(caps, H),
+                        mn_dmx_partial_floats(caps, c.f_node)});
+  if (c.flags & HG_FLAG_NODE_HEAD) {
+    pf = std::max(pf, (size_t)32 * Hf * (H + 1));  // (the node head's W1n Gram: kMnDMxSplits x Hf x (H + 1))
+    p.nh_hpre = take(sizeof(float) * N * Hf);
+    p.nh_dhn = take(sizeof(float) * N * Hf);
+    p.nh_yn = take(sizeof(float) * N);
+    p.nh_sq = take(sizeof(float) * N);
+    p.nh_dyn = take(sizeof(float) * N);
+    p.nh_part = take(sizeof(float) * node_head_partial_floats(caps));
+  }
   p.part = take(sizeof(float) * 4);
   p.part2 = take(sizeof(float) * pf);
   p.part3 = take(sizeof(float) * pf);
@@ -261,6 +276,28 @@ int bucket_count(const hg_ctx *x);
 int bucket_closed_by(const hg_ctx *x, int l);
 
 // ---- the step's kernel sequence (enqueue only) ----
+// node-level head (HG_FLAG_NODE_HEAD): forward, and with bwd its gradient into dZ_L (after the
+// graph head wrote dZ_L), dyn and dhn for its parameter gradients (enqueue_node_head_grads)
+void enqueue_node_head(hg_ctx *x, cudaStream_t st, int slot, bool bwd) {
+  const Plan &p = x->plan;
+  const int L = x->cfg.layers;
+  launch_node_head(st, x->caps, x->b(p.slot[slot]), x->f(p.X[L - 1]), x->param("head_n.W1"), x->param("head_n.b1"),
+                   x->param("head_n.W2"), x->param("head_n.b2"), x->cfg.node_weight, x->f(p.nh_hpre), x->f(p.nh_yn),
+                   x->f(p.nh_sq), x->f(p.nh_dyn), x->f(p.nh_dhn), x->f(p.dZ[L - 1]),
+                   reinterpret_cast<const int *>(x->b(p.pos)), bwd);
+}
+void enqueue_node_head_grads(hg_ctx *x, cudaStream_t st, int slot, float *part) {
+  const Plan &p = x->plan;
+  const uint8_t *blob = x->b(p.slot[slot]);
+  const int L = x->cfg.layers, H = x->cfg.hidden, Hf = x->cfg.fc_hidden;
+  // dW1n = dhn^T X_L and db1n = sum dhn: the MN-major Gram over nodes (rows = Hf)
+  launch_mn_dMx(st, x->caps, blob, x->f(p.nh_dhn), x->f(p.X[L - 1]), H, H, x->f(p.ones), part,
+                x->grad("head_n.W1"), x->grad("head_n.b1"), Hf);
+  // dW2n = sum dyn ReLU(hpre), db2n = sum dyn (b2n follows W2n in the arena: Hf % 64 == 0)
+  launch_node_head_w2(st, x->caps, blob, x->f(p.nh_hpre), x->f(p.nh_dyn), x->f(p.nh_part));
+  launch_reduce_cols(st, x->f(p.nh_part), node_head_chunks(x->caps), Hf + 4, Hf + 4, x->grad("head_n.W2"));
+}
+
 void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, bool fuse_head_bwd = false) {
   const hg_config &c = x->cfg;
   g_gemm_passes = (c.flags & HG_FLAG_TF32) ? 1 : 3;
@@ -279,7 +316,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   phase(pr, HG_PHASE_SCALERS, [&] {
     launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
                    reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
-                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)), gram_ks(x->caps));
+                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)),
+                   reinterpret_cast<int4 *>(x->b(p.gslice)), scaler_mask(x->cfg), c.delta_lin, gram_ks(x->caps));
   });
   if (fork) cudaEventRecord(x->ev_start, st);
   // the prep branch is enqueued after layer 0's projection so that the main chain is the
@@ -291,15 +329,16 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
       // kernels are not kept off the SMs
       g_low_prio = fork;
       const int64_t *uo = reinterpret_cast<const int64_t *>(x->b(p.u_off));
-      launch_prep_W2(wst, x->caps, x->f(p.params), uo, 0, 1, p.cmax, dinfo, x->f(p.Wf), x->f(p.Wf_lo), x->f(p.WbT),
-                     x->f(p.WbT_lo));
+      const int64_t *uxo = reinterpret_cast<const int64_t *>(x->b(p.ux_off));
+      launch_prep_W2(wst, x->caps, x->f(p.params), uo, uxo, 0, 1, p.cmax, dinfo, x->f(p.Wf), x->f(p.Wf_lo),
+                     x->f(p.WbT), x->f(p.WbT_lo));
       if (fork) cudaEventRecord(x->ev_prep, wst);
       launch_prep_Mx(wst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
                      x->f(p.Mx_lo), x->f(p.MxT), x->f(p.MxT_lo));
       if (fork) cudaEventRecord(x->ev_prepmx, wst);
       if (c.layers > 1)
-        launch_prep_W2(wst, x->caps, x->f(p.params), uo, 1, c.layers, p.cmax, dinfo, x->f(p.Wf), x->f(p.Wf_lo),
-                       x->f(p.WbT), x->f(p.WbT_lo));
+        launch_prep_W2(wst, x->caps, x->f(p.params), uo, uxo, 1, c.layers, p.cmax, dinfo, x->f(p.Wf),
+                       x->f(p.Wf_lo), x->f(p.WbT), x->f(p.WbT_lo));
       launch_pad_x0(wst, x->caps, blob, x->f(p.xpad), x->dxda ? pos : nullptr);
       if (fork) cudaEventRecord(x->ev_prepw, wst);
       g_low_prio = false;
@@ -311,42 +350,49 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     phase(pr, HG_PHASE_PROJ, [&] {
       if (l > 0)
         launch_d_proj(st, x->caps, blob, x->f(p.X[l - 1]), F, x->param(lname(l, "M_x")),
-                      x->f(p.Mx_lo) + (size_t)(l - 1) * HH, x->f(p.P[l]));
+                      x->f(p.Mx_lo) + (size_t)(l - 1) * HH * (x->caps.self_t ? 2 : 1), x->f(p.P[l]));
       else
         launch_proj(st, x->caps, blob, nullptr, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
     });
     if (l == 0) enqueue_prep();
     phase(pr, HG_PHASE_AGG_FWD, [&] {
-      launch_agg_fwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
-                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), pos);
+      launch_agg_fwd(st, x->caps, blob, reinterpret_cast<const int4 *>(x->b(p.gslice)), x->f(p.P[l]),
+                     x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
+                     c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), pos, l == 0 ? nullptr : x->f(p.X[l - 1]), F);
     });
     if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_prep, 0);
     if (fork && l == 1) cudaStreamWaitEvent(st, x->ev_prepw, 0);
     phase(pr, HG_PHASE_UPDATE, [&] {
       const bool keep_sorted = x->dxda && l + 1 < c.layers;  // X_l operands of the fused dX -> dA kernel
+      const size_t wl = (size_t)l * p.cmax * c.hidden * x->caps.KA();  // layer l's class weights
       launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), reinterpret_cast<const int *>(x->b(p.perm)), dinfo,
-                          reinterpret_cast<const int4 *>(x->b(p.tiles)), x->f(p.Wf) + (size_t)l * p.cmax * 4 * HH,
-                          x->f(p.Wf_lo) + (size_t)l * p.cmax * 4 * HH, x->param(lname(l, "b_U")), x->f(p.X[l]),
+                          reinterpret_cast<const int4 *>(x->b(p.tiles)), x->f(p.Wf) + wl, x->f(p.Wf_lo) + wl,
+                          x->param(lname(l, "b_U")), x->f(p.X[l]),
                           keep_sorted ? x->f(p.Xs[l]) : nullptr,
                           keep_sorted ? reinterpret_cast<uint32_t *>(x->b(p.Xmask[l])) : nullptr);
     });
   }
   if (fork && c.layers < 2) cudaStreamWaitEvent(st, x->ev_prepw, 0);  // join side stream 2
   phase(pr, HG_PHASE_HEAD_FWD, [&] {
+    const bool nh = (c.flags & HG_FLAG_NODE_HEAD) != 0;
     if (fuse_head_bwd) {
       launch_head_fused(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
                         x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
                         x->f(p.sqerr), x->f(p.loss), x->f(p.dy), x->f(p.dhid), x->f(p.dZ[c.layers - 1]), pos);
+      if (nh) enqueue_node_head(x, st, slot, true);  // (adds its part of dZ_L after the graph head's)
       // the loss value is an output only: reduce it on the side stream (joined at the end of the backward)
       if (fork) {
         cudaEventRecord(x->ev_head, st);
         cudaStreamWaitEvent(x->side_stream, x->ev_head, 0);
       }
-      launch_loss(fork ? x->side_stream : st, blob, x->f(p.sqerr), x->f(p.loss));
-    } else
+      launch_loss(fork ? x->side_stream : st, blob, x->f(p.sqerr), x->f(p.loss), nh ? x->f(p.nh_sq) : nullptr,
+                  c.node_weight);
+    } else {
+      if (nh) enqueue_node_head(x, st, slot, false);
       launch_head_fwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.b1"),
                       x->param("head.W2"), x->param("head.b2"), x->f(p.G), x->f(p.hpre), x->f(p.yhat),
-                      x->f(p.sqerr), x->f(p.loss));
+                      x->f(p.sqerr), x->f(p.loss), nh ? x->f(p.nh_sq) : nullptr, c.node_weight);
+    }
   });
 }
 
@@ -366,17 +412,20 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   auto wait = [&](cudaStream_t s, cudaEvent_t ev) { if (fork) cudaStreamWaitEvent(s, ev, 0); };
   bool adam_forked = false;
   phase(pr, HG_PHASE_HEAD_BWD, [&] {
-    if (!head_done)  // dZ of the last layer on the main stream
+    if (!head_done) {  // dZ of the last layer on the main stream
       launch_head_bwd(st, x->caps, blob, x->f(p.X[c.layers - 1]), x->param("head.W1"), x->param("head.W2"),
                       x->f(p.G), x->f(p.hpre), x->f(p.yhat), x->f(p.dy), x->f(p.dhid), x->f(p.dZ[c.layers - 1]),
                       x->grad("head.W1"), x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"), false, pos,
                       false);
+      if (c.flags & HG_FLAG_NODE_HEAD) enqueue_node_head(x, st, slot, true);
+    }
     rec(x->ev_head, st);
     wait(side, x->ev_head);
     g_low_prio = fork;
     // head parameter gradients: off the critical chain
     launch_head_grads(side, x->caps, blob, x->f(p.G), x->f(p.hpre), x->f(p.dy), x->f(p.dhid), x->grad("head.W1"),
                       x->grad("head.b1"), x->grad("head.W2"), x->grad("head.b2"));
+    if (c.flags & HG_FLAG_NODE_HEAD) enqueue_node_head_grads(x, side, slot, x->f(p.part2));
     g_low_prio = false;
   });
   const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
@@ -400,7 +449,8 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       g_mn_grid_override = l == 0 ? kNumSMs : 0;
       launch_mn_dU_cls(side, x->caps, p.cmax, dZ, x->f(p.A[l]), x->f(p.ones), dinfo,
                        reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
-                       x->grad(lname(l, "b_U")));
+                       x->grad(lname(l, "b_U")), x->caps.self_t ? x->grad(lname(l, "U_x")) : nullptr,
+                       l == 0 ? c.f_node : c.hidden);
       g_mn_grid_override = 0;
     });
     rec(x->ev_gram[l], side);
@@ -408,11 +458,13 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     // ---- main: dA, aggregation backward
     phase(pr, HG_PHASE_DA, [&] {
       if (!(x->dxda && l + 1 < c.layers))  // (else dA_l came with dZ_l from layer l+1's fused dX -> dA)
-        launch_d_dA_cls(st, x->caps, p.cmax, dZ, perm, dinfo, tiles, x->f(p.WbT) + (size_t)l * p.cmax * 4 * HH,
-                        x->f(p.WbT_lo) + (size_t)l * p.cmax * 4 * HH, x->f(p.dA));
+        launch_d_dA_cls(st, x->caps, p.cmax, dZ, perm, dinfo, tiles,
+                        x->f(p.WbT) + (size_t)l * p.cmax * c.hidden * x->caps.KA(),
+                        x->f(p.WbT_lo) + (size_t)l * p.cmax * c.hidden * x->caps.KA(), x->f(p.dA));
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
-      launch_agg_bwd(st, x->caps, blob, x->f(p.P[l]), x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
+      launch_agg_bwd(st, x->caps, blob, reinterpret_cast<const int4 *>(x->b(p.gslice)), x->f(p.P[l]),
+                     x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
                      x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, pos, x->dxda ? pos : nullptr,
                      x->f(p.dm_scratch));
     });
@@ -457,8 +509,9 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
                       x->f(p.WbT_lo) + (size_t)(l - 1) * p.cmax * 4 * HH, perm, dinfo, tiles,
                       reinterpret_cast<const uint32_t *>(x->b(p.Xmask[l - 1])), dZn, x->f(p.dA));
         else
-          launch_d_dX(st, x->caps, blob, dP, x->f(p.MxT) + (size_t)(l - 1) * HH,
-                      x->f(p.MxT_lo) + (size_t)(l - 1) * HH, F, x->f(p.X[l - 1]), dZn, pos);
+          launch_d_dX(st, x->caps, blob, dP, x->f(p.MxT) + (size_t)(l - 1) * HH * (x->caps.self_t ? 2 : 1),
+                      x->f(p.MxT_lo) + (size_t)(l - 1) * HH * (x->caps.self_t ? 2 : 1), F, x->f(p.X[l - 1]), dZn, pos,
+                      x->caps.self_t ? x->f(p.dA) + 4 * c.hidden : nullptr);
       });
       if (early_adamw && fork && l == 1) {
         // every parameter of layers >= 1 and the head is final (and averaged) and no longer
@@ -649,6 +702,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   x->cfg_l = cl;
   x->padded = config_is_padded(cl);
   x->caps = Caps{c->max_graphs, c->max_nodes, c->max_edges, c->f_node, c->f_edge, c->hidden, c->fc_hidden, cl.hidden};
+  x->caps.S = n_scalers(*c);
+  x->caps.self_t = self_term(*c) ? 1 : 0;
   x->plan = plan;
   x->lay = param_layout(*c);
   x->n_params = param_total(x->lay);
@@ -710,16 +765,24 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   if ((e = agg_configure()) != cudaSuccess) return bail(e, "agg_configure");
   x->dxda = dxda_supported(x->caps);  // fused dX -> dA backward: +2.3% at config B
   {
-    std::vector<int64_t> uo, mo;
+    std::vector<int64_t> uo, mo, uxo((size_t)c->layers, 0);
     for (int l = 0; l < c->layers; ++l)
       for (auto &t : x->lay) {
         if (t.name == lname(l, "U")) uo.push_back(t.offset);
         if (t.name == lname(l, "M_x")) mo.push_back(t.offset);
+        if (t.name == lname(l, "U_x")) uxo[l] = t.offset;
+        // the kernels read [M_x; M_s] as one 2H-row matrix (projection, dX, dM): adjacent tensors
+        if (t.name == lname(l, "M_s") && t.offset != mo.back() + (int64_t)c->hidden * (l == 0 ? c->f_node : c->hidden)) {
+          hg_ctx_destroy(x);
+          return fail(HG_E_INVALID, "internal: M_s not adjacent to M_x");
+        }
       }
     std::vector<float> one((size_t)c->max_nodes * 32, 1.0f);
     if ((e = cudaMemcpyAsync(x->b(plan.u_off), uo.data(), sizeof(int64_t) * uo.size(), cudaMemcpyHostToDevice,
                              x->stream)) != cudaSuccess ||
         (e = cudaMemcpyAsync(x->b(plan.mx_off), mo.data(), sizeof(int64_t) * mo.size(), cudaMemcpyHostToDevice,
+                             x->stream)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(x->b(plan.ux_off), uxo.data(), sizeof(int64_t) * uxo.size(), cudaMemcpyHostToDevice,
                              x->stream)) != cudaSuccess ||
         (e = cudaMemcpyAsync(x->b(plan.ones), one.data(), sizeof(float) * one.size(), cudaMemcpyHostToDevice,
                              x->stream)) != cudaSuccess)
@@ -906,8 +969,8 @@ hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_
   const bool needs_layer = what >= 0 && what <= 3;
   if (needs_layer && (layer < 0 || layer >= c.layers)) return fail(HG_E_RANGE, "layer out of range");
   switch (what) {
-    case 0: *offset = p.P[layer]; *bytes = 4 * N * H; break;
-    case 1: *offset = p.A[layer]; *bytes = 16 * N * H; break;
+    case 0: *offset = p.P[layer]; *bytes = 4 * N * x->caps.PW(); break;
+    case 1: *offset = p.A[layer]; *bytes = 4 * N * x->caps.KA(); break;
     case 2: *offset = p.arg[layer]; *bytes = 2 * N * H; break;
     case 3: *offset = p.X[layer]; *bytes = 4 * N * H; break;
     case 4:
@@ -920,8 +983,10 @@ hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_
     case 9: *offset = p.grads; *bytes = 4 * x->n_params; break;
     case 10: *offset = p.amp; *bytes = 4 * N; break;
     case 11: *offset = p.att; *bytes = 4 * N; break;
+    case 12: if (!p.nh_yn) return fail(HG_E_RANGE, "no node head"); *offset = p.nh_yn; *bytes = 4 * N; break;
+    case 13: if (!p.nh_hpre) return fail(HG_E_RANGE, "no node head"); *offset = p.nh_hpre; *bytes = 4 * N * c.fc_hidden; break;
     // (debug views, not in the header: per-layer dP, dP_lo; padded layer-0 features)
-    case 100: if (layer < 0 || layer >= c.layers) return fail(HG_E_RANGE, "layer"); *offset = p.dPl[layer]; *bytes = 4 * N * H; break;
+    case 100: if (layer < 0 || layer >= c.layers) return fail(HG_E_RANGE, "layer"); *offset = p.dPl[layer]; *bytes = 4 * N * x->caps.PW(); break;
     case 102: if (!p.xpad) return fail(HG_E_RANGE, "no xpad"); *offset = p.xpad; *bytes = 4 * N * pad_x0_width(c.f_node); break;
     default: return fail(HG_E_RANGE, "unknown view %d", what);
   }

@@ -36,24 +36,29 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
                                                   float *__restrict__ amp, float *__restrict__ att,
                                                   int *__restrict__ perm, DegInfo *__restrict__ info,
                                                   int4 *__restrict__ tiles, int4 *__restrict__ splits,
-                                                  int *__restrict__ pos) {
+                                                  int *__restrict__ pos, int4 *__restrict__ gslice, int smask,
+                                                  double delta_lin) {
   pdl_enter();
   __shared__ int hist[kDeg], bstart[kDeg];
   __shared__ int wcnt[32][kDeg];  // per-warp degree counts, then per-warp bases within the degree
-  __shared__ float tamp[kDeg], tatt[kDeg];
+  __shared__ float tsc[kMaxScalers][kDeg];  // scaler k (bit order) of every degree
   const BatchView b = load_batch(blob);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid < kDeg) {  // scalers of every degree, fp64 as the oracle, stored fp32
-    if (tid == 0) {
-      tamp[0] = 1.0f;
-      tatt[0] = 1.0f;
-    } else {
-      const double ld = log((double)tid + 1.0);
-      tamp[tid] = (float)(ld / delta);
-      tatt[tid] = (float)(delta / ld);
-    }
+  if (tid < kDeg) {  // scalers of every degree, fp64 as the oracle, stored fp32; all 1 at d = 0
+    const double d = (double)tid, ld = log(d + 1.0);
+    tsc[0][tid] = 1.0f;
+    tsc[1][tid] = tid ? (float)(ld / delta) : 1.0f;
+    tsc[2][tid] = tid ? (float)(delta / ld) : 1.0f;
+    tsc[3][tid] = tid ? (float)(d / delta_lin) : 1.0f;
+    tsc[4][tid] = tid ? (float)(delta_lin / d) : 1.0f;
   }
   for (int e = tid; e < 32 * kDeg; e += blockDim.x) wcnt[e / kDeg][e % kDeg] = 0;
+  // per graph (n0, n1, e0, e1): the aggregation kernels' CTAs read their graph's node and edge
+  // ranges with one load instead of the dependent graph_ptr -> rowptr chain
+  for (int g = tid; g < b.B; g += blockDim.x) {
+    const int n0 = b.gp[g], n1 = b.gp[g + 1];
+    gslice[g] = make_int4(n0, n1, b.rowptr[n0], b.rowptr[n1]);
+  }
   __syncthreads();
   // warp w owns the contiguous node range [w*per, (w+1)*per), in rounds of 32 nodes; ranks
   // inside a round come from __match_any_sync (stable within the warp's range)
@@ -63,8 +68,8 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
     const int i = base + lane;
     const int d = i < w1 ? min(b.rowptr[i + 1] - b.rowptr[i], kDeg - 1) : -1;
     if (i < w1) {
-      amp[i] = tamp[d];
-      att[i] = tatt[d];
+      amp[i] = tsc[1][d];
+      att[i] = tsc[2][d];
     }
     const unsigned mask = __match_any_sync(0xffffffffu, d);
     const int rank = __popc(mask & ((1u << lane) - 1u));
@@ -91,8 +96,8 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
           info->deg[C] = d;
           info->start[C] = off;
           info->count[C] = hist[d];
-          info->amp[C] = tamp[d];
-          info->att[C] = tatt[d];
+          for (int q = 0, k = 0; q < kMaxScalers; ++q)
+            if (smask & (1 << q)) info->scal[k++][C] = tsc[q][d];
           // tiles and splits carry the class index c: the class weights W_c are indexed by it
           for (int r = 0; r < hist[d]; r += kTileRows)
             tiles[T++] = make_int4(C, off + r, min(kTileRows, hist[d] - r), 0);
@@ -135,9 +140,10 @@ int tc_max_tiles(const Caps &c, int cmax) { return (c.maxN + kTileRows - 1) / kT
 int tc_max_splits(const Caps &c, int cmax) { return (c.maxN + gram_ks(c) - 1) / gram_ks(c) + cmax; }
 
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
-                    DegInfo *info, int4 *tiles, int4 *splits, int *pos, int ks) {
+                    DegInfo *info, int4 *tiles, int4 *splits, int *pos, int4 *gslice, int smask, double delta_lin,
+                    int ks) {
   launch_ex(k_degsort, 1, 1024, 0, st, blob, delta, cmax, ks > 0 ? ks : kGramKS, amp, att, perm, info, tiles, splits,
-            pos);
+            pos, gslice, smask, delta_lin);
   g_launches += 1;
 }
 

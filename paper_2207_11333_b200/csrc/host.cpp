@@ -77,19 +77,30 @@ std::vector<TensorInfo> param_layout(const hg_config &c) {
     off += ((int64_t)rows * cols + 63) / 64 * 64;  // 256-byte aligned tensors
     v.push_back(t);
   };
+  const int S = n_scalers(c);
+  const bool st = self_term(c);
   for (int l = 0; l < c.layers; ++l) {
     const int Fl = l == 0 ? c.f_node : H;
     std::string p = "conv" + std::to_string(l) + ".";
-    add(p + "M_x", H, Fl, Fl + Fe, H);
-    add(p + "M_e", H, Fe, Fl + Fe, H);
+    const int fm = (st ? 2 * Fl : Fl) + Fe, fu = 4 * S * H + (st ? Fl : 0);  // fans of M, [U | U_x]
+    add(p + "M_x", H, Fl, fm, H);
+    if (st) add(p + "M_s", H, Fl, fm, H);
+    add(p + "M_e", H, Fe, fm, H);
     add(p + "b_M", 1, H, 0, 0);
-    add(p + "U", H, 12 * H, 12 * H, H);
+    add(p + "U", H, 4 * S * H, fu, H);
+    if (st) add(p + "U_x", H, Fl, fu, H);
     add(p + "b_U", 1, H, 0, 0);
   }
   add("head.W1", Hf, H, H, Hf);
   add("head.b1", 1, Hf, 0, 0);
   add("head.W2", 1, Hf, Hf, 1);
   add("head.b2", 1, 1, 0, 0);
+  if (c.flags & HG_FLAG_NODE_HEAD) {  // node-level head (reading R-node-head): the graph head's shape
+    add("head_n.W1", Hf, H, H, Hf);
+    add("head_n.b1", 1, Hf, 0, 0);
+    add("head_n.W2", 1, Hf, Hf, 1);
+    add("head_n.b2", 1, 1, 0, 0);
+  }
   return v;
 }
 
@@ -112,8 +123,25 @@ hg_status check_config(const hg_config *c) {
   if (!(c->var_floor > 0.0f)) return fail(HG_E_INVALID, "var_floor must be > 0");
   if (c->max_degree < 0 || c->max_degree > HG_MAX_DEGREE) return fail(HG_E_INVALID, "max_degree out of range");
   if (c->flags & ~HG_FLAGS_KNOWN) return fail(HG_E_INVALID, "unknown flags 0x%x", c->flags);
+  const int sm = scaler_mask(*c);
+  if (sm & ~31) return fail(HG_E_INVALID, "unknown scaler bits 0x%x", c->scalers);
+  if (!(sm & HG_SCALER_IDENTITY)) return fail(HG_E_INVALID, "the identity scaler is required (SPEC.md:327)");
+  if ((sm & (HG_SCALER_LINEAR | HG_SCALER_INVERSE_LINEAR)) && !(c->delta_lin > 0.0))
+    return fail(HG_E_INVALID, "delta_lin must be > 0 with the linear scalers");
+  if ((c->flags & HG_FLAG_NODE_HEAD) && !(c->node_weight >= 0.f))
+    return fail(HG_E_INVALID, "node_weight must be >= 0");
+  if ((c->flags & HG_FLAG_NODE_HEAD) && c->fc_hidden != c->hidden && c->fc_hidden % 128)
+    return fail(HG_E_INVALID, "the node-level head needs fc_hidden == hidden or a multiple of 128");
+  if (self_term(*c) && c->f_node > c->hidden)
+    return fail(HG_E_INVALID, "the self-term variant needs f_node <= hidden (got %d > %d)", c->f_node, c->hidden);
   return HG_OK;
 }
+
+int scaler_mask(const hg_config &c) {
+  return c.scalers ? c.scalers : (HG_SCALER_IDENTITY | HG_SCALER_AMPLIFICATION | HG_SCALER_ATTENUATION);
+}
+int n_scalers(const hg_config &c) { return __builtin_popcount((unsigned)scaler_mask(c) & 31u); }
+bool self_term(const hg_config &c) { return (c.flags & HG_FLAG_SELF_TERM) != 0; }
 
 bool config_is_padded(const hg_config &c) { return c.hidden % kChannelTile != 0; }
 
@@ -133,7 +161,7 @@ static void arena_map(const hg_config &logical, const float *src, float *dst, bo
   const auto ll = param_layout(logical), lp = param_layout(pc);
   for (size_t t = 0; t < ll.size(); ++t) {
     const TensorInfo &a = ll[t], &b = lp[t];
-    const int nb = a.name.size() >= 2 && a.name.compare(a.name.size() - 2, 2, ".U") == 0 ? 12 : 1;
+    const int nb = a.name.size() >= 2 && a.name.compare(a.name.size() - 2, 2, ".U") == 0 ? 4 * n_scalers(logical) : 1;
     const int W = a.cols / nb, Wp = b.cols / nb;
     for (int r = 0; r < a.rows; ++r)
       for (int q = 0; q < nb; ++q)
@@ -312,12 +340,15 @@ hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads,
     s->own_x.assign(d->x, d->x + s->N * s->F0);
     s->own_ea.assign(d->edge_attr, d->edge_attr + s->E * s->Fe);
     s->own_y.assign(d->y, d->y + G);
+    if (d->y_node) s->own_yn.assign(d->y_node, d->y_node + s->N);
     s->own_ei.assign(d->edge_index, d->edge_index + 2 * s->E);
     s->no = s->own_no.data(); s->eo = s->own_eo.data(); s->x = s->own_x.data();
     s->ea = s->own_ea.data(); s->y = s->own_y.data();
+    s->yn = d->y_node ? s->own_yn.data() : nullptr;
     s->src = s->own_ei.data(); s->dst = s->own_ei.data() + s->E;
   } else {
     s->no = d->node_offset; s->eo = d->edge_offset; s->x = d->x; s->ea = d->edge_attr; s->y = d->y;
+    s->yn = d->y_node;
     s->src = d->edge_index; s->dst = d->edge_index + s->E;
   }
   hg_status fst = store_finish(s, threads);
@@ -367,6 +398,21 @@ hg_status hg_degree_stat(const hg_store *s, const int64_t *ids, int64_t n, doubl
   return HG_OK;
 }
 
+hg_status hg_degree_stat_linear(const hg_store *s, const int64_t *ids, int64_t n, double *delta_lin) {
+  if (!s || !delta_lin) return fail(HG_E_INVALID, "null argument");
+  if (!ids) n = s->G;
+  if (n < 1) return fail(HG_E_EMPTY, "no graphs");
+  int64_t ne = 0, nn = 0;
+  for (int64_t q = 0; q < n; ++q) {
+    const int64_t g = ids ? ids[q] : q;
+    if (g < 0 || g >= s->G) return fail(HG_E_RANGE, "graph id %lld out of range", (long long)g);
+    ne += s->eo[g + 1] - s->eo[g];  // symmetric edge lists: sum of in-degrees = directed edges
+    nn += s->no[g + 1] - s->no[g];
+  }
+  *delta_lin = (double)ne / (double)nn;
+  return HG_OK;
+}
+
 hg_status hg_shard(uint64_t seed, int64_t epoch, int32_t rank, int32_t world, int64_t n,
                    int64_t *ids_out, int64_t *n_out) {
   if (world < 1 || rank < 0 || rank >= world) return fail(HG_E_INVALID, "rank/world out of range");
@@ -385,7 +431,7 @@ hg_status hg_batch_offsets_get(int32_t B, int32_t N, int32_t E, int32_t f_node, 
                                hg_batch_offsets *off) {
   if (!off || B < 0 || N < 0 || E < 0) return fail(HG_E_INVALID, "bad arguments");
   BatchOffsets o = batch_offsets(B, N, E, f_node, f_edge);
-  off->graph_ptr = o.graph_ptr; off->y = o.y; off->rowptr = o.rowptr; off->col = o.col;
+  off->graph_ptr = o.graph_ptr; off->y = o.y; off->y_node = o.y_node; off->rowptr = o.rowptr; off->col = o.col;
   off->x = o.x; off->eattr = o.eattr; off->slot = o.slot; off->total = o.total;
   return HG_OK;
 }
@@ -416,6 +462,7 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
   hdr[0] = B; hdr[1] = (int32_t)N; hdr[2] = (int32_t)E; hdr[3] = s->F0; hdr[4] = s->Fe;
   int32_t *gp = (int32_t *)(base + o.graph_ptr);
   float *y = (float *)(base + o.y);
+  float *yn = (float *)(base + o.y_node);
   int32_t *rp = (int32_t *)(base + o.rowptr);
   int32_t *col = (int32_t *)(base + o.col);
   float *x = (float *)(base + o.x);
@@ -448,6 +495,8 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
     const int64_t g = ids[b], nb = nbp[b], eb = ebp[b];
     const int64_t n0 = s->no[g], n = s->no[g + 1] - n0, e0 = s->eo[g], e = s->eo[g + 1] - e0;
     y[b] = s->y[g];
+    if (s->yn) std::memcpy(yn + nb, s->yn + n0, sizeof(float) * n);
+    else std::memset(yn + nb, 0, sizeof(float) * n);
     std::memcpy(x + nb * s->F0, s->x + n0 * s->F0, sizeof(float) * n * s->F0);
     std::memcpy(ea + eb * s->Fe, s->ea + e0 * s->Fe, sizeof(float) * e * s->Fe);
     std::memcpy(sl + eb, s->slot.data() + e0, (size_t)e);

@@ -31,7 +31,10 @@ void init_params_host(const hg_config &c, uint64_t seed, float *dst);
 // logical one exactly. The public arena (hg_param_info, get/set) stays logical.
 constexpr int kChannelTile = 128;
 constexpr int kClassSlots = 32;  // degree-class slots at most (kernels.h kMaxClasses)
-constexpr int HG_FLAGS_KNOWN = HG_FLAG_TF32;
+constexpr int HG_FLAGS_KNOWN = HG_FLAG_TF32 | HG_FLAG_SELF_TERM | HG_FLAG_NODE_HEAD;
+int scaler_mask(const hg_config &c);  // c.scalers, or the default identity | amplification | attenuation
+int n_scalers(const hg_config &c);
+bool self_term(const hg_config &c);
 hg_config padded_config(const hg_config &c);
 // degree classes a ctx of this configuration holds: min(max_degree + 1, kClassSlots); a batch
 // with more distinct node degrees is rejected when it is packed (HG_E_DEGREE)
@@ -57,10 +60,10 @@ struct hg_store {
   int64_t G = 0, N = 0, E = 0;
   int32_t F0 = 0, Fe = 0;
   const int64_t *no = nullptr, *eo = nullptr;
-  const float *x = nullptr, *ea = nullptr, *y = nullptr;
+  const float *x = nullptr, *ea = nullptr, *y = nullptr, *yn = nullptr;  // yn: node targets or null
   const int32_t *src = nullptr, *dst = nullptr;
   std::vector<int64_t> own_no, own_eo;
-  std::vector<float> own_x, own_ea, own_y;
+  std::vector<float> own_x, own_ea, own_y, own_yn;
   std::vector<int32_t> own_ei;
   std::vector<uint8_t> slot;
   int32_t max_nodes = 0, max_deg = 0;

@@ -154,8 +154,8 @@ struct OpProj {
 };
 void launch_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
                  float *P) {
-  OpProj op{blob, X, Mx, P, F, c.H};
-  run_gemm<true, true>(st, op, c.maxN, c.H, 1);
+  OpProj op{blob, X, Mx, P, F, c.PW()};  // (self-term: the 2H rows [M_x; M_s] -> [P | Q])
+  run_gemm<true, true>(st, op, c.maxN, c.PW(), 1);
 }
 
 // ------------------------------------------------------------------ head
@@ -459,15 +459,171 @@ __global__ void __launch_bounds__(256) k_head_fast(const uint8_t *__restrict__ b
   }
 }
 
+// loss = (1/B) sum_g sqerr_g [+ w (1/N) sum_i sqn_i: node-level head, R-node-head]
 __global__ void __launch_bounds__(256) k_loss(const uint8_t *__restrict__ blob, const float *__restrict__ sqerr,
-                                              float *__restrict__ loss) {
+                                              float *__restrict__ loss, const float *__restrict__ sqn, float w) {
   pdl_enter();
   __shared__ float red[256];
   const BatchView b = load_batch(blob);
   float part = 0.f;
   for (int g = threadIdx.x; g < b.B; g += blockDim.x) part += sqerr[g];
   const float s = block_sum_256(part, red);
-  if (threadIdx.x == 0) *loss = s / (float)b.B;
+  float sn = 0.f;
+  if (sqn) {
+    float pn = 0.f;
+    for (int i = threadIdx.x; i < b.N; i += blockDim.x) pn += sqn[i];
+    sn = block_sum_256(pn, red);
+  }
+  if (threadIdx.x == 0) *loss = s / (float)b.B + (sqn ? w * (sn / (float)b.N) : 0.f);
+}
+
+// ------------------------------------------------------------------ node-level head
+// Model variant (HG_FLAG_NODE_HEAD; reading R-node-head). Per node i:
+//   hn_pre = W1n x_i + b1n [Hf],  yn_i = W2n ReLU(hn_pre) + b2n,  sqn_i = (yn_i - y_node,i)^2;
+// training (BWD): dyn_i = 2 w (yn_i - y_node,i) / N, dhn = dyn_i W2n * [hn_pre > 0] (-> dhn_out for
+// the W1n Gram), dZ_L[pos[i]] += (W1n^T dhn) * [x_i > 0] (after the graph head wrote dZ_L).
+// One warp per group of NB nodes (their x rows and dhn staged in shared memory); lanes over
+// output rows in chunks of 128 (forward) and over input channels (backward); W1n through L1.
+constexpr int kNHNodes = 4;
+__global__ void __launch_bounds__(256) k_node_head(const uint8_t *__restrict__ blob, const float *__restrict__ XL,
+                                                   const float *__restrict__ W1, const float *__restrict__ b1,
+                                                   const float *__restrict__ W2, const float *__restrict__ b2, float w,
+                                                   int H, int Hf, float *__restrict__ hpre, float *__restrict__ yn,
+                                                   float *__restrict__ sqn, float *__restrict__ dyn,
+                                                   float *__restrict__ dhn, float *__restrict__ dZL,
+                                                   const int *__restrict__ pos, int bwd) {
+  constexpr int NB = kNHNodes;
+  extern __shared__ float nsm[];  // per warp: xs[NB][H], dh[NB][Hf]
+  pdl_enter();
+  const BatchView b = load_batch(blob);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  float *xs = nsm + (size_t)warp * NB * (H + Hf), *dh = xs + NB * H;
+  const float invN = 1.0f / (float)b.N;
+  for (int i0 = (blockIdx.x * wpb + warp) * NB; i0 < b.N; i0 += gridDim.x * wpb * NB) {
+    const int nn = min(NB, b.N - i0);
+    for (int e = lane; e < NB * H / 4; e += 32) {  // the group's x rows (zeros past the batch)
+      const int n = e / (H / 4), c = 4 * (e - n * (H / 4));
+      reinterpret_cast<float4 *>(xs)[e] = n < nn ? ldg4(XL + (size_t)(i0 + n) * H + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    __syncwarp();
+    float ydot[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) ydot[n] = 0.f;
+    for (int r0 = 0; r0 < Hf; r0 += 128) {  // 4 rows per lane: r = r0 + lane + 32 k
+      float acc[NB][4];
+#pragma unroll
+      for (int n = 0; n < NB; ++n)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[n][k] = 0.f;
+      for (int c = 0; c < H; c += 4) {
+        float4 wv[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int r = r0 + lane + 32 * k;
+          wv[k] = r < Hf ? ldg4(W1 + (size_t)r * H + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          const float4 xv = *reinterpret_cast<const float4 *>(xs + n * H + c);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            acc[n][k] = fmaf(wv[k].x, xv.x, acc[n][k]);
+            acc[n][k] = fmaf(wv[k].y, xv.y, acc[n][k]);
+            acc[n][k] = fmaf(wv[k].z, xv.z, acc[n][k]);
+            acc[n][k] = fmaf(wv[k].w, xv.w, acc[n][k]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = r0 + lane + 32 * k;
+        if (r >= Hf) continue;
+        const float bb = b1[r], w2 = W2[r];
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          const float hp = acc[n][k] + bb;
+          if (n < nn) hpre[(size_t)(i0 + n) * Hf + r] = hp;
+          ydot[n] = fmaf(w2, fmaxf(hp, 0.f), ydot[n]);
+        }
+      }
+    }
+    float dy[NB];
+#pragma unroll
+    for (int n = 0; n < NB; ++n) {
+      float v = ydot[n];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // fixed tree
+      const float y = v + b2[0];
+      const float e = n < nn ? y - b.y_node[i0 + n] : 0.f;
+      dy[n] = 2.0f * w * e * invN;
+      if (lane == 0 && n < nn) {
+        yn[i0 + n] = y;
+        sqn[i0 + n] = e * e;
+        if (bwd) dyn[i0 + n] = dy[n];
+      }
+    }
+    if (bwd) {
+      __syncwarp();  // (hpre rows of the group written by this warp)
+      for (int r = lane; r < Hf; r += 32) {
+        const float w2 = W2[r];
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          const float d = n < nn && hpre[(size_t)(i0 + n) * Hf + r] > 0.f ? dy[n] * w2 : 0.f;
+          dh[n * Hf + r] = d;
+          if (n < nn) dhn[(size_t)(i0 + n) * Hf + r] = d;
+        }
+      }
+      __syncwarp();
+      for (int c = 4 * lane; c < H; c += 128) {  // dX = W1n^T dhn, 4 channels per lane
+        float4 dx[NB];
+#pragma unroll
+        for (int n = 0; n < NB; ++n) dx[n] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < Hf; ++r) {
+          const float4 wv = ldg4(W1 + (size_t)r * H + c);
+#pragma unroll
+          for (int n = 0; n < NB; ++n) {
+            const float d = dh[n * Hf + r];
+            dx[n].x = fmaf(wv.x, d, dx[n].x); dx[n].y = fmaf(wv.y, d, dx[n].y);
+            dx[n].z = fmaf(wv.z, d, dx[n].z); dx[n].w = fmaf(wv.w, d, dx[n].w);
+          }
+        }
+#pragma unroll
+        for (int n = 0; n < NB; ++n) {
+          if (n >= nn) continue;
+          const float4 x = *reinterpret_cast<const float4 *>(xs + n * H + c);
+          float4 *o = reinterpret_cast<float4 *>(dZL + (size_t)pos[i0 + n] * H + c);
+          float4 z = *o;
+          z.x += x.x > 0.f ? dx[n].x : 0.f; z.y += x.y > 0.f ? dx[n].y : 0.f;
+          z.z += x.z > 0.f ? dx[n].z : 0.f; z.w += x.w > 0.f ? dx[n].w : 0.f;
+          *o = z;
+        }
+      }
+    }
+    __syncwarp();
+  }
+}
+
+// dW2n[r] = sum_i dyn_i ReLU(hpre_i[r]), db2n = sum_i dyn_i: per-block partials over fixed 64-node
+// chunks (thread per r), then k_reduce_rows32-style fixed-order sums (tcmn.cu launch_reduce_cols)
+constexpr int kNHChunk = 64;
+__global__ void __launch_bounds__(256) k_node_head_w2(const uint8_t *__restrict__ blob, const float *__restrict__ hpre,
+                                                      const float *__restrict__ dyn, int Hf, int nchunks,
+                                                      float *__restrict__ part) {
+  pdl_enter();
+  const int N = batch_N(blob);
+  const int stride = Hf + 4;  // per chunk: Hf weights, db2n, 3 pad (float4 rows)
+  for (int ch = blockIdx.x; ch < nchunks; ch += gridDim.x) {
+    const int i0 = ch * kNHChunk, i1 = min(N, i0 + kNHChunk);
+    for (int r = threadIdx.x; r < stride; r += blockDim.x) {
+      float s = 0.f;
+      if (r < Hf) {
+        for (int i = i0; i < i1; ++i) s = fmaf(dyn[i], fmaxf(hpre[(size_t)i * Hf + r], 0.f), s);
+      } else if (r == Hf) {
+        for (int i = i0; i < i1; ++i) s += dyn[i];
+      }
+      part[(size_t)ch * stride + r] = s;
+    }
+  }
 }
 
 template <bool FWD, bool BWD>
@@ -491,7 +647,9 @@ static void head_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, con
             dhid, dZL, c.H, c.Hf, in_smem, pos);
 }
 
+size_t node_head_smem(const Caps &c);
 void head_configure(const Caps &c) {  // outside graph capture: opt into large dynamic smem
+  cudaFuncSetAttribute(k_node_head, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)node_head_smem(c));
   const size_t base = sizeof(float) * (c.H + 2 * c.Hf + 256);
   const size_t w1 = sizeof(float) * (size_t)c.Hf * c.H;
   const int v = (int)(base + (base + w1 <= 200 * 1024 ? w1 : 0));
@@ -502,10 +660,30 @@ void head_configure(const Caps &c) {  // outside graph capture: opt into large d
 
 void launch_head_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *b1, const float *W2, const float *b2, float *G, float *hpre, float *yhat,
-                     float *sqerr, float *loss) {
+                     float *sqerr, float *loss, const float *sqn, float w) {
   head_launch<true, false>(st, c, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, nullptr, nullptr, nullptr);
   counted();
-  launch_ex(k_loss, 1, 256, 0, st, blob, sqerr, loss);
+  launch_ex(k_loss, 1, 256, 0, st, blob, sqerr, loss, sqn, w);
+  counted();
+}
+
+size_t node_head_smem(const Caps &c) { return sizeof(float) * 8 * kNHNodes * (c.H + c.Hf); }
+int node_head_chunks(const Caps &c) { return (c.maxN + kNHChunk - 1) / kNHChunk; }
+size_t node_head_partial_floats(const Caps &c) { return (size_t)node_head_chunks(c) * (c.Hf + 4); }
+
+void launch_node_head(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
+                      const float *b1, const float *W2, const float *b2, float w, float *hpre, float *yn, float *sqn,
+                      float *dyn, float *dhn, float *dZL, const int *pos, bool bwd) {
+  const int groups = cdiv(c.maxN, kNHNodes);
+  launch_ex(k_node_head, std::max(1, std::min(cdiv(groups, 8), kSMs * 4)), 256, node_head_smem(c), st, blob, XL, W1,
+            b1, W2, b2, w, c.H, c.Hf, hpre, yn, sqn, dyn, dhn, dZL, pos, bwd ? 1 : 0);
+  counted();
+}
+
+void launch_node_head_w2(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *hpre, const float *dyn,
+                         float *part) {
+  launch_ex(k_node_head_w2, std::min(node_head_chunks(c), kSMs * 4), 256, 0, st, blob, hpre, dyn, c.Hf,
+            node_head_chunks(c), part);
   counted();
 }
 
@@ -516,8 +694,8 @@ void launch_head_fused(cudaStream_t st, const Caps &c, const uint8_t *blob, cons
   counted();
 }
 
-void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float *loss) {
-  launch_ex(k_loss, 1, 256, 0, st, blob, sqerr, loss);
+void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float *loss, const float *sqn, float w) {
+  launch_ex(k_loss, 1, 256, 0, st, blob, sqerr, loss, sqn, w);
   counted();
 }
 

@@ -17,7 +17,7 @@ HG_HD int64_t align16(int64_t v) { return (v + 15) & ~int64_t(15); }
 HG_HD int64_t align256(int64_t v) { return (v + 255) & ~int64_t(255); }
 
 struct BatchOffsets {
-  int64_t graph_ptr, y, rowptr, col, x, eattr, slot, total;
+  int64_t graph_ptr, y, y_node, rowptr, col, x, eattr, slot, total;
 };
 
 // offsets of each array inside a batch blob with B graphs, N nodes, E edges
@@ -26,6 +26,7 @@ HG_HD BatchOffsets batch_offsets(int64_t B, int64_t N, int64_t E, int64_t F0, in
   int64_t p = kHeaderInts * 4;
   o.graph_ptr = p; p = align16(p + 4 * (B + 1));
   o.y = p;         p = align16(p + 4 * B);
+  o.y_node = p;    p = align16(p + 4 * N);
   o.rowptr = p;    p = align16(p + 4 * (N + 1));
   o.col = p;       p = align16(p + 4 * E);
   o.x = p;         p = align16(p + 4 * N * F0);

@@ -291,6 +291,7 @@ struct TUpdC {
   const int *perm; const DegInfo *info; const int4 *tiles; const float *bU; float *X1; int H; int items_cap;
   float *X1s;        // optional: the same rows in degree-sorted order (backward dX/dM_x operands)
   uint32_t *X1mask;  // optional: ReLU mask bits of the sorted rows, [rows][H/32] words
+  int KA;            // contraction length: 4H aggregates (+ H: the self-term's x_i block)
   int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     const int nt = H / BN, ti = t / nt;
@@ -300,7 +301,7 @@ struct TUpdC {
     row_end = tl.y + tl.z;
     n0 = (t % nt) * BN;
     by = tl.x * H + n0;
-    ke = 4 * H;
+    ke = KA;
     return true;
   }
   struct Pre { int node; float4 b; };
@@ -329,15 +330,16 @@ template <int BN_>
 struct TDAC {
   static constexpr int BN = BN_;
   const int *perm; const DegInfo *info; const int4 *tiles; float *dA; int H; int items_cap;
+  int KA;  // output width: 4H (+ H: the self-term's dX_self = dZ U_x block)
   int row_end;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
-    const int nt = 4 * H / BN, ti = t / nt;
+    const int nt = KA / BN, ti = t / nt;
     if (ti >= info->T) return false;
     const int4 tl = tiles[ti];
     m0 = ay = tl.y;
     row_end = tl.y + tl.z;
     n0 = (t % nt) * BN;
-    by = tl.x * 4 * H + n0;
+    by = tl.x * KA + n0;
     ke = H;
     return true;
   }
@@ -345,7 +347,7 @@ struct TDAC {
   __device__ Pre pre(int m, int) const { return Pre{m < row_end ? perm[m] : 0}; }
   __device__ void emit(int m, int n, float4 v, const Pre &p) const {
     if (m >= row_end) return;
-    *reinterpret_cast<float4 *>(dA + (size_t)p.node * 4 * H + n) = v;
+    *reinterpret_cast<float4 *>(dA + (size_t)p.node * KA + n) = v;
   }
 };
 
@@ -354,10 +356,11 @@ template <int BN_>
 struct TProj {
   static constexpr int BN = BN_;
   const uint8_t *blob; float *P; int F, H; int items_cap;
+  int PW;  // output width: H (+ H: the self-term's Q = X M_s^T)
   int N;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     N = batch_N(blob);
-    const int nt = H / BN;
+    const int nt = PW / BN;
     m0 = ay = (t / nt) * T_BM;
     n0 = by = (t % nt) * BN;
     ke = F;
@@ -367,7 +370,7 @@ struct TProj {
   __device__ Pre pre(int, int) const { return Pre{}; }
   __device__ void emit(int m, int n, float4 v, const Pre &) const {
     if (m >= N) return;
-    *reinterpret_cast<float4 *>(P + (size_t)m * H + n) = v;
+    *reinterpret_cast<float4 *>(P + (size_t)m * PW + n) = v;
   }
 };
 
@@ -376,21 +379,26 @@ template <int BN_>
 struct TDX {
   static constexpr int BN = BN_;
   const uint8_t *blob; const float *Xl; float *dZ; const int *pos; int H, F; int items_cap;
+  int PW;                // contraction length: H (dP) or 2H ([dP | dQ] . [M_x; M_s], self-term)
+  const float *dXself;   // self-term: dX_self rows (the dA buffer's x block, row stride 5H), else null
   int N;
   __device__ bool tile(int t, int &m0, int &n0, int &ke, int &ay, int &by) {
     N = batch_N(blob);
     const int nt = F / BN;
     m0 = ay = (t / nt) * T_BM;
     n0 = by = (t % nt) * BN;
-    ke = H;
+    ke = PW;
     return m0 < N;
   }
-  struct Pre { int row; float4 x; };
+  struct Pre { int row; float4 x, s; };
   __device__ Pre pre(int m, int n) const {
-    return m < N ? Pre{pos[m], ldg4(Xl + (size_t)m * F + n)} : Pre{0, make_float4(0.f, 0.f, 0.f, 0.f)};
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    return m < N ? Pre{pos[m], ldg4(Xl + (size_t)m * F + n), dXself ? ldg4(dXself + (size_t)m * 5 * H + n) : z}
+                 : Pre{0, z, z};
   }
   __device__ void emit(int m, int n, float4 v, const Pre &p) const {
     if (m >= N) return;
+    v.x += p.s.x; v.y += p.s.y; v.z += p.s.z; v.w += p.s.w;
     const float4 x = p.x;
     const float4 z = make_float4(x.x > 0.f ? v.x : 0.f, x.y > 0.f ? v.y : 0.f, x.z > 0.f ? v.z : 0.f,
                                  x.w > 0.f ? v.w : 0.f);
@@ -635,12 +643,13 @@ __global__ void __launch_bounds__(XD_THREADS, 1) k_dxda(const __grid_constant__ 
 }
 
 // ---------------------------------------------------------------- weight preparation
-// per layer l >= 1: Mx_lo = lo(M_x) [H][F]; MxT = M_x^T [F][H] and its lo
+// per layer l >= 1: Mx_lo = lo(M) [H][F]; MxT = M^T [F][H] and its lo, where M is the R = H
+// rows of M_x, or (self-term) the R = 2H rows [M_x; M_s] (adjacent in the parameter arena)
 __global__ void k_prep_Mx(const float *__restrict__ params, const int64_t *__restrict__ mx_off, int L, int H, int F,
                           float *__restrict__ Mx_lo, float *__restrict__ MxT, float *__restrict__ MxT_lo) {
   pdl_enter();
   __shared__ float tile[32][33];
-  const int tf = F / 32, th = H / 32, per = tf * th;
+  const int tf = F / 32, th = H / 32, per = tf * th;  // (H here: the R rows)
   for (int t = blockIdx.x; t < (L - 1) * per; t += gridDim.x) {
     const int l = 1 + t / per, tt = t % per, h0 = (tt / tf) * 32, f0 = (tt % tf) * 32;
     const float *M = params + mx_off[l];
@@ -665,12 +674,15 @@ __global__ void k_prep_Mx(const float *__restrict__ params, const int64_t *__res
 // class weights of the batch's degree classes with their lo terms: Wf[c] = W_c [H][4H],
 // WbT[c] = W_c^T [4H][H], W_c = U_id + amp(d_c) U_amp + att(d_c) U_att (scalers from the
 // class table k_degsort wrote; slots c >= info->C are not touched)
-__global__ void k_prep_W2(const float *__restrict__ params, const int64_t *__restrict__ u_off, int l0, int l1, int H,
-                          int cmax, const DegInfo *__restrict__ info, float *__restrict__ Wf, float *__restrict__ Wf_lo,
+// (S scalers: W_c = sum_s scal[s][c] U_s over the 4H aggregate columns, s in U's block order;
+// self-term: columns [4H, 5H) hold U_x [H][Fl] (layer input width Fl), zero-padded to H)
+__global__ void k_prep_W2(const float *__restrict__ params, const int64_t *__restrict__ u_off,
+                          const int64_t *__restrict__ ux_off, int l0, int l1, int H, int S, int F0, int cmax,
+                          const DegInfo *__restrict__ info, float *__restrict__ Wf, float *__restrict__ Wf_lo,
                           float *__restrict__ WbT, float *__restrict__ WbT_lo) {
   pdl_enter();
   __shared__ float tile[32][33];
-  const int K = 4 * H, tk = K / 32, th = H / 32;
+  const int K4 = 4 * H, K = ux_off ? 5 * H : K4, tk = K / 32, th = H / 32;
   const int per_cls = tk * th;
   const int C = info->C;
   for (int t = blockIdx.x; t < (l1 - l0) * cmax * per_cls; t += gridDim.x) {
@@ -679,12 +691,20 @@ __global__ void k_prep_W2(const float *__restrict__ params, const int64_t *__res
     if (c >= C) continue;  // uniform per block
     const int tt = t % per_cls, h0 = (tt / tk) * 32, k0 = (tt % tk) * 32;
     const float *U = params + u_off[l];
-    const float a = info->amp[c], b = info->att[c];
     const size_t base = ((size_t)l * cmax + c) * H * K;
+    const int Fl = l == 0 ? F0 : H;
     for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-      const float *u = U + (size_t)(h0 + r) * 3 * K + k0 + threadIdx.x;
-      const float w = u[0] + a * u[K] + b * u[2 * K];
-      const size_t o = base + (size_t)(h0 + r) * K + k0 + threadIdx.x;
+      const int k = k0 + threadIdx.x;
+      float w;
+      if (k < K4) {
+        const float *u = U + (size_t)(h0 + r) * S * K4 + k;
+        w = u[0];
+        for (int q = 1; q < S; ++q) w += info->scal[q][c] * u[(size_t)q * K4];
+      } else {  // self-term block: U_x, not scaled
+        const int kx = k - K4;
+        w = kx < Fl ? params[ux_off[l] + (size_t)(h0 + r) * Fl + kx] : 0.f;
+      }
+      const size_t o = base + (size_t)(h0 + r) * K + k;
       Wf[o] = w;
       Wf_lo[o] = lo_of(w);
       tile[r][threadIdx.x] = w;
@@ -772,34 +792,35 @@ template <int BN>
 void update_bn(cudaStream_t st, const Caps &c, int cmax, const float *A, const int *perm, const DegInfo *info,
                const int4 *tiles, const float *Wf, const float *Wf_lo, const float *bU, float *X1, float *X1s,
                uint32_t *X1mask) {
-  const int K = 4 * c.H;
+  const int K = c.KA();
   const CUtensorMap a = map2d(A, c.maxN, K, T_BM);
   const TmaMaps mp{a, a, map2d(Wf, (uint64_t)cmax * c.H, K, BN), map2d(Wf_lo, (uint64_t)cmax * c.H, K, BN)};
-  TUpdC<BN> op{perm, info, tiles, bU, X1, c.H, 0, X1s, X1mask, 0};
+  TUpdC<BN> op{perm, info, tiles, bU, X1, c.H, 0, X1s, X1mask, K, 0};
   trun(st, mp, op, tc_max_tiles(c, cmax) * (c.H / BN));
 }
 template <int BN>
 void dA_bn(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const int *perm, const DegInfo *info,
            const int4 *tiles, const float *WbT, const float *WbT_lo, float *dA) {
   const CUtensorMap a = map2d(dZ, c.maxN, c.H, T_BM);
-  const TmaMaps mp{a, a, map2d(WbT, (uint64_t)cmax * 4 * c.H, c.H, BN), map2d(WbT_lo, (uint64_t)cmax * 4 * c.H, c.H, BN)};
-  TDAC<BN> op{perm, info, tiles, dA, c.H, 0, 0};
-  trun(st, mp, op, tc_max_tiles(c, cmax) * (4 * c.H / BN));
+  const int K = c.KA();
+  const TmaMaps mp{a, a, map2d(WbT, (uint64_t)cmax * K, c.H, BN), map2d(WbT_lo, (uint64_t)cmax * K, c.H, BN)};
+  TDAC<BN> op{perm, info, tiles, dA, c.H, 0, K, 0};
+  trun(st, mp, op, tc_max_tiles(c, cmax) * (K / BN));
 }
 template <int BN>
 void proj_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
              const float *Mx_lo, float *P) {
   const CUtensorMap a = map2d(X, c.maxN, F, T_BM);
-  const TmaMaps mp{a, a, map2d(Mx, c.H, F, BN), map2d(Mx_lo, c.H, F, BN)};
-  TProj<BN> op{blob, P, F, c.H, 0, 0};
-  trun(st, mp, op, mt(c.maxN) * (c.H / BN));
+  const TmaMaps mp{a, a, map2d(Mx, c.PW(), F, BN), map2d(Mx_lo, c.PW(), F, BN)};
+  TProj<BN> op{blob, P, F, c.H, 0, c.PW(), 0};
+  trun(st, mp, op, mt(c.maxN) * (c.PW() / BN));
 }
 template <int BN>
 void dX_bn(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *MxT, const float *MxT_lo,
-           int F, const float *Xl, float *dZ, const int *pos) {
-  const CUtensorMap a = map2d(dP, c.maxN, c.H, T_BM);
-  const TmaMaps mp{a, a, map2d(MxT, F, c.H, BN), map2d(MxT_lo, F, c.H, BN)};
-  TDX<BN> op{blob, Xl, dZ, pos, c.H, F, 0, 0};
+           int F, const float *Xl, float *dZ, const int *pos, const float *dXself) {
+  const CUtensorMap a = map2d(dP, c.maxN, c.PW(), T_BM);
+  const TmaMaps mp{a, a, map2d(MxT, F, c.PW(), BN), map2d(MxT_lo, F, c.PW(), BN)};
+  TDX<BN> op{blob, Xl, dZ, pos, c.H, F, 0, c.PW(), dXself, 0};
   trun(st, mp, op, mt(c.maxN) * (F / BN));
 }
 }  // namespace
@@ -845,14 +866,14 @@ void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
 }
 
 void launch_d_dX(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *MxT,
-                 const float *MxT_lo, int F, const float *Xl, float *dZ, const int *pos) {
+                 const float *MxT_lo, int F, const float *Xl, float *dZ, const int *pos, const float *dXself) {
   const int bn = bn_auto(c);
-  if (bn == 32) dX_bn<32>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos);
-  else if (bn == 128) dX_bn<128>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos);
-  else dX_bn<64>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos);
+  if (bn == 32) dX_bn<32>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos, dXself);
+  else if (bn == 128) dX_bn<128>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos, dXself);
+  else dX_bn<64>(st, c, blob, dP, MxT, MxT_lo, F, Xl, dZ, pos, dXself);
 }
 
-bool dxda_supported(const Caps &c) { return c.H == 128; }
+bool dxda_supported(const Caps &c) { return c.H == 128 && !c.self_t; }
 
 void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, const float *MxT, const float *MxT_lo,
                  const float *WbT, const float *WbT_lo, const int *perm, const DegInfo *info, const int4 *tiles,
@@ -867,17 +888,18 @@ void launch_dxda(cudaStream_t st, const Caps &c, int cmax, const float *dP_s, co
 void launch_prep_Mx(cudaStream_t st, const Caps &c, const float *params, const int64_t *mx_off_dev, int L,
                     float *Mx_lo, float *MxT, float *MxT_lo) {
   if (L < 2) return;
-  const int blocks = std::min((L - 1) * (c.H / 32) * (c.H / 32), kSMs);
-  launch_ex(k_prep_Mx, blocks, dim3(32, 8), 0, st, params, mx_off_dev, L, c.H, c.H, Mx_lo, MxT, MxT_lo);
+  const int blocks = std::min((L - 1) * (c.PW() / 32) * (c.H / 32), kSMs);
+  launch_ex(k_prep_Mx, blocks, dim3(32, 8), 0, st, params, mx_off_dev, L, c.PW(), c.H, Mx_lo, MxT, MxT_lo);
   g_launches += 1;
 }
 
-void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev, int l0, int l1,
-                    int cmax, const DegInfo *info, float *Wf, float *Wf_lo, float *WbT, float *WbT_lo) {
+void launch_prep_W2(cudaStream_t st, const Caps &c, const float *params, const int64_t *u_off_dev,
+                    const int64_t *ux_off_dev, int l0, int l1, int cmax, const DegInfo *info, float *Wf, float *Wf_lo,
+                    float *WbT, float *WbT_lo) {
   // (side-stream kernel: a grid of two waves leaves room for the main chain's first kernels)
-  const int blocks = std::max(1, std::min((l1 - l0) * cmax * (4 * c.H / 32) * (c.H / 32), kSMs * 2));
-  launch_ex(k_prep_W2, blocks, dim3(32, 8), 0, st, params, u_off_dev, l0, l1, c.H, cmax, info, Wf, Wf_lo, WbT,
-            WbT_lo);
+  const int blocks = std::max(1, std::min((l1 - l0) * cmax * (c.KA() / 32) * (c.H / 32), kSMs * 2));
+  launch_ex(k_prep_W2, blocks, dim3(32, 8), 0, st, params, u_off_dev, c.self_t ? ux_off_dev : nullptr, l0, l1, c.H,
+            c.S, c.F0, cmax, info, Wf, Wf_lo, WbT, WbT_lo);
   g_launches += 1;
 }
 

@@ -275,9 +275,9 @@ __global__ void __launch_bounds__(N_THREADS, 1) k_tmn(const __grid_constant__ Tm
 // degree-sorted, so a split is a contiguous row range), cs[sp][h] = sum_k dZ[k][h]
 struct MnGram {
   static constexpr int BN = 128;
-  const DegInfo *info; const int4 *splits; float *part, *cs; int H; int items_cap;
+  const DegInfo *info; const int4 *splits; float *part, *cs; int H, K; int items_cap;
   __device__ bool item(int t, MnItem &w) const {
-    const int NT = 4 * H / BN + 1, MT = H / N_BM;
+    const int NT = K / BN + 1, MT = H / N_BM;
     const int nt = t % NT, mt = (t / NT) % MT, sp = t / (NT * MT);
     if (sp >= info->S) return false;
     const int4 s = splits[sp];
@@ -285,7 +285,7 @@ struct MnGram {
     return true;
   }
   __device__ void emit(const MnItem &w, int m, int n, float4 v) const {
-    *reinterpret_cast<float4 *>(part + ((size_t)w.sp * H + m) * 4 * H + n) = v;
+    *reinterpret_cast<float4 *>(part + ((size_t)w.sp * H + m) * K + n) = v;
   }
   __device__ void emit_cs(const MnItem &w, int m, float v) const { cs[(size_t)w.sp * H + m] = v; }
 };
@@ -379,54 +379,66 @@ __global__ void __launch_bounds__(32 * RW) k_reduce_jobs(RJob j0, RJob j1, RJob 
 }
 static int reduce_blocks(const RJob &j) { return (j.count / 4 + 31) / 32; }
 
-// dU[h][s*4H + n] = sum_sp s(class(sp)) part[sp][h][n] for the three scalers
-// (blocks over the H x 4H partial), db_U[h] = sum_sp cs[sp][h] (trailing blocks);
-// S = info->S splits (device-side)
+// dU[h][s*4H + n] = sum_sp s(class(sp)) part[sp][h][n] for the S scalers over the 4H aggregate
+// columns (blocks over the H x K partial, K = 4H or 5H); the self-term's x block (columns
+// [4H, 5H), not scaled): dUx[h][n - 4H] = sum_sp part[sp][h][n] for n - 4H < Fl; db_U[h] =
+// sum_sp cs[sp][h] (trailing blocks); info->S splits (device-side). Split order fixed.
 __global__ void __launch_bounds__(256) k_reduce_gram(const float *__restrict__ part, const float *__restrict__ cs,
                                                      const DegInfo *__restrict__ info, const int4 *__restrict__ splits,
-                                                     int H, float *__restrict__ dU, float *__restrict__ dbU) {
+                                                     int H, int K, int NS, int Fl, float *__restrict__ dU,
+                                                     float *__restrict__ dbU, float *__restrict__ dUx) {
   pdl_enter();
-  __shared__ float4 red[3][8][32];
+  __shared__ float4 red[kMaxScalers][8][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int S = info->S, K = 4 * H, bU = H * K / 128;
+  const int S = info->S, K4 = 4 * H, bU = H * K / 128;
   const bool gram = (int)blockIdx.x < bU;
   const int e = 4 * (((int)blockIdx.x - (gram ? 0 : bU)) * 32 + lane);
   const bool ok = gram || e < H;
-  float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0;
+  const int h = gram ? e / K : 0, n = gram ? e - h * K : 0;
+  const int ns = gram && n < K4 ? NS : 1;  // sums this thread keeps (uniform per 32-column block)
+  float4 acc[kMaxScalers];
+#pragma unroll
+  for (int q = 0; q < kMaxScalers; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   if (ok) {
     for (int sp = warp; sp < S; sp += 8) {
       if (gram) {
         const int c = splits[sp].x;
-        const float a = info->amp[c], t = info->att[c];
         const float4 v = ldg4(part + (size_t)sp * H * K + e);
-        add4(s0, v);
-        s1.x = fmaf(a, v.x, s1.x); s1.y = fmaf(a, v.y, s1.y); s1.z = fmaf(a, v.z, s1.z); s1.w = fmaf(a, v.w, s1.w);
-        s2.x = fmaf(t, v.x, s2.x); s2.y = fmaf(t, v.y, s2.y); s2.z = fmaf(t, v.z, s2.z); s2.w = fmaf(t, v.w, s2.w);
+        add4(acc[0], v);
+#pragma unroll
+        for (int q = 1; q < kMaxScalers; ++q)
+          if (q < ns) {
+            const float a = info->scal[q][c];
+            acc[q].x = fmaf(a, v.x, acc[q].x); acc[q].y = fmaf(a, v.y, acc[q].y);
+            acc[q].z = fmaf(a, v.z, acc[q].z); acc[q].w = fmaf(a, v.w, acc[q].w);
+          }
       } else {
-        add4(s0, ldg4(cs + (size_t)sp * H + e));
+        add4(acc[0], ldg4(cs + (size_t)sp * H + e));
       }
     }
   }
-  red[0][warp][lane] = s0;
-  red[1][warp][lane] = s1;
-  red[2][warp][lane] = s2;
+#pragma unroll
+  for (int q = 0; q < kMaxScalers; ++q) red[q][warp][lane] = acc[q];
   __syncthreads();
   if (warp == 0 && ok) {
-    float4 t0 = red[0][0][lane], t1 = red[1][0][lane], t2 = red[2][0][lane];
+    float4 t[kMaxScalers];
 #pragma unroll
-    for (int w = 1; w < 8; ++w) {
-      add4(t0, red[0][w][lane]);
-      add4(t1, red[1][w][lane]);
-      add4(t2, red[2][w][lane]);
+    for (int q = 0; q < kMaxScalers; ++q) {
+      t[q] = red[q][0][lane];
+#pragma unroll
+      for (int w = 1; w < 8; ++w) add4(t[q], red[q][w][lane]);
     }
-    if (gram) {
-      const int h = e / K, n = e - h * K;
-      float *row = dU + (size_t)h * 3 * K + n;
-      *reinterpret_cast<float4 *>(row) = t0;
-      *reinterpret_cast<float4 *>(row + K) = t1;
-      *reinterpret_cast<float4 *>(row + 2 * K) = t2;
-    } else {
-      *reinterpret_cast<float4 *>(dbU + e) = t0;
+    if (!gram) {
+      *reinterpret_cast<float4 *>(dbU + e) = t[0];
+    } else if (n < K4) {
+#pragma unroll
+      for (int q = 0; q < kMaxScalers; ++q)
+        if (q < ns) *reinterpret_cast<float4 *>(dU + (size_t)h * NS * K4 + (size_t)q * K4 + n) = t[q];
+    } else {  // self-term block -> U_x [H][Fl] (Fl may be the raw feature width: scalar stores)
+      const float v[4] = {t[0].x, t[0].y, t[0].z, t[0].w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (n - K4 + u < Fl) dUx[(size_t)h * Fl + n - K4 + u] = v[u];
     }
   }
 }
@@ -460,35 +472,39 @@ cudaError_t tmn_configure() {
 
 size_t mn_gram_partial_floats(const Caps &c, int cmax) {
   const size_t S = (size_t)tc_max_splits(c, cmax);
-  return S * c.H * 4 * c.H + S * c.H;
+  return S * c.H * c.KA() + S * c.H;
 }
-size_t mn_dmx_partial_floats(const Caps &c, int F) { return (size_t)kMnDMxSplits * c.H * (F + 1); }
+size_t mn_dmx_partial_floats(const Caps &c, int F) { return (size_t)kMnDMxSplits * c.PW() * (F + 1); }
 
 void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *A, const float *ones,
-                      const DegInfo *info, const int4 *splits, float *partial, float *dU, float *dbU) {
+                      const DegInfo *info, const int4 *splits, float *partial, float *dU, float *dbU, float *dUx,
+                      int Fl) {
   const int smax = tc_max_splits(c, cmax);
-  const int total = c.H * 4 * c.H;
+  const int K = c.KA(), total = c.H * K;
   float *cs = partial + (size_t)smax * total;
-  const CUtensorMap a = tma_map2d(dZ, c.maxN, c.H, N_BK, true), b = tma_map2d(A, c.maxN, 4 * c.H, N_BK, true);
+  const CUtensorMap a = tma_map2d(dZ, c.maxN, c.H, N_BK, true), b = tma_map2d(A, c.maxN, K, N_BK, true);
   const TmaMaps mp{a, a, b, b};  // (lo slots unused: derived in shared memory)
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
-  MnGram op{info, splits, partial, cs, c.H, 0};
-  nrun(st, mp, om, op, smax * (c.H / N_BM) * (4 * c.H / MnGram::BN + 1));
-  launch_ex(k_reduce_gram, total / 128 + cdiv(c.H, 128), 256, 0, st, partial, cs, info, splits, c.H, dU, dbU);
+  MnGram op{info, splits, partial, cs, c.H, K, 0};
+  nrun(st, mp, om, op, smax * (c.H / N_BM) * (K / MnGram::BN + 1));
+  launch_ex(k_reduce_gram, total / 128 + cdiv(c.H, 128), 256, 0, st, partial, cs, info, splits, c.H, K, c.S, Fl, dU,
+            dbU, dUx);
   g_launches += 1;
 }
 
 void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *dP, const float *X, int F, int Fp,
-                   const float *ones, float *partial, float *dMx, float *dbM) {
-  const int count = c.H * F;
+                   const float *ones, float *partial, float *dMx, float *dbM, int Rr) {
+  // rows: dP (H), or [dP | dQ] (2H) -> [dM_x; dM_s], adjacent in the gradient arena (or Rr)
+  const int R = Rr > 0 ? Rr : c.PW();
+  const int count = R * F;
   float *cs = partial + (size_t)kMnDMxSplits * count;
-  const CUtensorMap a = tma_map2d(dP, c.maxN, c.H, N_BK, true), b = tma_map2d(X, c.maxN, Fp, N_BK, true);
+  const CUtensorMap a = tma_map2d(dP, c.maxN, R, N_BK, true), b = tma_map2d(X, c.maxN, Fp, N_BK, true);
   const TmaMaps mp{a, a, b, b};  // (lo slots unused: derived in shared memory)
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
   const int with_cs = dbM ? 1 : 0;
-  MnDMx op{blob, partial, cs, c.H, F, 0, with_cs};
-  nrun(st, mp, om, op, kMnDMxSplits * (c.H / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + with_cs));
-  const RJob j0{partial, kMnDMxSplits, count, dMx, 0}, j1{cs, kMnDMxSplits, with_cs ? c.H : 0, dbM, 0},
+  MnDMx op{blob, partial, cs, R, F, 0, with_cs};
+  nrun(st, mp, om, op, kMnDMxSplits * (R / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + with_cs));
+  const RJob j0{partial, kMnDMxSplits, count, dMx, 0}, j1{cs, kMnDMxSplits, with_cs ? R : 0, dbM, 0},
       j2{nullptr, 0, 0, nullptr, 0};
   launch_ex(k_reduce_jobs, reduce_blocks(j0) + (with_cs ? reduce_blocks(j1) : 0), 32 * RW, 0, st, j0, j1, j2);
   g_launches += 1;
@@ -527,6 +543,11 @@ void launch_reduce_dMe(cudaStream_t st, const Caps &c, const float *partial, flo
   const int stride = c.H * (c.Fe + 1), cnt_e = c.H * c.Fe, cnt_b = c.H;  // (both % 4 == 0: H % 128 == 0)
   launch_ex(k_reduce_rows32, (cnt_e + cnt_b + 127) / 128, 1024, 0, st, partial, c.maxB, stride, cnt_e, dMe, cnt_b,
             dbM);
+  g_launches += 1;
+}
+
+void launch_reduce_cols(cudaStream_t st, const float *part, int parts, int stride, int count, float *out) {
+  launch_ex(k_reduce_rows32, (count + 127) / 128, 1024, 0, st, part, parts, stride, count, out, 0, out);
   g_launches += 1;
 }
 

@@ -32,7 +32,7 @@ PHASES = ["scalers", "proj", "agg_fwd", "update", "head_fwd", "head_bwd", "dA", 
 
 P2P_HANDLE_BYTES = 72  # include/hgnn.h HG_P2P_HANDLE_BYTES
 VIEW_P, VIEW_A, VIEW_ARG, VIEW_X, VIEW_SLOT, VIEW_YHAT, VIEW_LOSS, VIEW_HPRE, VIEW_PARAMS, VIEW_GRADS, \
-    VIEW_AMP, VIEW_ATT = range(12)
+    VIEW_AMP, VIEW_ATT, VIEW_NODE_YHAT, VIEW_NODE_HPRE = range(14)
 
 
 class HgError(RuntimeError):
@@ -46,7 +46,8 @@ class hg_store_desc(ctypes.Structure):
     _fields_ = [("num_graphs", ctypes.c_int64), ("num_nodes", ctypes.c_int64), ("num_edges", ctypes.c_int64),
                 ("f_node", ctypes.c_int32), ("f_edge", ctypes.c_int32),
                 ("node_offset", ctypes.c_void_p), ("edge_offset", ctypes.c_void_p), ("x", ctypes.c_void_p),
-                ("edge_index", ctypes.c_void_p), ("edge_attr", ctypes.c_void_p), ("y", ctypes.c_void_p)]
+                ("edge_index", ctypes.c_void_p), ("edge_attr", ctypes.c_void_p), ("y", ctypes.c_void_p),
+                ("y_node", ctypes.c_void_p)]
 
 
 class hg_config(ctypes.Structure):
@@ -54,7 +55,8 @@ class hg_config(ctypes.Structure):
                 ("layers", ctypes.c_int32), ("fc_hidden", ctypes.c_int32), ("max_graphs", ctypes.c_int32),
                 ("max_nodes", ctypes.c_int32), ("max_edges", ctypes.c_int32), ("n_slots", ctypes.c_int32),
                 ("flags", ctypes.c_int32), ("delta", ctypes.c_double), ("var_floor", ctypes.c_float),
-                ("max_degree", ctypes.c_int32)]
+                ("max_degree", ctypes.c_int32), ("scalers", ctypes.c_int32), ("delta_lin", ctypes.c_double),
+                ("node_weight", ctypes.c_float)]
 
 
 class hg_adamw(ctypes.Structure):
@@ -63,7 +65,8 @@ class hg_adamw(ctypes.Structure):
 
 
 class hg_batch_offsets_t(ctypes.Structure):
-    _fields_ = [(k, ctypes.c_int64) for k in ("graph_ptr", "y", "rowptr", "col", "x", "eattr", "slot", "total")]
+    _fields_ = [(k, ctypes.c_int64) for k in ("graph_ptr", "y", "y_node", "rowptr", "col", "x", "eattr", "slot",
+                                              "total")]
 
 
 _P = ctypes.c_void_p
@@ -79,6 +82,7 @@ SIGNATURES = {
     "hg_store_destroy": [_P],
     "hg_store_stats": [_P, _I64P, _I64P, _I64P, _I32P, _I32P],
     "hg_degree_stat": [_P, _P, _I64, _DP],
+    "hg_degree_stat_linear": [_P, _P, _I64, _DP],
     "hg_shard": [_U64, _I64, _I32, _I32, _I64, _P, _I64P],
     "hg_batch_offsets_get": [_I32, _I32, _I32, _I32, _I32, ctypes.POINTER(hg_batch_offsets_t)],
     "hg_pack_host": [_P, _P, _I32, ctypes.POINTER(hg_config), _P, _SZ, _SZP],
@@ -176,13 +180,31 @@ DEFAULT_ADAMW = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0
 
 HG_LOSS_RING = 4  # include/hgnn.h
 HG_FLAG_TF32 = 1  # reduced-precision (single-pass TF32) GEMM mode
+HG_FLAG_SELF_TERM = 2  # PNA self-term variant (x_i into M and U)
+HG_FLAG_NODE_HEAD = 4  # node-level head beside the graph head (multitask)
+SCALER_BITS = {"identity": 1, "amplification": 2, "attenuation": 4, "linear": 8, "inverse_linear": 16}
+
+
+def scaler_mask(names) -> int:
+    m = 0
+    for n in names:
+        m |= SCALER_BITS[n]
+    return m
+
+
+def scaler_names(mask: int) -> tuple:
+    """The U block order of a scaler bit set (bit order), as the oracle's cfg['scalers']."""
+    mask = mask or 7
+    return tuple(n for n, b in SCALER_BITS.items() if mask & b)
 
 
 def make_config(f_node, f_edge, hidden, layers, max_graphs, max_nodes, max_edges, delta, fc_hidden=None,
-                n_slots=2, var_floor=1e-10, flags=0, max_degree=0) -> hg_config:
+                n_slots=2, var_floor=1e-10, flags=0, max_degree=0, scalers=0, delta_lin=0.0,
+                node_weight=1.0) -> hg_config:
     return hg_config(f_node=f_node, f_edge=f_edge, hidden=hidden, layers=layers, fc_hidden=fc_hidden or hidden,
                      max_graphs=max_graphs, max_nodes=max_nodes, max_edges=max_edges, n_slots=n_slots, flags=flags,
-                     delta=float(delta), var_floor=var_floor, max_degree=max_degree)
+                     delta=float(delta), var_floor=var_floor, max_degree=max_degree, scalers=int(scalers),
+                     delta_lin=float(delta_lin), node_weight=float(node_weight))
 
 
 def make_adamw(**kw) -> hg_adamw:
@@ -206,6 +228,8 @@ class Store:
             "edge_attr": np.ascontiguousarray(data["edge_attr"], np.float32),
             "y": np.ascontiguousarray(data["y"], np.float32),
         }
+        if "y_node" in data:
+            self._arrays["y_node"] = np.ascontiguousarray(data["y_node"], np.float32)
         a = self._arrays
         G = len(a["node_offset"]) - 1
         self.f_node = int(a["x"].shape[1])
@@ -214,7 +238,7 @@ class Store:
                           f_node=self.f_node, f_edge=self.f_edge, node_offset=a["node_offset"].ctypes.data,
                           edge_offset=a["edge_offset"].ctypes.data, x=a["x"].ctypes.data,
                           edge_index=a["edge_index"].ctypes.data, edge_attr=a["edge_attr"].ctypes.data,
-                          y=a["y"].ctypes.data)
+                          y=a["y"].ctypes.data, y_node=a["y_node"].ctypes.data if "y_node" in a else None)
         h = ctypes.c_void_p()
         _check(_lib.hg_store_create(ctypes.byref(d), int(copy), int(threads), ctypes.byref(h)))
         self.handle = h
@@ -265,6 +289,15 @@ class Store:
                                    ctypes.byref(md)))
         return {"graphs": g.value, "nodes": n.value, "edges": e.value, "max_nodes_per_graph": mn.value,
                 "max_degree": md.value}
+
+    def degree_stat_linear(self, ids=None) -> float:
+        out = _D()
+        if ids is None:
+            _check(_lib.hg_degree_stat_linear(self.handle, None, 0, ctypes.byref(out)))
+        else:
+            ids = np.ascontiguousarray(ids, np.int64)
+            _check(_lib.hg_degree_stat_linear(self.handle, _ptr(ids), len(ids), ctypes.byref(out)))
+        return out.value
 
     def degree_stat(self, ids=None) -> float:
         out = _D()
@@ -324,6 +357,7 @@ def unpack_blob(blob: np.ndarray) -> dict:
     def arr(key, dtype, count):
         return blob[o[key]:o[key] + count * np.dtype(dtype).itemsize].view(dtype)
     return {"B": B, "N": N, "E": E, "graph_ptr": arr("graph_ptr", np.int32, B + 1), "y": arr("y", np.float32, B),
+            "y_node": arr("y_node", np.float32, N),
             "rowptr": arr("rowptr", np.int32, N + 1), "col": arr("col", np.int32, E),
             "x": arr("x", np.float32, N * F0).reshape(N, F0), "eattr": arr("eattr", np.float32, E * Fe).reshape(E, Fe),
             "slot": arr("slot", np.uint8, E)}

@@ -36,8 +36,12 @@ def capacity_for(data, B):
 
 
 def oracle_cfg(cfg):
+    """The oracle's model dict of a C-ABI configuration (variants: scaler set, self-term)."""
     return {"f_node": cfg.f_node, "f_edge": cfg.f_edge, "hidden": cfg.hidden, "layers": cfg.layers,
-            "fc_hidden": cfg.fc_hidden, "var_floor": float(np.float32(cfg.var_floor))}
+            "fc_hidden": cfg.fc_hidden, "var_floor": float(np.float32(cfg.var_floor)),
+            "scalers": hgnn.scaler_names(cfg.scalers), "self_term": bool(cfg.flags & hgnn.HG_FLAG_SELF_TERM),
+            "delta_lin": float(cfg.delta_lin), "node_head": bool(cfg.flags & hgnn.HG_FLAG_NODE_HEAD),
+            "node_weight": float(np.float32(cfg.node_weight))}
 
 
 def gpu_X(ctx, l, N, H):
@@ -63,7 +67,7 @@ class StepResult(dict):
     pass
 
 
-def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=False):
+def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=False, tau_arg=1e-6):
     """One step on GPU (ctx must hold the parameters) and on the oracle from the
     GPU's current parameters / optimizer state. Returns StepResult of metrics."""
     import torch
@@ -99,6 +103,13 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
         ref = np.maximum(cache["layers"][l]["Z"], 0)
         xs.append(float(np.abs(X - ref).max() / max(np.abs(ref).max(), 1e-30)))
     res["X"] = max(xs)
+    node_relu = None
+    if cfg.flags & hgnn.HG_FLAG_NODE_HEAD:  # node-level head outputs (variant)
+        yn = ctx.view_f32(hgnn.VIEW_NODE_YHAT)[:N].cpu().numpy()
+        ref_n = cache["head"]["yn"]
+        res["yhat_node"] = float(np.abs(yn - ref_n).max() / max(np.abs(ref_n).max(), 1e-30))
+        Hfi = ctx.internal_cfg.fc_hidden
+        node_relu = ctx.view_f32(hgnn.VIEW_NODE_HPRE)[:N * Hfi].cpu().numpy().reshape(N, Hfi)[:, :cfg.fc_hidden] > 0
     Hfp = ctx.internal_cfg.fc_hidden
     hpre = ctx.view_f32(hgnn.VIEW_HPRE)[:B * Hfp].cpu().numpy().reshape(B, Hfp)[:, :cfg.fc_hidden]
     # ReLU replay band per layer: the GPU's measured forward error of that layer (x2), at least
@@ -107,8 +118,10 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
     hp_ref = cache["head"]["hpre"]
     tau_head = max(1e-6, 2.0 * float(np.abs(hpre - hp_ref).max() / max(np.abs(hp_ref).max(), 1e-30)))
     res["tau_relu"] = max(tau_relu)
-    dec, counts = O.replay(cache, gpu_decisions(ctx, N, H, L), tau_arg=1e-6, tau_relu=tau_relu, tau_head=tau_head,
-                           head_relu_gpu=hpre > 0)
+    if tau_arg is None:  # (reduced-precision mode: argmin/argmax band at the measured forward error too)
+        tau_arg = max(tau_relu)
+    dec, counts = O.replay(cache, gpu_decisions(ctx, N, H, L), tau_arg=tau_arg, tau_relu=tau_relu, tau_head=tau_head,
+                           head_relu_gpu=hpre > 0, node_relu_gpu=node_relu)
     res["overrides"] = counts["overrides"]
     res["overrides_by"] = counts["overrides_by"]
     res["tie_overrides"] = counts["tie_overrides"]
@@ -154,22 +167,25 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
     return res
 
 
-def make_ctx(data, B, H, L, seed=2, n_slots=2, Hf=None, flags=0, max_degree=None):
-    """A ctx sized for the B largest graphs of `data`, parameters from the C12 init."""
+def make_ctx(data, B, H, L, seed=2, n_slots=2, Hf=None, flags=0, max_degree=None, scalers=0, node_weight=1.0):
+    """A ctx sized for the B largest graphs of `data`, parameters from the C12 init
+    (scalers: an HG_SCALER_* bit set; flags: HG_FLAG_*)."""
     delta = O.degree_stat(data)
+    delta_lin = O.degree_stat_linear(data)
     maxn, maxe = capacity_for(data, B)
     store = hgnn.Store(data)
     if max_degree is None:
         max_degree = store.stats()["max_degree"]
     cfg = hgnn.make_config(data["f_node"], 4, H, L, B, maxn, maxe, delta, fc_hidden=Hf, n_slots=n_slots,
-                           flags=flags, max_degree=max_degree)
+                           flags=flags, max_degree=max_degree, scalers=scalers, delta_lin=delta_lin,
+                           node_weight=node_weight)
     ctx = hgnn.Context(cfg)
     ctx.params_init(seed)
     ctx._store = store
     return ctx, cfg, delta
 
 
-def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
+def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL, override_frac=1e-4):
     bad = []
     if res["yhat"] > fwd_tol:
         bad.append(("yhat", res["yhat"]))
@@ -177,6 +193,8 @@ def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
         bad.append(("loss", res["loss"]))
     if res["X"] > fwd_tol:
         bad.append(("X", res["X"]))
+    if res.get("yhat_node", 0.0) > fwd_tol:
+        bad.append(("yhat_node", res["yhat_node"]))
     # GPU discrete decisions (ReLU masks, argmin/argmax, std floor) must agree with the
     # oracle wherever the oracle's margin exceeds tau; in-band
     # overrides are equally valid choices and only bounded loosely; overrides at
@@ -184,7 +202,7 @@ def assert_parity(res, fwd_tol=FWD_TOL, grad_tol=GRAD_TOL, param_tol=PARAM_TOL):
     # oracle's own summation order picks the position) are not bounded.
     if res["out_of_band"] > max(2, 1e-5 * res["cells"]):
         bad.append(("out_of_band", res["out_of_band"], res["out_of_band_by"]))
-    if res["overrides"] > 1e-4 * res["cells"]:  # overrides < 1e-4 of the cells
+    if res["overrides"] > override_frac * res["cells"]:  # overrides < 1e-4 of the cells
         bad.append(("overrides", res["overrides"], res["cells"]))
     if "grad_maxscaled" in res:
         for k, v in res["grad_maxscaled"].items():

@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
     for name in decl:
         assert hasattr(lib, name), name
     assert set(decl) == set(hgnn.SIGNATURES), set(decl) ^ set(hgnn.SIGNATURES)
-    assert lib.hg_abi_version() == 1
+    assert lib.hg_abi_version() == 2
 
 
 @pytest.fixture(scope="module")
@@ -250,3 +250,36 @@ def test_pack_threads_setting_does_not_change_the_bytes(pcqm):
     hgnn.pack_threads_set(4)
     with pytest.raises(hgnn.HgError):
         hgnn.pack_threads_set(0)
+
+
+@pytest.mark.parametrize("flags,scalers", [(2, 0), (0, 31), (2, 1 | 8), (2, 31)])
+def test_variant_param_layout_and_init_match_the_oracle(flags, scalers):
+    """Model variants (self-term: M_s after M_x, U_x after U; scaler sets: U = [H, 4SH]): the
+    C-ABI layout and the counter-based init equal the oracle's param_specs / init_params."""
+    cfg = hgnn.make_config(34, 4, 128, 2, 4, 100, 400, 1.0, flags=flags, scalers=scalers, delta_lin=2.0)
+    lay, total = hgnn.hg_param_layout(cfg)
+    flat = hgnn.hg_params_init_host(cfg, 77)
+    ocfg = {"f_node": 34, "f_edge": 4, "hidden": 128, "layers": 2, "fc_hidden": 128,
+            "self_term": bool(flags & 2), "scalers": hgnn.scaler_names(scalers), "delta_lin": 2.0}
+    ref = O.init_params(ocfg, 77)
+    assert [n for n, *_ in lay] == list(ref)
+    for name, off, r, c in lay:
+        np.testing.assert_array_equal(flat[off:off + r * c], ref[name].reshape(-1).astype(np.float32), err_msg=name)
+
+
+def test_variant_config_validation():
+    for kw in ({"scalers": 2}, {"scalers": 8 | 1, "delta_lin": 0.0}, {"scalers": 64}):
+        cfg = hgnn.make_config(34, 4, 128, 2, 4, 100, 400, 1.0, **kw)
+        with pytest.raises(hgnn.HgError) as e:
+            hgnn.hg_config_internal(cfg)
+        assert e.value.name == "HG_E_INVALID"
+    cfg = hgnn.make_config(200, 4, 128, 2, 4, 100, 400, 1.0, flags=hgnn.HG_FLAG_SELF_TERM)  # f_node > hidden
+    with pytest.raises(hgnn.HgError):
+        hgnn.hg_config_internal(cfg)
+
+
+def test_degree_stat_linear_matches_oracle(pcqm):
+    store = hgnn.Store(pcqm)
+    assert abs(store.degree_stat_linear() - O.degree_stat_linear(pcqm)) <= 1e-14
+    ids = np.arange(5, 3000, 11)
+    assert abs(store.degree_stat_linear(ids) - O.degree_stat_linear(pcqm, ids)) <= 1e-14

@@ -93,6 +93,25 @@ def test_p1s_self_term_worked_example():
         np.testing.assert_allclose(grads[k], np.asarray(v), rtol=1e-9, atol=1e-14, err_msg=k)
 
 
+def test_p1n_node_head_worked_example():
+    """Model variant: a node-level head beside the graph head (multitask), hand-derived."""
+    g = _golden("p1n_two_node_node_head.json")
+    st = make_store([(g["graph"]["x"], [(a, b, e) for a, b, e in g["graph"]["bonds"]], g["graph"]["y"])])
+    st["y_node"] = np.asarray(g["graph"]["y_node"], np.float32)
+    cfg = g["model"]
+    p = _params_from(g["params"])
+    assert [n for n, *_ in O.param_specs(cfg)] == list(g["params"])
+    b = O.pack(st, [0])
+    loss, yhat, cache = O.forward(p, b, cfg, cfg["delta"])
+    ex = g["expected"]
+    np.testing.assert_allclose(cache["head"]["yn"], ex["yn"], atol=1e-12)
+    assert abs(loss - ex["loss"]) < 1e-12
+    grads = O.backward(p, b, cfg, cache)
+    assert set(grads) == set(p)
+    for k, v in ex["grads"].items():
+        np.testing.assert_allclose(grads[k], np.asarray(v), rtol=1e-9, atol=1e-14, err_msg=k)
+
+
 def test_p2s_five_scalers_worked_example():
     """Model variant: PNA's linear / inverse_linear scalers beside C2's three, hand-derived."""
     g = _golden("p2s_star_five_scalers.json")
@@ -284,7 +303,15 @@ VARIANTS = {
     "five_scalers": {"scalers": O.SCALERS, "delta_lin": 1.9},
     "self_five": {"self_term": True, "scalers": ("identity", "linear", "amplification", "inverse_linear"),
                   "delta_lin": 2.1},
+    "node_head": {"node_head": True, "node_weight": 0.7},
 }
+
+
+def _with_node_targets(st, seed):
+    """Per-node targets for the node-head variant (continuous, so no kink within FD's h)."""
+    st = dict(st)
+    st["y_node"] = np.random.default_rng(seed).standard_normal(len(st["x"])).astype(np.float32)
+    return st
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
@@ -297,7 +324,7 @@ def test_p5_finite_difference_gradients(seed, variant):
     if variant != "default" and seed % 4:
         pytest.skip("variants: every 4th seed")
     st = molgen.generate("tiny", 3, seed=100 + seed, first_id=0)
-    st = molgen.perturb_features(st, seed=200 + seed, scale=0.2)
+    st = _with_node_targets(molgen.perturb_features(st, seed=200 + seed, scale=0.2), seed)
     cfg = dict(small_cfg(st["f_node"], 4, 2, Hf=3), **VARIANTS[variant])
     p = _jitter_params(O.init_params(cfg, seed), seed)
     delta = 0.8 + 0.05 * seed
@@ -447,7 +474,14 @@ def _torch_model_loss(torch, params, st, ids, cfg, delta):
     G = torch.zeros(B, H, dtype=dt).index_add_(0, gidt, X) / cnt[:, None]
     hid = torch.relu(G @ params["head.W1"].T + params["head.b1"])
     yhat = (hid @ params["head.W2"].T)[:, 0] + params["head.b2"][0]
-    return torch.mean((yhat - torch.tensor(ys, dtype=dt)) ** 2), yhat
+    loss = torch.mean((yhat - torch.tensor(ys, dtype=dt)) ** 2)
+    if cfg.get("node_head", False):  # HydraGNN multitask: per-node head, weighted MSE sum
+        yn_t = torch.cat([torch.tensor(st["y_node"][st["node_offset"][g]:st["node_offset"][g + 1]], dtype=dt)
+                          for g in ids])
+        yn = (torch.relu(X @ params["head_n.W1"].T + params["head_n.b1"]) @ params["head_n.W2"].T)[:, 0] \
+            + params["head_n.b2"][0]
+        loss = loss + cfg.get("node_weight", 1.0) * torch.mean((yn - yn_t) ** 2)
+    return loss, yhat
 
 
 @pytest.mark.parametrize("variant", list(VARIANTS))
@@ -455,6 +489,7 @@ def test_p9i_torch_autograd_crosscheck(pcqm_small, variant):
     torch = pytest.importorskip("torch")
     st, cfg, p, delta = pcqm_small
     cfg = dict(cfg, **VARIANTS[variant])
+    st = _with_node_targets(st, 4)
     p = _jitter_params(O.init_params(cfg, 9), 3, 0.2)
     ids = [0, 4, 9, 2]
     tp = {k: torch.tensor(v, dtype=torch.float64, requires_grad=True) for k, v in p.items()}
