@@ -86,6 +86,16 @@ typedef struct {
  * neighbour row. */
 hg_status hg_store_create(const hg_store_desc *d, int32_t copy, int32_t threads, hg_store **out);
 hg_status hg_store_destroy(hg_store *s);
+/* One copy of the store shared by every rank of the node: hg_store_create_shared
+ * validates `d` like hg_store_create, derives the slots and writes everything into the new POSIX
+ * shared-memory object `name` ("/..."; HG_E_IO if it exists); hg_store_open_shared maps an
+ * existing one read-only in another process (HG_E_IO: missing, or not a store). pin_memory != 0
+ * page-locks the mapping (cudaHostRegister; HG_E_CUDA if that fails, e.g. without a GPU).
+ * hg_store_destroy unmaps; hg_store_unlink_shared removes the name (once every rank opened it). */
+hg_status hg_store_create_shared(const hg_store_desc *d, const char *name, int32_t pin_memory, int32_t threads,
+                                 hg_store **out);
+hg_status hg_store_open_shared(const char *name, int32_t pin_memory, hg_store **out);
+hg_status hg_store_unlink_shared(const char *name);
 /* Totals and maxima over the store (Table 2 style summary). */
 hg_status hg_store_stats(const hg_store *s, int64_t *graphs, int64_t *nodes, int64_t *edges,
                          int32_t *max_nodes_per_graph, int32_t *max_degree);

@@ -21,7 +21,7 @@ OBJDIR = os.path.join(HERE, "build")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["kernels.cu", "agg.cu", "degsort.cu", "tcdirect.cu", "tcmn.cu", "p2p.cu", "ctx.cu"]
-CPP_SOURCES = ["host.cpp", "container.cpp"]
+CPP_SOURCES = ["host.cpp", "container.cpp", "shm.cpp"]
 
 
 def _nccl_dirs():
@@ -66,7 +66,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         jobs.append((cmd, obj))
     for f in CPP_SOURCES:
         obj = os.path.join(OBJDIR, f + ".o")
-        cmd = ["g++", "-fPIC", "-Wall", "-pthread", "-fopenmp", "-msse4.2"] + common + ["-c", os.path.join(CSRC, f), "-o", obj]
+        cmd = ["g++", "-fPIC", "-Wall", "-pthread", "-fopenmp", "-msse4.2", "-I/usr/local/cuda/include"] + common + \
+            ["-c", os.path.join(CSRC, f), "-o", obj]
         jobs.append((cmd, obj))
 
     def run(job):

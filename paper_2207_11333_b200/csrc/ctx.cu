@@ -125,7 +125,7 @@ Plan make_plan(const hg_config &c) {
   size_t pf = std::max({mn_gram_partial_floats(caps, p.cmax), mn_dmx_partial_floats(caps, H),
                         mn_dmx_partial_floats(caps, c.f_node)});
   if (c.flags & HG_FLAG_NODE_HEAD) {
-    pf = std::max(pf, (size_t)32 * Hf * (H + 1));  // (the node head's W1n Gram: kMnDMxSplits x Hf x (H + 1))
+    pf = std::max(pf, mn_dmx_partial_floats(caps, H, Hf));  // (the node head's W1n Gram)
     p.nh_hpre = take(sizeof(float) * N * Hf);
     p.nh_dhn = take(sizeof(float) * N * Hf);
     p.nh_yn = take(sizeof(float) * N);

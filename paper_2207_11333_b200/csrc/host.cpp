@@ -309,6 +309,7 @@ hg_status store_finish(hg_store *s, int32_t threads) {
     s->max_nodes = std::max(s->max_nodes, mxn[t]);
     s->max_deg = std::max(s->max_deg, mxd[t]);
   }
+  s->slotp = s->slot.data();
   return HG_OK;
 }
 }  // namespace hg
@@ -499,7 +500,7 @@ hg_status hg_pack_host(const hg_store *s, const int64_t *ids, int32_t B, const h
     else std::memset(yn + nb, 0, sizeof(float) * n);
     std::memcpy(x + nb * s->F0, s->x + n0 * s->F0, sizeof(float) * n * s->F0);
     std::memcpy(ea + eb * s->Fe, s->ea + e0 * s->Fe, sizeof(float) * e * s->Fe);
-    std::memcpy(sl + eb, s->slot.data() + e0, (size_t)e);
+    std::memcpy(sl + eb, s->slotp + e0, (size_t)e);
     // CSR row i (destination) = edges with src == i (symmetric store):
     // in-neighbours are their dst values, already ascending.
     int64_t k = 0;

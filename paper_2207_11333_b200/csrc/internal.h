@@ -66,5 +66,10 @@ struct hg_store {
   std::vector<float> own_x, own_ea, own_y, own_yn;
   std::vector<int32_t> own_ei;
   std::vector<uint8_t> slot;
+  const uint8_t *slotp = nullptr;  // = slot.data(), or the shared-memory copy (hg_store_open_shared)
+  void *shm_base = nullptr;        // POSIX shared-memory mapping of a shared store (shm.cpp)
+  size_t shm_bytes = 0;
+  bool shm_pinned = false;         // the mapping is cudaHostRegister-ed
+  ~hg_store();
   int32_t max_nodes = 0, max_deg = 0;
 };

@@ -190,7 +190,7 @@ extern int g_mn_grid_override;  // tcmn.cu: grid cap override for MN Grams (0 = 
 // TMA-fed MN-major Grams (tcmn.cu): per-class-split dU / db_U and per-split dM_x / db_M,
 // partials reduced in fixed order (rows of dZ / A degree-sorted)
 size_t mn_gram_partial_floats(const Caps &c, int cmax);
-size_t mn_dmx_partial_floats(const Caps &c, int F);
+size_t mn_dmx_partial_floats(const Caps &c, int F, int R = 0);  // (R: rows, 0 = c.PW())
 // (dUx: the self-term's U_x gradient [H][Fl] from the Gram's x block, or null)
 void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *A, const float *ones,
                       const DegInfo *info, const int4 *splits, float *partial, float *dU, float *dbU, float *dUx = nullptr,

@@ -291,22 +291,26 @@ struct MnGram {
 };
 
 // dM_x partials over node splits: part[sp][h][f] = sum_{k in split} dP[k][h] X[k][f]; cs = sum_k dP[k][h]
-constexpr int kMnDMxSplits = 32;
+// node splits of the dM_x Grams: scaled with the capacity (about 256 nodes per split, 16..148),
+// so a large batch fills every SM instead of a fixed 32 CTAs
+constexpr int kMaxDMxSplits = 148;
+int dmx_splits(const Caps &c) { return std::max(16, std::min(kMaxDMxSplits, (c.maxN + 255) / 256)); }
 struct MnDMx {
   static constexpr int BN = 128;
   const uint8_t *blob; float *part, *cs; int H, F; int items_cap;
   int with_cs;  // 1: a trailing ones tile per (m, split) gives cs = sum_k dP[k][h] (db_M)
+  int nsplit;   // node splits (dmx_splits)
   __device__ bool item(int t, MnItem &w) const {
     const int NT = (F + BN - 1) / BN + with_cs, MT = H / N_BM;
     const int nt = t % NT, mt = (t / NT) % MT, sp = t / (NT * MT);
     const int N = batch_N(blob);
-    int kc = (N + kMnDMxSplits - 1) / kMnDMxSplits;
+    int kc = (N + nsplit - 1) / nsplit;
     kc = (kc + N_BK - 1) / N_BK * N_BK;
     const int k0 = sp * kc, len = max(0, min(N - k0, kc));
     w = MnItem{mt * N_BM, nt * BN, k0, len, sp, with_cs && nt == NT - 1};
     // every split is an item, also an empty one (len 0: its partial is written as zeros),
-    // because the fixed-order reduction sums all kMnDMxSplits partials
-    return sp < kMnDMxSplits;
+    // because the fixed-order reduction sums all nsplit partials
+    return sp < nsplit;
   }
   __device__ void emit(const MnItem &w, int m, int n, float4 v) const {
     float *o = part + ((size_t)w.sp * H + m) * F + n;
@@ -474,7 +478,9 @@ size_t mn_gram_partial_floats(const Caps &c, int cmax) {
   const size_t S = (size_t)tc_max_splits(c, cmax);
   return S * c.H * c.KA() + S * c.H;
 }
-size_t mn_dmx_partial_floats(const Caps &c, int F) { return (size_t)kMnDMxSplits * c.PW() * (F + 1); }
+size_t mn_dmx_partial_floats(const Caps &c, int F, int R) {
+  return (size_t)dmx_splits(c) * (R > 0 ? R : c.PW()) * (F + 1);
+}
 
 void launch_mn_dU_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, const float *A, const float *ones,
                       const DegInfo *info, const int4 *splits, float *partial, float *dU, float *dbU, float *dUx,
@@ -497,14 +503,15 @@ void launch_mn_dMx(cudaStream_t st, const Caps &c, const uint8_t *blob, const fl
   // rows: dP (H), or [dP | dQ] (2H) -> [dM_x; dM_s], adjacent in the gradient arena (or Rr)
   const int R = Rr > 0 ? Rr : c.PW();
   const int count = R * F;
-  float *cs = partial + (size_t)kMnDMxSplits * count;
+  const int ns = dmx_splits(c);
+  float *cs = partial + (size_t)ns * count;
   const CUtensorMap a = tma_map2d(dP, c.maxN, R, N_BK, true), b = tma_map2d(X, c.maxN, Fp, N_BK, true);
   const TmaMaps mp{a, a, b, b};  // (lo slots unused: derived in shared memory)
   const CUtensorMap om = tma_map2d(ones, c.maxN, 32, N_BK, true);
   const int with_cs = dbM ? 1 : 0;
-  MnDMx op{blob, partial, cs, R, F, 0, with_cs};
-  nrun(st, mp, om, op, kMnDMxSplits * (R / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + with_cs));
-  const RJob j0{partial, kMnDMxSplits, count, dMx, 0}, j1{cs, kMnDMxSplits, with_cs ? R : 0, dbM, 0},
+  MnDMx op{blob, partial, cs, R, F, 0, with_cs, ns};
+  nrun(st, mp, om, op, ns * (R / N_BM) * ((F + MnDMx::BN - 1) / MnDMx::BN + with_cs));
+  const RJob j0{partial, ns, count, dMx, 0}, j1{cs, ns, with_cs ? R : 0, dbM, 0},
       j2{nullptr, 0, 0, nullptr, 0};
   launch_ex(k_reduce_jobs, reduce_blocks(j0) + (with_cs ? reduce_blocks(j1) : 0), 32 * RW, 0, st, j0, j1, j2);
   g_launches += 1;

@@ -80,6 +80,9 @@ SIGNATURES = {
     "hg_abi_version": [],
     "hg_store_create": [ctypes.POINTER(hg_store_desc), _I32, _I32, ctypes.POINTER(_P)],
     "hg_store_destroy": [_P],
+    "hg_store_create_shared": [ctypes.POINTER(hg_store_desc), ctypes.c_char_p, _I32, _I32, ctypes.POINTER(_P)],
+    "hg_store_open_shared": [ctypes.c_char_p, _I32, ctypes.POINTER(_P)],
+    "hg_store_unlink_shared": [ctypes.c_char_p],
     "hg_store_stats": [_P, _I64P, _I64P, _I64P, _I32P, _I32P],
     "hg_degree_stat": [_P, _P, _I64, _DP],
     "hg_degree_stat_linear": [_P, _P, _I64, _DP],
@@ -218,7 +221,9 @@ class Store:
     """Table-1 store. Borrows the numpy arrays (copy=0) and
     keeps them alive for the store's lifetime."""
 
-    def __init__(self, data: dict, copy: bool = False, threads: int = 0):
+    def __init__(self, data: dict, copy: bool = False, threads: int = 0, shared_name: str = None, pin: bool = False):
+        """shared_name: create the POSIX shared-memory store of that name (hg_store_create_shared;
+        other processes attach with Store.open_shared); the arrays are copied into it."""
         load()
         self._arrays = {
             "node_offset": np.ascontiguousarray(data["node_offset"], np.int64),
@@ -240,6 +245,12 @@ class Store:
                           edge_index=a["edge_index"].ctypes.data, edge_attr=a["edge_attr"].ctypes.data,
                           y=a["y"].ctypes.data, y_node=a["y_node"].ctypes.data if "y_node" in a else None)
         h = ctypes.c_void_p()
+        if shared_name:
+            _check(_lib.hg_store_create_shared(ctypes.byref(d), shared_name.encode(), int(pin), int(threads),
+                                               ctypes.byref(h)))
+            self.handle = h
+            self._arrays = None
+            return
         _check(_lib.hg_store_create(ctypes.byref(d), int(copy), int(threads), ctypes.byref(h)))
         self.handle = h
         if copy:
@@ -254,6 +265,19 @@ class Store:
         _check(_lib.hg_store_stats(handle, ctypes.byref(g), ctypes.byref(n), ctypes.byref(e), ctypes.byref(mn),
                                    ctypes.byref(md)))
         return s
+
+    @classmethod
+    def open_shared(cls, name: str, pin: bool = False) -> "Store":
+        """Attach to a store another process created with shared_name (hg_store_open_shared)."""
+        load()
+        h = ctypes.c_void_p()
+        _check(_lib.hg_store_open_shared(name.encode(), int(pin), ctypes.byref(h)))
+        return cls._adopt(h)
+
+    @staticmethod
+    def unlink_shared(name: str):
+        load()
+        _check(_lib.hg_store_unlink_shared(name.encode()))
 
     @classmethod
     def from_container(cls, path: str, threads: int = 0) -> "Store":
