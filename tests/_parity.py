@@ -67,7 +67,17 @@ class StepResult(dict):
     pass
 
 
-def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=False, tau_arg=1e-6):
+def adam_ratio_bound(t, hyper):
+    """Largest |m^_t / sqrt(v^_t)| any gradient sequence can give at Adam step t (Cauchy-Schwarz
+    on m_t = (1-b1) sum_k b1^k g_(t-k), v_t = (1-b2) sum_k b2^k g_(t-k)^2, with the bias
+    corrections): 1 at t = 1, slightly above 1 later (b1^2 < b2)."""
+    b1, b2 = hyper["beta1"], hyper["beta2"]
+    r = sum((b1 * b1 / b2) ** k for k in range(t))
+    return (1 - b1) / np.sqrt(1 - b2) * np.sqrt(r) * np.sqrt(1 - b2 ** t) / (1 - b1 ** t)
+
+
+def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=False, tau_arg=1e-6,
+                    grad_bar=None):
     """One step on GPU (ctx must hold the parameters) and on the oracle from the
     GPU's current parameters / optimizer state. Returns StepResult of metrics."""
     import torch
@@ -147,19 +157,23 @@ def run_step_parity(data, ids, ctx, cfg, delta, hyper=None, do_step=True, graph=
         res["m_normwise"] = {k: normwise(gm[k], newst["m"][k]) for k in g}
         res["v_normwise"] = {k: normwise(gv[k], newst["v"][k]) for k in g}
         # DESIGN.md reading R-adam-eps: theta1 = theta0 (1 - lr wd) - lr m^/(sqrt(v^) + eps) has
-        # sensitivity lr/eps = 1e5 to g at g = 0, so theta1 is compared only where the oracle
-        # gradient is >= 100 eps; elsewhere the GPU's step must respect |m^/(sqrt(v^)+eps)| <= 1
+        # sensitivity lr/eps = 1e5 to g at g = 0 and is ~ -lr sign(g) elsewhere, so theta1 is
+        # compared only where the oracle gradient is >= 100 eps AND its sign is fixed by the
+        # gradient bar (|g| >= grad_bar max|g| of its tensor: the GPU gradient may differ by up to
+        # that much); elsewhere the GPU's step must respect |m^/(sqrt(v^)+eps)| <= 1. The mask
+        # uses oracle values only.
         floor = 100.0 * hyper["eps"]
+        gbar = GRAD_TOL if grad_bar is None else grad_bar
         pn, n_ill, bound_bad = {}, 0, 0
         decay = 1.0 - hyper["lr"] * hyper["weight_decay"]
         for k in g:
-            ok = np.abs(g[k]) >= floor
+            ok = np.abs(g[k]) >= max(floor, gbar * float(np.abs(g[k]).max()))
             a_ = np.asarray(gp[k], np.float64).reshape(g[k].shape)
             n_ill += int((~ok).sum())
             if ok.any():
                 pn[k] = normwise(a_[ok], newp[k][ok])
             step_ = np.abs(a_[~ok] - params[k][~ok] * decay)
-            bound_bad += int((step_ > hyper["lr"] * (1 + 1e-3) + 1e-7).sum())
+            bound_bad += int((step_ > hyper["lr"] * adam_ratio_bound(newst["step"], hyper) * (1 + 1e-3) + 1e-7).sum())
         res["param_normwise"] = pn
         res["adam_ill_conditioned"] = n_ill
         res["adam_step_bound_violations"] = bound_bad

@@ -49,7 +49,7 @@ def test_tf32_mode_parity(torch_cuda, flags, H):
     data = PT.generate("pcqm", 600, 71)
     ctx, cfg, delta = PT.make_ctx(data, 128, H, 6, seed=3, flags=flags)
     ids = O.shard(8, 0, 0, 1, len(data["y"]))[:128]
-    res = PT.run_step_parity(data, ids, ctx, cfg, delta, tau_arg=None)
+    res = PT.run_step_parity(data, ids, ctx, cfg, delta, tau_arg=None, grad_bar=5e-2)
     print("tf32", flags, {k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     # (the decision bands follow the measured forward error, which is ~100x the 3xTF32 one, so
     # more near-tie decisions fall inside them: overrides bounded at 1e-3 of the cells)
