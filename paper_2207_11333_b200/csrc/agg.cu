@@ -6,18 +6,23 @@
 // max, std with variance floor eps_v) and the backward SPEC.md:369-371.
 //
 // Molecules are graph-local and a batch's graphs are contiguous node ranges, so one CTA owns
-// one graph (and one chunk of channels): every row it touches -- the CSR slice, the P rows of
-// the messages' sources, the per-destination gradients -- belongs to its graph. The CTA
-// stages the graph's CSR slice and P rows in shared memory with bulk async copies
-// (cp.async.bulk, one mbarrier), so the rowptr -> col -> P dependency chain runs at
-// shared-memory latency and HBM sees only large contiguous reads and coalesced row writes.
-// A graph larger than the staging capacity runs the same arithmetic straight from global
-// memory (L2), so any graph size is supported.
+// one graph (and one 64-channel chunk): every row it touches -- the CSR slice, the P rows of
+// the messages' sources, the per-destination gradients -- belongs to its graph. Warp 0 stages
+// the graph's CSR slice and P rows in shared memory with bulk async copies (cp.async.bulk, one
+// mbarrier) while the other threads issue their own global loads (weights, the first node's
+// rows), so the rowptr -> col -> P dependency chain runs at shared-memory latency and HBM sees
+// only large contiguous reads and coalesced row writes. One node per half-warp (16 lanes x 4
+// channels): per-node control work is shared by two nodes, channel pairs use the packed
+// fp32x2 pipe. A graph larger than the staging capacity runs the same arithmetic straight from
+// global memory (L2), so any graph size is supported.
 //
-// Determinism: no atomics. Forward: one warp per destination node, fixed edge order. Backward
-// (two phases): each edge's message gradient dm_{j->i} is computed once by its destination's
-// warp into a per-edge buffer (global, L2-resident), then each source sums its edges' dm in its
-// row order (dP_j); dM_e / db_M are per-CTA partials reduced in fixed order afterwards.
+// Determinism: no atomics. Forward: one half-warp per destination node, fixed edge order.
+// Backward (three phases): each edge's message gradient dm_{j->i} is computed once by its
+// destination's half-warp and stored at the same pair's entry of the SOURCE's row (staged
+// graphs: rows in shared memory, source-major, so phase 2 reads them contiguously; larger
+// graphs: the global [E][H] buffer, destination-major); each source sums its row of dm in row
+// order (dP_j); dM_e / db_M are per-CTA partials over the graph's edges, reduced in fixed order
+// afterwards.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -35,29 +40,37 @@ extern std::atomic<int64_t> g_launches;
 
 namespace {
 
-constexpr int kWarps = 8;            // 256 threads per CTA
-constexpr int kCapNodes = 128;       // nodes of one graph staged in shared memory
-constexpr int kCapEdgesFwd = 320;    // its directed edges (forward)
-constexpr int kCapEdgesBwd = 320;    // (backward)
-constexpr int kChFwd = 64;           // channels per forward CTA (2 per lane)
-constexpr int kChBwd = 64;           // channels per backward CTA (2 per lane)
+constexpr int kWarpsF = 4;             // forward: 128 threads per CTA (ncu: with 256, the CTA's
+                                       // last node round left 30% of the warps idle at EXIT)
+constexpr int kHalvesF = 2 * kWarpsF;  // half-warps per CTA: one node per half-warp
+constexpr int kWarpsB = 8;             // backward: 256 threads (its smem holds the dm rows too)
+constexpr int kHalvesB = 2 * kWarpsB;
+constexpr int CPL = 4;                 // channels per lane (16 lanes x 4 = one 64-channel chunk)
+constexpr int kCapNodes = 128;         // nodes of one graph staged in shared memory
+constexpr int kCapEdgesFwd = 320;      // its directed edges (forward)
+constexpr int kCapEdgesBwd = 256;      // (backward: the per-edge dm rows are staged too)
+constexpr int kCh = 64;                // channels per CTA
 
 __host__ __device__ constexpr uint32_t r16(uint32_t b) { return (b + 15u) & ~15u; }
 
 // dynamic shared-memory layout (byte offsets) of one CTA
 struct SmemLayout {
-  uint32_t P, rp, col, ea, pos, slot, dm, total;
+  uint32_t P, dm, rp, col, ea, pos, slot, rev, total;
 };
-__host__ __device__ inline SmemLayout smem_layout(int ch, int cap_n, int cap_e, int Fe, bool bwd) {
+__host__ __device__ inline SmemLayout smem_layout(int cap_n, int cap_e, int Fe, bool bwd) {
   SmemLayout L;
   L.P = 0;
-  L.rp = L.P + (uint32_t)cap_n * ch * 4;
+  L.dm = L.P + (uint32_t)cap_n * kCh * 4;  // (backward: the graph's dm rows, source-major)
+  L.rp = L.dm + (bwd ? (uint32_t)cap_e * kCh * 4 : 0);
   L.col = L.rp + r16((cap_n + 8) * 4);
   L.ea = L.col + r16((cap_e + 8) * 4);
   L.pos = L.ea + r16(cap_e * Fe * 4 + 32);
   L.slot = L.pos + r16((cap_n + 8) * 4);
-  L.dm = L.slot + (bwd ? r16(cap_e + 32) : 0);
-  L.total = L.dm;  // (the backward's per-edge dm rows live in global memory, L2-resident)
+  L.rev = L.slot + (bwd ? r16(cap_e + 32) : 0);
+  L.total = L.rev + (bwd ? r16(cap_e * 2) : 0);
+  // (the backward's partial reduction reuses the area: kHalvesB x 16 lanes x CPL x (Fe + 1))
+  const uint32_t red = (uint32_t)kHalvesB * 16 * CPL * ((Fe <= 4 ? 4 : 8) + 1) * 4;  // (FE template width)
+  if (L.total < red) L.total = red;
   return L;
 }
 
@@ -75,35 +88,42 @@ struct Slice {
   int n0, n1, e0, e1, r0, c0, p0, s0, ea_skip;
 };
 
-// Thread 0: stage rowptr[n0..n1], col/ea/slot[e0..e1), pos[n0..n1) and the graph's P rows
-// (channels [ch0, ch0 + CH)) with bulk copies completing on one mbarrier; then every thread
-// waits for it. Blob arrays start 16-byte aligned and the copies round up to 16 bytes (the
-// overhang stays inside the blob).
-template <int CH>
-__device__ void stage_graph(const BatchView &b, const float *P, int PW, int ch0, const int *pos, bool with_slot,
-                            const SmemLayout &L, uint8_t *sm, uint64_t *bar, const Slice &s, uint32_t parity) {
-  if (threadIdx.x == 0) {
+// Warp 0: stage rowptr[n0..n1], col/ea/slot[e0..e1), pos[n0..n1) and the graph's P rows
+// (channels [ch0, ch0 + 64)) with bulk copies completing on one mbarrier (lane 0 posts the
+// byte count, the lanes issue the row copies in parallel). Blob arrays start 16-byte aligned
+// and the copies round up to 16 bytes (the overhang stays inside the blob). The caller issues
+// its own global loads (weights, first node's rows) before stage_wait.
+__device__ void stage_issue(const BatchView &b, const float *P, int PW, int ch0, const int *pos, bool with_slot,
+                            const SmemLayout &L, uint8_t *sm, uint64_t *bar, const Slice &s) {
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
     const uint32_t brp = r16((uint32_t)(s.n1 + 1 - s.r0) * 4);
     const uint32_t bcol = s.e1 > s.e0 ? r16((uint32_t)(s.e1 - s.c0) * 4) : 0;
     const uint32_t ea_a = ((uint32_t)s.e0 * b.Fe * 4) & ~15u;
     const uint32_t bea = s.e1 > s.e0 ? r16((uint32_t)s.e1 * b.Fe * 4 - ea_a) : 0;
     const uint32_t bpos = r16((uint32_t)(s.n1 - s.p0) * 4);
     const uint32_t bsl = with_slot && s.e1 > s.e0 ? r16((uint32_t)(s.e1 - s.s0)) : 0;
-    const uint32_t brow = CH * 4, bP = (uint32_t)(s.n1 - s.n0) * brow;
-    tc::mbar_expect_tx(bar, bP + brp + bcol + bea + bpos + bsl);
-    if (PW == CH) {
-      bulk_g2s(sm + L.P, P + (size_t)s.n0 * PW, bP, bar);
-    } else {  // (P rows of PW floats: this chunk's CH columns of each row)
-      for (int r = 0; r < s.n1 - s.n0; ++r)
-        bulk_g2s(sm + L.P + r * brow, P + (size_t)(s.n0 + r) * PW + ch0, brow, bar);
+    const int rows = s.n1 - s.n0;
+    const uint32_t brow = kCh * 4, bP = (uint32_t)rows * brow;
+    if (lane == 0) tc::mbar_expect_tx(bar, bP + brp + bcol + bea + bpos + bsl);
+    __syncwarp();
+    if (PW == kCh) {
+      if (lane == 0 && bP) bulk_g2s(sm + L.P, P + (size_t)s.n0 * PW, bP, bar);
+    } else {  // (P rows of PW floats: this chunk's 64 columns of each row, one copy per row)
+      for (int r = lane; r < rows; r += 32) bulk_g2s(sm + L.P + r * brow, P + (size_t)(s.n0 + r) * PW + ch0, brow, bar);
     }
-    bulk_g2s(sm + L.rp, b.rowptr + s.r0, brp, bar);
-    if (bcol) bulk_g2s(sm + L.col, b.col + s.c0, bcol, bar);
-    if (bea) bulk_g2s(sm + L.ea, reinterpret_cast<const uint8_t *>(b.ea) + ea_a, bea, bar);
-    bulk_g2s(sm + L.pos, pos + s.p0, bpos, bar);
-    if (bsl) bulk_g2s(sm + L.slot, b.slot + s.s0, bsl, bar);
+    if (lane == 1) bulk_g2s(sm + L.rp, b.rowptr + s.r0, brp, bar);
+    if (lane == 2 && bcol) bulk_g2s(sm + L.col, b.col + s.c0, bcol, bar);
+    if (lane == 3 && bea) bulk_g2s(sm + L.ea, reinterpret_cast<const uint8_t *>(b.ea) + ea_a, bea, bar);
+    if (lane == 4) bulk_g2s(sm + L.pos, pos + s.p0, bpos, bar);
+    if (lane == 5 && bsl) bulk_g2s(sm + L.slot, b.slot + s.s0, bsl, bar);
   }
-  tc::mbar_wait(bar, parity);
+}
+// one thread polls the mbarrier; the others wait at the CTA barrier (no issue slots spent
+// spinning: ncu showed the 256-thread poll at 10-14% of the kernels' instructions)
+__device__ __forceinline__ void stage_wait(uint64_t *bar, uint32_t parity) {
+  if (threadIdx.x == 0) tc::mbar_wait(bar, parity);
+  __syncthreads();
 }
 
 __device__ __forceinline__ void init_bar(uint64_t *bar) {
@@ -113,79 +133,122 @@ __device__ __forceinline__ void init_bar(uint64_t *bar) {
   }
 }
 
-template <int CPL>
-__device__ __forceinline__ void ld_vec(const float *p, float (&v)[CPL]) {
-  if constexpr (CPL == 4) {
-    const float4 t = *reinterpret_cast<const float4 *>(p);
-    v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
-  } else {
-    const float2 t = *reinterpret_cast<const float2 *>(p);
-    v[0] = t.x; v[1] = t.y;
-  }
+// MUFU approximations without the denormal fix-up (their arguments are normal: the variance
+// floor eps_v > 0, degrees >= 1)
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
-template <int CPL>
-__device__ __forceinline__ void st_vec(float *p, const float (&v)[CPL]) {
-  if constexpr (CPL == 4) *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  else *reinterpret_cast<float2 *>(p) = make_float2(v[0], v[1]);
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 1/d for d = 0..127 (IEEE-rounded, as __frcp_rn), one table per CTA
+__device__ __forceinline__ void fill_rcp(float *t) {
+  if (threadIdx.x < 128) t[threadIdx.x] = threadIdx.x ? __frcp_rn((float)threadIdx.x) : 0.f;
+}
+// (degrees are <= HG_MAX_DEGREE = 127: hg_pack rejects larger ones, HG_E_DEGREE)
+__device__ __forceinline__ float rcp_deg(const float *t, int d) { return t[min(d, 127)]; }
+
+__device__ __forceinline__ float4 ld4(const float *p) { return *reinterpret_cast<const float4 *>(p); }
+__device__ __forceinline__ void st4(float *p, const float (&v)[CPL]) {
+  *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
 }
 template <int FE>
 __device__ __forceinline__ void ld_edge(const float *ea, int Fe, float (&ef)[FE]) {
   if constexpr (FE == 4) {
-    const float4 t = *reinterpret_cast<const float4 *>(ea);
+    const float4 t = ld4(ea);
     ef[0] = t.x; ef[1] = t.y; ef[2] = t.z; ef[3] = t.w;
   } else {
 #pragma unroll
     for (int f = 0; f < FE; ++f) ef[f] = f < Fe ? ea[f] : 0.f;
   }
 }
-// message for CPL channels: m = (P + b_M) + sum_f M_e[:,f] e_f (same order in K2 and K8)
-template <int CPL, int FE>
-__device__ __forceinline__ void message(const float (&pj)[CPL], const float (&bm)[CPL], const float (&me)[CPL][FE],
+// message for the lane's 4 channels: m = (P + b_M) + sum_f M_e[:,f] e_f, f ascending (the same
+// order in K2 and K8); channel pairs on the packed fp32x2 pipe (each lane of a pair rounds as
+// the scalar fadd / fma)
+template <int FE>
+__device__ __forceinline__ void message(const float4 pj, const float2 (&bm)[2], const float2 (&me)[2][FE],
                                         const float (&ef)[FE], float (&m)[CPL]) {
+  float2 v0 = __fadd2_rn(make_float2(pj.x, pj.y), bm[0]);
+  float2 v1 = __fadd2_rn(make_float2(pj.z, pj.w), bm[1]);
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    float v = pj[c] + bm[c];
-#pragma unroll
-    for (int f = 0; f < FE; ++f) v = fmaf(me[c][f], ef[f], v);
-    m[c] = v;
+  for (int f = 0; f < FE; ++f) {
+    const float2 e2 = make_float2(ef[f], ef[f]);
+    v0 = __ffma2_rn(me[0][f], e2, v0);
+    v1 = __ffma2_rn(me[1][f], e2, v1);
   }
+  m[0] = v0.x; m[1] = v0.y; m[2] = v1.x; m[3] = v1.y;
+}
+// the same with M_e read from the CTA's shared copy sme[f][64] (chunk channels; the backward,
+// whose registers hold the per-edge gradient sums instead)
+template <int FE>
+__device__ __forceinline__ void message_sm(const float4 pj, const float2 (&bm)[2], const float *sme, int lc,
+                                           const float (&ef)[FE], float (&m)[CPL]) {
+  float2 v0 = __fadd2_rn(make_float2(pj.x, pj.y), bm[0]);
+  float2 v1 = __fadd2_rn(make_float2(pj.z, pj.w), bm[1]);
+#pragma unroll
+  for (int f = 0; f < FE; ++f) {
+    const float4 w = ld4(sme + f * kCh + lc);
+    const float2 e2 = make_float2(ef[f], ef[f]);
+    v0 = __ffma2_rn(make_float2(w.x, w.y), e2, v0);
+    v1 = __ffma2_rn(make_float2(w.z, w.w), e2, v1);
+  }
+  m[0] = v0.x; m[1] = v0.y; m[2] = v1.x; m[3] = v1.y;
 }
 
 // Graph arrays read either from the staged copy (S) or straight from global memory.
-template <bool S, int CH>
+template <bool S>
 struct View {
   const int *rp, *col, *pos;
   const uint8_t *slot;
+  const uint16_t *rev;  // (backward, staged) in-edge -> the same pair's entry in the source's row
   const float *ea, *P;
-  int r0, c0, p0, s0, e0, n0, Fe, Pstride, ch0;
+  float *dm;
+  int r0, c0, p0, s0, e0, n0, Fe, Pstride, ch0, H;
   __device__ int rowptr(int i) const { return S ? rp[i - r0] : rp[i]; }
   __device__ int colv(int k) const { return S ? col[k - c0] : col[k]; }
   __device__ int posv(int i) const { return S ? pos[i - p0] : pos[i]; }
   __device__ int slotv(int k) const { return S ? slot[k - s0] : slot[k]; }
   __device__ const float *edge(int k) const { return S ? ea + (size_t)(k - e0) * Fe : ea + (size_t)k * Fe; }
   __device__ const float *prow(int j, int lc) const {  // lc = lane's first channel within the chunk
-    return S ? P + (j - n0) * CH + lc : P + (size_t)j * Pstride + ch0 + lc;
+    return S ? P + (j - n0) * kCh + lc : P + (size_t)j * Pstride + ch0 + lc;
   }
+  // message-gradient row k: staged, the graph's rows in shared memory; else the global [E][H]
+  // buffer (L2-resident)
+  __device__ float *dmrow(int k, int lc) const {
+    return S ? dm + (k - e0) * kCh + lc : dm + (size_t)k * H + ch0 + lc;
+  }
+  // where phase 1 stores the gradient of in-edge k (j -> i, k in i's row) and where phase 2
+  // finds that of row-j entry k: staged graphs use source-major order (the row-j entry of the
+  // same pair, so phase 2 reads its rows contiguously); otherwise destination-major
+  __device__ int dm_store(int k) const { return S ? e0 + rev[k - e0] : k; }
+  __device__ int dm_load(int k) const { return S ? k : rowptr(colv(k)) + slotv(k); }
 };
-template <bool S, int CH>
-__device__ View<S, CH> make_view(const BatchView &b, const float *P, int PW, int ch0, const int *pos,
-                                 const SmemLayout &L, uint8_t *sm, const Slice &s) {
-  View<S, CH> v;
+template <bool S>
+__device__ View<S> make_view(const BatchView &b, const float *P, int PW, int ch0, const int *pos, const SmemLayout &L,
+                             uint8_t *sm, const Slice &s, float *dmbuf, int H) {
+  View<S> v;
   v.Fe = b.Fe;
   v.ch0 = ch0;
   v.Pstride = PW;
   v.n0 = s.n0;
   v.e0 = s.e0;
+  v.H = H;
   if constexpr (S) {
     v.rp = reinterpret_cast<const int *>(sm + L.rp);
     v.col = reinterpret_cast<const int *>(sm + L.col);
     v.pos = reinterpret_cast<const int *>(sm + L.pos);
     v.slot = sm + L.slot;
+    v.rev = reinterpret_cast<const uint16_t *>(sm + L.rev);
     v.ea = reinterpret_cast<const float *>(sm + L.ea) + s.ea_skip;
     v.P = reinterpret_cast<const float *>(sm + L.P);
+    v.dm = reinterpret_cast<float *>(sm + L.dm);
     v.r0 = s.r0; v.c0 = s.c0; v.p0 = s.p0; v.s0 = s.s0;
   } else {
-    v.rp = b.rowptr; v.col = b.col; v.pos = pos; v.slot = b.slot; v.ea = b.ea; v.P = P;
+    v.rp = b.rowptr; v.col = b.col; v.pos = pos; v.slot = b.slot; v.ea = b.ea; v.P = P; v.dm = dmbuf;
     v.r0 = v.c0 = v.p0 = v.s0 = 0;
   }
   return v;
@@ -206,15 +269,28 @@ __device__ __forceinline__ Slice slice_of(const BatchView &b, const int4 *gslice
   return s;
 }
 
+// M_e (this lane's 4 channels as packed pairs) and b_M
+template <int FE>
+__device__ __forceinline__ void load_edge_weights(const float *Me, const float *bM, int ch, int Fe, float2 (&me)[2][FE],
+                                                  float2 (&bm)[2]) {
+  bm[0] = make_float2(bM[ch], bM[ch + 1]);
+  bm[1] = make_float2(bM[ch + 2], bM[ch + 3]);
+#pragma unroll
+  for (int f = 0; f < FE; ++f) {
+    me[0][f] = f < Fe ? make_float2(Me[ch * Fe + f], Me[(ch + 1) * Fe + f]) : make_float2(0.f, 0.f);
+    me[1][f] = f < Fe ? make_float2(Me[(ch + 2) * Fe + f], Me[(ch + 3) * Fe + f]) : make_float2(0.f, 0.f);
+  }
+}
+
 // ---------------------------------------------------------------- K2 forward
-// Per destination node i (one warp), lanes over CPL = 4 channels each: messages
+// Per destination node i (one half-warp; 16 lanes x 4 channels), messages
 // m = P[j] + b_M + M_e e_ji over the CSR row (j ascending) are recomputed, never stored in
 // memory; pass 1: sum, min, max with first-position argmin / argmax; pass 2:
-// the centred sum of squares (two-pass variance). Rows of degree <= 4 (molecules:
-// all but hubs) keep their messages in registers between the passes; larger rows recompute
-// them. d = 0 -> all aggregates 0 (C5). Writes A at the degree-sorted row pos[i]
-// ([mean | min | max | std], 4H) and arg[i] ([argmin | argmax with bit 7 = var > eps_v], 2H).
-template <int CPL>
+// the centred sum of squares (two-pass variance). When both nodes of a warp have
+// degree <= 4 (molecules: all but hubs) the messages stay in registers between the passes;
+// otherwise they are recomputed. d = 0 -> all aggregates 0 (C5). Writes A at the
+// degree-sorted row pos[i] ([mean | min | max | std], 4H) and arg[i] ([argmin | argmax with
+// bit 7 = var > eps_v], 2H bytes).
 __device__ __forceinline__ void fold(const float (&m)[CPL], int p, float (&sum)[CPL], float (&mx)[CPL],
                                      float (&mn)[CPL], int (&amx)[CPL], int (&amn)[CPL]) {
 #pragma unroll
@@ -222,6 +298,13 @@ __device__ __forceinline__ void fold(const float (&m)[CPL], int p, float (&sum)[
     sum[c] += m[c];
     if (m[c] > mx[c]) { mx[c] = m[c]; amx[c] = p; }
     if (m[c] < mn[c]) { mn[c] = m[c]; amn[c] = p; }
+  }
+}
+__device__ __forceinline__ void centred(const float (&m)[CPL], const float (&sum)[CPL], float rd, float (&ss)[CPL]) {
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const float t = m[c] - sum[c] * rd;
+    ss[c] = fmaf(t, t, ss[c]);
   }
 }
 
@@ -236,16 +319,25 @@ struct SelfIn {
 };
 
 template <bool S, bool SELF, int FE>
-__device__ void fwd_nodes(const View<S, kChFwd> &v, const Slice &s, const float (&me)[2][FE], const float (&bm)[2],
-                          float var_floor, float *A, uint8_t *arg, int H, int Hl, int KA, const SelfIn &si) {
-  constexpr int CPL = 2, RM = 4;  // RM: messages held in registers
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lc = lane * CPL, ch = v.ch0 + lc;
-  for (int i = s.n0 + warp; i < s.n1; i += kWarps) {
-    const int k0 = v.rowptr(i), k1 = v.rowptr(i + 1), d = k1 - k0;
-    const int prow = v.posv(i);
-    float q[CPL] = {0.f, 0.f}, xi[CPL] = {0.f, 0.f};
-    if (SELF) {  // (issued early: hidden behind the edge loop)
-      ld_vec<CPL>(si.P + (size_t)i * si.PW + H + ch, q);
+__device__ void fwd_nodes(const View<S> &v, const Slice &s, const float2 (&me)[2][FE], const float2 (&bm)[2],
+                          float var_floor, float *A, uint8_t *arg, int H, int Hl, int KA, const SelfIn &si,
+                          const float *rcp) {
+  constexpr int RM = 4;  // messages held in registers
+  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4, lc = hl * CPL, ch = v.ch0 + lc;
+  const int n = s.n1 - s.n0;
+  for (int t = 0; t < n; t += kHalvesF) {  // (trip count uniform over the CTA)
+    const int i = s.n0 + t + hw;
+    const bool valid = t + hw < n;
+    int k0 = 0, d = 0, prow = 0;
+    if (valid) {
+      k0 = v.rowptr(i);
+      d = v.rowptr(i + 1) - k0;
+      prow = v.posv(i);
+    }
+    float q[CPL] = {0.f, 0.f, 0.f, 0.f}, xi[CPL] = {0.f, 0.f, 0.f, 0.f};
+    if (SELF && valid) {  // (issued early: hidden behind the edge loop)
+      const float4 t4 = ld4(si.P + (size_t)i * si.PW + H + ch);
+      q[0] = t4.x; q[1] = t4.y; q[2] = t4.z; q[3] = t4.w;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) xi[c] = ch + c < si.Fl ? si.xin[(size_t)i * si.Fl + ch + c] : 0.f;
     }
@@ -255,58 +347,50 @@ __device__ void fwd_nodes(const View<S, kChFwd> &v, const Slice &s, const float 
     for (int c = 0; c < CPL; ++c) {
       sum[c] = 0.f; mx[c] = -INFINITY; mn[c] = INFINITY; amx[c] = 0; amn[c] = 0; ss[c] = 0.f;
     }
-    const float rd = d > 0 ? __frcp_rn((float)d) : 0.f;
-    if (d <= RM) {  // (warp-uniform) one load pass, messages kept for the variance pass
+    const float rd = rcp_deg(rcp, d);
+    const int dw = __reduce_max_sync(0xffffffffu, d);  // the warp's largest degree (uniform)
+    if (dw <= RM) {  // one load pass, messages kept for the variance pass
       float m[RM][CPL];
 #pragma unroll
       for (int e = 0; e < RM; ++e) {
-        if (e < d) {
+        if (e < dw && e < d) {
           const int j = v.colv(k0 + e);
-          float ef[FE], pj[CPL];
+          float ef[FE];
           ld_edge<FE>(v.edge(k0 + e), v.Fe, ef);
-          ld_vec<CPL>(v.prow(j, lc), pj);
-          message<CPL, FE>(pj, bm, me, ef, m[e]);
+          message<FE>(ld4(v.prow(j, lc)), bm, me, ef, m[e]);
         }
       }
+      // position 0 initialises (d = 0 rows are overwritten below)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) { sum[c] = m[0][c]; mx[c] = m[0][c]; mn[c] = m[0][c]; }
+#pragma unroll
+      for (int e = 1; e < RM; ++e)
+        if (e < dw && e < d) fold(m[e], e, sum, mx, mn, amx, amn);
 #pragma unroll
       for (int e = 0; e < RM; ++e)
-        if (e < d) fold<CPL>(m[e], e, sum, mx, mn, amx, amn);
-#pragma unroll
-      for (int e = 0; e < RM; ++e)
-        if (e < d) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            const float t = m[e][c] - sum[c] * rd;
-            ss[c] = fmaf(t, t, ss[c]);
-          }
-        }
+        if (e < dw && e < d) centred(m[e], sum, rd, ss);
     } else {
-      for (int k = k0; k < k1; ++k) {
+      for (int k = k0; k < k0 + d; ++k) {
         const int j = v.colv(k);
-        float ef[FE], pj[CPL], m[CPL];
+        float ef[FE], m[CPL];
         ld_edge<FE>(v.edge(k), v.Fe, ef);
-        ld_vec<CPL>(v.prow(j, lc), pj);
-        message<CPL, FE>(pj, bm, me, ef, m);
-        fold<CPL>(m, k - k0, sum, mx, mn, amx, amn);
+        message<FE>(ld4(v.prow(j, lc)), bm, me, ef, m);
+        fold(m, k - k0, sum, mx, mn, amx, amn);
       }
-      for (int k = k0; k < k1; ++k) {  // pass 2: recompute the messages
+      for (int k = k0; k < k0 + d; ++k) {  // pass 2: recompute the messages
         const int j = v.colv(k);
-        float ef[FE], pj[CPL], m[CPL];
+        float ef[FE], m[CPL];
         ld_edge<FE>(v.edge(k), v.Fe, ef);
-        ld_vec<CPL>(v.prow(j, lc), pj);
-        message<CPL, FE>(pj, bm, me, ef, m);
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          const float t = m[c] - sum[c] * rd;
-          ss[c] = fmaf(t, t, ss[c]);
-        }
+        message<FE>(ld4(v.prow(j, lc)), bm, me, ef, m);
+        centred(m, sum, rd, ss);
       }
     }
+    if (!valid) continue;
     float mean[CPL], sd[CPL];
-    int flag[CPL];
+    uint32_t flags = 0;
     if (d == 0) {
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) { mean[c] = 0.f; mx[c] = 0.f; mn[c] = 0.f; sd[c] = 0.f; flag[c] = 0; }
+      for (int c = 0; c < CPL; ++c) { mean[c] = 0.f; mx[c] = 0.f; mn[c] = 0.f; sd[c] = 0.f; }
     } else {
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
@@ -314,30 +398,31 @@ __device__ void fwd_nodes(const View<S, kChFwd> &v, const Slice &s, const float 
         mx[c] += q[c];
         mn[c] += q[c];
         const float var = ss[c] * rd;
-        flag[c] = var > var_floor;
+        flags |= (var > var_floor ? 0x80u : 0u) << (8 * c);
         // channels >= Hl are padding (internal width H > logical Hl): their messages are
         // exactly 0, and their std is forced to 0 instead of sqrt(var_floor) so that no
-        // gradient reaches the zero padded parameters (SURVEY §8(d) padding hazard)
-        // (sqrt as v * rsqrt(v): two MUFU-based instructions instead of the IEEE sqrt sequence,
-        // ~2 ulp -- ncu: the IEEE sqrtf was 14% of this kernel's instructions)
+        // gradient reaches the zero padded parameters (SURVEY §8(d) padding hazard).
+        // (sqrt as v * rsqrt(v), ~2 ulp: the IEEE sqrtf sequence was 14% of the instructions)
         const float vf = fmaxf(var, var_floor);
-        sd[c] = ch + c < Hl ? vf * rsqrtf(vf) : 0.f;
+        sd[c] = ch + c < Hl ? vf * rsqrt_ftz(vf) : 0.f;
       }
     }
     float *Ai = A + (size_t)prow * KA + ch;
-    st_vec<CPL>(Ai, mean);
-    st_vec<CPL>(Ai + H, mn);
-    st_vec<CPL>(Ai + 2 * H, mx);
-    st_vec<CPL>(Ai + 3 * H, sd);
-    if (SELF) st_vec<CPL>(Ai + 4 * H, xi);
+    st4(Ai, mean);
+    st4(Ai + H, mn);
+    st4(Ai + 2 * H, mx);
+    st4(Ai + 3 * H, sd);
+    if (SELF) st4(Ai + 4 * H, xi);
     uint8_t *ai = arg + (size_t)i * (2 * H) + ch;
-    *reinterpret_cast<uchar2 *>(ai) = make_uchar2(amn[0], amn[1]);
-    *reinterpret_cast<uchar2 *>(ai + H) = make_uchar2(amx[0] | (flag[0] << 7), amx[1] | (flag[1] << 7));
+    *reinterpret_cast<uint32_t *>(ai) = (uint32_t)amn[0] | (uint32_t)amn[1] << 8 | (uint32_t)amn[2] << 16 |
+                                        (uint32_t)amn[3] << 24;
+    *reinterpret_cast<uint32_t *>(ai + H) =
+        ((uint32_t)amx[0] | (uint32_t)amx[1] << 8 | (uint32_t)amx[2] << 16 | (uint32_t)amx[3] << 24) | flags;
   }
 }
 
 template <bool SELF, int FE>
-__global__ void __launch_bounds__(32 * kWarps, 4) k_agg_fwd(const uint8_t *__restrict__ blob,
+__global__ void __launch_bounds__(32 * kWarpsF, 4) k_agg_fwd(const uint8_t *__restrict__ blob,
                                                             const int4 *__restrict__ gslice,
                                                             const float *__restrict__ P, const float *__restrict__ Me,
                                                             const float *__restrict__ bM, float var_floor,
@@ -345,149 +430,187 @@ __global__ void __launch_bounds__(32 * kWarps, 4) k_agg_fwd(const uint8_t *__res
                                                             const int *__restrict__ pos, int Hl, int KA, SelfIn si) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
+  __shared__ float rcp[128];
   pdl_enter();
   const BatchView b = load_batch(blob);
-  constexpr int CPL = 2;
-  const int lane = threadIdx.x & 31, nch = H / kChFwd, PW = si.PW;
-  const int Fe = b.Fe;
-  const SmemLayout L = smem_layout(kChFwd, kCapNodes, kCapEdgesFwd, Fe, false);
+  const int nch = H / kCh, PW = si.PW;
+  const SmemLayout L = smem_layout(kCapNodes, kCapEdgesFwd, b.Fe, false);
   if (SELF && !si.xin) si.xin = b.x;  // layer 0: the batch's node features
   init_bar(&bar);
-  const uint32_t parity = 0;
-  {  // one work item (graph, channel chunk) per CTA
-    const int item = blockIdx.x;
-    if (item >= b.B * nch) return;
-    __syncthreads();  // (the barrier's initialisation is visible)
-    const int g = item / nch, ch0 = (item - g * nch) * kChFwd, ch = ch0 + lane * CPL;
-    const Slice s = slice_of(b, gslice, g);
-    const bool staged = s.n1 - s.n0 <= kCapNodes && s.e1 - s.e0 <= kCapEdgesFwd;  // uniform per CTA
-    if (staged) stage_graph<kChFwd>(b, P, PW, ch0, pos, false, L, sm, &bar, s, parity);
-    float me[CPL][FE], bm[CPL];
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      bm[c] = bM[ch + c];
-#pragma unroll
-      for (int f = 0; f < FE; ++f) me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f;
-    }
-    if (staged)
-      fwd_nodes<true, SELF, FE>(make_view<true, kChFwd>(b, P, PW, ch0, pos, L, sm, s), s, me, bm, var_floor, A, arg, H,
-                                Hl, KA, si);
-    else
-      fwd_nodes<false, SELF, FE>(make_view<false, kChFwd>(b, P, PW, ch0, pos, L, sm, s), s, me, bm, var_floor, A, arg,
-                                 H, Hl, KA, si);
-  }
+  // one work item (graph, channel chunk) per CTA
+  const int item = blockIdx.x;
+  if (item >= b.B * nch) return;
+  __syncthreads();  // (the barrier's initialisation is visible)
+  const int g = item / nch, ch0 = (item - g * nch) * kCh, ch = ch0 + (threadIdx.x & 15) * CPL;
+  const Slice s = slice_of(b, gslice, g);
+  const bool staged = s.n1 - s.n0 <= kCapNodes && s.e1 - s.e0 <= kCapEdgesFwd;  // uniform per CTA
+  if (staged) stage_issue(b, P, PW, ch0, pos, false, L, sm, &bar, s);
+  float2 me[2][FE], bm[2];
+  load_edge_weights<FE>(Me, bM, ch, b.Fe, me, bm);  // (in flight with the staging copies)
+  fill_rcp(rcp);
+  if (staged) stage_wait(&bar, 0);
+  else __syncthreads();
+  if (staged)
+    fwd_nodes<true, SELF, FE>(make_view<true>(b, P, PW, ch0, pos, L, sm, s, nullptr, H), s, me, bm, var_floor, A, arg,
+                              H, Hl, KA, si, rcp);
+  else
+    fwd_nodes<false, SELF, FE>(make_view<false>(b, P, PW, ch0, pos, L, sm, s, nullptr, H), s, me, bm, var_floor, A,
+                               arg, H, Hl, KA, si, rcp);
 }
 
 // ---------------------------------------------------------------- K8 backward
-// Phase 1, one warp per DESTINATION node i (lanes over CPL = 2 channels): its gradients
-// dA_i, mu_i, sigma_i and decisions are read once (coalesced rows; the next node's are
-// requested before this node is processed), and for each in-edge (j -> i) at row position p
+// Phase 1, one half-warp per DESTINATION node i (16 lanes x 4 channels): its gradients dA_i,
+// mu_i, sigma_i and decisions are read once (coalesced rows; the next node's are requested
+// before this node is processed), and for each in-edge (j -> i) at row position p
 // (SURVEY §8(a10)):
 //   dm = dA_mean[i]/d_i + [p = argmax_i] dA_max[i] + [p = argmin_i] dA_min[i]
 //        + [var_i > eps_v] dA_std[i] (m - mu_i)/(d_i sigma_i)
 // with the message m recomputed from the staged P rows; dm goes to the per-edge buffer
 // (destination-major like the CSR, [E][H], L2-resident) and into this CTA's dM_e = sum dm e^T
 // and db_M = sum dm partials.
-// Phase 2, one warp per SOURCE node j: dP_j = sum over its CSR row (edges j -> i, i = col[k])
-// of dm at i's row position slot[k] (where phase 1 stored it), in row order.
-struct DstIn {  // one destination's per-channel inputs (CPL = 2)
-  float2 gmean, gmin, gmax, gstd, mu, sg, q;
-  uchar2 amn, amx;
-  int k0, k1;
+// Phase 2, one half-warp per SOURCE node j: dP_j = sum over its CSR row (edges j -> i,
+// i = col[k]) of dm at i's row position slot[k] (where phase 1 stored it), in row order.
+struct DstIn {  // one destination's per-channel inputs
+  float4 gmean, gmin, gmax, gstd, mu, sg, q;
+  uint32_t amn, amx;
+  int k0, d;
 };
-template <bool S, bool SELF>
-__device__ __forceinline__ DstIn load_dst(const View<S, kChBwd> &v, int i, const float *A, const uint8_t *arg,
-                                          const float *dA, int H, int ch, int KA, const float *Q, int PW) {
+// rp / ps: rowptr and pos, either the staged copies (offsets r0 / p0) or global memory (0)
+template <bool SELF>
+__device__ __forceinline__ DstIn load_dst(const int *rp, int r0, const int *ps, int p0, int i, bool valid,
+                                          const float *A, const uint8_t *arg, const float *dA, int H, int ch, int KA,
+                                          const float *Q, int PW) {
   DstIn t;
-  t.k0 = v.rowptr(i);
-  t.k1 = v.rowptr(i + 1);
+  if (!valid) {
+    t.k0 = 0;
+    t.d = 0;
+    return t;
+  }
   const float *dAi = dA + (size_t)i * KA + ch;
-  const float *Ai = A + (size_t)v.posv(i) * KA + ch;
-  t.q = SELF ? *reinterpret_cast<const float2 *>(Q + (size_t)i * PW + ch) : make_float2(0.f, 0.f);
-  t.gmean = *reinterpret_cast<const float2 *>(dAi);
-  t.gmin = *reinterpret_cast<const float2 *>(dAi + H);
-  t.gmax = *reinterpret_cast<const float2 *>(dAi + 2 * H);
-  t.gstd = *reinterpret_cast<const float2 *>(dAi + 3 * H);
-  t.mu = *reinterpret_cast<const float2 *>(Ai);
-  t.sg = *reinterpret_cast<const float2 *>(Ai + 3 * H);
-  t.amn = *reinterpret_cast<const uchar2 *>(arg + (size_t)i * (2 * H) + ch);
-  t.amx = *reinterpret_cast<const uchar2 *>(arg + (size_t)i * (2 * H) + H + ch);
+  t.gmean = ld4(dAi);
+  t.gmin = ld4(dAi + H);
+  t.gmax = ld4(dAi + 2 * H);
+  t.gstd = ld4(dAi + 3 * H);
+  t.amn = *reinterpret_cast<const uint32_t *>(arg + (size_t)i * (2 * H) + ch);
+  t.amx = *reinterpret_cast<const uint32_t *>(arg + (size_t)i * (2 * H) + H + ch);
+  t.q = SELF ? ld4(Q + (size_t)i * PW + ch) : make_float4(0.f, 0.f, 0.f, 0.f);
+  t.k0 = rp[i - r0];
+  t.d = rp[i + 1 - r0] - t.k0;
+  const float *Ai = A + (size_t)ps[i - p0] * KA + ch;
+  t.mu = ld4(Ai);
+  t.sg = ld4(Ai + 3 * H);
   return t;
 }
+__device__ __forceinline__ void f4(const float4 a, float (&v)[CPL]) { v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; }
 
-// (self-term: Qp = the [P | Q] buffer's Q half (stride PW), the messages include Q_i, and the
-// destination's dQ_i = dA_mean + dA_min + dA_max (d > 0, else 0) goes to dPQ[i][H + ch])
+// one destination's in-edges (self-term: Qp = the [P | Q] buffer's Q half (stride PW), the
+// messages include Q_i, and the destination's dQ_i = dA_mean + dA_min + dA_max (d > 0, else 0)
+// goes to dPQ[i][H + ch])
 template <bool S, bool SELF, int FE>
-__device__ void bwd_phase1(const View<S, kChBwd> &v, const Slice &s, const float (&me)[2][FE], const float (&bm)[2],
-                           const float *A, const uint8_t *arg, const float *dA, int H, float *dmbuf,
-                           float (&acc)[2][FE], float (&bsum)[2], int KA, const float *Qp, int PW, float *dPQ) {
-  constexpr int CPL = 2;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lc = lane * CPL, ch = v.ch0 + lc;
-  int i = s.n0 + warp;
-  if (i >= s.n1) return;
-  DstIn cur = load_dst<S, SELF>(v, i, A, arg, dA, H, ch, KA, Qp, PW);
-  for (; i < s.n1; i += kWarps) {
-    DstIn nxt;
-    if (i + kWarps < s.n1) nxt = load_dst<S, SELF>(v, i + kWarps, A, arg, dA, H, ch, KA, Qp, PW);  // in flight meanwhile
-    const int d = cur.k1 - cur.k0;
-    if (SELF)
-      *reinterpret_cast<float2 *>(dPQ + (size_t)i * PW + H + ch) =
-          d > 0 ? make_float2(cur.gmean.x + cur.gmin.x + cur.gmax.x, cur.gmean.y + cur.gmin.y + cur.gmax.y)
-                : make_float2(0.f, 0.f);
-    if (d > 0) {
-      const float inv_d = __frcp_rn((float)d);
-      const float gm[CPL] = {cur.gmean.x * inv_d, cur.gmean.y * inv_d};
-      const float gx[CPL] = {cur.gmax.x, cur.gmax.y}, gn[CPL] = {cur.gmin.x, cur.gmin.y};
-      const float mu[CPL] = {cur.mu.x - cur.q.x, cur.mu.y - cur.q.y};  // (m below excludes Q_i)
-      const int an[CPL] = {cur.amn.x, cur.amn.y}, ax[CPL] = {cur.amx.x, cur.amx.y};
-      // (fast division: ~2 ulp, no IEEE reciprocal sequence)
-      const float gs[CPL] = {(ax[0] & 0x80) ? __fdividef(cur.gstd.x * inv_d, cur.sg.x) : 0.f,
-                             (ax[1] & 0x80) ? __fdividef(cur.gstd.y * inv_d, cur.sg.y) : 0.f};
-      for (int k = cur.k0; k < cur.k1; ++k) {
-        const int j = v.colv(k), p = k - cur.k0;
-        float ef[FE], pj[CPL], m[CPL], dm[CPL];
-        ld_edge<FE>(v.edge(k), v.Fe, ef);
-        ld_vec<CPL>(v.prow(j, lc), pj);
-        message<CPL, FE>(pj, bm, me, ef, m);
+__device__ __forceinline__ void bwd_dst(const View<S> &v, const DstIn &cur, int i, bool valid, int lc, int ch,
+                                        const float *sme, const float2 (&bm)[2], int H, int PW, float *dPQ,
+                                        const float *rcp) {
+  const int d = cur.d;
+  if (SELF && valid)
+    *reinterpret_cast<float4 *>(dPQ + (size_t)i * PW + H + ch) =
+        d > 0 ? make_float4(cur.gmean.x + cur.gmin.x + cur.gmax.x, cur.gmean.y + cur.gmin.y + cur.gmax.y,
+                            cur.gmean.z + cur.gmin.z + cur.gmax.z, cur.gmean.w + cur.gmin.w + cur.gmax.w)
+              : make_float4(0.f, 0.f, 0.f, 0.f);
+  if (d <= 0) return;
+  const float inv_d = rcp_deg(rcp, d);
+  float gm[CPL], gx[CPL], gn[CPL], mu[CPL], q[CPL], gstd[CPL], sg[CPL], gs[CPL];
+  int an[CPL], ax[CPL];
+  f4(cur.gmean, gm); f4(cur.gmax, gx); f4(cur.gmin, gn); f4(cur.mu, mu); f4(cur.q, q); f4(cur.gstd, gstd);
+  f4(cur.sg, sg);
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          float gg = gm[c];
-          if ((ax[c] & 0x7f) == p) gg += gx[c];
-          if (an[c] == p) gg += gn[c];
-          if (ax[c] & 0x80) gg += gs[c] * (m[c] - mu[c]);
-          dm[c] = gg;
-          bsum[c] += gg;
+  for (int c = 0; c < CPL; ++c) {
+    gm[c] *= inv_d;
+    mu[c] -= q[c];  // (m below excludes Q_i)
+    an[c] = (cur.amn >> (8 * c)) & 0xff;
+    ax[c] = (cur.amx >> (8 * c)) & 0xff;
+    // (approximate reciprocal, ~1 ulp: sigma >= sqrt(eps_v) is normal)
+    gs[c] = (ax[c] & 0x80) ? gstd[c] * inv_d * rcp_ftz(sg[c]) : 0.f;
+    ax[c] &= 0x7f;
+  }
+  for (int p = 0; p < d; ++p) {
+    const int k = cur.k0 + p, j = v.colv(k);
+    float ef[FE], m[CPL], dm[CPL];
+    ld_edge<FE>(v.edge(k), v.Fe, ef);
+    message_sm<FE>(ld4(v.prow(j, lc)), bm, sme, lc, ef, m);
 #pragma unroll
-          for (int f = 0; f < FE; ++f) acc[c][f] = fmaf(gg, ef[f], acc[c][f]);
-        }
-        st_vec<CPL>(dmbuf + (size_t)k * H + ch, dm);
-      }
+    for (int c = 0; c < CPL; ++c) {
+      float gg = gm[c];
+      if (ax[c] == p) gg += gx[c];
+      if (an[c] == p) gg += gn[c];
+      dm[c] = fmaf(gs[c], m[c] - mu[c], gg);  // (gs = 0 when var <= eps_v)
     }
-    cur = nxt;
+    st4(v.dmrow(v.dm_store(k), lc), dm);
+  }
+}
+
+// nodes t + hw (t = 0, 16, 32, ...): two register sets alternate (no copies), the next node's
+// rows in flight while this one is processed; `first` = the first node's rows, loaded by the
+// caller before the staging wait
+template <bool S, bool SELF, int FE>
+__device__ void bwd_phase1(const View<S> &v, const Slice &s, const float *sme, const float2 (&bm)[2],
+                           const float *A, const uint8_t *arg, const float *dA, int H, int KA, const float *Qp,
+                           int PW, float *dPQ, const float *rcp,
+                           const DstIn &first) {
+  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4, lc = hl * CPL, ch = v.ch0 + lc;
+  const int n = s.n1 - s.n0;
+  DstIn a = first, b;
+  for (int t = 0; t < n; t += 2 * kHalvesB) {
+    const int i0 = s.n0 + t + hw, i1 = i0 + kHalvesB, i2 = i1 + kHalvesB;
+    b = load_dst<SELF>(v.rp, v.r0, v.pos, v.p0, i1, t + kHalvesB + hw < n, A, arg, dA, H, ch, KA, Qp, PW);
+    bwd_dst<S, SELF, FE>(v, a, i0, t + hw < n, lc, ch, sme, bm, H, PW, dPQ, rcp);
+    if (t + kHalvesB >= n) break;
+    a = load_dst<SELF>(v.rp, v.r0, v.pos, v.p0, i2, t + 2 * kHalvesB + hw < n, A, arg, dA, H, ch, KA, Qp, PW);
+    bwd_dst<S, SELF, FE>(v, b, i1, t + kHalvesB + hw < n, lc, ch, sme, bm, H, PW, dPQ, rcp);
   }
 }
 
 template <bool S>
-__device__ void bwd_phase2(const View<S, kChBwd> &v, const Slice &s, const float *dmbuf, float *dP, int H,
-                           const int *dp_pos, int PW) {
-  constexpr int CPL = 2;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, lc = lane * CPL, ch = v.ch0 + lc;
-  for (int j = s.n0 + warp; j < s.n1; j += kWarps) {
+__device__ void bwd_phase2(const View<S> &v, const Slice &s, float *dP, int H, const int *dp_pos, int PW) {
+  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4, lc = hl * CPL, ch = v.ch0 + lc;
+  for (int j = s.n0 + hw; j < s.n1; j += kHalvesB) {
     const int k0 = v.rowptr(j), k1 = v.rowptr(j + 1);
-    float dp[CPL] = {0.f, 0.f};
-    for (int k = k0; k < k1; ++k) {
-      const int kd = v.rowptr(v.colv(k)) + v.slotv(k);  // edge j -> i in i's row
-      float dm[CPL];
-      ld_vec<CPL>(dmbuf + (size_t)kd * H + ch, dm);
+    float dp[CPL] = {0.f, 0.f, 0.f, 0.f};
+    for (int k = k0; k < k1; k += 4) {  // (four edges' loads in flight; sums in row order)
+      float4 r[4];
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) dp[c] += dm[c];
+      for (int u = 0; u < 4; ++u)
+        if (k + u < k1) r[u] = ld4(v.dmrow(v.dm_load(k + u), lc));
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k + u < k1) { dp[0] += r[u].x; dp[1] += r[u].y; dp[2] += r[u].z; dp[3] += r[u].w; }
     }
-    st_vec<CPL>(dP + (size_t)(dp_pos ? v.posv(j) : j) * PW + ch, dp);
+    st4(dP + (size_t)(dp_pos ? v.posv(j) : j) * PW + ch, dp);
+  }
+}
+
+// Phase 3: this CTA's dM_e = sum_k dm_k e_k^T and db_M = sum_k dm_k partials over the graph's
+// edges (half-warp t takes edges e0 + t, e0 + t + 16, ...), from the dm rows phase 1 stored
+template <bool S, int FE>
+__device__ void bwd_edge_partials(const View<S> &v, const Slice &s, float2 (&acc)[2][FE], float2 (&bsum)[2]) {
+  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4, lc = hl * CPL;
+  for (int k = s.e0 + hw; k < s.e1; k += kHalvesB) {
+    float ef[FE];
+    ld_edge<FE>(v.edge(k), v.Fe, ef);
+    const float4 dm = ld4(v.dmrow(v.dm_store(k), lc));
+    const float2 d01 = make_float2(dm.x, dm.y), d23 = make_float2(dm.z, dm.w);
+    bsum[0] = __fadd2_rn(bsum[0], d01);
+    bsum[1] = __fadd2_rn(bsum[1], d23);
+#pragma unroll
+    for (int f = 0; f < FE; ++f) {
+      const float2 e2 = make_float2(ef[f], ef[f]);
+      acc[0][f] = __ffma2_rn(d01, e2, acc[0][f]);
+      acc[1][f] = __ffma2_rn(d23, e2, acc[1][f]);
+    }
   }
 }
 
 template <bool SELF, int FE>
-__global__ void __launch_bounds__(32 * kWarps, 3) k_agg_bwd(const uint8_t *__restrict__ blob,
+__global__ void __launch_bounds__(32 * kWarpsB, 2) k_agg_bwd(const uint8_t *__restrict__ blob,
                                                             const int4 *__restrict__ gslice,
                                                             const float *__restrict__ P, const float *__restrict__ Me,
                                                             const float *__restrict__ bM, const float *__restrict__ A,
@@ -498,75 +621,91 @@ __global__ void __launch_bounds__(32 * kWarps, 3) k_agg_bwd(const uint8_t *__res
                                                             float *__restrict__ dmbuf, int maxB, int KA, int PW) {
   extern __shared__ __align__(128) uint8_t sm[];
   __shared__ uint64_t bar;
+  __shared__ float rcp[128];
+  __shared__ __align__(16) float sme[8 * kCh];  // M_e of the chunk, [f][channel]
   pdl_enter();
   const BatchView b = load_batch(blob);
-  constexpr int CPL = 2;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nch = H / kChBwd;
+  const int hl = threadIdx.x & 15, hw = threadIdx.x >> 4, nch = H / kCh;
   const int Fe = b.Fe;
-  const SmemLayout L = smem_layout(kChBwd, kCapNodes, kCapEdgesBwd, Fe, true);
+  const SmemLayout L = smem_layout(kCapNodes, kCapEdgesBwd, Fe, true);
   init_bar(&bar);
-  const uint32_t parity = 0;
   // one item (graph slot, channel chunk) per CTA; slots past the batch write zero partials
-  {
-    const int item = blockIdx.x;
-    __syncthreads();  // (the barrier's initialisation is visible)
-    const int g = item / nch, ch0 = (item - g * nch) * kChBwd, ch = ch0 + lane * CPL;
-    float me[CPL][FE], bm[CPL], acc[CPL][FE], bsum[CPL];
+  const int item = blockIdx.x;
+  __syncthreads();  // (the barrier's initialisation is visible)
+  const int g = item / nch, ch0 = (item - g * nch) * kCh, ch = ch0 + hl * CPL;
+  float2 acc[2][FE], bsum[2];
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      bsum[c] = 0.f;
+  for (int c = 0; c < 2; ++c) {
+    bsum[c] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int f = 0; f < FE; ++f) acc[c][f] = 0.f;
+    for (int f = 0; f < FE; ++f) acc[c][f] = make_float2(0.f, 0.f);
+  }
+  if (g < b.B) {
+    const Slice s = slice_of(b, gslice, g);
+    const bool staged = s.n1 - s.n0 <= kCapNodes && s.e1 - s.e0 <= kCapEdgesBwd;  // uniform per CTA
+    if (staged) stage_issue(b, P, PW, ch0, pos, true, L, sm, &bar, s);
+    const float *Qp = SELF ? P + H : nullptr;
+    // in flight with the staging copies: the weights and the first node's rows (global)
+    const float2 bm[2] = {make_float2(bM[ch], bM[ch + 1]), make_float2(bM[ch + 2], bM[ch + 3])};
+    for (int t = threadIdx.x; t < FE * kCh; t += blockDim.x) {
+      const int f = t / kCh, cc = t - f * kCh;
+      sme[t] = f < Fe ? Me[(ch0 + cc) * Fe + f] : 0.f;
     }
-    if (g < b.B) {
-      const Slice s = slice_of(b, gslice, g);
-      const bool staged = s.n1 - s.n0 <= kCapNodes && s.e1 - s.e0 <= kCapEdgesBwd;  // uniform per CTA
-      if (staged) stage_graph<kChBwd>(b, P, PW, ch0, pos, true, L, sm, &bar, s, parity);
-      const float *Qp = SELF ? P + H : nullptr;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        bm[c] = bM[ch + c];
-#pragma unroll
-        for (int f = 0; f < FE; ++f) me[c][f] = f < Fe ? Me[(ch + c) * Fe + f] : 0.f;
-      }
-      if (staged) {
-        const View<true, kChBwd> v = make_view<true, kChBwd>(b, P, PW, ch0, pos, L, sm, s);
-        bwd_phase1<true, SELF, FE>(v, s, me, bm, A, arg, dA, H, dmbuf, acc, bsum, KA, Qp, PW, dP);
-        __syncthreads();  // (orders the block's dm writes before phase 2's reads)
-        bwd_phase2<true>(v, s, dmbuf, dP, H, dp_pos, PW);
-      } else {  // a graph too large to stage
-        const View<false, kChBwd> v = make_view<false, kChBwd>(b, P, PW, ch0, pos, L, sm, s);
-        bwd_phase1<false, SELF, FE>(v, s, me, bm, A, arg, dA, H, dmbuf, acc, bsum, KA, Qp, PW, dP);
+    const DstIn first = load_dst<SELF>(b.rowptr, 0, pos, 0, s.n0 + hw, hw < s.n1 - s.n0, A, arg, dA, H, ch, KA, Qp, PW);
+    fill_rcp(rcp);
+    if (staged) {
+      stage_wait(&bar, 0);
+      {  // rev: for row-j entry k (pair i -> j, i = col[k]) the in-edge j -> i sits at rowptr[i] + slot[k]
+        const int *rp = reinterpret_cast<const int *>(sm + L.rp), *cl = reinterpret_cast<const int *>(sm + L.col);
+        uint16_t *rv = reinterpret_cast<uint16_t *>(sm + L.rev);
+        for (int t = threadIdx.x; t < s.e1 - s.e0; t += blockDim.x) {
+          const int k = s.e0 + t;
+          rv[rp[cl[k - s.c0] - s.r0] + sm[L.slot + k - s.s0] - s.e0] = (uint16_t)t;
+        }
         __syncthreads();
-        bwd_phase2<false>(v, s, dmbuf, dP, H, dp_pos, PW);
       }
-    }
-    // this item's partials of dM_e and db_M, warps combined in fixed order; layout per graph
-    // row: [H][Fe] (M_e's layout) then [H] (b_M). The staging area is free again: it holds
-    // the per-warp sums red[warp][lane][c * (FE + 1) + f].
-    constexpr int RS = CPL * (FE + 1);
-    float *red = reinterpret_cast<float *>(sm);
-    __syncthreads();
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      red[(warp * 32 + lane) * RS + c * (FE + 1) + FE] = bsum[c];
-#pragma unroll
-      for (int f = 0; f < FE; ++f) red[(warp * 32 + lane) * RS + c * (FE + 1) + f] = acc[c][f];
-    }
-    __syncthreads();
-    float *pb = partial + (size_t)g * H * (Fe + 1);
-    for (int t = threadIdx.x; t < kChBwd * (Fe + 1); t += blockDim.x) {
-      const bool isb = t >= kChBwd * Fe;
-      const int cc = isb ? t - kChBwd * Fe : t / Fe, f = isb ? FE : t - (t / Fe) * Fe;  // channel in chunk, feature
-      const int l = cc / CPL, c = cc - l * CPL;
-      float sum = 0.f;
-      for (int w = 0; w < kWarps; ++w) sum += red[(w * 32 + l) * RS + c * (FE + 1) + f];
-      if (isb) pb[(size_t)H * Fe + ch0 + cc] = sum;
-      else pb[(size_t)(ch0 + cc) * Fe + f] = sum;
+      const View<true> v = make_view<true>(b, P, PW, ch0, pos, L, sm, s, dmbuf, H);
+      bwd_phase1<true, SELF, FE>(v, s, sme, bm, A, arg, dA, H, KA, Qp, PW, dP, rcp, first);
+      __syncthreads();  // (orders the block's dm writes before phase 2's reads)
+      bwd_phase2<true>(v, s, dP, H, dp_pos, PW);
+      bwd_edge_partials<true, FE>(v, s, acc, bsum);
+    } else {  // a graph too large to stage
+      __syncthreads();
+      const View<false> v = make_view<false>(b, P, PW, ch0, pos, L, sm, s, dmbuf, H);
+      bwd_phase1<false, SELF, FE>(v, s, sme, bm, A, arg, dA, H, KA, Qp, PW, dP, rcp, first);
+      __syncthreads();
+      bwd_phase2<false>(v, s, dP, H, dp_pos, PW);
+      bwd_edge_partials<false, FE>(v, s, acc, bsum);
     }
   }
+  // this item's partials of dM_e and db_M, half-warps combined in fixed order; layout per
+  // graph row: [H][Fe] (M_e's layout) then [H] (b_M). The staging area is free again: it
+  // holds the per-half-warp sums red[hw][hl][c * (FE + 1) + f].
+  constexpr int RS = CPL * (FE + 1);
+  float *red = reinterpret_cast<float *>(sm);
+  __syncthreads();
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    const float2 bs = bsum[c >> 1];
+    red[(hw * 16 + hl) * RS + c * (FE + 1) + FE] = (c & 1) ? bs.y : bs.x;
+#pragma unroll
+    for (int f = 0; f < FE; ++f) {
+      const float2 a = acc[c >> 1][f];
+      red[(hw * 16 + hl) * RS + c * (FE + 1) + f] = (c & 1) ? a.y : a.x;
+    }
+  }
+  __syncthreads();
+  float *pb = partial + (size_t)g * H * (Fe + 1);
+  for (int t = threadIdx.x; t < kCh * (Fe + 1); t += blockDim.x) {
+    const bool isb = t >= kCh * Fe;
+    const int cc = isb ? t - kCh * Fe : t / Fe, f = isb ? FE : t - (t / Fe) * Fe;  // channel in chunk, feature
+    const int l = cc / CPL, c = cc - l * CPL;
+    float sum = 0.f;
+    for (int w = 0; w < kHalvesB; ++w) sum += red[(w * 16 + l) * RS + c * (FE + 1) + f];
+    if (isb) pb[(size_t)H * Fe + ch0 + cc] = sum;
+    else pb[(size_t)(ch0 + cc) * Fe + f] = sum;
+  }
 }
-
 
 }  // namespace
 
@@ -577,10 +716,10 @@ static cudaError_t set_smem(K kern, uint32_t bytes) {
 
 cudaError_t agg_configure() {
   cudaError_t e;
-  const uint32_t f4 = smem_layout(kChFwd, kCapNodes, kCapEdgesFwd, 4, false).total;
-  const uint32_t f8 = smem_layout(kChFwd, kCapNodes, kCapEdgesFwd, 8, false).total;
-  const uint32_t b4 = smem_layout(kChBwd, kCapNodes, kCapEdgesBwd, 4, true).total;
-  const uint32_t b8 = smem_layout(kChBwd, kCapNodes, kCapEdgesBwd, 8, true).total;
+  const uint32_t f4 = smem_layout(kCapNodes, kCapEdgesFwd, 4, false).total;
+  const uint32_t f8 = smem_layout(kCapNodes, kCapEdgesFwd, 8, false).total;
+  const uint32_t b4 = smem_layout(kCapNodes, kCapEdgesBwd, 4, true).total;
+  const uint32_t b8 = smem_layout(kCapNodes, kCapEdgesBwd, 8, true).total;
   if ((e = set_smem(k_agg_fwd<false, 4>, f4)) || (e = set_smem(k_agg_fwd<false, 8>, f8)) ||
       (e = set_smem(k_agg_fwd<true, 4>, f4)) || (e = set_smem(k_agg_fwd<true, 8>, f8)) ||
       (e = set_smem(k_agg_bwd<false, 4>, b4)) || (e = set_smem(k_agg_bwd<false, 8>, b8)) ||
@@ -592,12 +731,13 @@ cudaError_t agg_configure() {
 void launch_agg_fwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const int4 *gslice, const float *P,
                     const float *Me, const float *bM, float var_floor, float *A, uint8_t *arg, const int *pos,
                     const float *xin, int Fl) {
-  const int items = c.maxB * (c.H / kChFwd), Hl = c.Hl > 0 ? c.Hl : c.H;
+  const int items = c.maxB * (c.H / kCh), Hl = c.Hl > 0 ? c.Hl : c.H;
   const SelfIn si{c.self_t ? P : nullptr, xin, c.PW(), Fl};
-  const uint32_t smem = smem_layout(kChFwd, kCapNodes, kCapEdgesFwd, c.Fe, false).total;
+  const uint32_t smem = smem_layout(kCapNodes, kCapEdgesFwd, c.Fe, false).total;
   auto kern = c.Fe == 4 ? (c.self_t ? k_agg_fwd<true, 4> : k_agg_fwd<false, 4>)
                         : (c.self_t ? k_agg_fwd<true, 8> : k_agg_fwd<false, 8>);
-  launch_ex(kern, items, 32 * kWarps, smem, st, blob, gslice, P, Me, bM, var_floor, A, arg, c.H, pos, Hl, c.KA(), si);
+  launch_ex(kern, items, 32 * kWarpsF, smem, st, blob, gslice, P, Me, bM, var_floor, A, arg, c.H, pos, Hl, c.KA(),
+            si);
   g_launches += 1;
 }
 
@@ -607,11 +747,11 @@ size_t agg_bwd_dm_floats(const Caps &c) { return (size_t)c.maxE * c.H; }
 void launch_agg_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const int4 *gslice, const float *P,
                     const float *Me, const float *bM, const float *A, const uint8_t *arg, const float *dA, float *dP,
                     float *partial, const int *pos, const int *dp_pos, float *dm_scratch) {
-  const int items = c.maxB * (c.H / kChBwd);
-  const uint32_t smem = smem_layout(kChBwd, kCapNodes, kCapEdgesBwd, c.Fe, true).total;
+  const int items = c.maxB * (c.H / kCh);
+  const uint32_t smem = smem_layout(kCapNodes, kCapEdgesBwd, c.Fe, true).total;
   auto kern = c.Fe == 4 ? (c.self_t ? k_agg_bwd<true, 4> : k_agg_bwd<false, 4>)
                         : (c.self_t ? k_agg_bwd<true, 8> : k_agg_bwd<false, 8>);
-  launch_ex(kern, items, 32 * kWarps, smem, st, blob, gslice, P, Me, bM, A, arg, dA, dP, partial, c.H, pos, dp_pos,
+  launch_ex(kern, items, 32 * kWarpsB, smem, st, blob, gslice, P, Me, bM, A, arg, dA, dP, partial, c.H, pos, dp_pos,
             dm_scratch, c.maxB, c.KA(), c.PW());
   g_launches += 1;
 }
