@@ -74,6 +74,10 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--store-dir", default="")
     ap.add_argument("--seed", type=int, default=11)
+    ap.add_argument("--precision", default="3xtf32", choices=["3xtf32", "tf32"],
+                    help="GEMM precision: 3xTF32 (fp32-accurate, default) or single-pass TF32 (HG_FLAG_TF32)")
+    ap.add_argument("--variant", default="base", choices=["base", "self", "scalers5", "nodehead", "all"],
+                    help="(f)3 model variants: PNA self-term, all five scalers, node-level head")
     ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
                     help="N>1 gradient exchange: fused peer-memory reduce/AdamW/all-gather kernel or bucketed NCCL")
     return ap.parse_args()
@@ -268,6 +272,9 @@ def main():
         data = molgen.load_dir(sdir)
     t_gen = time.time() - t0
     t0 = time.time()
+    if args.variant in ("nodehead", "all"):  # node-level targets: seeded synthetic, one per atom
+        data = dict(data)
+        data["y_node"] = np.random.default_rng(args.seed).standard_normal(len(data["x"])).astype(np.float32)
     store = hgnn.Store(data, copy=False)
     st = store.stats()
     delta = store.degree_stat()
@@ -278,8 +285,17 @@ def main():
     max_edges = B * int(np.diff(np.asarray(data["edge_offset"])).max())
     n_res = max(1, min(args.resident, args.steps))
     e2e_slots = 0 if args.no_e2e else 2
+    flags = hgnn.HG_FLAG_TF32 if args.precision == "tf32" else 0
+    scalers = 0
+    if args.variant in ("self", "all"):
+        flags |= hgnn.HG_FLAG_SELF_TERM
+    if args.variant in ("nodehead", "all"):
+        flags |= hgnn.HG_FLAG_NODE_HEAD
+    if args.variant in ("scalers5", "all"):
+        scalers = sum(hgnn.SCALER_BITS.values())
     cfg = hgnn.make_config(data["f_node"], 4, H, L, B, max_nodes, max_edges, delta, n_slots=n_res + e2e_slots,
-                           max_degree=st["max_degree"])
+                           max_degree=st["max_degree"], flags=flags, scalers=scalers,
+                           delta_lin=store.degree_stat_linear() if scalers else 0.0)
     ctx = hgnn.Context(cfg, device=local_rank)
     ctx.params_init(1234)
     ctx.comm_init(rank, world)
@@ -461,7 +477,10 @@ def main():
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     bf16_peak = float(peaks.get("bf16_tflops", 2250.0))
     # 3xTF32: three tf32 MMAs per fp32 MAC; tf32 dense = bf16 dense x 0.5 (nominal ratio, B200_PROFILING.md)
-    tc_peak = bf16_peak * 0.5 / 3.0
+    passes = 1 if args.precision == "tf32" else 3
+    tc_peak = bf16_peak * 0.5 / passes
+    tc_peak_source = ("MEASURED_PEAKS.json bf16_tflops x 0.5 (tf32, single pass)" if passes == 1 else
+                      "MEASURED_PEAKS.json bf16_tflops x 0.5 (tf32) / 3 (3xTF32 passes)")
     ridge = tc_peak * 1e12 / (hbm_peak * 1e9)  # flop / byte
     step_ms_prof = sum(v[0] for v in phases.values())
     traffic_db = {}
@@ -478,7 +497,7 @@ def main():
         if fl > 0 and fl / byt >= ridge:
             ach = fl / t / 1e12
             r = {"bound": "tensor", "achieved": ach, "peak": tc_peak, "unit": "TFLOP/s", "frac": ach / tc_peak,
-                 "peak_source": "MEASURED_PEAKS.json bf16_tflops x 0.5 (tf32) / 3 (3xTF32 passes)"}
+                 "peak_source": tc_peak_source}
         else:
             ach = byt / t / 1e9
             r = {"bound": "hbm", "achieved": ach, "peak": hbm_peak, "unit": "GB/s", "frac": ach / hbm_peak,
@@ -564,14 +583,20 @@ def main():
     out = {
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": K, "warmup": args.warmup,
         "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32", "data": "synthetic (molgen seeded molecules, Table-2 calibrated; random-init weights)",
+        "dtype": "tf32" if args.precision == "tf32" else "f32", "data": "synthetic (molgen seeded molecules, Table-2 calibrated; random-init weights)",
         "config": {"workload": desc, "graphs_in_store": n_graphs, "global_batch": B * world, "batch_per_gpu": B,
                    "layers": L, "hidden": H, "hidden_internal": int(ctx.internal_cfg.hidden),
                    "nodes_per_batch_mean": Nn, "edges_per_batch_mean": Ee,
                    "parallelism": f"dp{world}", "resident_batches": n_res,
                    "grad_exchange": exchange,
                    "l2": f"flushed between timed steps ({args.flush_mb} MB write, outside the step events)",
-                   "gemm_precision": "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs, TMA-fed"},
+                   "gemm_precision": ("single-pass TF32 tcgen05 (HG_FLAG_TF32), degree-class GEMMs, TMA-fed"
+                                      if args.precision == "tf32" else
+                                      "3xTF32 tcgen05 (fp32-accurate), degree-class GEMMs, TMA-fed"),
+                   "variant": {"name": args.variant, "flags": flags, "scalers": list(hgnn.scaler_names(scalers))
+                               if scalers else ["identity", "amplification", "attenuation"],
+                               "work_accounting": "base model terms (variant extra terms not counted)"
+                               if args.variant != "base" else "base model"}},
         "roofline": prof, "phase_roofline": phase_roof, "aggregation": agg, "pack_rate": pack_rate,
         "exchange": exch,
         "phases_ms": {k: round(v[0], 4) for k, v in phases.items()},

@@ -174,7 +174,7 @@ struct hg_ctx {
   uint8_t *peer_ws[kP2PMaxWorld] = {};     // every rank's workspace ([rank] = ws)
   void *peer_base[kP2PMaxWorld] = {};      // opened IPC mappings (closed at destroy)
   unsigned long long timeout_ns = 0;       // fail-stop bound of device flag waits and hg_sync (0 = none)
-  std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx;  // per layer fork / join points
+  std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx, ev_upd, ev_pl;  // per layer fork / join points
   cudaEvent_t ev_head = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_prepmx = nullptr, ev_prepw = nullptr,
               ev_ar1 = nullptr, ev_adam = nullptr;
   float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
@@ -317,7 +317,8 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
                    reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
                    reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)),
-                   reinterpret_cast<int4 *>(x->b(p.gslice)), scaler_mask(x->cfg), c.delta_lin, gram_ks(x->caps));
+                   reinterpret_cast<int4 *>(x->b(p.gslice)), scaler_mask(x->cfg), c.delta_lin, gram_ks(x->caps),
+                   x->caps.maxN);
   });
   if (fork) cudaEventRecord(x->ev_start, st);
   // the prep branch is enqueued after layer 0's projection so that the main chain is the
@@ -336,9 +337,6 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
       launch_prep_Mx(wst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
                      x->f(p.Mx_lo), x->f(p.MxT), x->f(p.MxT_lo));
       if (fork) cudaEventRecord(x->ev_prepmx, wst);
-      if (c.layers > 1)
-        launch_prep_W2(wst, x->caps, x->f(p.params), uo, uxo, 1, c.layers, p.cmax, dinfo, x->f(p.Wf),
-                       x->f(p.Wf_lo), x->f(p.WbT), x->f(p.WbT_lo));
       launch_pad_x0(wst, x->caps, blob, x->f(p.xpad), x->dxda ? pos : nullptr);
       if (fork) cudaEventRecord(x->ev_prepw, wst);
       g_low_prio = false;
@@ -362,6 +360,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     });
     if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_prep, 0);
     if (fork && l == 1) cudaStreamWaitEvent(st, x->ev_prepw, 0);
+    if (fork && l >= 1) cudaStreamWaitEvent(st, x->ev_pl[l], 0);
     phase(pr, HG_PHASE_UPDATE, [&] {
       const bool keep_sorted = x->dxda && l + 1 < c.layers;  // X_l operands of the fused dX -> dA kernel
       const size_t wl = (size_t)l * p.cmax * c.hidden * x->caps.KA();  // layer l's class weights
@@ -371,6 +370,24 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
                           keep_sorted ? x->f(p.Xs[l]) : nullptr,
                           keep_sorted ? reinterpret_cast<uint32_t *>(x->b(p.Xmask[l])) : nullptr);
     });
+    if (l + 1 < c.layers) {
+      // layer l+1's class weights, on side stream 2 once update_l is done: they run beside
+      // proj_{l+1} / agg_{l+1} instead of beside update_l, whose persistent TMA CTAs need whole
+      // SMs (timeline, config B: all layers' weights prepared beside update_0 made it 30 us
+      // instead of 16)
+      if (fork) {
+        cudaEventRecord(x->ev_upd[l], st);
+        cudaStreamWaitEvent(wst, x->ev_upd[l], 0);
+      }
+      phase(pr, HG_PHASE_SCALERS, [&] {
+        g_low_prio = fork;
+        launch_prep_W2(wst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.u_off)),
+                       reinterpret_cast<const int64_t *>(x->b(p.ux_off)), l + 1, l + 2, p.cmax, dinfo, x->f(p.Wf),
+                       x->f(p.Wf_lo), x->f(p.WbT), x->f(p.WbT_lo));
+        g_low_prio = false;
+      });
+      if (fork) cudaEventRecord(x->ev_pl[l + 1], wst);
+    }
   }
   if (fork && c.layers < 2) cudaStreamWaitEvent(st, x->ev_prepw, 0);  // join side stream 2
   phase(pr, HG_PHASE_HEAD_FWD, [&] {
@@ -738,7 +755,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   for (int i = 0; i < HG_LOSS_RING; ++i)
     if ((e = cudaEventCreateWithFlags(&x->loss_ev[i], cudaEventDisableTiming)) != cudaSuccess)
       return bail(e, "cudaEventCreate");
-  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
+  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx, &x->ev_upd, &x->ev_pl})
     for (int l = 0; l < c->layers; ++l) {
       cudaEvent_t ev;
       if ((e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
@@ -763,6 +780,7 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   head_configure(x->caps);
   if ((e = tcd_configure()) != cudaSuccess) return bail(e, "tcd_configure");
   if ((e = agg_configure()) != cudaSuccess) return bail(e, "agg_configure");
+  if ((e = degsort_configure()) != cudaSuccess) return bail(e, "degsort_configure");
   x->dxda = dxda_supported(x->caps);  // fused dX -> dA backward: +2.3% at config B
   {
     std::vector<int64_t> uo, mo, uxo((size_t)c->layers, 0);
@@ -808,7 +826,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->side_stream) cudaStreamDestroy(x->side_stream);
   if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
   if (x->adam_stream) cudaStreamDestroy(x->adam_stream);
-  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx})
+  for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx, &x->ev_upd, &x->ev_pl})
     for (auto ev : *v) cudaEventDestroy(ev);
   for (cudaEvent_t ev : {x->ev_head, x->ev_prep, x->ev_start, x->ev_prepmx, x->ev_prepw, x->ev_ar1, x->ev_adam})
     if (ev) cudaEventDestroy(ev);

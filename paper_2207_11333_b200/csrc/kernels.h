@@ -152,7 +152,8 @@ int tc_max_splits(const Caps &c, int cmax);
 // (smask: the configured scaler bit set, hgnn.h HG_SCALER_*; delta_lin: the linear scalers' normaliser)
 void launch_degsort(cudaStream_t st, const uint8_t *blob, double delta, int cmax, float *amp, float *att, int *perm,
                     DegInfo *info, int4 *tiles, int4 *splits, int *pos, int4 *gslice, int smask, double delta_lin,
-                    int ks = 0);
+                    int ks, int maxN);
+cudaError_t degsort_configure();  // opt-in shared memory for the staged degrees (outside capture)
 
 // TMA-fed tcgen05 GEMMs (tcdirect.cu): activation operands are read once as fp32 (their tf32
 // lo terms are derived in shared memory), weight operands with their lo terms (prep kernels).

@@ -452,11 +452,12 @@ namespace {
 // the critical chain's kernels that run concurrently
 // Small steps (config B: ~150 Gram items) run the Grams beside the latency-bound main chain,
 // where fewer CTAs interfere less (148 -> 40 measured +2%); large ones (config D/E: thousands
-// of items) need every SM. Cap = clamp(items / 4, 40, 148) unless the step builder overrides
-// it (g_mn_grid_override: the Grams that end the step use every SM).
+// of items) need every SM. Cap = clamp(items / 2, 40, 148) (items / 4 measured 1% slower at
+// B and D, round 2) unless the step builder overrides it (g_mn_grid_override: the Grams that
+// end the step use every SM).
 int mn_grid_cap(int items) {
   if (g_mn_grid_override > 0) return g_mn_grid_override;
-  return std::max(40, std::min(kSMs, items / 4));
+  return std::max(40, std::min(kSMs, items / 2));
 }
 template <class Op>
 void nrun(cudaStream_t st, const TmaMaps &mp, const CUtensorMap &ones, Op op, int items) {

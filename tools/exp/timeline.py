@@ -21,12 +21,13 @@ from paper_2207_11333_b200 import hgnn  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--graphs", type=int, default=20000)
 ap.add_argument("--B", type=int, default=128)
+ap.add_argument("--dataset", default="pcqm", choices=["pcqm", "aisd"])
 ap.add_argument("--json", default="gpurun_out/timeline_trace.json")
 ap.add_argument("--nosync", action="store_true", help="launch the profiled steps back to back")
 args = ap.parse_args()
 
 d = tempfile.mkdtemp(dir="/dev/shm" if os.path.isdir("/dev/shm") else None)
-data = molgen.generate_to(d, "pcqm", args.graphs, 7)
+data = molgen.generate_to(d, args.dataset, args.graphs, 7)
 store = hgnn.Store(data, copy=False)
 st = store.stats()
 B, H, L = args.B, 128, 6
