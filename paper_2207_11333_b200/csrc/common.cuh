@@ -48,7 +48,8 @@ extern bool g_low_prio;
 extern int g_prio_lo, g_prio_hi;
 // Every kernel starts with pdl_enter() (griddepcontrol.wait / launch_dependents): a no-op
 // under plain stream ordering, it makes the kernels safe to launch with programmatic
-// dependent launch (measured slower for this step: DESIGN.md §7, so it is not enabled).
+// dependent launch (measured slower for this step, round 2 again: config B 268k vs 314k graphs/s,
+// D 367k vs 377k, profiles/r02_pdl_rejected_*.json; so it is not enabled).
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

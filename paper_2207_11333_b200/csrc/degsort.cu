@@ -64,11 +64,26 @@ __global__ void __launch_bounds__(1024) k_degsort(const uint8_t *__restrict__ bl
   // degrees and per-node scalers in one coalesced pass (independent loads; the rounds below
   // then read shared memory instead of a dependent global chain per round)
   const bool sd = b.N <= deg_cap;
-  for (int i = tid; i < b.N; i += blockDim.x) {
-    const int d = min(b.rowptr[i + 1] - b.rowptr[i], kDeg - 1);
-    if (sd) sdeg[i] = (uint8_t)d;
-    amp[i] = tsc[1][d];
-    att[i] = tsc[2][d];
+  // (four nodes per thread per round: their rowptr loads are issued before any store, so the
+  // round costs one memory latency -- ncu: the one-node loop stalled on every load)
+  for (int i0 = tid; i0 < b.N; i0 += 4 * blockDim.x) {
+    int r0[4], r1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      r0[u] = i < b.N ? __ldg(b.rowptr + i) : 0;
+      r1[u] = i < b.N ? __ldg(b.rowptr + i + 1) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < b.N) {
+        const int d = min(r1[u] - r0[u], kDeg - 1);
+        if (sd) sdeg[i] = (uint8_t)d;
+        amp[i] = tsc[1][d];
+        att[i] = tsc[2][d];
+      }
+    }
   }
   __syncthreads();
   // warp w owns the contiguous node range [w*per, (w+1)*per), in rounds of 32 nodes; ranks

@@ -17,17 +17,21 @@ os.makedirs(vdir, exist_ok=True)
 nccl_inc, nccl_lib = B._nccl_dirs()
 for spec in sys.argv[1:]:
     name, _, rest = spec.partition(":")
-    src, _, flags = rest.partition(":") if rest.endswith(".cu") or ".cu:" in rest else ("agg.cu", "", rest)
+    src, _, flags = rest.partition(":") if (".cu" in rest or rest.startswith("all")) else ("agg.cu", "", rest)
     defs = [f for f in flags.split(",") if f]
-    obj = os.path.join(B.OBJDIR, f"{src[:-3]}_{name}.o")
-    cmd = [B.NVCC] + B.ARCH + ["-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr", "-O3",
-                               "-std=c++17", f"-I{B.INC}", f"-I{B.CSRC}", f"-I{nccl_inc}"] + defs + \
-        ["-c", os.path.join(B.CSRC, src), "-o", obj]
-    r = subprocess.run(cmd, capture_output=True, text=True)
-    if r.returncode:
-        sys.exit(r.stderr)
-    spills = [l for l in r.stderr.splitlines() if "spill" in l or "Used" in l]
-    objs = [os.path.join(B.OBJDIR, f + ".o") for f in B.CU_SOURCES + B.CPP_SOURCES if f != src] + [obj]
+    srcs = B.CU_SOURCES if src == "all" else [src]
+    vobjs, spills = [], []
+    for sf in srcs:
+        obj = os.path.join(B.OBJDIR, f"{sf[:-3]}_{name}.o")
+        cmd = [B.NVCC] + B.ARCH + ["-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
+                                   "-O3", "-std=c++17", f"-I{B.INC}", f"-I{B.CSRC}", f"-I{nccl_inc}"] + defs + \
+            ["-c", os.path.join(B.CSRC, sf), "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode:
+            sys.exit(r.stderr)
+        spills += [l for l in r.stderr.splitlines() if "spill" in l or "Used" in l]
+        vobjs.append(obj)
+    objs = [os.path.join(B.OBJDIR, f + ".o") for f in B.CU_SOURCES + B.CPP_SOURCES if f not in srcs] + vobjs
     out = os.path.join(vdir, f"libhgnn_{name}.so")
     link = [B.NVCC] + B.ARCH + ["-shared", "-cudart", "shared", "-o", out] + objs + \
         [f"-L{nccl_lib}", "-lnccl", "-Xlinker", f"-rpath,{nccl_lib}", "-Xlinker", "-rpath,/usr/local/cuda/lib64",
