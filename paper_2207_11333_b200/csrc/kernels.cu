@@ -635,12 +635,15 @@ static void head_launch(cudaStream_t st, const Caps &c, const uint8_t *blob, con
   const int in_smem = base + w1 <= 200 * 1024 ? 1 : 0;  // attribute set once by head_configure
   const size_t smem = base + (in_smem ? w1 : 0);
   if (c.H == 128 && (c.Hf == 128 || c.Hf == 64)) {  // latency-optimised kernel
+    // (two blocks per SM: the graphs of one block are processed serially, so at config D's 512
+    // graphs one block per SM put ~3.5 graph latencies on the step's critical path)
+    const int grid = std::min(c.maxB, 2 * kSMs);
     if (c.Hf == 128)
-      launch_ex(k_head_fast<FWD, BWD, 1, 16>, std::min(c.maxB, kSMs), 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre,
-                yhat, sqerr, dy, dhid, dZL, pos);
+      launch_ex(k_head_fast<FWD, BWD, 1, 16>, grid, 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
+                dhid, dZL, pos);
     else
-      launch_ex(k_head_fast<FWD, BWD, 1, 8>, std::min(c.maxB, kSMs), 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre,
-                yhat, sqerr, dy, dhid, dZL, pos);
+      launch_ex(k_head_fast<FWD, BWD, 1, 8>, grid, 256, 0, st, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
+                dhid, dZL, pos);
     return;
   }
   launch_ex(k_head<FWD, BWD>, std::min(c.maxB, kSMs), 256, smem, st, blob, XL, W1, b1, W2, b2, G, hpre, yhat, sqerr, dy,
@@ -764,6 +767,80 @@ __global__ void k_head_grads(const uint8_t *__restrict__ blob, const float *__re
   }
 }
 
+// H = 128 form: block b < Hf/8 owns W1 rows [8b, 8b + 8) (warp w: row 8b + w, lane: 4 columns),
+// the graphs' G rows and dhid entries staged through shared memory in chunks of 32 (the next
+// chunk's loads in flight while this one is summed); every output keeps the fixed ascending
+// order over graphs of k_head_grads, so the two kernels agree bitwise. The last block does the
+// b1 / W2 / b2 gradients. (Thread-per-element with all B graphs from L2 was ~58 us at config D.)
+__global__ void __launch_bounds__(256) k_head_grads128(const uint8_t *__restrict__ blob, const float *__restrict__ G,
+                                                      const float *__restrict__ hpre, const float *__restrict__ dy,
+                                                      const float *__restrict__ dhid, float *__restrict__ gW1,
+                                                      float *__restrict__ gb1, float *__restrict__ gW2,
+                                                      float *__restrict__ gb2, int Hf) {
+  constexpr int H = 128, CG = 32;
+  __shared__ float4 sG[2][CG][H / 4];
+  __shared__ float sd[2][CG][8];
+  pdl_enter();
+  const int B = reinterpret_cast<const int *>(blob)[0];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if ((int)blockIdx.x == Hf / 8) {  // b1, W2, b2
+    for (int e = threadIdx.x; e < 2 * Hf + 1; e += blockDim.x) {
+      float s = 0.f;
+      if (e < Hf) {
+        for (int g = 0; g < B; ++g) s += dhid[(size_t)g * Hf + e];
+        gb1[e] = s;
+      } else if (e < 2 * Hf) {
+        const int r = e - Hf;
+        for (int g = 0; g < B; ++g) s = fmaf(dy[g], fmaxf(hpre[(size_t)g * Hf + r], 0.f), s);
+        gW2[r] = s;
+      } else {
+        for (int g = 0; g < B; ++g) s += dy[g];
+        gb2[0] = s;
+      }
+    }
+    return;
+  }
+  const int r0 = blockIdx.x * 8;
+  float4 pg[4];
+  float pd = 0.f;
+  auto fetch = [&](int g0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {  // 32 graphs x 32 float4 = 1024 float4, 4 per thread
+      const int t = threadIdx.x + 256 * u, gg = t >> 5, q = t & 31;
+      pg[u] = g0 + gg < B ? ldg4(G + (size_t)(g0 + gg) * H + 4 * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    const int gg = threadIdx.x >> 3, rr = threadIdx.x & 7;
+    pd = g0 + gg < B ? dhid[(size_t)(g0 + gg) * Hf + r0 + rr] : 0.f;
+  };
+  auto store = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int t = threadIdx.x + 256 * u;
+      sG[buf][t >> 5][t & 31] = pg[u];
+    }
+    sd[buf][threadIdx.x >> 3][threadIdx.x & 7] = pd;
+  };
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  fetch(0);
+  store(0);
+  __syncthreads();
+  for (int g0 = 0, buf = 0; g0 < B; g0 += CG, buf ^= 1) {
+    if (g0 + CG < B) fetch(g0 + CG);
+    const int n = min(CG, B - g0);
+    for (int gg = 0; gg < n; ++gg) {
+      const float d = sd[buf][gg][warp];
+      const float4 gv = sG[buf][gg][lane];
+      s.x = fmaf(d, gv.x, s.x);
+      s.y = fmaf(d, gv.y, s.y);
+      s.z = fmaf(d, gv.z, s.z);
+      s.w = fmaf(d, gv.w, s.w);
+    }
+    if (g0 + CG < B) store(buf ^ 1);
+    __syncthreads();
+  }
+  *reinterpret_cast<float4 *>(gW1 + (size_t)(r0 + warp) * H + 4 * lane) = s;
+}
+
 void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *XL, const float *W1,
                      const float *W2, const float *G, const float *hpre, const float *yhat, float *dy,
                      float *dhid, float *dZL, float *gW1, float *gb1, float *gW2, float *gb2, bool head_done,
@@ -778,6 +855,11 @@ void launch_head_bwd(cudaStream_t st, const Caps &c, const uint8_t *blob, const 
 
 void launch_head_grads(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *G, const float *hpre,
                        const float *dy, const float *dhid, float *gW1, float *gb1, float *gW2, float *gb2) {
+  if (c.H == 128 && c.Hf % 8 == 0) {
+    launch_ex(k_head_grads128, c.Hf / 8 + 1, 256, 0, st, blob, G, hpre, dy, dhid, gW1, gb1, gW2, gb2, c.Hf);
+    counted();
+    return;
+  }
   const int total = c.Hf * c.H + 2 * c.Hf + 1;
   launch_ex(k_head_grads, std::min(cdiv(total, 256), kSMs * 4), 256, 0, st, blob, G, hpre, dy, dhid, gW1, gb1, gW2,
             gb2, c.H, c.Hf);

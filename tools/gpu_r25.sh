@@ -1,0 +1,7 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r25_pytest.log 2>&1; echo "pytest=$?" > gpurun_out/r25_status.txt
+timeout 300 python bench.py --workload B --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r25_benchB.json 2> gpurun_out/r25_benchB.err; echo "benchB=$?" >> gpurun_out/r25_status.txt
+timeout 300 python bench.py --workload D --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --graphs 300000 > gpurun_out/r25_benchD.json 2> gpurun_out/r25_benchD.err; echo "benchD=$?" >> gpurun_out/r25_status.txt
+timeout 300 python tools/exp/timeline.py --graphs 40000 --B 512 --dataset aisd > gpurun_out/r25_timeline_D.txt 2>&1; echo "tlD=$?" >> gpurun_out/r25_status.txt
+timeout 300 python tools/exp/timeline.py --graphs 20000 --B 128 > gpurun_out/r25_timeline_B.txt 2>&1; echo "tlB=$?" >> gpurun_out/r25_status.txt
