@@ -247,3 +247,17 @@ def test_separate_dx_da_path_wide(torch_cuda):
     res = PT.run_step_parity(data, ids, ctx, cfg, delta)
     print({k: (max(v.values()) if isinstance(v, dict) else v) for k, v in res.items()})
     PT.assert_parity(res)
+
+
+def test_many_graphs_per_batch(torch_cuda):
+    """A batch of 320 small graphs: more (graph, 64-channel chunk) aggregation items than two
+    waves of resident CTAs (maxB x H/64 > 592), two graph steps."""
+    data = PT.generate("tiny", 1200, 4)
+    B = 320
+    assert B * (128 // 64) > 2 * 2 * 148
+    ctx, cfg, delta = PT.make_ctx(data, B, 128, 2, seed=3)
+    ids = O.shard(5, 0, 0, 1, 1200)
+    for k in range(2):
+        res = PT.run_step_parity(data, ids[k * B:(k + 1) * B], ctx, cfg, delta, graph=(k == 1))
+        print("many graphs", k, {kk: (max(v.values()) if isinstance(v, dict) else v) for kk, v in res.items()})
+        PT.assert_parity(res)
