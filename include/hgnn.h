@@ -254,6 +254,18 @@ hg_status hg_grads_get(hg_ctx *x, float *dst, int32_t on_device);
 hg_status hg_opt_state_get(hg_ctx *x, float *m, float *v, int64_t *step, int32_t on_device);
 hg_status hg_opt_state_set(hg_ctx *x, const float *m, const float *v, int64_t step, int32_t on_device);
 
+/* Checkpoint / resume ("versioned binary dump of config + named parameter tensors +
+ * optimizer state, little-endian, with CRC"). File: "HGNNCKPT", u32 version 1, the
+ * model part of hg_config (f_node, f_edge, hidden, layers, fc_hidden, flags, scalers, delta,
+ * delta_lin, var_floor, node_weight), the named tensor table (name, offset, rows, cols), the
+ * parameter arena, the Adam step, m and v (logical widths, hg_param_layout), then a CRC-32C of
+ * everything before it. Save gathers sharded moments first (peer-memory exchange) and writes
+ * path atomically (path.tmp, then rename). Load requires the same model configuration (the
+ * TF32 flag may differ) and tensor table: HG_E_SHAPE otherwise; HG_E_IO for a missing,
+ * truncated or corrupt file (nothing is changed then). Synchronous. */
+hg_status hg_checkpoint_save(hg_ctx *x, const char *path);
+hg_status hg_checkpoint_load(hg_ctx *x, const char *path);
+
 /* Debug / parity views into the workspace: byte offset and size of a named
  * buffer. what: 0 = P_l [N,H] ([N,2H] = [P | Q] with the self-term), 1 = A_l [N,4H]
  * (mean|min|max|std, degree-sorted rows; [N,5H] with the self-term's x_i block), 2 = arg_l

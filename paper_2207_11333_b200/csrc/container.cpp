@@ -33,12 +33,10 @@
 #include "internal.h"
 
 namespace hg {
-namespace {
 
-constexpr uint32_t kVersion = 1;
-
-// CRC-32C (Castagnoli) with the SSE4.2 instruction, 8 bytes per step
-uint32_t crc32(const void *data, size_t n, uint32_t crc = 0) {
+// CRC-32C (Castagnoli) with the SSE4.2 instruction, 8 bytes per step (container files and
+// checkpoints)
+uint32_t crc32c(const void *data, size_t n, uint32_t crc) {
   const uint8_t *p = (const uint8_t *)data;
   uint64_t c = ~crc;
   while (n >= 8) {
@@ -52,6 +50,12 @@ uint32_t crc32(const void *data, size_t n, uint32_t crc = 0) {
   while (n--) c32 = __builtin_ia32_crc32qi(c32, *p++);
   return ~c32;
 }
+
+namespace {
+
+constexpr uint32_t kVersion = 1;
+
+uint32_t crc32(const void *data, size_t n, uint32_t crc = 0) { return crc32c(data, n, crc); }
 
 struct File {
   FILE *f = nullptr;

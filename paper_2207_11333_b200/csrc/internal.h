@@ -10,6 +10,10 @@
 
 namespace hg {
 
+// CRC-32C (Castagnoli), container.cpp
+uint32_t crc32c(const void *data, size_t n, uint32_t crc = 0);
+
+
 hg_status fail(hg_status st, const char *fmt, ...);
 uint64_t splitmix64(uint64_t x);
 

@@ -104,6 +104,8 @@ SIGNATURES = {
     "hg_grads_get": [_P, _P, _I32],
     "hg_opt_state_get": [_P, _P, _P, _I64P, _I32],
     "hg_opt_state_set": [_P, _P, _P, _I64, _I32],
+    "hg_checkpoint_save": [_P, ctypes.c_char_p],
+    "hg_checkpoint_load": [_P, ctypes.c_char_p],
     "hg_workspace_view": [_P, _I32, _I32, _I64P, _I64P],
     "hg_batch_get": [_P, _I32, _P, _SZ, _SZP],
     "hg_pack": [_P, _P, _P, _I32, _I32],
@@ -511,6 +513,13 @@ class Context:
         m = np.ascontiguousarray(m, np.float32)
         v = np.ascontiguousarray(v, np.float32)
         _check(_lib.hg_opt_state_set(self.handle, _ptr(m), _ptr(v), step, 0))
+
+    def checkpoint_save(self, path: str):
+        """hg_checkpoint_save: config + named parameters + Adam state, CRC-32C."""
+        _check(_lib.hg_checkpoint_save(self.handle, os.fsencode(path)))
+
+    def checkpoint_load(self, path: str):
+        _check(_lib.hg_checkpoint_load(self.handle, os.fsencode(path)))
 
     # ---- the training path
     def pack(self, store: Store, ids, slot: int = 0):
