@@ -38,7 +38,7 @@ struct Plan {
   // write-after-read waits)
   std::vector<size_t> dZ, dPl, pagg;
   size_t G = 0, hpre = 0, dhid = 0, yhat = 0, dy = 0, sqerr = 0;
-  size_t part = 0, part2 = 0, part3 = 0;  // split partials: spare, Gram (dU), dM_x
+  size_t part = 0, part2 = 0, part3 = 0, part2b = 0;  // split partials: spare, Gram (dU), dM_x, layer 0's Gram
   size_t eval_acc = 0;
   size_t u_off = 0, ux_off = 0;
   int cmax = 0;  // degree-class slots
@@ -136,6 +136,7 @@ Plan make_plan(const hg_config &c) {
   }
   p.part = take(sizeof(float) * 4);
   p.part2 = take(sizeof(float) * pf);
+  p.part2b = take(sizeof(float) * pf);
   p.part3 = take(sizeof(float) * pf);
   for (int l = 0; l < c.layers; ++l) p.pagg.push_back(take(sizeof(float) * agg_bwd_partial_floats(caps)));
   p.dm_scratch = take(sizeof(float) * agg_bwd_dm_floats(caps));  // graphs too large to stage (agg.cu)
@@ -169,6 +170,7 @@ struct hg_ctx {
   std::vector<cudaEvent_t> bucket_ready;         // per bucket (head, conv L-1 .. conv 0)
   cudaEvent_t comm_done = nullptr;
   cudaStream_t side_stream = nullptr, side2_stream = nullptr;  // weight-gradient GEMMs beside the critical chain
+  cudaStream_t side3_stream = nullptr;  // layer 0's Gram (its own stream: it need not queue behind layer 1's)
   cudaStream_t adam_stream = nullptr;  // early AdamW of layers >= 1 (must not delay layer 0's side-stream work)
   bool p2p = false;                        // captured steps exchange over peer memory (hg_p2p_open)
   bool mv_sharded = false;                 // Adam moments valid on this rank's shard only (after p2p steps)
@@ -458,20 +460,23 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   for (int l = c.layers - 1; l >= 0; --l) {
     float *dZ = x->f(p.dZ[l]);
     float *dP = x->f(p.dPl[l]), *pagg = x->f(p.pagg[l]);
-    // ---- side: Gram (dU, db_U) as soon as dZ_l is ready
+    // ---- side: Gram (dU, db_U) as soon as dZ_l is ready (layer 0's on a stream of its own:
+    // behind layer 1's Gram and reduction it started ~18 us after dZ_0, in the step's tail)
+    cudaStream_t gs = (fork && l == 0) ? x->side3_stream : side;
     rec(x->ev_dz[l], st);
-    wait(side, x->ev_dz[l]);
+    wait(gs, x->ev_dz[l]);
     g_low_prio = fork;
     phase(pr, HG_PHASE_DU, [&] {  // (side stream 1)
       // layer 0's Gram ends the step (only agg_bwd_0 and dM_x0 run beside it): every SM
       g_mn_grid_override = l == 0 ? kNumSMs : 0;
-      launch_mn_dU_cls(side, x->caps, p.cmax, dZ, x->f(p.A[l]), x->f(p.ones), dinfo,
-                       reinterpret_cast<const int4 *>(x->b(p.splits)), part_dU, x->grad(lname(l, "U")),
+      launch_mn_dU_cls(gs, x->caps, p.cmax, dZ, x->f(p.A[l]), x->f(p.ones), dinfo,
+                       reinterpret_cast<const int4 *>(x->b(p.splits)), gs == side ? part_dU : x->f(p.part2b),
+                       x->grad(lname(l, "U")),
                        x->grad(lname(l, "b_U")), x->caps.self_t ? x->grad(lname(l, "U_x")) : nullptr,
                        l == 0 ? c.f_node : c.hidden);
       g_mn_grid_override = 0;
     });
-    rec(x->ev_gram[l], side);
+    rec(x->ev_gram[l], gs);
     g_low_prio = false;
     // ---- main: dA, aggregation backward
     phase(pr, HG_PHASE_DA, [&] {
@@ -550,7 +555,10 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       }
     }
   }
-  wait(st, x->ev_gram[0]);  // join: every gradient is complete on the main stream
+  // join: every gradient is complete on the main stream (layer 0's Gram runs on its own stream,
+  // so the side stream's last Gram, layer 1's, is joined explicitly)
+  wait(st, x->ev_gram[0]);
+  if (c.layers > 1) wait(st, x->ev_gram[1]);
   wait(st, x->ev_side[0]);
   if (adam_forked) wait(st, x->ev_adam);
 }
@@ -802,6 +810,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
     return bail(e, "cudaStreamCreate");
   if ((e = cudaStreamCreateWithPriority(&x->side_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
     return bail(e, "cudaStreamCreate");
+  if ((e = cudaStreamCreateWithPriority(&x->side3_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
+    return bail(e, "cudaStreamCreate");
   if ((e = cudaStreamCreateWithPriority(&x->side2_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
     return bail(e, "cudaStreamCreate");
   if ((e = cudaStreamCreateWithPriority(&x->adam_stream, cudaStreamNonBlocking, prio_lo)) != cudaSuccess)
@@ -885,6 +895,7 @@ hg_status hg_ctx_destroy(hg_ctx *x) {
   if (x->cap_stream) cudaStreamDestroy(x->cap_stream);
   if (x->side_stream) cudaStreamDestroy(x->side_stream);
   if (x->side2_stream) cudaStreamDestroy(x->side2_stream);
+  if (x->side3_stream) cudaStreamDestroy(x->side3_stream);
   if (x->adam_stream) cudaStreamDestroy(x->adam_stream);
   for (auto *v : {&x->ev_dz, &x->ev_gram, &x->ev_dp, &x->ev_side, &x->ev_dx, &x->ev_upd, &x->ev_pl})
     for (auto ev : *v) cudaEventDestroy(ev);
