@@ -30,7 +30,6 @@ struct Plan {
   size_t params = 0, grads = 0, m = 0, v = 0, adam = 0, loss = 0;
   std::vector<size_t> slot;
   size_t blob_max = 0;
-  size_t amp = 0, att = 0;
   std::vector<size_t> P, A, arg, X;  // X[l] = output of layer l (X_{l+1})
   size_t dA = 0;
   // per layer l: dZ[l] = dL/dX_l (degree-sorted rows), dP[l] and the dM_e block partials --
@@ -42,7 +41,10 @@ struct Plan {
   size_t eval_acc = 0;
   size_t u_off = 0, ux_off = 0;
   int cmax = 0;  // degree-class slots
-  size_t perm = 0, pos = 0, deginfo = 0, tiles = 0, splits = 0, Wf = 0, WbT = 0, gslice = 0;
+  // per slot (computed when the slot's batch is uploaded, on the copy stream): the degree
+  // sort's perm / pos, class table, GEMM tiles, Gram splits, per-graph ranges, node scalers
+  std::vector<size_t> perm, pos, deginfo, tiles, splits, gslice, amp, att;
+  size_t Wf = 0, WbT = 0;
   // residuals w - trunc19(w) of the weight operands (activations' lo terms are derived in
   // shared memory by the GEMM kernels)
   size_t Wf_lo = 0, WbT_lo = 0, ones = 0, xpad = 0;
@@ -80,8 +82,6 @@ Plan make_plan(const hg_config &c) {
   p.eval_acc = take(sizeof(double) * 4);  // evaluation sums: sq err, abs err, graphs
   p.blob_max = (size_t)batch_offsets(c.max_graphs, c.max_nodes, c.max_edges, c.f_node, c.f_edge).total;
   for (int s = 0; s < c.n_slots; ++s) p.slot.push_back(take(p.blob_max));
-  p.amp = take(sizeof(float) * N);
-  p.att = take(sizeof(float) * N);
   for (int l = 0; l < c.layers; ++l) {
     p.P.push_back(take(sizeof(float) * N * PW));
     p.A.push_back(take(sizeof(float) * N * KA));
@@ -103,12 +103,16 @@ Plan make_plan(const hg_config &c) {
   p.cmax = tc_num_classes(c.max_degree);
   p.u_off = take(sizeof(int64_t) * (size_t)c.layers);
   p.ux_off = take(sizeof(int64_t) * (size_t)c.layers);
-  p.perm = take(sizeof(int) * N);
-  p.pos = take(sizeof(int) * N);
-  p.deginfo = take(sizeof(DegInfo));
-  p.gslice = take(sizeof(int4) * B);
-  p.tiles = take(sizeof(int4) * (size_t)tc_max_tiles(caps, p.cmax));
-  p.splits = take(sizeof(int4) * (size_t)tc_max_splits(caps, p.cmax));
+  for (int s = 0; s < c.n_slots; ++s) {
+    p.perm.push_back(take(sizeof(int) * N));
+    p.pos.push_back(take(sizeof(int) * N));
+    p.deginfo.push_back(take(sizeof(DegInfo)));
+    p.gslice.push_back(take(sizeof(int4) * B));
+    p.tiles.push_back(take(sizeof(int4) * (size_t)tc_max_tiles(caps, p.cmax)));
+    p.splits.push_back(take(sizeof(int4) * (size_t)tc_max_splits(caps, p.cmax)));
+    p.amp.push_back(take(sizeof(float) * N));
+    p.att.push_back(take(sizeof(float) * N));
+  }
   p.Wf = take(sizeof(float) * (size_t)c.layers * p.cmax * H * KA);
   p.WbT = take(sizeof(float) * (size_t)c.layers * p.cmax * H * KA);
   p.Wf_lo = take(sizeof(float) * (size_t)c.layers * p.cmax * H * KA);
@@ -279,6 +283,22 @@ int bucket_count(const hg_ctx *x);
 int bucket_closed_by(const hg_ctx *x, int l);
 
 // ---- the step's kernel sequence (enqueue only) ----
+// The batch's degree classes (stable sort by degree, class table with the configured scalers,
+// GEMM tiles, Gram splits, per-graph ranges): a property of the packed batch like its
+// reverse-edge slots, computed once per upload on the copy stream (one CTA beside the running
+// step) into the slot's buffers instead of at the head of every step's critical chain.
+void enqueue_degsort(hg_ctx *x, int slot, cudaStream_t st) {
+  const Plan &p = x->plan;
+  const hg_config &c = x->cfg;
+  g_low_prio = true;
+  launch_degsort(st, x->b(p.slot[slot]), c.delta, p.cmax, x->f(p.amp[slot]), x->f(p.att[slot]),
+                 reinterpret_cast<int *>(x->b(p.perm[slot])), reinterpret_cast<DegInfo *>(x->b(p.deginfo[slot])),
+                 reinterpret_cast<int4 *>(x->b(p.tiles[slot])), reinterpret_cast<int4 *>(x->b(p.splits[slot])),
+                 reinterpret_cast<int *>(x->b(p.pos[slot])), reinterpret_cast<int4 *>(x->b(p.gslice[slot])),
+                 scaler_mask(c), c.delta_lin, gram_ks(x->caps), x->caps.maxN);
+  g_low_prio = false;
+}
+
 // node-level head (HG_FLAG_NODE_HEAD): forward, and with bwd its gradient into dZ_L (after the
 // graph head wrote dZ_L), dyn and dhn for its parameter gradients (enqueue_node_head_grads)
 void enqueue_node_head(hg_ctx *x, cudaStream_t st, int slot, bool bwd) {
@@ -287,7 +307,7 @@ void enqueue_node_head(hg_ctx *x, cudaStream_t st, int slot, bool bwd) {
   launch_node_head(st, x->caps, x->b(p.slot[slot]), x->f(p.X[L - 1]), x->param("head_n.W1"), x->param("head_n.b1"),
                    x->param("head_n.W2"), x->param("head_n.b2"), x->cfg.node_weight, x->f(p.nh_hpre), x->f(p.nh_yn),
                    x->f(p.nh_sq), x->f(p.nh_dyn), x->f(p.nh_dhn), x->f(p.dZ[L - 1]),
-                   reinterpret_cast<const int *>(x->b(p.pos)), bwd);
+                   reinterpret_cast<const int *>(x->b(p.pos[slot])), bwd);
 }
 void enqueue_node_head_grads(hg_ctx *x, cudaStream_t st, int slot, float *part) {
   const Plan &p = x->plan;
@@ -306,23 +326,15 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   g_gemm_passes = (c.flags & HG_FLAG_TF32) ? 1 : 3;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
-  float *amp = x->f(p.amp), *att = x->f(p.att);
-  const int *pos = reinterpret_cast<const int *>(x->b(p.pos));  // sorted A / dZ rows
-  const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
+  const int *pos = reinterpret_cast<const int *>(x->b(p.pos[slot]));  // sorted A / dZ rows
+  const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo[slot]));
   const size_t HH = (size_t)c.hidden * c.hidden;
-  // Degree sort first (the graph's single root: measured, with several root branches the main
-  // stream's first kernel started ~14 us late), then the class-weight / M_x preparation on
-  // side stream 2, concurrent with layer 0's projection; the main chain joins the class
-  // weights before layer 0's update and M_x before layer 1's projection.
+  // The batch's degree classes were computed when it was uploaded (enqueue_degsort, copy
+  // stream). The class-weight / M_x preparation runs on side stream 2, concurrent with layer
+  // 0's projection; the main chain joins the class weights before layer 0's update and M_x
+  // before layer 1's projection.
   const bool fork = !pr && x->side_stream != nullptr;
   cudaStream_t wst = fork ? x->side2_stream : st;
-  phase(pr, HG_PHASE_SCALERS, [&] {
-    launch_degsort(st, blob, c.delta, p.cmax, amp, att, reinterpret_cast<int *>(x->b(p.perm)),
-                   reinterpret_cast<DegInfo *>(x->b(p.deginfo)), reinterpret_cast<int4 *>(x->b(p.tiles)),
-                   reinterpret_cast<int4 *>(x->b(p.splits)), reinterpret_cast<int *>(x->b(p.pos)),
-                   reinterpret_cast<int4 *>(x->b(p.gslice)), scaler_mask(x->cfg), c.delta_lin, gram_ks(x->caps),
-                   x->caps.maxN);
-  });
   if (fork) cudaEventRecord(x->ev_start, st);
   // the prep branch is enqueued after layer 0's projection so that the main chain is the
   // sort's first successor in the graph (measured: the other successor starts later)
@@ -357,7 +369,7 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     });
     if (l == 0) enqueue_prep();
     phase(pr, HG_PHASE_AGG_FWD, [&] {
-      launch_agg_fwd(st, x->caps, blob, reinterpret_cast<const int4 *>(x->b(p.gslice)), x->f(p.P[l]),
+      launch_agg_fwd(st, x->caps, blob, reinterpret_cast<const int4 *>(x->b(p.gslice[slot])), x->f(p.P[l]),
                      x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
                      c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), pos, l == 0 ? nullptr : x->f(p.X[l - 1]), F);
     });
@@ -367,8 +379,9 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     phase(pr, HG_PHASE_UPDATE, [&] {
       const bool keep_sorted = x->dxda && l + 1 < c.layers;  // X_l operands of the fused dX -> dA kernel
       const size_t wl = (size_t)l * p.cmax * c.hidden * x->caps.KA();  // layer l's class weights
-      launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), reinterpret_cast<const int *>(x->b(p.perm)), dinfo,
-                          reinterpret_cast<const int4 *>(x->b(p.tiles)), x->f(p.Wf) + wl, x->f(p.Wf_lo) + wl,
+      launch_d_update_cls(st, x->caps, p.cmax, x->f(p.A[l]), reinterpret_cast<const int *>(x->b(p.perm[slot])),
+                          dinfo, reinterpret_cast<const int4 *>(x->b(p.tiles[slot])), x->f(p.Wf) + wl,
+                          x->f(p.Wf_lo) + wl,
                           x->param(lname(l, "b_U")), x->f(p.X[l]),
                           keep_sorted ? x->f(p.Xs[l]) : nullptr,
                           keep_sorted ? reinterpret_cast<uint32_t *>(x->b(p.Xmask[l])) : nullptr);
@@ -424,7 +437,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
   g_gemm_passes = (c.flags & HG_FLAG_TF32) ? 1 : 3;
   const Plan &p = x->plan;
   const uint8_t *blob = x->b(p.slot[slot]);
-  const int *pos = reinterpret_cast<const int *>(x->b(p.pos));  // sorted A / dZ rows
+  const int *pos = reinterpret_cast<const int *>(x->b(p.pos[slot]));  // sorted A / dZ rows
   const size_t HH = (size_t)c.hidden * c.hidden;
   const bool fork = !pr && x->side_stream != nullptr;
   cudaStream_t side = fork ? x->side_stream : st, side2 = fork ? x->side2_stream : st;
@@ -448,9 +461,9 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
     if (c.flags & HG_FLAG_NODE_HEAD) enqueue_node_head_grads(x, side, slot, x->f(p.part2));
     g_low_prio = false;
   });
-  const int *perm = reinterpret_cast<const int *>(x->b(p.perm));
-  const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo));
-  const int4 *tiles = reinterpret_cast<const int4 *>(x->b(p.tiles));
+  const int *perm = reinterpret_cast<const int *>(x->b(p.perm[slot]));
+  const DegInfo *dinfo = reinterpret_cast<const DegInfo *>(x->b(p.deginfo[slot]));
+  const int4 *tiles = reinterpret_cast<const int4 *>(x->b(p.tiles[slot]));
   // Weight-gradient GEMMs (dU / db_U from the class Gram, dM_x / db_M) feed only the
   // exchange and AdamW, so they run on low-priority side streams while the main stream
   // walks the critical chain dA -> agg_bwd -> dX of each layer.
@@ -470,7 +483,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
       // layer 0's Gram ends the step (only agg_bwd_0 and dM_x0 run beside it): every SM
       g_mn_grid_override = l == 0 ? kNumSMs : 0;
       launch_mn_dU_cls(gs, x->caps, p.cmax, dZ, x->f(p.A[l]), x->f(p.ones), dinfo,
-                       reinterpret_cast<const int4 *>(x->b(p.splits)), gs == side ? part_dU : x->f(p.part2b),
+                       reinterpret_cast<const int4 *>(x->b(p.splits[slot])), gs == side ? part_dU : x->f(p.part2b),
                        x->grad(lname(l, "U")),
                        x->grad(lname(l, "b_U")), x->caps.self_t ? x->grad(lname(l, "U_x")) : nullptr,
                        l == 0 ? c.f_node : c.hidden);
@@ -486,7 +499,7 @@ void enqueue_backward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, 
                         x->f(p.WbT_lo) + (size_t)l * p.cmax * c.hidden * x->caps.KA(), x->f(p.dA));
     });
     phase(pr, HG_PHASE_AGG_BWD, [&] {
-      launch_agg_bwd(st, x->caps, blob, reinterpret_cast<const int4 *>(x->b(p.gslice)), x->f(p.P[l]),
+      launch_agg_bwd(st, x->caps, blob, reinterpret_cast<const int4 *>(x->b(p.gslice[slot])), x->f(p.P[l]),
                      x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
                      x->f(p.A[l]), x->b(p.arg[l]), x->f(p.dA), dP, pagg, pos, x->dxda ? pos : nullptr,
                      x->f(p.dm_scratch));
@@ -1161,8 +1174,10 @@ hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_
     case 7: *offset = p.hpre; *bytes = 4 * B * c.fc_hidden; break;
     case 8: *offset = p.params; *bytes = 4 * x->n_params; break;
     case 9: *offset = p.grads; *bytes = 4 * x->n_params; break;
-    case 10: *offset = p.amp; *bytes = 4 * N; break;
-    case 11: *offset = p.att; *bytes = 4 * N; break;
+    case 10:
+    case 11:  // (per slot: layer = slot)
+      if (layer < 0 || layer >= c.n_slots) return fail(HG_E_RANGE, "slot out of range");
+      *offset = what == 10 ? p.amp[layer] : p.att[layer]; *bytes = 4 * N; break;
     case 12: if (!p.nh_yn) return fail(HG_E_RANGE, "no node head"); *offset = p.nh_yn; *bytes = 4 * N; break;
     case 13: if (!p.nh_hpre) return fail(HG_E_RANGE, "no node head"); *offset = p.nh_hpre; *bytes = 4 * N * c.fc_hidden; break;
     // (debug views, not in the header: per-layer dP, dP_lo; padded layer-0 features)
@@ -1185,6 +1200,7 @@ hg_status hg_pack(hg_ctx *x, const hg_store *s, const int64_t *ids, int32_t B, i
   // the device slot may still be read by an earlier step
   CK(x, cudaStreamWaitEvent(x->copy_stream, x->compute_done[slot], 0));
   CK(x, cudaMemcpyAsync(x->b(x->plan.slot[slot]), x->staging[slot], used, cudaMemcpyHostToDevice, x->copy_stream));
+  enqueue_degsort(x, slot, x->copy_stream);
   CK(x, cudaEventRecord(x->copy_done[slot], x->copy_stream));
   return HG_OK;
 }
@@ -1201,6 +1217,7 @@ hg_status hg_upload_packed(hg_ctx *x, const void *blob, size_t bytes, int32_t sl
   std::memcpy(x->staging[slot], blob, need);
   CK(x, cudaStreamWaitEvent(x->copy_stream, x->compute_done[slot], 0));
   CK(x, cudaMemcpyAsync(x->b(x->plan.slot[slot]), x->staging[slot], need, cudaMemcpyHostToDevice, x->copy_stream));
+  enqueue_degsort(x, slot, x->copy_stream);
   CK(x, cudaEventRecord(x->copy_done[slot], x->copy_stream));
   return HG_OK;
 }

@@ -134,6 +134,7 @@ constexpr int kMaxScalers = 5;   // identity, amplification, attenuation, linear
 constexpr int kGramKS = 256;     // minimum nodes per K-split of the per-class Gram GEMM
 // nodes per Gram K-split for a capacity: >= kGramKS, about 64 splits at large capacities
 // (the split partials are reduced afterwards, so their number bounds that traffic)
+// (32 or 128 splits measured no better at configs B and D, round 2)
 inline int gram_ks(const Caps &c) {
   const int k = (c.maxN + 63) / 64;
   return k <= kGramKS ? kGramKS : (k + 31) / 32 * 32;

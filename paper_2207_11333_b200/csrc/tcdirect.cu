@@ -40,12 +40,7 @@ extern std::atomic<int64_t> g_launches;
 // shared-memory-read bound); at H = 128, 32 for small batches (config B: 4x51 CTAs instead
 // of 2x51 for these latency-bound GEMMs, +1.5%), 64 for large ones (config D)
 static int bn_auto(const Caps &c) { return c.H >= 256 ? 128 : c.maxN <= 16384 ? 32 : 64; }
-#ifndef UPD_BN
-#define UPD_BN 0
-#endif
-#ifndef PROJ_BN
-#define PROJ_BN 0
-#endif
+
 
 
 // GEMM passes of the tf32 tensor-core GEMMs: 3 = 3xTF32 (fp32-accurate, the graded mode),
@@ -854,7 +849,7 @@ void launch_d_update_cls(cudaStream_t st, const Caps &c, int cmax, const float *
                          float *X1, float *X1s, uint32_t *X1mask) {
   // (the update at config D: BN = 128 measured 3.5% faster per step than 64, round 2; at B's
   // small batches the 4x more CTAs of BN = 32 win)
-  const int bn = UPD_BN ? UPD_BN : (c.maxN <= 16384 && c.H < 256 ? 32 : 128);
+  const int bn = c.maxN <= 16384 && c.H < 256 ? 32 : 128;
   if (bn == 32) update_bn<32>(st, c, cmax, A, perm, info, tiles, Wf, Wf_lo, bU, X1, X1s, X1mask);
   else if (bn == 128) update_bn<128>(st, c, cmax, A, perm, info, tiles, Wf, Wf_lo, bU, X1, X1s, X1mask);
   else update_bn<64>(st, c, cmax, A, perm, info, tiles, Wf, Wf_lo, bU, X1, X1s, X1mask);
@@ -867,7 +862,7 @@ void launch_d_dA_cls(cudaStream_t st, const Caps &c, int cmax, const float *dZ, 
 
 void launch_d_proj(cudaStream_t st, const Caps &c, const uint8_t *blob, const float *X, int F, const float *Mx,
                    const float *Mx_lo, float *P) {
-  const int bn = PROJ_BN ? PROJ_BN : (c.maxN <= 16384 && c.H < 256 ? 32 : 128);  // (as the update: D +0.7%)
+  const int bn = c.maxN <= 16384 && c.H < 256 ? 32 : 128;  // (as the update: D +0.7%)
   if (bn == 32) proj_bn<32>(st, c, blob, X, F, Mx, Mx_lo, P);
   else if (bn == 128) proj_bn<128>(st, c, blob, X, F, Mx, Mx_lo, P);
   else proj_bn<64>(st, c, blob, X, F, Mx, Mx_lo, P);

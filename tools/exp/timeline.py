@@ -67,10 +67,11 @@ prof.export_chrome_trace(args.json)
 ev = json.load(open(args.json))["traceEvents"]
 k = [e for e in ev if e.get("cat") == "kernel"]
 k.sort(key=lambda e: e["ts"])
-# split into steps at the degree sort (first kernel of every step)
+# split into steps at layer 0's projection (the first kernel of every step; the degree sort
+# runs at upload time on the copy stream)
 steps, cur = [], []
 for e in k:
-    if "degsort" in e["name"] and cur:
+    if "OpProj" in e["name"] and cur:
         steps.append(cur)
         cur = []
     cur.append(e)

@@ -1,0 +1,9 @@
+set -x
+mkdir -p gpurun_out
+cp paper_2207_11333_b200/lib/libhgnn.so /tmp/libhgnn_default.so
+for v in default g128 g32; do
+  if [ $v = default ]; then cp /tmp/libhgnn_default.so paper_2207_11333_b200/lib/libhgnn.so; else cp paper_2207_11333_b200/lib/variants/libhgnn_$v.so paper_2207_11333_b200/lib/libhgnn.so; fi
+  timeout 300 python bench.py --workload D --steps 10 --warmup 3 --no-cpu-baseline --no-e2e --graphs 300000 > gpurun_out/r30_benchD_$v.json 2> gpurun_out/r30_benchD_$v.err; echo "benchD_$v=$?" >> gpurun_out/r30_status.txt
+  timeout 300 python bench.py --workload B --steps 30 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/r30_benchB_$v.json 2> gpurun_out/r30_benchB_$v.err; echo "benchB_$v=$?" >> gpurun_out/r30_status.txt
+done
+cp /tmp/libhgnn_default.so paper_2207_11333_b200/lib/libhgnn.so
