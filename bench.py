@@ -483,11 +483,13 @@ def main():
                       "MEASURED_PEAKS.json bf16_tflops x 0.5 (tf32) / 3 (3xTF32 passes)")
     ridge = tc_peak * 1e12 / (hbm_peak * 1e9)  # flop / byte
     step_ms_prof = sum(v[0] for v in phases.values())
-    traffic_db = {}
+    traffic_db = {}  # this workload's ncu DRAM read + write bytes per launch (tools/traffic_from_ncu.py)
     try:
         with open(os.path.join(ROOT, "profiles", "traffic_per_launch.json")) as f:
-            traffic_db = json.load(f)
-    except (OSError, ValueError):
+            traffic_db = json.load(f).get(args.workload, {})
+        if not isinstance(traffic_db, dict) or args.precision != "3xtf32" or args.variant != "base":
+            traffic_db = {}  # (captured for the base model in 3xTF32 only)
+    except (OSError, ValueError, AttributeError):
         pass
 
     def roof(k):
