@@ -286,11 +286,13 @@ int bucket_closed_by(const hg_ctx *x, int l);
 // The batch's degree classes (stable sort by degree, class table with the configured scalers,
 // GEMM tiles, Gram splits, per-graph ranges): a property of the packed batch like its
 // reverse-edge slots, computed once per upload on the copy stream (one CTA beside the running
-// step) into the slot's buffers instead of at the head of every step's critical chain.
+// step) into the slot's buffers instead of at the head of every step's critical chain. High
+// priority: the next step waits for it, and at low priority the running step's kernels kept
+// it off the SMs until that step ended.
 void enqueue_degsort(hg_ctx *x, int slot, cudaStream_t st) {
   const Plan &p = x->plan;
   const hg_config &c = x->cfg;
-  g_low_prio = true;
+  g_low_prio = false;
   launch_degsort(st, x->b(p.slot[slot]), c.delta, p.cmax, x->f(p.amp[slot]), x->f(p.att[slot]),
                  reinterpret_cast<int *>(x->b(p.perm[slot])), reinterpret_cast<DegInfo *>(x->b(p.deginfo[slot])),
                  reinterpret_cast<int4 *>(x->b(p.tiles[slot])), reinterpret_cast<int4 *>(x->b(p.splits[slot])),
@@ -335,10 +337,12 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
   // before layer 1's projection.
   const bool fork = !pr && x->side_stream != nullptr;
   cudaStream_t wst = fork ? x->side2_stream : st;
-  if (fork) cudaEventRecord(x->ev_start, st);
   // the prep branch is enqueued after layer 0's projection so that the main chain is the
   // sort's first successor in the graph (measured: the other successor starts later)
   auto enqueue_prep = [&] {
+    // (forked after layer 0's projection, ev_start, and enqueued after layer 0's aggregation so
+    // that the main chain is the projection's first successor in the graph: a second root
+    // branch, or the prep branch as the first successor, measured starting the other late)
     if (fork) cudaStreamWaitEvent(wst, x->ev_start, 0);
     phase(pr, HG_PHASE_SCALERS, [&] {  // (class weights belong with the scalers)
       // layer 0's weights first (needed soonest); low priority so the main chain's first
@@ -367,12 +371,13 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
       else
         launch_proj(st, x->caps, blob, nullptr, F, x->param(lname(l, "M_x")), x->f(p.P[l]));
     });
-    if (l == 0) enqueue_prep();
+    if (fork && l == 0) cudaEventRecord(x->ev_start, st);
     phase(pr, HG_PHASE_AGG_FWD, [&] {
       launch_agg_fwd(st, x->caps, blob, reinterpret_cast<const int4 *>(x->b(p.gslice[slot])), x->f(p.P[l]),
                      x->param(lname(l, "M_e")), x->param(lname(l, "b_M")),
                      c.var_floor, x->f(p.A[l]), x->b(p.arg[l]), pos, l == 0 ? nullptr : x->f(p.X[l - 1]), F);
     });
+    if (l == 0) enqueue_prep();
     if (fork && l == 0) cudaStreamWaitEvent(st, x->ev_prep, 0);
     if (fork && l == 1) cudaStreamWaitEvent(st, x->ev_prepw, 0);
     if (fork && l >= 1) cudaStreamWaitEvent(st, x->ev_pl[l], 0);
