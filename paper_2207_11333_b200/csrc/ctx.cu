@@ -345,14 +345,15 @@ void enqueue_forward(hg_ctx *x, cudaStream_t st, int slot, Prof *pr = nullptr, b
     // branch, or the prep branch as the first successor, measured starting the other late)
     if (fork) cudaStreamWaitEvent(wst, x->ev_start, 0);
     phase(pr, HG_PHASE_SCALERS, [&] {  // (class weights belong with the scalers)
-      // layer 0's weights first (needed soonest); low priority so the main chain's first
-      // kernels are not kept off the SMs
-      g_low_prio = fork;
+      // layer 0's weights first, at high priority (update_0 waits for them: at low priority they
+      // ran only after agg_0 had drained); the rest at low priority
+      g_low_prio = false;
       const int64_t *uo = reinterpret_cast<const int64_t *>(x->b(p.u_off));
       const int64_t *uxo = reinterpret_cast<const int64_t *>(x->b(p.ux_off));
       launch_prep_W2(wst, x->caps, x->f(p.params), uo, uxo, 0, 1, p.cmax, dinfo, x->f(p.Wf), x->f(p.Wf_lo),
                      x->f(p.WbT), x->f(p.WbT_lo));
       if (fork) cudaEventRecord(x->ev_prep, wst);
+      g_low_prio = fork;
       launch_prep_Mx(wst, x->caps, x->f(p.params), reinterpret_cast<const int64_t *>(x->b(p.mx_off)), c.layers,
                      x->f(p.Mx_lo), x->f(p.MxT), x->f(p.MxT_lo));
       if (fork) cudaEventRecord(x->ev_prepmx, wst);
