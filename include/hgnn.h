@@ -271,8 +271,10 @@ hg_status hg_checkpoint_load(hg_ctx *x, const char *path);
  * (mean|min|max|std, degree-sorted rows; [N,5H] with the self-term's x_i block), 2 = arg_l
  * [N,2H] u8 (argmin | argmax with bit7 = var>floor), 3 = X_{l+1} [N,H],
  * 4 = batch slot `layer` blob, 5 = yhat [B], 6 = loss [1], 7 = head hidden
- * pre-activation [B,Hf], 8 = params, 9 = grads, 10 = amp [N], 11 = att [N], 12 = node-level
- * head yhat [N], 13 = its hidden pre-activation [N,Hf] (HG_FLAG_NODE_HEAD). */
+ * pre-activation [B,Hf], 8 = params, 9 = grads, 10 = amp [N] and 11 = att [N] of batch slot
+ * `layer` (the node scalers, computed with the slot's degree classes when its batch is
+ * uploaded), 12 = node-level head yhat [N], 13 = its hidden pre-activation [N,Hf]
+ * (HG_FLAG_NODE_HEAD). */
 hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_t *offset, int64_t *bytes);
 
 /* Debug: copy batch slot `slot`'s packed blob (layout above; its header gives B, N, E) to
@@ -281,12 +283,14 @@ hg_status hg_workspace_view(const hg_ctx *x, int32_t what, int32_t layer, int64_
 hg_status hg_batch_get(hg_ctx *x, int32_t slot, void *dst, size_t cap, size_t *used);
 
 /* Collate `ids` from the store on the host (pinned staging buffer of `slot`)
- * and enqueue the H2D copy on the ctx's copy stream; later device work on
- * that slot waits for it. The staging buffer is reused only after its
- * previous copy completed. Errors as hg_pack_host. */
+ * and enqueue the H2D copy on the ctx's copy stream, followed there by the batch's degree
+ * classes (stable sort by in-degree, class table, GEMM tiles, per-graph ranges: DESIGN.md §5,
+ * one CTA beside any running step); later device work on that slot waits for both. The
+ * staging buffer is reused only after its previous copy completed. Errors as hg_pack_host. */
 hg_status hg_pack(hg_ctx *x, const hg_store *s, const int64_t *ids, int32_t B, int32_t slot);
 /* Copy an already packed blob (host pointer, e.g. from hg_pack_host) into `slot`. The blob is
- * validated first (header, capacities, offsets, degrees, distinct-degree count). */
+ * validated first (header, capacities, offsets, degrees, distinct-degree count); the degree
+ * classes follow on the copy stream as in hg_pack. */
 hg_status hg_upload_packed(hg_ctx *x, const void *blob, size_t bytes, int32_t slot);
 
 /* Forward pass on the batch in `slot`: L GC layers, global
