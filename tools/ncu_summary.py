@@ -62,6 +62,7 @@ def full(path):
     cols = [m for m in METRICS if m in idx]
     print("| kernel | " + " | ".join(cols) + " |")
     print("|---|" + "---|" * len(cols))
+    print("| (unit) | " + " | ".join(rows[1][idx[m]] for m in cols) + " |")
     for r in rows[2:]:
         if len(r) <= ki:
             continue
