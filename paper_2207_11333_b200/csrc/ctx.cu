@@ -184,7 +184,8 @@ struct hg_ctx {
   std::vector<cudaEvent_t> ev_dz, ev_gram, ev_dp, ev_side, ev_dx, ev_upd, ev_pl;  // per layer fork / join points
   cudaEvent_t ev_head = nullptr, ev_prep = nullptr, ev_start = nullptr, ev_prepmx = nullptr, ev_prepw = nullptr,
               ev_ar1 = nullptr, ev_adam = nullptr;
-  float *loss_ring = nullptr;  // pinned, HG_LOSS_RING entries
+  float *loss_ring = nullptr;  // pinned and mapped, HG_LOSS_RING entries
+  float *loss_ring_dev = nullptr;  // its device address
   cudaEvent_t loss_ev[HG_LOSS_RING] = {};
   int64_t launches = 0;
   bool dxda = false;    // fused dX -> dA backward kernel (H == 128)
@@ -839,7 +840,8 @@ hg_status hg_ctx_create(const hg_config *c, int32_t device, void *workspace, siz
   g_prio_hi = prio_hi;
   for (cudaEvent_t *ev : {&x->ev_head, &x->ev_prep, &x->ev_start, &x->ev_prepmx, &x->ev_prepw, &x->ev_ar1, &x->ev_adam})
     if ((e = cudaEventCreateWithFlags(ev, cudaEventDisableTiming)) != cudaSuccess) return bail(e, "cudaEventCreate");
-  if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocDefault)) != cudaSuccess)
+  if ((e = cudaHostAlloc((void **)&x->loss_ring, sizeof(float) * HG_LOSS_RING, cudaHostAllocMapped)) != cudaSuccess ||
+      (e = cudaHostGetDevicePointer((void **)&x->loss_ring_dev, x->loss_ring, 0)) != cudaSuccess)
     return bail(e, "cudaHostAlloc");
   for (int i = 0; i < HG_LOSS_RING; ++i)
     if ((e = cudaEventCreateWithFlags(&x->loss_ev[i], cudaEventDisableTiming)) != cudaSuccess)
@@ -1592,7 +1594,8 @@ hg_status hg_loss_enqueue(hg_ctx *x, int32_t i) {
   hg_status st = usable(x);
   if (st) return st;
   if (i < 0 || i >= HG_LOSS_RING) return fail(HG_E_RANGE, "loss ring index %d out of range", i);
-  CK(x, cudaMemcpyAsync(x->loss_ring + i, x->f(x->plan.loss), sizeof(float), cudaMemcpyDeviceToHost, x->stream));
+  launch_loss_to_host(x->stream, x->f(x->plan.loss), x->loss_ring_dev + i);
+  CK(x, cudaGetLastError());
   CK(x, cudaEventRecord(x->loss_ev[i], x->stream));
   return HG_OK;
 }

@@ -702,6 +702,19 @@ void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float
   counted();
 }
 
+// the loss value into host-mapped pinned memory by a one-thread kernel: a DMA read-back queued
+// behind the next batch's H2D copy on the copy engine (measured ~23 us per step in the
+// end-to-end loop), a store from the SMs is not
+__global__ void k_loss_to_host(const float *__restrict__ loss, float *__restrict__ host) {
+  pdl_enter();
+  *reinterpret_cast<volatile float *>(host) = loss[0];
+  __threadfence_system();
+}
+void launch_loss_to_host(cudaStream_t st, const float *loss, float *host_mapped) {
+  launch_ex(k_loss_to_host, 1, 32, 0, st, loss, host_mapped);
+  counted();
+}
+
 // evaluation sums: acc[0] += sum (yhat-y)^2, acc[1] += sum |yhat-y|,
 // acc[2] += B, in fp64 with a fixed-order block tree (deterministic)
 __global__ void __launch_bounds__(256) k_eval_accum(const uint8_t *__restrict__ blob, const float *__restrict__ yhat,

@@ -79,6 +79,7 @@ void launch_head_grads(cudaStream_t st, const Caps &c, const uint8_t *blob, cons
 // evaluation sums of one batch into acc[0..2] (fp64: squared error, absolute error, graphs)
 void launch_eval_accum(cudaStream_t st, const uint8_t *blob, const float *yhat, double *acc);
 // mean squared error over the batch from the per-graph terms (after launch_head_fused)
+void launch_loss_to_host(cudaStream_t st, const float *loss, float *host_mapped);  // one float, mapped pinned dst
 void launch_loss(cudaStream_t st, const uint8_t *blob, const float *sqerr, float *loss, const float *sqn = nullptr,
                  float w = 0.f);
 void head_configure(const Caps &c);

@@ -1,0 +1,12 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/r39_pytest.log 2>&1; echo "pytest=$?" > gpurun_out/r39_status.txt
+timeout 300 python tools/exp/e2e_timeline.py > gpurun_out/r39_e2e_timeline.txt 2>&1; echo "tl=$?" >> gpurun_out/r39_status.txt
+cp paper_2207_11333_b200/lib/libhgnn.so /tmp/libhgnn_default.so
+for i in 1 2; do
+for v in default old; do
+  if [ $v = default ]; then cp /tmp/libhgnn_default.so paper_2207_11333_b200/lib/libhgnn.so; else cp paper_2207_11333_b200/lib/variants/libhgnn_$v.so paper_2207_11333_b200/lib/libhgnn.so; fi
+  timeout 300 python bench.py --workload B --steps 50 --warmup 5 --no-cpu-baseline > gpurun_out/r39_benchB_${v}_$i.json 2> gpurun_out/r39_benchB_${v}_$i.err; echo "benchB_$v=$?" >> gpurun_out/r39_status.txt
+done
+done
+cp /tmp/libhgnn_default.so paper_2207_11333_b200/lib/libhgnn.so
