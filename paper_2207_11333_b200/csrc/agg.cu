@@ -55,7 +55,7 @@ __host__ __device__ constexpr uint32_t r16(uint32_t b) { return (b + 15u) & ~15u
 
 // dynamic shared-memory layout (byte offsets) of one CTA
 struct SmemLayout {
-  uint32_t P, dm, rp, col, ea, pos, slot, rev, total;
+  uint32_t P, dm, rp, col, ea, pos, slot, total;
 };
 __host__ __device__ inline SmemLayout smem_layout(int cap_n, int cap_e, int Fe, bool bwd) {
   SmemLayout L;
@@ -66,8 +66,7 @@ __host__ __device__ inline SmemLayout smem_layout(int cap_n, int cap_e, int Fe, 
   L.ea = L.col + r16((cap_e + 8) * 4);
   L.pos = L.ea + r16(cap_e * Fe * 4 + 32);
   L.slot = L.pos + r16((cap_n + 8) * 4);
-  L.rev = L.slot + (bwd ? r16(cap_e + 32) : 0);
-  L.total = L.rev + (bwd ? r16(cap_e * 2) : 0);
+  L.total = L.slot + (bwd ? r16(cap_e + 32) : 0);
   // (the backward's partial reduction reuses the area: kHalvesB x 16 lanes x CPL x (Fe + 1))
   const uint32_t red = (uint32_t)kHalvesB * 16 * CPL * ((Fe <= 4 ? 4 : 8) + 1) * 4;  // (FE template width)
   if (L.total < red) L.total = red;
@@ -204,7 +203,6 @@ template <bool S>
 struct View {
   const int *rp, *col, *pos;
   const uint8_t *slot;
-  const uint16_t *rev;  // (backward, staged) in-edge -> the same pair's entry in the source's row
   const float *ea, *P;
   float *dm;
   int r0, c0, p0, s0, e0, n0, Fe, Pstride, ch0, H;
@@ -224,7 +222,8 @@ struct View {
   // where phase 1 stores the gradient of in-edge k (j -> i, k in i's row) and where phase 2
   // finds that of row-j entry k: staged graphs use source-major order (the row-j entry of the
   // same pair, so phase 2 reads its rows contiguously); otherwise destination-major
-  __device__ int dm_store(int k) const { return S ? e0 + rev[k - e0] : k; }
+  // (the CSR is symmetric: in-edge k of row i, from j = col[k], is the entry slot[k] of row j)
+  __device__ int dm_store(int k) const { return S ? rowptr(colv(k)) + slotv(k) : k; }
   __device__ int dm_load(int k) const { return S ? k : rowptr(colv(k)) + slotv(k); }
 };
 template <bool S>
@@ -242,7 +241,6 @@ __device__ View<S> make_view(const BatchView &b, const float *P, int PW, int ch0
     v.col = reinterpret_cast<const int *>(sm + L.col);
     v.pos = reinterpret_cast<const int *>(sm + L.pos);
     v.slot = sm + L.slot;
-    v.rev = reinterpret_cast<const uint16_t *>(sm + L.rev);
     v.ea = reinterpret_cast<const float *>(sm + L.ea) + s.ea_skip;
     v.P = reinterpret_cast<const float *>(sm + L.P);
     v.dm = reinterpret_cast<float *>(sm + L.dm);
@@ -655,15 +653,6 @@ __global__ void __launch_bounds__(32 * kWarpsB, 2) k_agg_bwd(const uint8_t *__re
     fill_rcp(rcp);
     if (staged) {
       stage_wait(&bar, 0);
-      {  // rev: for row-j entry k (pair i -> j, i = col[k]) the in-edge j -> i sits at rowptr[i] + slot[k]
-        const int *rp = reinterpret_cast<const int *>(sm + L.rp), *cl = reinterpret_cast<const int *>(sm + L.col);
-        uint16_t *rv = reinterpret_cast<uint16_t *>(sm + L.rev);
-        for (int t = threadIdx.x; t < s.e1 - s.e0; t += blockDim.x) {
-          const int k = s.e0 + t;
-          rv[rp[cl[k - s.c0] - s.r0] + sm[L.slot + k - s.s0] - s.e0] = (uint16_t)t;
-        }
-        __syncthreads();
-      }
       const View<true> v = make_view<true>(b, P, PW, ch0, pos, L, sm, s, dmbuf, H);
       bwd_phase1<true, SELF, FE>(v, s, sme, bm, A, arg, dA, H, KA, Qp, PW, dP, rcp, first);
       __syncthreads();  // (orders the block's dm writes before phase 2's reads)
