@@ -37,19 +37,22 @@ def _ctxs(data, W, Bl, H, L):
     return ctxs, cfg, delta, store
 
 
-def _well_conditioned_normwise(gpu, ref, g, params0, lr=1e-3, wd=0.01, eps=1e-8):
-    """C19 one-step parameter bar with reading R-adam-eps (tests/_parity.py)."""
+def _well_conditioned_normwise(gpu, ref, g, params0, t=1, lr=1e-3, wd=0.01, eps=1e-8):
+    """C19 one-step parameter bar with reading R-adam-eps (tests/_parity.py): compared where the
+    oracle gradient is >= 100 eps and its sign is fixed by the gradient bar; elsewhere the Adam
+    step bound of step t."""
     worst, viol = 0.0, 0
+    bound = lr * PT.adam_ratio_bound(t, dict(beta1=hgnn.DEFAULT_ADAMW["beta1"], beta2=hgnn.DEFAULT_ADAMW["beta2"]))
     for k in ref:
-        ok = np.abs(g[k]) >= 100 * eps
+        ok = np.abs(g[k]) >= max(100 * eps, PT.GRAD_TOL * float(np.abs(g[k]).max()))
         a = np.asarray(gpu[k], np.float64).reshape(ref[k].shape)
         if ok.any():
             worst = max(worst, normwise(a[ok], ref[k][ok]))
-        viol += int((np.abs(a[~ok] - params0[k][~ok] * (1 - lr * wd)) > lr * 1.001 + 1e-7).sum())
+        viol += int((np.abs(a[~ok] - params0[k][~ok] * (1 - lr * wd)) > bound * 1.001 + 1e-7).sum())
     return worst, viol
 
 
-@pytest.mark.parametrize("W,H,L", [(2, 128, 3), (4, 128, 2), (3, 55, 2)])
+@pytest.mark.parametrize("W,H,L", [(2, 128, 3), (4, 128, 2), (3, 55, 2), (8, 128, 2)])
 def test_p2p_exchange_emulated_ranks_match_oracle_ddp_step(torch_cuda, W, H, L):
     data = PT.generate("pcqm", 900, 21)
     Bl = 24
@@ -73,7 +76,7 @@ def test_p2p_exchange_emulated_ranks_match_oracle_ddp_step(torch_cuda, W, H, L):
         # the oracle's DDP step (rank sub-batches, gradient mean, AdamW) from the same state
         newp, newst, _, g = O.train_step(params, st, data, bg, ocfg, delta, hyper=hyper, world=W)
         gp = hgnn.arena_to_dict(got[0], lay)
-        worst, viol = _well_conditioned_normwise(gp, newp, g, params)
+        worst, viol = _well_conditioned_normwise(gp, newp, g, params, t=k + 1)
         print(W, H, k, "param normwise", worst, "bound violations", viol)
         assert worst <= 1e-3 and viol == 0
         # moments: sharded after the exchange; opt_state_get gathers them whole (collective)
