@@ -386,24 +386,26 @@ __device__ void fwd_nodes(const View<S> &v, const Slice &s, const float2 (&me)[2
     if (!valid) continue;
     float mean[CPL], sd[CPL];
     uint32_t flags = 0;
-    if (d == 0) {
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) {
+      mean[c] = sum[c] * rd + q[c];  // (q = 0 without the self-term)
+      mx[c] += q[c];
+      mn[c] += q[c];
+      const float var = ss[c] * rd;
+      flags |= (var > var_floor ? 0x80u : 0u) << (8 * c);
+      // channels >= Hl are padding (internal width H > logical Hl): their messages are
+      // exactly 0, and their std is forced to 0 instead of sqrt(var_floor) so that no
+      // gradient reaches the zero padded parameters (SURVEY §8(d) padding hazard).
+      // (sqrt as v * rsqrt(v), ~2 ulp: the IEEE sqrtf sequence was 14% of the instructions)
+      const float vf = fmaxf(var, var_floor);
+      sd[c] = ch + c < Hl ? vf * rsqrt_ftz(vf) : 0.f;
+    }
+    // isolated nodes (d = 0, rare): every aggregate 0 (C5) -- a warp-uniform branch, so the
+    // common warps skip the per-channel selects
+    if (__any_sync(__activemask(), d == 0) && d == 0) {
+      flags = 0;
 #pragma unroll
       for (int c = 0; c < CPL; ++c) { mean[c] = 0.f; mx[c] = 0.f; mn[c] = 0.f; sd[c] = 0.f; }
-    } else {
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        mean[c] = sum[c] * rd + q[c];  // (q = 0 without the self-term)
-        mx[c] += q[c];
-        mn[c] += q[c];
-        const float var = ss[c] * rd;
-        flags |= (var > var_floor ? 0x80u : 0u) << (8 * c);
-        // channels >= Hl are padding (internal width H > logical Hl): their messages are
-        // exactly 0, and their std is forced to 0 instead of sqrt(var_floor) so that no
-        // gradient reaches the zero padded parameters (SURVEY §8(d) padding hazard).
-        // (sqrt as v * rsqrt(v), ~2 ulp: the IEEE sqrtf sequence was 14% of the instructions)
-        const float vf = fmaxf(var, var_floor);
-        sd[c] = ch + c < Hl ? vf * rsqrt_ftz(vf) : 0.f;
-      }
     }
     float *Ai = A + (size_t)prow * KA + ch;
     st4(Ai, mean);
