@@ -158,7 +158,7 @@ typedef struct {
  * PAPER.md:212): every tensor-core contraction runs ONE tf32 pass (operands truncated to
  * tf32, fp32 accumulate) instead of the fp32-accurate 3xTF32 default. Everything else
  * (aggregation, head, loss, AdamW, the exchange) stays fp32. Its parity bars are looser
- * (DESIGN.md §3 "TF32 mode": forward 1e-2, gradients 5e-2 normwise). */
+ * (DESIGN.md §3 "TF32 mode": forward 2e-2 max-scaled, gradients / moments / parameters 5e-2). */
 #define HG_FLAG_TF32 1
 /* hg_config.flags: HG_FLAG_SELF_TERM selects the PNA self-term variant (SURVEY C1 / §8(f)
  * row 3, reading R-self): the message is M [x_j || x_i || e_ij] + b_M and the update
